@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 ADI hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--method both|mfd|cfd] [--n NODES]
+
+Workload (config 4 of BASELINE.json at one GPU): a single 16384 x 16384-node
+grid, the paper's Γ = 0 harmonic test (eq. 11, dense manufactured source,
+homogeneous Dirichlet), K = 8 sweeps, cfl 0.91 (CFD) / 0.81 (MFD), fp64.  A
+"step" is one full Peaceman–Rachford time step (both half-steps) of each
+method; `value` is grid-point updates per second summed over the job.
+Each field is 2.1 GB (> 126 MB L2), so no L2 flush is needed between steps.
+
+Under torchrun (N > 1) every rank advances its own independent grid
+(replicas; weak scaling) — the line-sharded single grid is future work
+(DESIGN.md §7).  Timing: CUDA events on the library's stream, barrier +
+synchronize on both sides, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 grid-point updates/sec per ADI step (CFD, MFD); % of HBM roofline; 1/2/4/8 GPU"
+UNIT = "grid-point updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--method", default="both", choices=["both", "mfd", "cfd"])
+    ap.add_argument("--n", type=int, default=16384, help="nodes per direction")
+    ap.add_argument("--K", type=int, default=8)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-n", type=int, default=4097, help="oracle sample grid (nodes)")
+    return ap.parse_args()
+
+
+def methods_of(a):
+    from adi_inputs import CFD, MFD
+    return {"both": [MFD, CFD], "mfd": [MFD], "cfd": [CFD]}[a.method]
+
+
+MNAME = {0: "cfd", 1: "mfd"}
+
+
+# ---------------------------------------------------------------------------
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allmax(ws, v):
+    if ws <= 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        cmd = ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+               "--format=csv,noheader,nounits", "-lms", "100"]
+        try:
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > i + 2 and s[i + 2].lower() == "active"})
+        loaded = [v for v in sm if v > 500] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes per launch from the committed ncu --set full capture, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    return json.load(open(p)) if os.path.exists(p) else {}
+
+
+# ---------------------------------------------------------------------------
+def make_problem(method, n, steps, K):
+    from adi_inputs import MMS, mms_problem
+    return mms_problem(method, n, MMS(), steps=steps, K=K)
+
+
+def kernel_bytes(method, n, kind, has_phi=True):
+    """Algorithmic HBM bytes of one launch: each line kernel reads the
+    carried pressure field S and its velocity, writes both, and reads the dense
+    source once — 8 B per value, interior sizes of SURVEY §8b."""
+    from adi_inputs import interior_shape, shapes
+    su, sv, sw = shapes(method, n, n)
+    ns = int(np.prod(interior_shape(method, n, n)))
+    nv, nw = int(np.prod(sv)), int(np.prod(sw))
+    phi = ns if has_phi else 0
+    if kind == "row":
+        return 8 * (2 * ns + 2 * nv + phi)
+    if kind == "col":
+        return 8 * (2 * ns + 2 * nw + phi)
+    if kind == "final":
+        return 8 * (2 * ns + 2 * nw)
+    if kind == "prologue":
+        return 8 * (ns + int(np.prod(su)) + 2 * nw + phi)
+    return 0
+
+
+def run_ours(a, ws, rank, local):
+    import torch
+    import paper_2006_07583_b200 as adi
+
+    torch.cuda.set_device(local)
+    stream = torch.cuda.Stream()
+    methods = methods_of(a)
+    n = a.n
+    total_steps = a.warmup + a.steps
+    res = {}
+    solvers = {}
+    for m in methods:
+        p = make_problem(m, n, total_steps + a.steps + 4, a.K)
+        s = adi.AdiSolver(p.nx, p.ny, p.h, p.dt, p.c, m, K=a.K, stream=stream.cuda_stream)
+        s.set_fields(p.U, p.V, p.W)
+        s.set_source(p.phi, p.src, p.gf)
+        s.set_boundary(p.edges, p.gb)
+        solvers[m] = (s, p)
+    # warm-up
+    for m, (s, p) in solvers.items():
+        s.step(a.warmup)
+    torch.cuda.synchronize()
+    for m, (s, p) in solvers.items():
+        s.set_param(adi.ADI_TIMING, 1)
+        s.kernel_times()  # reset
+    # ---- device-timed region: exactly K steps of each method
+    launches0 = sum(s.stats()["kernel_launches"] for s, _ in solvers.values())
+    per = {}
+    with Clocks(local) as clk:
+        for m, (s, p) in solvers.items():
+            barrier(ws)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            s.step(a.steps)
+            e1.record(stream)
+            e1.synchronize()
+            torch.cuda.synchronize()
+            barrier(ws)
+            ms = allmax(ws, e0.elapsed_time(e1))
+            per[m] = ms
+    launches = sum(s.stats()["kernel_launches"] for s, _ in solvers.values()) - launches0
+    clocks = clk.summary()
+    # kernel times (CUDA events around every launch inside the timed region)
+    kt = {m: s.kernel_times() for m, (s, p) in solvers.items()}
+    for m, (s, p) in solvers.items():
+        s.set_param(adi.ADI_TIMING, 0)
+    pts = n * n
+    total_ms = sum(per.values())
+    value = ws * pts * a.steps * len(methods) / (total_ms * 1e-3)
+    peak, peak_src = measured_peaks()
+    traffic = ncu_traffic()
+    per_method = {}
+    dominant = None
+    for m in methods:
+        ksum = {k: v for k, v in kt[m].items() if v[1] > 0}
+        step_ms = per[m] / a.steps
+        tot = sum(v[0] for v in ksum.values())
+        top = max(ksum.items(), key=lambda kv: kv[1][0])
+        kind, (kms, kcnt) = top
+        byt = kernel_bytes(m, n, kind)
+        ach = byt / (kms / kcnt * 1e-3) / 1e9
+        bytes_step = kernel_bytes(m, n, "row") + kernel_bytes(m, n, "col")
+        per_method[MNAME[m]] = {
+            "value": ws * pts * a.steps / (per[m] * 1e-3), "ms_per_step": step_ms,
+            "hbm_gbs_step": bytes_step / (step_ms * 1e-3) / 1e9,
+            "hbm_frac_step": bytes_step / (step_ms * 1e-3) / 1e9 / peak,
+            "kernel_ms_share": {k: round(v[0] / tot, 4) for k, v in ksum.items()},
+            "kernel_avg_ms": {k: v[0] / v[1] for k, v in ksum.items()},
+            "dominant": kind}
+        cand = {"method": MNAME[m], "kind": kind, "achieved": ach, "bytes": byt, "share": kms / tot,
+                "avg_ms": kms / kcnt}
+        if dominant is None or cand["avg_ms"] * kcnt > dominant["avg_ms"] * dominant.get("cnt", 1):
+            dominant = dict(cand, cnt=kcnt)
+    tkey = f"{dominant['method']}_{dominant['kind']}_{n}"
+    roof = {"bound": "hbm", "achieved": round(dominant["achieved"], 1), "peak": peak, "unit": "GB/s",
+            "frac": round(dominant["achieved"] / peak, 4),
+            "traffic": traffic.get(tkey, {}).get("dram_bytes_per_launch"),
+            "kernel": f"adi_tile_kernel[{dominant['method']},{dominant['kind']}]",
+            "algorithmic_bytes_per_launch": dominant["bytes"], "peak_source": peak_src,
+            "avg_launch_ms": round(dominant["avg_ms"], 4)}
+    # ---- end to end through the C-ABI with host buffers (pinned), copies timed
+    e2e = None
+    if not a.no_e2e:
+        e2e_ms = 0.0
+        bi = bo = 0
+        for m, (s, p) in solvers.items():
+            hU = torch.from_numpy(p.U).pin_memory()
+            hV = torch.from_numpy(p.V).pin_memory()
+            hW = torch.from_numpy(p.W).pin_memory()
+            oU, oV, oW = (torch.empty_like(x).pin_memory() for x in (hU, hV, hW))
+            barrier(ws)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            adi.adi_set_fields(s.handle, hU.numpy(), hV.numpy(), hW.numpy())   # H2D, pinned
+            s.step(a.steps)
+            adi.adi_get_fields(s.handle, oU.numpy(), oV.numpy(), oW.numpy())   # D2H, synchronizes
+            t1 = time.perf_counter()
+            barrier(ws)
+            e2e_ms += allmax(ws, (t1 - t0) * 1e3)
+            nb = (hU.numel() + hV.numel() + hW.numel()) * 8
+            bi += nb / a.steps
+            bo += nb / a.steps
+            del hU, hV, hW, oU, oV, oW
+        e2e = {"value": ws * pts * a.steps * len(methods) / (e2e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo),
+               "note": "adi_set_fields(host) + adi_step(K) + adi_get_fields(host), pinned buffers"}
+    for s, _ in solvers.values():
+        s.close()
+    return {"value": value, "ms_per_step": total_ms / a.steps, "roofline": roof, "clocks": clocks,
+            "e2e": e2e, "gpu_launches": launches, "per_method": per_method}
+
+
+# ---------------------------------------------------------------------------
+def oracle_rate(methods, n, steps, K, threads=0):
+    """Oracle pt-updates/s on an n x n sample (bounded CPU work)."""
+    import oracle
+    tot_pts = 0
+    tot_s = 0.0
+    for m in methods:
+        p = make_problem(m, n, steps + 1, K)
+        t0 = time.perf_counter()
+        oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, p.U, p.V, p.W, nsteps=steps,
+                   nthreads=threads, **p.oracle_kwargs())
+        tot_s += time.perf_counter() - t0
+        tot_pts += n * n * steps
+    return tot_pts / tot_s, tot_s
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def main():
+    a = parse()
+    ws, rank, local = dist_setup()
+    methods = methods_of(a)
+    cfg = {"workload": f"config4: single {a.n}x{a.n}-node grid, Gamma=0 harmonic MMS (eq. 11), "
+                       f"dense source, {'+'.join(MNAME[m].upper() for m in methods)}",
+           "grid_nodes": a.n, "methods": [MNAME[m] for m in methods], "K_sweeps": a.K,
+           "cfl": {"cfd": 0.91, "mfd": 0.81}, "l2": "inputs larger than L2 (2.1 GB per field); no flush",
+           "parallelism": "1 GPU" if ws == 1 else f"{ws} independent replica grids (weak)"}
+    if a.impl == "reference":
+        # Reference arm = the CPU oracle as it stands, bounded sample per step.
+        if rank != 0:
+            return
+        import oracle
+        oracle.build()
+        nthr = cpu_cores()
+        n = a.cpu_n
+        for _ in range(a.warmup):
+            oracle_rate(methods, n, 1, a.K, nthr)
+        rate, secs = oracle_rate(methods, n, a.steps, a.K, nthr)
+        line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": ws,
+                "steps": a.steps, "warmup": a.warmup, "ms_per_step": secs * 1e3 / a.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": cfg,
+                "cpu_baseline": {"value": rate, "unit": UNIT, "cores": nthr, "kind": "oracle",
+                                 "sample": f"{n}x{n} nodes, {a.steps} steps per method "
+                                           f"(oracle C, OpenMP over lines)"},
+                "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    r = run_ours(a, ws, rank, local)
+    if rank != 0:
+        return
+    cpu = None
+    if not a.no_cpu and ws == 1:
+        import oracle
+        oracle.build()
+        nthr = cpu_cores()
+        rate, secs = oracle_rate(methods, a.cpu_n, 2, a.K, nthr)
+        cpu = {"value": rate, "unit": UNIT, "cores": nthr, "kind": "oracle",
+               "sample": f"{a.cpu_n}x{a.cpu_n} nodes, 2 steps per method, same MMS data "
+                         f"({secs:.1f} s of CPU time)"}
+    line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": ws, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+            "roofline": r["roofline"], "cpu_baseline": cpu, "clocks": r["clocks"], "e2e": r["e2e"],
+            "gpu_launches": r["gpu_launches"], "per_method": r["per_method"]}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,172 @@
+/*
+ * adi.h — C-ABI of the B200-native Peaceman–Rachford ADI library
+ * (arXiv:2006.07583, Otero, Rojas, Moya & Castillo).  Library: libadi.so.
+ *
+ * The library advances the 2-D velocity–pressure acoustic system (eq. 1,
+ * PAPER.md:57-63) with the Peaceman–Rachford splitting of Crank–Nicolson
+ * (eqs. 4-6).  Each ADI stage resolves its implicit
+ * pressure/velocity coupling with K fixed-point sweeps along grid lines
+ * (eqs. 8-9; Alg. 3/4), K fixed
+ * (default K = k_max = 8).  Two spatial
+ * variants:
+ *   ADI_CFD — nodal compact FD: every derivative is a stencil Q, Q̄ plus a
+ *             tridiagonal solve with P, P̄ (Appendix A).
+ *   ADI_MFD — staggered mimetic FD: D4 / G4 stencils with wide boundary
+ *             closures (Appendix B).
+ * Everything is IEEE fp64.  All compute runs in the library's sm_100a CUDA
+ * kernels; there is no CPU fallback — without a usable CUDA device every
+ * call returns ADI_ECUDA.
+ *
+ * ---------------------------------------------------------------------------
+ * Grid and state layout (row index = y, column index = x; row-major, C order).
+ * nx, ny are node counts per direction (N = n-1 cells, spacing h).
+ *
+ *   CFD (nodal):
+ *     U  : ny x nx            pressure incl. the Dirichlet boundary
+ *     V  : (ny-2) x nx        V̄ = rows 1..ny-2 of the horizontal velocity
+ *     W  : ny x (nx-2)        W̄ = columns 1..nx-2 of the vertical velocity
+ *   MFD (staggered):
+ *     U  : (ny+1) x (nx+1)    pressure on X_cb x Y_cb incl. the boundary
+ *     V  : (ny-1) x nx        V̄: x nodes x y cell centres
+ *     W  : ny x (nx-1)        W̄: y nodes x x cell centres
+ * The velocity lines on the boundary that the paper never updates are not
+ * part of the state.  The pressure-interior block ("I") is
+ * (ny-2) x (nx-2) for CFD and (ny-1) x (nx-1) for MFD.
+ *
+ * Time: step m advances t^m = t0 + m*dt to t^{m+1}.  Source and boundary
+ * time functions are given as tables sampled at HALF steps,
+ * g[j] = g(t0 + j*dt/2), because the method needs t^m, t^m + dt/2 and
+ * t^{m+1}.  A table must cover every step run:
+ * adi_step returns ADI_EINVAL if 2*(m_end) >= ng.  A NULL table means the
+ * constant 1.
+ *
+ * Ownership: the library owns all device memory (cudaMalloc).  Host pointers
+ * are read or written only during the call; tables and patterns are copied.
+ * Device pointers passed to *_device calls must stay valid for the call and
+ * are accessed on the handle's stream.
+ *
+ * Errors: every call returns a status (ADI_OK = 0, negative = error,
+ * positive = warning, state still usable); adi_last_error() gives the
+ * message.  Arguments are validated before any allocation.
+ * Threading: one host thread per handle at a time.
+ * ---------------------------------------------------------------------------
+ */
+#ifndef ADI_H_
+#define ADI_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct adi_ctx* adi_handle;
+
+enum adi_method { ADI_CFD = 0, ADI_MFD = 1 };
+
+enum adi_status {
+  ADI_OK = 0,
+  ADI_EINVAL = -1,      /* bad argument / shape / too small grid (N < 8) / short table */
+  ADI_ENOMEM = -2,      /* device or host allocation failed */
+  ADI_ECUDA = -3,       /* CUDA runtime error (incl. no device) */
+  ADI_EZEROPIVOT = -4,  /* zero pivot in the LU of P or P̄ */
+  ADI_ENONFINITE = -5,  /* a field became NaN/Inf (checked when ADI_CHECK_FINITE=1) */
+  ADI_ESTATE = -6,      /* call out of order (e.g. step before set_fields) */
+  ADI_WUNSTABLE = 1     /* warning: c*dt/h above the inner-iteration limit
+                           (2/sqrt(6) ~ 0.8165 MFD, 2/sqrt(3) ~ 1.155 CFD; SURVEY SA-3) */
+};
+
+enum adi_param {
+  ADI_K_SWEEPS = 0,     /* fixed-point sweeps per stage, integer >= 1; default 8 */
+  ADI_RHO = 1,          /* density rho > 0 (kappa = rho c^2); default 1 */
+  ADI_CHECK_FINITE = 2, /* 1: adi_step synchronizes and checks for NaN/Inf; default 0 */
+  ADI_TILE_CHUNKS = 3,  /* cap on chunks (16 points each) per line in one tile; 0 = auto.
+                           Testing aid: forces the segmented (halo) tiling on small grids. */
+  ADI_TIMING = 4        /* 1: bracket every kernel launch with CUDA events on the handle's
+                           stream (read with adi_get_kernel_times); default 0 */
+};
+
+/* Kernel kinds launched by adi_step (index of adi_get_kernel_times arrays). */
+enum adi_kernel_kind {
+  ADI_KK_PROLOGUE = 0,  /* explicit y-half of the first step of a call (a2) */
+  ADI_KK_ROW = 1,       /* ADI-rows: K sweeps along x + fused C / V^{m+1} (a3, a4) */
+  ADI_KK_COL = 2,       /* ADI-columns: K sweeps along y + fused a2 of the next step (a6) */
+  ADI_KK_FINAL = 3,     /* ADI-columns of the last step of a call, writes U, W̄ (a6) */
+  ADI_KK_EDGE = 4,      /* Dirichlet columns of U */
+  ADI_NKINDS = 5
+};
+
+typedef struct adi_stats {
+  long long steps;      /* steps taken since creation */
+  double t;             /* t0 + steps*dt */
+  int nonfinite;        /* 1 if a non-finite value was produced (needs ADI_CHECK_FINITE) */
+  int k_sweeps;
+  long long kernel_launches; /* kernels launched by adi_step since creation */
+} adi_stats;
+
+/* Create a solver for one grid (batch = 1).  nx, ny >= 9 nodes (N >= 8);
+ * h > 0 grid spacing, dt > 0, c > 0 wave speed; method ADI_CFD or ADI_MFD.
+ * Returns ADI_WUNSTABLE (handle valid) when c*dt/h exceeds the K-sweep
+ * iteration limit.  Fields start at zero, t0 = 0. */
+int adi_create(int nx, int ny, double h, double dt, double c, int method, adi_handle* out);
+
+/* As adi_create with `batch` independent grids ("shots") of the same shape
+ * advanced together by every adi_step (config 5).  Field arrays of the
+ * *_fields calls then hold `batch` consecutive grids. */
+int adi_create_batch(int nx, int ny, double h, double dt, double c, int method, int batch,
+                     adi_handle* out);
+
+int adi_set_param(adi_handle h, int key, double value);
+
+/* Stream on which all work of this handle is enqueued (cudaStream_t as void*;
+ * NULL = the legacy default stream). */
+int adi_set_stream(adi_handle h, void* cuda_stream);
+
+/* Set the state at the current time from HOST arrays (shapes above, times batch). */
+int adi_set_fields(adi_handle h, const double* U, const double* V, const double* W);
+/* Same from DEVICE arrays (contiguous, same shapes). */
+int adi_set_fields_device(adi_handle h, const double* dU, const double* dV, const double* dW);
+
+/* Source term F(x,y,t) of eq. 1 on the pressure-interior points, entering
+ * eqs. 5-6 as dt/2 (F^m + F^{m+1}):
+ *   F = phi(x,y) * g(t)                      if phi != NULL (phi: I-block, host), plus
+ *   F = g(t) / h^2 at U-array point (ix, iy) if ix >= 1 (point source; batch 1).
+ * g: table at half steps, ng entries (NULL: g = 1). */
+int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double* g, int ng);
+
+/* Point sources for a batch: shot b has F = g(t)/h^2 at U-array point (ix[b], iy[b]). */
+int adi_set_point_sources(adi_handle h, const int* ix, const int* iy, const double* g, int ng);
+
+/* Dirichlet data u0 = b(x,y) g(t) on the pressure boundary.
+ * edges: host array of the four U edges concatenated: row 0 (y = 0, length
+ * ncolsU), last row (y = 1, ncolsU), column 0 (x = 0, nrowsU), last column
+ * (x = 1, nrowsU); NULL = homogeneous.  g: table at half steps (NULL: 1). */
+int adi_set_boundary(adi_handle h, const double* edges, const double* g, int ng);
+
+/* Enqueue n >= 0 time steps on the handle's stream (asynchronous unless
+ * ADI_CHECK_FINITE is set). */
+int adi_step(adi_handle h, int n);
+
+/* Copy the state to HOST arrays (synchronizes the stream). */
+int adi_get_fields(adi_handle h, double* U, double* V, double* W);
+/* Copy the state to DEVICE arrays, enqueued on the handle's stream. */
+int adi_get_fields_device(adi_handle h, double* dU, double* dV, double* dW);
+
+int adi_get_stats(adi_handle h, adi_stats* s);
+
+/* With ADI_TIMING = 1: synchronize the stream, then for each kernel kind k < nkinds
+ * return the summed device time ms[k] (CUDA events around each launch) and the
+ * launch count since the previous call; the accumulators are reset.  Either array
+ * may be NULL. */
+int adi_get_kernel_times(adi_handle h, double* ms, long long* launches, int nkinds);
+
+/* Message for the last error on this handle ("" if none); valid until the next call. */
+const char* adi_last_error(adi_handle h);
+
+void adi_destroy(adi_handle h);
+
+/* Library version string and the compiled device architecture ("sm_100a"). */
+const char* adi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADI_H_ */

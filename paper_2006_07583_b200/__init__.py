@@ -1,0 +1,282 @@
+"""B200-native Peaceman–Rachford ADI (arXiv:2006.07583) — Python binding.
+
+A thin ctypes layer over ``libadi.so`` (the C-ABI of ``include/adi.h``).  It
+only marshals arguments: every step of the method runs in the library's
+sm_100a CUDA kernels.  There is no CPU fallback; if the library or a CUDA
+device is missing, calls raise.
+
+Module-level functions carry the C names (``adi_create``, ``adi_step`` ...);
+``AdiSolver`` wraps a handle.  Host arrays are numpy float64 (C order); device
+arrays are anything exposing ``data_ptr()`` (torch CUDA tensors, float64,
+contiguous).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .build import LIB_PATH, build as build_library  # noqa: F401
+
+ADI_CFD = 0
+ADI_MFD = 1
+ADI_OK = 0
+ADI_EINVAL = -1
+ADI_ENOMEM = -2
+ADI_ECUDA = -3
+ADI_EZEROPIVOT = -4
+ADI_ENONFINITE = -5
+ADI_ESTATE = -6
+ADI_WUNSTABLE = 1
+ADI_K_SWEEPS = 0
+ADI_RHO = 1
+ADI_CHECK_FINITE = 2
+ADI_TILE_CHUNKS = 3
+ADI_TIMING = 4
+KERNEL_KINDS = ("prologue", "row", "col", "final", "edge")
+
+_STATUS = {0: "ADI_OK", -1: "ADI_EINVAL", -2: "ADI_ENOMEM", -3: "ADI_ECUDA", -4: "ADI_EZEROPIVOT",
+           -5: "ADI_ENONFINITE", -6: "ADI_ESTATE", 1: "ADI_WUNSTABLE"}
+
+
+class AdiError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{_STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class adi_stats(ctypes.Structure):
+    _fields_ = [("steps", ctypes.c_longlong), ("t", ctypes.c_double), ("nonfinite", ctypes.c_int),
+                ("k_sweeps", ctypes.c_int), ("kernel_launches", ctypes.c_longlong)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libadi.so (built in-tree by ``build()``); raise if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"CUDA extension {LIB_PATH} is missing: run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        I, D, P = ctypes.c_int, ctypes.c_double, ctypes.c_void_p
+        H = ctypes.c_void_p
+        L.adi_create.argtypes = [I, I, D, D, D, I, ctypes.POINTER(H)]
+        L.adi_create_batch.argtypes = [I, I, D, D, D, I, I, ctypes.POINTER(H)]
+        L.adi_set_param.argtypes = [H, I, D]
+        L.adi_set_stream.argtypes = [H, P]
+        L.adi_set_fields.argtypes = [H, P, P, P]
+        L.adi_set_fields_device.argtypes = [H, P, P, P]
+        L.adi_set_source.argtypes = [H, P, I, I, P, I]
+        L.adi_set_point_sources.argtypes = [H, P, P, P, I]
+        L.adi_set_boundary.argtypes = [H, P, P, I]
+        L.adi_step.argtypes = [H, I]
+        L.adi_get_fields.argtypes = [H, P, P, P]
+        L.adi_get_fields_device.argtypes = [H, P, P, P]
+        L.adi_get_stats.argtypes = [H, ctypes.POINTER(adi_stats)]
+        L.adi_get_kernel_times.argtypes = [H, P, P, I]
+        L.adi_last_error.argtypes = [H]
+        L.adi_last_error.restype = ctypes.c_char_p
+        L.adi_destroy.argtypes = [H]
+        L.adi_destroy.restype = None
+        L.adi_version.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+EXPORTS = ["adi_create", "adi_create_batch", "adi_set_param", "adi_set_stream", "adi_set_fields",
+           "adi_set_fields_device", "adi_set_source", "adi_set_point_sources", "adi_set_boundary",
+           "adi_step", "adi_get_fields", "adi_get_fields_device", "adi_get_stats", "adi_get_kernel_times",
+           "adi_last_error",
+           "adi_destroy", "adi_version"]
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return ctypes.c_void_p(a.data_ptr())
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _host(a, dtype=np.float64):
+    return None if a is None else np.ascontiguousarray(a, dtype=dtype)
+
+
+def _check(h, rc, what):
+    if rc < 0:
+        msg = lib().adi_last_error(h).decode() if h else ""
+        raise AdiError(rc, f"{what}: {msg}")
+    return rc
+
+
+# ---- C-named functions ------------------------------------------------------
+def adi_create(nx, ny, h, dt, c, method):
+    return adi_create_batch(nx, ny, h, dt, c, method, 1)
+
+
+def adi_create_batch(nx, ny, h, dt, c, method, batch):
+    hd = ctypes.c_void_p()
+    rc = lib().adi_create_batch(nx, ny, h, dt, c, method, batch, ctypes.byref(hd))
+    _check(None, rc, "adi_create")
+    return hd, rc
+
+
+def adi_set_param(hd, key, value):
+    return _check(hd, lib().adi_set_param(hd, key, float(value)), "adi_set_param")
+
+
+def adi_set_stream(hd, stream_ptr):
+    return _check(hd, lib().adi_set_stream(hd, ctypes.c_void_p(stream_ptr)), "adi_set_stream")
+
+
+def adi_set_fields(hd, U, V, W):
+    U, V, W = _host(U), _host(V), _host(W)
+    return _check(hd, lib().adi_set_fields(hd, _ptr(U), _ptr(V), _ptr(W)), "adi_set_fields")
+
+
+def adi_set_fields_device(hd, dU, dV, dW):
+    return _check(hd, lib().adi_set_fields_device(hd, _ptr(dU), _ptr(dV), _ptr(dW)),
+                  "adi_set_fields_device")
+
+
+def adi_set_source(hd, phi=None, ix=-1, iy=-1, g=None):
+    phi, g = _host(phi), _host(g)
+    return _check(hd, lib().adi_set_source(hd, _ptr(phi), ix, iy, _ptr(g), 0 if g is None else g.size),
+                  "adi_set_source")
+
+
+def adi_set_point_sources(hd, ix, iy, g=None):
+    ix, iy, g = _host(ix, np.int32), _host(iy, np.int32), _host(g)
+    return _check(hd, lib().adi_set_point_sources(hd, _ptr(ix), _ptr(iy), _ptr(g),
+                                                   0 if g is None else g.size), "adi_set_point_sources")
+
+
+def adi_set_boundary(hd, edges=None, g=None):
+    e = None if edges is None else np.concatenate([np.asarray(x, np.float64).ravel() for x in edges])
+    g = _host(g)
+    return _check(hd, lib().adi_set_boundary(hd, _ptr(e), _ptr(g), 0 if g is None else g.size),
+                  "adi_set_boundary")
+
+
+def adi_step(hd, n):
+    return _check(hd, lib().adi_step(hd, int(n)), "adi_step")
+
+
+def adi_get_fields(hd, U, V, W):
+    return _check(hd, lib().adi_get_fields(hd, _ptr(U), _ptr(V), _ptr(W)), "adi_get_fields")
+
+
+def adi_get_fields_device(hd, dU, dV, dW):
+    return _check(hd, lib().adi_get_fields_device(hd, _ptr(dU), _ptr(dV), _ptr(dW)),
+                  "adi_get_fields_device")
+
+
+def adi_get_stats(hd):
+    s = adi_stats()
+    _check(hd, lib().adi_get_stats(hd, ctypes.byref(s)), "adi_get_stats")
+    return {k: getattr(s, k) for k, _ in adi_stats._fields_}
+
+
+def adi_get_kernel_times(hd):
+    """{kind: (ms, launches)} accumulated since the previous call (needs ADI_TIMING=1)."""
+    n = len(KERNEL_KINDS)
+    ms = np.zeros(n)
+    cnt = np.zeros(n, dtype=np.int64)
+    _check(hd, lib().adi_get_kernel_times(hd, _ptr(ms), _ptr(cnt), n), "adi_get_kernel_times")
+    return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNEL_KINDS)}
+
+
+def adi_last_error(hd):
+    return lib().adi_last_error(hd).decode()
+
+
+def adi_destroy(hd):
+    lib().adi_destroy(hd)
+
+
+def adi_version():
+    return lib().adi_version().decode()
+
+
+# ---- convenience wrapper ------------------------------------------------------
+def shapes(method, nx, ny):
+    if method == ADI_CFD:
+        return (ny, nx), (ny - 2, nx), (ny, nx - 2)
+    return (ny + 1, nx + 1), (ny - 1, nx), (ny, nx - 1)
+
+
+class AdiSolver:
+    """One ADI handle (optionally a batch of independent grids)."""
+
+    def __init__(self, nx, ny, h, dt, c, method, *, batch=1, K=8, rho=1.0, check_finite=False,
+                 stream=None):
+        self.nx, self.ny, self.h, self.dt, self.c, self.method, self.batch = nx, ny, h, dt, c, method, batch
+        self.handle, self.create_status = adi_create_batch(nx, ny, h, dt, c, method, batch)
+        adi_set_param(self.handle, ADI_K_SWEEPS, K)
+        adi_set_param(self.handle, ADI_RHO, rho)
+        adi_set_param(self.handle, ADI_CHECK_FINITE, 1 if check_finite else 0)
+        if stream is not None:
+            adi_set_stream(self.handle, stream)
+        self.su, self.sv, self.sw = shapes(method, nx, ny)
+
+    def close(self):
+        if self.handle:
+            adi_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_param(self, key, value):
+        adi_set_param(self.handle, key, value)
+
+    def set_fields(self, U, V, W):
+        if hasattr(U, "data_ptr"):
+            adi_set_fields_device(self.handle, U, V, W)
+        else:
+            adi_set_fields(self.handle, U, V, W)
+
+    def set_source(self, phi=None, point=None, g=None):
+        ix, iy = (-1, -1) if point is None else point
+        adi_set_source(self.handle, phi, ix, iy, g)
+
+    def set_point_sources(self, ix, iy, g=None):
+        adi_set_point_sources(self.handle, ix, iy, g)
+
+    def set_boundary(self, edges=None, g=None):
+        adi_set_boundary(self.handle, edges, g)
+
+    def step(self, n=1):
+        return adi_step(self.handle, n)
+
+    def get_fields(self):
+        B = (self.batch,) if self.batch > 1 else ()
+        U = np.empty(B + self.su)
+        V = np.empty(B + self.sv)
+        W = np.empty(B + self.sw)
+        adi_get_fields(self.handle, U, V, W)
+        return U, V, W
+
+    def get_fields_device(self, U, V, W):
+        adi_get_fields_device(self.handle, U, V, W)
+
+    def stats(self):
+        return adi_get_stats(self.handle)
+
+    def kernel_times(self):
+        return adi_get_kernel_times(self.handle)
+
+    @classmethod
+    def from_problem(cls, p, **kw):
+        """Build a solver from an ``adi_inputs.Problem`` (test/bench helper)."""
+        s = cls(p.nx, p.ny, p.h, p.dt, p.c, p.method, K=p.K, rho=p.rho, **kw)
+        s.set_fields(p.U, p.V, p.W)
+        s.set_source(p.phi, p.src, p.gf)
+        s.set_boundary(p.edges, p.gb)
+        return s

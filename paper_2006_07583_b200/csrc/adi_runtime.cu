@@ -1,0 +1,701 @@
+// adi_runtime.cu — host runtime and C-ABI (include/adi.h) of the B200 ADI
+// library.  Builds the operators of App. A/B once per handle, plans the line
+// tiles, owns the device buffers and enqueues the per-step kernels:
+//
+//   adi_step(n):  PROLOGUE (y)  : U, W̄        -> S1, W*          (a2, Alg.1/2 l.8,10)
+//                 n x { ROW (x) : S1, V̄       -> S2, V̄^{m+1}     (a3+a4, l.11-14)
+//                       COL (y) : S2, W*      -> S1', W*'        (a6 + a2 of m+1, l.15)
+//                 }   the last COL is FINAL   -> U^{m+n}, W̄^{m+n}
+//                 EDGE          : Dirichlet columns of U at t^{m+n}
+//
+// Every arithmetic step runs in the kernels of adi_kernels.cuh.  The host only
+// computes the operator coefficient tables (exact rationals of the paper, LU
+// without pivoting — PAPER.md:113,192) and scalar time factors.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "adi.h"
+#include "adi_kernels.cuh"
+
+namespace adi {
+
+constexpr int TM = 16;    // points per thread chunk
+constexpr int TNT = 256;  // threads per CTA
+
+struct Axis {
+  int n = 0;            // cells along the sweep direction
+  int nlines = 0;       // interior pressure lines swept
+  int NL = 1;
+  int plo = 0, phi = -1;
+  std::vector<Seg> segs;
+  Seg* d_segs = nullptr;
+  double* d_tabU = nullptr;  // CFD only
+  double* d_tabX = nullptr;
+  int* d_ptl = nullptr;      // per batch: point source line / position for this direction
+  int* d_ptp = nullptr;
+};
+
+}  // namespace adi
+
+struct adi_ctx {
+  int method, nx, ny, batch;
+  double h, dt, c, rho;
+  int K = 8;
+  int check_finite = 0;
+  int tile_chunks = 0;  // 0 = auto
+  int timing = 0;
+  struct Rec { int kind; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaStream_t stream = nullptr;
+  // shapes
+  int nxu, nyu, nxi, nyi, nxv, nyv;
+  size_t nU, nV, nW, nS;  // per grid
+  // device buffers
+  double *U = nullptr, *V = nullptr, *W = nullptr;
+  double *V2 = nullptr, *W2 = nullptr, *Sa = nullptr, *Sb = nullptr;
+  double* phi = nullptr;
+  double* edges = nullptr;  // y0 | y1 | x0 | x1
+  int* flag = nullptr;
+  adi::Axis ax, ay;
+  // time tables (host)
+  std::vector<double> gf, gb;
+  bool has_pt = false;
+  long long m = 0;  // steps taken
+  long long launches = 0;
+  bool fields_set = false;
+  int nonfinite = 0;
+  std::string err;
+};
+
+namespace {
+
+const char* kVersion = "adi-b200 0.1 (sm_100a)";
+bool g_const_ready = false;
+
+int fail(adi_ctx* h, int code, const std::string& msg) {
+  if (h) h->err = msg;
+  return code;
+}
+
+#define CUDA_TRY(h, call)                                                                  \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail((h), ADI_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+// ---- constants: MFD closures as the printed rationals (App. B), CFD interior LU
+int init_constants(adi_ctx* h) {
+  if (g_const_ready) return ADI_OK;
+  const double d4r0[6] = {-4751.0 / 5192.0, 909.0 / 1298.0, 6091.0 / 15576.0,
+                          -1165.0 / 5192.0, 129.0 / 2596.0, -25.0 / 15576.0};
+  const double g4r0[6] = {-47888.0 / 14245.0, 1790.0 / 407.0, -14545.0 / 9768.0,
+                          8997.0 / 16280.0, -2335.0 / 22792.0, 25.0 / 9768.0};
+  const double g4r1[5] = {16.0 / 105.0, -31.0 / 24.0, 29.0 / 24.0, -3.0 / 40.0, 1.0 / 168.0};
+  CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_d4r0, d4r0, sizeof d4r0));
+  CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_g4r0, g4r0, sizeof g4r0));
+  CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_g4r1, g4r1, sizeof g4r1));
+  // interior rows (1, 4, 1): the no-pivot LU recursion d <- 4 - 1/d converges to 2+sqrt(3)
+  double d = 4.0;
+  for (int i = 0; i < 200; ++i) d = 4.0 - 1.0 / d;
+  const double l = 1.0 / d, invd = 1.0 / d;
+  const int M = adi::TM;
+  double G[adi::MMAX], Kc[adi::MMAX], Jc[adi::MMAX];
+  double g = 1.0;
+  for (int i = 0; i < M; ++i) { g *= -l; G[i] = g; }
+  double k = 0.0, j = 1.0;
+  for (int i = M - 1; i >= 0; --i) {
+    k = (G[i] - k) * invd;  // c = 1
+    j *= -invd;
+    Kc[i] = k;
+    Jc[i] = j;
+  }
+  for (int i = M; i < adi::MMAX; ++i) Kc[i] = Jc[i] = 0.0;
+  const double F = G[M - 1], Ks = Kc[0], Ke = Kc[M - 1], Js = Jc[0], Je = Jc[M - 1];
+  CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cl, &l, sizeof l));
+  CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cinvd, &invd, sizeof invd));
+  CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cK, Kc, sizeof Kc));
+  CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cJ, Jc, sizeof Jc));
+  CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cF, &F, sizeof F));
+  CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cKs, &Ks, sizeof Ks));
+  CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cKe, &Ke, sizeof Ke));
+  CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cJs, &Js, sizeof Js));
+  CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cJe, &Je, sizeof Je));
+  g_const_ready = true;
+  return ADI_OK;
+}
+
+// ---- CFD LU tables (position-indexed, 3 x (n+1)): l, 1/d, c.  P̄ (u-op) lives on
+// positions 1..n-1 (eq. 14), P (x-op) on 0..n (eq. 12); LU without pivoting.
+bool cfd_table(int n, bool bar, std::vector<double>& tab, double& maxdev_lo, int& plo) {
+  const int np1 = n + 1;
+  tab.assign(3 * np1, 0.0);
+  const int p0 = bar ? 1 : 0, p1 = bar ? n - 1 : n;
+  std::vector<double> a(np1, 1.0), bb(np1, 4.0), cc(np1, 1.0);
+  if (bar) { bb[1] = 6; cc[1] = 6; a[n - 1] = 6; bb[n - 1] = 6; cc[n - 1] = 0; }
+  else { bb[0] = 6; cc[0] = 18; a[n] = 18; bb[n] = 6; cc[n] = 0; }
+  double dprev = 0.0;
+  for (int p = p0; p <= p1; ++p) {
+    double l = (p == p0) ? 0.0 : a[p] / dprev;
+    double d = bb[p] - l * ((p == p0) ? 0.0 : cc[p - 1]);
+    if (d == 0.0) return false;
+    tab[p] = l;
+    tab[np1 + p] = 1.0 / d;
+    tab[2 * np1 + p] = (p == p1) ? 0.0 : cc[p];
+    dprev = d;
+  }
+  // first position from which (l, 1/d) equal the interior constants to 2 ulp
+  double dstar = 4.0;
+  for (int i = 0; i < 200; ++i) dstar = 4.0 - 1.0 / dstar;
+  plo = p1;
+  for (int p = p0 + 1; p < p1; ++p) {
+    bool ok = true;
+    for (int q = p; q < std::min(p1, p + 8); ++q)
+      ok = ok && std::fabs(tab[np1 + q] * dstar - 1.0) < 5e-16 && std::fabs(tab[q] * dstar - 1.0) < 5e-16;
+    if (ok) { plo = p; break; }
+  }
+  maxdev_lo = 0.0;
+  return true;
+}
+
+// ---- tile planning along one axis
+bool plan_axis(adi::Axis& A, int method, int nlmin, int cap) {
+  const int M = adi::TM, NT = adi::TNT;
+  const int chmax = cap > 0 ? std::min(cap, NT / nlmin) : NT / nlmin;
+  const int P = A.n + 1;                       // positions 0..n
+  const int halo = (method == ADI_CFD) ? 64 : 32;
+  A.segs.clear();
+  const int D = (M - P % M) % M;
+  const int nch1 = (P + D) / M;
+  if (nch1 <= chmax) {
+    int pw = 1;
+    while (pw < nch1) pw <<= 1;
+    A.NL = std::min(64, std::max(nlmin, NT / pw));  // exchange pad grows with NL
+    A.segs.push_back({-(D / 2), nch1, 0, P});
+    return true;
+  }
+  A.NL = nlmin;
+  const int CH = chmax;
+  for (int S = 2; S <= P / M; ++S) {
+    std::vector<adi::Seg> segs;
+    bool fits = true;
+    for (int s = 0; s < S; ++s) {
+      const int lo = (int)((long long)s * P / S), hi = (int)((long long)(s + 1) * P / S);
+      adi::Seg g;
+      g.out_lo = lo;
+      g.out_hi = hi;
+      if (s == 0) { g.start = 0; g.nchunks = (hi + halo + M - 1) / M; }
+      else if (s == S - 1) { g.nchunks = (P - lo + halo + M - 1) / M; g.start = P - g.nchunks * M; }
+      else { g.start = lo - halo; g.nchunks = (hi - lo + 2 * halo + M - 1) / M; }
+      // only the first tile may contain the line start, only the last the line end
+      if ((s > 0 && g.start < 1) || (s < S - 1 && g.start + g.nchunks * M > P - 1)) return false;
+      if (g.nchunks > CH) fits = false;
+      segs.push_back(g);
+    }
+    if (fits) { A.segs = segs; return true; }
+  }
+  return false;
+}
+
+int setup_axis(adi_ctx* h, adi::Axis& A, int n, int nlines, int nlmin) {
+  A.n = n;
+  A.nlines = nlines;
+  if (!plan_axis(A, h->method, nlmin, h->tile_chunks))
+    return fail(h, ADI_EINVAL, "tile planning failed (grid too small for the tile cap)");
+  if (A.d_segs) { cudaFree(A.d_segs); A.d_segs = nullptr; }
+  if (A.d_tabU) { cudaFree(A.d_tabU); A.d_tabU = nullptr; }
+  if (A.d_tabX) { cudaFree(A.d_tabX); A.d_tabX = nullptr; }
+  if (h->method == ADI_CFD) {
+    std::vector<double> tu, tx;
+    double dev;
+    int plo_u, plo_x;
+    if (!cfd_table(n, true, tu, dev, plo_u) || !cfd_table(n, false, tx, dev, plo_x))
+      return fail(h, ADI_EZEROPIVOT, "zero pivot in the LU of P or P-bar");
+    A.plo = std::max(std::max(plo_u, plo_x), 2);
+    A.phi = n - 2;
+    CUDA_TRY(h, cudaMalloc(&A.d_tabU, tu.size() * sizeof(double)));
+    CUDA_TRY(h, cudaMalloc(&A.d_tabX, tx.size() * sizeof(double)));
+    CUDA_TRY(h, cudaMemcpy(A.d_tabU, tu.data(), tu.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CUDA_TRY(h, cudaMemcpy(A.d_tabX, tx.data(), tx.size() * sizeof(double), cudaMemcpyHostToDevice));
+  } else {
+    A.plo = 2;
+    A.phi = n - 2;
+  }
+  CUDA_TRY(h, cudaMalloc(&A.d_segs, A.segs.size() * sizeof(adi::Seg)));
+  CUDA_TRY(h, cudaMemcpy(A.d_segs, A.segs.data(), A.segs.size() * sizeof(adi::Seg),
+                         cudaMemcpyHostToDevice));
+  return ADI_OK;
+}
+
+cudaEvent_t take_event(adi_ctx* h) {
+  if (!h->pool.empty()) {
+    cudaEvent_t e = h->pool.back();
+    h->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+// bracket a launch with events when timing is on
+struct TimeScope {
+  adi_ctx* h;
+  int kind;
+  cudaEvent_t a = nullptr;
+  TimeScope(adi_ctx* hh, int k) : h(hh), kind(k) {
+    if (h->timing) { a = take_event(h); cudaEventRecord(a, h->stream); }
+  }
+  ~TimeScope() {
+    if (h->timing) {
+      cudaEvent_t b = take_event(h);
+      cudaEventRecord(b, h->stream);
+      h->recs.push_back({kind, a, b});
+    }
+  }
+};
+
+template <int METHOD, int MODE>
+int launch_t(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
+  auto kern = adi::adi_tile_kernel<METHOD, adi::TM, adi::TNT, MODE>;
+  const size_t smem = (size_t)(2 * adi::DYN + adi::NSTAT) * (adi::TNT + 4 * A.NL) * sizeof(double);
+  static bool attr[2][3] = {};
+  if (!attr[METHOD][MODE]) {
+    CUDA_TRY(h, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr[METHOD][MODE] = true;
+  }
+  dim3 grid((A.nlines + A.NL - 1) / A.NL, (unsigned)A.segs.size(), h->batch);
+  kern<<<grid, adi::TNT, smem, h->stream>>>(p);
+  CUDA_TRY(h, cudaGetLastError());
+  h->launches++;
+  return ADI_OK;
+}
+
+int launch(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p, int kind) {
+  TimeScope ts(h, kind);
+  if (h->method == ADI_CFD) {
+    if (mode == adi::KM_SWEEP) return launch_t<adi::M_CFD, adi::KM_SWEEP>(h, A, p);
+    if (mode == adi::KM_FINAL) return launch_t<adi::M_CFD, adi::KM_FINAL>(h, A, p);
+    return launch_t<adi::M_CFD, adi::KM_PROLOGUE>(h, A, p);
+  }
+  if (mode == adi::KM_SWEEP) return launch_t<adi::M_MFD, adi::KM_SWEEP>(h, A, p);
+  if (mode == adi::KM_FINAL) return launch_t<adi::M_MFD, adi::KM_FINAL>(h, A, p);
+  return launch_t<adi::M_MFD, adi::KM_PROLOGUE>(h, A, p);
+}
+
+// Dirichlet columns (x = 0, x = 1) of U at time factor gb, all rows (corners included)
+__global__ void edge_cols_kernel(double* U, int nyu, int nxu, long long ubatch,
+                                 const double* ex0, const double* ex1, double gb) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nyu) return;
+  double* Ub = U + blockIdx.y * ubatch + (long long)r * nxu;
+  Ub[0] = ex0 ? ex0[r] * gb : 0.0;
+  Ub[nxu - 1] = ex1 ? ex1[r] * gb : 0.0;
+}
+// Dirichlet rows (y = 0, y = 1) of U, all columns (used by adi_set_boundary consistency)
+__global__ void edge_rows_kernel(double* U, int nyu, int nxu, long long ubatch,
+                                 const double* ey0, const double* ey1, double gb) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nxu) return;
+  double* Ub = U + blockIdx.y * ubatch;
+  Ub[i] = ey0 ? ey0[i] * gb : 0.0;
+  Ub[(long long)(nyu - 1) * nxu + i] = ey1 ? ey1[i] * gb : 0.0;
+}
+
+double tabv(const std::vector<double>& g, long long j) { return g.empty() ? 1.0 : g[(size_t)j]; }
+
+adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
+  adi::KParams p;
+  std::memset(&p, 0, sizeof p);
+  p.n = A.n;
+  p.nlines = A.nlines;
+  p.NL = A.NL;
+  p.plo = A.plo;
+  p.phi = A.phi;
+  p.segs = A.d_segs;
+  if (!ydir) {
+    p.s_line = h->nxi; p.s_pt = 1;
+    p.x_line = h->nxv; p.x_pt = 1;
+    p.u_line = h->nxu; p.u_pt = 1;
+    p.edgeL = h->edges ? h->edges + 2 * h->nxu : nullptr;
+    p.edgeR = h->edges ? h->edges + 2 * h->nxu + h->nyu : nullptr;
+  } else {
+    p.s_line = 1; p.s_pt = h->nxi;
+    p.x_line = 1; p.x_pt = h->nxi;
+    p.u_line = 1; p.u_pt = h->nxu;
+    p.edgeL = h->edges ? h->edges : nullptr;
+    p.edgeR = h->edges ? h->edges + h->nxu : nullptr;
+  }
+  p.s_batch = (long long)h->nS;
+  p.x_batch = (long long)(ydir ? h->nW : h->nV);
+  p.u_batch = (long long)h->nU;
+  p.phi_src = h->phi;
+  p.pt_line = h->has_pt ? A.d_ptl : nullptr;
+  p.pt_pos = h->has_pt ? A.d_ptp : nullptr;
+  p.pt_amp = 1.0 / (h->h * h->h);
+  const double kappa = h->rho * h->c * h->c;
+  const double alpha = kappa * h->dt / 2.0, beta = h->dt / (2.0 * h->rho);
+  const double f = (h->method == ADI_CFD) ? 3.0 : 1.0;
+  p.cu = f * alpha / h->h;
+  p.cx = f * beta / h->h;
+  p.half_dt = h->dt / 2.0;
+  p.K = h->K;
+  p.tabU = A.d_tabU;
+  p.tabX = A.d_tabX;
+  p.flag = h->flag;
+  return p;
+}
+
+void free_ctx(adi_ctx* h) {
+  for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : h->pool) cudaEventDestroy(e);
+  for (void* q : {(void*)h->U, (void*)h->V, (void*)h->W, (void*)h->V2, (void*)h->W2,
+                  (void*)h->Sa, (void*)h->Sb, (void*)h->phi, (void*)h->edges, (void*)h->flag})
+    if (q) cudaFree(q);
+  for (adi::Axis* A : {&h->ax, &h->ay})
+    for (void* q : {(void*)A->d_segs, (void*)A->d_tabU, (void*)A->d_tabX, (void*)A->d_ptl,
+                    (void*)A->d_ptp})
+      if (q) cudaFree(q);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* adi_version(void) { return kVersion; }
+
+int adi_create_batch(int nx, int ny, double hh, double dt, double c, int method, int batch,
+                     adi_handle* out) {
+  if (!out) return ADI_EINVAL;
+  *out = nullptr;
+  if (method != ADI_CFD && method != ADI_MFD) return ADI_EINVAL;
+  if (nx < 9 || ny < 9 || batch < 1) return ADI_EINVAL;
+  if (!(hh > 0) || !(dt > 0) || !(c > 0) || !std::isfinite(hh) || !std::isfinite(dt) ||
+      !std::isfinite(c))
+    return ADI_EINVAL;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return ADI_ECUDA;
+  }
+  adi_ctx* h = new adi_ctx();
+  h->method = method; h->nx = nx; h->ny = ny; h->batch = batch;
+  h->h = hh; h->dt = dt; h->c = c; h->rho = 1.0;
+  if (method == ADI_CFD) {
+    h->nxu = nx; h->nyu = ny; h->nxi = nx - 2; h->nyi = ny - 2;
+  } else {
+    h->nxu = nx + 1; h->nyu = ny + 1; h->nxi = nx - 1; h->nyi = ny - 1;
+  }
+  h->nxv = nx; h->nyv = ny;
+  h->nU = (size_t)h->nyu * h->nxu;
+  h->nV = (size_t)h->nyi * h->nxv;
+  h->nW = (size_t)h->nyv * h->nxi;
+  h->nS = (size_t)h->nyi * h->nxi;
+  int rc = init_constants(h);
+  auto bail = [&](int code) {
+    free_ctx(h);
+    delete h;
+    return code;
+  };
+  if (rc) return bail(rc);
+  const size_t B = (size_t)batch;
+  if (cudaMalloc(&h->U, B * h->nU * 8) || cudaMalloc(&h->V, B * h->nV * 8) ||
+      cudaMalloc(&h->W, B * h->nW * 8) || cudaMalloc(&h->V2, B * h->nV * 8) ||
+      cudaMalloc(&h->W2, B * h->nW * 8) || cudaMalloc(&h->Sa, B * h->nS * 8) ||
+      cudaMalloc(&h->Sb, B * h->nS * 8) || cudaMalloc(&h->flag, sizeof(int))) {
+    cudaGetLastError();
+    return bail(ADI_ENOMEM);
+  }
+  cudaMemset(h->U, 0, B * h->nU * 8);
+  cudaMemset(h->V, 0, B * h->nV * 8);
+  cudaMemset(h->W, 0, B * h->nW * 8);
+  cudaMemset(h->flag, 0, sizeof(int));
+  if ((rc = setup_axis(h, h->ax, nx - 1, h->nyi, 1))) return bail(rc);
+  if ((rc = setup_axis(h, h->ay, ny - 1, h->nxi, 4))) return bail(rc);
+  if (cudaDeviceSynchronize() != cudaSuccess) return bail(ADI_ECUDA);
+  h->fields_set = true;  // zero fields are a valid state
+  *out = h;
+  const double cfl = c * dt / hh;
+  const double lim = (method == ADI_MFD) ? 2.0 / std::sqrt(6.0) : 2.0 / std::sqrt(3.0);
+  if (cfl > lim) {
+    h->err = "c*dt/h above the inner-iteration limit";
+    return ADI_WUNSTABLE;
+  }
+  return ADI_OK;
+}
+
+int adi_create(int nx, int ny, double hh, double dt, double c, int method, adi_handle* out) {
+  return adi_create_batch(nx, ny, hh, dt, c, method, 1, out);
+}
+
+int adi_set_param(adi_handle h, int key, double v) {
+  if (!h) return ADI_EINVAL;
+  h->err.clear();
+  if (key == ADI_K_SWEEPS) {
+    if (!(v >= 1) || v != std::floor(v) || v > 1000) return fail(h, ADI_EINVAL, "K must be an integer >= 1");
+    h->K = (int)v;
+  } else if (key == ADI_RHO) {
+    if (!(v > 0) || !std::isfinite(v)) return fail(h, ADI_EINVAL, "rho must be > 0");
+    h->rho = v;
+  } else if (key == ADI_CHECK_FINITE) {
+    h->check_finite = (v != 0);
+  } else if (key == ADI_TIMING) {
+    h->timing = (v != 0);
+  } else if (key == ADI_TILE_CHUNKS) {
+    if (!(v >= 0) || v != std::floor(v)) return fail(h, ADI_EINVAL, "tile chunks must be >= 0");
+    h->tile_chunks = (int)v;
+    int rc = setup_axis(h, h->ax, h->nx - 1, h->nyi, 1);
+    if (!rc) rc = setup_axis(h, h->ay, h->ny - 1, h->nxi, 4);
+    if (rc) return rc;
+  } else {
+    return fail(h, ADI_EINVAL, "unknown parameter");
+  }
+  return ADI_OK;
+}
+
+int adi_set_stream(adi_handle h, void* s) {
+  if (!h) return ADI_EINVAL;
+  h->stream = (cudaStream_t)s;
+  return ADI_OK;
+}
+
+static int set_fields_impl(adi_handle h, const double* U, const double* V, const double* W,
+                           cudaMemcpyKind kind) {
+  if (!h) return ADI_EINVAL;
+  h->err.clear();
+  if (!U || !V || !W) return fail(h, ADI_EINVAL, "null field pointer");
+  const size_t B = (size_t)h->batch;
+  CUDA_TRY(h, cudaMemcpyAsync(h->U, U, B * h->nU * 8, kind, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(h->V, V, B * h->nV * 8, kind, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(h->W, W, B * h->nW * 8, kind, h->stream));
+  if (kind == cudaMemcpyHostToDevice) CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  h->fields_set = true;
+  return ADI_OK;
+}
+
+int adi_set_fields(adi_handle h, const double* U, const double* V, const double* W) {
+  return set_fields_impl(h, U, V, W, cudaMemcpyHostToDevice);
+}
+int adi_set_fields_device(adi_handle h, const double* U, const double* V, const double* W) {
+  return set_fields_impl(h, U, V, W, cudaMemcpyDeviceToDevice);
+}
+
+static int set_points(adi_handle h, const int* ix, const int* iy) {
+  // x-direction lines are interior rows (line = iy-1, pos = ix); y-direction: line = ix-1, pos = iy
+  const int B = h->batch;
+  std::vector<int> xl(B), xp(B), yl(B), yp(B);
+  const int uhx = (h->method == ADI_CFD) ? h->nx - 2 : h->nx - 1;
+  const int uhy = (h->method == ADI_CFD) ? h->ny - 2 : h->ny - 1;
+  for (int b = 0; b < B; ++b) {
+    if (ix[b] < 1 || ix[b] > uhx || iy[b] < 1 || iy[b] > uhy)
+      return fail(h, ADI_EINVAL, "point source outside the pressure interior");
+    xl[b] = iy[b] - 1; xp[b] = ix[b];
+    yl[b] = ix[b] - 1; yp[b] = iy[b];
+  }
+  for (adi::Axis* A : {&h->ax, &h->ay}) {
+    if (!A->d_ptl) {
+      CUDA_TRY(h, cudaMalloc(&A->d_ptl, B * sizeof(int)));
+      CUDA_TRY(h, cudaMalloc(&A->d_ptp, B * sizeof(int)));
+    }
+  }
+  CUDA_TRY(h, cudaMemcpy(h->ax.d_ptl, xl.data(), B * sizeof(int), cudaMemcpyHostToDevice));
+  CUDA_TRY(h, cudaMemcpy(h->ax.d_ptp, xp.data(), B * sizeof(int), cudaMemcpyHostToDevice));
+  CUDA_TRY(h, cudaMemcpy(h->ay.d_ptl, yl.data(), B * sizeof(int), cudaMemcpyHostToDevice));
+  CUDA_TRY(h, cudaMemcpy(h->ay.d_ptp, yp.data(), B * sizeof(int), cudaMemcpyHostToDevice));
+  h->has_pt = true;
+  return ADI_OK;
+}
+
+int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double* g, int ng) {
+  if (!h) return ADI_EINVAL;
+  h->err.clear();
+  if (g && ng < 1) return fail(h, ADI_EINVAL, "empty source table");
+  if (ix >= 1 && h->batch != 1) return fail(h, ADI_EINVAL, "use adi_set_point_sources for a batch");
+  if (phi) {
+    if (!h->phi) CUDA_TRY(h, cudaMalloc(&h->phi, h->nS * 8));
+    CUDA_TRY(h, cudaMemcpy(h->phi, phi, h->nS * 8, cudaMemcpyHostToDevice));
+  } else if (h->phi) {
+    cudaFree(h->phi);
+    h->phi = nullptr;
+  }
+  h->has_pt = false;
+  if (ix >= 1) {
+    int rc = set_points(h, &ix, &iy);
+    if (rc) return rc;
+  }
+  h->gf.assign(g ? g : nullptr, g ? g + ng : nullptr);
+  return ADI_OK;
+}
+
+int adi_set_point_sources(adi_handle h, const int* ix, const int* iy, const double* g, int ng) {
+  if (!h || !ix || !iy) return ADI_EINVAL;
+  h->err.clear();
+  if (g && ng < 1) return fail(h, ADI_EINVAL, "empty source table");
+  int rc = set_points(h, ix, iy);
+  if (rc) return rc;
+  h->gf.assign(g ? g : nullptr, g ? g + ng : nullptr);
+  return ADI_OK;
+}
+
+int adi_set_boundary(adi_handle h, const double* edges, const double* g, int ng) {
+  if (!h) return ADI_EINVAL;
+  h->err.clear();
+  if (g && ng < 1) return fail(h, ADI_EINVAL, "empty boundary table");
+  const size_t ne = 2 * (size_t)h->nxu + 2 * (size_t)h->nyu;
+  if (edges) {
+    if (!h->edges) CUDA_TRY(h, cudaMalloc(&h->edges, ne * 8));
+    CUDA_TRY(h, cudaMemcpy(h->edges, edges, ne * 8, cudaMemcpyHostToDevice));
+  } else if (h->edges) {
+    cudaFree(h->edges);
+    h->edges = nullptr;
+  }
+  h->gb.assign(g ? g : nullptr, g ? g + ng : nullptr);
+  return ADI_OK;
+}
+
+int adi_step(adi_handle h, int nsteps) {
+  if (!h) return ADI_EINVAL;
+  h->err.clear();
+  if (nsteps < 0) return fail(h, ADI_EINVAL, "n < 0");
+  if (nsteps == 0) return ADI_OK;
+  if (!h->fields_set) return fail(h, ADI_ESTATE, "fields not set");
+  const long long m0 = h->m, m1 = h->m + nsteps;
+  if (!h->gf.empty() && (long long)h->gf.size() < 2 * m1 + 1)
+    return fail(h, ADI_EINVAL, "source table too short for the requested steps");
+  if (!h->gb.empty() && (long long)h->gb.size() < 2 * m1 + 1)
+    return fail(h, ADI_EINVAL, "boundary table too short for the requested steps");
+  int rc;
+  // a2 (standalone once per call): S1 = U - alpha D̄_y W + dt/2 F(t^m), W* = W - beta D_y U
+  {
+    adi::KParams p = base_params(h, h->ay, true);
+    p.U_in = h->U;
+    p.X_in = h->W; p.X_out = h->W2;
+    p.S_out = h->Sa;
+    p.gf = tabv(h->gf, 2 * m0);
+    if ((rc = launch(h, adi::KM_PROLOGUE, h->ay, p, ADI_KK_PROLOGUE))) return rc;
+  }
+  double* Vcur = h->V; double* Valt = h->V2;
+  double* Wcur = h->W2; double* Walt = h->W;
+  for (long long m = m0; m < m1; ++m) {
+    const bool last = (m + 1 == m1);
+    {  // ADI-rows + C / V^{m+1}
+      adi::KParams p = base_params(h, h->ax, false);
+      p.S_in = h->Sa; p.S_out = h->Sb;
+      p.X_in = Vcur; p.X_out = Valt;
+      p.gb = tabv(h->gb, 2 * m + 1);
+      p.gf = tabv(h->gf, 2 * m + 2);
+      if ((rc = launch(h, adi::KM_SWEEP, h->ax, p, ADI_KK_ROW))) return rc;
+      std::swap(Vcur, Valt);
+    }
+    {  // ADI-columns (+ the explicit y-half of step m+1 unless last)
+      adi::KParams p = base_params(h, h->ay, true);
+      p.S_in = h->Sb;
+      p.X_in = Wcur;
+      p.gb = tabv(h->gb, 2 * m + 2);
+      p.gf = tabv(h->gf, 2 * m + 2);
+      if (last) {
+        p.U_out = h->U;
+        p.X_out = h->W;  // Wcur is W2 or W; FINAL writes the canonical W (Wcur != W when last? see below)
+        if (Wcur == h->W) p.X_out = h->W2;
+        if ((rc = launch(h, adi::KM_FINAL, h->ay, p, ADI_KK_FINAL))) return rc;
+        if (Wcur == h->W) std::swap(h->W, h->W2);
+      } else {
+        p.S_out = h->Sa;
+        p.X_out = Walt;
+        if ((rc = launch(h, adi::KM_SWEEP, h->ay, p, ADI_KK_COL))) return rc;
+        std::swap(Wcur, Walt);
+      }
+    }
+  }
+  if (Vcur != h->V) std::swap(h->V, h->V2);
+  {  // Dirichlet columns of U^{m1}
+    dim3 g((h->nyu + 255) / 256, h->batch);
+    const double* ex0 = h->edges ? h->edges + 2 * h->nxu : nullptr;
+    const double* ex1 = h->edges ? h->edges + 2 * h->nxu + h->nyu : nullptr;
+    TimeScope ts(h, ADI_KK_EDGE);
+    edge_cols_kernel<<<g, 256, 0, h->stream>>>(h->U, h->nyu, h->nxu, (long long)h->nU, ex0, ex1,
+                                                tabv(h->gb, 2 * m1));
+    CUDA_TRY(h, cudaGetLastError());
+    h->launches++;
+    // corner-free rows y = 0, 1 are written by the FINAL column kernel; the two
+    // corner columns are covered above.
+  }
+  h->m = m1;
+  if (h->check_finite) {
+    int f = 0;
+    CUDA_TRY(h, cudaMemcpyAsync(&f, h->flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if (f) {
+      h->nonfinite = 1;
+      return fail(h, ADI_ENONFINITE, "non-finite value in the fields");
+    }
+  }
+  return ADI_OK;
+}
+
+static int get_fields_impl(adi_handle h, double* U, double* V, double* W, cudaMemcpyKind kind) {
+  if (!h) return ADI_EINVAL;
+  h->err.clear();
+  if (!U || !V || !W) return fail(h, ADI_EINVAL, "null field pointer");
+  const size_t B = (size_t)h->batch;
+  CUDA_TRY(h, cudaMemcpyAsync(U, h->U, B * h->nU * 8, kind, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(V, h->V, B * h->nV * 8, kind, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(W, h->W, B * h->nW * 8, kind, h->stream));
+  if (kind == cudaMemcpyDeviceToHost) CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  return ADI_OK;
+}
+
+int adi_get_fields(adi_handle h, double* U, double* V, double* W) {
+  return get_fields_impl(h, U, V, W, cudaMemcpyDeviceToHost);
+}
+int adi_get_fields_device(adi_handle h, double* U, double* V, double* W) {
+  return get_fields_impl(h, U, V, W, cudaMemcpyDeviceToDevice);
+}
+
+int adi_get_stats(adi_handle h, adi_stats* s) {
+  if (!h || !s) return ADI_EINVAL;
+  s->steps = h->m;
+  s->t = h->m * h->dt;
+  s->nonfinite = h->nonfinite;
+  s->k_sweeps = h->K;
+  s->kernel_launches = h->launches;
+  return ADI_OK;
+}
+
+int adi_get_kernel_times(adi_handle h, double* ms, long long* launches, int nkinds) {
+  if (!h || nkinds < 0) return ADI_EINVAL;
+  h->err.clear();
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  for (int k = 0; k < nkinds; ++k) {
+    if (ms) ms[k] = 0.0;
+    if (launches) launches[k] = 0;
+  }
+  for (auto& r : h->recs) {
+    float t = 0.f;
+    CUDA_TRY(h, cudaEventElapsedTime(&t, r.a, r.b));
+    if (r.kind < nkinds) {
+      if (ms) ms[r.kind] += t;
+      if (launches) launches[r.kind] += 1;
+    }
+    h->pool.push_back(r.a);
+    h->pool.push_back(r.b);
+  }
+  h->recs.clear();
+  return ADI_OK;
+}
+
+const char* adi_last_error(adi_handle h) { return h ? h->err.c_str() : "null handle"; }
+
+void adi_destroy(adi_handle h) {
+  if (!h) return;
+  free_ctx(h);
+  delete h;
+}
+
+}  // extern "C"

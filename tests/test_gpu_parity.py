@@ -1,0 +1,199 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle, element by
+element on the same seeded inputs.  Tolerance: relative L2 <= 1e-12 per field
+(BASELINE.json north_star).  CFD runs are limited to horizons where round-off
+amplification of the literal CFD reading stays below that bound (DESIGN.md §4,
+SURVEY §8c P10); the 200-step config-1 run is checked against the oracle's own
+round-off sensitivity instead."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from adi_inputs import CFD, MFD, MMS, mms_problem, random_problem, ricker_problem
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def adi():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2006_07583_b200 as m
+    m.lib()
+    return m
+
+
+def run_oracle(p, nsteps, **over):
+    kw = p.oracle_kwargs()
+    kw.update(over)
+    return oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, p.U, p.V, p.W, nsteps=nsteps, **kw)
+
+
+def run_gpu(adi, p, nsteps, chunks=0, split=None):
+    s = adi.AdiSolver.from_problem(p)
+    if chunks:
+        s.set_param(adi.ADI_TILE_CHUNKS, chunks)
+    if split:
+        for k in split:
+            s.step(k)
+    else:
+        s.step(nsteps)
+    out = s.get_fields()
+    s.close()
+    return out
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def assert_parity(g, o, tol=TOL, what="", floor=None):
+    """rel L2 per field <= tol; where ``floor`` (the oracle's own relative change
+    under a 1-ulp input perturbation, per field) is given, <= max(tol, 10*floor):
+    a comparison cannot be better conditioned than the problem."""
+    for k, (name, a, b) in enumerate(zip("UVW", g, o)):
+        r = rel(a, b)
+        lim = tol if floor is None else max(tol, 10 * floor[k])
+        assert r <= lim, f"{what} {name}: rel L2 {r:.3e} > {lim:.1e}"
+
+
+def oracle_sensitivity(p, nsteps, o):
+    """Relative change of the oracle's result when U0 is perturbed by 1 ulp."""
+    import copy
+    q = copy.copy(p)
+    q.U = p.U * (1 + 2.0 ** -52)
+    o2 = run_oracle(q, nsteps)
+    return [rel(c, b) for c, b in zip(o2, o)]
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+@pytest.mark.parametrize("n", [9, 17, 33, 41, 100])
+def test_random_parity_small(adi, method, n):
+    """Random state, dense source, boundary data; single-tile lines incl. N=8 and ragged ends."""
+    p = random_problem(method, n, seed=n, steps=3)
+    assert_parity(run_gpu(adi, p, 3), run_oracle(p, 3), what=f"n={n}")
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+@pytest.mark.parametrize("n,chunks", [(301, 16), (517, 17), (1001, 20)])
+def test_random_parity_segmented(adi, method, n, chunks):
+    """Forced multi-segment tiling with halos: still exact to round-off."""
+    p = random_problem(method, n, seed=3 * n, steps=2)
+    assert_parity(run_gpu(adi, p, 2, chunks=chunks), run_oracle(p, 2), what=f"n={n} cap={chunks}")
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+def test_parity_default_tiling_large(adi, method):
+    """A grid whose column sweep is segmented by the default planner (lines > 1024 points)."""
+    p = random_problem(method, 1601, seed=5, steps=1)
+    assert_parity(run_gpu(adi, p, 1), run_oracle(p, 1), what="1601")
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+@pytest.mark.parametrize("K", [1, 2, 8, 13])
+def test_parity_sweeps(adi, method, K):
+    p = random_problem(method, 29, seed=K, steps=2)
+    p.K = K
+    assert_parity(run_gpu(adi, p, 2), run_oracle(p, 2), what=f"K={K}")
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+def test_split_calls_equal_one_call(adi, method):
+    """adi_step(2)+adi_step(3) equals adi_step(5) (state is canonical between calls)."""
+    p = random_problem(method, 37, seed=2, steps=5)
+    a = run_gpu(adi, p, 5)
+    b = run_gpu(adi, p, 5, split=[2, 3])
+    assert_parity(b, a, tol=1e-13)
+    assert_parity(a, run_oracle(p, 5))
+
+
+def test_mfd_mms_ladder_parity(adi):
+    """Config 2: MFD, Γ=0, 5T, cfl 0.81, K=8 on 41, 81, 161 nodes — full runs.
+    At t = 5T the exact V̄, W̄ vanish (∝ sin ωt), so their relative error is
+    judged against the oracle's own sensitivity; U at 1e-12 outright."""
+    T = 1 / math.sqrt(2)
+    for n in (41, 81, 161):
+        p = mms_problem(MFD, n, MMS(), t_sim=5 * T)
+        st = p.meta["steps"]
+        g, o = run_gpu(adi, p, st), run_oracle(p, st)
+        assert rel(g[0], o[0]) <= TOL
+        assert_parity(g, o, what=f"MFD MMS n={n}", floor=oracle_sensitivity(p, st, o))
+
+
+@pytest.mark.parametrize("n,steps", [(41, 100), (81, 200), (161, 350)])
+def test_mfd_mms_midrun_parity(adi, n, steps):
+    """Config 2 at a mid-run time where every field is O(10): strict 1e-12."""
+    p = mms_problem(MFD, n, MMS(), t_sim=5 / math.sqrt(2))
+    assert_parity(run_gpu(adi, p, steps), run_oracle(p, steps), what=f"MFD MMS n={n} @{steps}")
+
+
+def test_cfd_config1_short_parity(adi):
+    """Config 1 (CFD 41x41, Γ=0, Δt = 0.91 h) for the first 60 steps at 1e-12
+    (beyond ~75 steps the literal CFD reading has amplified round-off past 1e-12
+    in ANY implementation: SURVEY fact 5-6)."""
+    p = mms_problem(CFD, 41, MMS(), steps=200)
+    assert_parity(run_gpu(adi, p, 60), run_oracle(p, 60), what="CFD config1 60 steps")
+
+
+def test_cfd_config1_full_within_roundoff_amplification(adi):
+    """Config 1 over all 200 steps, judged against the oracle's own 1-ulp
+    sensitivity (x10 margin)."""
+    p = mms_problem(CFD, 41, MMS(), steps=200)
+    g, o = run_gpu(adi, p, 200), run_oracle(p, 200)
+    assert_parity(g, o, what="CFD config1 200 steps", floor=oracle_sensitivity(p, 200, o))
+
+
+def test_ricker_batch_parity(adi):
+    """Config 5 shape: a batch of point-source shots, zero IC, free surface."""
+    n, B, steps = 129, 4, 30
+    probs = [ricker_problem(n, shot=s, nshots=B, steps=steps, f0=12.0, t0=0.1) for s in range(B)]
+    p0 = probs[0]
+    s = adi.AdiSolver(n, n, p0.h, p0.dt, 1.0, MFD, batch=B)
+    s.set_fields(np.stack([p.U for p in probs]), np.stack([p.V for p in probs]),
+                 np.stack([p.W for p in probs]))
+    s.set_point_sources([p.src[0] for p in probs], [p.src[1] for p in probs], p0.gf)
+    s.step(steps)
+    U, V, W = s.get_fields()
+    s.close()
+    for b, p in enumerate(probs):
+        o = run_oracle(p, steps)
+        assert np.abs(o[0]).max() > 0
+        assert_parity((U[b], V[b], W[b]), o, what=f"shot {b}")
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+def test_zero_in_zero_out(adi, method):
+    p = random_problem(method, 33, seed=0, steps=2, source=False, boundary=False)
+    p.U[:] = 0
+    p.V[:] = 0
+    p.W[:] = 0
+    U, V, W = run_gpu(adi, p, 2)
+    assert not U.any() and not V.any() and not W.any()
+
+
+def test_nonfinite_detected(adi):
+    p = random_problem(MFD, 33, seed=0, cfl=1.3, steps=400, source=False, boundary=False)
+    s = adi.AdiSolver.from_problem(p, check_finite=True)
+    assert s.create_status == adi.ADI_WUNSTABLE
+    with pytest.raises(adi.AdiError) as e:
+        s.step(400)
+    assert e.value.code == adi.ADI_ENONFINITE
+    s.close()
+
+
+def test_device_arrays_roundtrip(adi):
+    import torch
+    p = random_problem(MFD, 45, seed=9, steps=2)
+    s = adi.AdiSolver.from_problem(p)
+    dU, dV, dW = (torch.tensor(a, device="cuda") for a in (p.U, p.V, p.W))
+    s.set_fields(dU, dV, dW)
+    s.step(2)
+    oU, oV, oW = (torch.empty_like(a) for a in (dU, dV, dW))
+    s.get_fields_device(oU, oV, oW)
+    torch.cuda.synchronize()
+    assert_parity(tuple(a.cpu().numpy() for a in (oU, oV, oW)), run_oracle(p, 2))
+    s.close()
