@@ -15,16 +15,20 @@
 // materialised.  HBM traffic is 32 B per point per half-step (+8 B for a dense
 // source) — DESIGN.md §5.
 //
-// Work decomposition: a CTA owns NL lines x (NT/NL) chunks of
-// M consecutive points; each thread owns one chunk IN REGISTERS.  Long lines
-// are cut into segments with a halo (MFD: exact, finite stencil support;
-// CFD: the P^{-1} influence decays like (2-sqrt 3)^d).
-// Chunks exchange edge values through shared memory once per operator
-// application (one __syncthreads per op).
+// Work decomposition.  A CTA owns NTEAM adjacent lines; each
+// line segment is owned by a TEAM of T warps; each thread owns one chunk of M
+// consecutive points of its line IN REGISTERS (u, x, S, X).  Chunk edge values
+// move between neighbouring chunks by warp shuffles; only the boundary lanes of
+// a warp go through shared memory, synchronised by a named barrier of the
+// team's 32*T threads — so one team waiting never idles the whole SM.  Global
+// memory is touched only at the tile load / store, coalesced through a padded
+// shared-memory staging tile.  Long lines are cut into segments with a halo
+// (MFD: exact, finite stencil support; CFD: the P^{-1} influence decays like
+// (2-sqrt 3)^d).
 //
 // CFD tridiagonal solves (P, P̄ with the global no-pivot LU)
 // are split across chunks by a truncated SPIKE scheme: each chunk solves
-// locally with zero carries, publishes (y_last, z_first, z_last), and adds the
+// locally with zero carries, exchanges (y_last, z_first, z_last), and adds the
 // carry responses K_i*ycarry + J_i*zcarry; carries from >= 2 chunks away are
 // below 1e-18 relative for M = 16 and are dropped.
 #pragma once
@@ -46,7 +50,7 @@ struct Seg {
 struct KParams {
   int n;        // cells along the line; positions 0..n
   int nlines;   // interior pressure lines
-  int NL;       // lines per tile (power of two, divides NT)
+  int xmajor;   // 1: positions contiguous in memory (row sweep); 0: lines contiguous
   int plo, phi; // chunks entirely inside [plo, phi] use the interior fast path
   const Seg* segs;
   // fields: element of (batch b, line l, position p)
@@ -86,33 +90,17 @@ __constant__ double c_cl, c_cinvd;
 __constant__ double c_cK[MMAX], c_cJ[MMAX];
 __constant__ double c_cF, c_cKs, c_cKe, c_cJs, c_cJe;
 
-// ---------------------------------------------------------------------------
-// shared-memory exchange area
-// ---------------------------------------------------------------------------
-// dynamic slots: 2 buffers x 4 values;  static slots (CFD): 2 systems x 5 + 4
-constexpr int DYN = 4;
-constexpr int NSTAT = 14;
-enum { ST_F = 0, ST_KS = 1, ST_KE = 2, ST_JS = 3, ST_JE = 4 };  // + 5*sys
-enum { ST_SF = 10, ST_SL = 11, ST_VF = 12, ST_VL = 13 };        // base first/last
-
-struct Xch {
-  double* a;     // base of the exchange area
-  int stride;    // entries per slot = NT + 4*NL
-  int pad;       // 2*NL
-  __device__ double* dyn(int buf, int k) const { return a + (buf * DYN + k) * stride + pad; }
-  __device__ double* st(int k) const { return a + (2 * DYN + k) * stride + pad; }
-};
-
-__device__ __forceinline__ bool finite_(double v) { return isfinite(v); }
+enum { ST_F = 0, ST_KS = 1, ST_KE = 2, ST_JS = 3, ST_JE = 4 };  // CFD chunk statics
 
 // ---------------------------------------------------------------------------
 // Thread context
 // ---------------------------------------------------------------------------
 template <int M>
 struct Ctx {
-  int t, NL, line, chunk, s, n;  // s = line position of chunk element 0
+  int t, line, chunk, s, n;  // s = line position of chunk element 0
   bool live;      // thread owns an existing chunk of an existing line
   bool interior;  // fast path allowed
+  bool nbint;     // chunks c-2 .. c+2 all exist and are interior (CFD constant statics)
   double gL, gR;  // Dirichlet values of this line for this half-step
 };
 
@@ -266,21 +254,117 @@ struct Cfd {
 
 namespace adi {
 
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(sz) : "memory");
+}
+
+__device__ __forceinline__ double shup(double v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
+__device__ __forceinline__ double shdn(double v, int d) { return __shfl_down_sync(0xffffffffu, v, d); }
+
+// ---------------------------------------------------------------------------
+// Team exchange: lanes of one warp are consecutive chunks of one line; the T
+// warps of a team cover consecutive runs of 32 chunks.  Cross-warp edge values
+// go through an 8-slot shared-memory mailbox per warp (double-buffered) and a
+// named barrier over the team's 32*T threads.
+// ---------------------------------------------------------------------------
+template <int T>
+struct Team {
+  double* box;  // [2][T][8]
+  int lane, wt, bar, buf;
+  __device__ __forceinline__ void sync() const {
+    if (T > 1) asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(32 * T) : "memory");
+  }
+  __device__ __forceinline__ double* slot(int w) const { return box + (buf * T + w) * 8; }
+  // neighbour warp's mailbox value k, 0 if there is no neighbour warp (branch-free)
+  __device__ __forceinline__ double pv(int k) const {
+    const double v = slot(wt > 0 ? wt - 1 : 0)[k];
+    return wt > 0 ? v : 0.0;
+  }
+  __device__ __forceinline__ double nx(int k) const {
+    const double v = slot(wt < T - 1 ? wt + 1 : wt)[k];
+    return wt < T - 1 ? v : 0.0;
+  }
+};
+
+// neighbours' edge values of a chunk array: prev chunk's a[M-2], a[M-1]; next chunk's a[0], a[1]
+template <int M, int T>
+__device__ __forceinline__ void edge_exchange(Team<T>& tm, const double (&a)[M], double& pm2,
+                                              double& pm1, double& np1, double& np2) {
+  pm2 = shup(a[M - 2], 1);
+  pm1 = shup(a[M - 1], 1);
+  np1 = shdn(a[0], 1);
+  np2 = shdn(a[1], 1);
+  if (T > 1) {
+    double* s = tm.slot(tm.wt);
+    if (tm.lane == 31) { s[0] = a[M - 2]; s[1] = a[M - 1]; }
+    if (tm.lane == 0) { s[2] = a[0]; s[3] = a[1]; }
+    tm.sync();
+    const double q0 = tm.pv(0), q1 = tm.pv(1), q2 = tm.nx(2), q3 = tm.nx(3);
+    pm2 = tm.lane == 0 ? q0 : pm2;
+    pm1 = tm.lane == 0 ? q1 : pm1;
+    np1 = tm.lane == 31 ? q2 : np1;
+    np2 = tm.lane == 31 ? q3 : np2;
+    tm.buf ^= 1;
+  } else {
+    pm2 = tm.lane == 0 ? 0.0 : pm2;
+    pm1 = tm.lane == 0 ? 0.0 : pm1;
+    np1 = tm.lane == 31 ? 0.0 : np1;
+    np2 = tm.lane == 31 ? 0.0 : np2;
+  }
+}
+
 // ===========================================================================
-// CFD: one operator application out = B - coef * T^{-1} r(o) on the tile
-// (T = P̄ for the u-op, P for the x-op), truncated-SPIKE across chunks.
-// Phase 1 (local solve, publish), __syncthreads, phase 2 (carries, fix-up).
-// Also returns the operand neighbour values of the NEXT op (this op's output
-// at the previous chunk's last and the next chunk's first position) without a
-// second barrier.
+// CFD statics of a chunk for one system: F = G_e, K_s, K_e, J_s, J_e.
 // ===========================================================================
-template <int M, bool UOP>
-__device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, const Xch& X,
-                                          int buf, const double (&o)[M], const double (&B)[M],
-                                          double (&out)[M], double coef, double om1, double op1,
-                                          double& nom1, double& nop1) {
-  const int t = c.t, NL = c.NL;
-  const int sys = UOP ? 0 : 1;
+template <int M>
+__device__ __forceinline__ void cfd_statics(const Ctx<M>& c, const double* tab, int np1,
+                                            double* st /* 5 */) {
+  if (c.interior) {
+    st[0] = c_cF; st[1] = c_cKs; st[2] = c_cKe; st[3] = c_cJs; st[4] = c_cJe;
+    return;
+  }
+  double G[M];
+  double g = 1.0;
+#pragma unroll
+  for (int i = 0; i < M; ++i) {
+    const int p = c.s + i;
+    const double l = (p >= 0 && p < np1) ? __ldg(tab + p) : 0.0;
+    g *= -l;
+    G[i] = g;
+  }
+  st[0] = G[M - 1];
+  double k = 0.0, j = 1.0;
+#pragma unroll
+  for (int i = M - 1; i >= 0; --i) {
+    const int p = c.s + i;
+    const bool in = (p >= 0 && p < np1);
+    const double iv = in ? __ldg(tab + np1 + p) : 0.0;
+    const double cc = in ? __ldg(tab + 2 * np1 + p) : 0.0;
+    k = (G[i] - cc * k) * iv;
+    j *= -cc * iv;
+    if (i == M - 1) { st[2] = k; st[4] = j; }
+  }
+  st[1] = k;
+  st[3] = j;
+}
+
+// ===========================================================================
+// CFD: one operator application out = B - coef * T^{-1} r(o) on the team's
+// segment (T = P̄ for the u-op, P for the x-op), truncated SPIKE across chunks.
+// Phase 1: local solve with zero carries; exchange (y_e, z_s, z_e) with the
+// neighbours; phase 2: carries + fix-up.  Also returns this op's output at the
+// previous chunk's last and the next chunk's first position (operand
+// neighbours of the next op) without another exchange.
+// st: shared table [5][CH] of this team's chunk statics for this system.
+// ===========================================================================
+template <int M, int T, bool UOP>
+__device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, Team<T>& tm,
+                                          const double* st, int CH, const double (&o)[M],
+                                          const double (&B)[M], double (&out)[M], double coef,
+                                          double om1, double op1, double Bn_first,
+                                          double Bp_last, double& nom1, double& nop1) {
   const double* tab = UOP ? P.tabU : P.tabX;
   const int np1 = c.n + 1;
   double yl_e, ws, we;
@@ -289,7 +373,6 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, con
     if (UOP) Cfd<M>::template rhs_u<true>(c, o, out, om1, op1);
     else Cfd<M>::template rhs_x<true>(c, o, out, om1, op1);
     const double l = c_cl, iv = c_cinvd;
-    out[0] = out[0];
 #pragma unroll
     for (int i = 1; i < M; ++i) out[i] = fma(-l, out[i - 1], out[i]);
     yl_e = out[M - 1];
@@ -323,22 +406,48 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, con
     ws = z;
   }
   if (!c.live) { yl_e = 0.0; ws = 0.0; we = 0.0; }
-  X.dyn(buf, 0)[t] = yl_e;
-  X.dyn(buf, 1)[t] = ws;
-  X.dyn(buf, 2)[t] = we;
-  __syncthreads();
+  // ---------------- exchange ----------------
+  double ylm1 = shup(yl_e, 1), ylm2 = shup(yl_e, 2), ylp1 = shdn(yl_e, 1);
+  double wsp1 = shdn(ws, 1), wsp2 = shdn(ws, 2), wem1 = shup(we, 1);
+  const int lane = tm.lane;
+  if (T > 1) {
+    double* s = tm.slot(tm.wt);
+    if (lane == 30) s[0] = yl_e;
+    if (lane == 31) { s[1] = yl_e; s[2] = we; }
+    if (lane == 0) { s[3] = ws; s[5] = yl_e; }
+    if (lane == 1) s[4] = ws;
+    tm.sync();
+    const double p0 = tm.pv(0), p1 = tm.pv(1), p2 = tm.pv(2);
+    const double n3 = tm.nx(3), n4 = tm.nx(4), n5 = tm.nx(5);
+    ylm1 = lane == 0 ? p1 : ylm1;
+    ylm2 = lane == 0 ? p0 : (lane == 1 ? p1 : ylm2);
+    wem1 = lane == 0 ? p2 : wem1;
+    ylp1 = lane == 31 ? n5 : ylp1;
+    wsp1 = lane == 31 ? n3 : wsp1;
+    wsp2 = lane == 31 ? n4 : (lane == 30 ? n3 : wsp2);
+    tm.buf ^= 1;
+  } else {
+    ylm1 = lane == 0 ? 0.0 : ylm1;
+    ylm2 = lane <= 1 ? 0.0 : ylm2;
+    wem1 = lane == 0 ? 0.0 : wem1;
+    ylp1 = lane == 31 ? 0.0 : ylp1;
+    wsp1 = lane == 31 ? 0.0 : wsp1;
+    wsp2 = lane >= 30 ? 0.0 : wsp2;
+  }
+  // statics of the neighbours (constants when all of c-2..c+2 are interior)
+  double Fm1, Fme, Ksp1, Jsp1, Ksp2, Kem1, Jem1;
+  if (c.nbint) {
+    Fm1 = Fme = c_cF; Ksp1 = Ksp2 = c_cKs; Jsp1 = c_cJs; Kem1 = c_cKe; Jem1 = c_cJe;
+  } else {
+    const int ch = c.chunk;
+    auto at = [&](int k, int cc) { return (cc >= 0 && cc < CH) ? st[k * CH + cc] : 0.0; };
+    Fm1 = at(ST_F, ch - 1); Fme = at(ST_F, ch);
+    Ksp1 = at(ST_KS, ch + 1); Jsp1 = at(ST_JS, ch + 1); Ksp2 = at(ST_KS, ch + 2);
+    Kem1 = at(ST_KE, ch - 1); Jem1 = at(ST_JE, ch - 1);
+  }
   // ---------------- phase 2: carries and fix-up ----------------
-  const double ylm1 = X.dyn(buf, 0)[t - NL], ylm2 = X.dyn(buf, 0)[t - 2 * NL];
-  const double ylp1 = X.dyn(buf, 0)[t + NL];
-  const double wsp1 = X.dyn(buf, 1)[t + NL], wsp2 = X.dyn(buf, 1)[t + 2 * NL];
-  const double wem1 = X.dyn(buf, 2)[t - NL];
-  const int so = 5 * sys;
-  const double Fm1 = X.st(so + ST_F)[t - NL], Fme = X.st(so + ST_F)[t];
-  const double Ksp1 = X.st(so + ST_KS)[t + NL], Jsp1 = X.st(so + ST_JS)[t + NL];
-  const double Ksp2 = X.st(so + ST_KS)[t + 2 * NL];
-  const double Kem1 = X.st(so + ST_KE)[t - NL], Jem1 = X.st(so + ST_JE)[t - NL];
-  const double ycarry = fma(Fm1, ylm2, ylm1);            // true y at s-1
-  const double ycn = fma(Fme, ycarry, yl_e);             // true y at s+M-1
+  const double ycarry = fma(Fm1, ylm2, ylm1);   // true y at s-1
+  const double ycn = fma(Fme, ycarry, yl_e);    // true y at s+M-1
   const double zcarry = fma(Jsp1, fma(Ksp2, ylp1, wsp2), fma(Ksp1, ycn, wsp1));  // true z at s+M
   double z0;
   if (c.interior) {
@@ -346,7 +455,8 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, con
     z0 = fma(c_cJ[0], zcarry, fma(c_cK[0], ycarry, iv * out[0]));
     const double cy = coef * ycarry, cz = coef * zcarry, ci = coef * iv;
 #pragma unroll
-    for (int i = 0; i < M; ++i) out[i] = fma(-c_cJ[i], cz, fma(-c_cK[i], cy, fma(-ci, out[i], B[i])));
+    for (int i = 0; i < M; ++i)
+      out[i] = fma(-c_cJ[i], cz, fma(-c_cK[i], cy, fma(-ci, out[i], B[i])));
   } else {
     double g = 1.0;
 #pragma unroll
@@ -376,98 +486,90 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, con
       out[i] = act ? fma(-coef, out[i], B[i]) : slot;
     }
   }
-  // operand neighbours of the next op
-  nop1 = fma(-coef, zcarry, X.st(UOP ? ST_SF : ST_VF)[t + NL]);
-  nom1 = fma(-coef, fma(Jem1, z0, fma(Kem1, ylm2, wem1)), X.st(UOP ? ST_SL : ST_VL)[t - NL]);
-}
-
-// CFD statics of a chunk for one system: F, K_s, K_e, J_s, J_e
-template <int M>
-__device__ __forceinline__ void cfd_statics(const Ctx<M>& c, const double* tab, int np1,
-                                            double& F, double& Ks, double& Ke, double& Js,
-                                            double& Je) {
-  if (c.interior) {
-    F = c_cF; Ks = c_cKs; Ke = c_cKe; Js = c_cJs; Je = c_cJe;
-    return;
-  }
-  double G[M];
-  double g = 1.0;
-#pragma unroll
-  for (int i = 0; i < M; ++i) {
-    const int p = c.s + i;
-    const double l = (p >= 0 && p < np1) ? __ldg(tab + p) : 0.0;
-    g *= -l;
-    G[i] = g;
-  }
-  F = G[M - 1];
-  double k = 0.0, j = 1.0;
-#pragma unroll
-  for (int i = M - 1; i >= 0; --i) {
-    const int p = c.s + i;
-    const bool in = (p >= 0 && p < np1);
-    const double iv = in ? __ldg(tab + np1 + p) : 0.0;
-    const double cc = in ? __ldg(tab + 2 * np1 + p) : 0.0;
-    k = (G[i] - cc * k) * iv;
-    j *= -cc * iv;
-    if (i == M - 1) { Ke = k; Je = j; }
-  }
-  Ks = k;
-  Js = j;
+  nop1 = fma(-coef, zcarry, Bn_first);
+  nom1 = fma(-coef, fma(Jem1, z0, fma(Kem1, ylm2, wem1)), Bp_last);
 }
 
 // ===========================================================================
-// MFD: publish the first two / last two values of a chunk array and read the
-// neighbours' (one __syncthreads).
+// The tile kernel.  CTA = NTEAM lines x (T warps x 32 chunks x M points).
 // ===========================================================================
-template <int M>
-__device__ __forceinline__ void mfd_exchange(const Ctx<M>& c, const Xch& X, int buf,
-                                             const double (&a)[M], double& m2, double& m1,
-                                             double& p1, double& p2) {
-  const int t = c.t, NL = c.NL;
-  X.dyn(buf, 0)[t] = c.live ? a[0] : 0.0;
-  X.dyn(buf, 1)[t] = c.live ? a[1] : 0.0;
-  X.dyn(buf, 2)[t] = c.live ? a[M - 2] : 0.0;
-  X.dyn(buf, 3)[t] = c.live ? a[M - 1] : 0.0;
-  __syncthreads();
-  m2 = X.dyn(buf, 2)[t - NL];
-  m1 = X.dyn(buf, 3)[t - NL];
-  p1 = X.dyn(buf, 0)[t + NL];
-  p2 = X.dyn(buf, 1)[t + NL];
-}
-
-// ===========================================================================
-// The tile kernel.
-// ===========================================================================
-template <int METHOD, int M, int NT, int MODE>
-__global__ void __launch_bounds__(NT, 1) adi_tile_kernel(const KParams P) {
+template <int METHOD, int M, int T, int NTEAM, int MODE>
+__global__ void __launch_bounds__(32 * T * NTEAM, 1) adi_tile_kernel(const KParams P) {
+  constexpr int NT = 32 * T * NTEAM;
+  constexpr int CH = 32 * T;     // chunks per team
+  constexpr int NPOS = CH * M;   // positions per team segment
+  constexpr int PADM = M + 1;    // padded chunk stride in the staging tile
   extern __shared__ double smem[];
+  double* stS = smem;                          // staging: S (or U in the prologue)
+  double* stX = stS + NTEAM * CH * PADM;       // staging: X
+  double* stF = stX + NTEAM * CH * PADM;       // staging: phi (source pattern)
+  double* stc = stF + NTEAM * CH * PADM;       // CFD statics [NTEAM][2 sys][5][CH]
+  double* boxes = stc + NTEAM * 10 * CH;       // team mailboxes [NTEAM][2][T][8]
+
   const int t = threadIdx.x;
-  const int NL = P.NL;
+  const int warp = t >> 5, lane = t & 31;
+  const int team = warp / T, wt = warp % T;
+  const int ch = wt * 32 + lane;
   const Seg sg = P.segs[blockIdx.y];
-  const int l = t & (NL - 1);
-  const int ch = t / NL;
-  const int line = blockIdx.x * NL + l;
+  const int line = blockIdx.x * NTEAM + team;
   const long long b = blockIdx.z;
   const int n = P.n;
+  const int uhi = (METHOD == M_CFD) ? n - 1 : n;  // u active on [1, uhi]
+  const int pR = (METHOD == M_CFD) ? n : n + 1;   // position of ū's right Dirichlet value
 
   Ctx<M> c;
-  c.t = t; c.NL = NL; c.line = line; c.chunk = ch; c.n = n;
+  c.t = t; c.line = line; c.chunk = ch; c.n = n;
   c.s = sg.start + ch * M;
   c.live = (line < P.nlines) && (ch < sg.nchunks);
-  c.interior = c.live && c.s >= P.plo && c.s + M - 1 <= P.phi;
+  // Dead chunks (beyond the tile's active chunks or the last line) also run the
+  // branch-free interior path: their values only reach the halo of the tile,
+  // whose width covers any bounded garbage, and no warp diverges.
+  const bool inner = c.s >= P.plo && c.s + M - 1 <= P.phi;
+  c.interior = !c.live || inner;
+  c.nbint = c.live && inner && ch >= 2 && ch + 2 < sg.nchunks && c.s - 2 * M >= P.plo &&
+            c.s + 3 * M - 1 <= P.phi;
 
-  Xch X;
-  X.stride = NT + 4 * NL;
-  X.pad = 2 * NL;
-  X.a = smem;
-  for (int k = t; k < (2 * DYN + NSTAT) * X.stride; k += NT) smem[k] = 0.0;
+  Team<T> tm;
+  tm.box = boxes + team * 2 * T * 8;
+  tm.lane = lane; tm.wt = wt; tm.bar = 1 + team; tm.buf = 0;
 
-  // ---- Dirichlet values of this line (ū at position 0 and at n (CFD) / n+1 (MFD))
-  const int pR = (METHOD == M_CFD) ? n : n + 1;
-  const double* Ub = P.U_in + b * P.u_batch + (long long)(line + 1) * P.u_line;
-  c.gL = 0.0; c.gR = 0.0;
-  if (c.live) {
+  // ---- cooperative coalesced load of the tile into the padded staging area
+  const double* Ubat = P.U_in ? P.U_in + b * P.u_batch : nullptr;
+  const double* Sbat = P.S_in ? P.S_in + b * P.s_batch : nullptr;
+  const double* Xbat = P.X_in + b * P.x_batch;
+  const bool want_phi = (MODE != KM_FINAL) && P.phi_src;
+  for (int e = t; e < NTEAM * NPOS; e += NT) {
+    int tmi, pos;
+    if (P.xmajor) { tmi = e / NPOS; pos = e - tmi * NPOS; }
+    else { pos = e / NTEAM; tmi = e - pos * NTEAM; }
+    const int ln = blockIdx.x * NTEAM + tmi;
+    const int p = sg.start + pos;
+    const bool lv = ln < P.nlines && pos < sg.nchunks * M;
+    const int si = (tmi * CH + pos / M) * PADM + pos % M;
+    const bool uin = lv && p >= 1 && p <= uhi;
+    const bool xin = lv && p >= 0 && p <= n;
+    // asynchronous 8-byte copies; an out-of-range element is zero-filled (src-size 0)
+    const double* sp = Xbat;
+    bool sok;
     if (MODE == KM_PROLOGUE) {
+      sok = xin;
+      if (sok) sp = Ubat + (long long)(ln + 1) * P.u_line + (long long)p * P.u_pt;
+    } else {
+      sok = uin;
+      if (sok) sp = Sbat + (long long)ln * P.s_line + (long long)(p - 1) * P.s_pt;
+    }
+    cp_async8(stS + si, sp, sok);
+    cp_async8(stX + si, xin ? Xbat + (long long)ln * P.x_line + (long long)p * P.x_pt : Xbat, xin);
+    if (want_phi)
+      cp_async8(stF + si, uin ? P.phi_src + (long long)ln * P.s_line + (long long)(p - 1) * P.s_pt
+                              : P.phi_src, uin);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  // Dirichlet values of this line
+  c.gL = 0.0; c.gR = 0.0;
+  if (line < P.nlines) {
+    if (MODE == KM_PROLOGUE) {
+      const double* Ub = Ubat + (long long)(line + 1) * P.u_line;
       c.gL = Ub[0];
       c.gR = Ub[(long long)pR * P.u_pt];
     } else {
@@ -475,42 +577,39 @@ __global__ void __launch_bounds__(NT, 1) adi_tile_kernel(const KParams P) {
       if (P.edgeR) c.gR = P.edgeR[line + 1] * P.gb;
     }
   }
-  const int uhi = (METHOD == M_CFD) ? n - 1 : n;  // u active on [1, uhi]
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
 
-  // ---- load the chunk
   double u[M], x[M], S[M], V[M];
-  const double* Sb = P.S_in + b * P.s_batch + (long long)line * P.s_line;
-  const double* Xb = P.X_in + b * P.x_batch + (long long)line * P.x_line;
+  {
+    const double* ss = stS + (team * CH + ch) * PADM;
+    const double* xs = stX + (team * CH + ch) * PADM;
 #pragma unroll
-  for (int i = 0; i < M; ++i) {
-    const int p = c.s + i;
-    const bool xin = c.live && p >= 0 && p <= n;
-    const bool uin = c.live && p >= 1 && p <= uhi;
-    x[i] = xin ? Xb[(long long)p * P.x_pt] : 0.0;
-    V[i] = x[i];
-    if (MODE == KM_PROLOGUE) {
-      u[i] = (c.live && p >= 0 && p <= n) ? Ub[(long long)p * P.u_pt] : 0.0;
-      S[i] = 0.0;
-    } else {
-      S[i] = uin ? Sb[(long long)(p - 1) * P.s_pt] : 0.0;
-      u[i] = (p == 0) ? c.gL : ((METHOD == M_CFD && p == n) ? c.gR : 0.0);
-      if (!c.live) u[i] = 0.0;
+    for (int i = 0; i < M; ++i) {
+      const int p = c.s + i;
+      x[i] = xs[i];
+      V[i] = x[i];
+      if (MODE == KM_PROLOGUE) {
+        u[i] = ss[i];
+        S[i] = 0.0;
+      } else {
+        S[i] = ss[i];
+        u[i] = (p == 0) ? c.gL : ((METHOD == M_CFD && p == n) ? c.gR : 0.0);
+        if (!c.live) u[i] = 0.0;
+      }
     }
   }
-  __syncthreads();  // exchange area zeroed
 
-  // source factor at this chunk's points, dt/2 F(t)
+  // dst = src + dt/2 F at this chunk's points (F = phi*gf + point source)
   auto add_source = [&](double (&dst)[M], const double (&src)[M]) {
-    const double* ph = P.phi_src ? P.phi_src + (long long)line * P.s_line : nullptr;
+    const double* fs = stF + (team * CH + ch) * PADM;
     const int ptl = P.pt_line ? P.pt_line[b] : -1;
     const int ptp = P.pt_pos ? P.pt_pos[b] : -1;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
       const int p = c.s + i;
-      const bool uin = c.live && p >= 1 && p <= uhi;
-      double f = 0.0;
-      if (uin && ph) f = ph[(long long)(p - 1) * P.s_pt] * P.gf;
-      if (uin && line == ptl && p == ptp) f += P.pt_amp * P.gf;
+      double f = want_phi ? fs[i] * P.gf : 0.0;
+      if (c.live && line == ptl && p == ptp) f += P.pt_amp * P.gf;
       dst[i] = fma(P.half_dt, f, src[i]);
     }
   };
@@ -518,39 +617,38 @@ __global__ void __launch_bounds__(NT, 1) adi_tile_kernel(const KParams P) {
   if (METHOD == M_CFD) {
     // ---------------- CFD ----------------
     const int np1 = n + 1;
-    if (c.live) {
-      double F, Ks, Ke, Js, Je;
-      cfd_statics<M>(c, P.tabU, np1, F, Ks, Ke, Js, Je);
-      X.st(ST_F)[t] = F; X.st(ST_KS)[t] = Ks; X.st(ST_KE)[t] = Ke; X.st(ST_JS)[t] = Js; X.st(ST_JE)[t] = Je;
-      cfd_statics<M>(c, P.tabX, np1, F, Ks, Ke, Js, Je);
-      X.st(5 + ST_F)[t] = F; X.st(5 + ST_KS)[t] = Ks; X.st(5 + ST_KE)[t] = Ke; X.st(5 + ST_JS)[t] = Js; X.st(5 + ST_JE)[t] = Je;
-      X.st(ST_SF)[t] = S[0]; X.st(ST_SL)[t] = S[M - 1];
-      X.st(ST_VF)[t] = V[0]; X.st(ST_VL)[t] = V[M - 1];
-      // initial operand exchange: x (and u in the prologue)
-      X.dyn(1, 0)[t] = x[0]; X.dyn(1, 1)[t] = x[M - 1];
-      X.dyn(1, 2)[t] = u[0]; X.dyn(1, 3)[t] = u[M - 1];
+    double* stU = stc + (team * 2 + 0) * 5 * CH;
+    double* stXs = stc + (team * 2 + 1) * 5 * CH;
+    {
+      double q[5];
+      cfd_statics<M>(c, P.tabU, np1, q);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) stU[k * CH + ch] = c.live ? q[k] : 0.0;
+      cfd_statics<M>(c, P.tabX, np1, q);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) stXs[k * CH + ch] = c.live ? q[k] : 0.0;
     }
-    __syncthreads();
-    double xm1 = X.dyn(1, 1)[t - NL], xp1 = X.dyn(1, 0)[t + NL];
-    double um1 = X.dyn(1, 3)[t - NL], up1 = X.dyn(1, 2)[t + NL];
-    __syncthreads();  // buffer 1 is reused by the second op
+    // neighbour edge values of x (and u in the prologue) and of the bases S, V
+    double d0, d1, xm1, xp1, um1, up1, SLp, SFn, VLp, VFn;
+    edge_exchange<M, T>(tm, x, d0, xm1, xp1, d1);
+    edge_exchange<M, T>(tm, u, d0, um1, up1, d1);
+    edge_exchange<M, T>(tm, S, d0, SLp, SFn, d1);
+    edge_exchange<M, T>(tm, V, d0, VLp, VFn, d1);
+    __syncthreads();  // statics visible
     if (MODE == KM_PROLOGUE) {
-      double d1, d2;
-      cfd_apply<M, false>(c, P, X, 0, u, V, x, P.cx, um1, up1, d1, d2);  // W* = W - beta D(U)
-      add_source(S, u);                                                    // S = U + dt/2 F
-      cfd_apply<M, true>(c, P, X, 1, V, S, u, P.cu, xm1, xp1, d1, d2);     // S1 = S - alpha D̄(W)
+      double e1, e2;
+      cfd_apply<M, T, false>(c, P, tm, stXs, CH, u, V, x, P.cx, um1, up1, 0.0, 0.0, e1, e2);
+      add_source(S, u);
+      cfd_apply<M, T, true>(c, P, tm, stU, CH, V, S, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
     } else {
-      int buf = 0;
       for (int k = 0; k < P.K; ++k) {
-        cfd_apply<M, true>(c, P, X, buf, x, S, u, P.cu, xm1, xp1, um1, up1);
-        buf ^= 1;
-        cfd_apply<M, false>(c, P, X, buf, u, V, x, P.cx, um1, up1, xm1, xp1);
-        buf ^= 1;
+        cfd_apply<M, T, true>(c, P, tm, stU, CH, x, S, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
+        cfd_apply<M, T, false>(c, P, tm, stXs, CH, u, V, x, P.cx, um1, up1, VFn, VLp, xm1, xp1);
       }
       if (MODE == KM_SWEEP) {
-        double d1, d2;
+        double e1, e2;
         add_source(S, u);
-        cfd_apply<M, true>(c, P, X, buf, x, S, u, P.cu, xm1, xp1, d1, d2);
+        cfd_apply<M, T, true>(c, P, tm, stU, CH, x, S, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
 #pragma unroll
         for (int i = 0; i < M; ++i) x[i] = fma(2.0, x[i], -V[i]);
       }
@@ -558,28 +656,23 @@ __global__ void __launch_bounds__(NT, 1) adi_tile_kernel(const KParams P) {
   } else {
     // ---------------- MFD ----------------
     double xm2, xm1, xp1, xp2, um2, um1, up1, up2;
-    mfd_exchange<M>(c, X, 0, x, xm2, xm1, xp1, xp2);
+    edge_exchange<M, T>(tm, x, xm2, xm1, xp1, xp2);
     const double au = P.cu, bx = P.cx;
     if (MODE == KM_PROLOGUE) {
-      mfd_exchange<M>(c, X, 1, u, um2, um1, up1, up2);
+      edge_exchange<M, T>(tm, u, um2, um1, up1, up2);
       if (c.interior) Mfd<M>::template xop<true>(c, u, V, x, bx, um1, up1, up2);
       else Mfd<M>::template xop<false>(c, u, V, x, bx, um1, up1, up2);
       add_source(S, u);
       if (c.interior) Mfd<M>::template uop<true>(c, V, S, u, au, xm2, xm1, xp1);
       else Mfd<M>::template uop<false>(c, V, S, u, au, xm2, xm1, xp1);
     } else {
-      int buf = 1;
       for (int k = 0; k < P.K; ++k) {
         if (c.interior) Mfd<M>::template uop<true>(c, x, S, u, au, xm2, xm1, xp1);
         else Mfd<M>::template uop<false>(c, x, S, u, au, xm2, xm1, xp1);
-        mfd_exchange<M>(c, X, buf, u, um2, um1, up1, up2);
-        buf ^= 1;
+        edge_exchange<M, T>(tm, u, um2, um1, up1, up2);
         if (c.interior) Mfd<M>::template xop<true>(c, u, V, x, bx, um1, up1, up2);
         else Mfd<M>::template xop<false>(c, u, V, x, bx, um1, up1, up2);
-        if (k + 1 < P.K || MODE == KM_SWEEP) {
-          mfd_exchange<M>(c, X, buf, x, xm2, xm1, xp1, xp2);
-          buf ^= 1;
-        }
+        if (k + 1 < P.K || MODE == KM_SWEEP) edge_exchange<M, T>(tm, x, xm2, xm1, xp1, xp2);
       }
       if (MODE == KM_SWEEP) {
         add_source(S, u);
@@ -591,29 +684,50 @@ __global__ void __launch_bounds__(NT, 1) adi_tile_kernel(const KParams P) {
     }
   }
 
-  // ---- store the owned output range
-  if (!c.live) return;
-  double acc = 0.0;
-  double* So = P.S_out + b * P.s_batch + (long long)line * P.s_line;
-  double* Xo = P.X_out + b * P.x_batch + (long long)line * P.x_line;
-  double* Uo = P.U_out ? P.U_out + b * P.u_batch + (long long)(line + 1) * P.u_line : nullptr;
+  // ---- stage the outputs (own chunk only) and store the owned range coalesced
+  {
+    double* ss = stS + (team * CH + ch) * PADM;
+    double* xs = stX + (team * CH + ch) * PADM;
 #pragma unroll
-  for (int i = 0; i < M; ++i) {
-    const int p = c.s + i;
+    for (int i = 0; i < M; ++i) { ss[i] = u[i]; xs[i] = x[i]; }
+  }
+  __syncthreads();
+  double* Sobat = P.S_out ? P.S_out + b * P.s_batch : nullptr;
+  double* Xobat = P.X_out + b * P.x_batch;
+  double* Uobat = P.U_out ? P.U_out + b * P.u_batch : nullptr;
+  double acc = 0.0;
+  for (int e = t; e < NTEAM * NPOS; e += NT) {
+    int tmi, pos;
+    if (P.xmajor) { tmi = e / NPOS; pos = e - tmi * NPOS; }
+    else { pos = e / NTEAM; tmi = e - pos * NTEAM; }
+    const int ln = blockIdx.x * NTEAM + tmi;
+    const int p = sg.start + pos;
+    if (ln >= P.nlines || pos >= sg.nchunks * M) continue;
     if (p < sg.out_lo || p >= sg.out_hi || p < 0 || p > n) continue;
-    Xo[(long long)p * P.x_pt] = x[i];
-    acc += x[i];
+    const int si = (tmi * CH + pos / M) * PADM + pos % M;
+    const double xv = stX[si], uv = stS[si];
+    Xobat[(long long)ln * P.x_line + (long long)p * P.x_pt] = xv;
+    acc += xv;
     if (MODE == KM_FINAL) {
-      Uo[(long long)p * P.u_pt] = u[i];  // interior values and the Dirichlet slots
-      acc += u[i];
-      if (METHOD == M_MFD && p == n) Uo[(long long)(n + 1) * P.u_pt] = c.gR;
-      if (METHOD == M_MFD && p == 0) Uo[0] = c.gL;
+      double* Ub = Uobat + (long long)(ln + 1) * P.u_line;
+      Ub[(long long)p * P.u_pt] = uv;   // interior values and the Dirichlet slots
+      acc += uv;
+      if (METHOD == M_MFD && p == n) {
+        const double gR = P.edgeR ? P.edgeR[ln + 1] * P.gb : 0.0;
+        Ub[(long long)(n + 1) * P.u_pt] = gR;
+      }
     } else if (p >= 1 && p <= uhi) {
-      So[(long long)(p - 1) * P.s_pt] = u[i];
-      acc += u[i];
+      Sobat[(long long)ln * P.s_line + (long long)(p - 1) * P.s_pt] = uv;
+      acc += uv;
     }
   }
-  if (P.flag && !finite_(acc)) atomicOr(P.flag, 1);
+  if (P.flag && !isfinite(acc)) atomicOr(P.flag, 1);
+}
+
+// shared memory bytes of one CTA
+template <int M, int T, int NTEAM>
+constexpr size_t tile_smem_bytes() {
+  return sizeof(double) * (size_t)(3 * NTEAM * 32 * T * (M + 1) + NTEAM * 10 * 32 * T + NTEAM * 2 * T * 8);
 }
 
 }  // namespace adi

@@ -25,8 +25,11 @@
 
 namespace adi {
 
-constexpr int TM = 16;    // points per thread chunk
-constexpr int TNT = 256;  // threads per CTA
+constexpr int TM = 16;     // points per thread chunk
+constexpr int TT = 2;      // warps per team (one team per line segment)
+constexpr int TNTEAM = 4;  // teams (lines) per CTA
+constexpr int TNT = 32 * TT * TNTEAM;
+constexpr int TCH = 32 * TT;  // chunks per line segment
 
 struct Axis {
   int n = 0;            // cells along the sweep direction
@@ -167,21 +170,19 @@ bool cfd_table(int n, bool bar, std::vector<double>& tab, double& maxdev_lo, int
 
 // ---- tile planning along one axis
 bool plan_axis(adi::Axis& A, int method, int nlmin, int cap) {
-  const int M = adi::TM, NT = adi::TNT;
-  const int chmax = cap > 0 ? std::min(cap, NT / nlmin) : NT / nlmin;
+  (void)nlmin;
+  const int M = adi::TM;
+  const int chmax = cap > 0 ? std::min(cap, adi::TCH) : adi::TCH;
   const int P = A.n + 1;                       // positions 0..n
   const int halo = (method == ADI_CFD) ? 64 : 32;
   A.segs.clear();
   const int D = (M - P % M) % M;
   const int nch1 = (P + D) / M;
+  A.NL = adi::TNTEAM;
   if (nch1 <= chmax) {
-    int pw = 1;
-    while (pw < nch1) pw <<= 1;
-    A.NL = std::min(64, std::max(nlmin, NT / pw));  // exchange pad grows with NL
     A.segs.push_back({-(D / 2), nch1, 0, P});
     return true;
   }
-  A.NL = nlmin;
   const int CH = chmax;
   for (int S = 2; S <= P / M; ++S) {
     std::vector<adi::Seg> segs;
@@ -263,8 +264,8 @@ struct TimeScope {
 
 template <int METHOD, int MODE>
 int launch_t(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
-  auto kern = adi::adi_tile_kernel<METHOD, adi::TM, adi::TNT, MODE>;
-  const size_t smem = (size_t)(2 * adi::DYN + adi::NSTAT) * (adi::TNT + 4 * A.NL) * sizeof(double);
+  auto kern = adi::adi_tile_kernel<METHOD, adi::TM, adi::TT, adi::TNTEAM, MODE>;
+  const size_t smem = adi::tile_smem_bytes<adi::TM, adi::TT, adi::TNTEAM>();
   static bool attr[2][3] = {};
   if (!attr[METHOD][MODE]) {
     CUDA_TRY(h, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -315,7 +316,7 @@ adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
   std::memset(&p, 0, sizeof p);
   p.n = A.n;
   p.nlines = A.nlines;
-  p.NL = A.NL;
+  p.xmajor = ydir ? 0 : 1;
   p.plo = A.plo;
   p.phi = A.phi;
   p.segs = A.d_segs;
