@@ -493,8 +493,11 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, Tea
 // ===========================================================================
 // The tile kernel.  CTA = NTEAM lines x (T warps x 32 chunks x M points).
 // ===========================================================================
-template <int METHOD, int M, int T, int NTEAM, int MODE>
-__global__ void __launch_bounds__(32 * T * NTEAM, 1) adi_tile_kernel(const KParams P) {
+// XM = 1: positions contiguous in memory (row sweep, s_pt = x_pt = 1);
+// XM = 0: lines contiguous (column sweep, s_line = x_line = u_line = 1).
+template <int METHOD, int M, int T, int NTEAM, int XM, int MODE>
+__global__ void __launch_bounds__(32 * T * NTEAM, (NTEAM >= 4 ? 1 : 4 / NTEAM))
+    adi_tile_kernel(const KParams P) {
   constexpr int NT = 32 * T * NTEAM;
   constexpr int CH = 32 * T;     // chunks per team
   constexpr int NPOS = CH * M;   // positions per team segment
@@ -538,31 +541,32 @@ __global__ void __launch_bounds__(32 * T * NTEAM, 1) adi_tile_kernel(const KPara
   const double* Sbat = P.S_in ? P.S_in + b * P.s_batch : nullptr;
   const double* Xbat = P.X_in + b * P.x_batch;
   const bool want_phi = (MODE != KM_FINAL) && P.phi_src;
-  for (int e = t; e < NTEAM * NPOS; e += NT) {
+  constexpr int EPT = NTEAM * NPOS / NT;  // elements per thread per array
+  static_assert(NPOS % NT == 0 || XM == 0, "row tiles: NPOS must be a multiple of NT");
+  const int nact = sg.nchunks * M;
+#pragma unroll 4
+  for (int k = 0; k < EPT; ++k) {
     int tmi, pos;
-    if (P.xmajor) { tmi = e / NPOS; pos = e - tmi * NPOS; }
-    else { pos = e / NTEAM; tmi = e - pos * NTEAM; }
+    if (XM) { tmi = (t + k * NT) / NPOS; pos = (t + k * NT) % NPOS; }
+    else { tmi = t % NTEAM; pos = t / NTEAM + k * (NT / NTEAM); }
     const int ln = blockIdx.x * NTEAM + tmi;
     const int p = sg.start + pos;
-    const bool lv = ln < P.nlines && pos < sg.nchunks * M;
+    const bool lv = ln < P.nlines && pos < nact;
     const int si = (tmi * CH + pos / M) * PADM + pos % M;
     const bool uin = lv && p >= 1 && p <= uhi;
     const bool xin = lv && p >= 0 && p <= n;
+    // element offsets (one stride is 1 by construction of XM)
+    const long long offS = XM ? (long long)ln * P.s_line + (p - 1) : ln + (long long)(p - 1) * P.s_pt;
+    const long long offX = XM ? (long long)ln * P.x_line + p : ln + (long long)p * P.x_pt;
     // asynchronous 8-byte copies; an out-of-range element is zero-filled (src-size 0)
-    const double* sp = Xbat;
-    bool sok;
     if (MODE == KM_PROLOGUE) {
-      sok = xin;
-      if (sok) sp = Ubat + (long long)(ln + 1) * P.u_line + (long long)p * P.u_pt;
+      const long long offU = (long long)(ln + 1) + (long long)p * P.u_pt;  // column sweep only
+      cp_async8(stS + si, xin ? Ubat + offU : Xbat, xin);
     } else {
-      sok = uin;
-      if (sok) sp = Sbat + (long long)ln * P.s_line + (long long)(p - 1) * P.s_pt;
+      cp_async8(stS + si, uin ? Sbat + offS : Xbat, uin);
     }
-    cp_async8(stS + si, sp, sok);
-    cp_async8(stX + si, xin ? Xbat + (long long)ln * P.x_line + (long long)p * P.x_pt : Xbat, xin);
-    if (want_phi)
-      cp_async8(stF + si, uin ? P.phi_src + (long long)ln * P.s_line + (long long)(p - 1) * P.s_pt
-                              : P.phi_src, uin);
+    cp_async8(stX + si, xin ? Xbat + offX : Xbat, xin);
+    if (want_phi) cp_async8(stF + si, uin ? P.phi_src + offS : P.phi_src, uin);
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
   // Dirichlet values of this line
@@ -696,20 +700,23 @@ __global__ void __launch_bounds__(32 * T * NTEAM, 1) adi_tile_kernel(const KPara
   double* Xobat = P.X_out + b * P.x_batch;
   double* Uobat = P.U_out ? P.U_out + b * P.u_batch : nullptr;
   double acc = 0.0;
-  for (int e = t; e < NTEAM * NPOS; e += NT) {
+#pragma unroll 4
+  for (int k = 0; k < EPT; ++k) {
     int tmi, pos;
-    if (P.xmajor) { tmi = e / NPOS; pos = e - tmi * NPOS; }
-    else { pos = e / NTEAM; tmi = e - pos * NTEAM; }
+    if (XM) { tmi = (t + k * NT) / NPOS; pos = (t + k * NT) % NPOS; }
+    else { tmi = t % NTEAM; pos = t / NTEAM + k * (NT / NTEAM); }
     const int ln = blockIdx.x * NTEAM + tmi;
     const int p = sg.start + pos;
-    if (ln >= P.nlines || pos >= sg.nchunks * M) continue;
-    if (p < sg.out_lo || p >= sg.out_hi || p < 0 || p > n) continue;
+    const bool own = ln < P.nlines && pos < nact && p >= sg.out_lo && p < sg.out_hi && p >= 0 &&
+                     p <= n;
+    if (!own) continue;
     const int si = (tmi * CH + pos / M) * PADM + pos % M;
     const double xv = stX[si], uv = stS[si];
-    Xobat[(long long)ln * P.x_line + (long long)p * P.x_pt] = xv;
+    const long long offX = XM ? (long long)ln * P.x_line + p : ln + (long long)p * P.x_pt;
+    Xobat[offX] = xv;
     acc += xv;
     if (MODE == KM_FINAL) {
-      double* Ub = Uobat + (long long)(ln + 1) * P.u_line;
+      double* Ub = Uobat + (ln + 1);  // column sweep only (u_line = 1)
       Ub[(long long)p * P.u_pt] = uv;   // interior values and the Dirichlet slots
       acc += uv;
       if (METHOD == M_MFD && p == n) {
@@ -717,7 +724,8 @@ __global__ void __launch_bounds__(32 * T * NTEAM, 1) adi_tile_kernel(const KPara
         Ub[(long long)(n + 1) * P.u_pt] = gR;
       }
     } else if (p >= 1 && p <= uhi) {
-      Sobat[(long long)ln * P.s_line + (long long)(p - 1) * P.s_pt] = uv;
+      const long long offS = XM ? (long long)ln * P.s_line + (p - 1) : ln + (long long)(p - 1) * P.s_pt;
+      Sobat[offS] = uv;
       acc += uv;
     }
   }

@@ -27,8 +27,8 @@ namespace adi {
 
 constexpr int TM = 16;     // points per thread chunk
 constexpr int TT = 2;      // warps per team (one team per line segment)
-constexpr int TNTEAM = 4;  // teams (lines) per CTA
-constexpr int TNT = 32 * TT * TNTEAM;
+constexpr int XTEAMS = 1;  // lines per CTA in the row sweep (4 CTAs / SM)
+constexpr int YTEAMS = 2;  // lines per CTA in the column sweep (32-byte coalescing)
 constexpr int TCH = 32 * TT;  // chunks per line segment
 
 struct Axis {
@@ -178,7 +178,6 @@ bool plan_axis(adi::Axis& A, int method, int nlmin, int cap) {
   A.segs.clear();
   const int D = (M - P % M) % M;
   const int nch1 = (P + D) / M;
-  A.NL = adi::TNTEAM;
   if (nch1 <= chmax) {
     A.segs.push_back({-(D / 2), nch1, 0, P});
     return true;
@@ -262,17 +261,18 @@ struct TimeScope {
   }
 };
 
-template <int METHOD, int MODE>
+template <int METHOD, int MODE, int XM>
 int launch_t(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
-  auto kern = adi::adi_tile_kernel<METHOD, adi::TM, adi::TT, adi::TNTEAM, MODE>;
-  const size_t smem = adi::tile_smem_bytes<adi::TM, adi::TT, adi::TNTEAM>();
-  static bool attr[2][3] = {};
-  if (!attr[METHOD][MODE]) {
-    CUDA_TRY(h, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr[METHOD][MODE] = true;
+  constexpr int NTEAM = XM ? adi::XTEAMS : adi::YTEAMS;
+  auto kern = adi::adi_tile_kernel<METHOD, adi::TM, adi::TT, NTEAM, XM, MODE>;
+  const size_t smem = adi::tile_smem_bytes<adi::TM, adi::TT, NTEAM>();
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(h, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
   }
-  dim3 grid((A.nlines + A.NL - 1) / A.NL, (unsigned)A.segs.size(), h->batch);
-  kern<<<grid, adi::TNT, smem, h->stream>>>(p);
+  dim3 grid((A.nlines + NTEAM - 1) / NTEAM, (unsigned)A.segs.size(), h->batch);
+  kern<<<grid, 32 * adi::TT * NTEAM, smem, h->stream>>>(p);
   CUDA_TRY(h, cudaGetLastError());
   h->launches++;
   return ADI_OK;
@@ -280,14 +280,17 @@ int launch_t(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
 
 int launch(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p, int kind) {
   TimeScope ts(h, kind);
+  const bool xm = p.xmajor != 0;
   if (h->method == ADI_CFD) {
-    if (mode == adi::KM_SWEEP) return launch_t<adi::M_CFD, adi::KM_SWEEP>(h, A, p);
-    if (mode == adi::KM_FINAL) return launch_t<adi::M_CFD, adi::KM_FINAL>(h, A, p);
-    return launch_t<adi::M_CFD, adi::KM_PROLOGUE>(h, A, p);
+    if (mode == adi::KM_SWEEP)
+      return xm ? launch_t<adi::M_CFD, adi::KM_SWEEP, 1>(h, A, p) : launch_t<adi::M_CFD, adi::KM_SWEEP, 0>(h, A, p);
+    if (mode == adi::KM_FINAL) return launch_t<adi::M_CFD, adi::KM_FINAL, 0>(h, A, p);
+    return launch_t<adi::M_CFD, adi::KM_PROLOGUE, 0>(h, A, p);
   }
-  if (mode == adi::KM_SWEEP) return launch_t<adi::M_MFD, adi::KM_SWEEP>(h, A, p);
-  if (mode == adi::KM_FINAL) return launch_t<adi::M_MFD, adi::KM_FINAL>(h, A, p);
-  return launch_t<adi::M_MFD, adi::KM_PROLOGUE>(h, A, p);
+  if (mode == adi::KM_SWEEP)
+    return xm ? launch_t<adi::M_MFD, adi::KM_SWEEP, 1>(h, A, p) : launch_t<adi::M_MFD, adi::KM_SWEEP, 0>(h, A, p);
+  if (mode == adi::KM_FINAL) return launch_t<adi::M_MFD, adi::KM_FINAL, 0>(h, A, p);
+  return launch_t<adi::M_MFD, adi::KM_PROLOGUE, 0>(h, A, p);
 }
 
 // Dirichlet columns (x = 0, x = 1) of U at time factor gb, all rows (corners included)
