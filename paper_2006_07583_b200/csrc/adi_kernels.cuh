@@ -113,7 +113,7 @@ struct Mfd {
   // u-op: out = B - a * D4 x  (a = alpha/h); neighbours xm2,xm1 (prev chunk), xp1
   template <bool INTERIOR>
   static __device__ __forceinline__ void uop(const Ctx<M>& c, const double (&x)[M],
-                                             const double (&B)[M], double (&out)[M], double a,
+                                             const double* __restrict__ B, double (&out)[M], double a,
                                              double xm2, double xm1, double xp1) {
     const double cA = a * (1.0 / 24.0), cB = a * (9.0 / 8.0);
 #pragma unroll
@@ -148,7 +148,7 @@ struct Mfd {
   // x-op: out = B - b * G4 ū ; neighbours um1 (prev chunk), up1, up2 (next chunk)
   template <bool INTERIOR>
   static __device__ __forceinline__ void xop(const Ctx<M>& c, const double (&u)[M],
-                                             const double (&B)[M], double (&out)[M], double b,
+                                             const double* __restrict__ B, double (&out)[M], double b,
                                              double um1, double up1, double up2) {
     const double cC = b * (1.0 / 24.0), cD = b * (9.0 / 8.0);
 #pragma unroll
@@ -263,19 +263,44 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
 __device__ __forceinline__ double shup(double v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
 __device__ __forceinline__ double shdn(double v, int d) { return __shfl_down_sync(0xffffffffu, v, d); }
 
+
 // ---------------------------------------------------------------------------
-// Team exchange: lanes of one warp are consecutive chunks of one line; the T
-// warps of a team cover consecutive runs of 32 chunks.  Cross-warp edge values
-// go through an 8-slot shared-memory mailbox per warp (double-buffered) and a
-// named barrier over the team's 32*T threads.
+// Split-phase team exchange.  Lanes of one warp are consecutive chunks of one
+// line and see each other's edge values by warp shuffles.  The T warps of a
+// team cover consecutive runs of 32 chunks; the two boundary lanes of each warp
+// post their edge values in an 8-slot shared-memory mailbox (double-buffered)
+// and ARRIVE on the team's mbarrier (publish); the consumer WAITS on it only
+// when it finally needs the values (collect), so the neighbour-independent
+// inner points of the next operator are computed while the barrier completes.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  unsigned ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
 template <int T>
 struct Team {
-  double* box;  // [2][T][8]
-  int lane, wt, bar, buf;
-  __device__ __forceinline__ void sync() const {
-    if (T > 1) asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(32 * T) : "memory");
-  }
+  double* box;               // [2][T][8] mailbox
+  unsigned long long* bar;   // team mbarrier (count 32*T)
+  int lane, wt, buf;
+  unsigned par;
   __device__ __forceinline__ double* slot(int w) const { return box + (buf * T + w) * 8; }
   // neighbour warp's mailbox value k, 0 if there is no neighbour warp (branch-free)
   __device__ __forceinline__ double pv(int k) const {
@@ -286,27 +311,39 @@ struct Team {
     const double v = slot(wt < T - 1 ? wt + 1 : wt)[k];
     return wt < T - 1 ? v : 0.0;
   }
+  __device__ __forceinline__ void arrive() { if (T > 1) mbar_arrive(bar); }
+  __device__ __forceinline__ void wait() {
+    if (T > 1) { mbar_wait(bar, par); par ^= 1u; }
+  }
+  __device__ __forceinline__ void flip() { buf ^= 1; }
 };
 
-// neighbours' edge values of a chunk array: prev chunk's a[M-2], a[M-1]; next chunk's a[0], a[1]
+// publish the edge values of a chunk array (a[0], a[1], a[M-2], a[M-1])
 template <int M, int T>
-__device__ __forceinline__ void edge_exchange(Team<T>& tm, const double (&a)[M], double& pm2,
-                                              double& pm1, double& np1, double& np2) {
+__device__ __forceinline__ void edge_publish(Team<T>& tm, const double (&a)[M]) {
+  if (T > 1) {
+    double* s = tm.slot(tm.wt);
+    if (tm.lane == 31) { s[0] = a[M - 2]; s[1] = a[M - 1]; }
+    if (tm.lane == 0) { s[2] = a[0]; s[3] = a[1]; }
+    tm.arrive();
+  }
+}
+// collect the neighbours' edge values: prev chunk's a[M-2], a[M-1]; next chunk's a[0], a[1]
+template <int M, int T>
+__device__ __forceinline__ void edge_collect(Team<T>& tm, const double (&a)[M], double& pm2,
+                                             double& pm1, double& np1, double& np2) {
   pm2 = shup(a[M - 2], 1);
   pm1 = shup(a[M - 1], 1);
   np1 = shdn(a[0], 1);
   np2 = shdn(a[1], 1);
   if (T > 1) {
-    double* s = tm.slot(tm.wt);
-    if (tm.lane == 31) { s[0] = a[M - 2]; s[1] = a[M - 1]; }
-    if (tm.lane == 0) { s[2] = a[0]; s[3] = a[1]; }
-    tm.sync();
+    tm.wait();
     const double q0 = tm.pv(0), q1 = tm.pv(1), q2 = tm.nx(2), q3 = tm.nx(3);
     pm2 = tm.lane == 0 ? q0 : pm2;
     pm1 = tm.lane == 0 ? q1 : pm1;
     np1 = tm.lane == 31 ? q2 : np1;
     np2 = tm.lane == 31 ? q3 : np2;
-    tm.buf ^= 1;
+    tm.flip();
   } else {
     pm2 = tm.lane == 0 ? 0.0 : pm2;
     pm1 = tm.lane == 0 ? 0.0 : pm1;
@@ -314,6 +351,46 @@ __device__ __forceinline__ void edge_exchange(Team<T>& tm, const double (&a)[M],
     np2 = tm.lane == 31 ? 0.0 : np2;
   }
 }
+template <int M, int T>
+__device__ __forceinline__ void edge_exchange(Team<T>& tm, const double (&a)[M], double& pm2,
+                                              double& pm1, double& np1, double& np2) {
+  edge_publish<M, T>(tm, a);
+  edge_collect<M, T>(tm, a, pm2, pm1, np1, np2);
+}
+
+// ===========================================================================
+// MFD interior operators split into neighbour-independent inner points and the
+// edge points that need the neighbours' values (same arithmetic as Mfd<M>).
+// ===========================================================================
+template <int M>
+struct MfdSplit {
+  // u-op: out_i = B_i + cA (x_{i+1} - x_{i-2}) + cB (x_{i-1} - x_i)
+  static __device__ __forceinline__ void u_inner(const double (&x)[M], const double* __restrict__ B,
+                                                 double (&out)[M], double cA, double cB) {
+#pragma unroll
+    for (int i = 2; i <= M - 2; ++i) out[i] = fma(cA, x[i + 1] - x[i - 2], fma(cB, x[i - 1] - x[i], B[i]));
+  }
+  static __device__ __forceinline__ void u_edges(const double (&x)[M], const double* __restrict__ B,
+                                                 double (&out)[M], double cA, double cB, double xm2,
+                                                 double xm1, double xp1) {
+    out[0] = fma(cA, x[1] - xm2, fma(cB, xm1 - x[0], B[0]));
+    out[1] = fma(cA, x[2] - xm1, fma(cB, x[0] - x[1], B[1]));
+    out[M - 1] = fma(cA, xp1 - x[M - 3], fma(cB, x[M - 2] - x[M - 1], B[M - 1]));
+  }
+  // x-op: out_i = B_i + cC (u_{i+2} - u_{i-1}) + cD (u_i - u_{i+1})
+  static __device__ __forceinline__ void x_inner(const double (&u)[M], const double* __restrict__ B,
+                                                 double (&out)[M], double cC, double cD) {
+#pragma unroll
+    for (int i = 1; i <= M - 3; ++i) out[i] = fma(cC, u[i + 2] - u[i - 1], fma(cD, u[i] - u[i + 1], B[i]));
+  }
+  static __device__ __forceinline__ void x_edges(const double (&u)[M], const double* __restrict__ B,
+                                                 double (&out)[M], double cC, double cD, double um1,
+                                                 double up1, double up2) {
+    out[0] = fma(cC, u[2] - um1, fma(cD, u[0] - u[1], B[0]));
+    out[M - 2] = fma(cC, up1 - u[M - 3], fma(cD, u[M - 2] - u[M - 1], B[M - 2]));
+    out[M - 1] = fma(cC, up2 - u[M - 2], fma(cD, u[M - 1] - up1, B[M - 1]));
+  }
+};
 
 // ===========================================================================
 // CFD statics of a chunk for one system: F = G_e, K_s, K_e, J_s, J_e.
@@ -350,11 +427,19 @@ __device__ __forceinline__ void cfd_statics(const Ctx<M>& c, const double* tab, 
   st[3] = j;
 }
 
+// CFD interior sub-chunking: a chunk of M points is solved as NSUB independent
+// sub-chunks of L points (NSUB interleaved recurrences), recombined with the
+// same carry algebra one level down.  c_sK/c_sJ/c_sF are the
+// responses of an interior sub-chunk of length L.
+constexpr int NSUB = 4;
+__constant__ double c_sK[MMAX], c_sJ[MMAX];
+__constant__ double c_sF;
+
 // ===========================================================================
 // CFD: one operator application out = B - coef * T^{-1} r(o) on the team's
 // segment (T = P̄ for the u-op, P for the x-op), truncated SPIKE across chunks.
-// Phase 1: local solve with zero carries; exchange (y_e, z_s, z_e) with the
-// neighbours; phase 2: carries + fix-up.  Also returns this op's output at the
+// Phase 1: local solve with zero carries; publish (y_e, z_s, z_e); collect the
+// neighbours'; phase 2: carries + fix-up.  Also returns this op's output at the
 // previous chunk's last and the next chunk's first position (operand
 // neighbours of the next op) without another exchange.
 // st: shared table [5][CH] of this team's chunk statics for this system.
@@ -362,24 +447,40 @@ __device__ __forceinline__ void cfd_statics(const Ctx<M>& c, const double* tab, 
 template <int M, int T, bool UOP>
 __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, Team<T>& tm,
                                           const double* st, int CH, const double (&o)[M],
-                                          const double (&B)[M], double (&out)[M], double coef,
+                                          const double* __restrict__ B, double (&out)[M], double coef,
                                           double om1, double op1, double Bn_first,
                                           double Bp_last, double& nom1, double& nop1) {
+  constexpr int L = M / NSUB;
   const double* tab = UOP ? P.tabU : P.tabX;
   const int np1 = c.n + 1;
   double yl_e, ws, we;
+  double ysub[NSUB];  // local y at the end of each sub-chunk (zero carries)
   // ---------------- phase 1: local solve with zero carries ----------------
   if (c.interior) {
     if (UOP) Cfd<M>::template rhs_u<true>(c, o, out, om1, op1);
     else Cfd<M>::template rhs_x<true>(c, o, out, om1, op1);
-    const double l = c_cl, iv = c_cinvd;
+    const double l = c_cl, iv = c_cinvd, FL = c_sF;
 #pragma unroll
-    for (int i = 1; i < M; ++i) out[i] = fma(-l, out[i - 1], out[i]);
-    yl_e = out[M - 1];
+    for (int i = 1; i < L; ++i)
 #pragma unroll
-    for (int i = M - 2; i >= 0; --i) out[i] = fma(-iv, out[i + 1], out[i]);
-    ws = iv * out[0];
-    we = iv * out[M - 1];
+      for (int j = 0; j < NSUB; ++j) out[j * L + i] = fma(-l, out[j * L + i - 1], out[j * L + i]);
+#pragma unroll
+    for (int j = 0; j < NSUB; ++j) ysub[j] = out[j * L + L - 1];
+#pragma unroll
+    for (int i = L - 2; i >= 0; --i)
+#pragma unroll
+      for (int j = 0; j < NSUB; ++j) out[j * L + i] = fma(-iv, out[j * L + i + 1], out[j * L + i]);
+    // chunk-level values with zero external carries
+    double Y[NSUB];
+    Y[0] = ysub[0];
+#pragma unroll
+    for (int j = 1; j < NSUB; ++j) Y[j] = fma(FL, Y[j - 1], ysub[j]);
+    yl_e = Y[NSUB - 1];
+    double zc = 0.0;  // z at the start of sub-chunk j+1
+#pragma unroll
+    for (int j = NSUB - 2; j >= 0; --j) zc = fma(c_sJ[0], zc, fma(c_sK[0], Y[j], iv * out[(j + 1) * L]));
+    ws = fma(c_sJ[0], zc, iv * out[0]);
+    we = fma(c_sK[L - 1], Y[NSUB - 2], iv * out[M - 1]);
   } else {
     if (UOP) Cfd<M>::template rhs_u<false>(c, o, out, om1, op1);
     else Cfd<M>::template rhs_x<false>(c, o, out, om1, op1);
@@ -407,8 +508,6 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, Tea
   }
   if (!c.live) { yl_e = 0.0; ws = 0.0; we = 0.0; }
   // ---------------- exchange ----------------
-  double ylm1 = shup(yl_e, 1), ylm2 = shup(yl_e, 2), ylp1 = shdn(yl_e, 1);
-  double wsp1 = shdn(ws, 1), wsp2 = shdn(ws, 2), wem1 = shup(we, 1);
   const int lane = tm.lane;
   if (T > 1) {
     double* s = tm.slot(tm.wt);
@@ -416,24 +515,10 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, Tea
     if (lane == 31) { s[1] = yl_e; s[2] = we; }
     if (lane == 0) { s[3] = ws; s[5] = yl_e; }
     if (lane == 1) s[4] = ws;
-    tm.sync();
-    const double p0 = tm.pv(0), p1 = tm.pv(1), p2 = tm.pv(2);
-    const double n3 = tm.nx(3), n4 = tm.nx(4), n5 = tm.nx(5);
-    ylm1 = lane == 0 ? p1 : ylm1;
-    ylm2 = lane == 0 ? p0 : (lane == 1 ? p1 : ylm2);
-    wem1 = lane == 0 ? p2 : wem1;
-    ylp1 = lane == 31 ? n5 : ylp1;
-    wsp1 = lane == 31 ? n3 : wsp1;
-    wsp2 = lane == 31 ? n4 : (lane == 30 ? n3 : wsp2);
-    tm.buf ^= 1;
-  } else {
-    ylm1 = lane == 0 ? 0.0 : ylm1;
-    ylm2 = lane <= 1 ? 0.0 : ylm2;
-    wem1 = lane == 0 ? 0.0 : wem1;
-    ylp1 = lane == 31 ? 0.0 : ylp1;
-    wsp1 = lane == 31 ? 0.0 : wsp1;
-    wsp2 = lane >= 30 ? 0.0 : wsp2;
+    tm.arrive();
   }
+  double ylm1 = shup(yl_e, 1), ylm2 = shup(yl_e, 2), ylp1 = shdn(yl_e, 1);
+  double wsp1 = shdn(ws, 1), wsp2 = shdn(ws, 2), wem1 = shup(we, 1);
   // statics of the neighbours (constants when all of c-2..c+2 are interior)
   double Fm1, Fme, Ksp1, Jsp1, Ksp2, Kem1, Jem1;
   if (c.nbint) {
@@ -445,18 +530,49 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, Tea
     Ksp1 = at(ST_KS, ch + 1); Jsp1 = at(ST_JS, ch + 1); Ksp2 = at(ST_KS, ch + 2);
     Kem1 = at(ST_KE, ch - 1); Jem1 = at(ST_JE, ch - 1);
   }
+  if (T > 1) {
+    tm.wait();
+    const double p0 = tm.pv(0), p1 = tm.pv(1), p2 = tm.pv(2);
+    const double n3 = tm.nx(3), n4 = tm.nx(4), n5 = tm.nx(5);
+    ylm1 = lane == 0 ? p1 : ylm1;
+    ylm2 = lane == 0 ? p0 : (lane == 1 ? p1 : ylm2);
+    wem1 = lane == 0 ? p2 : wem1;
+    ylp1 = lane == 31 ? n5 : ylp1;
+    wsp1 = lane == 31 ? n3 : wsp1;
+    wsp2 = lane == 31 ? n4 : (lane == 30 ? n3 : wsp2);
+    tm.flip();
+  } else {
+    ylm1 = lane == 0 ? 0.0 : ylm1;
+    ylm2 = lane <= 1 ? 0.0 : ylm2;
+    wem1 = lane == 0 ? 0.0 : wem1;
+    ylp1 = lane == 31 ? 0.0 : ylp1;
+    wsp1 = lane == 31 ? 0.0 : wsp1;
+    wsp2 = lane >= 30 ? 0.0 : wsp2;
+  }
   // ---------------- phase 2: carries and fix-up ----------------
   const double ycarry = fma(Fm1, ylm2, ylm1);   // true y at s-1
   const double ycn = fma(Fme, ycarry, yl_e);    // true y at s+M-1
   const double zcarry = fma(Jsp1, fma(Ksp2, ylp1, wsp2), fma(Ksp1, ycn, wsp1));  // true z at s+M
   double z0;
   if (c.interior) {
-    const double iv = c_cinvd;
-    z0 = fma(c_cJ[0], zcarry, fma(c_cK[0], ycarry, iv * out[0]));
-    const double cy = coef * ycarry, cz = coef * zcarry, ci = coef * iv;
+    const double iv = c_cinvd, FL = c_sF;
+    double ycT[NSUB], zcT[NSUB];
+    ycT[0] = ycarry;
 #pragma unroll
-    for (int i = 0; i < M; ++i)
-      out[i] = fma(-c_cJ[i], cz, fma(-c_cK[i], cy, fma(-ci, out[i], B[i])));
+    for (int j = 1; j < NSUB; ++j) ycT[j] = fma(FL, ycT[j - 1], ysub[j - 1]);
+    zcT[NSUB - 1] = zcarry;
+#pragma unroll
+    for (int j = NSUB - 2; j >= 0; --j)
+      zcT[j] = fma(c_sJ[0], zcT[j + 1], fma(c_sK[0], ycT[j + 1], iv * out[(j + 1) * L]));
+    z0 = fma(c_sJ[0], zcT[0], fma(c_sK[0], ycT[0], iv * out[0]));
+    const double ci = coef * iv;
+#pragma unroll
+    for (int j = 0; j < NSUB; ++j) {
+      const double cy = coef * ycT[j], cz = coef * zcT[j];
+#pragma unroll
+      for (int i = 0; i < L; ++i)
+        out[j * L + i] = fma(-c_sJ[i], cz, fma(-c_sK[i], cy, fma(-ci, out[j * L + i], B[j * L + i])));
+    }
   } else {
     double g = 1.0;
 #pragma unroll
@@ -495,8 +611,15 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, Tea
 // ===========================================================================
 // XM = 1: positions contiguous in memory (row sweep, s_pt = x_pt = 1);
 // XM = 0: lines contiguous (column sweep, s_line = x_line = u_line = 1).
+// Occupancy target (resident CTAs per SM) per method and CTA size: the kernels
+// are latency-bound, so registers are capped to keep >= 12-14 warps per SM.
+template <int METHOD, int NTEAM>
+struct Occ {
+  static constexpr int value = (METHOD == M_MFD) ? (NTEAM == 1 ? 7 : 3) : (NTEAM == 1 ? 6 : 3);
+};
+
 template <int METHOD, int M, int T, int NTEAM, int XM, int MODE>
-__global__ void __launch_bounds__(32 * T * NTEAM, (NTEAM >= 4 ? 1 : 4 / NTEAM))
+__global__ void __launch_bounds__(32 * T * NTEAM, (Occ<METHOD, NTEAM>::value))
     adi_tile_kernel(const KParams P) {
   constexpr int NT = 32 * T * NTEAM;
   constexpr int CH = 32 * T;     // chunks per team
@@ -508,6 +631,7 @@ __global__ void __launch_bounds__(32 * T * NTEAM, (NTEAM >= 4 ? 1 : 4 / NTEAM))
   double* stF = stX + NTEAM * CH * PADM;       // staging: phi (source pattern)
   double* stc = stF + NTEAM * CH * PADM;       // CFD statics [NTEAM][2 sys][5][CH]
   double* boxes = stc + NTEAM * 10 * CH;       // team mailboxes [NTEAM][2][T][8]
+  unsigned long long* mbars = (unsigned long long*)(boxes + NTEAM * 2 * T * 8);  // [NTEAM]
 
   const int t = threadIdx.x;
   const int warp = t >> 5, lane = t & 31;
@@ -534,7 +658,9 @@ __global__ void __launch_bounds__(32 * T * NTEAM, (NTEAM >= 4 ? 1 : 4 / NTEAM))
 
   Team<T> tm;
   tm.box = boxes + team * 2 * T * 8;
-  tm.lane = lane; tm.wt = wt; tm.bar = 1 + team; tm.buf = 0;
+  tm.bar = mbars + team;
+  tm.lane = lane; tm.wt = wt; tm.buf = 0; tm.par = 0u;
+  if (T > 1 && t < NTEAM) mbar_init(mbars + t, 32 * T);
 
   // ---- cooperative coalesced load of the tile into the padded staging area
   const double* Ubat = P.U_in ? P.U_in + b * P.u_batch : nullptr;
@@ -584,28 +710,25 @@ __global__ void __launch_bounds__(32 * T * NTEAM, (NTEAM >= 4 ? 1 : 4 / NTEAM))
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
 
-  double u[M], x[M], S[M], V[M];
-  {
-    const double* ss = stS + (team * CH + ch) * PADM;
-    const double* xs = stX + (team * CH + ch) * PADM;
+  // The read-only bases S (u-op) and X (x-op) stay in the staging tile (shared
+  // memory); only the iterated u and x live in registers.
+  double* Sm = stS + (team * CH + ch) * PADM;
+  double* Vm = stX + (team * CH + ch) * PADM;
+  double u[M], x[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i) {
-      const int p = c.s + i;
-      x[i] = xs[i];
-      V[i] = x[i];
-      if (MODE == KM_PROLOGUE) {
-        u[i] = ss[i];
-        S[i] = 0.0;
-      } else {
-        S[i] = ss[i];
-        u[i] = (p == 0) ? c.gL : ((METHOD == M_CFD && p == n) ? c.gR : 0.0);
-        if (!c.live) u[i] = 0.0;
-      }
+  for (int i = 0; i < M; ++i) {
+    const int p = c.s + i;
+    x[i] = Vm[i];
+    if (MODE == KM_PROLOGUE) {
+      u[i] = Sm[i];
+    } else {
+      u[i] = (p == 0) ? c.gL : ((METHOD == M_CFD && p == n) ? c.gR : 0.0);
+      if (!c.live) u[i] = 0.0;
     }
   }
 
   // dst = src + dt/2 F at this chunk's points (F = phi*gf + point source)
-  auto add_source = [&](double (&dst)[M], const double (&src)[M]) {
+  auto add_source = [&](double* dst, const double (&src)[M]) {
     const double* fs = stF + (team * CH + ch) * PADM;
     const int ptl = P.pt_line ? P.pt_line[b] : -1;
     const int ptp = P.pt_pos ? P.pt_pos[b] : -1;
@@ -632,69 +755,89 @@ __global__ void __launch_bounds__(32 * T * NTEAM, (NTEAM >= 4 ? 1 : 4 / NTEAM))
 #pragma unroll
       for (int k = 0; k < 5; ++k) stXs[k * CH + ch] = c.live ? q[k] : 0.0;
     }
-    // neighbour edge values of x (and u in the prologue) and of the bases S, V
-    double d0, d1, xm1, xp1, um1, up1, SLp, SFn, VLp, VFn;
+    // neighbour edge values of x (and u in the prologue); the bases' neighbour
+    // values are read straight from the staging tile
+    double d0, d1, xm1, xp1, um1, up1;
+    const double* tS = stS + team * CH * PADM;
+    const double* tX = stX + team * CH * PADM;
+    const double SLp = ch > 0 ? tS[(ch - 1) * PADM + M - 1] : 0.0;
+    const double SFn = ch + 1 < CH ? tS[(ch + 1) * PADM] : 0.0;
+    const double VLp = ch > 0 ? tX[(ch - 1) * PADM + M - 1] : 0.0;
+    const double VFn = ch + 1 < CH ? tX[(ch + 1) * PADM] : 0.0;
+    __syncthreads();  // statics visible, mbarriers initialised
     edge_exchange<M, T>(tm, x, d0, xm1, xp1, d1);
     edge_exchange<M, T>(tm, u, d0, um1, up1, d1);
-    edge_exchange<M, T>(tm, S, d0, SLp, SFn, d1);
-    edge_exchange<M, T>(tm, V, d0, VLp, VFn, d1);
-    __syncthreads();  // statics visible
     if (MODE == KM_PROLOGUE) {
       double e1, e2;
-      cfd_apply<M, T, false>(c, P, tm, stXs, CH, u, V, x, P.cx, um1, up1, 0.0, 0.0, e1, e2);
-      add_source(S, u);
-      cfd_apply<M, T, true>(c, P, tm, stU, CH, V, S, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
+      double w[M];
+#pragma unroll
+      for (int i = 0; i < M; ++i) w[i] = x[i];
+      cfd_apply<M, T, false>(c, P, tm, stXs, CH, u, Vm, x, P.cx, um1, up1, 0.0, 0.0, e1, e2);
+      add_source(Sm, u);
+      cfd_apply<M, T, true>(c, P, tm, stU, CH, w, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
     } else {
       for (int k = 0; k < P.K; ++k) {
-        cfd_apply<M, T, true>(c, P, tm, stU, CH, x, S, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
-        cfd_apply<M, T, false>(c, P, tm, stXs, CH, u, V, x, P.cx, um1, up1, VFn, VLp, xm1, xp1);
+        cfd_apply<M, T, true>(c, P, tm, stU, CH, x, Sm, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
+        cfd_apply<M, T, false>(c, P, tm, stXs, CH, u, Vm, x, P.cx, um1, up1, VFn, VLp, xm1, xp1);
       }
       if (MODE == KM_SWEEP) {
         double e1, e2;
-        add_source(S, u);
-        cfd_apply<M, T, true>(c, P, tm, stU, CH, x, S, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
+        add_source(Sm, u);
+        cfd_apply<M, T, true>(c, P, tm, stU, CH, x, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
 #pragma unroll
-        for (int i = 0; i < M; ++i) x[i] = fma(2.0, x[i], -V[i]);
+        for (int i = 0; i < M; ++i) x[i] = fma(2.0, x[i], -Vm[i]);
       }
     }
   } else {
     // ---------------- MFD ----------------
-    double xm2, xm1, xp1, xp2, um2, um1, up1, up2;
-    edge_exchange<M, T>(tm, x, xm2, xm1, xp1, xp2);
     const double au = P.cu, bx = P.cx;
+    const double cA = au * (1.0 / 24.0), cB = au * (9.0 / 8.0);
+    const double cC = bx * (1.0 / 24.0), cD = bx * (9.0 / 8.0);
+    double xm2, xm1, xp1, xp2, um2, um1, up1, up2;
+    // u-op with its operand's exchange already published: inner points first,
+    // then collect the neighbours' edge values, then the edge points
+    auto u_op = [&](const double (&opd)[M], const double* __restrict__ B) {
+      if (c.interior) MfdSplit<M>::u_inner(opd, B, u, cA, cB);
+      edge_collect<M, T>(tm, opd, xm2, xm1, xp1, xp2);
+      if (c.interior) MfdSplit<M>::u_edges(opd, B, u, cA, cB, xm2, xm1, xp1);
+      else Mfd<M>::template uop<false>(c, opd, B, u, au, xm2, xm1, xp1);
+    };
+    auto x_op = [&](const double* __restrict__ B) {
+      if (c.interior) MfdSplit<M>::x_inner(u, B, x, cC, cD);
+      edge_collect<M, T>(tm, u, um2, um1, up1, up2);
+      if (c.interior) MfdSplit<M>::x_edges(u, B, x, cC, cD, um1, up1, up2);
+      else Mfd<M>::template xop<false>(c, u, B, x, bx, um1, up1, up2);
+    };
+    __syncthreads();  // mbarriers initialised
     if (MODE == KM_PROLOGUE) {
-      edge_exchange<M, T>(tm, u, um2, um1, up1, up2);
-      if (c.interior) Mfd<M>::template xop<true>(c, u, V, x, bx, um1, up1, up2);
-      else Mfd<M>::template xop<false>(c, u, V, x, bx, um1, up1, up2);
-      add_source(S, u);
-      if (c.interior) Mfd<M>::template uop<true>(c, V, S, u, au, xm2, xm1, xp1);
-      else Mfd<M>::template uop<false>(c, V, S, u, au, xm2, xm1, xp1);
+      double w[M];
+#pragma unroll
+      for (int i = 0; i < M; ++i) w[i] = x[i];
+      edge_publish<M, T>(tm, u);
+      x_op(Vm);                     // W* = W - beta D(U)
+      add_source(Sm, u);            // S = U + dt/2 F
+      edge_publish<M, T>(tm, w);
+      u_op(w, Sm);                  // S1 = S - alpha D̄(W)
     } else {
+      edge_publish<M, T>(tm, x);
       for (int k = 0; k < P.K; ++k) {
-        if (c.interior) Mfd<M>::template uop<true>(c, x, S, u, au, xm2, xm1, xp1);
-        else Mfd<M>::template uop<false>(c, x, S, u, au, xm2, xm1, xp1);
-        edge_exchange<M, T>(tm, u, um2, um1, up1, up2);
-        if (c.interior) Mfd<M>::template xop<true>(c, u, V, x, bx, um1, up1, up2);
-        else Mfd<M>::template xop<false>(c, u, V, x, bx, um1, up1, up2);
-        if (k + 1 < P.K || MODE == KM_SWEEP) edge_exchange<M, T>(tm, x, xm2, xm1, xp1, xp2);
+        u_op(x, Sm);
+        edge_publish<M, T>(tm, u);
+        x_op(Vm);
+        if (k + 1 < P.K || MODE == KM_SWEEP) edge_publish<M, T>(tm, x);
       }
       if (MODE == KM_SWEEP) {
-        add_source(S, u);
-        if (c.interior) Mfd<M>::template uop<true>(c, x, S, u, au, xm2, xm1, xp1);
-        else Mfd<M>::template uop<false>(c, x, S, u, au, xm2, xm1, xp1);
+        add_source(Sm, u);
+        u_op(x, Sm);
 #pragma unroll
-        for (int i = 0; i < M; ++i) x[i] = fma(2.0, x[i], -V[i]);
+        for (int i = 0; i < M; ++i) x[i] = fma(2.0, x[i], -Vm[i]);
       }
     }
   }
 
   // ---- stage the outputs (own chunk only) and store the owned range coalesced
-  {
-    double* ss = stS + (team * CH + ch) * PADM;
-    double* xs = stX + (team * CH + ch) * PADM;
 #pragma unroll
-    for (int i = 0; i < M; ++i) { ss[i] = u[i]; xs[i] = x[i]; }
-  }
+  for (int i = 0; i < M; ++i) { Sm[i] = u[i]; Vm[i] = x[i]; }
   __syncthreads();
   double* Sobat = P.S_out ? P.S_out + b * P.s_batch : nullptr;
   double* Xobat = P.X_out + b * P.x_batch;
@@ -735,7 +878,7 @@ __global__ void __launch_bounds__(32 * T * NTEAM, (NTEAM >= 4 ? 1 : 4 / NTEAM))
 // shared memory bytes of one CTA
 template <int M, int T, int NTEAM>
 constexpr size_t tile_smem_bytes() {
-  return sizeof(double) * (size_t)(3 * NTEAM * 32 * T * (M + 1) + NTEAM * 10 * 32 * T + NTEAM * 2 * T * 8);
+  return sizeof(double) * (size_t)(3 * NTEAM * 32 * T * (M + 1) + NTEAM * 10 * 32 * T + NTEAM * 2 * T * 8 + NTEAM);
 }
 
 }  // namespace adi

@@ -131,6 +131,25 @@ int init_constants(adi_ctx* h) {
   CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cKe, &Ke, sizeof Ke));
   CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cJs, &Js, sizeof Js));
   CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cJe, &Je, sizeof Je));
+  // responses of an interior sub-chunk of L = M / NSUB points (same formulas)
+  {
+    const int L = M / adi::NSUB;
+    double Gs[adi::MMAX], sK[adi::MMAX], sJ[adi::MMAX];
+    double gg = 1.0;
+    for (int i = 0; i < L; ++i) { gg *= -l; Gs[i] = gg; }
+    double kk = 0.0, jj = 1.0;
+    for (int i = L - 1; i >= 0; --i) {
+      kk = (Gs[i] - kk) * invd;
+      jj *= -invd;
+      sK[i] = kk;
+      sJ[i] = jj;
+    }
+    for (int i = L; i < adi::MMAX; ++i) sK[i] = sJ[i] = 0.0;
+    const double sF = Gs[L - 1];
+    CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_sK, sK, sizeof sK));
+    CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_sJ, sJ, sizeof sJ));
+    CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_sF, &sF, sizeof sF));
+  }
   g_const_ready = true;
   return ADI_OK;
 }
