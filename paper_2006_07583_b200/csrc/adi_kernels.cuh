@@ -615,7 +615,7 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, Tea
 // are latency-bound, so registers are capped to keep >= 12-14 warps per SM.
 template <int METHOD, int NTEAM>
 struct Occ {
-  static constexpr int value = (METHOD == M_MFD) ? (NTEAM == 1 ? 7 : 3) : (NTEAM == 1 ? 6 : 3);
+  static constexpr int value = (METHOD == M_MFD) ? (NTEAM == 1 ? 7 : (NTEAM == 2 ? 3 : 2)) : (NTEAM == 1 ? 6 : (NTEAM == 2 ? 3 : 2));
 };
 
 template <int METHOD, int M, int T, int NTEAM, int XM, int MODE>
@@ -625,11 +625,12 @@ __global__ void __launch_bounds__(32 * T * NTEAM, (Occ<METHOD, NTEAM>::value))
   constexpr int CH = 32 * T;     // chunks per team
   constexpr int NPOS = CH * M;   // positions per team segment
   constexpr int PADM = M + 1;    // padded chunk stride in the staging tile
+  constexpr int TSTR = CH * PADM + 2;  // team stride (+2 doubles: teams on different banks)
   extern __shared__ double smem[];
   double* stS = smem;                          // staging: S (or U in the prologue)
-  double* stX = stS + NTEAM * CH * PADM;       // staging: X
-  double* stF = stX + NTEAM * CH * PADM;       // staging: phi (source pattern)
-  double* stc = stF + NTEAM * CH * PADM;       // CFD statics [NTEAM][2 sys][5][CH]
+  double* stX = stS + NTEAM * TSTR;       // staging: X
+  double* stF = stX + NTEAM * TSTR;       // staging: phi (source pattern)
+  double* stc = stF + NTEAM * TSTR;       // CFD statics [NTEAM][2 sys][5][CH]
   double* boxes = stc + NTEAM * 10 * CH;       // team mailboxes [NTEAM][2][T][8]
   unsigned long long* mbars = (unsigned long long*)(boxes + NTEAM * 2 * T * 8);  // [NTEAM]
 
@@ -678,7 +679,7 @@ __global__ void __launch_bounds__(32 * T * NTEAM, (Occ<METHOD, NTEAM>::value))
     const int ln = blockIdx.x * NTEAM + tmi;
     const int p = sg.start + pos;
     const bool lv = ln < P.nlines && pos < nact;
-    const int si = (tmi * CH + pos / M) * PADM + pos % M;
+    const int si = tmi * TSTR + (pos / M) * PADM + pos % M;
     const bool uin = lv && p >= 1 && p <= uhi;
     const bool xin = lv && p >= 0 && p <= n;
     // element offsets (one stride is 1 by construction of XM)
@@ -712,8 +713,8 @@ __global__ void __launch_bounds__(32 * T * NTEAM, (Occ<METHOD, NTEAM>::value))
 
   // The read-only bases S (u-op) and X (x-op) stay in the staging tile (shared
   // memory); only the iterated u and x live in registers.
-  double* Sm = stS + (team * CH + ch) * PADM;
-  double* Vm = stX + (team * CH + ch) * PADM;
+  double* Sm = stS + team * TSTR + ch * PADM;
+  double* Vm = stX + team * TSTR + ch * PADM;
   double u[M], x[M];
 #pragma unroll
   for (int i = 0; i < M; ++i) {
@@ -729,7 +730,7 @@ __global__ void __launch_bounds__(32 * T * NTEAM, (Occ<METHOD, NTEAM>::value))
 
   // dst = src + dt/2 F at this chunk's points (F = phi*gf + point source)
   auto add_source = [&](double* dst, const double (&src)[M]) {
-    const double* fs = stF + (team * CH + ch) * PADM;
+    const double* fs = stF + team * TSTR + ch * PADM;
     const int ptl = P.pt_line ? P.pt_line[b] : -1;
     const int ptp = P.pt_pos ? P.pt_pos[b] : -1;
 #pragma unroll
@@ -758,8 +759,8 @@ __global__ void __launch_bounds__(32 * T * NTEAM, (Occ<METHOD, NTEAM>::value))
     // neighbour edge values of x (and u in the prologue); the bases' neighbour
     // values are read straight from the staging tile
     double d0, d1, xm1, xp1, um1, up1;
-    const double* tS = stS + team * CH * PADM;
-    const double* tX = stX + team * CH * PADM;
+    const double* tS = stS + team * TSTR;
+    const double* tX = stX + team * TSTR;
     const double SLp = ch > 0 ? tS[(ch - 1) * PADM + M - 1] : 0.0;
     const double SFn = ch + 1 < CH ? tS[(ch + 1) * PADM] : 0.0;
     const double VLp = ch > 0 ? tX[(ch - 1) * PADM + M - 1] : 0.0;
@@ -853,7 +854,7 @@ __global__ void __launch_bounds__(32 * T * NTEAM, (Occ<METHOD, NTEAM>::value))
     const bool own = ln < P.nlines && pos < nact && p >= sg.out_lo && p < sg.out_hi && p >= 0 &&
                      p <= n;
     if (!own) continue;
-    const int si = (tmi * CH + pos / M) * PADM + pos % M;
+    const int si = tmi * TSTR + (pos / M) * PADM + pos % M;
     const double xv = stX[si], uv = stS[si];
     const long long offX = XM ? (long long)ln * P.x_line + p : ln + (long long)p * P.x_pt;
     Xobat[offX] = xv;
@@ -878,7 +879,7 @@ __global__ void __launch_bounds__(32 * T * NTEAM, (Occ<METHOD, NTEAM>::value))
 // shared memory bytes of one CTA
 template <int M, int T, int NTEAM>
 constexpr size_t tile_smem_bytes() {
-  return sizeof(double) * (size_t)(3 * NTEAM * 32 * T * (M + 1) + NTEAM * 10 * 32 * T + NTEAM * 2 * T * 8 + NTEAM);
+  return sizeof(double) * (size_t)(3 * NTEAM * (32 * T * (M + 1) + 2) + NTEAM * 10 * 32 * T + NTEAM * 2 * T * 8 + NTEAM);
 }
 
 }  // namespace adi

@@ -28,7 +28,7 @@ namespace adi {
 constexpr int TM = 16;     // points per thread chunk
 constexpr int TT = 2;      // warps per team (one team per line segment)
 constexpr int XTEAMS = 1;  // lines per CTA in the row sweep (4 CTAs / SM)
-constexpr int YTEAMS = 2;  // lines per CTA in the column sweep (32-byte coalescing)
+constexpr int YTEAMS = 4;  // lines per CTA in the column sweep (32-byte coalescing)
 constexpr int TCH = 32 * TT;  // chunks per line segment
 
 struct Axis {
