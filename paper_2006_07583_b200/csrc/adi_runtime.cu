@@ -21,15 +21,13 @@
 #include <vector>
 
 #include "adi.h"
-#include "adi_kernels.cuh"
+#include "adi_line.cuh"
 
 namespace adi {
 
-constexpr int TM = 16;     // points per thread chunk
-constexpr int TT = 2;      // warps per team (one team per line segment)
-constexpr int XTEAMS = 1;  // lines per CTA in the row sweep (4 CTAs / SM)
-constexpr int YTEAMS = 4;  // lines per CTA in the column sweep (32-byte coalescing)
-constexpr int TCH = 32 * TT;  // chunks per line segment
+constexpr int TM = 32;     // points per thread chunk
+constexpr int NW = 4;      // lines (warps) per CTA: S' is written in 32-byte runs
+constexpr int TCH = 32;    // chunks per line segment (one per lane)
 
 struct Axis {
   int n = 0;            // cells along the sweep direction
@@ -63,8 +61,10 @@ struct adi_ctx {
   // device buffers
   double *U = nullptr, *V = nullptr, *W = nullptr;
   double *V2 = nullptr, *W2 = nullptr, *Sa = nullptr, *Sb = nullptr;
-  double* phi = nullptr;
+  double* phi = nullptr;    // source pattern, S layout (row-major)
+  double* phiT = nullptr;   // its transpose (column sweep)
   double* edges = nullptr;  // y0 | y1 | x0 | x1
+  // internal layouts: Sa, V, V2 row-major; Sb = S^T; W, W2 = W̄^T (columns contiguous)
   int* flag = nullptr;
   adi::Axis ax, ay;
   // time tables (host)
@@ -124,8 +124,6 @@ int init_constants(adi_ctx* h) {
   const double F = G[M - 1], Ks = Kc[0], Ke = Kc[M - 1], Js = Jc[0], Je = Jc[M - 1];
   CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cl, &l, sizeof l));
   CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cinvd, &invd, sizeof invd));
-  CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cK, Kc, sizeof Kc));
-  CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cJ, Jc, sizeof Jc));
   CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cF, &F, sizeof F));
   CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cKs, &Ks, sizeof Ks));
   CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_cKe, &Ke, sizeof Ke));
@@ -280,18 +278,17 @@ struct TimeScope {
   }
 };
 
-template <int METHOD, int MODE, int XM>
+template <int METHOD, int MODE>
 int launch_t(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
-  constexpr int NTEAM = XM ? adi::XTEAMS : adi::YTEAMS;
-  auto kern = adi::adi_tile_kernel<METHOD, adi::TM, adi::TT, NTEAM, XM, MODE>;
-  const size_t smem = adi::tile_smem_bytes<adi::TM, adi::TT, NTEAM>();
+  auto kern = adi::adi_line_kernel<METHOD, adi::TM, adi::NW, MODE>;
+  const size_t smem = adi::line_smem_bytes<METHOD, adi::TM, adi::NW>();
   static bool attr = false;
   if (!attr) {
     CUDA_TRY(h, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  dim3 grid((A.nlines + NTEAM - 1) / NTEAM, (unsigned)A.segs.size(), h->batch);
-  kern<<<grid, 32 * adi::TT * NTEAM, smem, h->stream>>>(p);
+  dim3 grid((A.nlines + adi::NW - 1) / adi::NW, (unsigned)A.segs.size(), h->batch);
+  kern<<<grid, 32 * adi::NW, smem, h->stream>>>(p);
   CUDA_TRY(h, cudaGetLastError());
   h->launches++;
   return ADI_OK;
@@ -299,17 +296,39 @@ int launch_t(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
 
 int launch(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p, int kind) {
   TimeScope ts(h, kind);
-  const bool xm = p.xmajor != 0;
   if (h->method == ADI_CFD) {
-    if (mode == adi::KM_SWEEP)
-      return xm ? launch_t<adi::M_CFD, adi::KM_SWEEP, 1>(h, A, p) : launch_t<adi::M_CFD, adi::KM_SWEEP, 0>(h, A, p);
-    if (mode == adi::KM_FINAL) return launch_t<adi::M_CFD, adi::KM_FINAL, 0>(h, A, p);
-    return launch_t<adi::M_CFD, adi::KM_PROLOGUE, 0>(h, A, p);
+    if (mode == adi::KM_SWEEP) return launch_t<adi::M_CFD, adi::KM_SWEEP>(h, A, p);
+    if (mode == adi::KM_FINAL) return launch_t<adi::M_CFD, adi::KM_FINAL>(h, A, p);
+    return launch_t<adi::M_CFD, adi::KM_PROLOGUE>(h, A, p);
   }
-  if (mode == adi::KM_SWEEP)
-    return xm ? launch_t<adi::M_MFD, adi::KM_SWEEP, 1>(h, A, p) : launch_t<adi::M_MFD, adi::KM_SWEEP, 0>(h, A, p);
-  if (mode == adi::KM_FINAL) return launch_t<adi::M_MFD, adi::KM_FINAL, 0>(h, A, p);
-  return launch_t<adi::M_MFD, adi::KM_PROLOGUE, 0>(h, A, p);
+  if (mode == adi::KM_SWEEP) return launch_t<adi::M_MFD, adi::KM_SWEEP>(h, A, p);
+  if (mode == adi::KM_FINAL) return launch_t<adi::M_MFD, adi::KM_FINAL>(h, A, p);
+  return launch_t<adi::M_MFD, adi::KM_PROLOGUE>(h, A, p);
+}
+
+// batched out[c][r] = in[r][c] for an R x C row-major matrix (32x32 shared tiles)
+__global__ void transpose_kernel(const double* __restrict__ in, double* __restrict__ out, int R, int C,
+                                 long long batch_stride) {
+  __shared__ double tile[32][33];
+  const double* ib = in + blockIdx.z * batch_stride;
+  double* ob = out + blockIdx.z * batch_stride;
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int r = r0 + k, cc = c0 + threadIdx.x;
+    if (r < R && cc < C) tile[k][threadIdx.x] = ib[(long long)r * C + cc];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int cc = c0 + k, r = r0 + threadIdx.x;
+    if (r < R && cc < C) ob[(long long)cc * R + r] = tile[threadIdx.x][k];
+  }
+}
+
+int transpose(adi_ctx* h, const double* in, double* out, int R, int C, int batch, long long bstride) {
+  dim3 grid((C + 31) / 32, (R + 31) / 32, batch);
+  transpose_kernel<<<grid, dim3(32, 8), 0, h->stream>>>(in, out, R, C, bstride);
+  CUDA_TRY(h, cudaGetLastError());
+  return ADI_OK;
 }
 
 // Dirichlet columns (x = 0, x = 1) of U at time factor gb, all rows (corners included)
@@ -338,27 +357,27 @@ adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
   std::memset(&p, 0, sizeof p);
   p.n = A.n;
   p.nlines = A.nlines;
-  p.xmajor = ydir ? 0 : 1;
   p.plo = A.plo;
   p.phi = A.phi;
   p.segs = A.d_segs;
-  if (!ydir) {
-    p.s_line = h->nxi; p.s_pt = 1;
-    p.x_line = h->nxv; p.x_pt = 1;
+  if (!ydir) {  // lines = interior rows; S_in = Sa (row-major), S_out = Sb (= S^T)
+    p.s_line = h->nxi; p.so_line = 1; p.so_pt = h->nyi;
+    p.x_line = h->nxv;
     p.u_line = h->nxu; p.u_pt = 1;
     p.edgeL = h->edges ? h->edges + 2 * h->nxu : nullptr;
     p.edgeR = h->edges ? h->edges + 2 * h->nxu + h->nyu : nullptr;
-  } else {
-    p.s_line = 1; p.s_pt = h->nxi;
-    p.x_line = 1; p.x_pt = h->nxi;
+    p.phi_src = h->phi;
+  } else {      // lines = interior columns; S_in = Sb (= S^T), S_out = Sa; X = W̄^T
+    p.s_line = h->nyi; p.so_line = 1; p.so_pt = h->nxi;
+    p.x_line = h->nyv;
     p.u_line = 1; p.u_pt = h->nxu;
     p.edgeL = h->edges ? h->edges : nullptr;
     p.edgeR = h->edges ? h->edges + h->nxu : nullptr;
+    p.phi_src = h->phiT;
   }
   p.s_batch = (long long)h->nS;
   p.x_batch = (long long)(ydir ? h->nW : h->nV);
   p.u_batch = (long long)h->nU;
-  p.phi_src = h->phi;
   p.pt_line = h->has_pt ? A.d_ptl : nullptr;
   p.pt_pos = h->has_pt ? A.d_ptp : nullptr;
   p.pt_amp = 1.0 / (h->h * h->h);
@@ -379,7 +398,8 @@ void free_ctx(adi_ctx* h) {
   for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
   for (void* q : {(void*)h->U, (void*)h->V, (void*)h->W, (void*)h->V2, (void*)h->W2,
-                  (void*)h->Sa, (void*)h->Sb, (void*)h->phi, (void*)h->edges, (void*)h->flag})
+                  (void*)h->Sa, (void*)h->Sb, (void*)h->phi, (void*)h->phiT, (void*)h->edges,
+                  (void*)h->flag})
     if (q) cudaFree(q);
   for (adi::Axis* A : {&h->ax, &h->ay})
     for (void* q : {(void*)A->d_segs, (void*)A->d_tabU, (void*)A->d_tabX, (void*)A->d_ptl,
@@ -496,7 +516,10 @@ static int set_fields_impl(adi_handle h, const double* U, const double* V, const
   const size_t B = (size_t)h->batch;
   CUDA_TRY(h, cudaMemcpyAsync(h->U, U, B * h->nU * 8, kind, h->stream));
   CUDA_TRY(h, cudaMemcpyAsync(h->V, V, B * h->nV * 8, kind, h->stream));
-  CUDA_TRY(h, cudaMemcpyAsync(h->W, W, B * h->nW * 8, kind, h->stream));
+  // W̄ (ny x nxi, row-major) -> internal W̄^T via the W2 scratch buffer
+  CUDA_TRY(h, cudaMemcpyAsync(h->W2, W, B * h->nW * 8, kind, h->stream));
+  int rc = transpose(h, h->W2, h->W, h->nyv, h->nxi, h->batch, (long long)h->nW);
+  if (rc) return rc;
   if (kind == cudaMemcpyHostToDevice) CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   h->fields_set = true;
   return ADI_OK;
@@ -542,10 +565,16 @@ int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double
   if (ix >= 1 && h->batch != 1) return fail(h, ADI_EINVAL, "use adi_set_point_sources for a batch");
   if (phi) {
     if (!h->phi) CUDA_TRY(h, cudaMalloc(&h->phi, h->nS * 8));
+    if (!h->phiT) CUDA_TRY(h, cudaMalloc(&h->phiT, h->nS * 8));
     CUDA_TRY(h, cudaMemcpy(h->phi, phi, h->nS * 8, cudaMemcpyHostToDevice));
+    int rc = transpose(h, h->phi, h->phiT, h->nyi, h->nxi, 1, 0);
+    if (rc) return rc;
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   } else if (h->phi) {
     cudaFree(h->phi);
+    cudaFree(h->phiT);
     h->phi = nullptr;
+    h->phiT = nullptr;
   }
   h->has_pt = false;
   if (ix >= 1) {
@@ -669,7 +698,10 @@ static int get_fields_impl(adi_handle h, double* U, double* V, double* W, cudaMe
   const size_t B = (size_t)h->batch;
   CUDA_TRY(h, cudaMemcpyAsync(U, h->U, B * h->nU * 8, kind, h->stream));
   CUDA_TRY(h, cudaMemcpyAsync(V, h->V, B * h->nV * 8, kind, h->stream));
-  CUDA_TRY(h, cudaMemcpyAsync(W, h->W, B * h->nW * 8, kind, h->stream));
+  // internal W̄^T -> W̄ via the W2 scratch buffer
+  int rc = transpose(h, h->W, h->W2, h->nxi, h->nyv, h->batch, (long long)h->nW);
+  if (rc) return rc;
+  CUDA_TRY(h, cudaMemcpyAsync(W, h->W2, B * h->nW * 8, kind, h->stream));
   if (kind == cudaMemcpyDeviceToHost) CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   return ADI_OK;
 }
