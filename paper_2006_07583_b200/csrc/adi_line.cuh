@@ -561,9 +561,10 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
       if (P.edgeR) c.gR = P.edgeR[line + 1] * P.gb;
     }
   }
-  // source pattern of this chunk: prefetch into L2 now, read at the epilogue
+  // source pattern of this segment (shared by the batch): prefetched into L2
+  // now, staged into the S tile before the epilogue
   const bool want_phi = (MODE != KM_FINAL) && P.phi_src;
-  const double* phl = want_phi ? P.phi_src + b * 0 + (long long)line * P.s_line - 1 : nullptr;
+  const double* phl = want_phi ? P.phi_src + (long long)line * P.s_line - 1 : nullptr;
   if (want_phi && c.live) {
     const double* a0 = phl + max(c.s, 1);
     asm volatile("prefetch.global.L2 [%0];" ::"l"(a0));
@@ -587,15 +588,33 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
     }
   }
 
-  // dst = src + dt/2 F at this chunk's points (F = phi*gf + point source)
+  // Stage this segment's source pattern into the S tile (coalesced, async).
+  // Only legal once S is dead (after the last u-op that uses it as a base).
+  auto stage_phi = [&]() {
+    if (!want_phi) return;
+    __syncwarp();
+#pragma unroll 8
+    for (int k = 0; k < M; ++k) {
+      const int pos = lane + 32 * k;
+      const int p = sg.start + pos;
+      const bool uin = lineok && pos < nact && p >= 1 && p <= uhi;
+      cp_async8(lS + (pos / M) * PADM + pos % M, uin ? phl + p : P.X_in, uin);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  // dst = src + dt/2 F at this chunk's points (F = phi*gf + point source); with
+  // a dense source, dst must be the S tile holding the staged phi
   auto add_source = [&](double* dst, const double (&src)[M]) {
     const int ptl = P.pt_line ? P.pt_line[b] : -1;
     const int ptp = P.pt_pos ? P.pt_pos[b] : -1;
+    if (want_phi) {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      __syncwarp();
+    }
 #pragma unroll
     for (int i = 0; i < M; ++i) {
       const int p = c.s + i;
-      const bool uin = c.live && p >= 1 && p <= uhi;
-      double f = (want_phi && uin) ? __ldg(phl + p) * P.gf : 0.0;
+      double f = want_phi ? dst[i] * P.gf : 0.0;
       if (c.live && line == ptl && p == ptp) f += P.pt_amp * P.gf;
       dst[i] = fma(P.half_dt, f, src[i]);
     }
@@ -628,12 +647,14 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
       double wv[M];
 #pragma unroll
       for (int i = 0; i < M; ++i) wv[i] = x[i];
+      stage_phi();
       cfd_apply<M, false>(c, P, lane, stXs, u, Vm, x, P.cx, um1, up1, 0.0, 0.0, e1, e2);
       add_source(Sm, u);
       cfd_apply<M, true>(c, P, lane, stU, wv, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
     } else {
       for (int k = 0; k < P.K; ++k) {
         cfd_apply<M, true>(c, P, lane, stU, x, Sm, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
+        if (MODE == KM_SWEEP && k + 1 == P.K) stage_phi();
         cfd_apply<M, false>(c, P, lane, stXs, u, Vm, x, P.cx, um1, up1, VFn, VLp, xm1, xp1);
       }
       if (MODE == KM_SWEEP) {
@@ -666,12 +687,14 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
       double wv[M];
 #pragma unroll
       for (int i = 0; i < M; ++i) wv[i] = x[i];
+      stage_phi();
       x_op(Vm);            // W* = W - beta D(U)
       add_source(Sm, u);   // S = U + dt/2 F
       u_op(wv, Sm);        // S1 = S - alpha D̄(W)
     } else {
       for (int k = 0; k < P.K; ++k) {
         u_op(x, Sm);
+        if (MODE == KM_SWEEP && k + 1 == P.K) stage_phi();
         x_op(Vm);
       }
       if (MODE == KM_SWEEP) {
