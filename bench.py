@@ -254,7 +254,7 @@ def run_ours(a, ws, rank, local):
     roof = {"bound": "hbm", "achieved": round(dominant["achieved"], 1), "peak": peak, "unit": "GB/s",
             "frac": round(dominant["achieved"] / peak, 4),
             "traffic": traffic.get(tkey, {}).get("dram_bytes_per_launch"),
-            "kernel": f"adi_tile_kernel[{dominant['method']},{dominant['kind']}]",
+            "kernel": f"adi_line_kernel[{dominant['method']},{dominant['kind']}]",
             "algorithmic_bytes_per_launch": dominant["bytes"], "peak_source": peak_src,
             "avg_launch_ms": round(dominant["avg_ms"], 4)}
     # ---- end to end through the C-ABI with host buffers (pinned), copies timed

@@ -57,7 +57,14 @@ struct adi_ctx {
   cudaStream_t stream = nullptr;
   // shapes
   int nxu, nyu, nxi, nyi, nxv, nyv;
-  size_t nU, nV, nW, nS;  // per grid
+  size_t nU, nV, nW, nS;  // per grid, dense (user layout)
+  // internal pitched layouts (pitches in doubles, multiples of 4 = 32 bytes):
+  //   U  : nyu rows x pu, stored at Ubase + 3 so that interior columns are aligned
+  //   Sa : nyi rows x pa (row-major S),   Sb : nxi rows x pb (S^T)
+  //   V  : nyi rows x pv,                 W  : nxi rows x pw (W̄^T)
+  int pu, pa, pb, pv, pw;
+  size_t aU, aS, aV, aW;  // allocation per grid (batch strides)
+  double* Ubase = nullptr;
   // device buffers
   double *U = nullptr, *V = nullptr, *W = nullptr;
   double *V2 = nullptr, *W2 = nullptr, *Sa = nullptr, *Sb = nullptr;
@@ -306,37 +313,38 @@ int launch(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p, int 
   return launch_t<adi::M_MFD, adi::KM_PROLOGUE>(h, A, p);
 }
 
-// batched out[c][r] = in[r][c] for an R x C row-major matrix (32x32 shared tiles)
+// batched out[c][r] = in[r][c] for an R x C matrix (row pitches ip, op; 32x32 shared tiles)
 __global__ void transpose_kernel(const double* __restrict__ in, double* __restrict__ out, int R, int C,
-                                 long long batch_stride) {
+                                 long long ip, long long op, long long ibs, long long obs) {
   __shared__ double tile[32][33];
-  const double* ib = in + blockIdx.z * batch_stride;
-  double* ob = out + blockIdx.z * batch_stride;
+  const double* ib = in + blockIdx.z * ibs;
+  double* ob = out + blockIdx.z * obs;
   const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int r = r0 + k, cc = c0 + threadIdx.x;
-    if (r < R && cc < C) tile[k][threadIdx.x] = ib[(long long)r * C + cc];
+    if (r < R && cc < C) tile[k][threadIdx.x] = ib[(long long)r * ip + cc];
   }
   __syncthreads();
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int cc = c0 + k, r = r0 + threadIdx.x;
-    if (r < R && cc < C) ob[(long long)cc * R + r] = tile[threadIdx.x][k];
+    if (r < R && cc < C) ob[(long long)cc * op + r] = tile[threadIdx.x][k];
   }
 }
 
-int transpose(adi_ctx* h, const double* in, double* out, int R, int C, int batch, long long bstride) {
+int transpose(adi_ctx* h, const double* in, double* out, int R, int C, long long ip, long long op,
+              int batch, long long ibs, long long obs) {
   dim3 grid((C + 31) / 32, (R + 31) / 32, batch);
-  transpose_kernel<<<grid, dim3(32, 8), 0, h->stream>>>(in, out, R, C, bstride);
+  transpose_kernel<<<grid, dim3(32, 8), 0, h->stream>>>(in, out, R, C, ip, op, ibs, obs);
   CUDA_TRY(h, cudaGetLastError());
   return ADI_OK;
 }
 
 // Dirichlet columns (x = 0, x = 1) of U at time factor gb, all rows (corners included)
-__global__ void edge_cols_kernel(double* U, int nyu, int nxu, long long ubatch,
+__global__ void edge_cols_kernel(double* U, int nyu, int nxu, int pu, long long ubatch,
                                  const double* ex0, const double* ex1, double gb) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nyu) return;
-  double* Ub = U + blockIdx.y * ubatch + (long long)r * nxu;
+  double* Ub = U + blockIdx.y * ubatch + (long long)r * pu;
   Ub[0] = ex0 ? ex0[r] * gb : 0.0;
   Ub[nxu - 1] = ex1 ? ex1[r] * gb : 0.0;
 }
@@ -361,23 +369,23 @@ adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
   p.phi = A.phi;
   p.segs = A.d_segs;
   if (!ydir) {  // lines = interior rows; S_in = Sa (row-major), S_out = Sb (= S^T)
-    p.s_line = h->nxi; p.so_line = 1; p.so_pt = h->nyi;
-    p.x_line = h->nxv;
-    p.u_line = h->nxu; p.u_pt = 1;
+    p.s_line = h->pa; p.so_line = 1; p.so_pt = h->pb;
+    p.x_line = h->pv;
+    p.u_line = h->pu; p.u_pt = 1;
     p.edgeL = h->edges ? h->edges + 2 * h->nxu : nullptr;
     p.edgeR = h->edges ? h->edges + 2 * h->nxu + h->nyu : nullptr;
     p.phi_src = h->phi;
   } else {      // lines = interior columns; S_in = Sb (= S^T), S_out = Sa; X = W̄^T
-    p.s_line = h->nyi; p.so_line = 1; p.so_pt = h->nxi;
-    p.x_line = h->nyv;
-    p.u_line = 1; p.u_pt = h->nxu;
+    p.s_line = h->pb; p.so_line = 1; p.so_pt = h->pa;
+    p.x_line = h->pw;
+    p.u_line = 1; p.u_pt = h->pu;
     p.edgeL = h->edges ? h->edges : nullptr;
     p.edgeR = h->edges ? h->edges + h->nxu : nullptr;
     p.phi_src = h->phiT;
   }
-  p.s_batch = (long long)h->nS;
-  p.x_batch = (long long)(ydir ? h->nW : h->nV);
-  p.u_batch = (long long)h->nU;
+  p.s_batch = (long long)h->aS;
+  p.x_batch = (long long)(ydir ? h->aW : h->aV);
+  p.u_batch = (long long)h->aU;
   p.pt_line = h->has_pt ? A.d_ptl : nullptr;
   p.pt_pos = h->has_pt ? A.d_ptp : nullptr;
   p.pt_amp = 1.0 / (h->h * h->h);
@@ -397,7 +405,7 @@ adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
 void free_ctx(adi_ctx* h) {
   for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
-  for (void* q : {(void*)h->U, (void*)h->V, (void*)h->W, (void*)h->V2, (void*)h->W2,
+  for (void* q : {(void*)h->Ubase, (void*)h->V, (void*)h->W, (void*)h->V2, (void*)h->W2,
                   (void*)h->Sa, (void*)h->Sb, (void*)h->phi, (void*)h->phiT, (void*)h->edges,
                   (void*)h->flag})
     if (q) cudaFree(q);
@@ -440,6 +448,16 @@ int adi_create_batch(int nx, int ny, double hh, double dt, double c, int method,
   h->nV = (size_t)h->nyi * h->nxv;
   h->nW = (size_t)h->nyv * h->nxi;
   h->nS = (size_t)h->nyi * h->nxi;
+  auto up4 = [](int v) { return (v + 3) / 4 * 4; };
+  h->pu = up4(h->nxu + 3);
+  h->pa = up4(h->nxi);
+  h->pb = up4(h->nyi);
+  h->pv = up4(h->nxv);
+  h->pw = up4(h->nyv);
+  h->aU = (size_t)h->nyu * h->pu + 4;
+  h->aS = std::max((size_t)h->nyi * h->pa, (size_t)h->nxi * h->pb);
+  h->aV = (size_t)h->nyi * h->pv;
+  h->aW = std::max((size_t)h->nxi * h->pw, h->nW);  // W2 also serves as a dense scratch
   int rc = init_constants(h);
   auto bail = [&](int code) {
     free_ctx(h);
@@ -448,16 +466,17 @@ int adi_create_batch(int nx, int ny, double hh, double dt, double c, int method,
   };
   if (rc) return bail(rc);
   const size_t B = (size_t)batch;
-  if (cudaMalloc(&h->U, B * h->nU * 8) || cudaMalloc(&h->V, B * h->nV * 8) ||
-      cudaMalloc(&h->W, B * h->nW * 8) || cudaMalloc(&h->V2, B * h->nV * 8) ||
-      cudaMalloc(&h->W2, B * h->nW * 8) || cudaMalloc(&h->Sa, B * h->nS * 8) ||
-      cudaMalloc(&h->Sb, B * h->nS * 8) || cudaMalloc(&h->flag, sizeof(int))) {
+  if (cudaMalloc(&h->Ubase, B * h->aU * 8) || cudaMalloc(&h->V, B * h->aV * 8) ||
+      cudaMalloc(&h->W, B * h->aW * 8) || cudaMalloc(&h->V2, B * h->aV * 8) ||
+      cudaMalloc(&h->W2, B * h->aW * 8) || cudaMalloc(&h->Sa, B * h->aS * 8) ||
+      cudaMalloc(&h->Sb, B * h->aS * 8) || cudaMalloc(&h->flag, sizeof(int))) {
     cudaGetLastError();
     return bail(ADI_ENOMEM);
   }
-  cudaMemset(h->U, 0, B * h->nU * 8);
-  cudaMemset(h->V, 0, B * h->nV * 8);
-  cudaMemset(h->W, 0, B * h->nW * 8);
+  h->U = h->Ubase + 3;
+  cudaMemset(h->Ubase, 0, B * h->aU * 8);
+  cudaMemset(h->V, 0, B * h->aV * 8);
+  cudaMemset(h->W, 0, B * h->aW * 8);
   cudaMemset(h->flag, 0, sizeof(int));
   if ((rc = setup_axis(h, h->ax, nx - 1, h->nyi, 1))) return bail(rc);
   if ((rc = setup_axis(h, h->ay, ny - 1, h->nxi, 4))) return bail(rc);
@@ -514,11 +533,15 @@ static int set_fields_impl(adi_handle h, const double* U, const double* V, const
   h->err.clear();
   if (!U || !V || !W) return fail(h, ADI_EINVAL, "null field pointer");
   const size_t B = (size_t)h->batch;
-  CUDA_TRY(h, cudaMemcpyAsync(h->U, U, B * h->nU * 8, kind, h->stream));
-  CUDA_TRY(h, cudaMemcpyAsync(h->V, V, B * h->nV * 8, kind, h->stream));
-  // W̄ (ny x nxi, row-major) -> internal W̄^T via the W2 scratch buffer
+  // user layouts are dense; internal rows are pitched (batch strides aU, aV, aW)
+  for (size_t b = 0; b < B; ++b)
+    CUDA_TRY(h, cudaMemcpy2DAsync(h->U + b * h->aU, h->pu * 8, U + b * h->nU, h->nxu * 8, h->nxu * 8,
+                                  h->nyu, kind, h->stream));
+  CUDA_TRY(h, cudaMemcpy2DAsync(h->V, h->pv * 8, V, h->nxv * 8, h->nxv * 8, B * h->nyi, kind, h->stream));
+  // W̄ (ny x nxi, dense) -> internal W̄^T via the W2 scratch buffer
   CUDA_TRY(h, cudaMemcpyAsync(h->W2, W, B * h->nW * 8, kind, h->stream));
-  int rc = transpose(h, h->W2, h->W, h->nyv, h->nxi, h->batch, (long long)h->nW);
+  int rc = transpose(h, h->W2, h->W, h->nyv, h->nxi, h->nxi, h->pw, h->batch, (long long)h->nW,
+                     (long long)h->aW);
   if (rc) return rc;
   if (kind == cudaMemcpyHostToDevice) CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   h->fields_set = true;
@@ -564,10 +587,10 @@ int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double
   if (g && ng < 1) return fail(h, ADI_EINVAL, "empty source table");
   if (ix >= 1 && h->batch != 1) return fail(h, ADI_EINVAL, "use adi_set_point_sources for a batch");
   if (phi) {
-    if (!h->phi) CUDA_TRY(h, cudaMalloc(&h->phi, h->nS * 8));
-    if (!h->phiT) CUDA_TRY(h, cudaMalloc(&h->phiT, h->nS * 8));
-    CUDA_TRY(h, cudaMemcpy(h->phi, phi, h->nS * 8, cudaMemcpyHostToDevice));
-    int rc = transpose(h, h->phi, h->phiT, h->nyi, h->nxi, 1, 0);
+    if (!h->phi) CUDA_TRY(h, cudaMalloc(&h->phi, h->aS * 8));
+    if (!h->phiT) CUDA_TRY(h, cudaMalloc(&h->phiT, h->aS * 8));
+    CUDA_TRY(h, cudaMemcpy2D(h->phi, h->pa * 8, phi, h->nxi * 8, h->nxi * 8, h->nyi, cudaMemcpyHostToDevice));
+    int rc = transpose(h, h->phi, h->phiT, h->nyi, h->nxi, h->pa, h->pb, 1, 0, 0);
     if (rc) return rc;
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   } else if (h->phi) {
@@ -671,7 +694,7 @@ int adi_step(adi_handle h, int nsteps) {
     const double* ex0 = h->edges ? h->edges + 2 * h->nxu : nullptr;
     const double* ex1 = h->edges ? h->edges + 2 * h->nxu + h->nyu : nullptr;
     TimeScope ts(h, ADI_KK_EDGE);
-    edge_cols_kernel<<<g, 256, 0, h->stream>>>(h->U, h->nyu, h->nxu, (long long)h->nU, ex0, ex1,
+    edge_cols_kernel<<<g, 256, 0, h->stream>>>(h->U, h->nyu, h->nxu, h->pu, (long long)h->aU, ex0, ex1,
                                                 tabv(h->gb, 2 * m1));
     CUDA_TRY(h, cudaGetLastError());
     h->launches++;
@@ -696,10 +719,13 @@ static int get_fields_impl(adi_handle h, double* U, double* V, double* W, cudaMe
   h->err.clear();
   if (!U || !V || !W) return fail(h, ADI_EINVAL, "null field pointer");
   const size_t B = (size_t)h->batch;
-  CUDA_TRY(h, cudaMemcpyAsync(U, h->U, B * h->nU * 8, kind, h->stream));
-  CUDA_TRY(h, cudaMemcpyAsync(V, h->V, B * h->nV * 8, kind, h->stream));
+  for (size_t b = 0; b < B; ++b)
+    CUDA_TRY(h, cudaMemcpy2DAsync(U + b * h->nU, h->nxu * 8, h->U + b * h->aU, h->pu * 8, h->nxu * 8,
+                                  h->nyu, kind, h->stream));
+  CUDA_TRY(h, cudaMemcpy2DAsync(V, h->nxv * 8, h->V, h->pv * 8, h->nxv * 8, B * h->nyi, kind, h->stream));
   // internal W̄^T -> W̄ via the W2 scratch buffer
-  int rc = transpose(h, h->W, h->W2, h->nxi, h->nyv, h->batch, (long long)h->nW);
+  int rc = transpose(h, h->W, h->W2, h->nxi, h->nyv, h->pw, h->nxi, h->batch, (long long)h->aW,
+                     (long long)h->nW);
   if (rc) return rc;
   CUDA_TRY(h, cudaMemcpyAsync(W, h->W2, B * h->nW * 8, kind, h->stream));
   if (kind == cudaMemcpyDeviceToHost) CUDA_TRY(h, cudaStreamSynchronize(h->stream));
