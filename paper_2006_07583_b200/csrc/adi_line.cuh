@@ -249,31 +249,40 @@ struct Cfd {
 
 template <int M>
 struct MfdSplit {
-  // u-op: out_i = B_i + cA (x_{i+1} - x_{i-2}) + cB (x_{i-1} - x_i)
-  static __device__ __forceinline__ void u_inner(const double (&x)[M], const double* __restrict__ B,
-                                                 double (&out)[M], double cA, double cB) {
+  // load the op's bases into the (dead) output registers: one burst of 128-bit
+  // shared loads, issued before any arithmetic so their latency overlaps
+  static __device__ __forceinline__ void bases(const double* __restrict__ B, double (&out)[M]) {
+    const double2* B2 = reinterpret_cast<const double2*>(B);
 #pragma unroll
-    for (int i = 2; i <= M - 2; ++i) out[i] = fma(cA, x[i + 1] - x[i - 2], fma(cB, x[i - 1] - x[i], B[i]));
+    for (int i = 0; i < M / 2; ++i) {
+      const double2 v = B2[i];
+      out[2 * i] = v.x;
+      out[2 * i + 1] = v.y;
+    }
   }
-  static __device__ __forceinline__ void u_edges(const double (&x)[M], const double* __restrict__ B,
-                                                 double (&out)[M], double cA, double cB, double xm2,
-                                                 double xm1, double xp1) {
-    out[0] = fma(cA, x[1] - xm2, fma(cB, xm1 - x[0], B[0]));
-    out[1] = fma(cA, x[2] - xm1, fma(cB, x[0] - x[1], B[1]));
-    out[M - 1] = fma(cA, xp1 - x[M - 3], fma(cB, x[M - 2] - x[M - 1], B[M - 1]));
-  }
-  // x-op: out_i = B_i + cC (u_{i+2} - u_{i-1}) + cD (u_i - u_{i+1})
-  static __device__ __forceinline__ void x_inner(const double (&u)[M], const double* __restrict__ B,
-                                                 double (&out)[M], double cC, double cD) {
+  // u-op: out_i = B_i + cA (x_{i+1} - x_{i-2}) + cB (x_{i-1} - x_i), out preloaded with B
+  static __device__ __forceinline__ void u_inner(const double (&x)[M], double (&out)[M], double cA,
+                                                 double cB) {
 #pragma unroll
-    for (int i = 1; i <= M - 3; ++i) out[i] = fma(cC, u[i + 2] - u[i - 1], fma(cD, u[i] - u[i + 1], B[i]));
+    for (int i = 2; i <= M - 2; ++i) out[i] = fma(cA, x[i + 1] - x[i - 2], fma(cB, x[i - 1] - x[i], out[i]));
   }
-  static __device__ __forceinline__ void x_edges(const double (&u)[M], const double* __restrict__ B,
-                                                 double (&out)[M], double cC, double cD, double um1,
-                                                 double up1, double up2) {
-    out[0] = fma(cC, u[2] - um1, fma(cD, u[0] - u[1], B[0]));
-    out[M - 2] = fma(cC, up1 - u[M - 3], fma(cD, u[M - 2] - u[M - 1], B[M - 2]));
-    out[M - 1] = fma(cC, up2 - u[M - 2], fma(cD, u[M - 1] - up1, B[M - 1]));
+  static __device__ __forceinline__ void u_edges(const double (&x)[M], double (&out)[M], double cA,
+                                                 double cB, double xm2, double xm1, double xp1) {
+    out[0] = fma(cA, x[1] - xm2, fma(cB, xm1 - x[0], out[0]));
+    out[1] = fma(cA, x[2] - xm1, fma(cB, x[0] - x[1], out[1]));
+    out[M - 1] = fma(cA, xp1 - x[M - 3], fma(cB, x[M - 2] - x[M - 1], out[M - 1]));
+  }
+  // x-op: out_i = B_i + cC (u_{i+2} - u_{i-1}) + cD (u_i - u_{i+1}), out preloaded with B
+  static __device__ __forceinline__ void x_inner(const double (&u)[M], double (&out)[M], double cC,
+                                                 double cD) {
+#pragma unroll
+    for (int i = 1; i <= M - 3; ++i) out[i] = fma(cC, u[i + 2] - u[i - 1], fma(cD, u[i] - u[i + 1], out[i]));
+  }
+  static __device__ __forceinline__ void x_edges(const double (&u)[M], double (&out)[M], double cC,
+                                                 double cD, double um1, double up1, double up2) {
+    out[0] = fma(cC, u[2] - um1, fma(cD, u[0] - u[1], out[0]));
+    out[M - 2] = fma(cC, up1 - u[M - 3], fma(cD, u[M - 2] - u[M - 1], out[M - 2]));
+    out[M - 1] = fma(cC, up2 - u[M - 2], fma(cD, u[M - 1] - up1, out[M - 1]));
   }
 };
 
@@ -488,7 +497,7 @@ struct Occ {
 // shared memory of one CTA: padded staging of S and X for NW lines (+ CFD statics)
 template <int METHOD, int M, int NW>
 constexpr size_t line_smem_bytes() {
-  return sizeof(double) * (size_t)(2 * NW * (32 * (M + 1) + 2) + (METHOD == M_CFD ? NW * 10 * 32 : 0));
+  return sizeof(double) * (size_t)(2 * NW * (32 * (M + 2) + 4) + (METHOD == M_CFD ? NW * 10 * 32 : 0));
 }
 
 // ===========================================================================
@@ -499,8 +508,8 @@ template <int METHOD, int M, int NW, int MODE>
 __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel(const KParams P) {
   constexpr int NT = 32 * NW;
   constexpr int NPOS = 32 * M;   // positions per segment
-  constexpr int PADM = M + 1;    // padded chunk stride of the staging tile
-  constexpr int LSTR = 32 * PADM + 2;  // line stride of the staging tile
+  constexpr int PADM = M + 2;    // padded chunk stride: 16-byte rows, conflict-free 128-bit loads
+  constexpr int LSTR = 32 * PADM + 4;  // line stride of the staging tile
   extern __shared__ double smem[];
   double* stS = smem;             // [NW][32][PADM]: S (or U in the prologue)
   double* stX = stS + NW * LSTR;  // [NW][32][PADM]: X
@@ -672,15 +681,15 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
     const double cC = bx * (1.0 / 24.0), cD = bx * (9.0 / 8.0);
     double xm2, xm1, xp1, xp2, um2, um1, up1, up2;
     auto u_op = [&](const double (&opd)[M], const double* __restrict__ B) {
-      if (c.interior) MfdSplit<M>::u_inner(opd, B, u, cA, cB);
+      if (c.interior) { MfdSplit<M>::bases(B, u); MfdSplit<M>::u_inner(opd, u, cA, cB); }
       warp_edges<M>(lane, opd, xm2, xm1, xp1, xp2);
-      if (c.interior) MfdSplit<M>::u_edges(opd, B, u, cA, cB, xm2, xm1, xp1);
+      if (c.interior) MfdSplit<M>::u_edges(opd, u, cA, cB, xm2, xm1, xp1);
       else Mfd<M>::template uop<false>(c, opd, B, u, au, xm2, xm1, xp1);
     };
     auto x_op = [&](const double* __restrict__ B) {
-      if (c.interior) MfdSplit<M>::x_inner(u, B, x, cC, cD);
+      if (c.interior) { MfdSplit<M>::bases(B, x); MfdSplit<M>::x_inner(u, x, cC, cD); }
       warp_edges<M>(lane, u, um2, um1, up1, up2);
-      if (c.interior) MfdSplit<M>::x_edges(u, B, x, cC, cD, um1, up1, up2);
+      if (c.interior) MfdSplit<M>::x_edges(u, x, cC, cD, um1, up1, up2);
       else Mfd<M>::template xop<false>(c, u, B, x, bx, um1, up1, up2);
     };
     if (MODE == KM_PROLOGUE) {
