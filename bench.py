@@ -11,10 +11,10 @@ homogeneous Dirichlet), K = 8 sweeps, cfl 0.91 (CFD) / 0.81 (MFD), fp64.  A
 method; `value` is grid-point updates per second summed over the job.
 Each field is 2.1 GB (> 126 MB L2), so no L2 flush is needed between steps.
 
-Under torchrun (N > 1) every rank advances its own independent grid
-(replicas; weak scaling) — the line-sharded single grid is future work
-(DESIGN.md §7).  Timing: CUDA events on the library's stream, barrier +
-synchronize on both sides, max over ranks.
+Under torchrun (N > 1) the same single grid is band-decomposed over the ranks
+(DESIGN.md §7): strong scaling, one NCCL halo exchange per step.  Timing: CUDA
+events on the library's stream (torch's current stream), barrier + synchronize
+on both sides, max over ranks.
 """
 from __future__ import annotations
 
@@ -176,15 +176,17 @@ def kernel_bytes(method, n, kind, has_phi=True):
 
 
 def run_ours(a, ws, rank, local):
+    """N = 1: one grid per method.  N > 1: the same grid band-decomposed over the
+    ranks (NCCL halo exchange through torch.distributed)."""
     import torch
     import paper_2006_07583_b200 as adi
+    from paper_2006_07583_b200 import dist as adist
 
     torch.cuda.set_device(local)
-    stream = torch.cuda.Stream()
+    stream = torch.cuda.current_stream()
     methods = methods_of(a)
     n = a.n
     total_steps = a.warmup + a.steps
-    res = {}
     solvers = {}
     for m in methods:
         p = make_problem(m, n, total_steps + a.steps + 4, a.K)
@@ -192,40 +194,53 @@ def run_ours(a, ws, rank, local):
         s.set_fields(p.U, p.V, p.W)
         s.set_source(p.phi, p.src, p.gf)
         s.set_boundary(p.edges, p.gb)
-        solvers[m] = (s, p)
-    # warm-up
-    for m, (s, p) in solvers.items():
-        s.step(a.warmup)
+        p.phi = None  # copied by the library; keep host memory low (8 ranks per box)
+        p.V = p.W = None  # zeros for the MMS start; recreated for the e2e leg
+        bs = None
+        if ws > 1:
+            y0, y1, halo, npos = adi.adi_band_info(s.handle)
+            bs = adist.BandSolver(s, rank, ws, adist.band_partition(npos, ws, halo))
+        solvers[m] = (s, p, bs)
+    transport = adist.TorchDistTransport(rank, ws) if ws > 1 else None
+
+    def run(m, k):
+        s, p, bs = solvers[m]
+        if bs is None:
+            s.step(k)
+        else:
+            adist.step_distributed(bs, transport, k)
+
+    for m in solvers:
+        run(m, a.warmup)
     torch.cuda.synchronize()
-    for m, (s, p) in solvers.items():
+    for m, (s, p, bs) in solvers.items():
         s.set_param(adi.ADI_TIMING, 1)
         s.kernel_times()  # reset
     # ---- device-timed region: exactly K steps of each method
-    launches0 = sum(s.stats()["kernel_launches"] for s, _ in solvers.values())
+    launches0 = sum(s.stats()["kernel_launches"] for s, _, _ in solvers.values())
     per = {}
     with Clocks(local) as clk:
-        for m, (s, p) in solvers.items():
+        for m in solvers:
             barrier(ws)
             torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            s.step(a.steps)
+            run(m, a.steps)
             e1.record(stream)
             e1.synchronize()
             torch.cuda.synchronize()
             barrier(ws)
-            ms = allmax(ws, e0.elapsed_time(e1))
-            per[m] = ms
-    launches = sum(s.stats()["kernel_launches"] for s, _ in solvers.values()) - launches0
+            per[m] = allmax(ws, e0.elapsed_time(e1))
+    launches = sum(s.stats()["kernel_launches"] for s, _, _ in solvers.values()) - launches0
     clocks = clk.summary()
-    # kernel times (CUDA events around every launch inside the timed region)
-    kt = {m: s.kernel_times() for m, (s, p) in solvers.items()}
-    for m, (s, p) in solvers.items():
+    kt = {m: s.kernel_times() for m, (s, p, bs) in solvers.items()}
+    for m, (s, p, bs) in solvers.items():
         s.set_param(adi.ADI_TIMING, 0)
     pts = n * n
     total_ms = sum(per.values())
-    value = ws * pts * a.steps * len(methods) / (total_ms * 1e-3)
+    scale = 1 if ws == 1 else 1   # strong scaling: one grid in total
+    value = scale * pts * a.steps * len(methods) / (total_ms * 1e-3)
     peak, peak_src = measured_peaks()
     traffic = ncu_traffic()
     per_method = {}
@@ -234,26 +249,25 @@ def run_ours(a, ws, rank, local):
         ksum = {k: v for k, v in kt[m].items() if v[1] > 0}
         step_ms = per[m] / a.steps
         tot = sum(v[0] for v in ksum.values())
-        top = max(ksum.items(), key=lambda kv: kv[1][0])
-        kind, (kms, kcnt) = top
-        byt = kernel_bytes(m, n, kind)
+        kind, (kms, kcnt) = max(ksum.items(), key=lambda kv: kv[1][0])
+        byt = kernel_bytes(m, n, kind) / ws
         ach = byt / (kms / kcnt * 1e-3) / 1e9
-        bytes_step = kernel_bytes(m, n, "row") + kernel_bytes(m, n, "col")
+        bytes_step = (kernel_bytes(m, n, "row") + kernel_bytes(m, n, "col")) / ws
         per_method[MNAME[m]] = {
-            "value": ws * pts * a.steps / (per[m] * 1e-3), "ms_per_step": step_ms,
-            "hbm_gbs_step": bytes_step / (step_ms * 1e-3) / 1e9,
+            "value": pts * a.steps / (per[m] * 1e-3), "ms_per_step": step_ms,
+            "hbm_gbs_step_per_gpu": bytes_step / (step_ms * 1e-3) / 1e9,
             "hbm_frac_step": bytes_step / (step_ms * 1e-3) / 1e9 / peak,
             "kernel_ms_share": {k: round(v[0] / tot, 4) for k, v in ksum.items()},
             "kernel_avg_ms": {k: v[0] / v[1] for k, v in ksum.items()},
             "dominant": kind}
         cand = {"method": MNAME[m], "kind": kind, "achieved": ach, "bytes": byt, "share": kms / tot,
-                "avg_ms": kms / kcnt}
-        if dominant is None or cand["avg_ms"] * kcnt > dominant["avg_ms"] * dominant.get("cnt", 1):
-            dominant = dict(cand, cnt=kcnt)
+                "avg_ms": kms / kcnt, "cnt": kcnt}
+        if dominant is None or cand["avg_ms"] * kcnt > dominant["avg_ms"] * dominant["cnt"]:
+            dominant = cand
     tkey = f"{dominant['method']}_{dominant['kind']}_{n}"
     roof = {"bound": "hbm", "achieved": round(dominant["achieved"], 1), "peak": peak, "unit": "GB/s",
             "frac": round(dominant["achieved"] / peak, 4),
-            "traffic": traffic.get(tkey, {}).get("dram_bytes_per_launch"),
+            "traffic": traffic.get(tkey, {}).get("dram_bytes_per_launch") if ws == 1 else None,
             "kernel": f"adi_line_kernel[{dominant['method']},{dominant['kind']}]",
             "algorithmic_bytes_per_launch": dominant["bytes"], "peak_source": peak_src,
             "avg_launch_ms": round(dominant["avg_ms"], 4)}
@@ -262,16 +276,20 @@ def run_ours(a, ws, rank, local):
     if not a.no_e2e:
         e2e_ms = 0.0
         bi = bo = 0
-        for m, (s, p) in solvers.items():
+        for m, (s, p, bs) in solvers.items():
+            from adi_inputs import shapes
+            su, sv, sw = shapes(m, n, n)
             hU = torch.from_numpy(p.U).pin_memory()
-            hV = torch.from_numpy(p.V).pin_memory()
-            hW = torch.from_numpy(p.W).pin_memory()
+            hV = torch.zeros(sv, dtype=torch.float64).pin_memory()
+            hW = torch.zeros(sw, dtype=torch.float64).pin_memory()
             oU, oV, oW = (torch.empty_like(x).pin_memory() for x in (hU, hV, hW))
             barrier(ws)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             adi.adi_set_fields(s.handle, hU.numpy(), hV.numpy(), hW.numpy())   # H2D, pinned
-            s.step(a.steps)
+            if bs is not None:
+                bs.fresh = True
+            run(m, a.steps)
             adi.adi_get_fields(s.handle, oU.numpy(), oV.numpy(), oW.numpy())   # D2H, synchronizes
             t1 = time.perf_counter()
             barrier(ws)
@@ -280,10 +298,11 @@ def run_ours(a, ws, rank, local):
             bi += nb / a.steps
             bo += nb / a.steps
             del hU, hV, hW, oU, oV, oW
-        e2e = {"value": ws * pts * a.steps * len(methods) / (e2e_ms * 1e-3), "unit": UNIT,
+        e2e = {"value": pts * a.steps * len(methods) / (e2e_ms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo),
-               "note": "adi_set_fields(host) + adi_step(K) + adi_get_fields(host), pinned buffers"}
-    for s, _ in solvers.values():
+               "note": "adi_set_fields(host) + adi_step(K) + adi_get_fields(host), pinned buffers"
+                       + ("" if ws == 1 else "; per rank, full-grid copies, max over ranks")}
+    for s, _, _ in solvers.values():
         s.close()
     return {"value": value, "ms_per_step": total_ms / a.steps, "roofline": roof, "clocks": clocks,
             "e2e": e2e, "gpu_launches": launches, "per_method": per_method}
@@ -320,7 +339,8 @@ def main():
                        f"dense source, {'+'.join(MNAME[m].upper() for m in methods)}",
            "grid_nodes": a.n, "methods": [MNAME[m] for m in methods], "K_sweeps": a.K,
            "cfl": {"cfd": 0.91, "mfd": 0.81}, "l2": "inputs larger than L2 (2.1 GB per field); no flush",
-           "parallelism": "1 GPU" if ws == 1 else f"{ws} independent replica grids (weak)"}
+           "parallelism": "1 GPU" if ws == 1 else
+           f"{ws} GPUs: one grid band-decomposed (rows), NCCL halo exchange per step"}
     if a.impl == "reference":
         # Reference arm = the CPU oracle as it stands, bounded sample per step.
         if rank != 0:
@@ -334,7 +354,7 @@ def main():
         rate, secs = oracle_rate(methods, n, a.steps, a.K, nthr)
         line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": ws,
                 "steps": a.steps, "warmup": a.warmup, "ms_per_step": secs * 1e3 / a.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": cfg,
                 "cpu_baseline": {"value": rate, "unit": UNIT, "cores": nthr, "kind": "oracle",
                                  "sample": f"{n}x{n} nodes, {a.steps} steps per method "
@@ -357,7 +377,7 @@ def main():
                          f"({secs:.1f} s of CPU time)"}
     line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": ws, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
             "roofline": r["roofline"], "cpu_baseline": cpu, "clocks": r["clocks"], "e2e": r["e2e"],
             "gpu_launches": r["gpu_launches"], "per_method": r["per_method"]}
     print(json.dumps(line))

@@ -54,6 +54,8 @@
 #ifndef ADI_H_
 #define ADI_H_
 
+#include <stddef.h>
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -144,6 +146,37 @@ int adi_set_boundary(adi_handle h, const double* edges, const double* g, int ng)
 /* Enqueue n >= 0 time steps on the handle's stream (asynchronous unless
  * ADI_CHECK_FINITE is set). */
 int adi_step(adi_handle h, int n);
+
+/* The phases of adi_step(n), for drivers that must act between the half-steps
+ * (the multi-GPU band decomposition exchanges halos after the row sweep):
+ *   adi_step_begin(h, n)            explicit y-half of the first step (a2)
+ *   n x { adi_step_rows(h);         ADI-rows of the step (a3, a4)
+ *         adi_step_cols(h); }       ADI-columns (a6; + a2 of the next step, or the
+ *                                   final U, W̄ of the call)
+ *   adi_step_end(h)                 Dirichlet columns of U; non-finite check
+ * adi_step(h, n) is exactly this sequence.  All are asynchronous on the stream. */
+int adi_step_begin(adi_handle h, int n);
+int adi_step_rows(adi_handle h);
+int adi_step_cols(adi_handle h);
+int adi_step_end(adi_handle h);
+
+/* Band decomposition of one grid over several handles / GPUs.
+ * adi_set_band restricts this handle to the y positions [y0, y1) of the pressure
+ * grid (0 <= y0 < y1 <= number of y positions): its row sweep processes the
+ * interior rows inside the band, its column sweep outputs only positions in
+ * the band.  Every handle still holds full-size arrays; only its band (plus
+ * halo) is kept current.  Between adi_step_rows and adi_step_cols the halo of
+ * `halo` positions on each side must be refreshed from the neighbour bands
+ * (kind 0: S2 and W*), and before adi_step_begin of every call but the first
+ * after adi_set_fields (kind 1: U and W̄).  side 0 = low-y neighbour, 1 = high.
+ * adi_halo_pack writes this band's edge positions that the neighbour on `side`
+ * needs into a contiguous device buffer of adi_halo_bytes bytes;
+ * adi_halo_unpack stores the neighbour's message into this band's halo. */
+int adi_set_band(adi_handle h, int y0, int y1);
+int adi_band_info(adi_handle h, int* y0, int* y1, int* halo, int* npos);
+int adi_halo_bytes(adi_handle h, int kind, int side, size_t* bytes);
+int adi_halo_pack(adi_handle h, int kind, int side, void* dev_buf);
+int adi_halo_unpack(adi_handle h, int kind, int side, const void* dev_buf);
 
 /* Copy the state to HOST arrays (synchronizes the stream). */
 int adi_get_fields(adi_handle h, double* U, double* V, double* W);

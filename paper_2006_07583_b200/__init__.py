@@ -77,6 +77,15 @@ def lib():
         L.adi_get_fields_device.argtypes = [H, P, P, P]
         L.adi_get_stats.argtypes = [H, ctypes.POINTER(adi_stats)]
         L.adi_get_kernel_times.argtypes = [H, P, P, I]
+        for f in ("adi_step_begin",):
+            getattr(L, f).argtypes = [H, I]
+        for f in ("adi_step_rows", "adi_step_cols", "adi_step_end"):
+            getattr(L, f).argtypes = [H]
+        L.adi_set_band.argtypes = [H, I, I]
+        L.adi_band_info.argtypes = [H, P, P, P, P]
+        L.adi_halo_bytes.argtypes = [H, I, I, ctypes.POINTER(ctypes.c_size_t)]
+        L.adi_halo_pack.argtypes = [H, I, I, P]
+        L.adi_halo_unpack.argtypes = [H, I, I, P]
         L.adi_last_error.argtypes = [H]
         L.adi_last_error.restype = ctypes.c_char_p
         L.adi_destroy.argtypes = [H]
@@ -88,7 +97,9 @@ def lib():
 
 EXPORTS = ["adi_create", "adi_create_batch", "adi_set_param", "adi_set_stream", "adi_set_fields",
            "adi_set_fields_device", "adi_set_source", "adi_set_point_sources", "adi_set_boundary",
-           "adi_step", "adi_get_fields", "adi_get_fields_device", "adi_get_stats", "adi_get_kernel_times",
+           "adi_step", "adi_step_begin", "adi_step_rows", "adi_step_cols", "adi_step_end", "adi_set_band",
+           "adi_band_info", "adi_halo_bytes", "adi_halo_pack", "adi_halo_unpack",
+           "adi_get_fields", "adi_get_fields_device", "adi_get_stats", "adi_get_kernel_times",
            "adi_last_error",
            "adi_destroy", "adi_version"]
 
@@ -163,6 +174,46 @@ def adi_set_boundary(hd, edges=None, g=None):
 
 def adi_step(hd, n):
     return _check(hd, lib().adi_step(hd, int(n)), "adi_step")
+
+
+def adi_step_begin(hd, n):
+    return _check(hd, lib().adi_step_begin(hd, int(n)), "adi_step_begin")
+
+
+def adi_step_rows(hd):
+    return _check(hd, lib().adi_step_rows(hd), "adi_step_rows")
+
+
+def adi_step_cols(hd):
+    return _check(hd, lib().adi_step_cols(hd), "adi_step_cols")
+
+
+def adi_step_end(hd):
+    return _check(hd, lib().adi_step_end(hd), "adi_step_end")
+
+
+def adi_set_band(hd, y0, y1):
+    return _check(hd, lib().adi_set_band(hd, int(y0), int(y1)), "adi_set_band")
+
+
+def adi_band_info(hd):
+    v = [ctypes.c_int() for _ in range(4)]
+    _check(hd, lib().adi_band_info(hd, *[ctypes.byref(x) for x in v]), "adi_band_info")
+    return tuple(x.value for x in v)  # (y0, y1, halo, npos)
+
+
+def adi_halo_bytes(hd, kind, side):
+    n = ctypes.c_size_t()
+    _check(hd, lib().adi_halo_bytes(hd, kind, side, ctypes.byref(n)), "adi_halo_bytes")
+    return n.value
+
+
+def adi_halo_pack(hd, kind, side, dev_buf):
+    return _check(hd, lib().adi_halo_pack(hd, kind, side, _ptr(dev_buf)), "adi_halo_pack")
+
+
+def adi_halo_unpack(hd, kind, side, dev_buf):
+    return _check(hd, lib().adi_halo_unpack(hd, kind, side, _ptr(dev_buf)), "adi_halo_unpack")
 
 
 def adi_get_fields(hd, U, V, W):

@@ -54,7 +54,8 @@ struct Seg {
 //   U_out: b*u_batch  + (l+1)*u_line + p*u_pt   (final)
 struct KParams {
   int n;        // cells along the line; positions 0..n
-  int nlines;   // interior pressure lines
+  int line0;    // first line of this launch (band decomposition; 0 otherwise)
+  int nlines;   // lines [line0, nlines) are processed
   int plo, phi; // chunks entirely inside [plo, phi] use the interior fast path
   const Seg* segs;
   const double* S_in;  double* S_out;
@@ -518,7 +519,7 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
   const int t = threadIdx.x;
   const int w = t >> 5, lane = t & 31;
   const Seg sg = P.segs[blockIdx.y];
-  const int line = blockIdx.x * NW + w;
+  const int line = P.line0 + blockIdx.x * NW + w;
   const long long b = blockIdx.z;
   const int n = P.n;
   const int uhi = (METHOD == M_CFD) ? n - 1 : n;  // u active on [1, uhi]
@@ -739,7 +740,7 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
   for (int k = 0; k < M; ++k) {
     const int e = t + NT * k;
     const int wl = e % NW, pos = e / NW;
-    const int ln = blockIdx.x * NW + wl;
+    const int ln = P.line0 + blockIdx.x * NW + wl;
     const int p = sg.start + pos;
     const bool own = ln < P.nlines && pos < nact && p >= sg.out_lo && p < sg.out_hi && p >= 0 && p <= n;
     if (!own) continue;

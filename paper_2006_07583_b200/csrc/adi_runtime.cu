@@ -31,7 +31,10 @@ constexpr int TCH = 32;    // chunks per line segment (one per lane)
 
 struct Axis {
   int n = 0;            // cells along the sweep direction
-  int nlines = 0;       // interior pressure lines swept
+  int nlines = 0;       // interior pressure lines of the grid
+  int l0 = 0, l1 = 0;   // lines processed by this handle (band decomposition)
+  int o0 = 0, o1 = 1 << 30;  // output positions of this handle (band decomposition)
+  int halo = 0;
   int NL = 1;
   int plo = 0, phi = -1;
   std::vector<Seg> segs;
@@ -82,6 +85,12 @@ struct adi_ctx {
   bool fields_set = false;
   int nonfinite = 0;
   std::string err;
+  // band decomposition (multi-GPU): this handle owns y positions [band_y0, band_y1)
+  int band_y0 = 0, band_y1 = 1 << 30;
+  // state of a call in progress (adi_step_begin .. adi_step_end)
+  bool in_call = false;
+  long long call_m1 = 0;
+  double *Vcur = nullptr, *Valt = nullptr, *Wcur = nullptr, *Walt = nullptr;
 };
 
 namespace {
@@ -199,6 +208,7 @@ bool plan_axis(adi::Axis& A, int method, int nlmin, int cap) {
   const int chmax = cap > 0 ? std::min(cap, adi::TCH) : adi::TCH;
   const int P = A.n + 1;                       // positions 0..n
   const int halo = (method == ADI_CFD) ? 64 : 32;
+  A.halo = halo;
   A.segs.clear();
   const int D = (M - P % M) % M;
   const int nch1 = (P + D) / M;
@@ -231,8 +241,20 @@ bool plan_axis(adi::Axis& A, int method, int nlmin, int cap) {
 int setup_axis(adi_ctx* h, adi::Axis& A, int n, int nlines, int nlmin) {
   A.n = n;
   A.nlines = nlines;
+  if (A.l1 == 0 && A.l0 == 0) A.l1 = nlines;
   if (!plan_axis(A, h->method, nlmin, h->tile_chunks))
     return fail(h, ADI_EINVAL, "tile planning failed (grid too small for the tile cap)");
+  // band decomposition: keep only the segments that output positions in [o0, o1)
+  {
+    std::vector<adi::Seg> keep;
+    for (adi::Seg g : A.segs) {
+      g.out_lo = std::max(g.out_lo, A.o0);
+      g.out_hi = std::min(g.out_hi, A.o1);
+      if (g.out_lo < g.out_hi) keep.push_back(g);
+    }
+    A.segs = keep;
+    if (A.segs.empty()) A.segs.push_back({0, 0, 0, 0});  // nothing to output: an idle tile
+  }
   if (A.d_segs) { cudaFree(A.d_segs); A.d_segs = nullptr; }
   if (A.d_tabU) { cudaFree(A.d_tabU); A.d_tabU = nullptr; }
   if (A.d_tabX) { cudaFree(A.d_tabX); A.d_tabX = nullptr; }
@@ -294,7 +316,9 @@ int launch_t(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
     CUDA_TRY(h, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  dim3 grid((A.nlines + adi::NW - 1) / adi::NW, (unsigned)A.segs.size(), h->batch);
+  const int nl = std::max(A.l1 - A.l0, 0);
+  if (nl == 0) return ADI_OK;
+  dim3 grid((nl + adi::NW - 1) / adi::NW, (unsigned)A.segs.size(), h->batch);
   kern<<<grid, 32 * adi::NW, smem, h->stream>>>(p);
   CUDA_TRY(h, cudaGetLastError());
   h->launches++;
@@ -364,7 +388,8 @@ adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
   adi::KParams p;
   std::memset(&p, 0, sizeof p);
   p.n = A.n;
-  p.nlines = A.nlines;
+  p.line0 = A.l0;
+  p.nlines = A.l1;
   p.plo = A.plo;
   p.phi = A.phi;
   p.segs = A.d_segs;
@@ -634,11 +659,13 @@ int adi_set_boundary(adi_handle h, const double* edges, const double* g, int ng)
   return ADI_OK;
 }
 
-int adi_step(adi_handle h, int nsteps) {
+// ---- one call = begin (prologue), n x {rows, cols}, end.  The phases are public so
+// that a multi-GPU driver can exchange halos between the row and column sweeps.
+int adi_step_begin(adi_handle h, int nsteps) {
   if (!h) return ADI_EINVAL;
   h->err.clear();
-  if (nsteps < 0) return fail(h, ADI_EINVAL, "n < 0");
-  if (nsteps == 0) return ADI_OK;
+  if (h->in_call) return fail(h, ADI_ESTATE, "a call is already in progress");
+  if (nsteps < 1) return fail(h, ADI_EINVAL, "n < 1");
   if (!h->fields_set) return fail(h, ADI_ESTATE, "fields not set");
   const long long m0 = h->m, m1 = h->m + nsteps;
   if (!h->gf.empty() && (long long)h->gf.size() < 2 * m1 + 1)
@@ -655,53 +682,69 @@ int adi_step(adi_handle h, int nsteps) {
     p.gf = tabv(h->gf, 2 * m0);
     if ((rc = launch(h, adi::KM_PROLOGUE, h->ay, p, ADI_KK_PROLOGUE))) return rc;
   }
-  double* Vcur = h->V; double* Valt = h->V2;
-  double* Wcur = h->W2; double* Walt = h->W;
-  for (long long m = m0; m < m1; ++m) {
-    const bool last = (m + 1 == m1);
-    {  // ADI-rows + C / V^{m+1}
-      adi::KParams p = base_params(h, h->ax, false);
-      p.S_in = h->Sa; p.S_out = h->Sb;
-      p.X_in = Vcur; p.X_out = Valt;
-      p.gb = tabv(h->gb, 2 * m + 1);
-      p.gf = tabv(h->gf, 2 * m + 2);
-      if ((rc = launch(h, adi::KM_SWEEP, h->ax, p, ADI_KK_ROW))) return rc;
-      std::swap(Vcur, Valt);
-    }
-    {  // ADI-columns (+ the explicit y-half of step m+1 unless last)
-      adi::KParams p = base_params(h, h->ay, true);
-      p.S_in = h->Sb;
-      p.X_in = Wcur;
-      p.gb = tabv(h->gb, 2 * m + 2);
-      p.gf = tabv(h->gf, 2 * m + 2);
-      if (last) {
-        p.U_out = h->U;
-        p.X_out = h->W;  // Wcur is W2 or W; FINAL writes the canonical W (Wcur != W when last? see below)
-        if (Wcur == h->W) p.X_out = h->W2;
-        if ((rc = launch(h, adi::KM_FINAL, h->ay, p, ADI_KK_FINAL))) return rc;
-        if (Wcur == h->W) std::swap(h->W, h->W2);
-      } else {
-        p.S_out = h->Sa;
-        p.X_out = Walt;
-        if ((rc = launch(h, adi::KM_SWEEP, h->ay, p, ADI_KK_COL))) return rc;
-        std::swap(Wcur, Walt);
-      }
-    }
+  h->Vcur = h->V; h->Valt = h->V2;
+  h->Wcur = h->W2; h->Walt = h->W;
+  h->call_m1 = m1;
+  h->in_call = true;
+  return ADI_OK;
+}
+
+int adi_step_rows(adi_handle h) {
+  if (!h) return ADI_EINVAL;
+  if (!h->in_call || h->m >= h->call_m1) return fail(h, ADI_ESTATE, "no step pending");
+  const long long m = h->m;
+  adi::KParams p = base_params(h, h->ax, false);
+  p.S_in = h->Sa; p.S_out = h->Sb;
+  p.X_in = h->Vcur; p.X_out = h->Valt;
+  p.gb = tabv(h->gb, 2 * m + 1);
+  p.gf = tabv(h->gf, 2 * m + 2);
+  int rc = launch(h, adi::KM_SWEEP, h->ax, p, ADI_KK_ROW);
+  if (rc) return rc;
+  std::swap(h->Vcur, h->Valt);
+  return ADI_OK;
+}
+
+int adi_step_cols(adi_handle h) {
+  if (!h) return ADI_EINVAL;
+  if (!h->in_call || h->m >= h->call_m1) return fail(h, ADI_ESTATE, "no step pending");
+  const long long m = h->m;
+  const bool last = (m + 1 == h->call_m1);
+  adi::KParams p = base_params(h, h->ay, true);
+  p.S_in = h->Sb;
+  p.X_in = h->Wcur;
+  p.gb = tabv(h->gb, 2 * m + 2);
+  p.gf = tabv(h->gf, 2 * m + 2);
+  int rc;
+  if (last) {  // write U^{m+1} and W̄^{m+1} into the canonical buffers
+    p.U_out = h->U;
+    p.X_out = (h->Wcur == h->W) ? h->W2 : h->W;
+    if ((rc = launch(h, adi::KM_FINAL, h->ay, p, ADI_KK_FINAL))) return rc;
+    if (h->Wcur == h->W) std::swap(h->W, h->W2);
+  } else {
+    p.S_out = h->Sa;
+    p.X_out = h->Walt;
+    if ((rc = launch(h, adi::KM_SWEEP, h->ay, p, ADI_KK_COL))) return rc;
+    std::swap(h->Wcur, h->Walt);
   }
-  if (Vcur != h->V) std::swap(h->V, h->V2);
+  h->m = m + 1;
+  return ADI_OK;
+}
+
+int adi_step_end(adi_handle h) {
+  if (!h) return ADI_EINVAL;
+  if (!h->in_call || h->m != h->call_m1) return fail(h, ADI_ESTATE, "steps of the call not finished");
+  if (h->Vcur != h->V) std::swap(h->V, h->V2);
   {  // Dirichlet columns of U^{m1}
     dim3 g((h->nyu + 255) / 256, h->batch);
     const double* ex0 = h->edges ? h->edges + 2 * h->nxu : nullptr;
     const double* ex1 = h->edges ? h->edges + 2 * h->nxu + h->nyu : nullptr;
     TimeScope ts(h, ADI_KK_EDGE);
     edge_cols_kernel<<<g, 256, 0, h->stream>>>(h->U, h->nyu, h->nxu, h->pu, (long long)h->aU, ex0, ex1,
-                                                tabv(h->gb, 2 * m1));
+                                                tabv(h->gb, 2 * h->m));
     CUDA_TRY(h, cudaGetLastError());
     h->launches++;
-    // corner-free rows y = 0, 1 are written by the FINAL column kernel; the two
-    // corner columns are covered above.
   }
-  h->m = m1;
+  h->in_call = false;
   if (h->check_finite) {
     int f = 0;
     CUDA_TRY(h, cudaMemcpyAsync(&f, h->flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
@@ -711,6 +754,147 @@ int adi_step(adi_handle h, int nsteps) {
       return fail(h, ADI_ENONFINITE, "non-finite value in the fields");
     }
   }
+  return ADI_OK;
+}
+
+int adi_step(adi_handle h, int nsteps) {
+  if (!h) return ADI_EINVAL;
+  if (nsteps < 0) return fail(h, ADI_EINVAL, "n < 0");
+  if (nsteps == 0) return ADI_OK;
+  int rc = adi_step_begin(h, nsteps);
+  for (int k = 0; k < nsteps && rc == ADI_OK; ++k) {
+    rc = adi_step_rows(h);
+    if (rc == ADI_OK) rc = adi_step_cols(h);
+  }
+  if (rc != ADI_OK) { h->in_call = false; return rc; }
+  return adi_step_end(h);
+}
+
+// ---- band decomposition --------------------------------------------------
+int adi_set_band(adi_handle h, int y0, int y1) {
+  if (!h) return ADI_EINVAL;
+  h->err.clear();
+  if (h->in_call) return fail(h, ADI_ESTATE, "call in progress");
+  const int ny_pos = h->ay.n + 1;  // y positions 0..n_y
+  if (y0 < 0 || y1 > ny_pos || y0 >= y1) return fail(h, ADI_EINVAL, "band out of range");
+  h->band_y0 = y0;
+  h->band_y1 = y1;
+  // row sweep: interior rows l (U row l+1) with y = l+1 in [y0, y1)
+  h->ax.l0 = std::max(y0 - 1, 0);
+  h->ax.l1 = std::min(y1 - 1, h->nyi);
+  // column sweep: outputs at y positions [y0, y1)
+  h->ay.o0 = y0;
+  h->ay.o1 = y1;
+  int rc = setup_axis(h, h->ay, h->ny - 1, h->nxi, 4);
+  if (rc) return rc;
+  const int hl = h->ay.halo;
+  if ((y0 > 0 && y1 - y0 < hl) || (y1 < ny_pos && y1 - y0 < hl))
+    return fail(h, ADI_EINVAL, "band thinner than the halo");
+  return ADI_OK;
+}
+
+// halo rows [a, b) (y positions) exchanged on one side of the band
+static void halo_range(adi_ctx* h, int side, int own, int* a, int* b) {
+  const int hl = h->ay.halo, npos = h->ay.n + 1;
+  if (side == 0) {  // low side
+    if (own) { *a = h->band_y0; *b = std::min(h->band_y0 + hl, h->band_y1); }
+    else { *a = std::max(h->band_y0 - hl, 0); *b = h->band_y0; }
+  } else {
+    if (own) { *a = std::max(h->band_y1 - hl, h->band_y0); *b = h->band_y1; }
+    else { *a = h->band_y1; *b = std::min(h->band_y1 + hl, npos); }
+  }
+}
+
+// layout of one halo message: kind 0 (after the row sweep): S (S^T layout) then W* (W̄^T);
+// kind 1 (before the prologue): U rows then W̄ (W̄^T layout).  Per grid of the batch.
+static size_t halo_elems(adi_ctx* h, int kind, int rows) {
+  if (kind == 0) return (size_t)h->batch * ((size_t)h->nxi * rows * 2);
+  return (size_t)h->batch * ((size_t)h->nxu * rows + (size_t)h->nxi * rows);
+}
+
+int adi_halo_bytes(adi_handle h, int kind, int side, size_t* bytes) {
+  if (!h || !bytes || kind < 0 || kind > 1 || side < 0 || side > 1) return ADI_EINVAL;
+  int a, b, c, d;
+  halo_range(h, side, 1, &a, &b);
+  halo_range(h, side, 0, &c, &d);
+  *bytes = 8 * halo_elems(h, kind, std::max(b - a, d - c));
+  return ADI_OK;
+}
+
+// copy y positions [a, b) of the halo fields between the internal arrays and a
+// contiguous device buffer (pack: dir = 0, unpack: dir = 1)
+static int halo_copy(adi_ctx* h, int kind, int a, int b, double* buf, int dir) {
+  const int rows = b - a;
+  if (rows <= 0) return ADI_OK;
+  double* q = buf;
+  auto cp = [&](double* arr, size_t pitch, int nr, int col0, size_t bstride) -> int {
+    for (int bb = 0; bb < h->batch; ++bb) {
+      double* base = arr + bb * bstride + col0;
+      cudaError_t e = dir == 0
+          ? cudaMemcpy2DAsync(q, rows * 8, base, pitch * 8, rows * 8, nr, cudaMemcpyDeviceToDevice, h->stream)
+          : cudaMemcpy2DAsync(base, pitch * 8, q, rows * 8, rows * 8, nr, cudaMemcpyDeviceToDevice, h->stream);
+      if (e != cudaSuccess) return fail(h, ADI_ECUDA, std::string("halo copy: ") + cudaGetErrorString(e));
+      q += (size_t)nr * rows;
+    }
+    return ADI_OK;
+  };
+  int rc;
+  if (kind == 0) {
+    // S: internal S^T (rows = interior columns, position y at index y-1); W*: W̄^T (index y)
+    // (a y position outside the u range is never read by the column sweep)
+    const int uhi = (h->method == ADI_CFD) ? h->ay.n - 1 : h->ay.n;
+    const int sa = std::max(a, 1), sb = std::min(std::max(b, 1), uhi + 1);
+    if (sb > sa) {
+      double* qq = q;
+      const int r2 = sb - sa;
+      for (int bb = 0; bb < h->batch; ++bb) {
+        double* base = h->Sb + bb * h->aS + (sa - 1);
+        cudaError_t e = dir == 0
+            ? cudaMemcpy2DAsync(qq, r2 * 8, base, h->pb * 8, r2 * 8, h->nxi, cudaMemcpyDeviceToDevice, h->stream)
+            : cudaMemcpy2DAsync(base, h->pb * 8, qq, r2 * 8, r2 * 8, h->nxi, cudaMemcpyDeviceToDevice, h->stream);
+        if (e != cudaSuccess) return fail(h, ADI_ECUDA, std::string("halo copy: ") + cudaGetErrorString(e));
+        qq += (size_t)h->nxi * rows;
+      }
+    }
+    q += (size_t)h->batch * h->nxi * rows;
+    if ((rc = cp(h->Wcur, h->pw, h->nxi, a, h->aW))) return rc;
+  } else {
+    // U rows a..b-1 (all columns, contiguous per row) and W̄ (W̄^T layout)
+    for (int bb = 0; bb < h->batch; ++bb) {
+      double* base = h->U + bb * h->aU + (size_t)a * h->pu;
+      cudaError_t e = dir == 0
+          ? cudaMemcpy2DAsync(q, h->nxu * 8, base, h->pu * 8, h->nxu * 8, rows, cudaMemcpyDeviceToDevice, h->stream)
+          : cudaMemcpy2DAsync(base, h->pu * 8, q, h->nxu * 8, h->nxu * 8, rows, cudaMemcpyDeviceToDevice, h->stream);
+      if (e != cudaSuccess) return fail(h, ADI_ECUDA, std::string("halo copy: ") + cudaGetErrorString(e));
+      q += (size_t)h->nxu * rows;
+    }
+    if ((rc = cp(h->W, h->pw, h->nxi, a, h->aW))) return rc;
+  }
+  return ADI_OK;
+}
+
+int adi_halo_pack(adi_handle h, int kind, int side, void* dev_buf) {
+  if (!h || !dev_buf || kind < 0 || kind > 1 || side < 0 || side > 1) return ADI_EINVAL;
+  h->err.clear();
+  int a, b;
+  halo_range(h, side, 1, &a, &b);
+  return halo_copy(h, kind, a, b, (double*)dev_buf, 0);
+}
+
+int adi_halo_unpack(adi_handle h, int kind, int side, const void* dev_buf) {
+  if (!h || !dev_buf || kind < 0 || kind > 1 || side < 0 || side > 1) return ADI_EINVAL;
+  h->err.clear();
+  int a, b;
+  halo_range(h, side, 0, &a, &b);
+  return halo_copy(h, kind, a, b, (double*)dev_buf, 1);
+}
+
+int adi_band_info(adi_handle h, int* y0, int* y1, int* halo, int* npos) {
+  if (!h) return ADI_EINVAL;
+  if (y0) *y0 = h->band_y0 > h->ay.n ? 0 : h->band_y0;
+  if (y1) *y1 = std::min(h->band_y1, h->ay.n + 1);
+  if (halo) *halo = h->ay.halo;
+  if (npos) *npos = h->ay.n + 1;
   return ADI_OK;
 }
 
