@@ -45,17 +45,18 @@ struct Seg {
   int out_hi;
 };
 
-// Element (batch b, line l, position p) of each field:
-//   S_in : b*s_batch  + l*s_line  + (p-1)      (lines contiguous)
-//   X_in : b*x_batch  + l*x_line  + p
-//   S_out: b*s_batch  + l*so_line + (p-1)*so_pt (written transposed)
-//   X_out: b*x_batch  + l*x_line  + p
-//   U_in : b*u_batch  + (l+1)*u_line + p*u_pt   (prologue; Dirichlet values too)
-//   U_out: b*u_batch  + (l+1)*u_line + p*u_pt   (final)
+// Lines and positions are grid POSITIONS (the line index is the position in the
+// cross direction; interior lines are 1..).  Element (batch b, line L, position p):
+//   S_in : b*s_batch + L*s_line  + p          (lines contiguous)
+//   X_in : b*x_batch + L*x_line  + p
+//   S_out: b*s_batch + L*so_line + p*so_pt    (written transposed)
+//   X_out: b*x_batch + L*x_line  + p
+//   U_in / U_out: b*u_batch + L*u_line + p*u_pt  (prologue / final)
 struct KParams {
   int n;        // cells along the line; positions 0..n
-  int line0;    // first line of this launch (band decomposition; 0 otherwise)
-  int nlines;   // lines [line0, nlines) are processed
+  int line0;    // line of (blockIdx.x = 0, warp 0); 4-aligned
+  int line_lo;  // lines [line_lo, nlines) are processed
+  int nlines;
   int plo, phi; // chunks entirely inside [plo, phi] use the interior fast path
   const Seg* segs;
   const double* S_in;  double* S_out;
@@ -519,13 +520,13 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
   const int t = threadIdx.x;
   const int w = t >> 5, lane = t & 31;
   const Seg sg = P.segs[blockIdx.y];
-  const int line = P.line0 + blockIdx.x * NW + w;
+  const int line = P.line0 + blockIdx.x * NW + w;   // cross position of this line
   const long long b = blockIdx.z;
   const int n = P.n;
   const int uhi = (METHOD == M_CFD) ? n - 1 : n;  // u active on [1, uhi]
   const int pR = (METHOD == M_CFD) ? n : n + 1;   // position of ū's right Dirichlet value
   const int nact = sg.nchunks * M;
-  const bool lineok = line < P.nlines;
+  const bool lineok = line >= P.line_lo && line < P.nlines;
 
   Ctx<M> c;
   c.t = t; c.line = line; c.chunk = lane; c.n = n;
@@ -542,9 +543,9 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
   double* lS = stS + w * LSTR;
   double* lX = stX + w * LSTR;
   {
-    const double* Sl = P.S_in ? P.S_in + b * P.s_batch + (long long)line * P.s_line - 1 : nullptr;
+    const double* Sl = P.S_in ? P.S_in + b * P.s_batch + (long long)line * P.s_line : nullptr;
     const double* Xl = P.X_in + b * P.x_batch + (long long)line * P.x_line;
-    const double* Ul = P.U_in ? P.U_in + b * P.u_batch + (long long)(line + 1) * P.u_line : nullptr;
+    const double* Ul = P.U_in ? P.U_in + b * P.u_batch + (long long)line * P.u_line : nullptr;
 #pragma unroll 8
     for (int k = 0; k < M; ++k) {
       const int pos = lane + 32 * k;
@@ -563,18 +564,18 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
   c.gL = 0.0; c.gR = 0.0;
   if (lineok) {
     if (MODE == KM_PROLOGUE) {
-      const double* Ub = P.U_in + b * P.u_batch + (long long)(line + 1) * P.u_line;
+      const double* Ub = P.U_in + b * P.u_batch + (long long)line * P.u_line;
       c.gL = Ub[0];
       c.gR = Ub[(long long)pR * P.u_pt];
     } else {
-      if (P.edgeL) c.gL = P.edgeL[line + 1] * P.gb;
-      if (P.edgeR) c.gR = P.edgeR[line + 1] * P.gb;
+      if (P.edgeL) c.gL = P.edgeL[line] * P.gb;
+      if (P.edgeR) c.gR = P.edgeR[line] * P.gb;
     }
   }
   // source pattern of this segment (shared by the batch): prefetched into L2
   // now, staged into the S tile before the epilogue
   const bool want_phi = (MODE != KM_FINAL) && P.phi_src;
-  const double* phl = want_phi ? P.phi_src + (long long)line * P.s_line - 1 : nullptr;
+  const double* phl = want_phi ? P.phi_src + (long long)line * P.s_line : nullptr;
   if (want_phi && c.live) {
     const double* a0 = phl + max(c.s, 1);
     asm volatile("prefetch.global.L2 [%0];" ::"l"(a0));
@@ -742,19 +743,20 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
     const int wl = e % NW, pos = e / NW;
     const int ln = P.line0 + blockIdx.x * NW + wl;
     const int p = sg.start + pos;
-    const bool own = ln < P.nlines && pos < nact && p >= sg.out_lo && p < sg.out_hi && p >= 0 && p <= n;
+    const bool own = ln >= P.line_lo && ln < P.nlines && pos < nact && p >= sg.out_lo &&
+                     p < sg.out_hi && p >= 0 && p <= n;
     if (!own) continue;
     const double v = stS[wl * LSTR + (pos / M) * PADM + pos % M];
     if (MODE == KM_FINAL) {
-      double* Ub = P.U_out + b * P.u_batch + (long long)(ln + 1) * P.u_line;
+      double* Ub = P.U_out + b * P.u_batch + (long long)ln * P.u_line;
       Ub[(long long)p * P.u_pt] = v;  // interior values and the Dirichlet slots
       acc += v;
       if (METHOD == M_MFD && p == n) {
-        const double gR = P.edgeR ? P.edgeR[ln + 1] * P.gb : 0.0;
+        const double gR = P.edgeR ? P.edgeR[ln] * P.gb : 0.0;
         Ub[(long long)(n + 1) * P.u_pt] = gR;
       }
     } else if (p >= 1 && p <= uhi) {
-      P.S_out[b * P.s_batch + (long long)ln * P.so_line + (long long)(p - 1) * P.so_pt] = v;
+      P.S_out[b * P.s_batch + (long long)ln * P.so_line + (long long)p * P.so_pt] = v;
       acc += v;
     }
   }

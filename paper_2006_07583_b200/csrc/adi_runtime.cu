@@ -61,10 +61,13 @@ struct adi_ctx {
   // shapes
   int nxu, nyu, nxi, nyi, nxv, nyv;
   size_t nU, nV, nW, nS;  // per grid, dense (user layout)
-  // internal pitched layouts (pitches in doubles, multiples of 4 = 32 bytes):
-  //   U  : nyu rows x pu, stored at Ubase + 3 so that interior columns are aligned
-  //   Sa : nyi rows x pa (row-major S),   Sb : nxi rows x pb (S^T)
-  //   V  : nyi rows x pv,                 W  : nxi rows x pw (W̄^T)
+  // internal layouts are POSITION-INDEXED full grids: the entry of
+  // (y position, x position) sits at row y, index x (or row x, index y for the
+  // transposed arrays), whatever the field; rows are pitched to multiples of 4
+  // doubles and padded by >= 32 so a 32-point chunk never crosses a row end.
+  //   U  [y][x] pu     Sa [y][x] pa (S)     Sb [x][y] pb (S^T)
+  //   V  [y][x] pv (V̄, rows 1..nyi)        W  [x][y] pw (W̄^T, rows 1..nxi)
+  //   phi [y][x] pa,  phiT [x][y] pb
   int pu, pa, pb, pv, pw;
   size_t aU, aS, aV, aW;  // allocation per grid (batch strides)
   double* Ubase = nullptr;
@@ -210,10 +213,12 @@ bool plan_axis(adi::Axis& A, int method, int nlmin, int cap) {
   const int halo = (method == ADI_CFD) ? 64 : 32;
   A.halo = halo;
   A.segs.clear();
+  // Chunk starts are kept even (16-byte aligned rows for the bulk copies).
   const int D = (M - P % M) % M;
   const int nch1 = (P + D) / M;
   if (nch1 <= chmax) {
-    A.segs.push_back({-(D / 2), nch1, 0, P});
+    const int ds = (D / 2) & ~1;   // dead positions before 0 (even); the rest after n
+    A.segs.push_back({-ds, nch1, 0, P});
     return true;
   }
   const int CH = chmax;
@@ -226,8 +231,16 @@ bool plan_axis(adi::Axis& A, int method, int nlmin, int cap) {
       g.out_lo = lo;
       g.out_hi = hi;
       if (s == 0) { g.start = 0; g.nchunks = (hi + halo + M - 1) / M; }
-      else if (s == S - 1) { g.nchunks = (P - lo + halo + M - 1) / M; g.start = P - g.nchunks * M; }
-      else { g.start = lo - halo; g.nchunks = (hi - lo + 2 * halo + M - 1) / M; }
+      else if (s == S - 1) {
+        // end the last chunk at n (or n+1, one dead position, to keep the start even)
+        g.nchunks = (P - lo + halo + M - 1) / M;
+        g.start = P - g.nchunks * M;
+        if (g.start & 1) g.start += 1;
+        if (g.start > lo - halo) { g.nchunks += 1; g.start -= M; }
+      } else {
+        g.start = (lo - halo) & ~1;
+        g.nchunks = (hi - g.start + halo + M - 1) / M;
+      }
       // only the first tile may contain the line start, only the last the line end
       if ((s > 0 && g.start < 1) || (s < S - 1 && g.start + g.nchunks * M > P - 1)) return false;
       if (g.nchunks > CH) fits = false;
@@ -241,7 +254,7 @@ bool plan_axis(adi::Axis& A, int method, int nlmin, int cap) {
 int setup_axis(adi_ctx* h, adi::Axis& A, int n, int nlines, int nlmin) {
   A.n = n;
   A.nlines = nlines;
-  if (A.l1 == 0 && A.l0 == 0) A.l1 = nlines;
+  if (A.l1 == 0 && A.l0 == 0) { A.l0 = 1; A.l1 = nlines + 1; }  // lines are positions 1..nlines
   if (!plan_axis(A, h->method, nlmin, h->tile_chunks))
     return fail(h, ADI_EINVAL, "tile planning failed (grid too small for the tile cap)");
   // band decomposition: keep only the segments that output positions in [o0, o1)
@@ -316,8 +329,8 @@ int launch_t(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
     CUDA_TRY(h, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  const int nl = std::max(A.l1 - A.l0, 0);
-  if (nl == 0) return ADI_OK;
+  const int nl = std::max(A.l1 - (A.l0 & ~3), 0);
+  if (A.l1 <= A.l0) return ADI_OK;
   dim3 grid((nl + adi::NW - 1) / adi::NW, (unsigned)A.segs.size(), h->batch);
   kern<<<grid, 32 * adi::NW, smem, h->stream>>>(p);
   CUDA_TRY(h, cudaGetLastError());
@@ -388,19 +401,20 @@ adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
   adi::KParams p;
   std::memset(&p, 0, sizeof p);
   p.n = A.n;
-  p.line0 = A.l0;
+  p.line0 = A.l0 & ~3;     // CTA line groups are 4-aligned (32-byte transposed writes)
+  p.line_lo = A.l0;
   p.nlines = A.l1;
   p.plo = A.plo;
   p.phi = A.phi;
   p.segs = A.d_segs;
-  if (!ydir) {  // lines = interior rows; S_in = Sa (row-major), S_out = Sb (= S^T)
+  if (!ydir) {  // lines = interior rows y; S_in = Sa, S_out = Sb (= S^T)
     p.s_line = h->pa; p.so_line = 1; p.so_pt = h->pb;
     p.x_line = h->pv;
     p.u_line = h->pu; p.u_pt = 1;
     p.edgeL = h->edges ? h->edges + 2 * h->nxu : nullptr;
     p.edgeR = h->edges ? h->edges + 2 * h->nxu + h->nyu : nullptr;
     p.phi_src = h->phi;
-  } else {      // lines = interior columns; S_in = Sb (= S^T), S_out = Sa; X = W̄^T
+  } else {      // lines = interior columns x; S_in = Sb, S_out = Sa; X = W̄^T
     p.s_line = h->pb; p.so_line = 1; p.so_pt = h->pa;
     p.x_line = h->pw;
     p.u_line = 1; p.u_pt = h->pu;
@@ -473,16 +487,16 @@ int adi_create_batch(int nx, int ny, double hh, double dt, double c, int method,
   h->nV = (size_t)h->nyi * h->nxv;
   h->nW = (size_t)h->nyv * h->nxi;
   h->nS = (size_t)h->nyi * h->nxi;
-  auto up4 = [](int v) { return (v + 3) / 4 * 4; };
-  h->pu = up4(h->nxu + 3);
-  h->pa = up4(h->nxi);
-  h->pb = up4(h->nyi);
-  h->pv = up4(h->nxv);
-  h->pw = up4(h->nyv);
-  h->aU = (size_t)h->nyu * h->pu + 4;
-  h->aS = std::max((size_t)h->nyi * h->pa, (size_t)h->nxi * h->pb);
-  h->aV = (size_t)h->nyi * h->pv;
-  h->aW = std::max((size_t)h->nxi * h->pw, h->nW);  // W2 also serves as a dense scratch
+  auto padp = [](int npos) { return (npos + 34 + 3) / 4 * 4; };
+  h->pu = padp(h->nxu);
+  h->pa = padp(h->nxu);
+  h->pb = padp(h->nyu);
+  h->pv = padp(h->nxu);
+  h->pw = padp(h->nyu);
+  h->aU = (size_t)h->nyu * h->pu;
+  h->aS = std::max((size_t)h->nyu * h->pa, (size_t)h->nxu * h->pb);
+  h->aV = (size_t)h->nyu * h->pv;
+  h->aW = std::max((size_t)h->nxu * h->pw, h->nW);  // W2 also serves as a dense scratch
   int rc = init_constants(h);
   auto bail = [&](int code) {
     free_ctx(h);
@@ -498,10 +512,10 @@ int adi_create_batch(int nx, int ny, double hh, double dt, double c, int method,
     cudaGetLastError();
     return bail(ADI_ENOMEM);
   }
-  h->U = h->Ubase + 3;
-  cudaMemset(h->Ubase, 0, B * h->aU * 8);
-  cudaMemset(h->V, 0, B * h->aV * 8);
-  cudaMemset(h->W, 0, B * h->aW * 8);
+  h->U = h->Ubase;
+  for (double* q : {h->Ubase, h->V, h->V2, h->W, h->W2, h->Sa, h->Sb})
+    cudaMemset(q, 0, B * (q == h->Ubase ? h->aU : (q == h->V || q == h->V2) ? h->aV
+                        : (q == h->W || q == h->W2) ? h->aW : h->aS) * 8);
   cudaMemset(h->flag, 0, sizeof(int));
   if ((rc = setup_axis(h, h->ax, nx - 1, h->nyi, 1))) return bail(rc);
   if ((rc = setup_axis(h, h->ay, ny - 1, h->nxi, 4))) return bail(rc);
@@ -559,13 +573,16 @@ static int set_fields_impl(adi_handle h, const double* U, const double* V, const
   if (!U || !V || !W) return fail(h, ADI_EINVAL, "null field pointer");
   const size_t B = (size_t)h->batch;
   // user layouts are dense; internal rows are pitched (batch strides aU, aV, aW)
-  for (size_t b = 0; b < B; ++b)
+  for (size_t b = 0; b < B; ++b) {
     CUDA_TRY(h, cudaMemcpy2DAsync(h->U + b * h->aU, h->pu * 8, U + b * h->nU, h->nxu * 8, h->nxu * 8,
                                   h->nyu, kind, h->stream));
-  CUDA_TRY(h, cudaMemcpy2DAsync(h->V, h->pv * 8, V, h->nxv * 8, h->nxv * 8, B * h->nyi, kind, h->stream));
-  // W̄ (ny x nxi, dense) -> internal W̄^T via the W2 scratch buffer
+    // V̄ row j is the y position j + 1
+    CUDA_TRY(h, cudaMemcpy2DAsync(h->V + b * h->aV + h->pv, h->pv * 8, V + b * h->nV, h->nxv * 8,
+                                  h->nxv * 8, h->nyi, kind, h->stream));
+  }
+  // W̄ (ny x nxi, dense) -> internal W̄^T (row = x position i + 1) via the W2 scratch buffer
   CUDA_TRY(h, cudaMemcpyAsync(h->W2, W, B * h->nW * 8, kind, h->stream));
-  int rc = transpose(h, h->W2, h->W, h->nyv, h->nxi, h->nxi, h->pw, h->batch, (long long)h->nW,
+  int rc = transpose(h, h->W2, h->W + h->pw, h->nyv, h->nxi, h->nxi, h->pw, h->batch, (long long)h->nW,
                      (long long)h->aW);
   if (rc) return rc;
   if (kind == cudaMemcpyHostToDevice) CUDA_TRY(h, cudaStreamSynchronize(h->stream));
@@ -589,8 +606,8 @@ static int set_points(adi_handle h, const int* ix, const int* iy) {
   for (int b = 0; b < B; ++b) {
     if (ix[b] < 1 || ix[b] > uhx || iy[b] < 1 || iy[b] > uhy)
       return fail(h, ADI_EINVAL, "point source outside the pressure interior");
-    xl[b] = iy[b] - 1; xp[b] = ix[b];
-    yl[b] = ix[b] - 1; yp[b] = iy[b];
+    xl[b] = iy[b]; xp[b] = ix[b];   // row sweep: line = y position, pos = x position
+    yl[b] = ix[b]; yp[b] = iy[b];
   }
   for (adi::Axis* A : {&h->ax, &h->ay}) {
     if (!A->d_ptl) {
@@ -614,8 +631,12 @@ int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double
   if (phi) {
     if (!h->phi) CUDA_TRY(h, cudaMalloc(&h->phi, h->aS * 8));
     if (!h->phiT) CUDA_TRY(h, cudaMalloc(&h->phiT, h->aS * 8));
-    CUDA_TRY(h, cudaMemcpy2D(h->phi, h->pa * 8, phi, h->nxi * 8, h->nxi * 8, h->nyi, cudaMemcpyHostToDevice));
-    int rc = transpose(h, h->phi, h->phiT, h->nyi, h->nxi, h->pa, h->pb, 1, 0, 0);
+    CUDA_TRY(h, cudaMemset(h->phi, 0, h->aS * 8));
+    CUDA_TRY(h, cudaMemset(h->phiT, 0, h->aS * 8));
+    // interior point (j, i) of the user's block is position (y, x) = (j + 1, i + 1)
+    CUDA_TRY(h, cudaMemcpy2D(h->phi + h->pa + 1, h->pa * 8, phi, h->nxi * 8, h->nxi * 8, h->nyi,
+                             cudaMemcpyHostToDevice));
+    int rc = transpose(h, h->phi + h->pa + 1, h->phiT + h->pb + 1, h->nyi, h->nxi, h->pa, h->pb, 1, 0, 0);
     if (rc) return rc;
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   } else if (h->phi) {
@@ -779,9 +800,9 @@ int adi_set_band(adi_handle h, int y0, int y1) {
   if (y0 < 0 || y1 > ny_pos || y0 >= y1) return fail(h, ADI_EINVAL, "band out of range");
   h->band_y0 = y0;
   h->band_y1 = y1;
-  // row sweep: interior rows l (U row l+1) with y = l+1 in [y0, y1)
-  h->ax.l0 = std::max(y0 - 1, 0);
-  h->ax.l1 = std::min(y1 - 1, h->nyi);
+  // row sweep: interior rows (lines = y positions 1..nyi) inside [y0, y1)
+  h->ax.l0 = std::max(y0, 1);
+  h->ax.l1 = std::min(y1, h->nyi + 1);
   // column sweep: outputs at y positions [y0, y1)
   h->ay.o0 = y0;
   h->ay.o1 = y1;
@@ -840,24 +861,9 @@ static int halo_copy(adi_ctx* h, int kind, int a, int b, double* buf, int dir) {
   };
   int rc;
   if (kind == 0) {
-    // S: internal S^T (rows = interior columns, position y at index y-1); W*: W̄^T (index y)
-    // (a y position outside the u range is never read by the column sweep)
-    const int uhi = (h->method == ADI_CFD) ? h->ay.n - 1 : h->ay.n;
-    const int sa = std::max(a, 1), sb = std::min(std::max(b, 1), uhi + 1);
-    if (sb > sa) {
-      double* qq = q;
-      const int r2 = sb - sa;
-      for (int bb = 0; bb < h->batch; ++bb) {
-        double* base = h->Sb + bb * h->aS + (sa - 1);
-        cudaError_t e = dir == 0
-            ? cudaMemcpy2DAsync(qq, r2 * 8, base, h->pb * 8, r2 * 8, h->nxi, cudaMemcpyDeviceToDevice, h->stream)
-            : cudaMemcpy2DAsync(base, h->pb * 8, qq, r2 * 8, r2 * 8, h->nxi, cudaMemcpyDeviceToDevice, h->stream);
-        if (e != cudaSuccess) return fail(h, ADI_ECUDA, std::string("halo copy: ") + cudaGetErrorString(e));
-        qq += (size_t)h->nxi * rows;
-      }
-    }
-    q += (size_t)h->batch * h->nxi * rows;
-    if ((rc = cp(h->Wcur, h->pw, h->nxi, a, h->aW))) return rc;
+    // S (S^T layout, row = x position, index = y) and W* (W̄^T, same indexing), rows 1..nxi
+    if ((rc = cp(h->Sb + h->pb, h->pb, h->nxi, a, h->aS))) return rc;
+    if ((rc = cp(h->Wcur + h->pw, h->pw, h->nxi, a, h->aW))) return rc;
   } else {
     // U rows a..b-1 (all columns, contiguous per row) and W̄ (W̄^T layout)
     for (int bb = 0; bb < h->batch; ++bb) {
@@ -868,7 +874,7 @@ static int halo_copy(adi_ctx* h, int kind, int a, int b, double* buf, int dir) {
       if (e != cudaSuccess) return fail(h, ADI_ECUDA, std::string("halo copy: ") + cudaGetErrorString(e));
       q += (size_t)h->nxu * rows;
     }
-    if ((rc = cp(h->W, h->pw, h->nxi, a, h->aW))) return rc;
+    if ((rc = cp(h->W + h->pw, h->pw, h->nxi, a, h->aW))) return rc;
   }
   return ADI_OK;
 }
@@ -903,12 +909,14 @@ static int get_fields_impl(adi_handle h, double* U, double* V, double* W, cudaMe
   h->err.clear();
   if (!U || !V || !W) return fail(h, ADI_EINVAL, "null field pointer");
   const size_t B = (size_t)h->batch;
-  for (size_t b = 0; b < B; ++b)
+  for (size_t b = 0; b < B; ++b) {
     CUDA_TRY(h, cudaMemcpy2DAsync(U + b * h->nU, h->nxu * 8, h->U + b * h->aU, h->pu * 8, h->nxu * 8,
                                   h->nyu, kind, h->stream));
-  CUDA_TRY(h, cudaMemcpy2DAsync(V, h->nxv * 8, h->V, h->pv * 8, h->nxv * 8, B * h->nyi, kind, h->stream));
+    CUDA_TRY(h, cudaMemcpy2DAsync(V + b * h->nV, h->nxv * 8, h->V + b * h->aV + h->pv, h->pv * 8,
+                                  h->nxv * 8, h->nyi, kind, h->stream));
+  }
   // internal W̄^T -> W̄ via the W2 scratch buffer
-  int rc = transpose(h, h->W, h->W2, h->nxi, h->nyv, h->pw, h->nxi, h->batch, (long long)h->aW,
+  int rc = transpose(h, h->W + h->pw, h->W2, h->nxi, h->nyv, h->pw, h->nxi, h->batch, (long long)h->aW,
                      (long long)h->nW);
   if (rc) return rc;
   CUDA_TRY(h, cudaMemcpyAsync(W, h->W2, B * h->nW * 8, kind, h->stream));
