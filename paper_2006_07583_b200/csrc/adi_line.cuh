@@ -293,6 +293,46 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
   const int sz = valid ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(sz) : "memory");
 }
+// TMA bulk copies (cp.async.bulk) with per-warp mbarrier completion
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  unsigned ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// global -> shared, `bytes` (multiple of 16, 16-byte aligned ends), completes on mbarrier
+__device__ __forceinline__ void bulk_g2s(double* dst, const double* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// shared -> global (bulk group)
+__device__ __forceinline__ void bulk_s2g(double* dst, const double* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void fence_async_shared() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ double shup(double v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
 __device__ __forceinline__ double shdn(double v, int d) { return __shfl_down_sync(0xffffffffu, v, d); }
 
@@ -499,7 +539,7 @@ struct Occ {
 // shared memory of one CTA: padded staging of S and X for NW lines (+ CFD statics)
 template <int METHOD, int M, int NW>
 constexpr size_t line_smem_bytes() {
-  return sizeof(double) * (size_t)(2 * NW * (32 * (M + 2) + 4) + (METHOD == M_CFD ? NW * 10 * 32 : 0));
+  return sizeof(double) * (size_t)(2 * NW * (32 * (M + 2) + 4) + (METHOD == M_CFD ? NW * 10 * 32 : 0) + NW);
 }
 
 // ===========================================================================
@@ -516,6 +556,8 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
   double* stS = smem;             // [NW][32][PADM]: S (or U in the prologue)
   double* stX = stS + NW * LSTR;  // [NW][32][PADM]: X
   double* stc = stX + NW * LSTR;  // CFD statics [NW][2 sys][5][32]
+  unsigned long long* wbars =
+      (unsigned long long*)(stc + (METHOD == M_CFD ? NW * 10 * 32 : 0));  // [NW] per-warp mbarriers
 
   const int t = threadIdx.x;
   const int w = t >> 5, lane = t & 31;
@@ -539,24 +581,54 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
   c.nbint = c.live && inner && lane >= 2 && lane + 2 < sg.nchunks && c.s - 2 * M >= P.plo &&
             c.s + 3 * M - 1 <= P.phi;
 
-  // ---- load this warp's line segment (coalesced: lanes take consecutive positions)
+  // ---- load this warp's line segment into the staging tile.  A chunk that starts
+  // at a position >= 0 arrives by one TMA bulk copy per lane and array (256 B,
+  // rows are padded so it never crosses a row end), completed on the warp's
+  // mbarrier; a chunk starting before position 0 (dead positions of a single-tile
+  // line) and the strided prologue read of U use 8-byte cp.async with zero fill.
   double* lS = stS + w * LSTR;
   double* lX = stX + w * LSTR;
+  unsigned long long* wbar = wbars + w;
+  unsigned wpar = 0;  // parity of the warp mbarrier's next phase
+  const bool live_chunk = lineok && lane < sg.nchunks;
+  const bool bulk = live_chunk && c.s >= 0;
   {
     const double* Sl = P.S_in ? P.S_in + b * P.s_batch + (long long)line * P.s_line : nullptr;
     const double* Xl = P.X_in + b * P.x_batch + (long long)line * P.x_line;
     const double* Ul = P.U_in ? P.U_in + b * P.u_batch + (long long)line * P.u_line : nullptr;
-#pragma unroll 8
-    for (int k = 0; k < M; ++k) {
-      const int pos = lane + 32 * k;
-      const int p = sg.start + pos;
-      const bool lv = lineok && pos < nact;
-      const bool uin = lv && p >= 1 && p <= uhi;
-      const bool xin = lv && p >= 0 && p <= n;
-      const int si = (pos / M) * PADM + pos % M;
-      if (MODE == KM_PROLOGUE) cp_async8(lS + si, xin ? Ul + (long long)p * P.u_pt : P.X_in, xin);
-      else cp_async8(lS + si, uin ? Sl + p : P.X_in, uin);
-      cp_async8(lX + si, xin ? Xl + p : P.X_in, xin);
+    const unsigned nb = __popc(__ballot_sync(0xffffffffu, bulk));
+    if (lane == 0) {
+      mbar_init(wbar, 1);
+      mbar_expect_tx(wbar, nb * M * 8 * (MODE == KM_PROLOGUE ? 1 : 2));
+    }
+    __syncwarp();
+    if (bulk) {
+      bulk_g2s(lX + lane * PADM, Xl + c.s, M * 8, wbar);
+      if (MODE != KM_PROLOGUE) bulk_g2s(lS + lane * PADM, Sl + c.s, M * 8, wbar);
+    }
+    if (!live_chunk) {
+      // dead chunk: zero its slots (neighbours read their edges; stale shared
+      // memory could hold NaN, which no halo absorbs)
+      double2* zs = reinterpret_cast<double2*>(lS + lane * PADM);
+      double2* zx = reinterpret_cast<double2*>(lX + lane * PADM);
+#pragma unroll
+      for (int i = 0; i < PADM / 2; ++i) {
+        zs[i] = make_double2(0.0, 0.0);
+        zx[i] = make_double2(0.0, 0.0);
+      }
+    }
+    if (live_chunk && (!bulk || MODE == KM_PROLOGUE)) {
+#pragma unroll 4
+      for (int i = 0; i < M; ++i) {
+        const int p = c.s + i;
+        const bool xin = p >= 0 && p <= n;
+        const bool uin = p >= 1 && p <= uhi;
+        if (!bulk) {
+          cp_async8(lX + lane * PADM + i, xin ? Xl + p : P.X_in, xin);
+          if (MODE != KM_PROLOGUE) cp_async8(lS + lane * PADM + i, uin ? Sl + p : P.X_in, uin);
+        }
+        if (MODE == KM_PROLOGUE) cp_async8(lS + lane * PADM + i, xin ? Ul + (long long)p * P.u_pt : P.X_in, xin);
+      }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   }
@@ -582,6 +654,8 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
     asm volatile("prefetch.global.L2 [%0];" ::"l"(a0 + 16));
   }
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  mbar_wait(wbar, wpar);
+  wpar ^= 1u;
   __syncwarp();
 
   double* Sm = lS + lane * PADM;  // this chunk's bases in shared memory
@@ -590,9 +664,9 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
 #pragma unroll
   for (int i = 0; i < M; ++i) {
     const int p = c.s + i;
-    x[i] = Vm[i];
+    x[i] = c.live ? Vm[i] : 0.0;
     if (MODE == KM_PROLOGUE) {
-      u[i] = Sm[i];
+      u[i] = c.live ? Sm[i] : 0.0;
     } else {
       u[i] = (p == 0) ? c.gL : ((METHOD == M_CFD && p == n) ? c.gR : 0.0);
       if (!c.live) u[i] = 0.0;
@@ -604,12 +678,18 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
   auto stage_phi = [&]() {
     if (!want_phi) return;
     __syncwarp();
-#pragma unroll 8
-    for (int k = 0; k < M; ++k) {
-      const int pos = lane + 32 * k;
-      const int p = sg.start + pos;
-      const bool uin = lineok && pos < nact && p >= 1 && p <= uhi;
-      cp_async8(lS + (pos / M) * PADM + pos % M, uin ? phl + p : P.X_in, uin);
+    fence_async_shared();   // generic-proxy reads of the S tile before the TMA overwrite
+    const unsigned nb = __popc(__ballot_sync(0xffffffffu, bulk));
+    if (lane == 0) mbar_expect_tx(wbar, nb * M * 8);
+    __syncwarp();
+    if (bulk) bulk_g2s(lS + lane * PADM, phl + c.s, M * 8, wbar);
+    if (live_chunk && !bulk) {
+#pragma unroll 4
+      for (int i = 0; i < M; ++i) {
+        const int p = c.s + i;
+        const bool uin = p >= 1 && p <= uhi;
+        cp_async8(lS + lane * PADM + i, uin ? phl + p : P.X_in, uin);
+      }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
@@ -620,6 +700,8 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
     const int ptp = P.pt_pos ? P.pt_pos[b] : -1;
     if (want_phi) {
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      mbar_wait(wbar, wpar);
+      wpar ^= 1u;
       __syncwarp();
     }
 #pragma unroll
@@ -717,49 +799,60 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
     }
   }
 
-  // ---- stage the outputs in the tile (own chunk), then store the owned range
-#pragma unroll
-  for (int i = 0; i < M; ++i) { Sm[i] = u[i]; Vm[i] = x[i]; }
-  __syncthreads();
+  // ---- stage the outputs in the tile (own chunk), then store the owned range.
   double acc = 0.0;
-  // X: this warp's own line, contiguous
-  if (lineok) {
-    double* Xo = P.X_out + b * P.x_batch + (long long)line * P.x_line;
-#pragma unroll 8
-    for (int k = 0; k < M; ++k) {
-      const int pos = lane + 32 * k;
-      const int p = sg.start + pos;
-      if (pos < nact && p >= sg.out_lo && p < sg.out_hi && p >= 0 && p <= n) {
-        const double v = lX[(pos / M) * PADM + pos % M];
-        Xo[p] = v;
-        acc += v;
-      }
+#pragma unroll
+  for (int i = 0; i < M; ++i) {
+    Sm[i] = u[i];
+    Vm[i] = x[i];
+    if (c.live) acc += u[i] + x[i];
+  }
+  // X: this warp's own line, contiguous.  Chunks entirely inside the owned range
+  // leave by one TMA bulk store each; partial chunks element by element.
+  const bool xown_all = live_chunk && c.s >= sg.out_lo && c.s + M <= sg.out_hi && c.s >= 0 &&
+                        c.s + M - 1 <= n;
+  double* Xo = P.X_out + b * P.x_batch + (long long)line * P.x_line;
+  fence_async_shared();
+  __syncwarp();
+  if (xown_all) bulk_s2g(Xo + c.s, Vm, M * 8);
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  if (live_chunk && !xown_all) {
+#pragma unroll 4
+    for (int i = 0; i < M; ++i) {
+      const int p = c.s + i;
+      if (p >= sg.out_lo && p < sg.out_hi && p >= 0 && p <= n) Xo[p] = Vm[i];
     }
   }
-  // S (or U): transposed — consecutive threads take consecutive lines of one position
+  __syncthreads();
+  // S (or U): transposed — a thread stores one position of a pair of lines (16 B)
 #pragma unroll 4
-  for (int k = 0; k < M; ++k) {
+  for (int k = 0; k < (NW / 2) * M; ++k) {
     const int e = t + NT * k;
-    const int wl = e % NW, pos = e / NW;
-    const int ln = P.line0 + blockIdx.x * NW + wl;
+    const int pr = e % (NW / 2), pos = e / (NW / 2);
+    const int l0 = 2 * pr;
+    const int ln = P.line0 + blockIdx.x * NW + l0;
     const int p = sg.start + pos;
-    const bool own = ln >= P.line_lo && ln < P.nlines && pos < nact && p >= sg.out_lo &&
-                     p < sg.out_hi && p >= 0 && p <= n;
-    if (!own) continue;
-    const double v = stS[wl * LSTR + (pos / M) * PADM + pos % M];
+    if (pos >= nact || p < sg.out_lo || p >= sg.out_hi || p < 0 || p > n) continue;
+    const bool ok0 = ln >= P.line_lo && ln < P.nlines;
+    const bool ok1 = ln + 1 >= P.line_lo && ln + 1 < P.nlines;
+    const int si = (pos / M) * PADM + pos % M;
+    const double v0 = stS[l0 * LSTR + si], v1 = stS[(l0 + 1) * LSTR + si];
     if (MODE == KM_FINAL) {
-      double* Ub = P.U_out + b * P.u_batch + (long long)ln * P.u_line;
-      Ub[(long long)p * P.u_pt] = v;  // interior values and the Dirichlet slots
-      acc += v;
+      double* Ub = P.U_out + b * P.u_batch + (long long)p * P.u_pt + (long long)ln * P.u_line;
+      if (ok0 && ok1) *reinterpret_cast<double2*>(Ub) = make_double2(v0, v1);
+      else { if (ok0) Ub[0] = v0; if (ok1) Ub[P.u_line] = v1; }
       if (METHOD == M_MFD && p == n) {
-        const double gR = P.edgeR ? P.edgeR[ln] * P.gb : 0.0;
-        Ub[(long long)(n + 1) * P.u_pt] = gR;
+        double* Ut = P.U_out + b * P.u_batch + (long long)(n + 1) * P.u_pt + (long long)ln * P.u_line;
+        if (ok0) Ut[0] = P.edgeR ? P.edgeR[ln] * P.gb : 0.0;
+        if (ok1) Ut[P.u_line] = P.edgeR ? P.edgeR[ln + 1] * P.gb : 0.0;
       }
     } else if (p >= 1 && p <= uhi) {
-      P.S_out[b * P.s_batch + (long long)ln * P.so_line + (long long)p * P.so_pt] = v;
-      acc += v;
+      double* So = P.S_out + b * P.s_batch + (long long)p * P.so_pt + (long long)ln * P.so_line;
+      if (ok0 && ok1) *reinterpret_cast<double2*>(So) = make_double2(v0, v1);
+      else { if (ok0) So[0] = v0; if (ok1) So[P.so_line] = v1; }
     }
   }
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   if (P.flag && !isfinite(acc)) atomicOr(P.flag, 1);
 }
 
