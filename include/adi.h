@@ -191,6 +191,14 @@ int adi_get_stats(adi_handle h, adi_stats* s);
  * may be NULL. */
 int adi_get_kernel_times(adi_handle h, double* ms, long long* launches, int nkinds);
 
+/* Profiling aid.  While dev_buf != NULL, every launch of the line kernel of the given
+ * kind (ADI_KK_*) records, for each tile id < cap, 8 unsigned 64-bit words at
+ * dev_buf[8 * tile]: {tile, SM id, t_start, t_loaded, t_ops_done, t_end, 0, 0}, times
+ * from the %globaltimer register (ns).  A later launch of that kind overwrites the
+ * records.  dev_buf is device memory owned by the caller and must hold 64 * cap bytes;
+ * NULL turns tracing off.  EINVAL for cap < 0 or an unknown kind. */
+int adi_set_trace(adi_handle h, void* dev_buf, long long cap, int kind);
+
 /* Message for the last error on this handle ("" if none); valid until the next call. */
 const char* adi_last_error(adi_handle h);
 

@@ -77,6 +77,7 @@ def lib():
         L.adi_get_fields_device.argtypes = [H, P, P, P]
         L.adi_get_stats.argtypes = [H, ctypes.POINTER(adi_stats)]
         L.adi_get_kernel_times.argtypes = [H, P, P, I]
+        L.adi_set_trace.argtypes = [H, P, ctypes.c_longlong, I]
         for f in ("adi_step_begin",):
             getattr(L, f).argtypes = [H, I]
         for f in ("adi_step_rows", "adi_step_cols", "adi_step_end"):
@@ -100,7 +101,7 @@ EXPORTS = ["adi_create", "adi_create_batch", "adi_set_param", "adi_set_stream", 
            "adi_step", "adi_step_begin", "adi_step_rows", "adi_step_cols", "adi_step_end", "adi_set_band",
            "adi_band_info", "adi_halo_bytes", "adi_halo_pack", "adi_halo_unpack",
            "adi_get_fields", "adi_get_fields_device", "adi_get_stats", "adi_get_kernel_times",
-           "adi_last_error",
+           "adi_set_trace", "adi_last_error",
            "adi_destroy", "adi_version"]
 
 
@@ -229,6 +230,12 @@ def adi_get_stats(hd):
     s = adi_stats()
     _check(hd, lib().adi_get_stats(hd, ctypes.byref(s)), "adi_get_stats")
     return {k: getattr(s, k) for k, _ in adi_stats._fields_}
+
+
+def adi_set_trace(hd, buf, cap: int, kind: int):
+    """Tile trace of one kernel kind into a device tensor of >= 8 * cap int64 (None: off)."""
+    _check(hd, lib().adi_set_trace(hd, _ptr(buf) if buf is not None else None, int(cap), int(kind)),
+           "adi_set_trace")
 
 
 def adi_get_kernel_times(hd):

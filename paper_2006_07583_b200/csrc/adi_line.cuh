@@ -30,6 +30,7 @@
 // (y_last, z_first, z_last), carry fix-up) and, inside a
 // chunk, across NSUB interleaved sub-chunks for instruction-level parallelism.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -43,7 +44,18 @@ struct Seg {
   int nchunks;  // active chunks per line in this tile
   int out_lo;   // positions [out_lo, out_hi) are written by this tile
   int out_hi;
+  int edge;     // 0: all 32 chunks are interior (plo <= p <= phi): the lean tile path
 };
+
+// Staging tiles arrive by TMA tensor copies of an OVERLAPPING-ROW view of a
+// pitched line array: d0 = 34 doubles, d1 = pair offset
+// (16 B), d2 = 32-position chunk (256 B), d3 = line, d4 = batch.  One box
+// {34, 1, 32, 1, 1} is a line segment in the padded [chunk][34] layout the
+// lanes read conflict-free.  Coordinates are taken relative to position
+// -TMA_P0 so that segment starts before position 0 stay non-negative.
+constexpr int TMA_P0 = 32;
+constexpr int BUF_GUARD_FRONT = 64;   // doubles before / after every staged array
+constexpr int BUF_GUARD_TAIL = 192;
 
 // Lines and positions are grid POSITIONS (the line index is the position in the
 // cross direction; interior lines are 1..).  Element (batch b, line L, position p):
@@ -53,6 +65,9 @@ struct Seg {
 //   X_out: b*x_batch + L*x_line  + p
 //   U_in / U_out: b*u_batch + L*u_line + p*u_pt  (prologue / final)
 struct KParams {
+  CUtensorMap tmS;   // S_in (or nothing in the prologue)
+  CUtensorMap tmX;   // X_in
+  CUtensorMap tmF;   // phi_src (batch extent 1)
   int n;        // cells along the line; positions 0..n
   int line0;    // line of (blockIdx.x = 0, warp 0); 4-aligned
   int line_lo;  // lines [line_lo, nlines) are processed
@@ -73,12 +88,23 @@ struct KParams {
   const int* pt_line; const int* pt_pos; double pt_amp;
   double cu;        // u-op scale: alpha/h (MFD) or 3 alpha/h (CFD)
   double cx;        // x-op scale: beta/h  (MFD) or 3 beta/h  (CFD)
+  double mA, mB, mC, mD;  // MFD interior stencil: cu/24, 9cu/8, cx/24, 9cx/8
   double half_dt;
   int K;
   // CFD per-position LU tables, 3 x (n+1): l, 1/d, c   (u-op: P̄, x-op: P)
   const double* tabU; const double* tabX;
-  int* flag;        // set to 1 if a non-finite value is stored
+  int* flag;        // if set: becomes 1 when a non-finite value is stored
+  // profiling aid (adi_set_trace): per tile, warp 0 records
+  // {tile, smid, t_start, t_loaded, t_ops_done, t_end} (%globaltimer ns)
+  unsigned long long* trace;
+  long long trace_cap;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 constexpr int MMAX = 64;
 // MFD closures (App. B), interior (1/24, -9/8, 9/8, -1/24)
@@ -393,7 +419,7 @@ constexpr int NSUB = 4;
 // previous chunk's last and the next chunk's first position (the operand
 // neighbours of the next op).  st: statics of this warp's chunks [5][32].
 // ===========================================================================
-template <int M, bool UOP>
+template <int M, bool UOP, bool EDGE>
 __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int lane,
                                           const double* st, const double (&o)[M],
                                           const double* __restrict__ B, double (&out)[M],
@@ -465,7 +491,13 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
   wsp1 = lane == 31 ? 0.0 : wsp1;
   wsp2 = lane >= 30 ? 0.0 : wsp2;
   double Fm1, Fme, Ksp1, Jsp1, Ksp2, Kem1, Jem1;
-  if (c.nbint) {
+  if (!EDGE) {
+    // interior tile: every chunk of the segment has the interior statics; the
+    // segment ends carry nothing (truncated SPIKE)
+    Fm1 = lane >= 1 ? c_cF : 0.0; Fme = c_cF;
+    Ksp1 = lane <= 30 ? c_cKs : 0.0; Jsp1 = lane <= 30 ? c_cJs : 0.0; Ksp2 = lane <= 29 ? c_cKs : 0.0;
+    Kem1 = lane >= 1 ? c_cKe : 0.0; Jem1 = lane >= 1 ? c_cJe : 0.0;
+  } else if (c.nbint) {
     Fm1 = Fme = c_cF; Ksp1 = Ksp2 = c_cKs; Jsp1 = c_cJs; Kem1 = c_cKe; Jem1 = c_cJe;
   } else {
     auto at = [&](int k, int cc) { return (cc >= 0 && cc < 32) ? st[k * 32 + cc] : 0.0; };
@@ -536,107 +568,105 @@ struct Occ {
   static constexpr int value = (METHOD == M_MFD) ? 3 : 2;
 };
 
+__host__ __device__ constexpr int PADM_OF(int M) { return M + 2; }
+// line stride of the staging tile: 32 padded chunks, rounded to 128 B (TMA destination)
+__host__ __device__ constexpr int LSTR_OF(int M) { return (32 * (M + 2) + 15) / 16 * 16; }
+
 // shared memory of one CTA: padded staging of S and X for NW lines (+ CFD statics)
 template <int METHOD, int M, int NW>
 constexpr size_t line_smem_bytes() {
-  return sizeof(double) * (size_t)(2 * NW * (32 * (M + 2) + 4) + (METHOD == M_CFD ? NW * 10 * 32 : 0) + NW);
+  return sizeof(double) * (size_t)(2 * NW * LSTR_OF(M) + (METHOD == M_CFD ? NW * 10 * 32 : 0) + NW) + 128;
+}
+
+// TMA tensor copy of one line segment (box {34,1,32,1,1}) into the staging tile
+__device__ __forceinline__ void tma_load_seg(double* dst, const CUtensorMap* tm, int c1, int c2, int line,
+                                             int b, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"((unsigned long long)tm), "r"(0), "r"(c1), "r"(c2), "r"(line), "r"(b), "r"(smem_u32(bar))
+      : "memory");
 }
 
 // ===========================================================================
-// The line kernel.  CTA = NW warps = NW consecutive lines x one segment of
-// 32*M positions.
+// One tile = NW lines x one segment.  EDGE = false: all 32 chunks of every line
+// are interior and live (the lean path, no generic closures, no per-chunk
+// predicates); EDGE = true: line ends, dead chunks, short lines.
 // ===========================================================================
-template <int METHOD, int M, int NW, int MODE>
-__global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel(const KParams P) {
+template <int METHOD, int M, int NW, int MODE, bool EDGE>
+__device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, double* smem) {
   constexpr int NT = 32 * NW;
-  constexpr int NPOS = 32 * M;   // positions per segment
-  constexpr int PADM = M + 2;    // padded chunk stride: 16-byte rows, conflict-free 128-bit loads
-  constexpr int LSTR = 32 * PADM + 4;  // line stride of the staging tile
-  extern __shared__ double smem[];
-  double* stS = smem;             // [NW][32][PADM]: S (or U in the prologue)
-  double* stX = stS + NW * LSTR;  // [NW][32][PADM]: X
-  double* stc = stX + NW * LSTR;  // CFD statics [NW][2 sys][5][32]
+  constexpr int PADM = PADM_OF(M);
+  constexpr int LSTR = LSTR_OF(M);
+  constexpr unsigned BOX_BYTES = 32u * PADM * 8u;
+  static_assert(M == 32, "the TMA box assumes 32-point chunks");
+  static_assert(NW == 4, "the transposed store pairs the 4 lines of a CTA by half-warps");
+  double* stS = smem;             // [NW][LSTR]: S (or U in the prologue), later phi, then S'
+  double* stX = stS + NW * LSTR;  // [NW][LSTR]: X, then X'
+  double* stc = stX + NW * LSTR;  // CFD statics [NW][2 sys][5][32] (edge tiles)
   unsigned long long* wbars =
       (unsigned long long*)(stc + (METHOD == M_CFD ? NW * 10 * 32 : 0));  // [NW] per-warp mbarriers
 
   const int t = threadIdx.x;
   const int w = t >> 5, lane = t & 31;
-  const Seg sg = P.segs[blockIdx.y];
   const int line = P.line0 + blockIdx.x * NW + w;   // cross position of this line
-  const long long b = blockIdx.z;
+  const int b = blockIdx.z;
   const int n = P.n;
   const int uhi = (METHOD == M_CFD) ? n - 1 : n;  // u active on [1, uhi]
   const int pR = (METHOD == M_CFD) ? n : n + 1;   // position of ū's right Dirichlet value
-  const int nact = sg.nchunks * M;
   const bool lineok = line >= P.line_lo && line < P.nlines;
+  const bool tr = P.trace && t == 0;
+  const long long tile = (long long)blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * b);
+  unsigned long long tr0 = tr ? gtimer() : 0ull, tr1 = 0ull, tr2 = 0ull;
 
   Ctx<M> c;
   c.t = t; c.line = line; c.chunk = lane; c.n = n;
   c.s = sg.start + lane * M;
-  c.live = lineok && (lane < sg.nchunks);
-  // dead chunks also run the branch-free interior path: their values only reach
-  // the tile halo, which absorbs any bounded garbage
-  const bool inner = c.s >= P.plo && c.s + M - 1 <= P.phi;
-  c.interior = !c.live || inner;
-  c.nbint = c.live && inner && lane >= 2 && lane + 2 < sg.nchunks && c.s - 2 * M >= P.plo &&
-            c.s + 3 * M - 1 <= P.phi;
+  if (EDGE) {
+    c.live = lineok && (lane < sg.nchunks);
+    // dead chunks also run the branch-free interior path: their values only reach
+    // the tile halo, which absorbs any bounded garbage
+    const bool inner = c.s >= P.plo && c.s + M - 1 <= P.phi;
+    c.interior = !c.live || inner;
+    c.nbint = c.live && inner && lane >= 2 && lane + 2 < sg.nchunks && c.s - 2 * M >= P.plo &&
+              c.s + 3 * M - 1 <= P.phi;
+  } else {
+    c.live = true;      // lines beyond the range compute on finite data; nothing is stored
+    c.interior = true;
+    c.nbint = true;
+  }
 
-  // ---- load this warp's line segment into the staging tile.  A chunk that starts
-  // at a position >= 0 arrives by one TMA bulk copy per lane and array (256 B,
-  // rows are padded so it never crosses a row end), completed on the warp's
-  // mbarrier; a chunk starting before position 0 (dead positions of a single-tile
-  // line) and the strided prologue read of U use 8-byte cp.async with zero fill.
+  // ---- load: one TMA tensor copy per array and warp (zero fill outside the array)
   double* lS = stS + w * LSTR;
   double* lX = stX + w * LSTR;
   unsigned long long* wbar = wbars + w;
   unsigned wpar = 0;  // parity of the warp mbarrier's next phase
-  const bool live_chunk = lineok && lane < sg.nchunks;
-  const bool bulk = live_chunk && c.s >= 0;
-  {
-    const double* Sl = P.S_in ? P.S_in + b * P.s_batch + (long long)line * P.s_line : nullptr;
-    const double* Xl = P.X_in + b * P.x_batch + (long long)line * P.x_line;
-    const double* Ul = P.U_in ? P.U_in + b * P.u_batch + (long long)line * P.u_line : nullptr;
-    const unsigned nb = __popc(__ballot_sync(0xffffffffu, bulk));
-    if (lane == 0) {
-      mbar_init(wbar, 1);
-      mbar_expect_tx(wbar, nb * M * 8 * (MODE == KM_PROLOGUE ? 1 : 2));
-    }
-    __syncwarp();
-    if (bulk) {
-      bulk_g2s(lX + lane * PADM, Xl + c.s, M * 8, wbar);
-      if (MODE != KM_PROLOGUE) bulk_g2s(lS + lane * PADM, Sl + c.s, M * 8, wbar);
-    }
-    if (!live_chunk) {
-      // dead chunk: zero its slots (neighbours read their edges; stale shared
-      // memory could hold NaN, which no halo absorbs)
-      double2* zs = reinterpret_cast<double2*>(lS + lane * PADM);
-      double2* zx = reinterpret_cast<double2*>(lX + lane * PADM);
-#pragma unroll
-      for (int i = 0; i < PADM / 2; ++i) {
-        zs[i] = make_double2(0.0, 0.0);
-        zx[i] = make_double2(0.0, 0.0);
-      }
-    }
-    if (live_chunk && (!bulk || MODE == KM_PROLOGUE)) {
+  const int sh = sg.start + TMA_P0;
+  const int c1 = (sh & 31) >> 1, c2 = sh >> 5;
+  if (lane == 0) {
+    mbar_init(wbar, 1);
+    mbar_expect_tx(wbar, BOX_BYTES * (MODE == KM_PROLOGUE ? 1u : 2u));
+    tma_load_seg(lX, &P.tmX, c1, c2, line, b, wbar);
+    if (MODE != KM_PROLOGUE) tma_load_seg(lS, &P.tmS, c1, c2, line, b, wbar);
+  }
+  __syncwarp();  // the barrier is initialised before any lane waits on it
+  if (MODE == KM_PROLOGUE) {
+    // U is read across its rows (stride u_pt): 8-byte cp.async with zero fill
+    const double* Ul = P.U_in + (long long)b * P.u_batch + (long long)line * P.u_line;
+    const bool lv = lineok && lane < sg.nchunks;
 #pragma unroll 4
-      for (int i = 0; i < M; ++i) {
-        const int p = c.s + i;
-        const bool xin = p >= 0 && p <= n;
-        const bool uin = p >= 1 && p <= uhi;
-        if (!bulk) {
-          cp_async8(lX + lane * PADM + i, xin ? Xl + p : P.X_in, xin);
-          if (MODE != KM_PROLOGUE) cp_async8(lS + lane * PADM + i, uin ? Sl + p : P.X_in, uin);
-        }
-        if (MODE == KM_PROLOGUE) cp_async8(lS + lane * PADM + i, xin ? Ul + (long long)p * P.u_pt : P.X_in, xin);
-      }
+    for (int i = 0; i < M; ++i) {
+      const int p = c.s + i;
+      const bool xin = lv && p >= 0 && p <= n;
+      cp_async8(lS + lane * PADM + i, xin ? Ul + (long long)p * P.u_pt : P.X_in, xin);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   }
-  // Dirichlet values of this line
+  // Dirichlet values of this line (edge tiles only use them)
   c.gL = 0.0; c.gR = 0.0;
-  if (lineok) {
+  if (EDGE && lineok) {
     if (MODE == KM_PROLOGUE) {
-      const double* Ub = P.U_in + b * P.u_batch + (long long)line * P.u_line;
+      const double* Ub = P.U_in + (long long)b * P.u_batch + (long long)line * P.u_line;
       c.gL = Ub[0];
       c.gR = Ub[(long long)pR * P.u_pt];
     } else {
@@ -644,71 +674,64 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
       if (P.edgeR) c.gR = P.edgeR[line] * P.gb;
     }
   }
-  // source pattern of this segment (shared by the batch): prefetched into L2
-  // now, staged into the S tile before the epilogue
   const bool want_phi = (MODE != KM_FINAL) && P.phi_src;
-  const double* phl = want_phi ? P.phi_src + (long long)line * P.s_line : nullptr;
-  if (want_phi && c.live) {
-    const double* a0 = phl + max(c.s, 1);
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(a0));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(a0 + 16));
-  }
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  if (MODE == KM_PROLOGUE) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   mbar_wait(wbar, wpar);
   wpar ^= 1u;
   __syncwarp();
+  if (tr) tr1 = gtimer();
 
   double* Sm = lS + lane * PADM;  // this chunk's bases in shared memory
   double* Vm = lX + lane * PADM;
   double u[M], x[M];
+  {
+    const double2* V2 = reinterpret_cast<const double2*>(Vm);
+    const double2* S2 = reinterpret_cast<const double2*>(Sm);
 #pragma unroll
-  for (int i = 0; i < M; ++i) {
-    const int p = c.s + i;
-    x[i] = c.live ? Vm[i] : 0.0;
-    if (MODE == KM_PROLOGUE) {
-      u[i] = c.live ? Sm[i] : 0.0;
-    } else {
-      u[i] = (p == 0) ? c.gL : ((METHOD == M_CFD && p == n) ? c.gR : 0.0);
-      if (!c.live) u[i] = 0.0;
+    for (int i = 0; i < M / 2; ++i) {
+      const double2 v = V2[i];
+      x[2 * i] = v.x;
+      x[2 * i + 1] = v.y;
+      if (MODE == KM_PROLOGUE) {
+        const double2 q = S2[i];
+        u[2 * i] = q.x;
+        u[2 * i + 1] = q.y;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      const int p = c.s + i;
+      if (EDGE && !c.live) { x[i] = 0.0; u[i] = 0.0; continue; }
+      if (MODE != KM_PROLOGUE) u[i] = (EDGE && p == 0) ? c.gL : ((EDGE && METHOD == M_CFD && p == n) ? c.gR : 0.0);
     }
   }
 
-  // Stage this segment's source pattern into the S tile (coalesced, async).
-  // Only legal once S is dead (after the last u-op that uses it as a base).
+  // Stage this segment's source pattern into the S tile (TMA).  Only legal once
+  // S is dead (after the last u-op that uses it as a base).
   auto stage_phi = [&]() {
     if (!want_phi) return;
+    fence_async_shared();   // generic-proxy reads of the S tile before the async overwrite
     __syncwarp();
-    fence_async_shared();   // generic-proxy reads of the S tile before the TMA overwrite
-    const unsigned nb = __popc(__ballot_sync(0xffffffffu, bulk));
-    if (lane == 0) mbar_expect_tx(wbar, nb * M * 8);
-    __syncwarp();
-    if (bulk) bulk_g2s(lS + lane * PADM, phl + c.s, M * 8, wbar);
-    if (live_chunk && !bulk) {
-#pragma unroll 4
-      for (int i = 0; i < M; ++i) {
-        const int p = c.s + i;
-        const bool uin = p >= 1 && p <= uhi;
-        cp_async8(lS + lane * PADM + i, uin ? phl + p : P.X_in, uin);
-      }
+    if (lane == 0) {
+      mbar_expect_tx(wbar, BOX_BYTES);
+      tma_load_seg(lS, &P.tmF, c1, c2, line, 0, wbar);
     }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
   // dst = src + dt/2 F at this chunk's points (F = phi*gf + point source); with
-  // a dense source, dst must be the S tile holding the staged phi
+  // a dense source, dst is the S tile holding the staged phi
   auto add_source = [&](double* dst, const double (&src)[M]) {
-    const int ptl = P.pt_line ? P.pt_line[b] : -1;
-    const int ptp = P.pt_pos ? P.pt_pos[b] : -1;
+    int ipt = -1;
+    if (P.pt_line && line == P.pt_line[b] && (!EDGE || c.live)) ipt = P.pt_pos[b] - c.s;
+    const double ptf = P.pt_amp * P.gf;
     if (want_phi) {
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
       mbar_wait(wbar, wpar);
       wpar ^= 1u;
       __syncwarp();
     }
 #pragma unroll
     for (int i = 0; i < M; ++i) {
-      const int p = c.s + i;
       double f = want_phi ? dst[i] * P.gf : 0.0;
-      if (c.live && line == ptl && p == ptp) f += P.pt_amp * P.gf;
+      if (i == ipt) f += ptf;
       dst[i] = fma(P.half_dt, f, src[i]);
     }
   };
@@ -718,7 +741,7 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
     const int np1 = n + 1;
     double* stU = stc + (w * 2 + 0) * 5 * 32;
     double* stXs = stc + (w * 2 + 1) * 5 * 32;
-    {
+    if (EDGE) {
       double q[5];
       cfd_statics<M>(c, P.tabU, np1, q);
 #pragma unroll
@@ -741,19 +764,19 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
 #pragma unroll
       for (int i = 0; i < M; ++i) wv[i] = x[i];
       stage_phi();
-      cfd_apply<M, false>(c, P, lane, stXs, u, Vm, x, P.cx, um1, up1, 0.0, 0.0, e1, e2);
+      cfd_apply<M, false, EDGE>(c, P, lane, stXs, u, Vm, x, P.cx, um1, up1, 0.0, 0.0, e1, e2);
       add_source(Sm, u);
-      cfd_apply<M, true>(c, P, lane, stU, wv, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
+      cfd_apply<M, true, EDGE>(c, P, lane, stU, wv, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
     } else {
       for (int k = 0; k < P.K; ++k) {
-        cfd_apply<M, true>(c, P, lane, stU, x, Sm, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
+        cfd_apply<M, true, EDGE>(c, P, lane, stU, x, Sm, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
         if (MODE == KM_SWEEP && k + 1 == P.K) stage_phi();
-        cfd_apply<M, false>(c, P, lane, stXs, u, Vm, x, P.cx, um1, up1, VFn, VLp, xm1, xp1);
+        cfd_apply<M, false, EDGE>(c, P, lane, stXs, u, Vm, x, P.cx, um1, up1, VFn, VLp, xm1, xp1);
       }
       if (MODE == KM_SWEEP) {
         double e1, e2;
         add_source(Sm, u);
-        cfd_apply<M, true>(c, P, lane, stU, x, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
+        cfd_apply<M, true, EDGE>(c, P, lane, stU, x, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
 #pragma unroll
         for (int i = 0; i < M; ++i) x[i] = fma(2.0, x[i], -Vm[i]);
       }
@@ -761,8 +784,7 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
   } else {
     // ---------------- MFD ----------------
     const double au = P.cu, bx = P.cx;
-    const double cA = au * (1.0 / 24.0), cB = au * (9.0 / 8.0);
-    const double cC = bx * (1.0 / 24.0), cD = bx * (9.0 / 8.0);
+    const double cA = P.mA, cB = P.mB, cC = P.mC, cD = P.mD;
     double xm2, xm1, xp1, xp2, um2, um1, up1, up2;
     auto u_op = [&](const double (&opd)[M], const double* __restrict__ B) {
       if (c.interior) { MfdSplit<M>::bases(B, u); MfdSplit<M>::u_inner(opd, u, cA, cB); }
@@ -798,62 +820,97 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value)) adi_line_kernel
       }
     }
   }
+  if (tr) tr2 = gtimer();
 
-  // ---- stage the outputs in the tile (own chunk), then store the owned range.
+  // ---- stage the outputs in the tile (own chunk)
   double acc = 0.0;
+  {
+    double2* S2 = reinterpret_cast<double2*>(Sm);
+    double2* V2 = reinterpret_cast<double2*>(Vm);
 #pragma unroll
-  for (int i = 0; i < M; ++i) {
-    Sm[i] = u[i];
-    Vm[i] = x[i];
-    if (c.live) acc += u[i] + x[i];
-  }
-  // X: this warp's own line, contiguous.  Chunks entirely inside the owned range
-  // leave by one TMA bulk store each; partial chunks element by element.
-  const bool xown_all = live_chunk && c.s >= sg.out_lo && c.s + M <= sg.out_hi && c.s >= 0 &&
-                        c.s + M - 1 <= n;
-  double* Xo = P.X_out + b * P.x_batch + (long long)line * P.x_line;
-  fence_async_shared();
-  __syncwarp();
-  if (xown_all) bulk_s2g(Xo + c.s, Vm, M * 8);
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  if (live_chunk && !xown_all) {
-#pragma unroll 4
-    for (int i = 0; i < M; ++i) {
-      const int p = c.s + i;
-      if (p >= sg.out_lo && p < sg.out_hi && p >= 0 && p <= n) Xo[p] = Vm[i];
+    for (int i = 0; i < M / 2; ++i) {
+      S2[i] = make_double2(u[2 * i], u[2 * i + 1]);
+      V2[i] = make_double2(x[2 * i], x[2 * i + 1]);
+    }
+    if (P.flag && lineok && (!EDGE || c.live)) {
+#pragma unroll
+      for (int i = 0; i < M; ++i) acc += u[i] + x[i];
     }
   }
   __syncthreads();
-  // S (or U): transposed — a thread stores one position of a pair of lines (16 B)
-#pragma unroll 4
-  for (int k = 0; k < (NW / 2) * M; ++k) {
-    const int e = t + NT * k;
-    const int pr = e % (NW / 2), pos = e / (NW / 2);
-    const int l0 = 2 * pr;
-    const int ln = P.line0 + blockIdx.x * NW + l0;
-    const int p = sg.start + pos;
-    if (pos >= nact || p < sg.out_lo || p >= sg.out_hi || p < 0 || p > n) continue;
-    const bool ok0 = ln >= P.line_lo && ln < P.nlines;
-    const bool ok1 = ln + 1 >= P.line_lo && ln + 1 < P.nlines;
-    const int si = (pos / M) * PADM + pos % M;
-    const double v0 = stS[l0 * LSTR + si], v1 = stS[(l0 + 1) * LSTR + si];
-    if (MODE == KM_FINAL) {
-      double* Ub = P.U_out + b * P.u_batch + (long long)p * P.u_pt + (long long)ln * P.u_line;
-      if (ok0 && ok1) *reinterpret_cast<double2*>(Ub) = make_double2(v0, v1);
-      else { if (ok0) Ub[0] = v0; if (ok1) Ub[P.u_line] = v1; }
-      if (METHOD == M_MFD && p == n) {
-        double* Ut = P.U_out + b * P.u_batch + (long long)(n + 1) * P.u_pt + (long long)ln * P.u_line;
-        if (ok0) Ut[0] = P.edgeR ? P.edgeR[ln] * P.gb : 0.0;
-        if (ok1) Ut[P.u_line] = P.edgeR ? P.edgeR[ln + 1] * P.gb : 0.0;
+  // X: this warp's own line, positions [xlo, xhi), pairs of positions per lane
+  // (16-byte loads and stores; chunk starts and line pitches are even)
+  if (lineok) {
+    const int xlo = max(sg.out_lo, 0), xhi = min(sg.out_hi, n + 1);
+    double* Xo = P.X_out + (long long)b * P.x_batch + (long long)line * P.x_line;
+    for (int p = (xlo & ~1) + 2 * lane; p < xhi; p += 64) {
+      const int q = p - sg.start;
+      const double2 v = *reinterpret_cast<const double2*>(lX + (q >> 5) * PADM + (q & 31));
+      if (p >= xlo && p + 1 < xhi) *reinterpret_cast<double2*>(Xo + p) = v;
+      else {
+        if (p >= xlo) Xo[p] = v.x;
+        if (p + 1 >= xlo && p + 1 < xhi) Xo[p + 1] = v.y;
       }
-    } else if (p >= 1 && p <= uhi) {
-      double* So = P.S_out + b * P.s_batch + (long long)p * P.so_pt + (long long)ln * P.so_line;
-      if (ok0 && ok1) *reinterpret_cast<double2*>(So) = make_double2(v0, v1);
-      else { if (ok0) So[0] = v0; if (ok1) So[P.so_line] = v1; }
     }
   }
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  // S (or U): transposed.  Half-warp h of warp w stores line pair h at positions
+  // 16 w + (lane & 15) + 64 k: the two half-warps fill one 32-byte sector each
+  {
+    const int pr = lane >> 4;
+    const int ln = P.line0 + blockIdx.x * NW + 2 * pr;
+    const bool ok0 = ln >= P.line_lo && ln < P.nlines;
+    const bool ok1 = ln + 1 >= P.line_lo && ln + 1 < P.nlines;
+    int plo_, phi_;   // output positions of this tile for S / U
+    if (MODE == KM_FINAL) { plo_ = max(sg.out_lo, 0); phi_ = min(sg.out_hi, n + 1); }
+    else { plo_ = max(sg.out_lo, 1); phi_ = min(sg.out_hi, uhi + 1); }
+    const double* r0 = stS + (2 * pr) * LSTR;
+    const double* r1 = r0 + LSTR;
+    for (int pos = 16 * w + (lane & 15); pos < 32 * M; pos += 16 * NW) {
+      const int p = sg.start + pos;
+      if (p < plo_ || p >= phi_) continue;
+      const int si = (pos >> 5) * PADM + (pos & 31);
+      const double v0 = r0[si], v1 = r1[si];
+      if (MODE == KM_FINAL) {
+        double* Ub = P.U_out + (long long)b * P.u_batch + (long long)p * P.u_pt + (long long)ln * P.u_line;
+        if (ok0 && ok1) *reinterpret_cast<double2*>(Ub) = make_double2(v0, v1);
+        else { if (ok0) Ub[0] = v0; if (ok1) Ub[P.u_line] = v1; }
+        if (METHOD == M_MFD && p == n) {
+          double* Ut = P.U_out + (long long)b * P.u_batch + (long long)(n + 1) * P.u_pt + (long long)ln * P.u_line;
+          if (ok0) Ut[0] = P.edgeR ? P.edgeR[ln] * P.gb : 0.0;
+          if (ok1) Ut[P.u_line] = P.edgeR ? P.edgeR[ln + 1] * P.gb : 0.0;
+        }
+      } else {
+        double* So = P.S_out + (long long)b * P.s_batch + (long long)p * P.so_pt + (long long)ln * P.so_line;
+        if (ok0 && ok1) *reinterpret_cast<double2*>(So) = make_double2(v0, v1);
+        else { if (ok0) So[0] = v0; if (ok1) So[P.so_line] = v1; }
+      }
+    }
+  }
   if (P.flag && !isfinite(acc)) atomicOr(P.flag, 1);
+  if (tr && tile < P.trace_cap) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    unsigned long long* r = P.trace + tile * 8;
+    r[0] = tile; r[1] = smid; r[2] = tr0; r[3] = tr1; r[4] = tr2; r[5] = gtimer();
+  }
+}
+
+// ===========================================================================
+// The line kernel: grid (line groups, segments, batch), NW warps per CTA.
+//   MODE = KM_SWEEP   : S_in, X_in -> K sweeps -> S'^T (S_out), X' (X_out)
+//   MODE = KM_FINAL   : as SWEEP without the fused explicit half; writes U_out
+//   MODE = KM_PROLOGUE: U_in, X_in -> a2 (explicit half only)
+// ===========================================================================
+template <int METHOD, int M, int NW, int MODE>
+__global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value))
+    adi_line_kernel(const __grid_constant__ KParams P) {
+  extern __shared__ __align__(128) double smem_raw[];
+  // TMA destinations need 128-byte alignment
+  // (pointer arithmetic on the shared array keeps the shared address space visible)
+  double* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u) / 8u;
+  const Seg sg = P.segs[blockIdx.y];
+  if (sg.edge) line_tile<METHOD, M, NW, MODE, true>(P, sg, smem);
+  else line_tile<METHOD, M, NW, MODE, false>(P, sg, smem);
 }
 
 }  // namespace adi

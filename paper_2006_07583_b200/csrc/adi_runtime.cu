@@ -54,6 +54,9 @@ struct adi_ctx {
   int check_finite = 0;
   int tile_chunks = 0;  // 0 = auto
   int timing = 0;
+  unsigned long long* trace = nullptr;  // adi_set_trace
+  long long trace_cap = 0;
+  int trace_kind = -1;
   struct Rec { int kind; cudaEvent_t a, b; };
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> pool;
@@ -94,6 +97,9 @@ struct adi_ctx {
   bool in_call = false;
   long long call_m1 = 0;
   double *Vcur = nullptr, *Valt = nullptr, *Wcur = nullptr, *Walt = nullptr;
+  // TMA tensor maps of the staged arrays (keyed by base pointer)
+  struct TMap { const double* ptr; CUtensorMap map; };
+  std::vector<TMap> tmaps;
 };
 
 namespace {
@@ -112,6 +118,72 @@ int fail(adi_ctx* h, int code, const std::string& msg) {
     if (e_ != cudaSuccess)                                                                 \
       return fail((h), ADI_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
   } while (0)
+
+// ---- device arrays read by the line kernels' TMA copies carry guard regions
+// (adi_line.cuh: a staged row may start TMA_P0 positions before a line and end
+// past the last line); allocations are zeroed.
+double* dalloc(size_t n) {
+  void* raw = nullptr;
+  const size_t tot = (n + adi::BUF_GUARD_FRONT + adi::BUF_GUARD_TAIL) * sizeof(double);
+  if (cudaMalloc(&raw, tot) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  if (cudaMemset(raw, 0, tot) != cudaSuccess) { cudaGetLastError(); cudaFree(raw); return nullptr; }
+  return static_cast<double*>(raw) + adi::BUF_GUARD_FRONT;
+}
+void dfree(double* p) {
+  if (p) cudaFree(p - adi::BUF_GUARD_FRONT);
+}
+
+// ---- TMA tensor maps (driver entry point fetched through the runtime)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+
+// the overlapping-row view of a pitched line array (adi_line.cuh, TMA_P0)
+int encode_lines(adi_ctx* h, const double* base, int pitch, int rows, size_t bstride, int batch,
+                 CUtensorMap* out) {
+  if (!g_encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+      cudaGetLastError();
+      return fail(h, ADI_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    }
+    g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+  }
+  const cuuint64_t dims[5] = {34, 16, (cuuint64_t)((pitch + adi::TMA_P0 + 31) / 32 + 1), (cuuint64_t)rows,
+                              (cuuint64_t)batch};
+  const cuuint64_t strides[4] = {16, 256, (cuuint64_t)pitch * 8, (cuuint64_t)bstride * 8};
+  const cuuint32_t box[5] = {34, 1, 32, 1, 1};
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  const CUresult r = g_encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)(base - adi::TMA_P0), dims, strides,
+                              box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(h, ADI_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return ADI_OK;
+}
+
+// tensor map of one of the handle's staged arrays
+int tmap_for(adi_ctx* h, const double* ptr, CUtensorMap* out) {
+  for (auto& e : h->tmaps)
+    if (e.ptr == ptr) { *out = e.map; return ADI_OK; }
+  int pitch, rows, batch = h->batch;
+  size_t bs;
+  if (ptr == h->Sa) { pitch = h->pa; rows = h->nyu; bs = h->aS; }
+  else if (ptr == h->Sb) { pitch = h->pb; rows = h->nxu; bs = h->aS; }
+  else if (ptr == h->V || ptr == h->V2) { pitch = h->pv; rows = h->nyu; bs = h->aV; }
+  else if (ptr == h->W || ptr == h->W2) { pitch = h->pw; rows = h->nxu; bs = h->aW; }
+  else if (ptr == h->phi) { pitch = h->pa; rows = h->nyu; bs = h->aS; batch = 1; }
+  else if (ptr == h->phiT) { pitch = h->pb; rows = h->nxu; bs = h->aS; batch = 1; }
+  else return fail(h, ADI_EINVAL, "internal: no tensor map for this array");
+  adi_ctx::TMap e;
+  e.ptr = ptr;
+  int rc = encode_lines(h, ptr, pitch, rows, bs, batch, &e.map);
+  if (rc) return rc;
+  h->tmaps.push_back(e);
+  *out = e.map;
+  return ADI_OK;
+}
 
 // ---- constants: MFD closures as the printed rationals (App. B), CFD interior LU
 int init_constants(adi_ctx* h) {
@@ -218,7 +290,7 @@ bool plan_axis(adi::Axis& A, int method, int nlmin, int cap) {
   const int nch1 = (P + D) / M;
   if (nch1 <= chmax) {
     const int ds = (D / 2) & ~1;   // dead positions before 0 (even); the rest after n
-    A.segs.push_back({-ds, nch1, 0, P});
+    A.segs.push_back({-ds, nch1, 0, P, 1});
     return true;
   }
   const int CH = chmax;
@@ -266,7 +338,7 @@ int setup_axis(adi_ctx* h, adi::Axis& A, int n, int nlines, int nlmin) {
       if (g.out_lo < g.out_hi) keep.push_back(g);
     }
     A.segs = keep;
-    if (A.segs.empty()) A.segs.push_back({0, 0, 0, 0});  // nothing to output: an idle tile
+    if (A.segs.empty()) A.segs.push_back({0, 0, 0, 0, 1});  // nothing to output: an idle tile
   }
   if (A.d_segs) { cudaFree(A.d_segs); A.d_segs = nullptr; }
   if (A.d_tabU) { cudaFree(A.d_tabU); A.d_tabU = nullptr; }
@@ -287,6 +359,8 @@ int setup_axis(adi_ctx* h, adi::Axis& A, int n, int nlines, int nlmin) {
     A.plo = 2;
     A.phi = n - 2;
   }
+  for (adi::Seg& g : A.segs)
+    g.edge = !(g.nchunks == adi::TCH && g.start >= A.plo && g.start + adi::TCH * adi::TM - 1 <= A.phi);
   CUDA_TRY(h, cudaMalloc(&A.d_segs, A.segs.size() * sizeof(adi::Seg)));
   CUDA_TRY(h, cudaMemcpy(A.d_segs, A.segs.data(), A.segs.size() * sizeof(adi::Seg),
                          cudaMemcpyHostToDevice));
@@ -338,8 +412,15 @@ int launch_t(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
   return ADI_OK;
 }
 
-int launch(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p, int kind) {
+int launch(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p0, int kind) {
   TimeScope ts(h, kind);
+  adi::KParams p = p0;
+  p.trace = (kind == h->trace_kind) ? h->trace : nullptr;
+  p.trace_cap = h->trace_cap;
+  int rc;
+  if (p.S_in && (rc = tmap_for(h, p.S_in, &p.tmS))) return rc;
+  if ((rc = tmap_for(h, p.X_in, &p.tmX))) return rc;
+  if (p.phi_src && (rc = tmap_for(h, p.phi_src, &p.tmF))) return rc;
   if (h->method == ADI_CFD) {
     if (mode == adi::KM_SWEEP) return launch_t<adi::M_CFD, adi::KM_SWEEP>(h, A, p);
     if (mode == adi::KM_FINAL) return launch_t<adi::M_CFD, adi::KM_FINAL>(h, A, p);
@@ -433,20 +514,23 @@ adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
   const double f = (h->method == ADI_CFD) ? 3.0 : 1.0;
   p.cu = f * alpha / h->h;
   p.cx = f * beta / h->h;
+  p.mA = p.cu * (1.0 / 24.0);
+  p.mB = p.cu * (9.0 / 8.0);
+  p.mC = p.cx * (1.0 / 24.0);
+  p.mD = p.cx * (9.0 / 8.0);
   p.half_dt = h->dt / 2.0;
   p.K = h->K;
   p.tabU = A.d_tabU;
   p.tabX = A.d_tabX;
-  p.flag = h->flag;
+  p.flag = h->check_finite ? h->flag : nullptr;
   return p;
 }
 
 void free_ctx(adi_ctx* h) {
   for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
-  for (void* q : {(void*)h->Ubase, (void*)h->V, (void*)h->W, (void*)h->V2, (void*)h->W2,
-                  (void*)h->Sa, (void*)h->Sb, (void*)h->phi, (void*)h->phiT, (void*)h->edges,
-                  (void*)h->flag})
+  for (double* q : {h->Ubase, h->V, h->W, h->V2, h->W2, h->Sa, h->Sb, h->phi, h->phiT}) dfree(q);
+  for (void* q : {(void*)h->edges, (void*)h->flag})
     if (q) cudaFree(q);
   for (adi::Axis* A : {&h->ax, &h->ay})
     for (void* q : {(void*)A->d_segs, (void*)A->d_tabU, (void*)A->d_tabX, (void*)A->d_ptl,
@@ -505,17 +589,13 @@ int adi_create_batch(int nx, int ny, double hh, double dt, double c, int method,
   };
   if (rc) return bail(rc);
   const size_t B = (size_t)batch;
-  if (cudaMalloc(&h->Ubase, B * h->aU * 8) || cudaMalloc(&h->V, B * h->aV * 8) ||
-      cudaMalloc(&h->W, B * h->aW * 8) || cudaMalloc(&h->V2, B * h->aV * 8) ||
-      cudaMalloc(&h->W2, B * h->aW * 8) || cudaMalloc(&h->Sa, B * h->aS * 8) ||
-      cudaMalloc(&h->Sb, B * h->aS * 8) || cudaMalloc(&h->flag, sizeof(int))) {
+  if (!(h->Ubase = dalloc(B * h->aU)) || !(h->V = dalloc(B * h->aV)) || !(h->W = dalloc(B * h->aW)) ||
+      !(h->V2 = dalloc(B * h->aV)) || !(h->W2 = dalloc(B * h->aW)) || !(h->Sa = dalloc(B * h->aS)) ||
+      !(h->Sb = dalloc(B * h->aS)) || cudaMalloc(&h->flag, sizeof(int))) {
     cudaGetLastError();
     return bail(ADI_ENOMEM);
   }
   h->U = h->Ubase;
-  for (double* q : {h->Ubase, h->V, h->V2, h->W, h->W2, h->Sa, h->Sb})
-    cudaMemset(q, 0, B * (q == h->Ubase ? h->aU : (q == h->V || q == h->V2) ? h->aV
-                        : (q == h->W || q == h->W2) ? h->aW : h->aS) * 8);
   cudaMemset(h->flag, 0, sizeof(int));
   if ((rc = setup_axis(h, h->ax, nx - 1, h->nyi, 1))) return bail(rc);
   if ((rc = setup_axis(h, h->ay, ny - 1, h->nxi, 4))) return bail(rc);
@@ -629,8 +709,11 @@ int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double
   if (g && ng < 1) return fail(h, ADI_EINVAL, "empty source table");
   if (ix >= 1 && h->batch != 1) return fail(h, ADI_EINVAL, "use adi_set_point_sources for a batch");
   if (phi) {
-    if (!h->phi) CUDA_TRY(h, cudaMalloc(&h->phi, h->aS * 8));
-    if (!h->phiT) CUDA_TRY(h, cudaMalloc(&h->phiT, h->aS * 8));
+    if (!h->phi || !h->phiT) {
+      h->tmaps.clear();
+      if (!h->phi && !(h->phi = dalloc(h->aS))) return fail(h, ADI_ENOMEM, "source pattern");
+      if (!h->phiT && !(h->phiT = dalloc(h->aS))) return fail(h, ADI_ENOMEM, "source pattern");
+    }
     CUDA_TRY(h, cudaMemset(h->phi, 0, h->aS * 8));
     CUDA_TRY(h, cudaMemset(h->phiT, 0, h->aS * 8));
     // interior point (j, i) of the user's block is position (y, x) = (j + 1, i + 1)
@@ -640,8 +723,9 @@ int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double
     if (rc) return rc;
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   } else if (h->phi) {
-    cudaFree(h->phi);
-    cudaFree(h->phiT);
+    h->tmaps.clear();
+    dfree(h->phi);
+    dfree(h->phiT);
     h->phi = nullptr;
     h->phiT = nullptr;
   }
@@ -960,6 +1044,16 @@ int adi_get_kernel_times(adi_handle h, double* ms, long long* launches, int nkin
     h->pool.push_back(r.b);
   }
   h->recs.clear();
+  return ADI_OK;
+}
+
+int adi_set_trace(adi_handle h, void* dev_buf, long long cap, int kind) {
+  if (!h) return ADI_EINVAL;
+  h->err.clear();
+  if (dev_buf && (cap < 0 || kind < 0 || kind >= ADI_NKINDS)) return fail(h, ADI_EINVAL, "bad trace arguments");
+  h->trace = (unsigned long long*)dev_buf;
+  h->trace_cap = dev_buf ? cap : 0;
+  h->trace_kind = dev_buf ? kind : -1;
   return ADI_OK;
 }
 
