@@ -563,9 +563,9 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
 }
 
 // Occupancy targets (resident CTAs per SM) for the NW-warp CTAs.
-template <int METHOD>
+template <int METHOD, bool EDGE>
 struct Occ {
-  static constexpr int value = (METHOD == M_MFD) ? 3 : 2;
+  static constexpr int value = (METHOD == M_MFD || !EDGE) ? 3 : 2;
 };
 
 __host__ __device__ constexpr int PADM_OF(int M) { return M + 2; }
@@ -573,9 +573,10 @@ __host__ __device__ constexpr int PADM_OF(int M) { return M + 2; }
 __host__ __device__ constexpr int LSTR_OF(int M) { return (32 * (M + 2) + 15) / 16 * 16; }
 
 // shared memory of one CTA: padded staging of S and X for NW lines (+ CFD statics)
-template <int METHOD, int M, int NW>
+// (the CFD chunk statics are only needed by edge tiles)
+template <int METHOD, int M, int NW, bool EDGE>
 constexpr size_t line_smem_bytes() {
-  return sizeof(double) * (size_t)(2 * NW * LSTR_OF(M) + (METHOD == M_CFD ? NW * 10 * 32 : 0) + NW) + 128;
+  return sizeof(double) * (size_t)(2 * NW * LSTR_OF(M) + (METHOD == M_CFD && EDGE ? NW * 10 * 32 : 0) + NW) + 128;
 }
 
 // TMA tensor copy of one line segment (box {34,1,32,1,1}) into the staging tile
@@ -605,7 +606,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   double* stX = stS + NW * LSTR;  // [NW][LSTR]: X, then X'
   double* stc = stX + NW * LSTR;  // CFD statics [NW][2 sys][5][32] (edge tiles)
   unsigned long long* wbars =
-      (unsigned long long*)(stc + (METHOD == M_CFD ? NW * 10 * 32 : 0));  // [NW] per-warp mbarriers
+      (unsigned long long*)(stc + (METHOD == M_CFD && EDGE ? NW * 10 * 32 : 0));  // [NW] per-warp mbarriers
 
   const int t = threadIdx.x;
   const int w = t >> 5, lane = t & 31;
@@ -675,6 +676,14 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     }
   }
   const bool want_phi = (MODE != KM_FINAL) && P.phi_src;
+  if (want_phi && lane == 0) {
+    // the source pattern is staged late (after the last u-op): warm L2 now
+    asm volatile(
+        "cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+            (unsigned long long)&P.tmF),
+        "r"(0), "r"(c1), "r"(c2), "r"(line), "r"(0)
+        : "memory");
+  }
   if (MODE == KM_PROLOGUE) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   mbar_wait(wbar, wpar);
   wpar ^= 1u;
@@ -896,21 +905,22 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
 }
 
 // ===========================================================================
-// The line kernel: grid (line groups, segments, batch), NW warps per CTA.
+// The line kernel: grid (line groups, segments, batch), NW warps per CTA.  The
+// interior segments (EDGE = false) and the segments holding line ends (EDGE =
+// true) are separate launches, so the main kernel carries only the lean path.
 //   MODE = KM_SWEEP   : S_in, X_in -> K sweeps -> S'^T (S_out), X' (X_out)
 //   MODE = KM_FINAL   : as SWEEP without the fused explicit half; writes U_out
 //   MODE = KM_PROLOGUE: U_in, X_in -> a2 (explicit half only)
 // ===========================================================================
-template <int METHOD, int M, int NW, int MODE>
-__global__ void __launch_bounds__(32 * NW, (Occ<METHOD>::value))
+template <int METHOD, int M, int NW, int MODE, bool EDGE>
+__global__ void __launch_bounds__(32 * NW, (Occ<METHOD, EDGE>::value))
     adi_line_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(128) double smem_raw[];
   // TMA destinations need 128-byte alignment
   // (pointer arithmetic on the shared array keeps the shared address space visible)
   double* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u) / 8u;
   const Seg sg = P.segs[blockIdx.y];
-  if (sg.edge) line_tile<METHOD, M, NW, MODE, true>(P, sg, smem);
-  else line_tile<METHOD, M, NW, MODE, false>(P, sg, smem);
+  line_tile<METHOD, M, NW, MODE, EDGE>(P, sg, smem);
 }
 
 }  // namespace adi

@@ -37,7 +37,8 @@ struct Axis {
   int halo = 0;
   int NL = 1;
   int plo = 0, phi = -1;
-  std::vector<Seg> segs;
+  std::vector<Seg> segs;   // interior segments (edge == 0) first
+  int nint = 0;            // number of interior segments
   Seg* d_segs = nullptr;
   double* d_tabU = nullptr;  // CFD only
   double* d_tabX = nullptr;
@@ -360,7 +361,13 @@ int setup_axis(adi_ctx* h, adi::Axis& A, int n, int nlines, int nlmin) {
     A.phi = n - 2;
   }
   for (adi::Seg& g : A.segs)
-    g.edge = !(g.nchunks == adi::TCH && g.start >= A.plo && g.start + adi::TCH * adi::TM - 1 <= A.phi);
+    // lean (interior) tile: every ACTIVE chunk is interior.  The lean kernel also
+    // runs the chunks beyond nchunks on the (finite) data past the segment; they
+    // only move the truncation boundary further from the owned range.
+    g.edge = !(g.nchunks > 0 && g.start >= A.plo && g.start + g.nchunks * adi::TM - 1 <= A.phi);
+  std::stable_partition(A.segs.begin(), A.segs.end(), [](const adi::Seg& g) { return g.edge == 0; });
+  A.nint = 0;
+  for (const adi::Seg& g : A.segs) A.nint += (g.edge == 0);
   CUDA_TRY(h, cudaMalloc(&A.d_segs, A.segs.size() * sizeof(adi::Seg)));
   CUDA_TRY(h, cudaMemcpy(A.d_segs, A.segs.data(), A.segs.size() * sizeof(adi::Seg),
                          cudaMemcpyHostToDevice));
@@ -394,22 +401,33 @@ struct TimeScope {
   }
 };
 
-template <int METHOD, int MODE>
-int launch_t(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
-  auto kern = adi::adi_line_kernel<METHOD, adi::TM, adi::NW, MODE>;
-  const size_t smem = adi::line_smem_bytes<METHOD, adi::TM, adi::NW>();
+template <int METHOD, int MODE, bool EDGE>
+int launch_e(adi_ctx* h, const adi::Axis& A, adi::KParams p, int seg0, int nseg) {
+  auto kern = adi::adi_line_kernel<METHOD, adi::TM, adi::NW, MODE, EDGE>;
+  const size_t smem = adi::line_smem_bytes<METHOD, adi::TM, adi::NW, EDGE>();
   static bool attr = false;
   if (!attr) {
     CUDA_TRY(h, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
+  if (nseg <= 0) return ADI_OK;
   const int nl = std::max(A.l1 - (A.l0 & ~3), 0);
-  if (A.l1 <= A.l0) return ADI_OK;
-  dim3 grid((nl + adi::NW - 1) / adi::NW, (unsigned)A.segs.size(), h->batch);
+  p.segs = A.d_segs + seg0;
+  dim3 grid((nl + adi::NW - 1) / adi::NW, (unsigned)nseg, h->batch);
   kern<<<grid, 32 * adi::NW, smem, h->stream>>>(p);
   CUDA_TRY(h, cudaGetLastError());
   h->launches++;
   return ADI_OK;
+}
+
+// interior segments first (lean kernel), then the segments with line ends
+template <int METHOD, int MODE>
+int launch_t(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
+  if (A.l1 <= A.l0) return ADI_OK;
+  const int nseg = (int)A.segs.size();
+  int rc = launch_e<METHOD, MODE, false>(h, A, p, 0, A.nint);
+  if (rc) return rc;
+  return launch_e<METHOD, MODE, true>(h, A, p, A.nint, nseg - A.nint);
 }
 
 int launch(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p0, int kind) {
