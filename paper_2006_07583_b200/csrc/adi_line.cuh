@@ -44,7 +44,9 @@ struct Seg {
   int nchunks;  // active chunks per line in this tile
   int out_lo;   // positions [out_lo, out_hi) are written by this tile
   int out_hi;
-  int edge;     // 0: all 32 chunks are interior (plo <= p <= phi): the lean tile path
+  int edge;     // 1: generic tile (short lines): per-chunk closures and LU tables
+  int end;      // lean tiles: 0 interior, 1 line start (start = 0), 2 line end at
+                // chunk 31 element 31 (position n), 3 line end at element 30 (n+1 dead)
 };
 
 // Staging tiles arrive by TMA tensor copies of an OVERLAPPING-ROW view of a
@@ -117,6 +119,15 @@ __constant__ double c_cl, c_cinvd;
 __constant__ double c_cF, c_cKs, c_cKe, c_cJs, c_cJe;
 __constant__ double c_sK[MMAX], c_sJ[MMAX];
 __constant__ double c_sF;
+// Line ends of lean CFD tiles: the lean solve applies T* = L*U*
+// (constant pivots); the true operator with the end rows (and identity rows at
+// positions outside the system) is A = T* + U V^T of rank <= 3, so
+// A^{-1} r = z - M (V^T z), z = T*^{-1} r, M = T*^{-1} U (I + V^T T*^{-1} U)^{-1}.
+// Case = system (0: u-op P̄, 1: x-op P) * 3 + end (0 start, 1 end at n, 2 end at
+// n+1); V acts on 4 chunk elements (0..3 at the start, 28..31 at the end), M on the
+// 32 elements of the end chunk (T*^{-1} U decays like (2-sqrt 3)^d).
+__constant__ double c_wbV[6][3][4];
+__constant__ double c_wbM[6][32][3];
 enum { ST_F = 0, ST_KS = 1, ST_KE = 2, ST_JS = 3, ST_JE = 4 };  // CFD chunk statics
 
 template <int M>
@@ -126,6 +137,8 @@ struct Ctx {
   bool interior;  // fast path allowed
   bool nbint;     // chunks c-2 .. c+2 all exist and are interior (CFD constant statics)
   double gL, gR;  // Dirichlet values of this line for this half-step
+  int endc;       // lean tiles: -1 interior, 0 line start, 1 end at n, 2 end at n+1
+  bool me;        // this lane owns the chunk with the line end (lane 0 / lane 31)
 };
 
 // ===========================================================================
@@ -314,6 +327,71 @@ struct MfdSplit {
   }
 };
 
+// MFD closure rows at the line end of a lean tile (same arithmetic as Mfd<M>::uop/xop)
+template <int M>
+__device__ __forceinline__ void mfd_end_u(const Ctx<M>& c, const double (&x)[M], const double* __restrict__ B,
+                                          double (&out)[M], double a) {
+  static_assert(M == 32, "end fix-ups assume 32-point chunks");
+  if (c.endc == 0) {
+    out[0] = c.gL;  // ū_0
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) s = fma(c_d4r0[k], x[k], s);
+    out[1] = fma(-a, s, B[1]);
+  } else {
+    const int i = (c.endc == 1) ? 31 : 30;  // position n
+    double s = 0.0;
+    if (c.endc == 1) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) s = fma(-c_d4r0[5 - k], x[26 + k], s);
+      out[31] = fma(-a, s, B[31]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) s = fma(-c_d4r0[5 - k], x[25 + k], s);
+      out[30] = fma(-a, s, B[30]);
+      out[31] = 0.0;
+    }
+    (void)i;
+  }
+}
+template <int M>
+__device__ __forceinline__ void mfd_end_x(const Ctx<M>& c, const double (&u)[M], const double* __restrict__ B,
+                                          double (&out)[M], double b) {
+  if (c.endc == 0) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) s = fma(c_g4r0[k], u[k], s);
+    out[0] = fma(-b, s, B[0]);
+    s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) s = fma(c_g4r1[k], u[k], s);
+    out[1] = fma(-b, s, B[1]);
+  } else if (c.endc == 1) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s = fma(-c_g4r1[4 - k], u[28 + k], s);
+    s = fma(-c_g4r1[0], c.gR, s);
+    out[30] = fma(-b, s, B[30]);
+    s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) s = fma(-c_g4r0[5 - k], u[27 + k], s);
+    s = fma(-c_g4r0[0], c.gR, s);
+    out[31] = fma(-b, s, B[31]);
+  } else {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s = fma(-c_g4r1[4 - k], u[27 + k], s);
+    s = fma(-c_g4r1[0], c.gR, s);
+    out[29] = fma(-b, s, B[29]);
+    s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) s = fma(-c_g4r0[5 - k], u[26 + k], s);
+    s = fma(-c_g4r0[0], c.gR, s);
+    out[30] = fma(-b, s, B[30]);
+    out[31] = 0.0;
+  }
+}
+
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   const int sz = valid ? 8 : 0;
@@ -376,8 +454,22 @@ __device__ __forceinline__ void warp_edges(int lane, const double (&a)[M], doubl
   np2 = lane == 31 ? 0.0 : np2;
 }
 
+// CFD LU tables of the line ends staged in shared memory by edge tiles:
+// [system 2][l, 1/d, c][ETAB], entries 0..63 = positions 0..63, entries 64..127 =
+// positions n-63..n.  Non-interior chunks only touch positions within 64 of an
+// end (plo <= 32, checked by the runtime), so the staged entries cover them.
+constexpr int ETAB = 128;
+struct EdgeTab {
+  const double* t;  // [3][ETAB] of one system
+  int n;
+  __device__ __forceinline__ double get(int arr, int p) const {
+    const int i = p < 64 ? p : 64 + p - (n - 63);
+    return t[arr * ETAB + i];
+  }
+};
+
 template <int M>
-__device__ __forceinline__ void cfd_statics(const Ctx<M>& c, const double* tab, int np1,
+__device__ __forceinline__ void cfd_statics(const Ctx<M>& c, const EdgeTab& T, int np1,
                                             double* st /* 5 */) {
   if (c.interior) {
     st[0] = c_cF; st[1] = c_cKs; st[2] = c_cKe; st[3] = c_cJs; st[4] = c_cJe;
@@ -388,7 +480,7 @@ __device__ __forceinline__ void cfd_statics(const Ctx<M>& c, const double* tab, 
 #pragma unroll
   for (int i = 0; i < M; ++i) {
     const int p = c.s + i;
-    const double l = (p >= 0 && p < np1) ? __ldg(tab + p) : 0.0;
+    const double l = (p >= 0 && p < np1) ? T.get(0, p) : 0.0;
     g *= -l;
     G[i] = g;
   }
@@ -398,8 +490,8 @@ __device__ __forceinline__ void cfd_statics(const Ctx<M>& c, const double* tab, 
   for (int i = M - 1; i >= 0; --i) {
     const int p = c.s + i;
     const bool in = (p >= 0 && p < np1);
-    const double iv = in ? __ldg(tab + np1 + p) : 0.0;
-    const double cc = in ? __ldg(tab + 2 * np1 + p) : 0.0;
+    const double iv = in ? T.get(1, p) : 0.0;
+    const double cc = in ? T.get(2, p) : 0.0;
     k = (G[i] - cc * k) * iv;
     j *= -cc * iv;
     if (i == M - 1) { st[2] = k; st[4] = j; }
@@ -421,12 +513,12 @@ constexpr int NSUB = 4;
 // ===========================================================================
 template <int M, bool UOP, bool EDGE>
 __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int lane,
-                                          const double* st, const double (&o)[M],
+                                          const double* st, const double* etab, const double (&o)[M],
                                           const double* __restrict__ B, double (&out)[M],
                                           double coef, double om1, double op1, double Bn_first,
                                           double Bp_last, double& nom1, double& nop1) {
   constexpr int L = M / NSUB;
-  const double* tab = UOP ? P.tabU : P.tabX;
+  const EdgeTab T{etab + (UOP ? 0 : 3 * ETAB), c.n};
   const int np1 = c.n + 1;
   double yl_e, ws, we;
   double ysub[NSUB];
@@ -434,6 +526,19 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
   if (c.interior) {
     if (UOP) Cfd<M>::template rhs_u<true>(c, o, out, om1, op1);
     else Cfd<M>::template rhs_x<true>(c, o, out, om1, op1);
+    if (!EDGE && c.me) {
+      // closure rows of Q̄ / Q at the line end; zero rows outside the system
+      static_assert(M == 32, "end fix-ups assume 32-point chunks");
+      if (UOP) {
+        if (c.endc == 0) { out[0] = 0.0; out[1] = (-o[0] - 9.0 * o[1] + 9.0 * o[2] + o[3]) * (1.0 / 3.0); }
+        else if (c.endc == 1) { out[31] = 0.0; out[30] = (-o[28] - 9.0 * o[29] + 9.0 * o[30] + o[31]) * (1.0 / 3.0); }
+        else { out[31] = 0.0; out[30] = 0.0; out[29] = (-o[27] - 9.0 * o[28] + 9.0 * o[29] + o[30]) * (1.0 / 3.0); }
+      } else {
+        if (c.endc == 0) out[0] = (-17.0 * o[0] + 9.0 * o[1] + 9.0 * o[2] - o[3]) * (1.0 / 3.0);
+        else if (c.endc == 1) out[31] = (o[28] - 9.0 * o[29] - 9.0 * o[30] + 17.0 * o[31]) * (1.0 / 3.0);
+        else { out[31] = 0.0; out[30] = (o[27] - 9.0 * o[28] - 9.0 * o[29] + 17.0 * o[30]) * (1.0 / 3.0); }
+      }
+    }
     const double l = c_cl, iv = c_cinvd, FL = c_sF;
 #pragma unroll
     for (int i = 1; i < L; ++i)
@@ -462,7 +567,7 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
 #pragma unroll
     for (int i = 0; i < M; ++i) {
       const int p = c.s + i;
-      const double l = (p >= 0 && p < np1) ? __ldg(tab + p) : 0.0;
+      const double l = (p >= 0 && p < np1) ? T.get(0, p) : 0.0;
       out[i] = fma(-l, yp, out[i]);
       yp = out[i];
     }
@@ -473,8 +578,8 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
     for (int i = M - 1; i >= 0; --i) {
       const int p = c.s + i;
       const bool in = (p >= 0 && p < np1);
-      const double iv = in ? __ldg(tab + np1 + p) : 0.0;
-      const double cc = in ? __ldg(tab + 2 * np1 + p) : 0.0;
+      const double iv = in ? T.get(1, p) : 0.0;
+      const double cc = in ? T.get(2, p) : 0.0;
       z = (out[i] - cc * z) * iv;
       if (i == M - 1) we = z;
     }
@@ -521,6 +626,25 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
     for (int j = NSUB - 2; j >= 0; --j)
       zcT[j] = fma(c_sJ[0], zcT[j + 1], fma(c_sK[0], ycT[j + 1], iv * out[(j + 1) * L]));
     z0 = fma(c_sJ[0], zcT[0], fma(c_sK[0], ycT[0], iv * out[0]));
+    double g0 = 0.0, g1 = 0.0, g2 = 0.0;  // V^T z of the line-end correction
+    const int wc = (UOP ? 0 : 3) + (c.endc < 0 ? 0 : c.endc);
+    if (!EDGE && c.me) {
+      double zz[4];
+      if (c.endc == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) zz[q] = fma(c_sJ[q], zcT[0], fma(c_sK[q], ycT[0], iv * out[q]));
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          zz[q] = fma(c_sJ[L - 4 + q], zcT[NSUB - 1], fma(c_sK[L - 4 + q], ycT[NSUB - 1], iv * out[M - 4 + q]));
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        g0 = fma(c_wbV[wc][0][q], zz[q], g0);
+        g1 = fma(c_wbV[wc][1][q], zz[q], g1);
+        g2 = fma(c_wbV[wc][2][q], zz[q], g2);
+      }
+    }
     const double ci = coef * iv;
 #pragma unroll
     for (int j = 0; j < NSUB; ++j) {
@@ -529,12 +653,25 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
       for (int i = 0; i < L; ++i)
         out[j * L + i] = fma(-c_sJ[i], cz, fma(-c_sK[i], cy, fma(-ci, out[j * L + i], B[j * L + i])));
     }
+    if (!EDGE && c.me) {
+#pragma unroll
+      for (int i = 0; i < M; ++i)
+        out[i] = fma(coef, fma(c_wbM[wc][i][2], g2, fma(c_wbM[wc][i][1], g1, c_wbM[wc][i][0] * g0)), out[i]);
+      // positions outside the system hold the Dirichlet slots (u-op) or nothing
+      if (UOP) {
+        if (c.endc == 0) out[0] = c.gL;
+        else if (c.endc == 1) out[31] = c.gR;
+        else { out[30] = c.gR; out[31] = 0.0; }
+      } else if (c.endc == 2) {
+        out[31] = 0.0;
+      }
+    }
   } else {
     double g = 1.0;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
       const int p = c.s + i;
-      const double l = (p >= 0 && p < np1) ? __ldg(tab + p) : 0.0;
+      const double l = (p >= 0 && p < np1) ? T.get(0, p) : 0.0;
       g *= -l;
       out[i] = fma(g, ycarry, out[i]);
     }
@@ -543,8 +680,8 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
     for (int i = M - 1; i >= 0; --i) {
       const int p = c.s + i;
       const bool in = (p >= 0 && p < np1);
-      const double iv = in ? __ldg(tab + np1 + p) : 0.0;
-      const double cc = in ? __ldg(tab + 2 * np1 + p) : 0.0;
+      const double iv = in ? T.get(1, p) : 0.0;
+      const double cc = in ? T.get(2, p) : 0.0;
       z = (out[i] - cc * z) * iv;
       out[i] = z;
     }
@@ -576,7 +713,9 @@ __host__ __device__ constexpr int LSTR_OF(int M) { return (32 * (M + 2) + 15) / 
 // (the CFD chunk statics are only needed by edge tiles)
 template <int METHOD, int M, int NW, bool EDGE>
 constexpr size_t line_smem_bytes() {
-  return sizeof(double) * (size_t)(2 * NW * LSTR_OF(M) + (METHOD == M_CFD && EDGE ? NW * 10 * 32 : 0) + NW) + 128;
+  return sizeof(double) *
+             (size_t)(2 * NW * LSTR_OF(M) + (METHOD == M_CFD && EDGE ? NW * 10 * 32 + 6 * ETAB : 0) + NW) +
+         128;
 }
 
 // TMA tensor copy of one line segment (box {34,1,32,1,1}) into the staging tile
@@ -605,8 +744,9 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   double* stS = smem;             // [NW][LSTR]: S (or U in the prologue), later phi, then S'
   double* stX = stS + NW * LSTR;  // [NW][LSTR]: X, then X'
   double* stc = stX + NW * LSTR;  // CFD statics [NW][2 sys][5][32] (edge tiles)
+  double* etab = stc + NW * 10 * 32;  // CFD line-end LU tables [2][3][ETAB] (edge tiles)
   unsigned long long* wbars =
-      (unsigned long long*)(stc + (METHOD == M_CFD && EDGE ? NW * 10 * 32 : 0));  // [NW] per-warp mbarriers
+      (unsigned long long*)(stc + (METHOD == M_CFD && EDGE ? NW * 10 * 32 + 6 * ETAB : 0));  // [NW] mbarriers
 
   const int t = threadIdx.x;
   const int w = t >> 5, lane = t & 31;
@@ -636,6 +776,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     c.interior = true;
     c.nbint = true;
   }
+  c.endc = EDGE ? -1 : sg.end - 1;
+  c.me = !EDGE && ((sg.end == 1 && lane == 0) || (sg.end >= 2 && lane == 31));
 
   // ---- load: one TMA tensor copy per array and warp (zero fill outside the array)
   double* lS = stS + w * LSTR;
@@ -663,9 +805,20 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   }
+  if (METHOD == M_CFD && EDGE) {
+    // stage the line-end LU tables (same for all lines of the tile)
+    const int np1 = n + 1;
+    for (int k = t; k < 6 * ETAB; k += NT) {
+      const int sys = k / (3 * ETAB), arr = (k / ETAB) % 3, i = k % ETAB;
+      const int p = i < 64 ? i : n - 63 + (i - 64);
+      const double* tab = sys ? P.tabX : P.tabU;
+      etab[k] = (p >= 0 && p <= n) ? tab[arr * np1 + p] : 0.0;
+    }
+    __syncthreads();
+  }
   // Dirichlet values of this line (edge tiles only use them)
   c.gL = 0.0; c.gR = 0.0;
-  if (EDGE && lineok) {
+  if ((EDGE || sg.end) && lineok) {
     if (MODE == KM_PROLOGUE) {
       const double* Ub = P.U_in + (long long)b * P.u_batch + (long long)line * P.u_line;
       c.gL = Ub[0];
@@ -752,10 +905,10 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     double* stXs = stc + (w * 2 + 1) * 5 * 32;
     if (EDGE) {
       double q[5];
-      cfd_statics<M>(c, P.tabU, np1, q);
+      cfd_statics<M>(c, EdgeTab{etab, n}, np1, q);
 #pragma unroll
       for (int k = 0; k < 5; ++k) stU[k * 32 + lane] = c.live ? q[k] : 0.0;
-      cfd_statics<M>(c, P.tabX, np1, q);
+      cfd_statics<M>(c, EdgeTab{etab + 3 * ETAB, n}, np1, q);
 #pragma unroll
       for (int k = 0; k < 5; ++k) stXs[k * 32 + lane] = c.live ? q[k] : 0.0;
     }
@@ -773,19 +926,19 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
 #pragma unroll
       for (int i = 0; i < M; ++i) wv[i] = x[i];
       stage_phi();
-      cfd_apply<M, false, EDGE>(c, P, lane, stXs, u, Vm, x, P.cx, um1, up1, 0.0, 0.0, e1, e2);
+      cfd_apply<M, false, EDGE>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, 0.0, 0.0, e1, e2);
       add_source(Sm, u);
-      cfd_apply<M, true, EDGE>(c, P, lane, stU, wv, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
+      cfd_apply<M, true, EDGE>(c, P, lane, stU, etab, wv, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
     } else {
       for (int k = 0; k < P.K; ++k) {
-        cfd_apply<M, true, EDGE>(c, P, lane, stU, x, Sm, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
+        cfd_apply<M, true, EDGE>(c, P, lane, stU, etab, x, Sm, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
         if (MODE == KM_SWEEP && k + 1 == P.K) stage_phi();
-        cfd_apply<M, false, EDGE>(c, P, lane, stXs, u, Vm, x, P.cx, um1, up1, VFn, VLp, xm1, xp1);
+        cfd_apply<M, false, EDGE>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, VFn, VLp, xm1, xp1);
       }
       if (MODE == KM_SWEEP) {
         double e1, e2;
         add_source(Sm, u);
-        cfd_apply<M, true, EDGE>(c, P, lane, stU, x, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
+        cfd_apply<M, true, EDGE>(c, P, lane, stU, etab, x, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
 #pragma unroll
         for (int i = 0; i < M; ++i) x[i] = fma(2.0, x[i], -Vm[i]);
       }
@@ -800,12 +953,14 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       warp_edges<M>(lane, opd, xm2, xm1, xp1, xp2);
       if (c.interior) MfdSplit<M>::u_edges(opd, u, cA, cB, xm2, xm1, xp1);
       else Mfd<M>::template uop<false>(c, opd, B, u, au, xm2, xm1, xp1);
+      if (!EDGE && c.me) mfd_end_u<M>(c, opd, B, u, au);
     };
     auto x_op = [&](const double* __restrict__ B) {
       if (c.interior) { MfdSplit<M>::bases(B, x); MfdSplit<M>::x_inner(u, x, cC, cD); }
       warp_edges<M>(lane, u, um2, um1, up1, up2);
       if (c.interior) MfdSplit<M>::x_edges(u, x, cC, cD, um1, up1, up2);
       else Mfd<M>::template xop<false>(c, u, B, x, bx, um1, up1, up2);
+      if (!EDGE && c.me) mfd_end_x<M>(c, u, B, x, bx);
     };
     if (MODE == KM_PROLOGUE) {
       double wv[M];

@@ -186,6 +186,86 @@ int tmap_for(adi_ctx* h, const double* ptr, CUtensorMap* out) {
   return ADI_OK;
 }
 
+// ---- Woodbury data of the lean CFD end tiles.  The lean solve
+// applies T* = L*U* on the segment (forward y_p = r_p - l y_{p-1}, backward
+// z_p = iv (y_p - z_{p+1}); first pivot 1/iv).  The operator with the line-end rows
+// of P̄ (u-op) or P (x-op), and identity rows at positions outside the system, is
+// A = T* + U V^T with U = [e_rows].  Work on a 64-position window at the end:
+// start: window = segment positions 0..63, end chunk = window 0..31; end: window =
+// positions e-63..e (e = segment end), end chunk = window 32..63.
+void wb_setup(double l, double iv, double V[6][3][4], double Mx[6][32][3]) {
+  typedef long double R;
+  const R dd = 1.0L / (R)iv;             // pivot of U*
+  const R a = (R)l * dd, b = (R)l + dd;  // T* sub-diagonal and diagonal (after the first row)
+  struct Ent { int row, col; R v; };
+  for (int cs = 0; cs < 6; ++cs) {
+    const int sys = cs / 3, e = cs % 3;  // sys 0: u-op (P̄), 1: x-op (P)
+    std::vector<Ent> E;
+    if (e == 0) {
+      if (sys == 0) E = {{0, 0, 1 - dd}, {0, 1, -1}, {1, 0, -a}, {1, 1, 6 - b}, {1, 2, 5}};
+      else E = {{0, 0, 6 - dd}, {0, 1, 17}};
+    } else if (e == 1) {  // position n = window 63
+      if (sys == 0) E = {{62, 61, 6 - a}, {62, 62, 6 - b}, {62, 63, -1}, {63, 62, -a}, {63, 63, 1 - b}};
+      else E = {{63, 62, 18 - a}, {63, 63, 6 - b}};
+    } else {              // position n+1 = window 63 (dead)
+      if (sys == 0)
+        E = {{61, 60, 6 - a}, {61, 61, 6 - b}, {61, 62, -1}, {62, 61, -a}, {62, 62, 1 - b}, {62, 63, -1},
+             {63, 62, -a}, {63, 63, 1 - b}};
+      else E = {{62, 61, 18 - a}, {62, 62, 6 - b}, {62, 63, -1}, {63, 62, -a}, {63, 63, 1 - b}};
+    }
+    std::vector<int> rows;
+    for (const Ent& x : E)
+      if (std::find(rows.begin(), rows.end(), x.row) == rows.end()) rows.push_back(x.row);
+    const int k = (int)rows.size();
+    // W_j = T*^{-1} e_{rows[j]} on the window
+    R W[3][64] = {};
+    for (int j = 0; j < k; ++j) {
+      R y[64], z[64];
+      R prev = 0;
+      for (int q = 0; q < 64; ++q) { y[q] = (q == rows[j] ? 1 : 0) - (R)l * prev; prev = y[q]; }
+      R nxt = 0;
+      for (int q = 63; q >= 0; --q) { z[q] = (R)iv * (y[q] - nxt); nxt = z[q]; }
+      for (int q = 0; q < 64; ++q) W[j][q] = z[q];
+    }
+    // C = I + V^T W, its inverse (k <= 3, Gauss-Jordan)
+    R C[3][3] = {}, Ci[3][3] = {};
+    for (int j = 0; j < 3; ++j) { C[j][j] = 1; Ci[j][j] = 1; }
+    for (const Ent& x : E) {
+      const int j = (int)(std::find(rows.begin(), rows.end(), x.row) - rows.begin());
+      for (int q = 0; q < k; ++q) C[j][q] += x.v * W[q][x.col];
+    }
+    for (int c = 0; c < k; ++c) {
+      int pv = c;
+      for (int r = c + 1; r < k; ++r)
+        if (std::fabs((double)C[r][c]) > std::fabs((double)C[pv][c])) pv = r;
+      for (int q = 0; q < 3; ++q) { std::swap(C[c][q], C[pv][q]); std::swap(Ci[c][q], Ci[pv][q]); }
+      const R inv = 1 / C[c][c];
+      for (int q = 0; q < 3; ++q) { C[c][q] *= inv; Ci[c][q] *= inv; }
+      for (int r = 0; r < k; ++r)
+        if (r != c) {
+          const R f = C[r][c];
+          for (int q = 0; q < 3; ++q) { C[r][q] -= f * C[c][q]; Ci[r][q] -= f * Ci[c][q]; }
+        }
+    }
+    // V over 4 chunk elements (0..3 at the start = window 0..3; 28..31 at the end = window 60..63)
+    const int w0 = (e == 0) ? 0 : 60;
+    for (int j = 0; j < 3; ++j)
+      for (int q = 0; q < 4; ++q) V[cs][j][q] = 0.0;
+    for (const Ent& x : E) {
+      const int j = (int)(std::find(rows.begin(), rows.end(), x.row) - rows.begin());
+      V[cs][j][x.col - w0] += (double)x.v;
+    }
+    // M = W C^{-1} on the end chunk
+    const int c0 = (e == 0) ? 0 : 32;
+    for (int i = 0; i < 32; ++i)
+      for (int j = 0; j < 3; ++j) {
+        R acc = 0;
+        for (int q = 0; q < k; ++q) acc += W[q][c0 + i] * Ci[q][j];
+        Mx[cs][i][j] = (j < k) ? (double)acc : 0.0;
+      }
+  }
+}
+
 // ---- constants: MFD closures as the printed rationals (App. B), CFD interior LU
 int init_constants(adi_ctx* h) {
   if (g_const_ready) return ADI_OK;
@@ -239,6 +319,13 @@ int init_constants(adi_ctx* h) {
     CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_sK, sK, sizeof sK));
     CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_sJ, sJ, sizeof sJ));
     CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_sF, &sF, sizeof sF));
+  }
+  // line-end corrections of the lean CFD tiles (adi_line.cuh, c_wbV / c_wbM)
+  {
+    double V[6][3][4], Mx[6][32][3];
+    wb_setup(l, invd, V, Mx);
+    CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_wbV, V, sizeof V));
+    CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_wbM, Mx, sizeof Mx));
   }
   g_const_ready = true;
   return ADI_OK;
@@ -305,8 +392,9 @@ bool plan_axis(adi::Axis& A, int method, int nlmin, int cap) {
       g.out_hi = hi;
       if (s == 0) { g.start = 0; g.nchunks = (hi + halo + M - 1) / M; }
       else if (s == S - 1) {
-        // end the last chunk at n (or n+1, one dead position, to keep the start even)
-        g.nchunks = (P - lo + halo + M - 1) / M;
+        // end the last chunk at n (or n+1, one dead position, to keep the start even);
+        // with the full chunk count the line end sits in chunk 31 (lean end tile)
+        g.nchunks = (CH == adi::TCH) ? CH : (P - lo + halo + M - 1) / M;
         g.start = P - g.nchunks * M;
         if (g.start & 1) g.start += 1;
         if (g.start > lo - halo) { g.nchunks += 1; g.start -= M; }
@@ -351,6 +439,9 @@ int setup_axis(adi_ctx* h, adi::Axis& A, int n, int nlines, int nlmin) {
     if (!cfd_table(n, true, tu, dev, plo_u) || !cfd_table(n, false, tx, dev, plo_x))
       return fail(h, ADI_EZEROPIVOT, "zero pivot in the LU of P or P-bar");
     A.plo = std::max(std::max(plo_u, plo_x), 2);
+    // edge tiles stage the LU tables of positions within 64 of a line end (adi_line.cuh)
+    if (n >= 64 && A.plo > 32)
+      return fail(h, ADI_EINVAL, "CFD LU pivots do not converge near the line ends");
     A.phi = n - 2;
     CUDA_TRY(h, cudaMalloc(&A.d_tabU, tu.size() * sizeof(double)));
     CUDA_TRY(h, cudaMalloc(&A.d_tabX, tx.size() * sizeof(double)));
@@ -360,11 +451,23 @@ int setup_axis(adi_ctx* h, adi::Axis& A, int n, int nlines, int nlmin) {
     A.plo = 2;
     A.phi = n - 2;
   }
-  for (adi::Seg& g : A.segs)
-    // lean (interior) tile: every ACTIVE chunk is interior.  The lean kernel also
-    // runs the chunks beyond nchunks on the (finite) data past the segment; they
-    // only move the truncation boundary further from the owned range.
-    g.edge = !(g.nchunks > 0 && g.start >= A.plo && g.start + g.nchunks * adi::TM - 1 <= A.phi);
+  for (adi::Seg& g : A.segs) {
+    // Lean tiles: the active chunks avoid the end rows (positions
+    // 0, 1 and n-1, n), or the segment starts at the line start, or the line end
+    // sits in chunk 31.  The lean kernel also runs the chunks beyond nchunks on the
+    // (finite) data past the segment; they only move the truncation boundary further
+    // from the owned range.  Everything else (short lines) takes the generic kernel.
+    const int last = g.start + g.nchunks * adi::TM - 1;
+    const int full = g.start + adi::TCH * adi::TM - 1;
+    g.edge = 0;
+    g.end = 0;
+    if (g.nchunks <= 0) g.edge = 1;
+    else if (g.start >= 2 && last <= n - 2) g.end = 0;
+    else if (g.start == 0 && last <= n - 2) g.end = 1;
+    else if (g.nchunks == adi::TCH && g.start >= 2 && full == n) g.end = 2;
+    else if (g.nchunks == adi::TCH && g.start >= 2 && full == n + 1) g.end = 3;
+    else g.edge = 1;
+  }
   std::stable_partition(A.segs.begin(), A.segs.end(), [](const adi::Seg& g) { return g.edge == 0; });
   A.nint = 0;
   for (const adi::Seg& g : A.segs) A.nint += (g.edge == 0);

@@ -94,6 +94,16 @@ def test_parity_default_tiling_large(adi, method):
 
 
 @pytest.mark.parametrize("method", [CFD, MFD])
+@pytest.mark.parametrize("n", [1601, 1602, 2100, 2101])
+def test_parity_lean_line_ends(adi, method, n):
+    """Lean tiles at the line ends: the first segment starts at the
+    line start, the last ends at position n (even n+1 - 1024) or n+1 (odd); closures
+    (MFD) and the rank <= 3 end corrections of the constant-pivot solve (CFD)."""
+    p = random_problem(method, n, seed=7 * n, steps=2)
+    assert_parity(run_gpu(adi, p, 2), run_oracle(p, 2), what=f"n={n}")
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
 @pytest.mark.parametrize("K", [1, 2, 8, 13])
 def test_parity_sweeps(adi, method, K):
     p = random_problem(method, 29, seed=K, steps=2)
