@@ -126,8 +126,40 @@ __constant__ double c_sF;
 // Case = system (0: u-op P̄, 1: x-op P) * 3 + end (0 start, 1 end at n, 2 end at
 // n+1); V acts on 4 chunk elements (0..3 at the start, 28..31 at the end), M on the
 // 32 elements of the end chunk (T*^{-1} U decays like (2-sqrt 3)^d).
+// M is applied as its exact entries on the 4 elements next to the end rows (c_wbN)
+// and, further in, as a geometric tail: M[i][j] = c_wbF[j] * rho^d, d = distance
+// from the line end, rho = -l* (c_rho[d] = rho^d; checked on the host to ~1e-18).
 __constant__ double c_wbV[6][3][4];
-__constant__ double c_wbM[6][32][3];
+__constant__ double c_wbN[6][4][3];
+__constant__ double c_wbF[6][3];
+__constant__ double c_rho[32];
+
+// V^T z of the end correction (zz: z on the 4 elements next to the end rows)
+template <int CS>
+__device__ __forceinline__ void wb_g(const double (&zz)[4], double& g0, double& g1, double& g2) {
+  g0 = 0.0; g1 = 0.0; g2 = 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    g0 = fma(c_wbV[CS][0][q], zz[q], g0);
+    g1 = fma(c_wbV[CS][1][q], zz[q], g1);
+    g2 = fma(c_wbV[CS][2][q], zz[q], g2);
+  }
+}
+// out += coef * M g on the end chunk (out = B - coef z, z <- z - M g)
+template <int CS, bool START, int M>
+__device__ __forceinline__ void wb_apply(double (&out)[M], double coef, double g0, double g1, double g2) {
+  const double ck = coef * fma(c_wbF[CS][2], g2, fma(c_wbF[CS][1], g1, c_wbF[CS][0] * g0));
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = START ? q : M - 4 + q;
+    out[i] = fma(coef, fma(c_wbN[CS][q][2], g2, fma(c_wbN[CS][q][1], g1, c_wbN[CS][q][0] * g0)), out[i]);
+  }
+#pragma unroll
+  for (int q = 4; q < M; ++q) {
+    const int i = START ? q : M - 1 - q;
+    out[i] = fma(ck, c_rho[q], out[i]);
+  }
+}
 enum { ST_F = 0, ST_KS = 1, ST_KE = 2, ST_JS = 3, ST_JE = 4 };  // CFD chunk statics
 
 template <int M>
@@ -627,22 +659,19 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
       zcT[j] = fma(c_sJ[0], zcT[j + 1], fma(c_sK[0], ycT[j + 1], iv * out[(j + 1) * L]));
     z0 = fma(c_sJ[0], zcT[0], fma(c_sK[0], ycT[0], iv * out[0]));
     double g0 = 0.0, g1 = 0.0, g2 = 0.0;  // V^T z of the line-end correction
-    const int wc = (UOP ? 0 : 3) + (c.endc < 0 ? 0 : c.endc);
+    constexpr int C0 = UOP ? 0 : 3;
     if (!EDGE && c.me) {
       double zz[4];
       if (c.endc == 0) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) zz[q] = fma(c_sJ[q], zcT[0], fma(c_sK[q], ycT[0], iv * out[q]));
+        wb_g<C0>(zz, g0, g1, g2);
       } else {
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           zz[q] = fma(c_sJ[L - 4 + q], zcT[NSUB - 1], fma(c_sK[L - 4 + q], ycT[NSUB - 1], iv * out[M - 4 + q]));
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        g0 = fma(c_wbV[wc][0][q], zz[q], g0);
-        g1 = fma(c_wbV[wc][1][q], zz[q], g1);
-        g2 = fma(c_wbV[wc][2][q], zz[q], g2);
+        if (c.endc == 1) wb_g<C0 + 1>(zz, g0, g1, g2);
+        else wb_g<C0 + 2>(zz, g0, g1, g2);
       }
     }
     const double ci = coef * iv;
@@ -654,9 +683,9 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
         out[j * L + i] = fma(-c_sJ[i], cz, fma(-c_sK[i], cy, fma(-ci, out[j * L + i], B[j * L + i])));
     }
     if (!EDGE && c.me) {
-#pragma unroll
-      for (int i = 0; i < M; ++i)
-        out[i] = fma(coef, fma(c_wbM[wc][i][2], g2, fma(c_wbM[wc][i][1], g1, c_wbM[wc][i][0] * g0)), out[i]);
+      if (c.endc == 0) wb_apply<C0, true, M>(out, coef, g0, g1, g2);
+      else if (c.endc == 1) wb_apply<C0 + 1, false, M>(out, coef, g0, g1, g2);
+      else wb_apply<C0 + 2, false, M>(out, coef, g0, g1, g2);
       // positions outside the system hold the Dirichlet slots (u-op) or nothing
       if (UOP) {
         if (c.endc == 0) out[0] = c.gL;
@@ -702,7 +731,10 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
 // Occupancy targets (resident CTAs per SM) for the NW-warp CTAs.
 template <int METHOD, bool EDGE>
 struct Occ {
-  static constexpr int value = (METHOD == M_MFD || !EDGE) ? 3 : 2;
+#ifndef ADI_CFD_OCC
+#define ADI_CFD_OCC 2
+#endif
+  static constexpr int value = (METHOD == M_MFD) ? 3 : ADI_CFD_OCC;
 };
 
 __host__ __device__ constexpr int PADM_OF(int M) { return M + 2; }

@@ -322,10 +322,30 @@ int init_constants(adi_ctx* h) {
   }
   // line-end corrections of the lean CFD tiles (adi_line.cuh, c_wbV / c_wbM)
   {
-    double V[6][3][4], Mx[6][32][3];
+    double V[6][3][4], Mx[6][32][3], N[6][4][3], F[6][3], rho[32];
     wb_setup(l, invd, V, Mx);
+    // near entries exact; the rest as the geometric tail F_j rho^d (d = distance
+    // from the line end) -- T*^{-1} e_r is geometric away from the rows
+    rho[0] = 1.0;
+    for (int q = 1; q < 32; ++q) rho[q] = rho[q - 1] * (-l);
+    for (int cs = 0; cs < 6; ++cs) {
+      const bool start = (cs % 3) == 0;
+      for (int q = 0; q < 4; ++q)
+        for (int j = 0; j < 3; ++j) N[cs][q][j] = Mx[cs][start ? q : 28 + q][j];
+      for (int j = 0; j < 3; ++j) {
+        F[cs][j] = Mx[cs][start ? 4 : 27][j] / rho[4];
+        double mx = 0.0, err = 0.0;
+        for (int i = 0; i < 32; ++i) mx = std::max(mx, std::fabs(Mx[cs][i][j]));
+        for (int q = 4; q < 32; ++q)
+          err = std::max(err, std::fabs(F[cs][j] * rho[q] - Mx[cs][start ? q : 31 - q][j]));
+        if (mx > 0 && err > 1e-15 * mx)
+          return fail(h, ADI_ECUDA, "internal: line-end correction is not geometric");
+      }
+    }
     CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_wbV, V, sizeof V));
-    CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_wbM, Mx, sizeof Mx));
+    CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_wbN, N, sizeof N));
+    CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_wbF, F, sizeof F));
+    CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_rho, rho, sizeof rho));
   }
   g_const_ready = true;
   return ADI_OK;
