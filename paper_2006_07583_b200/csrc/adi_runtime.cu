@@ -8,7 +8,7 @@
 //                 }   the last COL is FINAL   -> U^{m+n}, W̄^{m+n}
 //                 EDGE          : Dirichlet columns of U at t^{m+n}
 //
-// Every arithmetic step runs in the kernels of adi_kernels.cuh.  The host only
+// Every arithmetic step runs in the kernels of adi_line.cuh.  The host only
 // computes the operator coefficient tables (exact rationals of the paper, LU
 // without pivoting — PAPER.md:113,192) and scalar time factors.
 #include <cuda_runtime.h>
