@@ -732,9 +732,11 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
 template <int METHOD, bool EDGE>
 struct Occ {
 #ifndef ADI_CFD_OCC
-#define ADI_CFD_OCC 2
+#define ADI_CFD_OCC 3
 #endif
-  static constexpr int value = (METHOD == M_MFD) ? 3 : ADI_CFD_OCC;
+  // 168 registers: MFD, and the lean CFD kernel (u_K parked in shared memory);
+  // the generic CFD kernel keeps 255 registers
+  static constexpr int value = (METHOD == M_MFD) ? 3 : (EDGE ? 2 : ADI_CFD_OCC);
 };
 
 __host__ __device__ constexpr int PADM_OF(int M) { return M + 2; }
@@ -930,6 +932,25 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     }
   };
 
+  // dst = dst + dt/2 F in place (dst: S tile holding u_K or U); phi read from global,
+  // warmed in L2 at tile start (CFD: keeps one 32-point array live)
+  auto add_source_global = [&](double* dst) {
+    int ipt = -1;
+    if (P.pt_line && line == P.pt_line[b] && (!EDGE || c.live)) ipt = P.pt_pos[b] - c.s;
+    const double ptf = P.pt_amp * P.gf;
+    const double2* ph = reinterpret_cast<const double2*>(P.phi_src + (long long)line * P.s_line + c.s);
+#pragma unroll
+    for (int i = 0; i < M / 2; ++i) {
+      // (lines past the last row of a CTA group compute but store nothing: no read)
+      const double2 f2 = (want_phi && lineok) ? __ldg(ph + i) : make_double2(0.0, 0.0);
+      double f0 = f2.x * P.gf, f1 = f2.y * P.gf;
+      if (2 * i == ipt) f0 += ptf;
+      if (2 * i + 1 == ipt) f1 += ptf;
+      dst[2 * i] = fma(P.half_dt, f0, dst[2 * i]);
+      dst[2 * i + 1] = fma(P.half_dt, f1, dst[2 * i + 1]);
+    }
+  };
+
   if (METHOD == M_CFD) {
     // ---------------- CFD ----------------
     const int np1 = n + 1;
@@ -953,23 +974,38 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     warp_edges<M>(lane, x, d0, xm1, xp1, d1);
     warp_edges<M>(lane, u, d0, um1, up1, d1);
     if (MODE == KM_PROLOGUE) {
+      // at most two 32-point arrays live: U stays in the S tile, W is re-read from
+      // the X tile, W* is staged for output before the u-op
       double e1, e2;
-      double wv[M];
-#pragma unroll
-      for (int i = 0; i < M; ++i) wv[i] = x[i];
-      stage_phi();
       cfd_apply<M, false, EDGE>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, 0.0, 0.0, e1, e2);
-      add_source(Sm, u);
+      add_source_global(Sm);   // S = U + dt/2 F
+      double wv[M];
+      {
+        double2* V2 = reinterpret_cast<double2*>(Vm);
+#pragma unroll
+        for (int i = 0; i < M / 2; ++i) {
+          const double2 v = V2[i];
+          wv[2 * i] = v.x;
+          wv[2 * i + 1] = v.y;
+          V2[i] = make_double2(x[2 * i], x[2 * i + 1]);
+        }
+      }
       cfd_apply<M, true, EDGE>(c, P, lane, stU, etab, wv, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
     } else {
       for (int k = 0; k < P.K; ++k) {
         cfd_apply<M, true, EDGE>(c, P, lane, stU, etab, x, Sm, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
-        if (MODE == KM_SWEEP && k + 1 == P.K) stage_phi();
+        if (k + 1 == P.K) {
+          // park u_K in the (now dead) S tile: u is then dead across every x-op,
+          // which keeps one 32-point array live instead of two (no spills at 3 CTAs/SM)
+          double2* S2 = reinterpret_cast<double2*>(Sm);
+#pragma unroll
+          for (int i = 0; i < M / 2; ++i) S2[i] = make_double2(u[2 * i], u[2 * i + 1]);
+        }
         cfd_apply<M, false, EDGE>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, VFn, VLp, xm1, xp1);
       }
       if (MODE == KM_SWEEP) {
         double e1, e2;
-        add_source(Sm, u);
+        add_source_global(Sm);   // S = u_K + dt/2 F
         cfd_apply<M, true, EDGE>(c, P, lane, stU, etab, x, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
 #pragma unroll
         for (int i = 0; i < M; ++i) x[i] = fma(2.0, x[i], -Vm[i]);
@@ -995,13 +1031,22 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       if (!EDGE && c.me) mfd_end_x<M>(c, u, B, x, bx);
     };
     if (MODE == KM_PROLOGUE) {
+      // at most two 32-point arrays live (as for CFD): U stays in the S tile, W is
+      // re-read from the X tile, W* is staged for output before the u-op
+      x_op(Vm);                 // W* = W - beta D(U)
+      add_source_global(Sm);    // S = U + dt/2 F
       double wv[M];
+      {
+        double2* V2 = reinterpret_cast<double2*>(Vm);
 #pragma unroll
-      for (int i = 0; i < M; ++i) wv[i] = x[i];
-      stage_phi();
-      x_op(Vm);            // W* = W - beta D(U)
-      add_source(Sm, u);   // S = U + dt/2 F
-      u_op(wv, Sm);        // S1 = S - alpha D̄(W)
+        for (int i = 0; i < M / 2; ++i) {
+          const double2 v = V2[i];
+          wv[2 * i] = v.x;
+          wv[2 * i + 1] = v.y;
+          V2[i] = make_double2(x[2 * i], x[2 * i + 1]);
+        }
+      }
+      u_op(wv, Sm);             // S1 = S - alpha D̄(W)
     } else {
       for (int k = 0; k < P.K; ++k) {
         u_op(x, Sm);
@@ -1018,19 +1063,19 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   }
   if (tr) tr2 = gtimer();
 
-  // ---- stage the outputs in the tile (own chunk)
+  // ---- stage the outputs in the tile (own chunk); the CFD FINAL u_K is already parked
   double acc = 0.0;
   {
     double2* S2 = reinterpret_cast<double2*>(Sm);
     double2* V2 = reinterpret_cast<double2*>(Vm);
 #pragma unroll
     for (int i = 0; i < M / 2; ++i) {
-      S2[i] = make_double2(u[2 * i], u[2 * i + 1]);
-      V2[i] = make_double2(x[2 * i], x[2 * i + 1]);
+      if (!(METHOD == M_CFD && MODE == KM_FINAL)) S2[i] = make_double2(u[2 * i], u[2 * i + 1]);
+      if (MODE != KM_PROLOGUE) V2[i] = make_double2(x[2 * i], x[2 * i + 1]);
     }
     if (P.flag && lineok && (!EDGE || c.live)) {
 #pragma unroll
-      for (int i = 0; i < M; ++i) acc += u[i] + x[i];
+      for (int i = 0; i < M; ++i) acc += Sm[i] + Vm[i];
     }
   }
   __syncthreads();

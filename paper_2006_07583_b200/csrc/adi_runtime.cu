@@ -200,22 +200,26 @@ void wb_setup(double l, double iv, double V[6][3][4], double Mx[6][32][3]) {
   struct Ent { int row, col; R v; };
   for (int cs = 0; cs < 6; ++cs) {
     const int sys = cs / 3, e = cs % 3;  // sys 0: u-op (P̄), 1: x-op (P)
-    std::vector<Ent> E;
+    Ent E[8];
+    int ne = 0;
+    auto put = [&](int r, int c, R v) { E[ne++] = Ent{r, c, v}; };
     if (e == 0) {
-      if (sys == 0) E = {{0, 0, 1 - dd}, {0, 1, -1}, {1, 0, -a}, {1, 1, 6 - b}, {1, 2, 5}};
-      else E = {{0, 0, 6 - dd}, {0, 1, 17}};
+      if (sys == 0) { put(0, 0, 1 - dd); put(0, 1, -1); put(1, 0, -a); put(1, 1, 6 - b); put(1, 2, 5); }
+      else { put(0, 0, 6 - dd); put(0, 1, 17); }
     } else if (e == 1) {  // position n = window 63
-      if (sys == 0) E = {{62, 61, 6 - a}, {62, 62, 6 - b}, {62, 63, -1}, {63, 62, -a}, {63, 63, 1 - b}};
-      else E = {{63, 62, 18 - a}, {63, 63, 6 - b}};
+      if (sys == 0) { put(62, 61, 6 - a); put(62, 62, 6 - b); put(62, 63, -1); put(63, 62, -a); put(63, 63, 1 - b); }
+      else { put(63, 62, 18 - a); put(63, 63, 6 - b); }
     } else {              // position n+1 = window 63 (dead)
-      if (sys == 0)
-        E = {{61, 60, 6 - a}, {61, 61, 6 - b}, {61, 62, -1}, {62, 61, -a}, {62, 62, 1 - b}, {62, 63, -1},
-             {63, 62, -a}, {63, 63, 1 - b}};
-      else E = {{62, 61, 18 - a}, {62, 62, 6 - b}, {62, 63, -1}, {63, 62, -a}, {63, 63, 1 - b}};
+      if (sys == 0) {
+        put(61, 60, 6 - a); put(61, 61, 6 - b); put(61, 62, -1); put(62, 61, -a); put(62, 62, 1 - b);
+        put(62, 63, -1); put(63, 62, -a); put(63, 63, 1 - b);
+      } else {
+        put(62, 61, 18 - a); put(62, 62, 6 - b); put(62, 63, -1); put(63, 62, -a); put(63, 63, 1 - b);
+      }
     }
     std::vector<int> rows;
-    for (const Ent& x : E)
-      if (std::find(rows.begin(), rows.end(), x.row) == rows.end()) rows.push_back(x.row);
+    for (int q = 0; q < ne; ++q)
+      if (std::find(rows.begin(), rows.end(), E[q].row) == rows.end()) rows.push_back(E[q].row);
     const int k = (int)rows.size();
     // W_j = T*^{-1} e_{rows[j]} on the window
     R W[3][64] = {};
@@ -230,7 +234,8 @@ void wb_setup(double l, double iv, double V[6][3][4], double Mx[6][32][3]) {
     // C = I + V^T W, its inverse (k <= 3, Gauss-Jordan)
     R C[3][3] = {}, Ci[3][3] = {};
     for (int j = 0; j < 3; ++j) { C[j][j] = 1; Ci[j][j] = 1; }
-    for (const Ent& x : E) {
+    for (int t = 0; t < ne; ++t) {
+      const Ent& x = E[t];
       const int j = (int)(std::find(rows.begin(), rows.end(), x.row) - rows.begin());
       for (int q = 0; q < k; ++q) C[j][q] += x.v * W[q][x.col];
     }
@@ -251,7 +256,8 @@ void wb_setup(double l, double iv, double V[6][3][4], double Mx[6][32][3]) {
     const int w0 = (e == 0) ? 0 : 60;
     for (int j = 0; j < 3; ++j)
       for (int q = 0; q < 4; ++q) V[cs][j][q] = 0.0;
-    for (const Ent& x : E) {
+    for (int t = 0; t < ne; ++t) {
+      const Ent& x = E[t];
       const int j = (int)(std::find(rows.begin(), rows.end(), x.row) - rows.begin());
       V[cs][j][x.col - w0] += (double)x.v;
     }
