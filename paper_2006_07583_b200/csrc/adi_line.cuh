@@ -828,14 +828,20 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   }
   __syncwarp();  // the barrier is initialised before any lane waits on it
   if (MODE == KM_PROLOGUE) {
-    // U is read across its rows (stride u_pt): 8-byte cp.async with zero fill
-    const double* Ul = P.U_in + (long long)b * P.u_batch + (long long)line * P.u_line;
-    const bool lv = lineok && lane < sg.nchunks;
+    // U is read across its rows (stride u_pt), cooperatively by the CTA: thread e
+    // takes line e&3 at segment position e>>2, so one warp instruction reads 8 rows
+    // x 4 consecutive lines = 8 full 32-byte sectors (8-byte cp.async, zero fill)
+    const double* Ub = P.U_in + (long long)b * P.u_batch;
+    const int lg0 = P.line0 + blockIdx.x * NW;
 #pragma unroll 4
-    for (int i = 0; i < M; ++i) {
-      const int p = c.s + i;
-      const bool xin = lv && p >= 0 && p <= n;
-      cp_async8(lS + lane * PADM + i, xin ? Ul + (long long)p * P.u_pt : P.X_in, xin);
+    for (int k = 0; k < 32 * M * NW / NT; ++k) {
+      const int e = t + NT * k;
+      const int wl = e % NW, pos = e / NW;
+      const int ln = lg0 + wl;
+      const int p = sg.start + pos;
+      const bool in = ln >= P.line_lo && ln < P.nlines && (!EDGE || pos < sg.nchunks * M) && p >= 0 && p <= n;
+      cp_async8(stS + wl * LSTR + (pos / M) * PADM + pos % M,
+                in ? Ub + (long long)p * P.u_pt + (long long)ln * P.u_line : P.X_in, in);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   }
@@ -871,7 +877,10 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
         "r"(0), "r"(c1), "r"(c2), "r"(line), "r"(0)
         : "memory");
   }
-  if (MODE == KM_PROLOGUE) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  if (MODE == KM_PROLOGUE) {
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();  // the U gather filled every warp's tile
+  }
   mbar_wait(wbar, wpar);
   wpar ^= 1u;
   __syncwarp();
