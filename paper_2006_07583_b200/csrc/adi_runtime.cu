@@ -390,46 +390,55 @@ bool cfd_table(int n, bool bar, std::vector<double>& tab, double& maxdev_lo, int
   return true;
 }
 
-// ---- tile planning along one axis
-bool plan_axis(adi::Axis& A, int method, int nlmin, int cap) {
-  (void)nlmin;
+// ---- tile planning along one axis.  The owned positions
+// [lo_all, hi_all) (the whole line, or a band of the decomposition, §7) are split
+// evenly into S segments; a segment's tile covers its part plus `halo` on each
+// side, except at a line end, where the tile contains the end itself (exact).
+bool plan_axis(adi::Axis& A, int method, int cap, int lo_all, int hi_all) {
   const int M = adi::TM;
   const int chmax = cap > 0 ? std::min(cap, adi::TCH) : adi::TCH;
   const int P = A.n + 1;                       // positions 0..n
   const int halo = (method == ADI_CFD) ? 64 : 32;
   A.halo = halo;
   A.segs.clear();
-  // Chunk starts are kept even (16-byte aligned rows for the bulk copies).
+  lo_all = std::max(lo_all, 0);
+  hi_all = std::min(hi_all, P);
+  // Chunk starts are kept even (16-byte aligned rows for the TMA copies).
   const int D = (M - P % M) % M;
   const int nch1 = (P + D) / M;
-  if (nch1 <= chmax) {
+  if (nch1 <= chmax) {  // the whole line in one tile
     const int ds = (D / 2) & ~1;   // dead positions before 0 (even); the rest after n
-    A.segs.push_back({-ds, nch1, 0, P, 1});
+    A.segs.push_back({-ds, nch1, lo_all, hi_all, 1});
     return true;
   }
   const int CH = chmax;
-  for (int S = 2; S <= P / M; ++S) {
+  const int R = hi_all - lo_all;
+  if (R <= 0) return true;
+  for (int S = 1; S <= R / 2 + 1; ++S) {
     std::vector<adi::Seg> segs;
     bool fits = true;
-    for (int s = 0; s < S; ++s) {
-      const int lo = (int)((long long)s * P / S), hi = (int)((long long)(s + 1) * P / S);
-      adi::Seg g;
+    for (int s = 0; s < S && fits; ++s) {
+      const int lo = lo_all + (int)((long long)s * R / S), hi = lo_all + (int)((long long)(s + 1) * R / S);
+      const int a = lo - halo, e = hi + halo;   // positions the tile must hold
+      adi::Seg g{};
       g.out_lo = lo;
       g.out_hi = hi;
-      if (s == 0) { g.start = 0; g.nchunks = (hi + halo + M - 1) / M; }
-      else if (s == S - 1) {
+      if (a <= 0 && e >= P) { fits = false; break; }      // would need the whole line
+      if (a <= 0) {                                       // holds the line start
+        g.start = 0;
+        g.nchunks = (e + M - 1) / M;
+      } else if (e >= P) {                                // holds the line end
         // end the last chunk at n (or n+1, one dead position, to keep the start even);
         // with the full chunk count the line end sits in chunk 31 (lean end tile)
-        g.nchunks = (CH == adi::TCH) ? CH : (P - lo + halo + M - 1) / M;
+        g.nchunks = (CH == adi::TCH) ? CH : (P - a + M - 1) / M;
         g.start = P - g.nchunks * M;
         if (g.start & 1) g.start += 1;
-        if (g.start > lo - halo) { g.nchunks += 1; g.start -= M; }
+        if (g.start > a) { g.nchunks += 1; g.start -= M; }
+        if (g.start < 1) { fits = false; break; }
       } else {
-        g.start = (lo - halo) & ~1;
-        g.nchunks = (hi - g.start + halo + M - 1) / M;
+        g.start = a & ~1;
+        g.nchunks = (e - g.start + M - 1) / M;
       }
-      // only the first tile may contain the line start, only the last the line end
-      if ((s > 0 && g.start < 1) || (s < S - 1 && g.start + g.nchunks * M > P - 1)) return false;
       if (g.nchunks > CH) fits = false;
       segs.push_back(g);
     }
@@ -442,16 +451,14 @@ int setup_axis(adi_ctx* h, adi::Axis& A, int n, int nlines, int nlmin) {
   A.n = n;
   A.nlines = nlines;
   if (A.l1 == 0 && A.l0 == 0) { A.l0 = 1; A.l1 = nlines + 1; }  // lines are positions 1..nlines
-  if (!plan_axis(A, h->method, nlmin, h->tile_chunks))
+  (void)nlmin;
+  // the owned positions: the whole line, or this handle's band (adi_set_band)
+  if (!plan_axis(A, h->method, h->tile_chunks, A.o0, A.o1))
     return fail(h, ADI_EINVAL, "tile planning failed (grid too small for the tile cap)");
-  // band decomposition: keep only the segments that output positions in [o0, o1)
   {
     std::vector<adi::Seg> keep;
-    for (adi::Seg g : A.segs) {
-      g.out_lo = std::max(g.out_lo, A.o0);
-      g.out_hi = std::min(g.out_hi, A.o1);
+    for (adi::Seg g : A.segs)
       if (g.out_lo < g.out_hi) keep.push_back(g);
-    }
     A.segs = keep;
     if (A.segs.empty()) A.segs.push_back({0, 0, 0, 0, 1});  // nothing to output: an idle tile
   }

@@ -34,7 +34,8 @@ def make_group(adi, p, world, **kw):
 
 
 @pytest.mark.parametrize("method", [CFD, MFD])
-@pytest.mark.parametrize("n,world,split", [(301, 2, [3]), (517, 3, [2, 2]), (1601, 4, [1, 1])])
+@pytest.mark.parametrize("n,world,split", [(301, 2, [3]), (517, 3, [2, 2]), (1601, 4, [1, 1]),
+                                            (2101, 8, [2])])
 def test_band_group_equals_single_and_oracle(adi, method, n, world, split):
     steps = sum(split)
     p = random_problem(method, n, seed=n + world, steps=steps)
