@@ -122,7 +122,10 @@ int adi_set_param(adi_handle h, int key, double value);
  * NULL = the legacy default stream). */
 int adi_set_stream(adi_handle h, void* cuda_stream);
 
-/* Set the state at the current time from HOST arrays (shapes above, times batch). */
+/* Set the state at the current time from HOST arrays (shapes above, times batch).
+ * With a band set (adi_set_band) only the rows the band uses are read: y positions
+ * [y0 - halo, y1 + halo) of U and W̄ and the V̄ rows of those positions; the other
+ * rows of the arrays are not accessed.  ESTATE while a call is in progress. */
 int adi_set_fields(adi_handle h, const double* U, const double* V, const double* W);
 /* Same from DEVICE arrays (contiguous, same shapes). */
 int adi_set_fields_device(adi_handle h, const double* dU, const double* dV, const double* dW);
@@ -165,7 +168,8 @@ int adi_step_end(adi_handle h);
  * grid (0 <= y0 < y1 <= number of y positions): its row sweep processes the
  * interior rows inside the band, its column sweep outputs only positions in
  * the band.  Every handle still holds full-size arrays; only its band (plus
- * halo) is kept current.  Between adi_step_rows and adi_step_cols the halo of
+ * halo) is kept current, and adi_set/get_fields move only those rows.  The
+ * column sweep plans its tiles over the band's own positions.  Between adi_step_rows and adi_step_cols the halo of
  * `halo` positions on each side must be refreshed from the neighbour bands
  * (kind 0: S2 and W*), and before adi_step_begin of every call but the first
  * after adi_set_fields (kind 1: U and W̄).  side 0 = low-y neighbour, 1 = high.
@@ -178,7 +182,9 @@ int adi_halo_bytes(adi_handle h, int kind, int side, size_t* bytes);
 int adi_halo_pack(adi_handle h, int kind, int side, void* dev_buf);
 int adi_halo_unpack(adi_handle h, int kind, int side, const void* dev_buf);
 
-/* Copy the state to HOST arrays (synchronizes the stream). */
+/* Copy the state to HOST arrays (synchronizes the stream).  With a band set only
+ * the band's rows [y0, y1) are written (the top band also writes the U rows above
+ * its last position); the other rows of the arrays are left untouched. */
 int adi_get_fields(adi_handle h, double* U, double* V, double* W);
 /* Copy the state to DEVICE arrays, enqueued on the handle's stream. */
 int adi_get_fields_device(adi_handle h, double* dU, double* dV, double* dW);

@@ -800,25 +800,48 @@ int adi_set_stream(adi_handle h, void* s) {
   return ADI_OK;
 }
 
+// Rows moved by adi_set/get_fields: all of them, or, with a band set (§7), the y
+// positions this handle uses: [y0 - halo, y1 + halo) on set (the first half-step
+// of a call reads the halo rows of U and W̄), [y0, y1) on get.  Rows of the U block
+// beyond the last band position (MFD: position n+1) belong to the top band.
+static void field_rows(adi_ctx* h, bool with_halo, int* ya, int* yb) {
+  const int npos = h->ay.n + 1;
+  const bool banded = h->band_y0 > 0 || h->band_y1 < npos;
+  if (!banded) { *ya = 0; *yb = h->nyu; return; }
+  const int hl = with_halo ? h->ay.halo : 0;
+  *ya = std::max(h->band_y0 - hl, 0);
+  *yb = (h->band_y1 >= npos) ? h->nyu : std::min(h->band_y1 + hl, h->nyu);
+}
+
 static int set_fields_impl(adi_handle h, const double* U, const double* V, const double* W,
                            cudaMemcpyKind kind) {
   if (!h) return ADI_EINVAL;
   h->err.clear();
   if (!U || !V || !W) return fail(h, ADI_EINVAL, "null field pointer");
+  if (h->in_call) return fail(h, ADI_ESTATE, "call in progress");
   const size_t B = (size_t)h->batch;
+  int ya, yb;
+  field_rows(h, true, &ya, &yb);
+  const int ja = std::max(ya - 1, 0), jb = std::min(yb - 1, h->nyi);   // V̄ row j = y position j + 1
+  const int wa = std::min(ya, h->nyv), wb = std::min(yb, h->nyv);      // W̄ rows are y positions
   // user layouts are dense; internal rows are pitched (batch strides aU, aV, aW)
   for (size_t b = 0; b < B; ++b) {
-    CUDA_TRY(h, cudaMemcpy2DAsync(h->U + b * h->aU, h->pu * 8, U + b * h->nU, h->nxu * 8, h->nxu * 8,
-                                  h->nyu, kind, h->stream));
-    // V̄ row j is the y position j + 1
-    CUDA_TRY(h, cudaMemcpy2DAsync(h->V + b * h->aV + h->pv, h->pv * 8, V + b * h->nV, h->nxv * 8,
-                                  h->nxv * 8, h->nyi, kind, h->stream));
+    CUDA_TRY(h, cudaMemcpy2DAsync(h->U + b * h->aU + (size_t)ya * h->pu, h->pu * 8,
+                                  U + b * h->nU + (size_t)ya * h->nxu, h->nxu * 8, h->nxu * 8, yb - ya, kind,
+                                  h->stream));
+    if (jb > ja)
+      CUDA_TRY(h, cudaMemcpy2DAsync(h->V + b * h->aV + (size_t)(ja + 1) * h->pv, h->pv * 8,
+                                    V + b * h->nV + (size_t)ja * h->nxv, h->nxv * 8, h->nxv * 8, jb - ja, kind,
+                                    h->stream));
+    // W̄ rows [wa, wb) (dense) -> internal W̄^T (row = x position i + 1, column = y)
+    // via the W2 scratch buffer
+    if (wb > wa) {
+      CUDA_TRY(h, cudaMemcpyAsync(h->W2, W + b * h->nW + (size_t)wa * h->nxi, (size_t)(wb - wa) * h->nxi * 8,
+                                  kind, h->stream));
+      int rc = transpose(h, h->W2, h->W + b * h->aW + h->pw + wa, wb - wa, h->nxi, h->nxi, h->pw, 1, 0, 0);
+      if (rc) return rc;
+    }
   }
-  // W̄ (ny x nxi, dense) -> internal W̄^T (row = x position i + 1) via the W2 scratch buffer
-  CUDA_TRY(h, cudaMemcpyAsync(h->W2, W, B * h->nW * 8, kind, h->stream));
-  int rc = transpose(h, h->W2, h->W + h->pw, h->nyv, h->nxi, h->nxi, h->pw, h->batch, (long long)h->nW,
-                     (long long)h->aW);
-  if (rc) return rc;
   if (kind == cudaMemcpyHostToDevice) CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   h->fields_set = true;
   return ADI_OK;
@@ -1146,18 +1169,28 @@ static int get_fields_impl(adi_handle h, double* U, double* V, double* W, cudaMe
   if (!h) return ADI_EINVAL;
   h->err.clear();
   if (!U || !V || !W) return fail(h, ADI_EINVAL, "null field pointer");
+  if (h->in_call) return fail(h, ADI_ESTATE, "call in progress");
   const size_t B = (size_t)h->batch;
+  int ya, yb;
+  field_rows(h, false, &ya, &yb);
+  const int ja = std::max(ya - 1, 0), jb = std::min(yb - 1, h->nyi);
+  const int wa = std::min(ya, h->nyv), wb = std::min(yb, h->nyv);
   for (size_t b = 0; b < B; ++b) {
-    CUDA_TRY(h, cudaMemcpy2DAsync(U + b * h->nU, h->nxu * 8, h->U + b * h->aU, h->pu * 8, h->nxu * 8,
-                                  h->nyu, kind, h->stream));
-    CUDA_TRY(h, cudaMemcpy2DAsync(V + b * h->nV, h->nxv * 8, h->V + b * h->aV + h->pv, h->pv * 8,
-                                  h->nxv * 8, h->nyi, kind, h->stream));
+    CUDA_TRY(h, cudaMemcpy2DAsync(U + b * h->nU + (size_t)ya * h->nxu, h->nxu * 8,
+                                  h->U + b * h->aU + (size_t)ya * h->pu, h->pu * 8, h->nxu * 8, yb - ya, kind,
+                                  h->stream));
+    if (jb > ja)
+      CUDA_TRY(h, cudaMemcpy2DAsync(V + b * h->nV + (size_t)ja * h->nxv, h->nxv * 8,
+                                    h->V + b * h->aV + (size_t)(ja + 1) * h->pv, h->pv * 8, h->nxv * 8, jb - ja,
+                                    kind, h->stream));
+    // internal W̄^T (columns [wa, wb)) -> W̄ rows via the W2 scratch buffer
+    if (wb > wa) {
+      int rc = transpose(h, h->W + b * h->aW + h->pw + wa, h->W2, h->nxi, wb - wa, h->pw, h->nxi, 1, 0, 0);
+      if (rc) return rc;
+      CUDA_TRY(h, cudaMemcpyAsync(W + b * h->nW + (size_t)wa * h->nxi, h->W2, (size_t)(wb - wa) * h->nxi * 8,
+                                  kind, h->stream));
+    }
   }
-  // internal W̄^T -> W̄ via the W2 scratch buffer
-  int rc = transpose(h, h->W + h->pw, h->W2, h->nxi, h->nyv, h->pw, h->nxi, h->batch, (long long)h->aW,
-                     (long long)h->nW);
-  if (rc) return rc;
-  CUDA_TRY(h, cudaMemcpyAsync(W, h->W2, B * h->nW * 8, kind, h->stream));
   if (kind == cudaMemcpyDeviceToHost) CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   return ADI_OK;
 }
