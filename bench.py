@@ -280,30 +280,59 @@ def run_ours(a, ws, rank, local):
             "avg_launch_ms": round(dominant["avg_ms"], 4)}
     # ---- end to end through the C-ABI with host buffers (pinned), copies timed
     e2e = None
-    if not a.no_e2e:
+    if not a.no_e2e and ws == 1:
+        # One GPU: both problems through the async C-ABI calls, each handle on its own
+        # stream, so the copies of one overlap the steps of the other (and H2D / D2H
+        # overlap each other).  Pinned host buffers; one host wait at the end.
+        from adi_inputs import shapes
+        bufs, streams = {}, {}
+        bi = bo = 0
+        for m, (s, p, bs) in solvers.items():
+            su, sv, sw = shapes(m, n, n)
+            hU = torch.from_numpy(p.U).pin_memory()
+            hV = torch.zeros(sv, dtype=torch.float64).pin_memory()
+            hW = torch.zeros(sw, dtype=torch.float64).pin_memory()
+            oU, oV, oW = (torch.empty_like(x).pin_memory() for x in (hU, hV, hW))
+            bufs[m] = [x.numpy() for x in (hU, hV, hW, oU, oV, oW)] + [hU, hV, hW, oU, oV, oW]
+            streams[m] = torch.cuda.Stream()
+            adi.adi_set_stream(s.handle, streams[m].cuda_stream)
+            nb = (hU.numel() + hV.numel() + hW.numel()) * 8
+            bi += nb / a.steps
+            bo += nb / a.steps
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for m, (s, p, bs) in solvers.items():
+            hU, hV, hW, oU, oV, oW = bufs[m][:6]
+            adi.adi_set_fields_async(s.handle, hU, hV, hW)   # H2D, enqueued
+            s.step(a.steps)
+            adi.adi_get_fields_async(s.handle, oU, oV, oW)   # D2H, enqueued
+        for m in solvers:
+            streams[m].synchronize()
+        t1 = time.perf_counter()
+        e2e_ms = (t1 - t0) * 1e3
+        for m, (s, p, bs) in solvers.items():
+            adi.adi_set_stream(s.handle, stream.cuda_stream)
+        bufs = None
+        e2e = {"value": pts * a.steps * len(methods) / (e2e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo),
+               "note": "adi_set_fields_async(pinned host) + adi_step(K) + adi_get_fields_async(pinned host) "
+                       "per method, the two methods on two streams (copies overlap the other "
+                       "method's steps), host wall clock from the first copy to the last result"}
+    elif not a.no_e2e:
         e2e_ms = 0.0
         bi = bo = 0
         for m, (s, p, bs) in solvers.items():
             from adi_inputs import shapes
             su, sv, sw = shapes(m, n, n)
-            if ws == 1:
-                # one GPU: full fields in pinned host memory
-                hU = torch.from_numpy(p.U).pin_memory()
-                hV = torch.zeros(sv, dtype=torch.float64).pin_memory()
-                hW = torch.zeros(sw, dtype=torch.float64).pin_memory()
-                oU, oV, oW = (torch.empty_like(x).pin_memory() for x in (hU, hV, hW))
-                hU, hV, hW, oU, oV, oW = (x.numpy() for x in (hU, hV, hW, oU, oV, oW))
-                nbi = nbo = (hU.size + hV.size + hW.size) * 8
-            else:
-                # a band: full-size host arrays whose pages outside the band are never
-                # touched (lazily zeroed); the library moves only the band's rows
-                hU, hV, hW, oU, oV, oW = (np.zeros(sh) for sh in (su, sv, sw, su, sv, sw))
-                ya, yb = p.rows
-                hU[ya:yb] = p.U
-                nrow = lambda shp, a0, b0: max(min(b0, shp[0]) - max(a0, 0), 0) * shp[1] * 8
-                nbi = nrow(su, ya, yb) + nrow(sv, ya - 1, yb - 1) + nrow(sw, ya, yb)
-                ga, gb = bs.y0, (su[0] if bs.y1 >= bs.npos else bs.y1)
-                nbo = nrow(su, ga, gb) + nrow(sv, ga - 1, gb - 1) + nrow(sw, ga, gb)
+            # a band: full-size host arrays whose pages outside the band are never
+            # touched (lazily zeroed); the library moves only the band's rows
+            hU, hV, hW, oU, oV, oW = (np.zeros(sh) for sh in (su, sv, sw, su, sv, sw))
+            ya, yb = p.rows
+            hU[ya:yb] = p.U
+            nrow = lambda shp, a0, b0: max(min(b0, shp[0]) - max(a0, 0), 0) * shp[1] * 8
+            nbi = nrow(su, ya, yb) + nrow(sv, ya - 1, yb - 1) + nrow(sw, ya, yb)
+            ga, gb = bs.y0, (su[0] if bs.y1 >= bs.npos else bs.y1)
+            nbo = nrow(su, ga, gb) + nrow(sv, ga - 1, gb - 1) + nrow(sw, ga, gb)
             barrier(ws)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -320,9 +349,8 @@ def run_ours(a, ws, rank, local):
             del hU, hV, hW, oU, oV, oW
         e2e = {"value": pts * a.steps * len(methods) / (e2e_ms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo),
-               "note": "adi_set_fields(host) + adi_step(K) + adi_get_fields(host), pinned buffers"
-                       + ("" if ws == 1 else "; per rank, the band's rows (pageable), max over ranks; "
-                                              "bytes per step of rank 0")}
+               "note": "adi_set_fields(host) + adi_step(K) + adi_get_fields(host) per method; per rank "
+                       "the band's rows (pageable), max over ranks; bytes per step of rank 0"}
     for s, _, _ in solvers.values():
         s.close()
     return {"value": value, "ms_per_step": total_ms / a.steps, "roofline": roof, "clocks": clocks,

@@ -182,6 +182,15 @@ int adi_halo_bytes(adi_handle h, int kind, int side, size_t* bytes);
 int adi_halo_pack(adi_handle h, int kind, int side, void* dev_buf);
 int adi_halo_unpack(adi_handle h, int kind, int side, const void* dev_buf);
 
+/* Asynchronous forms of adi_set_fields / adi_get_fields: the copies (and the
+ * W̄ transposes) are only ENQUEUED on the handle's stream, in order with the
+ * handle's steps.  The host arrays should be page-locked (cudaHostAlloc /
+ * cudaHostRegister) for the copies to overlap other work; they must stay valid
+ * and, for the set, unmodified until the stream has been synchronized.  Same
+ * shapes, band rule and errors as the synchronous calls. */
+int adi_set_fields_async(adi_handle h, const double* U, const double* V, const double* W);
+int adi_get_fields_async(adi_handle h, double* U, double* V, double* W);
+
 /* Copy the state to HOST arrays (synchronizes the stream).  With a band set only
  * the band's rows [y0, y1) are written (the top band also writes the U rows above
  * its last position); the other rows of the arrays are left untouched. */

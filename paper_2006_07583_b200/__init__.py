@@ -69,6 +69,8 @@ def lib():
         L.adi_set_stream.argtypes = [H, P]
         L.adi_set_fields.argtypes = [H, P, P, P]
         L.adi_set_fields_device.argtypes = [H, P, P, P]
+        L.adi_set_fields_async.argtypes = [H, P, P, P]
+        L.adi_get_fields_async.argtypes = [H, P, P, P]
         L.adi_set_source.argtypes = [H, P, I, I, P, I]
         L.adi_set_point_sources.argtypes = [H, P, P, P, I]
         L.adi_set_boundary.argtypes = [H, P, P, I]
@@ -100,7 +102,7 @@ EXPORTS = ["adi_create", "adi_create_batch", "adi_set_param", "adi_set_stream", 
            "adi_set_fields_device", "adi_set_source", "adi_set_point_sources", "adi_set_boundary",
            "adi_step", "adi_step_begin", "adi_step_rows", "adi_step_cols", "adi_step_end", "adi_set_band",
            "adi_band_info", "adi_halo_bytes", "adi_halo_pack", "adi_halo_unpack",
-           "adi_get_fields", "adi_get_fields_device", "adi_get_stats", "adi_get_kernel_times",
+           "adi_get_fields", "adi_get_fields_device", "adi_set_fields_async", "adi_get_fields_async", "adi_get_stats", "adi_get_kernel_times",
            "adi_set_trace", "adi_last_error",
            "adi_destroy", "adi_version"]
 
@@ -147,6 +149,27 @@ def adi_set_stream(hd, stream_ptr):
 def adi_set_fields(hd, U, V, W):
     U, V, W = _host(U), _host(V), _host(W)
     return _check(hd, lib().adi_set_fields(hd, _ptr(U), _ptr(V), _ptr(W)), "adi_set_fields")
+
+
+def _pinned_host(a, what):
+    # async copies read/write the caller's buffer later: no temporary copies allowed
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]):
+        raise ValueError(f"{what}: async transfers need C-contiguous float64 numpy arrays "
+                         "(page-locked memory, e.g. torch.empty(...).pin_memory().numpy())")
+    return a
+
+
+def adi_set_fields_async(hd, U, V, W):
+    """Enqueue the host->device copy of (U, V̄, W̄) on the handle's stream (buffers must
+    stay valid and unmodified until the stream is synchronized)."""
+    U, V, W = (_pinned_host(x, "adi_set_fields_async") for x in (U, V, W))
+    return _check(hd, lib().adi_set_fields_async(hd, _ptr(U), _ptr(V), _ptr(W)), "adi_set_fields_async")
+
+
+def adi_get_fields_async(hd, U, V, W):
+    """Enqueue the device->host copy of the state into (U, V̄, W̄) on the handle's stream."""
+    U, V, W = (_pinned_host(x, "adi_get_fields_async") for x in (U, V, W))
+    return _check(hd, lib().adi_get_fields_async(hd, _ptr(U), _ptr(V), _ptr(W)), "adi_get_fields_async")
 
 
 def adi_set_fields_device(hd, dU, dV, dW):

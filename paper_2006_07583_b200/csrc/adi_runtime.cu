@@ -120,6 +120,15 @@ int fail(adi_ctx* h, int code, const std::string& msg) {
       return fail((h), ADI_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
   } while (0)
 
+// Host -> device copies of set-up data.  They go on the handle's stream and are
+// waited for: a plain cudaMemcpy from pageable memory may return before the DMA
+// lands, and a non-blocking user stream would not wait for the legacy stream.
+#define H2D_SYNC(h, dst, src, bytes)                                                             \
+  do {                                                                                           \
+    CUDA_TRY((h), cudaMemcpyAsync((dst), (src), (bytes), cudaMemcpyHostToDevice, (h)->stream)); \
+    CUDA_TRY((h), cudaStreamSynchronize((h)->stream));                                           \
+  } while (0)
+
 // ---- device arrays read by the line kernels' TMA copies carry guard regions
 // (adi_line.cuh: a staged row may start TMA_P0 positions before a line and end
 // past the last line); allocations are zeroed.
@@ -127,7 +136,10 @@ double* dalloc(size_t n) {
   void* raw = nullptr;
   const size_t tot = (n + adi::BUF_GUARD_FRONT + adi::BUF_GUARD_TAIL) * sizeof(double);
   if (cudaMalloc(&raw, tot) != cudaSuccess) { cudaGetLastError(); return nullptr; }
-  if (cudaMemset(raw, 0, tot) != cudaSuccess) { cudaGetLastError(); cudaFree(raw); return nullptr; }
+  // zeroed synchronously: later work may run on a non-blocking stream
+  if (cudaMemset(raw, 0, tot) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+    cudaGetLastError(); cudaFree(raw); return nullptr;
+  }
   return static_cast<double*>(raw) + adi::BUF_GUARD_FRONT;
 }
 void dfree(double* p) {
@@ -478,8 +490,8 @@ int setup_axis(adi_ctx* h, adi::Axis& A, int n, int nlines, int nlmin) {
     A.phi = n - 2;
     CUDA_TRY(h, cudaMalloc(&A.d_tabU, tu.size() * sizeof(double)));
     CUDA_TRY(h, cudaMalloc(&A.d_tabX, tx.size() * sizeof(double)));
-    CUDA_TRY(h, cudaMemcpy(A.d_tabU, tu.data(), tu.size() * sizeof(double), cudaMemcpyHostToDevice));
-    CUDA_TRY(h, cudaMemcpy(A.d_tabX, tx.data(), tx.size() * sizeof(double), cudaMemcpyHostToDevice));
+    H2D_SYNC(h, A.d_tabU, tu.data(), tu.size() * sizeof(double));
+    H2D_SYNC(h, A.d_tabX, tx.data(), tx.size() * sizeof(double));
   } else {
     A.plo = 2;
     A.phi = n - 2;
@@ -505,8 +517,7 @@ int setup_axis(adi_ctx* h, adi::Axis& A, int n, int nlines, int nlmin) {
   A.nint = 0;
   for (const adi::Seg& g : A.segs) A.nint += (g.edge == 0);
   CUDA_TRY(h, cudaMalloc(&A.d_segs, A.segs.size() * sizeof(adi::Seg)));
-  CUDA_TRY(h, cudaMemcpy(A.d_segs, A.segs.data(), A.segs.size() * sizeof(adi::Seg),
-                         cudaMemcpyHostToDevice));
+  H2D_SYNC(h, A.d_segs, A.segs.data(), A.segs.size() * sizeof(adi::Seg));
   return ADI_OK;
 }
 
@@ -796,6 +807,10 @@ int adi_set_param(adi_handle h, int key, double v) {
 
 int adi_set_stream(adi_handle h, void* s) {
   if (!h) return ADI_EINVAL;
+  h->err.clear();
+  if (h->in_call) return fail(h, ADI_ESTATE, "call in progress");
+  // work already enqueued on the previous stream finishes first
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   h->stream = (cudaStream_t)s;
   return ADI_OK;
 }
@@ -814,7 +829,7 @@ static void field_rows(adi_ctx* h, bool with_halo, int* ya, int* yb) {
 }
 
 static int set_fields_impl(adi_handle h, const double* U, const double* V, const double* W,
-                           cudaMemcpyKind kind) {
+                           cudaMemcpyKind kind, bool sync = true) {
   if (!h) return ADI_EINVAL;
   h->err.clear();
   if (!U || !V || !W) return fail(h, ADI_EINVAL, "null field pointer");
@@ -842,7 +857,7 @@ static int set_fields_impl(adi_handle h, const double* U, const double* V, const
       if (rc) return rc;
     }
   }
-  if (kind == cudaMemcpyHostToDevice) CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  if (kind == cudaMemcpyHostToDevice && sync) CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   h->fields_set = true;
   return ADI_OK;
 }
@@ -852,6 +867,9 @@ int adi_set_fields(adi_handle h, const double* U, const double* V, const double*
 }
 int adi_set_fields_device(adi_handle h, const double* U, const double* V, const double* W) {
   return set_fields_impl(h, U, V, W, cudaMemcpyDeviceToDevice);
+}
+int adi_set_fields_async(adi_handle h, const double* U, const double* V, const double* W) {
+  return set_fields_impl(h, U, V, W, cudaMemcpyHostToDevice, false);
 }
 
 static int set_points(adi_handle h, const int* ix, const int* iy) {
@@ -872,10 +890,10 @@ static int set_points(adi_handle h, const int* ix, const int* iy) {
       CUDA_TRY(h, cudaMalloc(&A->d_ptp, B * sizeof(int)));
     }
   }
-  CUDA_TRY(h, cudaMemcpy(h->ax.d_ptl, xl.data(), B * sizeof(int), cudaMemcpyHostToDevice));
-  CUDA_TRY(h, cudaMemcpy(h->ax.d_ptp, xp.data(), B * sizeof(int), cudaMemcpyHostToDevice));
-  CUDA_TRY(h, cudaMemcpy(h->ay.d_ptl, yl.data(), B * sizeof(int), cudaMemcpyHostToDevice));
-  CUDA_TRY(h, cudaMemcpy(h->ay.d_ptp, yp.data(), B * sizeof(int), cudaMemcpyHostToDevice));
+  H2D_SYNC(h, h->ax.d_ptl, xl.data(), B * sizeof(int));
+  H2D_SYNC(h, h->ax.d_ptp, xp.data(), B * sizeof(int));
+  H2D_SYNC(h, h->ay.d_ptl, yl.data(), B * sizeof(int));
+  H2D_SYNC(h, h->ay.d_ptp, yp.data(), B * sizeof(int));
   h->has_pt = true;
   return ADI_OK;
 }
@@ -891,11 +909,11 @@ int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double
       if (!h->phi && !(h->phi = dalloc(h->aS))) return fail(h, ADI_ENOMEM, "source pattern");
       if (!h->phiT && !(h->phiT = dalloc(h->aS))) return fail(h, ADI_ENOMEM, "source pattern");
     }
-    CUDA_TRY(h, cudaMemset(h->phi, 0, h->aS * 8));
-    CUDA_TRY(h, cudaMemset(h->phiT, 0, h->aS * 8));
+    CUDA_TRY(h, cudaMemsetAsync(h->phi, 0, h->aS * 8, h->stream));
+    CUDA_TRY(h, cudaMemsetAsync(h->phiT, 0, h->aS * 8, h->stream));
     // interior point (j, i) of the user's block is position (y, x) = (j + 1, i + 1)
-    CUDA_TRY(h, cudaMemcpy2D(h->phi + h->pa + 1, h->pa * 8, phi, h->nxi * 8, h->nxi * 8, h->nyi,
-                             cudaMemcpyHostToDevice));
+    CUDA_TRY(h, cudaMemcpy2DAsync(h->phi + h->pa + 1, h->pa * 8, phi, h->nxi * 8, h->nxi * 8, h->nyi,
+                                  cudaMemcpyHostToDevice, h->stream));
     int rc = transpose(h, h->phi + h->pa + 1, h->phiT + h->pb + 1, h->nyi, h->nxi, h->pa, h->pb, 1, 0, 0);
     if (rc) return rc;
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
@@ -932,7 +950,7 @@ int adi_set_boundary(adi_handle h, const double* edges, const double* g, int ng)
   const size_t ne = 2 * (size_t)h->nxu + 2 * (size_t)h->nyu;
   if (edges) {
     if (!h->edges) CUDA_TRY(h, cudaMalloc(&h->edges, ne * 8));
-    CUDA_TRY(h, cudaMemcpy(h->edges, edges, ne * 8, cudaMemcpyHostToDevice));
+    H2D_SYNC(h, h->edges, edges, ne * 8);
   } else if (h->edges) {
     cudaFree(h->edges);
     h->edges = nullptr;
@@ -1165,7 +1183,8 @@ int adi_band_info(adi_handle h, int* y0, int* y1, int* halo, int* npos) {
   return ADI_OK;
 }
 
-static int get_fields_impl(adi_handle h, double* U, double* V, double* W, cudaMemcpyKind kind) {
+static int get_fields_impl(adi_handle h, double* U, double* V, double* W, cudaMemcpyKind kind,
+                           bool sync = true) {
   if (!h) return ADI_EINVAL;
   h->err.clear();
   if (!U || !V || !W) return fail(h, ADI_EINVAL, "null field pointer");
@@ -1191,12 +1210,15 @@ static int get_fields_impl(adi_handle h, double* U, double* V, double* W, cudaMe
                                   kind, h->stream));
     }
   }
-  if (kind == cudaMemcpyDeviceToHost) CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  if (kind == cudaMemcpyDeviceToHost && sync) CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   return ADI_OK;
 }
 
 int adi_get_fields(adi_handle h, double* U, double* V, double* W) {
   return get_fields_impl(h, U, V, W, cudaMemcpyDeviceToHost);
+}
+int adi_get_fields_async(adi_handle h, double* U, double* V, double* W) {
+  return get_fields_impl(h, U, V, W, cudaMemcpyDeviceToHost, false);
 }
 int adi_get_fields_device(adi_handle h, double* U, double* V, double* W) {
   return get_fields_impl(h, U, V, W, cudaMemcpyDeviceToDevice);
