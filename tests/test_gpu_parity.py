@@ -246,3 +246,14 @@ def test_nonblocking_stream_equals_default(adi, method):
         s.close()
         for name, a, b in zip("UVW", got, ref):
             assert np.array_equal(a, b), name
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("method,steps", [(CFD, 50), (MFD, 100)])
+@pytest.mark.parametrize("k", [2, 9])
+def test_config3_parity(adi, method, steps, k):
+    """Γ = k ∈ {2, 9} (polynomial part of S, boundary S|∂Ω cos ωt,
+    dense source with the polynomial part), 1601² nodes, parity after 50 (CFD) / 100 (MFD)
+    steps against the oracle."""
+    p = mms_problem(method, 1601, MMS(gamma=float(k), k=k), steps=steps)
+    assert_parity(run_gpu(adi, p, steps), run_oracle(p, steps), what=f"config3 k={k}")
