@@ -996,7 +996,7 @@ int adi_step_rows(adi_handle h) {
   adi::KParams p = base_params(h, h->ax, false);
   p.S_in = h->Sa; p.S_out = h->Sb;
   p.X_in = h->Vcur; p.X_out = h->Valt;
-  p.gb = tabv(h->gb, 2 * m + 1);
+  p.gb = tabv(h->gb, 2 * m + 1);   // boundary values of the intermediate U* at t^m + dt/2 [G9]
   p.gf = tabv(h->gf, 2 * m + 2);
   int rc = launch(h, adi::KM_SWEEP, h->ax, p, ADI_KK_ROW);
   if (rc) return rc;
