@@ -42,7 +42,7 @@ def lib():
         I = ctypes.c_int
         P = ctypes.c_void_p
         _lib.or_run_flat.argtypes = [I, I, I, D, D, D, D, I, P, I, I, P, I, P, P, P, P, P, I,
-                                     P, P, P, I, I, I]
+                                     P, P, P, I, I, I, D, I, P, P]
         _lib.or_run_flat.restype = I
         _lib.or_apply_D.argtypes = [I, I, D, P, P]
         _lib.or_apply_Dbar.argtypes = [I, I, D, P, P]
@@ -81,8 +81,13 @@ def interior_shape(method: int, nx: int, ny: int):
 
 
 def run(method, nx, ny, h, dt, c, K, U, V, W, *, rho=1.0, phi=None, src=None, gf=None,
-        edges=None, gb=None, m0=0, nsteps=1, nthreads=0):
+        edges=None, gb=None, m0=0, nsteps=1, nthreads=0, eps=0.0, kmin=6, info=None):
     """Advance copies of (U, V̄, W̄) by ``nsteps`` ADI steps; returns new arrays.
+
+    ``eps`` > 0 applies the stopping rule of Alg. 3/4 (sweeps ``kmin``..K tested,
+    test_k = ||U_k - U_{k-1}||_F + ||V_k - V_{k-1}||_F over the stage); ``info``
+    (a dict) then receives "k" [nsteps, 2] (chosen sweeps, rows / columns) and
+    "tests" [nsteps, 2, K+1].
 
     ``edges`` = (y0, y1, x0, x1) boundary pattern on the U edges (or None for
     homogeneous Dirichlet); ``gf``/``gb`` are the source / boundary time
@@ -104,12 +109,17 @@ def run(method, nx, ny, h, dt, c, K, U, V, W, *, rho=1.0, phi=None, src=None, gf
         e = [_f64(x) for x in edges]
         assert e[0].size == su[1] and e[1].size == su[1] and e[2].size == su[0] and e[3].size == su[0]
     ix, iy = (-1, -1) if src is None else src
+    kch = np.zeros((max(nsteps, 1), 2), dtype=np.int32)
+    tests = np.zeros((max(nsteps, 1), 2, K + 1))
     rc = lib().or_run_flat(method, nx, ny, h, dt, c, rho, K, _p(phi), ix, iy, _p(gf),
                            0 if gf is None else gf.size, _p(e[0]), _p(e[1]), _p(e[2]), _p(e[3]),
                            _p(gb), 0 if gb is None else gb.size, _p(U), _p(V), _p(W), m0, nsteps,
-                           nthreads)
+                           nthreads, float(eps), int(kmin), _p(kch), _p(tests))
     if rc != 0:
         raise RuntimeError(f"oracle or_run failed: {rc}")
+    if info is not None:
+        info["k"] = kch[:nsteps]
+        info["tests"] = tests[:nsteps]
     return U, V, W
 
 

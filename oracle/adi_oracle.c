@@ -245,11 +245,57 @@ static void stage_line(const axis_t* a, int K, double alpha, double beta,
   }
 }
 
+/* The same iteration to kmax sweeps, recording for k = 2..kmax the squared
+ * changes du2[k] = sum_i (u_k - u_{k-1})^2, dv2[k] = sum_i (v_k - v_{k-1})^2 of
+ * this line (Alg. 3/4 "test"; the Frobenius norms of the
+ * whole matrices are the square roots of the sums over the lines). */
+static void stage_line_norms(const axis_t* a, int kmax, double alpha, double beta,
+                             const double* s, const double* v0, double gL, double gR,
+                             double* u, double* v, double* ub, double* tmp, double* uold,
+                             double* vold, double* du2, double* dv2) {
+  for (int i = 0; i < a->nv; ++i) v[i] = v0[i];
+  for (int k = 1; k <= kmax; ++k) {
+    for (int i = 0; i < a->nu; ++i) uold[i] = u[i];
+    for (int i = 0; i < a->nv; ++i) vold[i] = v[i];
+    axis_Dbar(a, v, tmp);
+    for (int i = 0; i < a->nu; ++i) u[i] = s[i] - alpha * tmp[i];
+    ub[0] = gL;
+    for (int i = 0; i < a->nu; ++i) ub[i + 1] = u[i];
+    ub[a->nub - 1] = gR;
+    axis_D(a, ub, tmp);
+    for (int i = 0; i < a->nv; ++i) v[i] = v0[i] - beta * tmp[i];
+    double su = 0.0, sv = 0.0;
+    if (k >= 2) {
+      for (int i = 0; i < a->nu; ++i) su += (u[i] - uold[i]) * (u[i] - uold[i]);
+      for (int i = 0; i < a->nv; ++i) sv += (v[i] - vold[i]) * (v[i] - vold[i]);
+    }
+    du2[k] = su;
+    dv2[k] = sv;
+  }
+}
+
+/* Alg. 3/4 stopping rule with the paper's GPU practice:
+ * sweeps k = kmin..kmax are tested, test_k = ||U_k - U_{k-1}||_F + ||V_k -
+ * V_{k-1}||_F over the whole stage (all lines); the stage stops at the first k
+ * with test_k <= eps, else at kmax. */
+static int pick_k(const double* su, const double* sv, int kmin, int kmax, double eps, double* tests) {
+  int ks = kmax;
+  for (int k = kmin; k <= kmax; ++k) {
+    const double t = sqrt(su[k]) + sqrt(sv[k]);
+    if (tests) tests[k] = t;
+    if (t <= eps && ks == kmax) ks = k;
+  }
+  return ks;
+}
+
 /* ------------------------------------------------------------------------ */
 /* Problem description (time tables sampled at half steps).      */
 /* ------------------------------------------------------------------------ */
 typedef struct {
   int method, nx, ny, K;
+  double eps; int kmin;          /* Alg. 3/4 stopping rule: eps > 0 tests sweeps kmin..K */
+  int* kchosen;                  /* if set: [2 * nsteps] chosen sweeps (rows, columns) */
+  double* tests;                 /* if set: [2 * nsteps][K + 1] test values (k >= kmin) */
   double h, dt, c, rho;
   const double* phi;  /* source pattern on pressure-interior points, or NULL */
   int src_ix, src_iy; /* point source (U-array indices), F = g_f / h^2; <0: none */
@@ -339,6 +385,38 @@ int or_run(const or_problem* p, double* U, double* Vb, double* Wb, int m0, int n
     }
 
     /* ---- a3 + a4: ADI-rows (line 11) then C and V^{m+1} (lines 12, 14) ---- */
+    int Kr = p->K;
+    if (p->eps > 0.0) {  /* stopping rule: pass 1 over all lines to K sweeps */
+      const int K1 = p->K + 1;
+      double* lu = (double*)calloc((size_t)nyi * K1 * 2, sizeof(double));
+      if (!lu) { free(S1); free(S2); free(Ws); axis_free(&ax); axis_free(&ay); return -2; }
+      double* lv = lu + (size_t)nyi * K1;
+#pragma omp parallel
+      {
+        double* buf = (double*)malloc(sizeof(double) * 8 * L);
+        double *u = buf, *v = buf + L, *ub = buf + 2 * L, *tmp = buf + 3 * L, *s = buf + 4 * L,
+               *v0 = buf + 5 * L, *uo = buf + 6 * L, *vo = buf + 7 * L;
+#pragma omp for schedule(static)
+        for (int jj = 0; jj < nyi; ++jj) {
+          const int j = jj + 1;
+          const double gL = (p->edges[2] ? p->edges[2][j] : 0.0) * gb_h;
+          const double gR = (p->edges[3] ? p->edges[3][j] : 0.0) * gb_h;
+          for (int i = 0; i < nxi; ++i) s[i] = S1[(size_t)jj * nxi + i];
+          for (int i = 0; i < nxv; ++i) v0[i] = Vb[(size_t)jj * nxv + i];
+          for (int i = 0; i < nxi; ++i) u[i] = 0.0;
+          stage_line_norms(&ax, p->K, alpha, beta, s, v0, gL, gR, u, v, ub, tmp, uo, vo,
+                           lu + (size_t)jj * K1, lv + (size_t)jj * K1);
+        }
+        free(buf);
+      }
+      double* su = (double*)calloc((size_t)K1 * 2, sizeof(double));
+      double* sv = su + K1;
+      for (int jj = 0; jj < nyi; ++jj)          /* sums in line order */
+        for (int k = 0; k < K1; ++k) { su[k] += lu[(size_t)jj * K1 + k]; sv[k] += lv[(size_t)jj * K1 + k]; }
+      Kr = pick_k(su, sv, p->kmin, p->K, p->eps, p->tests ? p->tests + (size_t)(2 * st) * K1 : NULL);
+      free(su); free(lu);
+    }
+    if (p->kchosen) p->kchosen[2 * st] = Kr;
 #pragma omp parallel
     {
       double* buf = (double*)malloc(sizeof(double) * 6 * L);
@@ -351,7 +429,7 @@ int or_run(const or_problem* p, double* U, double* Vb, double* Wb, int m0, int n
         const double gR = (p->edges[3] ? p->edges[3][j] : 0.0) * gb_h;
         for (int i = 0; i < nxi; ++i) s[i] = S1[(size_t)jj * nxi + i];
         for (int i = 0; i < nxv; ++i) v0[i] = Vb[(size_t)jj * nxv + i];
-        stage_line(&ax, p->K, alpha, beta, s, v0, gL, gR, u, v, ub, tmp);
+        stage_line(&ax, Kr, alpha, beta, s, v0, gL, gR, u, v, ub, tmp);
         /* C / S2 = U* - alpha D̄_x(V*) + dt/2 F^{m+1} */
         axis_Dbar(&ax, v, tmp);
         for (int i = 0; i < nxi; ++i)
@@ -368,6 +446,38 @@ int or_run(const or_problem* p, double* U, double* Vb, double* Wb, int m0, int n
     }
 
     /* ---- a6: ADI-columns (line 15), boundary at t^{m+1} ---- */
+    int Kc = p->K;
+    if (p->eps > 0.0) {  /* stopping rule: pass 1 over all columns to K sweeps */
+      const int K1 = p->K + 1;
+      double* lu = (double*)calloc((size_t)nxi * K1 * 2, sizeof(double));
+      if (!lu) { free(S1); free(S2); free(Ws); axis_free(&ax); axis_free(&ay); return -2; }
+      double* lw = lu + (size_t)nxi * K1;
+#pragma omp parallel
+      {
+        double* buf = (double*)malloc(sizeof(double) * 8 * L);
+        double *u = buf, *w = buf + L, *ub = buf + 2 * L, *tmp = buf + 3 * L, *s = buf + 4 * L,
+               *w0 = buf + 5 * L, *uo = buf + 6 * L, *wo = buf + 7 * L;
+#pragma omp for schedule(static)
+        for (int ii = 0; ii < nxi; ++ii) {
+          const int i = ii + 1;
+          const double gB = (p->edges[0] ? p->edges[0][i] : 0.0) * gb_1;
+          const double gT = (p->edges[1] ? p->edges[1][i] : 0.0) * gb_1;
+          for (int r = 0; r < nyi; ++r) s[r] = S2[(size_t)r * nxi + ii];
+          for (int r = 0; r < nyv; ++r) w0[r] = Ws[(size_t)r * nxi + ii];
+          for (int r = 0; r < nyi; ++r) u[r] = 0.0;
+          stage_line_norms(&ay, p->K, alpha, beta, s, w0, gB, gT, u, w, ub, tmp, uo, wo,
+                           lu + (size_t)ii * K1, lw + (size_t)ii * K1);
+        }
+        free(buf);
+      }
+      double* su = (double*)calloc((size_t)K1 * 2, sizeof(double));
+      double* sw = su + K1;
+      for (int ii = 0; ii < nxi; ++ii)
+        for (int k = 0; k < K1; ++k) { su[k] += lu[(size_t)ii * K1 + k]; sw[k] += lw[(size_t)ii * K1 + k]; }
+      Kc = pick_k(su, sw, p->kmin, p->K, p->eps, p->tests ? p->tests + (size_t)(2 * st + 1) * K1 : NULL);
+      free(su); free(lu);
+    }
+    if (p->kchosen) p->kchosen[2 * st + 1] = Kc;
 #pragma omp parallel
     {
       double* buf = (double*)malloc(sizeof(double) * 6 * L);
@@ -380,7 +490,7 @@ int or_run(const or_problem* p, double* U, double* Vb, double* Wb, int m0, int n
         const double gT = (p->edges[1] ? p->edges[1][i] : 0.0) * gb_1;
         for (int r = 0; r < nyi; ++r) s[r] = S2[(size_t)r * nxi + ii];
         for (int r = 0; r < nyv; ++r) w0[r] = Ws[(size_t)r * nxi + ii];
-        stage_line(&ay, p->K, alpha, beta, s, w0, gB, gT, u, w, ub, tmp);
+        stage_line(&ay, Kc, alpha, beta, s, w0, gB, gT, u, w, ub, tmp);
         for (int r = 0; r < nyi; ++r) U[(size_t)(r + 1) * nxu + i] = u[r];
         for (int r = 0; r < nyv; ++r) Wb[(size_t)r * nxi + ii] = w[r];
       }
@@ -406,9 +516,11 @@ int or_run_flat(int method, int nx, int ny, double h, double dt, double c, doubl
                 const double* phi, int src_ix, int src_iy, const double* gf, int ngf,
                 const double* ey0, const double* ey1, const double* ex0, const double* ex1,
                 const double* gb, int ngb, double* U, double* Vb, double* Wb, int m0,
-                int nsteps, int nthreads) {
+                int nsteps, int nthreads, double eps, int kmin, int* kchosen, double* tests) {
   or_problem p;
   p.method = method; p.nx = nx; p.ny = ny; p.K = K;
+  p.eps = eps; p.kmin = kmin; p.kchosen = kchosen; p.tests = tests;
+  if (eps > 0.0 && (kmin < 2 || kmin > K)) return -1;
   p.h = h; p.dt = dt; p.c = c; p.rho = rho;
   p.phi = phi; p.src_ix = src_ix; p.src_iy = src_iy;
   p.gf = gf; p.ngf = ngf;
