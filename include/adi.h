@@ -82,8 +82,16 @@ enum adi_param {
   ADI_CHECK_FINITE = 2, /* 1: adi_step synchronizes and checks for NaN/Inf; default 0 */
   ADI_TILE_CHUNKS = 3,  /* cap on chunks (16 points each) per line in one tile; 0 = auto.
                            Testing aid: forces the segmented (halo) tiling on small grids. */
-  ADI_TIMING = 4        /* 1: bracket every kernel launch with CUDA events on the handle's
+  ADI_TIMING = 4,       /* 1: bracket every kernel launch with CUDA events on the handle's
                            stream (read with adi_get_kernel_times); default 0 */
+  ADI_EPS = 5,          /* inner stopping rule of Alg. 3/4: 0 (default)
+                           = fixed ADI_K_SWEEPS sweeps [G10]; eps > 0 = each stage stops at the
+                           first sweep k in [ADI_K_MIN, ADI_K_SWEEPS] with
+                           ||U_k - U_{k-1}||_F + ||V_k - V_{k-1}||_F <= eps (Frobenius norms over
+                           the stage's whole interior pressure / velocity matrices), else at
+                           ADI_K_SWEEPS.  Costs one extra pass of the stage's sweeps; decided on
+                           the device (no host round trip).  Whole grid only (no band). */
+  ADI_K_MIN = 6         /* first sweep tested by the stopping rule; integer >= 2, default 6 */
 };
 
 /* Kernel kinds launched by adi_step (index of adi_get_kernel_times arrays). */
@@ -213,6 +221,10 @@ int adi_get_kernel_times(adi_handle h, double* ms, long long* launches, int nkin
  * records.  dev_buf is device memory owned by the caller and must hold 64 * cap bytes;
  * NULL turns tracing off.  EINVAL for cap < 0 or an unknown kind. */
 int adi_set_trace(adi_handle h, void* dev_buf, long long cap, int kind);
+
+/* Sweeps used by the last step's ADI-rows / ADI-columns stages (ADI_K_SWEEPS when
+ * ADI_EPS = 0).  Synchronizes the stream. */
+int adi_get_last_sweeps(adi_handle h, int* k_rows, int* k_cols);
 
 /* Message for the last error on this handle ("" if none); valid until the next call. */
 const char* adi_last_error(adi_handle h);

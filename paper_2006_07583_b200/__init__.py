@@ -34,6 +34,8 @@ ADI_RHO = 1
 ADI_CHECK_FINITE = 2
 ADI_TILE_CHUNKS = 3
 ADI_TIMING = 4
+ADI_EPS = 5
+ADI_K_MIN = 6
 KERNEL_KINDS = ("prologue", "row", "col", "final", "edge")
 
 _STATUS = {0: "ADI_OK", -1: "ADI_EINVAL", -2: "ADI_ENOMEM", -3: "ADI_ECUDA", -4: "ADI_EZEROPIVOT",
@@ -80,6 +82,7 @@ def lib():
         L.adi_get_stats.argtypes = [H, ctypes.POINTER(adi_stats)]
         L.adi_get_kernel_times.argtypes = [H, P, P, I]
         L.adi_set_trace.argtypes = [H, P, ctypes.c_longlong, I]
+        L.adi_get_last_sweeps.argtypes = [H, ctypes.POINTER(I), ctypes.POINTER(I)]
         for f in ("adi_step_begin",):
             getattr(L, f).argtypes = [H, I]
         for f in ("adi_step_rows", "adi_step_cols", "adi_step_end"):
@@ -103,7 +106,7 @@ EXPORTS = ["adi_create", "adi_create_batch", "adi_set_param", "adi_set_stream", 
            "adi_step", "adi_step_begin", "adi_step_rows", "adi_step_cols", "adi_step_end", "adi_set_band",
            "adi_band_info", "adi_halo_bytes", "adi_halo_pack", "adi_halo_unpack",
            "adi_get_fields", "adi_get_fields_device", "adi_set_fields_async", "adi_get_fields_async", "adi_get_stats", "adi_get_kernel_times",
-           "adi_set_trace", "adi_last_error",
+           "adi_set_trace", "adi_get_last_sweeps", "adi_last_error",
            "adi_destroy", "adi_version"]
 
 
@@ -259,6 +262,13 @@ def adi_set_trace(hd, buf, cap: int, kind: int):
     """Tile trace of one kernel kind into a device tensor of >= 8 * cap int64 (None: off)."""
     _check(hd, lib().adi_set_trace(hd, _ptr(buf) if buf is not None else None, int(cap), int(kind)),
            "adi_set_trace")
+
+
+def adi_get_last_sweeps(hd):
+    """(rows, columns) sweeps used by the last step's stages."""
+    kr, kc = ctypes.c_int(0), ctypes.c_int(0)
+    _check(hd, lib().adi_get_last_sweeps(hd, ctypes.byref(kr), ctypes.byref(kc)), "adi_get_last_sweeps")
+    return kr.value, kc.value
 
 
 def adi_get_kernel_times(hd):

@@ -37,7 +37,7 @@
 namespace adi {
 
 enum { M_CFD = 0, M_MFD = 1 };
-enum { KM_SWEEP = 0, KM_FINAL = 1, KM_PROLOGUE = 2 };
+enum { KM_SWEEP = 0, KM_FINAL = 1, KM_PROLOGUE = 2, KM_NORM = 3 };
 
 struct Seg {
   int start;    // line position of the first point of chunk 0 (may be < 0)
@@ -93,6 +93,12 @@ struct KParams {
   double mA, mB, mC, mD;  // MFD interior stencil: cu/24, 9cu/8, cx/24, 9cx/8
   double half_dt;
   int K;
+  // inner stopping rule (Alg. 3/4): the sweep count read from device memory when
+  // Kdev is set; KM_NORM accumulates per sweep s >= kmin the owned squared changes
+  // of u and x into norms[2 s], norms[2 s + 1]
+  const int* Kdev;
+  double* norms;
+  int kmin;
   // CFD per-position LU tables, 3 x (n+1): l, 1/d, c   (u-op: P̄, x-op: P)
   const double* tabU; const double* tabX;
   int* flag;        // if set: becomes 1 when a non-finite value is stored
@@ -729,14 +735,15 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
 }
 
 // Occupancy targets (resident CTAs per SM) for the NW-warp CTAs.
-template <int METHOD, bool EDGE>
+template <int METHOD, bool EDGE, int MODE>
 struct Occ {
 #ifndef ADI_CFD_OCC
 #define ADI_CFD_OCC 3
 #endif
   // 168 registers: MFD, and the lean CFD kernel (u_K parked in shared memory);
   // the generic CFD kernel keeps 255 registers
-  static constexpr int value = (METHOD == M_MFD) ? 3 : (EDGE ? 2 : ADI_CFD_OCC);
+  // (the norm pass of the stopping rule keeps the previous iterates: 255 registers)
+  static constexpr int value = (MODE == KM_NORM) ? 2 : (METHOD == M_MFD) ? 3 : (EDGE ? 2 : ADI_CFD_OCC);
 };
 
 __host__ __device__ constexpr int PADM_OF(int M) { return M + 2; }
@@ -868,7 +875,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       if (P.edgeR) c.gR = P.edgeR[line] * P.gb;
     }
   }
-  const bool want_phi = (MODE != KM_FINAL) && P.phi_src;
+  const bool want_phi = (MODE != KM_FINAL && MODE != KM_NORM) && P.phi_src;
+  const int KK = P.Kdev ? *P.Kdev : P.K;   // sweeps (the stopping rule's choice, if any)
   if (want_phi && lane == 0) {
     // the source pattern is staged late (after the last u-op): warm L2 now
     asm volatile(
@@ -960,6 +968,34 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     }
   };
 
+  // stopping rule (Alg. 3/4): this warp's share of
+  // ||u_s - u_{s-1}||^2 and ||x_s - x_{s-1}||^2 over its owned positions
+  auto norm_add = [&](int s_, const double (&un)[M], const double (&uo)[M], const double (&xn)[M],
+                      const double (&xo)[M]) {
+    double su = 0.0, sx = 0.0;
+    if (lineok && (!EDGE || c.live)) {
+      const int ua = max(sg.out_lo, 1), ub = min(sg.out_hi, uhi + 1);
+      const int xa = max(sg.out_lo, 0), xb = min(sg.out_hi, n + 1);
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        const int p = c.s + i;
+        const double du = (p >= ua && p < ub) ? un[i] - uo[i] : 0.0;
+        const double dx = (p >= xa && p < xb) ? xn[i] - xo[i] : 0.0;
+        su = fma(du, du, su);
+        sx = fma(dx, dx, sx);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      su += __shfl_xor_sync(0xffffffffu, su, o);
+      sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    }
+    if (lane == 0) {
+      atomicAdd(P.norms + 2 * s_, su);
+      atomicAdd(P.norms + 2 * s_ + 1, sx);
+    }
+  };
+
   if (METHOD == M_CFD) {
     // ---------------- CFD ----------------
     const int np1 = n + 1;
@@ -1000,10 +1036,19 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
         }
       }
       cfd_apply<M, true, EDGE>(c, P, lane, stU, etab, wv, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
-    } else {
-      for (int k = 0; k < P.K; ++k) {
+    } else if (MODE == KM_NORM) {
+      double uo[M], xo[M];
+      for (int s_ = 1; s_ <= KK; ++s_) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) { uo[i] = u[i]; xo[i] = x[i]; }
         cfd_apply<M, true, EDGE>(c, P, lane, stU, etab, x, Sm, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
-        if (k + 1 == P.K) {
+        cfd_apply<M, false, EDGE>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, VFn, VLp, xm1, xp1);
+        if (s_ >= P.kmin) norm_add(s_, u, uo, x, xo);
+      }
+    } else {
+      for (int k = 0; k < KK; ++k) {
+        cfd_apply<M, true, EDGE>(c, P, lane, stU, etab, x, Sm, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
+        if (k + 1 == KK) {
           // park u_K in the (now dead) S tile: u is then dead across every x-op,
           // which keeps one 32-point array live instead of two (no spills at 3 CTAs/SM)
           double2* S2 = reinterpret_cast<double2*>(Sm);
@@ -1056,10 +1101,19 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
         }
       }
       u_op(wv, Sm);             // S1 = S - alpha D̄(W)
-    } else {
-      for (int k = 0; k < P.K; ++k) {
+    } else if (MODE == KM_NORM) {
+      double uo[M], xo[M];
+      for (int s_ = 1; s_ <= KK; ++s_) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) { uo[i] = u[i]; xo[i] = x[i]; }
         u_op(x, Sm);
-        if (MODE == KM_SWEEP && k + 1 == P.K) stage_phi();
+        x_op(Vm);
+        if (s_ >= P.kmin) norm_add(s_, u, uo, x, xo);
+      }
+    } else {
+      for (int k = 0; k < KK; ++k) {
+        u_op(x, Sm);
+        if (MODE == KM_SWEEP && k + 1 == KK) stage_phi();
         x_op(Vm);
       }
       if (MODE == KM_SWEEP) {
@@ -1071,6 +1125,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     }
   }
   if (tr) tr2 = gtimer();
+  if (MODE == KM_NORM) return;   // the norm pass stores nothing (every thread returns here)
 
   // ---- stage the outputs in the tile (own chunk); the CFD FINAL u_K is already parked
   double acc = 0.0;
@@ -1154,7 +1209,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
 //   MODE = KM_PROLOGUE: U_in, X_in -> a2 (explicit half only)
 // ===========================================================================
 template <int METHOD, int M, int NW, int MODE, bool EDGE>
-__global__ void __launch_bounds__(32 * NW, (Occ<METHOD, EDGE>::value))
+__global__ void __launch_bounds__(32 * NW, (Occ<METHOD, EDGE, MODE>::value))
     adi_line_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(128) double smem_raw[];
   // TMA destinations need 128-byte alignment
@@ -1162,6 +1217,16 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD, EDGE>::value))
   double* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u) / 8u;
   const Seg sg = P.segs[blockIdx.y];
   line_tile<METHOD, M, NW, MODE, EDGE>(P, sg, smem);
+}
+
+// The stopping rule's choice for one stage: the first sweep s in [kmin, K] with
+// sqrt(norms[2s]) + sqrt(norms[2s+1]) <= eps, else K (Alg. 3/4 "until test <= eps
+// or k >= k_max").  One thread.
+__global__ void pick_sweeps_kernel(const double* norms, int K, int kmin, double eps, int* kout) {
+  int ks = K;
+  for (int s = kmin; s <= K; ++s)
+    if (sqrt(norms[2 * s]) + sqrt(norms[2 * s + 1]) <= eps) { ks = s; break; }
+  *kout = ks;
 }
 
 }  // namespace adi

@@ -55,6 +55,11 @@ struct adi_ctx {
   int check_finite = 0;
   int tile_chunks = 0;  // 0 = auto
   int timing = 0;
+  double eps = 0.0;      // ADI_EPS: inner stopping rule off (fixed K sweeps) when 0
+  int kmin = 6;          // ADI_K_MIN
+  double* d_norms = nullptr;  // [K+1][2] per-sweep squared changes of one stage
+  int d_norms_cap = 0;
+  int* d_k = nullptr;         // chosen sweeps: rows, columns of the last step
   unsigned long long* trace = nullptr;  // adi_set_trace
   long long trace_cap = 0;
   int trace_kind = -1;
@@ -589,10 +594,12 @@ int launch(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p0, int
   if (h->method == ADI_CFD) {
     if (mode == adi::KM_SWEEP) return launch_t<adi::M_CFD, adi::KM_SWEEP>(h, A, p);
     if (mode == adi::KM_FINAL) return launch_t<adi::M_CFD, adi::KM_FINAL>(h, A, p);
+    if (mode == adi::KM_NORM) return launch_t<adi::M_CFD, adi::KM_NORM>(h, A, p);
     return launch_t<adi::M_CFD, adi::KM_PROLOGUE>(h, A, p);
   }
   if (mode == adi::KM_SWEEP) return launch_t<adi::M_MFD, adi::KM_SWEEP>(h, A, p);
   if (mode == adi::KM_FINAL) return launch_t<adi::M_MFD, adi::KM_FINAL>(h, A, p);
+  if (mode == adi::KM_NORM) return launch_t<adi::M_MFD, adi::KM_NORM>(h, A, p);
   return launch_t<adi::M_MFD, adi::KM_PROLOGUE>(h, A, p);
 }
 
@@ -691,11 +698,28 @@ adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
   return p;
 }
 
+// Inner stopping rule for one stage (Alg. 3/4): a norm pass over all
+// tiles (K sweeps, no stores), then one thread picks the sweep count into d_k[which],
+// which the stage's own launch reads.  Everything stays on the handle's stream.
+int stop_rule(adi_ctx* h, const adi::Axis& A, adi::KParams p, int kind, int which) {
+  CUDA_TRY(h, cudaMemsetAsync(h->d_norms, 0, sizeof(double) * 2 * (h->K + 1), h->stream));
+  p.norms = h->d_norms;
+  p.kmin = h->kmin;
+  p.Kdev = nullptr;
+  p.K = h->K;
+  int rc = launch(h, adi::KM_NORM, A, p, kind);
+  if (rc) return rc;
+  adi::pick_sweeps_kernel<<<1, 1, 0, h->stream>>>(h->d_norms, h->K, h->kmin, h->eps, h->d_k + which);
+  CUDA_TRY(h, cudaGetLastError());
+  h->launches++;
+  return ADI_OK;
+}
+
 void free_ctx(adi_ctx* h) {
   for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
   for (double* q : {h->Ubase, h->V, h->W, h->V2, h->W2, h->Sa, h->Sb, h->phi, h->phiT}) dfree(q);
-  for (void* q : {(void*)h->edges, (void*)h->flag})
+  for (void* q : {(void*)h->edges, (void*)h->flag, (void*)h->d_norms, (void*)h->d_k})
     if (q) cudaFree(q);
   for (adi::Axis* A : {&h->ax, &h->ay})
     for (void* q : {(void*)A->d_segs, (void*)A->d_tabU, (void*)A->d_tabX, (void*)A->d_ptl,
@@ -793,6 +817,12 @@ int adi_set_param(adi_handle h, int key, double v) {
     h->check_finite = (v != 0);
   } else if (key == ADI_TIMING) {
     h->timing = (v != 0);
+  } else if (key == ADI_EPS) {
+    if (!(v >= 0) || !std::isfinite(v)) return fail(h, ADI_EINVAL, "eps must be finite and >= 0");
+    h->eps = v;
+  } else if (key == ADI_K_MIN) {
+    if (!(v >= 2) || v != std::floor(v) || v > 1000) return fail(h, ADI_EINVAL, "k_min must be an integer >= 2");
+    h->kmin = (int)v;
   } else if (key == ADI_TILE_CHUNKS) {
     if (!(v >= 0) || v != std::floor(v)) return fail(h, ADI_EINVAL, "tile chunks must be >= 0");
     h->tile_chunks = (int)v;
@@ -972,6 +1002,20 @@ int adi_step_begin(adi_handle h, int nsteps) {
     return fail(h, ADI_EINVAL, "source table too short for the requested steps");
   if (!h->gb.empty() && (long long)h->gb.size() < 2 * m1 + 1)
     return fail(h, ADI_EINVAL, "boundary table too short for the requested steps");
+  if (h->eps > 0.0) {
+    // the stopping rule tests norms of the whole grid: no band decomposition
+    if (h->band_y0 > 0 || h->band_y1 < h->ay.n + 1)
+      return fail(h, ADI_EINVAL, "the stopping rule (ADI_EPS > 0) needs the whole grid on one handle");
+    if (h->kmin > h->K) return fail(h, ADI_EINVAL, "ADI_K_MIN exceeds ADI_K_SWEEPS");
+    if (h->d_norms_cap < h->K + 1) {
+      if (h->d_norms) cudaFree(h->d_norms);
+      h->d_norms = nullptr;
+      h->d_norms_cap = 0;
+      CUDA_TRY(h, cudaMalloc(&h->d_norms, sizeof(double) * 2 * (h->K + 1)));
+      h->d_norms_cap = h->K + 1;
+    }
+    if (!h->d_k) CUDA_TRY(h, cudaMalloc(&h->d_k, 2 * sizeof(int)));
+  }
   int rc;
   // a2 (standalone once per call): S1 = U - alpha D̄_y W + dt/2 F(t^m), W* = W - beta D_y U
   {
@@ -998,7 +1042,12 @@ int adi_step_rows(adi_handle h) {
   p.X_in = h->Vcur; p.X_out = h->Valt;
   p.gb = tabv(h->gb, 2 * m + 1);   // boundary values of the intermediate U* at t^m + dt/2 [G9]
   p.gf = tabv(h->gf, 2 * m + 2);
-  int rc = launch(h, adi::KM_SWEEP, h->ax, p, ADI_KK_ROW);
+  int rc;
+  if (h->eps > 0.0) {
+    if ((rc = stop_rule(h, h->ax, p, ADI_KK_ROW, 0))) return rc;
+    p.Kdev = h->d_k;
+  }
+  rc = launch(h, adi::KM_SWEEP, h->ax, p, ADI_KK_ROW);
   if (rc) return rc;
   std::swap(h->Vcur, h->Valt);
   return ADI_OK;
@@ -1015,6 +1064,10 @@ int adi_step_cols(adi_handle h) {
   p.gb = tabv(h->gb, 2 * m + 2);
   p.gf = tabv(h->gf, 2 * m + 2);
   int rc;
+  if (h->eps > 0.0) {
+    if ((rc = stop_rule(h, h->ay, p, last ? ADI_KK_FINAL : ADI_KK_COL, 1))) return rc;
+    p.Kdev = h->d_k + 1;
+  }
   if (last) {  // write U^{m+1} and W̄^{m+1} into the canonical buffers
     p.U_out = h->U;
     p.X_out = (h->Wcur == h->W) ? h->W2 : h->W;
@@ -1222,6 +1275,19 @@ int adi_get_fields_async(adi_handle h, double* U, double* V, double* W) {
 }
 int adi_get_fields_device(adi_handle h, double* U, double* V, double* W) {
   return get_fields_impl(h, U, V, W, cudaMemcpyDeviceToDevice);
+}
+
+int adi_get_last_sweeps(adi_handle h, int* k_rows, int* k_cols) {
+  if (!h) return ADI_EINVAL;
+  h->err.clear();
+  int k[2] = {h->K, h->K};
+  if (h->eps > 0.0 && h->d_k && h->m > 0) {
+    CUDA_TRY(h, cudaMemcpyAsync(k, h->d_k, sizeof k, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  }
+  if (k_rows) *k_rows = k[0];
+  if (k_cols) *k_cols = k[1];
+  return ADI_OK;
 }
 
 int adi_get_stats(adi_handle h, adi_stats* s) {
