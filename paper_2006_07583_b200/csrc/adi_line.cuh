@@ -37,7 +37,10 @@
 namespace adi {
 
 enum { M_CFD = 0, M_MFD = 1 };
-enum { KM_SWEEP = 0, KM_FINAL = 1, KM_PROLOGUE = 2, KM_NORM = 3 };
+enum { KM_SWEEP = 0, KM_FINAL = 1, KM_PROLOGUE = 2,
+       // stopping-rule attempts: SWEEP / FINAL that also accumulate the last sweep's
+       // squared changes (Alg. 3/4 test) and exit at once when the stage is decided
+       KM_SWEEP_T = 4, KM_FINAL_T = 5 };
 
 struct Seg {
   int start;    // line position of the first point of chunk 0 (may be < 0)
@@ -93,12 +96,12 @@ struct KParams {
   double mA, mB, mC, mD;  // MFD interior stencil: cu/24, 9cu/8, cx/24, 9cx/8
   double half_dt;
   int K;
-  // inner stopping rule (Alg. 3/4): the sweep count read from device memory when
-  // Kdev is set; KM_NORM accumulates per sweep s >= kmin the owned squared changes
-  // of u and x into norms[2 s], norms[2 s + 1]
-  const int* Kdev;
+  // inner stopping rule (Alg. 3/4): an attempt (KM_*_T) runs K sweeps, adds the
+  // owned squared changes of u and x in its last sweep to norms[0], norms[1], and
+  // does nothing when *gate is set (the stage is already decided)
+  const int* Kdev;   // if set: the sweep count (else K)
   double* norms;
-  int kmin;
+  const int* gate;
   // CFD per-position LU tables, 3 x (n+1): l, 1/d, c   (u-op: P̄, x-op: P)
   const double* tabU; const double* tabX;
   int* flag;        // if set: becomes 1 when a non-finite value is stored
@@ -743,7 +746,8 @@ struct Occ {
   // 168 registers: MFD, and the lean CFD kernel (u_K parked in shared memory);
   // the generic CFD kernel keeps 255 registers
   // (the norm pass of the stopping rule keeps the previous iterates: 255 registers)
-  static constexpr int value = (MODE == KM_NORM) ? 2 : (METHOD == M_MFD) ? 3 : (EDGE ? 2 : ADI_CFD_OCC);
+  static constexpr int value = (MODE == KM_SWEEP_T || MODE == KM_FINAL_T) ? 2
+                               : (METHOD == M_MFD) ? 3 : (EDGE ? 2 : ADI_CFD_OCC);
 };
 
 __host__ __device__ constexpr int PADM_OF(int M) { return M + 2; }
@@ -774,8 +778,11 @@ __device__ __forceinline__ void tma_load_seg(double* dst, const CUtensorMap* tm,
 // are interior and live (the lean path, no generic closures, no per-chunk
 // predicates); EDGE = true: line ends, dead chunks, short lines.
 // ===========================================================================
-template <int METHOD, int M, int NW, int MODE, bool EDGE>
+template <int METHOD, int M, int NW, int MODE_, bool EDGE>
 __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, double* smem) {
+  // stopping-rule attempts are SWEEP / FINAL tiles with the last-sweep test
+  constexpr bool TEST = (MODE_ == KM_SWEEP_T || MODE_ == KM_FINAL_T);
+  constexpr int MODE = (MODE_ == KM_SWEEP_T) ? KM_SWEEP : (MODE_ == KM_FINAL_T) ? KM_FINAL : MODE_;
   constexpr int NT = 32 * NW;
   constexpr int PADM = PADM_OF(M);
   constexpr int LSTR = LSTR_OF(M);
@@ -875,7 +882,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       if (P.edgeR) c.gR = P.edgeR[line] * P.gb;
     }
   }
-  const bool want_phi = (MODE != KM_FINAL && MODE != KM_NORM) && P.phi_src;
+  const bool want_phi = (MODE != KM_FINAL) && P.phi_src;
   const int KK = P.Kdev ? *P.Kdev : P.K;   // sweeps (the stopping rule's choice, if any)
   if (want_phi && lane == 0) {
     // the source pattern is staged late (after the last u-op): warm L2 now
@@ -970,7 +977,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
 
   // stopping rule (Alg. 3/4): this warp's share of
   // ||u_s - u_{s-1}||^2 and ||x_s - x_{s-1}||^2 over its owned positions
-  auto norm_add = [&](int s_, const double (&un)[M], const double (&uo)[M], const double (&xn)[M],
+  auto norm_add = [&](const double (&un)[M], const double (&uo)[M], const double (&xn)[M],
                       const double (&xo)[M]) {
     double su = 0.0, sx = 0.0;
     if (lineok && (!EDGE || c.live)) {
@@ -991,8 +998,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       sx += __shfl_xor_sync(0xffffffffu, sx, o);
     }
     if (lane == 0) {
-      atomicAdd(P.norms + 2 * s_, su);
-      atomicAdd(P.norms + 2 * s_ + 1, sx);
+      atomicAdd(P.norms, su);
+      atomicAdd(P.norms + 1, sx);
     }
   };
 
@@ -1036,17 +1043,15 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
         }
       }
       cfd_apply<M, true, EDGE>(c, P, lane, stU, etab, wv, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
-    } else if (MODE == KM_NORM) {
-      double uo[M], xo[M];
-      for (int s_ = 1; s_ <= KK; ++s_) {
-#pragma unroll
-        for (int i = 0; i < M; ++i) { uo[i] = u[i]; xo[i] = x[i]; }
-        cfd_apply<M, true, EDGE>(c, P, lane, stU, etab, x, Sm, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
-        cfd_apply<M, false, EDGE>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, VFn, VLp, xm1, xp1);
-        if (s_ >= P.kmin) norm_add(s_, u, uo, x, xo);
-      }
     } else {
+      double uo[TEST ? M : 1], xo[TEST ? M : 1];
       for (int k = 0; k < KK; ++k) {
+        if constexpr (TEST) {
+          if (k + 1 == KK) {
+#pragma unroll
+            for (int i = 0; i < M; ++i) { uo[i] = u[i]; xo[i] = x[i]; }
+          }
+        }
         cfd_apply<M, true, EDGE>(c, P, lane, stU, etab, x, Sm, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
         if (k + 1 == KK) {
           // park u_K in the (now dead) S tile: u is then dead across every x-op,
@@ -1056,6 +1061,9 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
           for (int i = 0; i < M / 2; ++i) S2[i] = make_double2(u[2 * i], u[2 * i + 1]);
         }
         cfd_apply<M, false, EDGE>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, VFn, VLp, xm1, xp1);
+        if constexpr (TEST) {
+          if (k + 1 == KK) norm_add(u, uo, x, xo);
+        }
       }
       if (MODE == KM_SWEEP) {
         double e1, e2;
@@ -1101,20 +1109,21 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
         }
       }
       u_op(wv, Sm);             // S1 = S - alpha D̄(W)
-    } else if (MODE == KM_NORM) {
-      double uo[M], xo[M];
-      for (int s_ = 1; s_ <= KK; ++s_) {
-#pragma unroll
-        for (int i = 0; i < M; ++i) { uo[i] = u[i]; xo[i] = x[i]; }
-        u_op(x, Sm);
-        x_op(Vm);
-        if (s_ >= P.kmin) norm_add(s_, u, uo, x, xo);
-      }
     } else {
+      double uo[TEST ? M : 1], xo[TEST ? M : 1];
       for (int k = 0; k < KK; ++k) {
+        if constexpr (TEST) {
+          if (k + 1 == KK) {
+#pragma unroll
+            for (int i = 0; i < M; ++i) { uo[i] = u[i]; xo[i] = x[i]; }
+          }
+        }
         u_op(x, Sm);
         if (MODE == KM_SWEEP && k + 1 == KK) stage_phi();
         x_op(Vm);
+        if constexpr (TEST) {
+          if (k + 1 == KK) norm_add(u, uo, x, xo);
+        }
       }
       if (MODE == KM_SWEEP) {
         add_source(Sm, u);
@@ -1125,7 +1134,6 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     }
   }
   if (tr) tr2 = gtimer();
-  if (MODE == KM_NORM) return;   // the norm pass stores nothing (every thread returns here)
 
   // ---- stage the outputs in the tile (own chunk); the CFD FINAL u_K is already parked
   double acc = 0.0;
@@ -1215,18 +1223,20 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD, EDGE, MODE>::value))
   // TMA destinations need 128-byte alignment
   // (pointer arithmetic on the shared array keeps the shared address space visible)
   double* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u) / 8u;
+  if (P.gate && *P.gate) return;   // stopping rule: the stage was decided by an earlier attempt
   const Seg sg = P.segs[blockIdx.y];
   line_tile<METHOD, M, NW, MODE, EDGE>(P, sg, smem);
 }
 
-// The stopping rule's choice for one stage: the first sweep s in [kmin, K] with
-// sqrt(norms[2s]) + sqrt(norms[2s+1]) <= eps, else K (Alg. 3/4 "until test <= eps
-// or k >= k_max").  One thread.
-__global__ void pick_sweeps_kernel(const double* norms, int K, int kmin, double eps, int* kout) {
-  int ks = K;
-  for (int s = kmin; s <= K; ++s)
-    if (sqrt(norms[2 * s]) + sqrt(norms[2 * s + 1]) <= eps) { ks = s; break; }
-  *kout = ks;
+// The stopping rule after the attempt with k sweeps (Alg. 3/4 "until test <= eps or
+// k >= k_max"): test = ||u_k - u_{k-1}||_F + ||x_k - x_{k-1}||_F from the attempt's
+// sums; a passing test (or k = kmax) closes the gate and records k.  One thread.
+__global__ void decide_sweeps_kernel(const double* norms, double eps, int k, int kmax, int* gate, int* kout) {
+  if (*gate) return;
+  if (sqrt(norms[0]) + sqrt(norms[1]) <= eps || k >= kmax) {
+    *gate = 1;
+    *kout = k;
+  }
 }
 
 }  // namespace adi

@@ -59,7 +59,7 @@ struct adi_ctx {
   int kmin = 6;          // ADI_K_MIN
   double* d_norms = nullptr;  // [K+1][2] per-sweep squared changes of one stage
   int d_norms_cap = 0;
-  int* d_k = nullptr;         // chosen sweeps: rows, columns of the last step
+  int* d_k = nullptr;         // [4]: chosen sweeps (rows, columns) of the last step, gates
   unsigned long long* trace = nullptr;  // adi_set_trace
   long long trace_cap = 0;
   int trace_kind = -1;
@@ -594,12 +594,14 @@ int launch(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p0, int
   if (h->method == ADI_CFD) {
     if (mode == adi::KM_SWEEP) return launch_t<adi::M_CFD, adi::KM_SWEEP>(h, A, p);
     if (mode == adi::KM_FINAL) return launch_t<adi::M_CFD, adi::KM_FINAL>(h, A, p);
-    if (mode == adi::KM_NORM) return launch_t<adi::M_CFD, adi::KM_NORM>(h, A, p);
+    if (mode == adi::KM_SWEEP_T) return launch_t<adi::M_CFD, adi::KM_SWEEP_T>(h, A, p);
+    if (mode == adi::KM_FINAL_T) return launch_t<adi::M_CFD, adi::KM_FINAL_T>(h, A, p);
     return launch_t<adi::M_CFD, adi::KM_PROLOGUE>(h, A, p);
   }
   if (mode == adi::KM_SWEEP) return launch_t<adi::M_MFD, adi::KM_SWEEP>(h, A, p);
   if (mode == adi::KM_FINAL) return launch_t<adi::M_MFD, adi::KM_FINAL>(h, A, p);
-  if (mode == adi::KM_NORM) return launch_t<adi::M_MFD, adi::KM_NORM>(h, A, p);
+  if (mode == adi::KM_SWEEP_T) return launch_t<adi::M_MFD, adi::KM_SWEEP_T>(h, A, p);
+  if (mode == adi::KM_FINAL_T) return launch_t<adi::M_MFD, adi::KM_FINAL_T>(h, A, p);
   return launch_t<adi::M_MFD, adi::KM_PROLOGUE>(h, A, p);
 }
 
@@ -698,20 +700,28 @@ adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
   return p;
 }
 
-// Inner stopping rule for one stage (Alg. 3/4): a norm pass over all
-// tiles (K sweeps, no stores), then one thread picks the sweep count into d_k[which],
-// which the stage's own launch reads.  Everything stays on the handle's stream.
-int stop_rule(adi_ctx* h, const adi::Axis& A, adi::KParams p, int kind, int which) {
+// Inner stopping rule for one stage (Alg. 3/4), decided on the device:
+// attempts with k = kmin..K sweeps are enqueued; each is the stage's own kernel
+// (outputs stored) that also sums its last sweep's squared changes, followed by a
+// one-thread decision.  Once a test passes the gate closes and the later attempts
+// exit at once, so the outputs are those of the chosen k (the stage's inputs are
+// never overwritten).
+int stage_with_rule(adi_ctx* h, int mode_t, const adi::Axis& A, adi::KParams p, int kind, int which) {
   CUDA_TRY(h, cudaMemsetAsync(h->d_norms, 0, sizeof(double) * 2 * (h->K + 1), h->stream));
-  p.norms = h->d_norms;
-  p.kmin = h->kmin;
+  CUDA_TRY(h, cudaMemsetAsync(h->d_k + 2 + which, 0, sizeof(int), h->stream));
   p.Kdev = nullptr;
-  p.K = h->K;
-  int rc = launch(h, adi::KM_NORM, A, p, kind);
-  if (rc) return rc;
-  adi::pick_sweeps_kernel<<<1, 1, 0, h->stream>>>(h->d_norms, h->K, h->kmin, h->eps, h->d_k + which);
-  CUDA_TRY(h, cudaGetLastError());
-  h->launches++;
+  p.gate = h->d_k + 2 + which;
+  for (int k = h->kmin; k <= h->K; ++k) {
+    adi::KParams q = p;
+    q.K = k;
+    q.norms = h->d_norms + 2 * k;
+    int rc = launch(h, mode_t, A, q, kind);
+    if (rc) return rc;
+    adi::decide_sweeps_kernel<<<1, 1, 0, h->stream>>>(h->d_norms + 2 * k, h->eps, k, h->K,
+                                                        h->d_k + 2 + which, h->d_k + which);
+    CUDA_TRY(h, cudaGetLastError());
+    h->launches++;
+  }
   return ADI_OK;
 }
 
@@ -1014,7 +1024,7 @@ int adi_step_begin(adi_handle h, int nsteps) {
       CUDA_TRY(h, cudaMalloc(&h->d_norms, sizeof(double) * 2 * (h->K + 1)));
       h->d_norms_cap = h->K + 1;
     }
-    if (!h->d_k) CUDA_TRY(h, cudaMalloc(&h->d_k, 2 * sizeof(int)));
+    if (!h->d_k) CUDA_TRY(h, cudaMalloc(&h->d_k, 4 * sizeof(int)));
   }
   int rc;
   // a2 (standalone once per call): S1 = U - alpha D̄_y W + dt/2 F(t^m), W* = W - beta D_y U
@@ -1043,11 +1053,8 @@ int adi_step_rows(adi_handle h) {
   p.gb = tabv(h->gb, 2 * m + 1);   // boundary values of the intermediate U* at t^m + dt/2 [G9]
   p.gf = tabv(h->gf, 2 * m + 2);
   int rc;
-  if (h->eps > 0.0) {
-    if ((rc = stop_rule(h, h->ax, p, ADI_KK_ROW, 0))) return rc;
-    p.Kdev = h->d_k;
-  }
-  rc = launch(h, adi::KM_SWEEP, h->ax, p, ADI_KK_ROW);
+  if (h->eps > 0.0) rc = stage_with_rule(h, adi::KM_SWEEP_T, h->ax, p, ADI_KK_ROW, 0);
+  else rc = launch(h, adi::KM_SWEEP, h->ax, p, ADI_KK_ROW);
   if (rc) return rc;
   std::swap(h->Vcur, h->Valt);
   return ADI_OK;
@@ -1064,19 +1071,19 @@ int adi_step_cols(adi_handle h) {
   p.gb = tabv(h->gb, 2 * m + 2);
   p.gf = tabv(h->gf, 2 * m + 2);
   int rc;
-  if (h->eps > 0.0) {
-    if ((rc = stop_rule(h, h->ay, p, last ? ADI_KK_FINAL : ADI_KK_COL, 1))) return rc;
-    p.Kdev = h->d_k + 1;
-  }
   if (last) {  // write U^{m+1} and W̄^{m+1} into the canonical buffers
     p.U_out = h->U;
     p.X_out = (h->Wcur == h->W) ? h->W2 : h->W;
-    if ((rc = launch(h, adi::KM_FINAL, h->ay, p, ADI_KK_FINAL))) return rc;
+    rc = (h->eps > 0.0) ? stage_with_rule(h, adi::KM_FINAL_T, h->ay, p, ADI_KK_FINAL, 1)
+                        : launch(h, adi::KM_FINAL, h->ay, p, ADI_KK_FINAL);
+    if (rc) return rc;
     if (h->Wcur == h->W) std::swap(h->W, h->W2);
   } else {
     p.S_out = h->Sa;
     p.X_out = h->Walt;
-    if ((rc = launch(h, adi::KM_SWEEP, h->ay, p, ADI_KK_COL))) return rc;
+    rc = (h->eps > 0.0) ? stage_with_rule(h, adi::KM_SWEEP_T, h->ay, p, ADI_KK_COL, 1)
+                        : launch(h, adi::KM_SWEEP, h->ay, p, ADI_KK_COL);
+    if (rc) return rc;
     std::swap(h->Wcur, h->Walt);
   }
   h->m = m + 1;
