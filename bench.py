@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--method", default="both", choices=["both", "mfd", "cfd"])
-    ap.add_argument("--n", type=int, default=16384, help="nodes per direction")
+    ap.add_argument("--grid", "--n", dest="n", type=int, default=16384, help="nodes per direction")
     ap.add_argument("--K", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -68,8 +68,17 @@ def dist_setup():
     if ws > 1:
         import torch
         import torch.distributed as dist
+        # test-only overrides (functional check of this path on a single GPU; never used
+        # for a reported number): BENCH_ONE_DEVICE maps every rank to device 0,
+        # BENCH_DIST_BACKEND=gloo exchanges halos through host memory
+        if os.environ.get("BENCH_ONE_DEVICE"):
+            local = 0
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return ws, rank, local
 
 
@@ -84,7 +93,8 @@ def allmax(ws, v):
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

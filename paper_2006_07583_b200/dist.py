@@ -68,14 +68,27 @@ class TorchDistTransport:
         self.rank, self.world, self.group = rank, world, group
 
     def exchange(self, send: Dict[int, "torch.Tensor"], recv: Dict[int, "torch.Tensor"]):
+        import torch
         import torch.distributed as dist
+        nb = neighbours(self.rank, self.world)
+        if not nb:
+            return
+        staged = dist.get_backend(self.group) != "nccl" and any(t.is_cuda for t in send.values())
+        if staged:   # gloo: host-staged messages (CPU tests, single-device functional checks)
+            torch.cuda.current_stream().synchronize()
+            snd = {k: v.cpu() for k, v in send.items()}
+            rcv = {k: torch.empty_like(v, device="cpu") for k, v in recv.items()}
+        else:
+            snd, rcv = send, recv
         ops = []
-        for side, peer in neighbours(self.rank, self.world).items():
-            ops.append(dist.P2POp(dist.isend, send[side], peer, group=self.group))
-            ops.append(dist.P2POp(dist.irecv, recv[side], peer, group=self.group))
-        if ops:
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
+        for side, peer in nb.items():
+            ops.append(dist.P2POp(dist.isend, snd[side], peer, group=self.group))
+            ops.append(dist.P2POp(dist.irecv, rcv[side], peer, group=self.group))
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+        if staged:
+            for k in recv:
+                recv[k].copy_(rcv[k])
 
 
 class BandSolver:
