@@ -35,7 +35,8 @@ class Problem:
 
 
 def random_problem(method: int, n: int, *, seed: int = 0, cfl: float = None, K: int = 8,
-                   steps: int = 4, source: bool = True, boundary: bool = True) -> Problem:
+                   steps: int = 4, source: bool = True, boundary: bool = True,
+                   ny: int = None) -> Problem:
     """Seeded random state with a random dense source and random boundary data.
 
     Values are O(1) normal; tables cover ``steps`` steps.  Used for parity
@@ -44,14 +45,14 @@ def random_problem(method: int, n: int, *, seed: int = 0, cfl: float = None, K: 
     rng = np.random.default_rng(seed)
     if cfl is None:
         cfl = 0.91 if method == CFD else 0.81
-    g = Grid(method, n, n)
-    h = g.h
+    nx, ny = n, (n if ny is None else ny)
+    h = 1.0 / (max(nx, ny) - 1)   # one spacing in both directions (the domain may be a rectangle)
     dt = h * cfl
-    su, sv, sw = shapes(method, n, n)
+    su, sv, sw = shapes(method, nx, ny)
     U = rng.standard_normal(su)
     V = rng.standard_normal(sv)
     W = rng.standard_normal(sw)
-    phi = rng.standard_normal(interior_shape(method, n, n)) if source else None
+    phi = rng.standard_normal(interior_shape(method, nx, ny)) if source else None
     nt = 2 * steps + 1
     gf = rng.standard_normal(nt) if source else None
     edges = None
@@ -60,5 +61,5 @@ def random_problem(method: int, n: int, *, seed: int = 0, cfl: float = None, K: 
         edges = (rng.standard_normal(su[1]), rng.standard_normal(su[1]),
                  rng.standard_normal(su[0]), rng.standard_normal(su[0]))
         gb = rng.standard_normal(nt)
-    return Problem(method, n, n, h, dt, 1.0, K, U, V, W, phi=phi, gf=gf, edges=edges, gb=gb,
+    return Problem(method, nx, ny, h, dt, 1.0, K, U, V, W, phi=phi, gf=gf, edges=edges, gb=gb,
                    meta=dict(kind="random", seed=seed, cfl=cfl, steps=steps))

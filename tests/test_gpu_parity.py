@@ -257,3 +257,54 @@ def test_config3_parity(adi, method, steps, k):
     steps against the oracle."""
     p = mms_problem(method, 1601, MMS(gamma=float(k), k=k), steps=steps)
     assert_parity(run_gpu(adi, p, steps), run_oracle(p, steps), what=f"config3 k={k}")
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+@pytest.mark.parametrize("nx,ny", [(1601, 300), (77, 2100), (2101, 1602)])
+def test_parity_rectangular_grids(adi, method, nx, ny):
+    """nx != ny: the two sweep directions plan different tilings (lean and generic tiles)."""
+    p = random_problem(method, nx, ny=ny, seed=nx + ny, steps=2)
+    assert_parity(run_gpu(adi, p, 2), run_oracle(p, 2), what=f"{nx}x{ny}")
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+def test_parity_batch_lean_tiles(adi, method):
+    """A batch of 3 grids (shared source and boundary data) at 1601^2 (lean tiles)."""
+    n, B, steps = 1601, 3, 2
+    ps = [random_problem(method, n, seed=40 + b, steps=steps) for b in range(B)]
+    p0 = ps[0]
+    s = adi.AdiSolver(p0.nx, p0.ny, p0.h, p0.dt, p0.c, method, batch=B, K=p0.K)
+    s.set_fields(np.stack([p.U for p in ps]), np.stack([p.V for p in ps]), np.stack([p.W for p in ps]))
+    s.set_source(p0.phi, None, p0.gf)
+    s.set_boundary(p0.edges, p0.gb)
+    s.step(steps)
+    g = s.get_fields()
+    s.close()
+    for b, p in enumerate(ps):
+        o = oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, p.U, p.V, p.W, nsteps=steps,
+                       rho=p.rho, phi=p0.phi, gf=p0.gf, edges=p0.edges, gb=p0.gb)
+        assert_parity([x[b] for x in g], o, what=f"batch member {b}")
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+def test_parity_point_source_lean_tiles(adi, method):
+    """Ricker point source on a 1601^2 grid (the source sits in a lean tile)."""
+    p = ricker_problem(1601, shot=5, nshots=8, method=method, steps=6, f0=20.0, t0=0.05)
+    assert_parity(run_gpu(adi, p, 6), run_oracle(p, 6), what="ricker 1601")
+
+
+def test_parity_point_sources_batch_lean_tiles(adi):
+    """A batch of shots with per-grid point sources (adi_set_point_sources) at 1601^2."""
+    n, B, steps = 1601, 3, 4
+    probs = [ricker_problem(n, shot=s, nshots=B, steps=steps, f0=20.0, t0=0.05) for s in range(B)]
+    p0 = probs[0]
+    s = adi.AdiSolver(n, n, p0.h, p0.dt, 1.0, MFD, batch=B)
+    s.set_fields(np.stack([p.U for p in probs]), np.stack([p.V for p in probs]),
+                 np.stack([p.W for p in probs]))
+    s.set_point_sources([p.src[0] for p in probs], [p.src[1] for p in probs], p0.gf)
+    s.step(steps)
+    got = s.get_fields()
+    s.close()
+    for b, p in enumerate(probs):
+        o = run_oracle(p, steps)
+        assert_parity([x[b] for x in got], o, what=f"shot {b}")
