@@ -459,21 +459,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
         : "memory");
   } while (!ok);
 }
-// global -> shared, `bytes` (multiple of 16, 16-byte aligned ends), completes on mbarrier
-__device__ __forceinline__ void bulk_g2s(double* dst, const double* src, unsigned bytes,
-                                         unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-// shared -> global (bulk group)
-__device__ __forceinline__ void bulk_s2g(double* dst, const double* src, unsigned bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
-               "r"(bytes)
-               : "memory");
-}
 __device__ __forceinline__ void fence_async_shared() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

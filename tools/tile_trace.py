@@ -17,7 +17,7 @@ for method in (MFD, CFD):
     mname = ("CFD", "MFD")[method]
     p = mms_problem(method, n, MMS(), steps=40)
     s = adi.AdiSolver.from_problem(p, stream=torch.cuda.current_stream().cuda_stream)
-    for persist in (0,):
+    if True:
         for kname in ("row", "col", "final", "prologue"):
             s.set_fields(p.U, p.V, p.W)
             s.step(1)
@@ -29,7 +29,7 @@ for method in (MFD, CFD):
             s.m = 0
             r = buf.view(cap, 8).cpu().numpy()
             r = r[r[:, 5] > 0]
-            np.save(f"{out}_{mname}_{kname}_p{persist}.npy", r)
+            np.save(f"{out}_{mname}_{kname}.npy", r)
             t0 = r[:, 2].min()
             a, b_, c_, d = (r[:, 2] - t0) / 1e3, (r[:, 3] - t0) / 1e3, (r[:, 4] - t0) / 1e3, (r[:, 5] - t0) / 1e3
             span = d.max()
@@ -43,7 +43,7 @@ for method in (MFD, CFD):
                 return np.cumsum(cnt)[:-1]
             cl, co, cs = conc(a, b_), conc(b_, c_), conc(c_, d)
             mid = slice(len(grid) // 10, 9 * len(grid) // 10)
-            print(f"{mname} {kname:8s} persist={persist} tiles={len(r)} span={span/1e3:.3f} ms "
+            print(f"{mname} {kname:8s} tiles={len(r)} span={span/1e3:.3f} ms "
                   f"tile us: load {np.mean(b_-a):.1f} ops {np.mean(c_-b_):.1f} store {np.mean(d-c_):.1f} "
                   f"total {np.mean(d-a):.1f} | resident avg {busy/span:.0f} ({busy/span/nsm:.2f}/SM) | "
                   f"in phase (mid 80%): load {cl[mid].mean():.0f} ops {co[mid].mean():.0f} store {cs[mid].mean():.0f}",
