@@ -28,19 +28,29 @@ class Problem:
     gb: Optional[np.ndarray] = None           # boundary time function at half steps
     rho: float = 1.0
     meta: dict = field(default_factory=dict)
+    # heterogeneous media (NEXT row f3): kappa on the U layout, rho^-1 on the V̄ and
+    # W̄ layouts; fp32 arrays (the GPU path's material precision)
+    kappa: Optional[np.ndarray] = None
+    rinv_v: Optional[np.ndarray] = None
+    rinv_w: Optional[np.ndarray] = None
 
     def oracle_kwargs(self):
-        return dict(rho=self.rho, phi=self.phi, src=self.src, gf=self.gf, edges=self.edges,
-                    gb=self.gb)
+        kw = dict(rho=self.rho, phi=self.phi, src=self.src, gf=self.gf, edges=self.edges,
+                  gb=self.gb)
+        if self.kappa is not None:
+            kw.update(kappa=self.kappa, rinv_v=self.rinv_v, rinv_w=self.rinv_w)
+        return kw
 
 
 def random_problem(method: int, n: int, *, seed: int = 0, cfl: float = None, K: int = 8,
                    steps: int = 4, source: bool = True, boundary: bool = True,
-                   ny: int = None) -> Problem:
+                   ny: int = None, media: bool = False) -> Problem:
     """Seeded random state with a random dense source and random boundary data.
 
     Values are O(1) normal; tables cover ``steps`` steps.  Used for parity
-    and invariant tests (no structure assumed by the method).
+    and invariant tests (no structure assumed by the method).  ``media``: random
+    fp32 kappa and rho^-1 fields, uniform in [0.6, 1] (c <= 1, so the homogeneous
+    CFL numbers still apply).
     """
     rng = np.random.default_rng(seed)
     if cfl is None:
@@ -61,5 +71,9 @@ def random_problem(method: int, n: int, *, seed: int = 0, cfl: float = None, K: 
         edges = (rng.standard_normal(su[1]), rng.standard_normal(su[1]),
                  rng.standard_normal(su[0]), rng.standard_normal(su[0]))
         gb = rng.standard_normal(nt)
+    med = {}
+    if media:
+        med = {k: rng.uniform(0.6, 1.0, s_).astype(np.float32)
+               for k, s_ in (("kappa", su), ("rinv_v", sv), ("rinv_w", sw))}
     return Problem(method, nx, ny, h, dt, 1.0, K, U, V, W, phi=phi, gf=gf, edges=edges, gb=gb,
-                   meta=dict(kind="random", seed=seed, cfl=cfl, steps=steps))
+                   meta=dict(kind="random", seed=seed, cfl=cfl, steps=steps), **med)

@@ -42,11 +42,11 @@ def lib():
         I = ctypes.c_int
         P = ctypes.c_void_p
         _lib.or_run_flat.argtypes = [I, I, I, D, D, D, D, I, P, I, I, P, I, P, P, P, P, P, I,
-                                     P, P, P, I, I, I, D, I, P, P]
+                                     P, P, P, I, I, I, D, I, P, P, P, P, P]
         _lib.or_run_flat.restype = I
         _lib.or_apply_D.argtypes = [I, I, D, P, P]
         _lib.or_apply_Dbar.argtypes = [I, I, D, P, P]
-        _lib.or_stage_line.argtypes = [I, I, D, I, D, D, P, P, D, D, P, P]
+        _lib.or_stage_line.argtypes = [I, I, D, I, D, D, P, P, P, P, D, D, P, P]
         _lib.or_cfd_factors.argtypes = [I, I, P, P]
         _lib.or_tri_factor.argtypes = [I, P, P, P, P, P]
         _lib.or_tri_solve.argtypes = [I, P, P, P, P, P]
@@ -81,7 +81,8 @@ def interior_shape(method: int, nx: int, ny: int):
 
 
 def run(method, nx, ny, h, dt, c, K, U, V, W, *, rho=1.0, phi=None, src=None, gf=None,
-        edges=None, gb=None, m0=0, nsteps=1, nthreads=0, eps=0.0, kmin=6, info=None):
+        edges=None, gb=None, m0=0, nsteps=1, nthreads=0, eps=0.0, kmin=6, info=None,
+        kappa=None, rinv_v=None, rinv_w=None):
     """Advance copies of (U, V̄, W̄) by ``nsteps`` ADI steps; returns new arrays.
 
     ``eps`` > 0 applies the stopping rule of Alg. 3/4 (sweeps ``kmin``..K tested,
@@ -93,6 +94,10 @@ def run(method, nx, ny, h, dt, c, K, U, V, W, *, rho=1.0, phi=None, src=None, gf
     homogeneous Dirichlet); ``gf``/``gb`` are the source / boundary time
     functions sampled at half steps, g[j] = g(j*dt/2) (None means 1).
     ``src`` = (ix, iy) U-array indices of a point source F = g_f/h^2.
+
+    Heterogeneous media (NEXT row f3): ``kappa`` on the U layout
+    (interior points used), ``rinv_v`` = rho^-1 on the V̄ layout, ``rinv_w`` on
+    the W̄ layout; all three or none (then the scalars c, rho: kappa = rho c^2).
     """
     su, sv, sw = shapes(method, nx, ny)
     U = np.array(U, dtype=np.float64, order="C", copy=True).reshape(su)
@@ -108,13 +113,19 @@ def run(method, nx, ny, h, dt, c, K, U, V, W, *, rho=1.0, phi=None, src=None, gf
     else:
         e = [_f64(x) for x in edges]
         assert e[0].size == su[1] and e[1].size == su[1] and e[2].size == su[0] and e[3].size == su[0]
+    med = [kappa, rinv_v, rinv_w]
+    if any(m is not None for m in med):
+        assert all(m is not None for m in med), "kappa, rinv_v, rinv_w: all or none"
+        med = [_f64(m) for m in med]
+        assert med[0].shape == su and med[1].shape == sv and med[2].shape == sw
     ix, iy = (-1, -1) if src is None else src
     kch = np.zeros((max(nsteps, 1), 2), dtype=np.int32)
     tests = np.zeros((max(nsteps, 1), 2, K + 1))
     rc = lib().or_run_flat(method, nx, ny, h, dt, c, rho, K, _p(phi), ix, iy, _p(gf),
                            0 if gf is None else gf.size, _p(e[0]), _p(e[1]), _p(e[2]), _p(e[3]),
                            _p(gb), 0 if gb is None else gb.size, _p(U), _p(V), _p(W), m0, nsteps,
-                           nthreads, float(eps), int(kmin), _p(kch), _p(tests))
+                           nthreads, float(eps), int(kmin), _p(kch), _p(tests), _p(med[0]),
+                           _p(med[1]), _p(med[2]))
     if rc != 0:
         raise RuntimeError(f"oracle or_run failed: {rc}")
     if info is not None:
@@ -140,11 +151,19 @@ def apply_Dbar(method, n, h, v):
 
 
 def stage_line(method, n, h, K, alpha, beta, s, v0, gL, gR):
+    """One stage on one line; ``alpha`` / ``beta`` scalars or per-point arrays (f3)."""
     s = _f64(s)
     v0 = _f64(v0)
     u = np.zeros(n - 1 if method == CFD else n)
     v = np.zeros(n + 1)
-    assert lib().or_stage_line(method, n, h, K, alpha, beta, _p(s), _p(v0), gL, gR, _p(u), _p(v)) == 0
+    av = None if np.isscalar(alpha) else _f64(alpha)
+    bv = None if np.isscalar(beta) else _f64(beta)
+    assert av is None or av.size == u.size
+    assert bv is None or bv.size == v.size
+    a0 = float(alpha) if av is None else 0.0
+    b0 = float(beta) if bv is None else 0.0
+    assert lib().or_stage_line(method, n, h, K, a0, b0, _p(av), _p(bv), _p(s), _p(v0), gL, gR,
+                               _p(u), _p(v)) == 0
     return u, v
 
 

@@ -228,20 +228,27 @@ int or_apply_Dbar(int method, int n, double h, const double* v, double* out) {
 /* Seidel coupling u before v [G11], initial guess v0 = (V^m | W*) [G7]:      */
 /*   repeat K:  u <- s - alpha * D̄(v)                                       */
 /*              v <- v0 - beta * D([gL, u, gR])                               */
-/* Returns u (nu), v (nv); also the last D([gL,u,gR]) in dlast (nv).         */
+/* Heterogeneous media (NEXT row f3; Alg. 3/4 "K.*( )", "R.*( )",            */
+/* PAPER.md:655-656, 695-696; K, R: grid values of kappa and rho^-1,         */
+/* PAPER.md:183): alpha and beta become per-point, alpha_i = dt/2 K_i after  */
+/* the derivative [G8], beta_j = dt/2 R_j; av (nu) / bv (nv) hold them, or   */
+/* NULL for the scalars alpha / beta.                                        */
+/* Returns u (nu), v (nv).                                                    */
 /* ------------------------------------------------------------------------ */
-static void stage_line(const axis_t* a, int K, double alpha, double beta,
-                       const double* s, const double* v0, double gL, double gR,
+#define OR_A(i) (av ? av[i] : alpha)
+#define OR_B(i) (bv ? bv[i] : beta)
+static void stage_line(const axis_t* a, int K, double alpha, double beta, const double* av,
+                       const double* bv, const double* s, const double* v0, double gL, double gR,
                        double* u, double* v, double* ub, double* tmp) {
   for (int i = 0; i < a->nv; ++i) v[i] = v0[i];
   for (int k = 0; k < K; ++k) {
     axis_Dbar(a, v, tmp);
-    for (int i = 0; i < a->nu; ++i) u[i] = s[i] - alpha * tmp[i];
+    for (int i = 0; i < a->nu; ++i) u[i] = s[i] - OR_A(i) * tmp[i];
     ub[0] = gL;
     for (int i = 0; i < a->nu; ++i) ub[i + 1] = u[i];
     ub[a->nub - 1] = gR;
     axis_D(a, ub, tmp);
-    for (int i = 0; i < a->nv; ++i) v[i] = v0[i] - beta * tmp[i];
+    for (int i = 0; i < a->nv; ++i) v[i] = v0[i] - OR_B(i) * tmp[i];
   }
 }
 
@@ -250,7 +257,7 @@ static void stage_line(const axis_t* a, int K, double alpha, double beta,
  * this line (Alg. 3/4 "test"; the Frobenius norms of the
  * whole matrices are the square roots of the sums over the lines). */
 static void stage_line_norms(const axis_t* a, int kmax, double alpha, double beta,
-                             const double* s, const double* v0, double gL, double gR,
+                             const double* av, const double* bv, const double* s, const double* v0, double gL, double gR,
                              double* u, double* v, double* ub, double* tmp, double* uold,
                              double* vold, double* du2, double* dv2) {
   for (int i = 0; i < a->nv; ++i) v[i] = v0[i];
@@ -258,12 +265,12 @@ static void stage_line_norms(const axis_t* a, int kmax, double alpha, double bet
     for (int i = 0; i < a->nu; ++i) uold[i] = u[i];
     for (int i = 0; i < a->nv; ++i) vold[i] = v[i];
     axis_Dbar(a, v, tmp);
-    for (int i = 0; i < a->nu; ++i) u[i] = s[i] - alpha * tmp[i];
+    for (int i = 0; i < a->nu; ++i) u[i] = s[i] - OR_A(i) * tmp[i];
     ub[0] = gL;
     for (int i = 0; i < a->nu; ++i) ub[i + 1] = u[i];
     ub[a->nub - 1] = gR;
     axis_D(a, ub, tmp);
-    for (int i = 0; i < a->nv; ++i) v[i] = v0[i] - beta * tmp[i];
+    for (int i = 0; i < a->nv; ++i) v[i] = v0[i] - OR_B(i) * tmp[i];
     double su = 0.0, sv = 0.0;
     if (k >= 2) {
       for (int i = 0; i < a->nu; ++i) su += (u[i] - uold[i]) * (u[i] - uold[i]);
@@ -302,6 +309,9 @@ typedef struct {
   const double* gf; int ngf;     /* g_f(t0 + j dt/2), j < ngf; NULL -> 1 */
   const double* edges[4];        /* y0 (U row 0), y1 (U last row), x0 (U col 0), x1 (U last col) */
   const double* gb; int ngb;     /* g_b(t0 + j dt/2); NULL -> 1 */
+  /* heterogeneous media (f3): kappa on the U layout (interior used), rho^-1 on
+   * the V̄ (rv) and W̄ (rw) layouts; all three set, or all NULL (scalar kappa, rho) */
+  const double* kappa; const double* rv; const double* rw;
 } or_problem;
 
 static double tab(const double* g, int ng, int j) {
@@ -317,6 +327,21 @@ static double source_at(const or_problem* p, int nxi, int jj, int ii, double gft
   if (p->src_ix >= 1 && p->src_iy >= 1 && ii == p->src_ix - 1 && jj == p->src_iy - 1)
     f += gft / (p->h * p->h);
   return f;
+}
+
+/* f3 (heterogeneous media): per-point alpha_i = dt/2 K, beta_j = dt/2 R of one
+ * row line jj (K at U(jj+1, i+1), R = rv at V̄(jj, i)) or one column line ii (K at
+ * U(r+1, ii+1), R = rw at W̄(r, ii)); Alg. 1/2 lines 8-14 and Alg. 3/4
+ * with K, R of PAPER.md:183. */
+static void row_coefs(const or_problem* p, int jj, int nxu, int nxi, int nxv, double* av,
+                      double* bv) {
+  for (int i = 0; i < nxi; ++i) av[i] = p->dt / 2.0 * p->kappa[(size_t)(jj + 1) * nxu + i + 1];
+  for (int i = 0; i < nxv; ++i) bv[i] = p->dt / 2.0 * p->rv[(size_t)jj * nxv + i];
+}
+static void col_coefs(const or_problem* p, int ii, int nxu, int nxi, int nyi, int nyv, double* av,
+                      double* bv) {
+  for (int r = 0; r < nyi; ++r) av[r] = p->dt / 2.0 * p->kappa[(size_t)(r + 1) * nxu + ii + 1];
+  for (int r = 0; r < nyv; ++r) bv[r] = p->dt / 2.0 * p->rw[(size_t)r * nxi + ii];
 }
 
 /*
@@ -347,6 +372,7 @@ int or_run(const or_problem* p, double* U, double* Vb, double* Wb, int m0, int n
   const double rho = p->rho, kappa = rho * p->c * p->c;
   const double dt = p->dt;
   const double alpha = kappa * dt / 2.0, beta = dt / (2.0 * rho);
+  const int het = p->kappa != NULL;   /* f3: per-point alpha, beta (row_coefs / col_coefs) */
   size_t nS = (size_t)nyi * nxi, nW = (size_t)nyv * nxi;
   double* S1 = (double*)malloc(sizeof(double) * nS);
   double* S2 = (double*)malloc(sizeof(double) * nS);
@@ -369,6 +395,7 @@ int or_run(const or_problem* p, double* U, double* Vb, double* Wb, int m0, int n
     {
       double* col = (double*)malloc(sizeof(double) * 6 * L);
       double *w = col + L, *t1 = col + 2 * L, *t2 = col + 3 * L;
+      double *av = het ? col + 4 * L : NULL, *bv = het ? col + 5 * L : NULL;
 #pragma omp for schedule(static)
       for (int ii = 0; ii < nxi; ++ii) {
         const int i = ii + 1; /* U column */
@@ -376,10 +403,11 @@ int or_run(const or_problem* p, double* U, double* Vb, double* Wb, int m0, int n
         for (int r = 0; r < nyv; ++r) w[r] = Wb[(size_t)r * nxi + ii];
         axis_D(&ay, col, t1);     /* D_y(U^m(:,i)), Dirichlet rows included */
         axis_Dbar(&ay, w, t2);    /* D̄_y(W̄^m(:,i)) */
-        for (int r = 0; r < nyv; ++r) Ws[(size_t)r * nxi + ii] = w[r] - beta * t1[r];
+        if (het) col_coefs(p, ii, nxu, nxi, nyi, nyv, av, bv);
+        for (int r = 0; r < nyv; ++r) Ws[(size_t)r * nxi + ii] = w[r] - OR_B(r) * t1[r];
         for (int r = 0; r < nyi; ++r)
           S1[(size_t)r * nxi + ii] =
-              col[r + 1] - alpha * t2[r] + (dt / 2.0) * source_at(p, nxi, r, ii, gf_m);
+              col[r + 1] - OR_A(r) * t2[r] + (dt / 2.0) * source_at(p, nxi, r, ii, gf_m);
       }
       free(col);
     }
@@ -393,9 +421,10 @@ int or_run(const or_problem* p, double* U, double* Vb, double* Wb, int m0, int n
       double* lv = lu + (size_t)nyi * K1;
 #pragma omp parallel
       {
-        double* buf = (double*)malloc(sizeof(double) * 8 * L);
+        double* buf = (double*)malloc(sizeof(double) * 10 * L);
         double *u = buf, *v = buf + L, *ub = buf + 2 * L, *tmp = buf + 3 * L, *s = buf + 4 * L,
                *v0 = buf + 5 * L, *uo = buf + 6 * L, *vo = buf + 7 * L;
+        double *av = het ? buf + 8 * L : NULL, *bv = het ? buf + 9 * L : NULL;
 #pragma omp for schedule(static)
         for (int jj = 0; jj < nyi; ++jj) {
           const int j = jj + 1;
@@ -404,7 +433,8 @@ int or_run(const or_problem* p, double* U, double* Vb, double* Wb, int m0, int n
           for (int i = 0; i < nxi; ++i) s[i] = S1[(size_t)jj * nxi + i];
           for (int i = 0; i < nxv; ++i) v0[i] = Vb[(size_t)jj * nxv + i];
           for (int i = 0; i < nxi; ++i) u[i] = 0.0;
-          stage_line_norms(&ax, p->K, alpha, beta, s, v0, gL, gR, u, v, ub, tmp, uo, vo,
+          if (het) row_coefs(p, jj, nxu, nxi, nxv, av, bv);
+          stage_line_norms(&ax, p->K, alpha, beta, av, bv, s, v0, gL, gR, u, v, ub, tmp, uo, vo,
                            lu + (size_t)jj * K1, lv + (size_t)jj * K1);
         }
         free(buf);
@@ -419,9 +449,10 @@ int or_run(const or_problem* p, double* U, double* Vb, double* Wb, int m0, int n
     if (p->kchosen) p->kchosen[2 * st] = Kr;
 #pragma omp parallel
     {
-      double* buf = (double*)malloc(sizeof(double) * 6 * L);
+      double* buf = (double*)malloc(sizeof(double) * 8 * L);
       double *u = buf, *v = buf + L, *ub = buf + 2 * L, *tmp = buf + 3 * L, *s = buf + 4 * L,
              *v0 = buf + 5 * L;
+      double *av = het ? buf + 6 * L : NULL, *bv = het ? buf + 7 * L : NULL;
 #pragma omp for schedule(static)
       for (int jj = 0; jj < nyi; ++jj) {
         const int j = jj + 1; /* U row */
@@ -429,18 +460,19 @@ int or_run(const or_problem* p, double* U, double* Vb, double* Wb, int m0, int n
         const double gR = (p->edges[3] ? p->edges[3][j] : 0.0) * gb_h;
         for (int i = 0; i < nxi; ++i) s[i] = S1[(size_t)jj * nxi + i];
         for (int i = 0; i < nxv; ++i) v0[i] = Vb[(size_t)jj * nxv + i];
-        stage_line(&ax, Kr, alpha, beta, s, v0, gL, gR, u, v, ub, tmp);
+        if (het) row_coefs(p, jj, nxu, nxi, nxv, av, bv);
+        stage_line(&ax, Kr, alpha, beta, av, bv, s, v0, gL, gR, u, v, ub, tmp);
         /* C / S2 = U* - alpha D̄_x(V*) + dt/2 F^{m+1} */
         axis_Dbar(&ax, v, tmp);
         for (int i = 0; i < nxi; ++i)
           S2[(size_t)jj * nxi + i] =
-              u[i] - alpha * tmp[i] + (dt / 2.0) * source_at(p, nxi, jj, i, gf_1);
+              u[i] - OR_A(i) * tmp[i] + (dt / 2.0) * source_at(p, nxi, jj, i, gf_1);
         /* V^{m+1} = V* - beta D_x([g(t+dt/2), U*, g(t+dt/2)]) */
         ub[0] = gL;
         for (int i = 0; i < nxi; ++i) ub[i + 1] = u[i];
         ub[nxu - 1] = gR;
         axis_D(&ax, ub, tmp);
-        for (int i = 0; i < nxv; ++i) Vb[(size_t)jj * nxv + i] = v[i] - beta * tmp[i];
+        for (int i = 0; i < nxv; ++i) Vb[(size_t)jj * nxv + i] = v[i] - OR_B(i) * tmp[i];
       }
       free(buf);
     }
@@ -454,9 +486,10 @@ int or_run(const or_problem* p, double* U, double* Vb, double* Wb, int m0, int n
       double* lw = lu + (size_t)nxi * K1;
 #pragma omp parallel
       {
-        double* buf = (double*)malloc(sizeof(double) * 8 * L);
+        double* buf = (double*)malloc(sizeof(double) * 10 * L);
         double *u = buf, *w = buf + L, *ub = buf + 2 * L, *tmp = buf + 3 * L, *s = buf + 4 * L,
                *w0 = buf + 5 * L, *uo = buf + 6 * L, *wo = buf + 7 * L;
+        double *av = het ? buf + 8 * L : NULL, *bv = het ? buf + 9 * L : NULL;
 #pragma omp for schedule(static)
         for (int ii = 0; ii < nxi; ++ii) {
           const int i = ii + 1;
@@ -465,7 +498,8 @@ int or_run(const or_problem* p, double* U, double* Vb, double* Wb, int m0, int n
           for (int r = 0; r < nyi; ++r) s[r] = S2[(size_t)r * nxi + ii];
           for (int r = 0; r < nyv; ++r) w0[r] = Ws[(size_t)r * nxi + ii];
           for (int r = 0; r < nyi; ++r) u[r] = 0.0;
-          stage_line_norms(&ay, p->K, alpha, beta, s, w0, gB, gT, u, w, ub, tmp, uo, wo,
+          if (het) col_coefs(p, ii, nxu, nxi, nyi, nyv, av, bv);
+          stage_line_norms(&ay, p->K, alpha, beta, av, bv, s, w0, gB, gT, u, w, ub, tmp, uo, wo,
                            lu + (size_t)ii * K1, lw + (size_t)ii * K1);
         }
         free(buf);
@@ -480,9 +514,10 @@ int or_run(const or_problem* p, double* U, double* Vb, double* Wb, int m0, int n
     if (p->kchosen) p->kchosen[2 * st + 1] = Kc;
 #pragma omp parallel
     {
-      double* buf = (double*)malloc(sizeof(double) * 6 * L);
+      double* buf = (double*)malloc(sizeof(double) * 8 * L);
       double *u = buf, *w = buf + L, *ub = buf + 2 * L, *tmp = buf + 3 * L, *s = buf + 4 * L,
              *w0 = buf + 5 * L;
+      double *av = het ? buf + 6 * L : NULL, *bv = het ? buf + 7 * L : NULL;
 #pragma omp for schedule(static)
       for (int ii = 0; ii < nxi; ++ii) {
         const int i = ii + 1;
@@ -490,7 +525,8 @@ int or_run(const or_problem* p, double* U, double* Vb, double* Wb, int m0, int n
         const double gT = (p->edges[1] ? p->edges[1][i] : 0.0) * gb_1;
         for (int r = 0; r < nyi; ++r) s[r] = S2[(size_t)r * nxi + ii];
         for (int r = 0; r < nyv; ++r) w0[r] = Ws[(size_t)r * nxi + ii];
-        stage_line(&ay, Kc, alpha, beta, s, w0, gB, gT, u, w, ub, tmp);
+        if (het) col_coefs(p, ii, nxu, nxi, nyi, nyv, av, bv);
+        stage_line(&ay, Kc, alpha, beta, av, bv, s, w0, gB, gT, u, w, ub, tmp);
         for (int r = 0; r < nyi; ++r) U[(size_t)(r + 1) * nxu + i] = u[r];
         for (int r = 0; r < nyv; ++r) Wb[(size_t)r * nxi + ii] = w[r];
       }
@@ -516,8 +552,11 @@ int or_run_flat(int method, int nx, int ny, double h, double dt, double c, doubl
                 const double* phi, int src_ix, int src_iy, const double* gf, int ngf,
                 const double* ey0, const double* ey1, const double* ex0, const double* ex1,
                 const double* gb, int ngb, double* U, double* Vb, double* Wb, int m0,
-                int nsteps, int nthreads, double eps, int kmin, int* kchosen, double* tests) {
+                int nsteps, int nthreads, double eps, int kmin, int* kchosen, double* tests,
+                const double* kappa, const double* rv, const double* rw) {
   or_problem p;
+  if ((kappa != NULL) != (rv != NULL) || (kappa != NULL) != (rw != NULL)) return -1;
+  p.kappa = kappa; p.rv = rv; p.rw = rw;
   p.method = method; p.nx = nx; p.ny = ny; p.K = K;
   p.eps = eps; p.kmin = kmin; p.kchosen = kchosen; p.tests = tests;
   if (eps > 0.0 && (kmin < 2 || kmin > K)) return -1;
@@ -535,13 +574,13 @@ int or_run_flat(int method, int nx, int ny, double h, double dt, double c, doubl
 
 /* One ADI stage on a single line (exported for the dense-LU stage pin). */
 int or_stage_line(int method, int n, double h, int K, double alpha, double beta,
-                  const double* s, const double* v0, double gL, double gR,
+                  const double* av, const double* bv, const double* s, const double* v0, double gL, double gR,
                   double* u, double* v) {
   axis_t a;
   int e = axis_init(&a, method, n, h);
   if (e) return e;
   double* ub = (double*)malloc(sizeof(double) * 2 * (n + 8));
-  stage_line(&a, K, alpha, beta, s, v0, gL, gR, u, v, ub, ub + n + 8);
+  stage_line(&a, K, alpha, beta, av, bv, s, v0, gL, gR, u, v, ub, ub + n + 8);
   free(ub);
   axis_free(&a);
   return 0;
