@@ -154,6 +154,23 @@ int adi_set_point_sources(adi_handle h, const int* ix, const int* iy, const doub
  * (x = 1, nrowsU); NULL = homogeneous.  g: table at half steps (NULL: 1). */
 int adi_set_boundary(adi_handle h, const double* edges, const double* g, int ng);
 
+/* Heterogeneous media: the material matrices K = kappa(x,y)
+ * and R = rho^-1(x,y) of Alg. 1-4 ("K.*( )", "R.*( )" after the
+ * derivative).  Host arrays, fp32, C order, one
+ * medium for every grid of a batch:
+ *   kappa  : the U layout (nrowsU x ncolsU); interior points used
+ *   rinv_v : rho^-1 on the V̄ layout (V's shape above)
+ *   rinv_w : rho^-1 on the W̄ layout (W's shape above)
+ * (CFD is nodal: rinv_v = R[1:-1, :], rinv_w = R[:, 1:-1] of one nodal field.)
+ * The step then uses alpha_i = dt/2 kappa_i and beta_j = dt/2 rho^-1_j per point
+ * in place of the scalars c, ADI_RHO; all arithmetic stays fp64 (the fp32 inputs
+ * are promoted exactly).  Copied synchronously; all three NULL returns to the
+ * scalar medium.  Errors: ADI_EINVAL if only some are NULL or a used value is not
+ * finite and > 0; ADI_ESTATE during a call; ADI_WUNSTABLE (fields set) if
+ * sqrt(max kappa * max rho^-1) dt/h exceeds the inner-iteration limit.  Not
+ * combinable with ADI_EPS > 0 (adi_step returns ADI_EINVAL). */
+int adi_set_media(adi_handle h, const float* kappa, const float* rinv_v, const float* rinv_w);
+
 /* Enqueue n >= 0 time steps on the handle's stream (asynchronous unless
  * ADI_CHECK_FINITE is set). */
 int adi_step(adi_handle h, int n);

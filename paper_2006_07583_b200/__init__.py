@@ -76,6 +76,7 @@ def lib():
         L.adi_set_source.argtypes = [H, P, I, I, P, I]
         L.adi_set_point_sources.argtypes = [H, P, P, P, I]
         L.adi_set_boundary.argtypes = [H, P, P, I]
+        L.adi_set_media.argtypes = [H, P, P, P]
         L.adi_step.argtypes = [H, I]
         L.adi_get_fields.argtypes = [H, P, P, P]
         L.adi_get_fields_device.argtypes = [H, P, P, P]
@@ -103,7 +104,7 @@ def lib():
 
 EXPORTS = ["adi_create", "adi_create_batch", "adi_set_param", "adi_set_stream", "adi_set_fields",
            "adi_set_fields_device", "adi_set_source", "adi_set_point_sources", "adi_set_boundary",
-           "adi_step", "adi_step_begin", "adi_step_rows", "adi_step_cols", "adi_step_end", "adi_set_band",
+           "adi_set_media", "adi_step", "adi_step_begin", "adi_step_rows", "adi_step_cols", "adi_step_end", "adi_set_band",
            "adi_band_info", "adi_halo_bytes", "adi_halo_pack", "adi_halo_unpack",
            "adi_get_fields", "adi_get_fields_device", "adi_set_fields_async", "adi_get_fields_async", "adi_get_stats", "adi_get_kernel_times",
            "adi_set_trace", "adi_get_last_sweeps", "adi_last_error",
@@ -197,6 +198,13 @@ def adi_set_boundary(hd, edges=None, g=None):
     g = _host(g)
     return _check(hd, lib().adi_set_boundary(hd, _ptr(e), _ptr(g), 0 if g is None else g.size),
                   "adi_set_boundary")
+
+
+def adi_set_media(hd, kappa=None, rinv_v=None, rinv_w=None):
+    """Heterogeneous media (f3): kappa (U layout), rho^-1 on the V̄ and W̄ layouts, as
+    fp32 (other dtypes are rounded to fp32); all None returns to the scalar medium."""
+    k, rv, rw = (_host(a, np.float32) for a in (kappa, rinv_v, rinv_w))
+    return _check(hd, lib().adi_set_media(hd, _ptr(k), _ptr(rv), _ptr(rw)), "adi_set_media")
 
 
 def adi_step(hd, n):
@@ -343,6 +351,9 @@ class AdiSolver:
     def set_boundary(self, edges=None, g=None):
         adi_set_boundary(self.handle, edges, g)
 
+    def set_media(self, kappa=None, rinv_v=None, rinv_w=None):
+        return adi_set_media(self.handle, kappa, rinv_v, rinv_w)
+
     def step(self, n=1):
         return adi_step(self.handle, n)
 
@@ -370,4 +381,6 @@ class AdiSolver:
         s.set_fields(p.U, p.V, p.W)
         s.set_source(p.phi, p.src, p.gf)
         s.set_boundary(p.edges, p.gb)
+        if getattr(p, "kappa", None) is not None:
+            s.set_media(p.kappa, p.rinv_v, p.rinv_w)
         return s

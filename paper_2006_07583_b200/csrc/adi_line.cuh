@@ -73,6 +73,7 @@ struct KParams {
   CUtensorMap tmS;   // S_in (or nothing in the prologue)
   CUtensorMap tmX;   // X_in
   CUtensorMap tmF;   // phi_src (batch extent 1)
+  CUtensorMap tmC;   // heterogeneous media (HET kernels): (kappa, rho^-1) fp32 pairs, batch extent 1
   int n;        // cells along the line; positions 0..n
   int line0;    // line of (blockIdx.x = 0, warp 0); 4-aligned
   int line_lo;  // lines [line_lo, nlines) are processed
@@ -95,6 +96,9 @@ struct KParams {
   double cx;        // x-op scale: beta/h  (MFD) or 3 beta/h  (CFD)
   double mA, mB, mC, mD;  // MFD interior stencil: cu/24, 9cu/8, cx/24, 9cx/8
   double half_dt;
+  // HET kernels (NEXT row f3): per-point coefficients a = ch * kappa (u-op), ch * rho^-1
+  // (x-op) from the staged (kappa, rho^-1) pairs; ch = dt/(2h) (MFD), 3 dt/(2h) (CFD)
+  double ch;
   int K;
   // inner stopping rule (Alg. 3/4): an attempt (KM_*_T) runs K sweeps, adds the
   // owned squared changes of u and x in its last sweep to norms[0], norms[1], and
@@ -189,7 +193,8 @@ struct Ctx {
 template <int M>
 struct Mfd {
   // u-op: out = B - a * D4 x  (a = alpha/h); neighbours xm2,xm1 (prev chunk), xp1
-  template <bool INTERIOR>
+  // (NOB: B = 0, the HET kernels' first pass)
+  template <bool INTERIOR, bool NOB = false>
   static __device__ __forceinline__ void uop(const Ctx<M>& c, const double (&x)[M],
                                              const double* __restrict__ B, double (&out)[M], double a,
                                              double xm2, double xm1, double xp1) {
@@ -200,31 +205,31 @@ struct Mfd {
       const double xl1 = (i >= 1) ? x[i - 1] : xm1;
       const double xr1 = (i + 1 < M) ? x[i + 1] : xp1;
       if (INTERIOR) {
-        out[i] = fma(cA, xr1 - xl2, fma(cB, xl1 - x[i], B[i]));
+        out[i] = fma(cA, xr1 - xl2, fma(cB, xl1 - x[i], (NOB ? 0.0 : B[i])));
       } else {
         const int p = c.s + i;
         if (p >= 2 && p <= c.n - 1) {
-          out[i] = fma(cA, xr1 - xl2, fma(cB, xl1 - x[i], B[i]));
+          out[i] = fma(cA, xr1 - xl2, fma(cB, xl1 - x[i], (NOB ? 0.0 : B[i])));
         } else if (p == 1) {
           if (i >= 1 && i + 4 < M) {
             double s = 0.0;
 #pragma unroll
             for (int k = 0; k < 6; ++k) s = fma(c_d4r0[k], x[i - 1 + k], s);
-            out[i] = fma(-a, s, B[i]);
+            out[i] = fma(-a, s, (NOB ? 0.0 : B[i]));
           }
         } else if (p == c.n) {
           if (i >= 5) {
             double s = 0.0;
 #pragma unroll
             for (int k = 0; k < 6; ++k) s = fma(-c_d4r0[5 - k], x[i - 5 + k], s);
-            out[i] = fma(-a, s, B[i]);
+            out[i] = fma(-a, s, (NOB ? 0.0 : B[i]));
           }
         }
       }
     }
   }
   // x-op: out = B - b * G4 ū ; neighbours um1 (prev chunk), up1, up2 (next chunk)
-  template <bool INTERIOR>
+  template <bool INTERIOR, bool NOB = false>
   static __device__ __forceinline__ void xop(const Ctx<M>& c, const double (&u)[M],
                                              const double* __restrict__ B, double (&out)[M], double b,
                                              double um1, double up1, double up2) {
@@ -235,25 +240,25 @@ struct Mfd {
       const double ur1 = (i + 1 < M) ? u[i + 1] : up1;
       const double ur2 = (i + 2 < M) ? u[i + 2] : (i + 1 == M ? up2 : up1);
       if (INTERIOR) {
-        out[i] = fma(cC, ur2 - ul1, fma(cD, u[i] - ur1, B[i]));
+        out[i] = fma(cC, ur2 - ul1, fma(cD, u[i] - ur1, (NOB ? 0.0 : B[i])));
       } else {
         const int p = c.s + i;
         const int n = c.n;
         if (p >= 2 && p <= n - 2) {
-          out[i] = fma(cC, ur2 - ul1, fma(cD, u[i] - ur1, B[i]));
+          out[i] = fma(cC, ur2 - ul1, fma(cD, u[i] - ur1, (NOB ? 0.0 : B[i])));
         } else if (p == 0) {
           if (i + 5 < M) {
             double s = 0.0;
 #pragma unroll
             for (int k = 0; k < 6; ++k) s = fma(c_g4r0[k], u[i + k], s);
-            out[i] = fma(-b, s, B[i]);
+            out[i] = fma(-b, s, (NOB ? 0.0 : B[i]));
           }
         } else if (p == 1) {
           if (i >= 1 && i + 3 < M) {
             double s = 0.0;
 #pragma unroll
             for (int k = 0; k < 5; ++k) s = fma(c_g4r1[k], u[i - 1 + k], s);
-            out[i] = fma(-b, s, B[i]);
+            out[i] = fma(-b, s, (NOB ? 0.0 : B[i]));
           }
         } else if (p == n - 1) {
           if (i >= 2 && i + 1 < M) {
@@ -262,7 +267,7 @@ struct Mfd {
 #pragma unroll
             for (int k = 0; k < 4; ++k) s = fma(-c_g4r1[4 - k], u[i - 2 + k], s);
             s = fma(-c_g4r1[0], c.gR, s);
-            out[i] = fma(-b, s, B[i]);
+            out[i] = fma(-b, s, (NOB ? 0.0 : B[i]));
           }
         } else if (p == n) {
           if (i >= 4) {
@@ -270,7 +275,7 @@ struct Mfd {
 #pragma unroll
             for (int k = 0; k < 5; ++k) s = fma(-c_g4r0[5 - k], u[i - 4 + k], s);
             s = fma(-c_g4r0[0], c.gR, s);
-            out[i] = fma(-b, s, B[i]);
+            out[i] = fma(-b, s, (NOB ? 0.0 : B[i]));
           }
         }
       }
@@ -369,7 +374,7 @@ struct MfdSplit {
 };
 
 // MFD closure rows at the line end of a lean tile (same arithmetic as Mfd<M>::uop/xop)
-template <int M>
+template <int M, bool NOB = false>
 __device__ __forceinline__ void mfd_end_u(const Ctx<M>& c, const double (&x)[M], const double* __restrict__ B,
                                           double (&out)[M], double a) {
   static_assert(M == 32, "end fix-ups assume 32-point chunks");
@@ -378,57 +383,57 @@ __device__ __forceinline__ void mfd_end_u(const Ctx<M>& c, const double (&x)[M],
     double s = 0.0;
 #pragma unroll
     for (int k = 0; k < 6; ++k) s = fma(c_d4r0[k], x[k], s);
-    out[1] = fma(-a, s, B[1]);
+    out[1] = fma(-a, s, (NOB ? 0.0 : B[1]));
   } else {
     const int i = (c.endc == 1) ? 31 : 30;  // position n
     double s = 0.0;
     if (c.endc == 1) {
 #pragma unroll
       for (int k = 0; k < 6; ++k) s = fma(-c_d4r0[5 - k], x[26 + k], s);
-      out[31] = fma(-a, s, B[31]);
+      out[31] = fma(-a, s, (NOB ? 0.0 : B[31]));
     } else {
 #pragma unroll
       for (int k = 0; k < 6; ++k) s = fma(-c_d4r0[5 - k], x[25 + k], s);
-      out[30] = fma(-a, s, B[30]);
+      out[30] = fma(-a, s, (NOB ? 0.0 : B[30]));
       out[31] = 0.0;
     }
     (void)i;
   }
 }
-template <int M>
+template <int M, bool NOB = false>
 __device__ __forceinline__ void mfd_end_x(const Ctx<M>& c, const double (&u)[M], const double* __restrict__ B,
                                           double (&out)[M], double b) {
   if (c.endc == 0) {
     double s = 0.0;
 #pragma unroll
     for (int k = 0; k < 6; ++k) s = fma(c_g4r0[k], u[k], s);
-    out[0] = fma(-b, s, B[0]);
+    out[0] = fma(-b, s, (NOB ? 0.0 : B[0]));
     s = 0.0;
 #pragma unroll
     for (int k = 0; k < 5; ++k) s = fma(c_g4r1[k], u[k], s);
-    out[1] = fma(-b, s, B[1]);
+    out[1] = fma(-b, s, (NOB ? 0.0 : B[1]));
   } else if (c.endc == 1) {
     double s = 0.0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) s = fma(-c_g4r1[4 - k], u[28 + k], s);
     s = fma(-c_g4r1[0], c.gR, s);
-    out[30] = fma(-b, s, B[30]);
+    out[30] = fma(-b, s, (NOB ? 0.0 : B[30]));
     s = 0.0;
 #pragma unroll
     for (int k = 0; k < 5; ++k) s = fma(-c_g4r0[5 - k], u[27 + k], s);
     s = fma(-c_g4r0[0], c.gR, s);
-    out[31] = fma(-b, s, B[31]);
+    out[31] = fma(-b, s, (NOB ? 0.0 : B[31]));
   } else {
     double s = 0.0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) s = fma(-c_g4r1[4 - k], u[27 + k], s);
     s = fma(-c_g4r1[0], c.gR, s);
-    out[29] = fma(-b, s, B[29]);
+    out[29] = fma(-b, s, (NOB ? 0.0 : B[29]));
     s = 0.0;
 #pragma unroll
     for (int k = 0; k < 5; ++k) s = fma(-c_g4r0[5 - k], u[26 + k], s);
     s = fma(-c_g4r0[0], c.gR, s);
-    out[30] = fma(-b, s, B[30]);
+    out[30] = fma(-b, s, (NOB ? 0.0 : B[30]));
     out[31] = 0.0;
   }
 }
@@ -478,6 +483,29 @@ __device__ __forceinline__ void warp_edges(int lane, const double (&a)[M], doubl
   pm1 = lane == 0 ? 0.0 : pm1;
   np1 = lane == 31 ? 0.0 : np1;
   np2 = lane == 31 ? 0.0 : np2;
+}
+
+// Heterogeneous media (NEXT row f3; Alg. 3/4 "K.*( )", "R.*( )"):
+// the second pass of a HET operator.  The first pass ran the homogeneous code with
+// a unit coefficient and no base (out = -T^{-1} r or the negated stencil); here
+// out_i = B_i + a_i out_i with a_i = ch * (kappa_i | rho^-1_i) read from the staged
+// (kappa, rho^-1) fp32 pairs, at the positions the operator defines ([lo, hi]);
+// the other positions keep their Dirichlet slots.
+template <int M, bool UOP, bool EDGE>
+__device__ __forceinline__ void het_apply(const Ctx<M>& c, const double* Crow, const double* __restrict__ B,
+                                          double (&out)[M], double ch, int lo, int hi) {
+  const float4* C4 = reinterpret_cast<const float4*>(Crow);   // (kappa, R) of 2 positions
+  const double2* B2 = reinterpret_cast<const double2*>(B);
+  const bool all = !EDGE && !c.me;   // lean tile, no line end in this chunk
+#pragma unroll
+  for (int i = 0; i < M / 2; ++i) {
+    const float4 q = C4[i];
+    const double2 b = B2[i];
+    const double a0 = (double)(UOP ? q.x : q.y) * ch, a1 = (double)(UOP ? q.z : q.w) * ch;
+    const int p = c.s + 2 * i;
+    if (all || (p >= lo && p <= hi && (!EDGE || c.live))) out[2 * i] = fma(a0, out[2 * i], b.x);
+    if (all || (p + 1 >= lo && p + 1 <= hi && (!EDGE || c.live))) out[2 * i + 1] = fma(a1, out[2 * i + 1], b.y);
+  }
 }
 
 // CFD LU tables of the line ends staged in shared memory by edge tiles:
@@ -537,7 +565,7 @@ constexpr int NSUB = 4;
 // previous chunk's last and the next chunk's first position (the operand
 // neighbours of the next op).  st: statics of this warp's chunks [5][32].
 // ===========================================================================
-template <int M, bool UOP, bool EDGE>
+template <int M, bool UOP, bool EDGE, bool NOB = false>
 __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int lane,
                                           const double* st, const double* etab, const double (&o)[M],
                                           const double* __restrict__ B, double (&out)[M],
@@ -674,7 +702,7 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
       const double cy = coef * ycT[j], cz = coef * zcT[j];
 #pragma unroll
       for (int i = 0; i < L; ++i)
-        out[j * L + i] = fma(-c_sJ[i], cz, fma(-c_sK[i], cy, fma(-ci, out[j * L + i], B[j * L + i])));
+        out[j * L + i] = fma(-c_sJ[i], cz, fma(-c_sK[i], cy, fma(-ci, out[j * L + i], NOB ? 0.0 : B[j * L + i])));
     }
     if (!EDGE && c.me) {
       if (c.endc == 0) wb_apply<C0, true, M>(out, coef, g0, g1, g2);
@@ -715,7 +743,7 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
       const bool act = UOP ? (p >= 1 && p <= c.n - 1) : (p >= 0 && p <= c.n);
       double slot = 0.0;
       if (UOP) slot = (p == 0) ? c.gL : ((p == c.n) ? c.gR : 0.0);
-      out[i] = act ? fma(-coef, out[i], B[i]) : slot;
+      out[i] = act ? fma(-coef, out[i], NOB ? 0.0 : B[i]) : slot;
     }
   }
   nop1 = fma(-coef, zcarry, Bn_first);
@@ -723,7 +751,7 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
 }
 
 // Occupancy targets (resident CTAs per SM) for the NW-warp CTAs.
-template <int METHOD, bool EDGE, int MODE>
+template <int METHOD, bool EDGE, int MODE, bool HET = false>
 struct Occ {
 #ifndef ADI_CFD_OCC
 #define ADI_CFD_OCC 3
@@ -731,7 +759,9 @@ struct Occ {
   // 168 registers: MFD, and the lean CFD kernel (u_K parked in shared memory);
   // the generic CFD kernel keeps 255 registers
   // (the norm pass of the stopping rule keeps the previous iterates: 255 registers)
-  static constexpr int value = (MODE == KM_SWEEP_T || MODE == KM_FINAL_T) ? 2
+  // HET (three staging tiles per line): 2, the CFD edge kernel 1 (shared memory)
+  static constexpr int value = HET ? ((METHOD == M_CFD && EDGE) ? 1 : 2)
+                               : (MODE == KM_SWEEP_T || MODE == KM_FINAL_T) ? 2
                                : (METHOD == M_MFD) ? 3 : (EDGE ? 2 : ADI_CFD_OCC);
 };
 
@@ -739,12 +769,12 @@ __host__ __device__ constexpr int PADM_OF(int M) { return M + 2; }
 // line stride of the staging tile: 32 padded chunks, rounded to 128 B (TMA destination)
 __host__ __device__ constexpr int LSTR_OF(int M) { return (32 * (M + 2) + 15) / 16 * 16; }
 
-// shared memory of one CTA: padded staging of S and X for NW lines (+ CFD statics)
-// (the CFD chunk statics are only needed by edge tiles)
-template <int METHOD, int M, int NW, bool EDGE>
+// shared memory of one CTA: padded staging of S and X (HET: and the media pairs) for
+// NW lines (+ CFD statics; the CFD chunk statics are only needed by edge tiles)
+template <int METHOD, int M, int NW, bool EDGE, bool HET = false>
 constexpr size_t line_smem_bytes() {
-  return sizeof(double) *
-             (size_t)(2 * NW * LSTR_OF(M) + (METHOD == M_CFD && EDGE ? NW * 10 * 32 + 6 * ETAB : 0) + NW) +
+  return sizeof(double) * (size_t)((HET ? 3 : 2) * NW * LSTR_OF(M) +
+                                   (METHOD == M_CFD && EDGE ? NW * 10 * 32 + 6 * ETAB : 0) + NW) +
          128;
 }
 
@@ -763,7 +793,7 @@ __device__ __forceinline__ void tma_load_seg(double* dst, const CUtensorMap* tm,
 // are interior and live (the lean path, no generic closures, no per-chunk
 // predicates); EDGE = true: line ends, dead chunks, short lines.
 // ===========================================================================
-template <int METHOD, int M, int NW, int MODE_, bool EDGE>
+template <int METHOD, int M, int NW, int MODE_, bool EDGE, bool HET = false>
 __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, double* smem) {
   // stopping-rule attempts are SWEEP / FINAL tiles with the last-sweep test
   constexpr bool TEST = (MODE_ == KM_SWEEP_T || MODE_ == KM_FINAL_T);
@@ -776,7 +806,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   static_assert(NW == 4, "the transposed store pairs the 4 lines of a CTA by half-warps");
   double* stS = smem;             // [NW][LSTR]: S (or U in the prologue), later phi, then S'
   double* stX = stS + NW * LSTR;  // [NW][LSTR]: X, then X'
-  double* stc = stX + NW * LSTR;  // CFD statics [NW][2 sys][5][32] (edge tiles)
+  double* stC = stX + NW * LSTR;  // HET: [NW][LSTR] (kappa, rho^-1) fp32 pairs
+  double* stc = stC + (HET ? NW * LSTR : 0);  // CFD statics [NW][2 sys][5][32] (edge tiles)
   double* etab = stc + NW * 10 * 32;  // CFD line-end LU tables [2][3][ETAB] (edge tiles)
   unsigned long long* wbars =
       (unsigned long long*)(stc + (METHOD == M_CFD && EDGE ? NW * 10 * 32 + 6 * ETAB : 0));  // [NW] mbarriers
@@ -815,14 +846,16 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   // ---- load: one TMA tensor copy per array and warp (zero fill outside the array)
   double* lS = stS + w * LSTR;
   double* lX = stX + w * LSTR;
+  double* lC = stC + w * LSTR;
   unsigned long long* wbar = wbars + w;
   unsigned wpar = 0;  // parity of the warp mbarrier's next phase
   const int sh = sg.start + TMA_P0;
   const int c1 = (sh & 31) >> 1, c2 = sh >> 5;
   if (lane == 0) {
     mbar_init(wbar, 1);
-    mbar_expect_tx(wbar, BOX_BYTES * (MODE == KM_PROLOGUE ? 1u : 2u));
+    mbar_expect_tx(wbar, BOX_BYTES * ((MODE == KM_PROLOGUE ? 1u : 2u) + (HET ? 1u : 0u)));
     tma_load_seg(lX, &P.tmX, c1, c2, line, b, wbar);
+    if (HET) tma_load_seg(lC, &P.tmC, c1, c2, line, 0, wbar);   // one medium for the batch
     if (MODE != KM_PROLOGUE) tma_load_seg(lS, &P.tmS, c1, c2, line, b, wbar);
   }
   __syncwarp();  // the barrier is initialised before any lane waits on it
@@ -888,6 +921,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
 
   double* Sm = lS + lane * PADM;  // this chunk's bases in shared memory
   double* Vm = lX + lane * PADM;
+  const double* Cm = lC + lane * PADM;  // HET: this chunk's (kappa, rho^-1) pairs
   double u[M], x[M];
   {
     const double2* V2 = reinterpret_cast<const double2*>(Vm);
@@ -1003,6 +1037,14 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       for (int k = 0; k < 5; ++k) stXs[k * 32 + lane] = c.live ? q[k] : 0.0;
     }
     double d0, d1, xm1, xp1, um1, up1;
+    // HET: coefficients at the previous chunk's last / the next chunk's first position
+    // (the neighbour outputs of each operator)
+    double kP = 0.0, kN = 0.0, rP = 0.0, rN = 0.0;
+    if constexpr (HET) {
+      const float* Cf = reinterpret_cast<const float*>(lC);
+      if (lane > 0) { kP = (double)Cf[2 * ((lane - 1) * PADM + M - 1)] * P.ch; rP = (double)Cf[2 * ((lane - 1) * PADM + M - 1) + 1] * P.ch; }
+      if (lane < 31) { kN = (double)Cf[2 * ((lane + 1) * PADM)] * P.ch; rN = (double)Cf[2 * ((lane + 1) * PADM) + 1] * P.ch; }
+    }
     const double SLp = lane > 0 ? lS[(lane - 1) * PADM + M - 1] : 0.0;
     const double SFn = lane < 31 ? lS[(lane + 1) * PADM] : 0.0;
     const double VLp = lane > 0 ? lX[(lane - 1) * PADM + M - 1] : 0.0;
@@ -1014,7 +1056,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       // at most two 32-point arrays live: U stays in the S tile, W is re-read from
       // the X tile, W* is staged for output before the u-op
       double e1, e2;
-      cfd_apply<M, false, EDGE>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, 0.0, 0.0, e1, e2);
+      cfd_apply<M, false, EDGE, HET>(c, P, lane, stXs, etab, u, Vm, x, HET ? 1.0 : P.cx, um1, up1, 0.0, 0.0, e1, e2);
+      if constexpr (HET) het_apply<M, false, EDGE>(c, Cm, Vm, x, P.ch, 0, n);
       add_source_global(Sm);   // S = U + dt/2 F
       double wv[M];
       {
@@ -1027,7 +1070,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
           V2[i] = make_double2(x[2 * i], x[2 * i + 1]);
         }
       }
-      cfd_apply<M, true, EDGE>(c, P, lane, stU, etab, wv, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
+      cfd_apply<M, true, EDGE, HET>(c, P, lane, stU, etab, wv, Sm, u, HET ? 1.0 : P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
+      if constexpr (HET) het_apply<M, true, EDGE>(c, Cm, Sm, u, P.ch, 1, uhi);
     } else {
       double uo[TEST ? M : 1], xo[TEST ? M : 1];
       for (int k = 0; k < KK; ++k) {
@@ -1037,7 +1081,14 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
             for (int i = 0; i < M; ++i) { uo[i] = u[i]; xo[i] = x[i]; }
           }
         }
-        cfd_apply<M, true, EDGE>(c, P, lane, stU, etab, x, Sm, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
+        if constexpr (HET) {
+          cfd_apply<M, true, EDGE, true>(c, P, lane, stU, etab, x, Sm, u, 1.0, xm1, xp1, 0.0, 0.0, um1, up1);
+          het_apply<M, true, EDGE>(c, Cm, Sm, u, P.ch, 1, uhi);
+          um1 = fma(kP, um1, SLp);
+          up1 = fma(kN, up1, SFn);
+        } else {
+          cfd_apply<M, true, EDGE>(c, P, lane, stU, etab, x, Sm, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
+        }
         if (k + 1 == KK) {
           // park u_K in the (now dead) S tile: u is then dead across every x-op,
           // which keeps one 32-point array live instead of two (no spills at 3 CTAs/SM)
@@ -1045,7 +1096,14 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
 #pragma unroll
           for (int i = 0; i < M / 2; ++i) S2[i] = make_double2(u[2 * i], u[2 * i + 1]);
         }
-        cfd_apply<M, false, EDGE>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, VFn, VLp, xm1, xp1);
+        if constexpr (HET) {
+          cfd_apply<M, false, EDGE, true>(c, P, lane, stXs, etab, u, Vm, x, 1.0, um1, up1, 0.0, 0.0, xm1, xp1);
+          het_apply<M, false, EDGE>(c, Cm, Vm, x, P.ch, 0, n);
+          xm1 = fma(rP, xm1, VLp);
+          xp1 = fma(rN, xp1, VFn);
+        } else {
+          cfd_apply<M, false, EDGE>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, VFn, VLp, xm1, xp1);
+        }
         if constexpr (TEST) {
           if (k + 1 == KK) norm_add(u, uo, x, xo);
         }
@@ -1053,7 +1111,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       if (MODE == KM_SWEEP) {
         double e1, e2;
         add_source_global(Sm);   // S = u_K + dt/2 F
-        cfd_apply<M, true, EDGE>(c, P, lane, stU, etab, x, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
+        cfd_apply<M, true, EDGE, HET>(c, P, lane, stU, etab, x, Sm, u, HET ? 1.0 : P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
+        if constexpr (HET) het_apply<M, true, EDGE>(c, Cm, Sm, u, P.ch, 1, uhi);
 #pragma unroll
         for (int i = 0; i < M; ++i) x[i] = fma(2.0, x[i], -Vm[i]);
       }
@@ -1064,18 +1123,45 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     const double cA = P.mA, cB = P.mB, cC = P.mC, cD = P.mD;
     double xm2, xm1, xp1, xp2, um2, um1, up1, up2;
     auto u_op = [&](const double (&opd)[M], const double* __restrict__ B) {
-      if (c.interior) { MfdSplit<M>::bases(B, u); MfdSplit<M>::u_inner(opd, u, cA, cB); }
-      warp_edges<M>(lane, opd, xm2, xm1, xp1, xp2);
-      if (c.interior) MfdSplit<M>::u_edges(opd, u, cA, cB, xm2, xm1, xp1);
-      else Mfd<M>::template uop<false>(c, opd, B, u, au, xm2, xm1, xp1);
-      if (!EDGE && c.me) mfd_end_u<M>(c, opd, B, u, au);
+      if constexpr (HET) {
+        // unit coefficient, no base; then out = B + ch kappa_i out (het_apply)
+        if (c.interior) {
+#pragma unroll
+          for (int i = 0; i < M; ++i) u[i] = 0.0;
+          MfdSplit<M>::u_inner(opd, u, 1.0 / 24.0, 9.0 / 8.0);
+        }
+        warp_edges<M>(lane, opd, xm2, xm1, xp1, xp2);
+        if (c.interior) MfdSplit<M>::u_edges(opd, u, 1.0 / 24.0, 9.0 / 8.0, xm2, xm1, xp1);
+        else Mfd<M>::template uop<false, true>(c, opd, B, u, 1.0, xm2, xm1, xp1);
+        if (!EDGE && c.me) mfd_end_u<M, true>(c, opd, B, u, 1.0);
+        het_apply<M, true, EDGE>(c, Cm, B, u, P.ch, 1, uhi);
+      } else {
+        if (c.interior) { MfdSplit<M>::bases(B, u); MfdSplit<M>::u_inner(opd, u, cA, cB); }
+        warp_edges<M>(lane, opd, xm2, xm1, xp1, xp2);
+        if (c.interior) MfdSplit<M>::u_edges(opd, u, cA, cB, xm2, xm1, xp1);
+        else Mfd<M>::template uop<false>(c, opd, B, u, au, xm2, xm1, xp1);
+        if (!EDGE && c.me) mfd_end_u<M>(c, opd, B, u, au);
+      }
     };
     auto x_op = [&](const double* __restrict__ B) {
-      if (c.interior) { MfdSplit<M>::bases(B, x); MfdSplit<M>::x_inner(u, x, cC, cD); }
-      warp_edges<M>(lane, u, um2, um1, up1, up2);
-      if (c.interior) MfdSplit<M>::x_edges(u, x, cC, cD, um1, up1, up2);
-      else Mfd<M>::template xop<false>(c, u, B, x, bx, um1, up1, up2);
-      if (!EDGE && c.me) mfd_end_x<M>(c, u, B, x, bx);
+      if constexpr (HET) {
+        if (c.interior) {
+#pragma unroll
+          for (int i = 0; i < M; ++i) x[i] = 0.0;
+          MfdSplit<M>::x_inner(u, x, 1.0 / 24.0, 9.0 / 8.0);
+        }
+        warp_edges<M>(lane, u, um2, um1, up1, up2);
+        if (c.interior) MfdSplit<M>::x_edges(u, x, 1.0 / 24.0, 9.0 / 8.0, um1, up1, up2);
+        else Mfd<M>::template xop<false, true>(c, u, B, x, 1.0, um1, up1, up2);
+        if (!EDGE && c.me) mfd_end_x<M, true>(c, u, B, x, 1.0);
+        het_apply<M, false, EDGE>(c, Cm, B, x, P.ch, 0, n);
+      } else {
+        if (c.interior) { MfdSplit<M>::bases(B, x); MfdSplit<M>::x_inner(u, x, cC, cD); }
+        warp_edges<M>(lane, u, um2, um1, up1, up2);
+        if (c.interior) MfdSplit<M>::x_edges(u, x, cC, cD, um1, up1, up2);
+        else Mfd<M>::template xop<false>(c, u, B, x, bx, um1, up1, up2);
+        if (!EDGE && c.me) mfd_end_x<M>(c, u, B, x, bx);
+      }
     };
     if (MODE == KM_PROLOGUE) {
       // at most two 32-point arrays live (as for CFD): U stays in the S tile, W is
@@ -1201,8 +1287,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
 //   MODE = KM_FINAL   : as SWEEP without the fused explicit half; writes U_out
 //   MODE = KM_PROLOGUE: U_in, X_in -> a2 (explicit half only)
 // ===========================================================================
-template <int METHOD, int M, int NW, int MODE, bool EDGE>
-__global__ void __launch_bounds__(32 * NW, (Occ<METHOD, EDGE, MODE>::value))
+template <int METHOD, int M, int NW, int MODE, bool EDGE, bool HET = false>
+__global__ void __launch_bounds__(32 * NW, (Occ<METHOD, EDGE, MODE, HET>::value))
     adi_line_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(128) double smem_raw[];
   // TMA destinations need 128-byte alignment
@@ -1210,7 +1296,7 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD, EDGE, MODE>::value))
   double* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u) / 8u;
   if (P.gate && *P.gate) return;   // stopping rule: the stage was decided by an earlier attempt
   const Seg sg = P.segs[blockIdx.y];
-  line_tile<METHOD, M, NW, MODE, EDGE>(P, sg, smem);
+  line_tile<METHOD, M, NW, MODE, EDGE, HET>(P, sg, smem);
 }
 
 // The stopping rule after the attempt with k sweeps (Alg. 3/4 "until test <= eps or

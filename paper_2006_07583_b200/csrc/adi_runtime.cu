@@ -86,6 +86,12 @@ struct adi_ctx {
   double* phi = nullptr;    // source pattern, S layout (row-major)
   double* phiT = nullptr;   // its transpose (column sweep)
   double* edges = nullptr;  // y0 | y1 | x0 | x1
+  // heterogeneous media (adi_set_media, NEXT row f3): (kappa, rho^-1) fp32 pairs per
+  // position, Ca [y][x] pa (row sweep: rho^-1 at V̄ points), Cb [x][y] pb (column
+  // sweep: rho^-1 at W̄ points); one medium for the whole batch
+  double* Ca = nullptr;
+  double* Cb = nullptr;
+  bool het = false;
   // internal layouts: Sa, V, V2 row-major; Sb = S^T; W, W2 = W̄^T (columns contiguous)
   int* flag = nullptr;
   adi::Axis ax, ay;
@@ -193,6 +199,8 @@ int tmap_for(adi_ctx* h, const double* ptr, CUtensorMap* out) {
   else if (ptr == h->W || ptr == h->W2) { pitch = h->pw; rows = h->nxu; bs = h->aW; }
   else if (ptr == h->phi) { pitch = h->pa; rows = h->nyu; bs = h->aS; batch = 1; }
   else if (ptr == h->phiT) { pitch = h->pb; rows = h->nxu; bs = h->aS; batch = 1; }
+  else if (ptr == h->Ca) { pitch = h->pa; rows = h->nyu; bs = h->aS; batch = 1; }
+  else if (ptr == h->Cb) { pitch = h->pb; rows = h->nxu; bs = h->aS; batch = 1; }
   else return fail(h, ADI_EINVAL, "internal: no tensor map for this array");
   adi_ctx::TMap e;
   e.ptr = ptr;
@@ -553,10 +561,10 @@ struct TimeScope {
   }
 };
 
-template <int METHOD, int MODE, bool EDGE>
+template <int METHOD, int MODE, bool EDGE, bool HET>
 int launch_e(adi_ctx* h, const adi::Axis& A, adi::KParams p, int seg0, int nseg) {
-  auto kern = adi::adi_line_kernel<METHOD, adi::TM, adi::NW, MODE, EDGE>;
-  const size_t smem = adi::line_smem_bytes<METHOD, adi::TM, adi::NW, EDGE>();
+  auto kern = adi::adi_line_kernel<METHOD, adi::TM, adi::NW, MODE, EDGE, HET>;
+  const size_t smem = adi::line_smem_bytes<METHOD, adi::TM, adi::NW, EDGE, HET>();
   static bool attr = false;
   if (!attr) {
     CUDA_TRY(h, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -573,13 +581,22 @@ int launch_e(adi_ctx* h, const adi::Axis& A, adi::KParams p, int seg0, int nseg)
 }
 
 // interior segments first (lean kernel), then the segments with line ends
-template <int METHOD, int MODE>
+template <int METHOD, int MODE, bool HET = false>
 int launch_t(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
   if (A.l1 <= A.l0) return ADI_OK;
   const int nseg = (int)A.segs.size();
-  int rc = launch_e<METHOD, MODE, false>(h, A, p, 0, A.nint);
+  int rc = launch_e<METHOD, MODE, false, HET>(h, A, p, 0, A.nint);
   if (rc) return rc;
-  return launch_e<METHOD, MODE, true>(h, A, p, A.nint, nseg - A.nint);
+  return launch_e<METHOD, MODE, true, HET>(h, A, p, A.nint, nseg - A.nint);
+}
+
+// heterogeneous-media kernels (fixed K sweeps: the stopping rule is not combined with media)
+template <int METHOD>
+int launch_het(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p) {
+  if (mode == adi::KM_SWEEP) return launch_t<METHOD, adi::KM_SWEEP, true>(h, A, p);
+  if (mode == adi::KM_FINAL) return launch_t<METHOD, adi::KM_FINAL, true>(h, A, p);
+  if (mode == adi::KM_PROLOGUE) return launch_t<METHOD, adi::KM_PROLOGUE, true>(h, A, p);
+  return fail(h, ADI_EINVAL, "internal: no media kernel for this mode");
 }
 
 int launch(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p0, int kind) {
@@ -591,6 +608,10 @@ int launch(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p0, int
   if (p.S_in && (rc = tmap_for(h, p.S_in, &p.tmS))) return rc;
   if ((rc = tmap_for(h, p.X_in, &p.tmX))) return rc;
   if (p.phi_src && (rc = tmap_for(h, p.phi_src, &p.tmF))) return rc;
+  if (h->het) {
+    if ((rc = tmap_for(h, (&A == &h->ay) ? h->Cb : h->Ca, &p.tmC))) return rc;
+    return h->method == ADI_CFD ? launch_het<adi::M_CFD>(h, mode, A, p) : launch_het<adi::M_MFD>(h, mode, A, p);
+  }
   if (h->method == ADI_CFD) {
     if (mode == adi::KM_SWEEP) return launch_t<adi::M_CFD, adi::KM_SWEEP>(h, A, p);
     if (mode == adi::KM_FINAL) return launch_t<adi::M_CFD, adi::KM_FINAL>(h, A, p);
@@ -693,6 +714,7 @@ adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
   p.mC = p.cx * (1.0 / 24.0);
   p.mD = p.cx * (9.0 / 8.0);
   p.half_dt = h->dt / 2.0;
+  p.ch = f * h->dt / (2.0 * h->h);   // media: a_i = ch * kappa_i, ch * rho^-1_i
   p.K = h->K;
   p.tabU = A.d_tabU;
   p.tabX = A.d_tabX;
@@ -728,13 +750,35 @@ int stage_with_rule(adi_ctx* h, int mode_t, const adi::Axis& A, adi::KParams p, 
 void free_ctx(adi_ctx* h) {
   for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
-  for (double* q : {h->Ubase, h->V, h->W, h->V2, h->W2, h->Sa, h->Sb, h->phi, h->phiT}) dfree(q);
+  for (double* q : {h->Ubase, h->V, h->W, h->V2, h->W2, h->Sa, h->Sb, h->phi, h->phiT, h->Ca, h->Cb}) dfree(q);
   for (void* q : {(void*)h->edges, (void*)h->flag, (void*)h->d_norms, (void*)h->d_k})
     if (q) cudaFree(q);
   for (adi::Axis* A : {&h->ax, &h->ay})
     for (void* q : {(void*)A->d_segs, (void*)A->d_tabU, (void*)A->d_tabX, (void*)A->d_ptl,
                     (void*)A->d_ptp})
       if (q) cudaFree(q);
+}
+
+// ---- heterogeneous media (NEXT row f3) ------------------------------------------
+// Ca[y][x] = (kappa(y, x) at u positions x = 1..nxi, rho^-1 of V̄ row y-1 at x = 0..nxv-1)
+__global__ void pack_media_rows(float2* Ca, int pa, int nyi, int nxi, int nxu, int nxv, const float* kap,
+                                const float* rv) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y + 1;
+  if (x >= pa || y > nyi) return;
+  float2 e;
+  e.x = (x >= 1 && x <= nxi) ? kap[(size_t)y * nxu + x] : 0.f;
+  e.y = (x < nxv) ? rv[(size_t)(y - 1) * nxv + x] : 0.f;
+  Ca[(size_t)y * pa + x] = e;
+}
+// Cb[x][y] = (kappa(y, x) at u positions y = 1..nyi, rho^-1 of W̄ (row y, column x-1) at y = 0..nyv-1)
+__global__ void pack_media_cols(float2* Cb, int pb, int nxi, int nyi, int nyv, int nxu, const float* kap,
+                                const float* rw) {
+  const int y = blockIdx.x * blockDim.x + threadIdx.x, x = blockIdx.y + 1;
+  if (y >= pb || x > nxi) return;
+  float2 e;
+  e.x = (y >= 1 && y <= nyi) ? kap[(size_t)y * nxu + x] : 0.f;
+  e.y = (y < nyv) ? rw[(size_t)y * nxi + (x - 1)] : 0.f;
+  Cb[(size_t)x * pb + y] = e;
 }
 
 }  // namespace
@@ -999,6 +1043,66 @@ int adi_set_boundary(adi_handle h, const double* edges, const double* g, int ng)
   return ADI_OK;
 }
 
+int adi_set_media(adi_handle h, const float* kappa, const float* rinv_v, const float* rinv_w) {
+  if (!h) return ADI_EINVAL;
+  h->err.clear();
+  if (h->in_call) return fail(h, ADI_ESTATE, "call in progress");
+  if (!kappa && !rinv_v && !rinv_w) {   // back to the scalar medium
+    h->tmaps.clear();
+    dfree(h->Ca); dfree(h->Cb);
+    h->Ca = h->Cb = nullptr;
+    h->het = false;
+    return ADI_OK;
+  }
+  if (!kappa || !rinv_v || !rinv_w) return fail(h, ADI_EINVAL, "kappa, rinv_v, rinv_w: all or none");
+  // values: finite and > 0; the CFL bound uses max kappa * max rho^-1 >= c_max^2
+  double kmax = 0, rmax = 0;
+  auto scan = [&](const float* a, size_t n, size_t r0, size_t r1, size_t rowlen, size_t c0, size_t c1,
+                  double& mx) -> bool {
+    (void)n;
+    for (size_t r = r0; r < r1; ++r)
+      for (size_t c = c0; c < c1; ++c) {
+        const float v = a[r * rowlen + c];
+        if (!(v > 0.f) || !std::isfinite(v)) return false;
+        mx = std::max(mx, (double)v);
+      }
+    return true;
+  };
+  if (!scan(kappa, h->nU, 1, h->nyu - 1, h->nxu, 1, h->nxu - 1, kmax) ||
+      !scan(rinv_v, h->nV, 0, h->nyi, h->nxv, 0, h->nxv, rmax) ||
+      !scan(rinv_w, h->nW, 0, h->nyv, h->nxi, 0, h->nxi, rmax))
+    return fail(h, ADI_EINVAL, "media values must be finite and > 0");
+  if (!h->Ca) {
+    h->tmaps.clear();
+    if (!(h->Ca = dalloc(h->aS)) || !(h->Cb = dalloc(h->aS))) {
+      dfree(h->Ca); h->Ca = nullptr;
+      return fail(h, ADI_ENOMEM, "media arrays");
+    }
+  }
+  float* tmp = nullptr;
+  const size_t nk = h->nU, nv = h->nV, nw = h->nW;
+  CUDA_TRY(h, cudaMalloc(&tmp, (nk + nv + nw) * sizeof(float)));
+  auto done = [&](int rc) { cudaStreamSynchronize(h->stream); cudaFree(tmp); return rc; };
+  if (cudaMemcpyAsync(tmp, kappa, nk * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
+      cudaMemcpyAsync(tmp + nk, rinv_v, nv * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
+      cudaMemcpyAsync(tmp + nk + nv, rinv_w, nw * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess)
+    return done(fail(h, ADI_ECUDA, "media copy"));
+  pack_media_rows<<<dim3((h->pa + 255) / 256, h->nyi), 256, 0, h->stream>>>(
+      reinterpret_cast<float2*>(h->Ca), h->pa, h->nyi, h->nxi, h->nxu, h->nxv, tmp, tmp + nk);
+  pack_media_cols<<<dim3((h->pb + 255) / 256, h->nxi), 256, 0, h->stream>>>(
+      reinterpret_cast<float2*>(h->Cb), h->pb, h->nxi, h->nyi, h->nyv, h->nxu, tmp, tmp + nk + nv);
+  if (cudaGetLastError() != cudaSuccess) return done(fail(h, ADI_ECUDA, "media pack"));
+  int rc = done(ADI_OK);
+  h->het = true;
+  const double cfl = std::sqrt(kmax * rmax) * h->dt / h->h;
+  const double lim = (h->method == ADI_MFD) ? 2.0 / std::sqrt(6.0) : 2.0 / std::sqrt(3.0);
+  if (rc == ADI_OK && cfl > lim) {
+    h->err = "c_max*dt/h above the inner-iteration limit";
+    return ADI_WUNSTABLE;
+  }
+  return rc;
+}
+
 // ---- one call = begin (prologue), n x {rows, cols}, end.  The phases are public so
 // that a multi-GPU driver can exchange halos between the row and column sweeps.
 int adi_step_begin(adi_handle h, int nsteps) {
@@ -1012,6 +1116,8 @@ int adi_step_begin(adi_handle h, int nsteps) {
     return fail(h, ADI_EINVAL, "source table too short for the requested steps");
   if (!h->gb.empty() && (long long)h->gb.size() < 2 * m1 + 1)
     return fail(h, ADI_EINVAL, "boundary table too short for the requested steps");
+  if (h->eps > 0.0 && h->het)
+    return fail(h, ADI_EINVAL, "the stopping rule (ADI_EPS > 0) is not available with media fields");
   if (h->eps > 0.0) {
     // the stopping rule tests norms of the whole grid: no band decomposition
     if (h->band_y0 > 0 || h->band_y1 < h->ay.n + 1)
