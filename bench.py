@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-n", type=int, default=4097, help="oracle sample grid (nodes)")
+    ap.add_argument("--media", action="store_true",
+                    help="NEXT row f3: the same workload in a smooth heterogeneous medium (adi_set_media)")
     return ap.parse_args()
 
 
@@ -160,20 +162,38 @@ def ncu_traffic():
 
 
 # ---------------------------------------------------------------------------
-def make_problem(method, n, steps, K):
+def make_problem(method, n, steps, K, media=False):
     from adi_inputs import MMS, mms_problem
-    return mms_problem(method, n, MMS(), steps=steps, K=K)
+    p = mms_problem(method, n, MMS(), steps=steps, K=K)
+    if media:
+        # a smooth medium (adi_inputs.media.Medium, scaled to c <= 1 so the CFL of the
+        # homogeneous workload holds), sampled as fp32 grids on the U, V̄, W̄ layouts
+        from adi_inputs.grid import Grid
+        from adi_inputs.media import Medium
+        md = Medium(k0=0.8, ak=0.25, r0=0.8, ar=0.25)
+        g = Grid(method, n, n)
+        xu, yu = g.u_xy()
+        xv, yv = g.v_xy()
+        xw, yw = g.w_xy()
+        f32 = lambda a: np.ascontiguousarray(a, dtype=np.float32)
+        p.kappa = f32(md.kappa(xu[None, :], yu[:, None]))
+        p.rinv_v = f32(md.R(xv[None, :], yv[:, None]))
+        p.rinv_w = f32(md.R(xw[None, :], yw[:, None]))
+    return p
 
 
-def kernel_bytes(method, n, kind, has_phi=True):
+def kernel_bytes(method, n, kind, has_phi=True, media=False):
     """Algorithmic HBM bytes of one launch: each line kernel reads the
     carried pressure field S and its velocity, writes both, and reads the dense
-    source once — 8 B per value, interior sizes of SURVEY §8b."""
+    source once — 8 B per value, interior sizes of SURVEY §8b; with media, one
+    8-byte (kappa, rho^-1) fp32 pair per line position."""
     from adi_inputs import interior_shape, shapes
     su, sv, sw = shapes(method, n, n)
     ns = int(np.prod(interior_shape(method, n, n)))
     nv, nw = int(np.prod(sv)), int(np.prod(sw))
     phi = ns if has_phi else 0
+    if media and kind in ("row", "col", "final", "prologue"):
+        return kernel_bytes(method, n, kind, has_phi) + 8 * (nv if kind == "row" else nw)
     if kind == "row":
         return 8 * (2 * ns + 2 * nv + phi)
     if kind == "col":
@@ -199,11 +219,14 @@ def run_ours(a, ws, rank, local):
     total_steps = a.warmup + a.steps
     solvers = {}
     for m in methods:
-        p = make_problem(m, n, total_steps + a.steps + 4, a.K)
+        p = make_problem(m, n, total_steps + a.steps + 4, a.K, a.media)
         s = adi.AdiSolver(p.nx, p.ny, p.h, p.dt, p.c, m, K=a.K, stream=stream.cuda_stream)
         s.set_fields(p.U, p.V, p.W)
         s.set_source(p.phi, p.src, p.gf)
         s.set_boundary(p.edges, p.gb)
+        if a.media:
+            s.set_media(p.kappa, p.rinv_v, p.rinv_w)
+            p.kappa = p.rinv_v = p.rinv_w = None
         p.phi = None  # copied by the library; keep host memory low (8 ranks per box)
         p.V = p.W = None  # zeros for the MMS start; recreated for the e2e leg
         bs = None
@@ -267,9 +290,9 @@ def run_ours(a, ws, rank, local):
         step_ms = per[m] / a.steps
         tot = sum(v[0] for v in ksum.values())
         kind, (kms, kcnt) = max(ksum.items(), key=lambda kv: kv[1][0])
-        byt = kernel_bytes(m, n, kind) / ws
+        byt = kernel_bytes(m, n, kind, media=a.media) / ws
         ach = byt / (kms / kcnt * 1e-3) / 1e9
-        bytes_step = (kernel_bytes(m, n, "row") + kernel_bytes(m, n, "col")) / ws
+        bytes_step = (kernel_bytes(m, n, "row", media=a.media) + kernel_bytes(m, n, "col", media=a.media)) / ws
         per_method[MNAME[m]] = {
             "value": pts * a.steps / (per[m] * 1e-3), "ms_per_step": step_ms,
             "hbm_gbs_step_per_gpu": bytes_step / (step_ms * 1e-3) / 1e9,
@@ -281,7 +304,7 @@ def run_ours(a, ws, rank, local):
                 "avg_ms": kms / kcnt, "cnt": kcnt}
         if dominant is None or cand["avg_ms"] * kcnt > dominant["avg_ms"] * dominant["cnt"]:
             dominant = cand
-    tkey = f"{dominant['method']}_{dominant['kind']}_{n}"
+    tkey = f"{dominant['method']}_{dominant['kind']}_{n}" + ("_media" if a.media else "")
     roof = {"bound": "hbm", "achieved": round(dominant["achieved"], 1), "peak": peak, "unit": "GB/s",
             "frac": round(dominant["achieved"] / peak, 4),
             "traffic": traffic.get(tkey, {}).get("dram_bytes_per_launch") if ws == 1 else None,
@@ -368,13 +391,13 @@ def run_ours(a, ws, rank, local):
 
 
 # ---------------------------------------------------------------------------
-def oracle_rate(methods, n, steps, K, threads=0):
+def oracle_rate(methods, n, steps, K, threads=0, media=False):
     """Oracle pt-updates/s on an n x n sample (bounded CPU work)."""
     import oracle
     tot_pts = 0
     tot_s = 0.0
     for m in methods:
-        p = make_problem(m, n, steps + 1, K)
+        p = make_problem(m, n, steps + 1, K, media)
         t0 = time.perf_counter()
         oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, p.U, p.V, p.W, nsteps=steps,
                    nthreads=threads, **p.oracle_kwargs())
@@ -400,6 +423,9 @@ def main():
            "cfl": {"cfd": 0.91, "mfd": 0.81}, "l2": "inputs larger than L2 (2.1 GB per field); no flush",
            "parallelism": "1 GPU" if ws == 1 else
            f"{ws} GPUs: one grid band-decomposed (rows), NCCL halo exchange per step"}
+    if a.media:
+        cfg["workload"] += " + heterogeneous medium (NEXT row f3: fp32 kappa, rho^-1 grids, adi_set_media)"
+        cfg["media"] = "smooth: kappa = 0.8 (1 + 0.25 sin(2 pi x + 0.3) cos(2 pi y)), rho^-1 analogous"
     if a.impl == "reference":
         # Reference arm = the CPU oracle as it stands, bounded sample per step.
         if rank != 0:
@@ -409,8 +435,8 @@ def main():
         nthr = cpu_cores()
         n = a.cpu_n
         for _ in range(a.warmup):
-            oracle_rate(methods, n, 1, a.K, nthr)
-        rate, secs = oracle_rate(methods, n, a.steps, a.K, nthr)
+            oracle_rate(methods, n, 1, a.K, nthr, a.media)
+        rate, secs = oracle_rate(methods, n, a.steps, a.K, nthr, a.media)
         line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": ws,
                 "steps": a.steps, "warmup": a.warmup, "ms_per_step": secs * 1e3 / a.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -430,7 +456,7 @@ def main():
         import oracle
         oracle.build()
         nthr = cpu_cores()
-        rate, secs = oracle_rate(methods, a.cpu_n, 12, a.K, nthr)
+        rate, secs = oracle_rate(methods, a.cpu_n, 12, a.K, nthr, a.media)
         cpu = {"value": rate, "unit": UNIT, "cores": nthr, "kind": "oracle",
                "sample": f"{a.cpu_n}x{a.cpu_n} nodes, 12 steps per method, same MMS data "
                          f"({secs:.1f} s of CPU time)"}

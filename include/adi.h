@@ -166,7 +166,7 @@ int adi_set_boundary(adi_handle h, const double* edges, const double* g, int ng)
  * in place of the scalars c, ADI_RHO; all arithmetic stays fp64 (the fp32 inputs
  * are promoted exactly).  Copied synchronously; all three NULL returns to the
  * scalar medium.  Errors: ADI_EINVAL if only some are NULL or a used value is not
- * finite and > 0; ADI_ESTATE during a call; ADI_WUNSTABLE (fields set) if
+ * finite, normal and > 0; ADI_ESTATE during a call; ADI_WUNSTABLE (fields set) if
  * sqrt(max kappa * max rho^-1) dt/h exceeds the inner-iteration limit.  Not
  * combinable with ADI_EPS > 0 (adi_step returns ADI_EINVAL). */
 int adi_set_media(adi_handle h, const float* kappa, const float* rinv_v, const float* rinv_w);

@@ -96,9 +96,6 @@ struct KParams {
   double cx;        // x-op scale: beta/h  (MFD) or 3 beta/h  (CFD)
   double mA, mB, mC, mD;  // MFD interior stencil: cu/24, 9cu/8, cx/24, 9cx/8
   double half_dt;
-  // HET kernels (NEXT row f3): per-point coefficients a = ch * kappa (u-op), ch * rho^-1
-  // (x-op) from the staged (kappa, rho^-1) pairs; ch = dt/(2h) (MFD), 3 dt/(2h) (CFD)
-  double ch;
   int K;
   // inner stopping rule (Alg. 3/4): an attempt (KM_*_T) runs K sweeps, adds the
   // owned squared changes of u and x in its last sweep to norms[0], norms[1], and
@@ -487,24 +484,54 @@ __device__ __forceinline__ void warp_edges(int lane, const double (&a)[M], doubl
 
 // Heterogeneous media (NEXT row f3; Alg. 3/4 "K.*( )", "R.*( )"):
 // the second pass of a HET operator.  The first pass ran the homogeneous code with
-// a unit coefficient and no base (out = -T^{-1} r or the negated stencil); here
-// out_i = B_i + a_i out_i with a_i = ch * (kappa_i | rho^-1_i) read from the staged
-// (kappa, rho^-1) fp32 pairs, at the positions the operator defines ([lo, hi]);
-// the other positions keep their Dirichlet slots.
-template <int M, bool UOP, bool EDGE>
+// kappa = rho = 1 and no base (out = -ch T^{-1} r, or the stencil times ch); here
+// out_i = B_i + m_i out_i with m_i = kappa_i (u-op) or rho^-1_i (x-op) from the staged
+// fp32 pairs, at the positions the operator defines ([lo, hi]); the other positions
+// keep their Dirichlet slots (lean tiles: restored after an unpredicated pass).
+//
+// fp32 -> fp64 of a positive normal float (adi_set_media admits only those): exact,
+// two integer operations instead of a conversion-unit F2F
+__device__ __forceinline__ double f32pos_to_f64(float f) {
+  const unsigned b = __float_as_uint(f);
+  return __hiloint2double((int)((b >> 3) + 0x38000000u), (int)(b << 29));
+}
+// 128-bit shared load of 4 floats (two (kappa, rho^-1) pairs); kept whole so the lanes'
+// 272-byte-strided rows stay bank-conflict free
+__device__ __forceinline__ float4 lds_f4(const void* p) {
+  float4 v;
+  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+template <int M, int METHOD, bool UOP, bool EDGE>
 __device__ __forceinline__ void het_apply(const Ctx<M>& c, const double* Crow, const double* __restrict__ B,
-                                          double (&out)[M], double ch, int lo, int hi) {
-  const float4* C4 = reinterpret_cast<const float4*>(Crow);   // (kappa, R) of 2 positions
+                                          double (&out)[M], int lo, int hi) {
   const double2* B2 = reinterpret_cast<const double2*>(B);
-  const bool all = !EDGE && !c.me;   // lean tile, no line end in this chunk
 #pragma unroll
   for (int i = 0; i < M / 2; ++i) {
-    const float4 q = C4[i];
+    const float4 q = lds_f4(Crow + 2 * i);
     const double2 b = B2[i];
-    const double a0 = (double)(UOP ? q.x : q.y) * ch, a1 = (double)(UOP ? q.z : q.w) * ch;
-    const int p = c.s + 2 * i;
-    if (all || (p >= lo && p <= hi && (!EDGE || c.live))) out[2 * i] = fma(a0, out[2 * i], b.x);
-    if (all || (p + 1 >= lo && p + 1 <= hi && (!EDGE || c.live))) out[2 * i + 1] = fma(a1, out[2 * i + 1], b.y);
+    const double m0 = f32pos_to_f64(UOP ? q.x : q.y), m1 = f32pos_to_f64(UOP ? q.z : q.w);
+    if (!EDGE) {
+      out[2 * i] = fma(m0, out[2 * i], b.x);
+      out[2 * i + 1] = fma(m1, out[2 * i + 1], b.y);
+    } else {
+      const int p = c.s + 2 * i;
+      if (p >= lo && p <= hi && c.live) out[2 * i] = fma(m0, out[2 * i], b.x);
+      if (p + 1 >= lo && p + 1 <= hi && c.live) out[2 * i + 1] = fma(m1, out[2 * i + 1], b.y);
+    }
+  }
+  if (!EDGE && c.me) {
+    // the slots of the line-end chunk (as the homogeneous end fix-ups leave them)
+    static_assert(M == 32, "end fix-ups assume 32-point chunks");
+    if (UOP) {
+      if (c.endc == 0) out[0] = c.gL;
+      else if (c.endc == 1) { if (METHOD == M_CFD) out[31] = c.gR; }
+      else { if (METHOD == M_CFD) out[30] = c.gR; out[31] = 0.0; }
+    } else if (c.endc == 2) {
+      out[31] = 0.0;
+    }
   }
 }
 
@@ -1042,8 +1069,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     double kP = 0.0, kN = 0.0, rP = 0.0, rN = 0.0;
     if constexpr (HET) {
       const float* Cf = reinterpret_cast<const float*>(lC);
-      if (lane > 0) { kP = (double)Cf[2 * ((lane - 1) * PADM + M - 1)] * P.ch; rP = (double)Cf[2 * ((lane - 1) * PADM + M - 1) + 1] * P.ch; }
-      if (lane < 31) { kN = (double)Cf[2 * ((lane + 1) * PADM)] * P.ch; rN = (double)Cf[2 * ((lane + 1) * PADM) + 1] * P.ch; }
+      if (lane > 0) { kP = (double)Cf[2 * ((lane - 1) * PADM + M - 1)]; rP = (double)Cf[2 * ((lane - 1) * PADM + M - 1) + 1]; }
+      if (lane < 31) { kN = (double)Cf[2 * ((lane + 1) * PADM)]; rN = (double)Cf[2 * ((lane + 1) * PADM) + 1]; }
     }
     const double SLp = lane > 0 ? lS[(lane - 1) * PADM + M - 1] : 0.0;
     const double SFn = lane < 31 ? lS[(lane + 1) * PADM] : 0.0;
@@ -1056,8 +1083,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       // at most two 32-point arrays live: U stays in the S tile, W is re-read from
       // the X tile, W* is staged for output before the u-op
       double e1, e2;
-      cfd_apply<M, false, EDGE, HET>(c, P, lane, stXs, etab, u, Vm, x, HET ? 1.0 : P.cx, um1, up1, 0.0, 0.0, e1, e2);
-      if constexpr (HET) het_apply<M, false, EDGE>(c, Cm, Vm, x, P.ch, 0, n);
+      cfd_apply<M, false, EDGE, HET>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, 0.0, 0.0, e1, e2);
+      if constexpr (HET) het_apply<M, METHOD, false, EDGE>(c, Cm, Vm, x, 0, n);
       add_source_global(Sm);   // S = U + dt/2 F
       double wv[M];
       {
@@ -1070,8 +1097,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
           V2[i] = make_double2(x[2 * i], x[2 * i + 1]);
         }
       }
-      cfd_apply<M, true, EDGE, HET>(c, P, lane, stU, etab, wv, Sm, u, HET ? 1.0 : P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
-      if constexpr (HET) het_apply<M, true, EDGE>(c, Cm, Sm, u, P.ch, 1, uhi);
+      cfd_apply<M, true, EDGE, HET>(c, P, lane, stU, etab, wv, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
+      if constexpr (HET) het_apply<M, METHOD, true, EDGE>(c, Cm, Sm, u, 1, uhi);
     } else {
       double uo[TEST ? M : 1], xo[TEST ? M : 1];
       for (int k = 0; k < KK; ++k) {
@@ -1082,8 +1109,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
           }
         }
         if constexpr (HET) {
-          cfd_apply<M, true, EDGE, true>(c, P, lane, stU, etab, x, Sm, u, 1.0, xm1, xp1, 0.0, 0.0, um1, up1);
-          het_apply<M, true, EDGE>(c, Cm, Sm, u, P.ch, 1, uhi);
+          cfd_apply<M, true, EDGE, true>(c, P, lane, stU, etab, x, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, um1, up1);
+          het_apply<M, METHOD, true, EDGE>(c, Cm, Sm, u, 1, uhi);
           um1 = fma(kP, um1, SLp);
           up1 = fma(kN, up1, SFn);
         } else {
@@ -1097,8 +1124,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
           for (int i = 0; i < M / 2; ++i) S2[i] = make_double2(u[2 * i], u[2 * i + 1]);
         }
         if constexpr (HET) {
-          cfd_apply<M, false, EDGE, true>(c, P, lane, stXs, etab, u, Vm, x, 1.0, um1, up1, 0.0, 0.0, xm1, xp1);
-          het_apply<M, false, EDGE>(c, Cm, Vm, x, P.ch, 0, n);
+          cfd_apply<M, false, EDGE, true>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, 0.0, 0.0, xm1, xp1);
+          het_apply<M, METHOD, false, EDGE>(c, Cm, Vm, x, 0, n);
           xm1 = fma(rP, xm1, VLp);
           xp1 = fma(rN, xp1, VFn);
         } else {
@@ -1111,8 +1138,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       if (MODE == KM_SWEEP) {
         double e1, e2;
         add_source_global(Sm);   // S = u_K + dt/2 F
-        cfd_apply<M, true, EDGE, HET>(c, P, lane, stU, etab, x, Sm, u, HET ? 1.0 : P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
-        if constexpr (HET) het_apply<M, true, EDGE>(c, Cm, Sm, u, P.ch, 1, uhi);
+        cfd_apply<M, true, EDGE, HET>(c, P, lane, stU, etab, x, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
+        if constexpr (HET) het_apply<M, METHOD, true, EDGE>(c, Cm, Sm, u, 1, uhi);
 #pragma unroll
         for (int i = 0; i < M; ++i) x[i] = fma(2.0, x[i], -Vm[i]);
       }
@@ -1128,13 +1155,13 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
         if (c.interior) {
 #pragma unroll
           for (int i = 0; i < M; ++i) u[i] = 0.0;
-          MfdSplit<M>::u_inner(opd, u, 1.0 / 24.0, 9.0 / 8.0);
+          MfdSplit<M>::u_inner(opd, u, cA, cB);
         }
         warp_edges<M>(lane, opd, xm2, xm1, xp1, xp2);
-        if (c.interior) MfdSplit<M>::u_edges(opd, u, 1.0 / 24.0, 9.0 / 8.0, xm2, xm1, xp1);
-        else Mfd<M>::template uop<false, true>(c, opd, B, u, 1.0, xm2, xm1, xp1);
-        if (!EDGE && c.me) mfd_end_u<M, true>(c, opd, B, u, 1.0);
-        het_apply<M, true, EDGE>(c, Cm, B, u, P.ch, 1, uhi);
+        if (c.interior) MfdSplit<M>::u_edges(opd, u, cA, cB, xm2, xm1, xp1);
+        else Mfd<M>::template uop<false, true>(c, opd, B, u, au, xm2, xm1, xp1);
+        if (!EDGE && c.me) mfd_end_u<M, true>(c, opd, B, u, au);
+        het_apply<M, METHOD, true, EDGE>(c, Cm, B, u, 1, uhi);
       } else {
         if (c.interior) { MfdSplit<M>::bases(B, u); MfdSplit<M>::u_inner(opd, u, cA, cB); }
         warp_edges<M>(lane, opd, xm2, xm1, xp1, xp2);
@@ -1148,13 +1175,13 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
         if (c.interior) {
 #pragma unroll
           for (int i = 0; i < M; ++i) x[i] = 0.0;
-          MfdSplit<M>::x_inner(u, x, 1.0 / 24.0, 9.0 / 8.0);
+          MfdSplit<M>::x_inner(u, x, cC, cD);
         }
         warp_edges<M>(lane, u, um2, um1, up1, up2);
-        if (c.interior) MfdSplit<M>::x_edges(u, x, 1.0 / 24.0, 9.0 / 8.0, um1, up1, up2);
-        else Mfd<M>::template xop<false, true>(c, u, B, x, 1.0, um1, up1, up2);
-        if (!EDGE && c.me) mfd_end_x<M, true>(c, u, B, x, 1.0);
-        het_apply<M, false, EDGE>(c, Cm, B, x, P.ch, 0, n);
+        if (c.interior) MfdSplit<M>::x_edges(u, x, cC, cD, um1, up1, up2);
+        else Mfd<M>::template xop<false, true>(c, u, B, x, bx, um1, up1, up2);
+        if (!EDGE && c.me) mfd_end_x<M, true>(c, u, B, x, bx);
+        het_apply<M, METHOD, false, EDGE>(c, Cm, B, x, 0, n);
       } else {
         if (c.interior) { MfdSplit<M>::bases(B, x); MfdSplit<M>::x_inner(u, x, cC, cD); }
         warp_edges<M>(lane, u, um2, um1, up1, up2);

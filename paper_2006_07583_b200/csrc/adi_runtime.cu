@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cfloat>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -704,8 +705,11 @@ adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
   p.pt_line = h->has_pt ? A.d_ptl : nullptr;
   p.pt_pos = h->has_pt ? A.d_ptp : nullptr;
   p.pt_amp = 1.0 / (h->h * h->h);
-  const double kappa = h->rho * h->c * h->c;
-  const double alpha = kappa * h->dt / 2.0, beta = h->dt / (2.0 * h->rho);
+  // with media the kernels' scalars are those of a unit medium (kappa = rho = 1); the
+  // per-point kappa_i, rho^-1_i multiply them in the HET second pass
+  const double kappa = h->het ? 1.0 : h->rho * h->c * h->c;
+  const double rho = h->het ? 1.0 : h->rho;
+  const double alpha = kappa * h->dt / 2.0, beta = h->dt / (2.0 * rho);
   const double f = (h->method == ADI_CFD) ? 3.0 : 1.0;
   p.cu = f * alpha / h->h;
   p.cx = f * beta / h->h;
@@ -714,7 +718,6 @@ adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
   p.mC = p.cx * (1.0 / 24.0);
   p.mD = p.cx * (9.0 / 8.0);
   p.half_dt = h->dt / 2.0;
-  p.ch = f * h->dt / (2.0 * h->h);   // media: a_i = ch * kappa_i, ch * rho^-1_i
   p.K = h->K;
   p.tabU = A.d_tabU;
   p.tabX = A.d_tabX;
@@ -1063,7 +1066,7 @@ int adi_set_media(adi_handle h, const float* kappa, const float* rinv_v, const f
     for (size_t r = r0; r < r1; ++r)
       for (size_t c = c0; c < c1; ++c) {
         const float v = a[r * rowlen + c];
-        if (!(v > 0.f) || !std::isfinite(v)) return false;
+        if (!(v >= FLT_MIN) || !std::isfinite(v)) return false;   // normal, > 0 (exact in-kernel widening)
         mx = std::max(mx, (double)v);
       }
     return true;
@@ -1071,7 +1074,7 @@ int adi_set_media(adi_handle h, const float* kappa, const float* rinv_v, const f
   if (!scan(kappa, h->nU, 1, h->nyu - 1, h->nxu, 1, h->nxu - 1, kmax) ||
       !scan(rinv_v, h->nV, 0, h->nyi, h->nxv, 0, h->nxv, rmax) ||
       !scan(rinv_w, h->nW, 0, h->nyv, h->nxi, 0, h->nxi, rmax))
-    return fail(h, ADI_EINVAL, "media values must be finite and > 0");
+    return fail(h, ADI_EINVAL, "media values must be finite normal floats > 0");
   if (!h->Ca) {
     h->tmaps.clear();
     if (!(h->Ca = dalloc(h->aS)) || !(h->Cb = dalloc(h->aS))) {
