@@ -58,6 +58,9 @@ def lib():
         for f in (_lib.or_cfd_Qf, _lib.or_cfd_Qbarf, _lib.or_mfd_D4f, _lib.or_mfd_G4f):
             f.restype = None
         _lib.or_num_threads.restype = I
+        _lib.or_run_full_flat.argtypes = [I, I, D, D, D, D, I, P, I, I, P, I, P, P, P, I, I, I, I, D]
+        _lib.or_run_full_flat.restype = I
+        _lib.or_stage_line_full.argtypes = [I, D, I, D, D, P, P, P, P]
     return _lib
 
 
@@ -205,3 +208,33 @@ def raw_operator(name, n, h, f):
 
 def num_threads() -> int:
     return lib().or_num_threads()
+
+
+def run_full(nx, ny, h, dt, c, K, U, V, W, *, rho=1.0, phi=None, src=None, gf=None, m0=0, nsteps=1,
+             nthreads=0, nb=0, a=0.015):
+    """NEXT row f4: the full-matrix CFD variant (readings F1-F2 in
+    adi_oracle.c): U, V, W are all ny x nx (every node unknown, no Dirichlet data),
+    every derivative is the full D = P^-1 Q, and after each step all fields are
+    multiplied by the Cerjan taper G(x) G(y) of width ``nb`` (0: none) and rate ``a``.
+    ``phi``: dense source on all nodes (ny x nx); ``src`` = (ix, iy) node of a point
+    source F = g_f / h^2."""
+    U, V, W = (np.array(x, dtype=np.float64, order="C", copy=True).reshape(ny, nx) for x in (U, V, W))
+    phi = _f64(phi)
+    if phi is not None:
+        assert phi.shape == (ny, nx)
+    gf = _f64(gf)
+    ix, iy = (-1, -1) if src is None else src
+    rc = lib().or_run_full_flat(nx, ny, h, dt, c, rho, K, _p(phi), ix, iy, _p(gf), 0 if gf is None else gf.size,
+                                _p(U), _p(V), _p(W), m0, nsteps, nthreads, int(nb), float(a))
+    if rc != 0:
+        raise RuntimeError(f"oracle or_run_full failed: {rc}")
+    return U, V, W
+
+
+def stage_line_full(n, h, K, alpha, beta, s, v0):
+    """One full-variant stage on one line (f4, reading F1): K sweeps of
+    u = s - alpha D v, v = v0 - beta D u with the full D = P^-1 Q (n+1 nodes)."""
+    s, v0 = _f64(s), _f64(v0)
+    u, v = np.zeros(n + 1), np.zeros(n + 1)
+    assert lib().or_stage_line_full(n, h, K, alpha, beta, _p(s), _p(v0), _p(u), _p(v)) == 0
+    return u, v

@@ -547,6 +547,167 @@ int or_run(const or_problem* p, double* U, double* Vb, double* Wb, int m0, int n
   return 0;
 }
 
+/* ------------------------------------------------------------------------ */
+/* NEXT row f4: the full-matrix CFD variant with a Cerjan absorbing layer.   */
+/* "By simply replacing reduced operators P̄ and Q̄, and reduced */
+/* matrices Ū, V̄, W̄, by their full matrix versions in previous formulation  */
+/* steps [...] the boundary wave fields can be also obtained.  These values  */
+/* can be further damped by the absorbing technique proposed in [Cerjan]."   */
+/* Readings (F1-F2):                                            */
+/*  F1  every node is unknown (U, V, W all ny x nx, no Dirichlet data); both   */
+/*      the pressure and the velocity derivatives are D = P^{-1} Q (full,     */
+/*      n+1 rows, App. A), in both directions; otherwise Alg. 1 / Alg. 3 in   */
+/*      their order: a2 W* = W - beta D_y U, S1 = U - alpha D_y W + dt/2 F^m;  */
+/*      rows: K sweeps u = S1 - alpha D_x v, v = V - beta D_x u; a4 S2 = u -   */
+/*      alpha D_x v + dt/2 F^{m+1}, V^{m+1} = v - beta D_x u; columns: K       */
+/*      sweeps u = S2 - alpha D_y w, w = W* - beta D_y u.                      */
+/*  F2  after each step U, V, W are multiplied by G(x) G(y), G(k) =            */
+/*      exp(-(a (nb - d_k))^2) for d_k = min(k, n - k) < nb, else 1 (the      */
+/*      Cerjan et al. 1985 taper; nb, a are parameters).                       */
+/* phi (if set) is on all nodes (ny x nx); a point source at U index (ix,iy). */
+/* ------------------------------------------------------------------------ */
+static void stage_line_full(const axis_t* a, int K, double alpha, double beta, const double* s,
+                            const double* v0, double* u, double* v, double* tmp) {
+  const int n1 = a->nv; /* n + 1 */
+  for (int i = 0; i < n1; ++i) v[i] = v0[i];
+  for (int k = 0; k < K; ++k) {
+    axis_D(a, v, tmp);
+    for (int i = 0; i < n1; ++i) u[i] = s[i] - alpha * tmp[i];
+    axis_D(a, u, tmp);
+    for (int i = 0; i < n1; ++i) v[i] = v0[i] - beta * tmp[i];
+  }
+}
+
+static double cerjan(int k, int n, int nb, double a) {
+  const int d = k < n - k ? k : n - k;
+  if (d >= nb) return 1.0;
+  const double t = a * (double)(nb - d);
+  return exp(-t * t);
+}
+
+static double source_full(const or_problem* p, int nx, int j, int i, double gft) {
+  double f = 0.0;
+  if (p->phi) f += p->phi[(size_t)j * nx + i] * gft;
+  if (p->src_ix >= 0 && p->src_iy >= 0 && i == p->src_ix && j == p->src_iy) f += gft / (p->h * p->h);
+  return f;
+}
+
+int or_run_full(const or_problem* p, double* U, double* V, double* W, int m0, int nsteps, int nthreads,
+                int nb, double ca) {
+  axis_t ax, ay;
+  int e = axis_init(&ax, OR_CFD, p->nx - 1, p->h);
+  if (e) return e;
+  e = axis_init(&ay, OR_CFD, p->ny - 1, p->h);
+  if (e) { axis_free(&ax); return e; }
+  const int nx = p->nx, ny = p->ny;
+  const double rho = p->rho, kappa = rho * p->c * p->c, dt = p->dt;
+  const double alpha = kappa * dt / 2.0, beta = dt / (2.0 * rho);
+  const size_t nn = (size_t)nx * ny;
+  double* S1 = (double*)malloc(sizeof(double) * nn);
+  double* S2 = (double*)malloc(sizeof(double) * nn);
+  double* Ws = (double*)malloc(sizeof(double) * nn);
+  if (!S1 || !S2 || !Ws) { free(S1); free(S2); free(Ws); axis_free(&ax); axis_free(&ay); return -2; }
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+  (void)nthreads;
+#endif
+  const int L = (nx > ny ? nx : ny) + 8;
+  for (int st = 0; st < nsteps; ++st) {
+    const int m = m0 + st;
+    const double gf_m = tab(p->gf, p->ngf, 2 * m), gf_1 = tab(p->gf, p->ngf, 2 * m + 2);
+    /* a2, per column */
+#pragma omp parallel
+    {
+      double* buf = (double*)malloc(sizeof(double) * 4 * L);
+      double *col = buf, *w = buf + L, *t1 = buf + 2 * L, *t2 = buf + 3 * L;
+#pragma omp for schedule(static)
+      for (int i = 0; i < nx; ++i) {
+        for (int r = 0; r < ny; ++r) { col[r] = U[(size_t)r * nx + i]; w[r] = W[(size_t)r * nx + i]; }
+        axis_D(&ay, col, t1);
+        axis_D(&ay, w, t2);
+        for (int r = 0; r < ny; ++r) {
+          Ws[(size_t)r * nx + i] = w[r] - beta * t1[r];
+          S1[(size_t)r * nx + i] = col[r] - alpha * t2[r] + (dt / 2.0) * source_full(p, nx, r, i, gf_m);
+        }
+      }
+      free(buf);
+    }
+    /* rows (all of them), then C and V^{m+1} */
+#pragma omp parallel
+    {
+      double* buf = (double*)malloc(sizeof(double) * 4 * L);
+      double *u = buf, *v = buf + L, *tmp = buf + 2 * L, *t2 = buf + 3 * L;
+#pragma omp for schedule(static)
+      for (int j = 0; j < ny; ++j) {
+        stage_line_full(&ax, p->K, alpha, beta, S1 + (size_t)j * nx, V + (size_t)j * nx, u, v, tmp);
+        axis_D(&ax, v, tmp);
+        axis_D(&ax, u, t2);
+        for (int i = 0; i < nx; ++i) {
+          S2[(size_t)j * nx + i] = u[i] - alpha * tmp[i] + (dt / 2.0) * source_full(p, nx, j, i, gf_1);
+          V[(size_t)j * nx + i] = v[i] - beta * t2[i];
+        }
+      }
+      free(buf);
+    }
+    /* columns (all of them) */
+#pragma omp parallel
+    {
+      double* buf = (double*)malloc(sizeof(double) * 5 * L);
+      double *u = buf, *w = buf + L, *tmp = buf + 2 * L, *s = buf + 3 * L, *w0 = buf + 4 * L;
+#pragma omp for schedule(static)
+      for (int i = 0; i < nx; ++i) {
+        for (int r = 0; r < ny; ++r) { s[r] = S2[(size_t)r * nx + i]; w0[r] = Ws[(size_t)r * nx + i]; }
+        stage_line_full(&ay, p->K, alpha, beta, s, w0, u, w, tmp);
+        for (int r = 0; r < ny; ++r) { U[(size_t)r * nx + i] = u[r]; W[(size_t)r * nx + i] = w[r]; }
+      }
+      free(buf);
+    }
+    /* F2: Cerjan taper of all three fields */
+    if (nb > 0) {
+      for (int r = 0; r < ny; ++r) {
+        const double gy = cerjan(r, ny - 1, nb, ca);
+        for (int i = 0; i < nx; ++i) {
+          const double g = gy * cerjan(i, nx - 1, nb, ca);
+          U[(size_t)r * nx + i] *= g;
+          V[(size_t)r * nx + i] *= g;
+          W[(size_t)r * nx + i] *= g;
+        }
+      }
+    }
+  }
+  free(S1); free(S2); free(Ws);
+  axis_free(&ax); axis_free(&ay);
+  return 0;
+}
+
+int or_run_full_flat(int nx, int ny, double h, double dt, double c, double rho, int K, const double* phi,
+                     int src_ix, int src_iy, const double* gf, int ngf, double* U, double* V, double* W,
+                     int m0, int nsteps, int nthreads, int nb, double ca) {
+  or_problem p;
+  memset(&p, 0, sizeof p);
+  p.method = OR_CFD; p.nx = nx; p.ny = ny; p.K = K;
+  p.h = h; p.dt = dt; p.c = c; p.rho = rho;
+  p.phi = phi; p.src_ix = src_ix; p.src_iy = src_iy;
+  p.gf = gf; p.ngf = ngf;
+  if (nx < 9 || ny < 9 || K < 1 || m0 < 0 || nsteps < 0 || nb < 0 || 2 * nb > nx || 2 * nb > ny) return -1;
+  if (gf && ngf < 2 * (m0 + nsteps) + 1) return -1;
+  return or_run_full(&p, U, V, W, m0, nsteps, nthreads, nb, ca);
+}
+
+/* One full-variant stage on a single line (exported for the dense-solve pin). */
+int or_stage_line_full(int n, double h, int K, double alpha, double beta, const double* s, const double* v0,
+                       double* u, double* v) {
+  axis_t a;
+  int e = axis_init(&a, OR_CFD, n, h);
+  if (e) return e;
+  double* tmp = (double*)malloc(sizeof(double) * (n + 8));
+  stage_line_full(&a, K, alpha, beta, s, v0, u, v, tmp);
+  free(tmp);
+  axis_free(&a);
+  return 0;
+}
+
 /* Flat-argument wrapper for ctypes. */
 int or_run_flat(int method, int nx, int ny, double h, double dt, double c, double rho, int K,
                 const double* phi, int src_ix, int src_iy, const double* gf, int ngf,
