@@ -29,6 +29,7 @@
  *     U  : (ny+1) x (nx+1)    pressure on X_cb x Y_cb incl. the boundary
  *     V  : (ny-1) x nx        V̄: x nodes x y cell centres
  *     W  : ny x (nx-1)        W̄: y nodes x x cell centres
+ *   CFD_FULL (f4, see ADI_CFD_FULL): U, V, W all ny x nx (every node).
  * The velocity lines on the boundary that the paper never updates are not
  * part of the state.  The pressure-interior block ("I") is
  * (ny-2) x (nx-2) for CFD and (ny-1) x (nx-1) for MFD.
@@ -62,7 +63,18 @@ extern "C" {
 
 typedef struct adi_ctx* adi_handle;
 
-enum adi_method { ADI_CFD = 0, ADI_MFD = 1 };
+/* ADI_CFD_FULL: the full-matrix CFD variant.
+ * "By simply replacing reduced operators P̄ and Q̄, and reduced matrices Ū, V̄, W̄,
+ * by their full matrix versions [...] the boundary wave fields can be also
+ * obtained.  These values can be further damped by the absorbing technique [of
+ * Cerjan et al.]."  Every node is unknown: U, V, W and a dense source pattern are
+ * all ny x nx; every derivative is D = P^{-1} Q (full, n+1 rows); there is no
+ * Dirichlet data (adi_set_boundary with edges returns ADI_EINVAL).  After each
+ * step U, V, W are multiplied by the Cerjan taper G(x) G(y) set by
+ * ADI_ABSORB_WIDTH / ADI_ABSORB_RATE (readings F1-F2).  The literal
+ * CFD closure's growth remains: the layer delays it.  No band
+ * decomposition, stopping rule or media for this variant (ADI_EINVAL). */
+enum adi_method { ADI_CFD = 0, ADI_MFD = 1, ADI_CFD_FULL = 2 };
 
 enum adi_status {
   ADI_OK = 0,
@@ -91,7 +103,12 @@ enum adi_param {
                            the stage's whole interior pressure / velocity matrices), else at
                            ADI_K_SWEEPS.  Costs one extra pass of the stage's sweeps; decided on
                            the device (no host round trip).  Whole grid only (no band). */
-  ADI_K_MIN = 6         /* first sweep tested by the stopping rule; integer >= 2, default 6 */
+  ADI_K_MIN = 6,        /* first sweep tested by the stopping rule; integer >= 2, default 6 */
+  ADI_ABSORB_WIDTH = 7, /* ADI_CFD_FULL only: Cerjan layer width nb in points, integer in
+                           [0, min(nx, ny)/2]; default 0 (no layer).  After each step the fields
+                           are multiplied by G(x)G(y), G = exp(-(a (nb - d))^2) at distance d < nb
+                           (points) from the nearest edge, else 1 */
+  ADI_ABSORB_RATE = 8   /* ADI_CFD_FULL only: the rate a > 0 of the taper; default 0.015 */
 };
 
 /* Kernel kinds launched by adi_step (index of adi_get_kernel_times arrays). */
@@ -141,7 +158,8 @@ int adi_set_fields_device(adi_handle h, const double* dU, const double* dV, cons
 /* Source term F(x,y,t) of eq. 1 on the pressure-interior points, entering
  * eqs. 5-6 as dt/2 (F^m + F^{m+1}):
  *   F = phi(x,y) * g(t)                      if phi != NULL (phi: I-block, host), plus
- *   F = g(t) / h^2 at U-array point (ix, iy) if ix >= 1 (point source; batch 1).
+ *   F = g(t) / h^2 at U-array point (ix, iy) if ix >= 1 (point source; batch 1;
+ *   ADI_CFD_FULL: any node, ix >= 0).
  * g: table at half steps, ng entries (NULL: g = 1). */
 int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double* g, int ng);
 

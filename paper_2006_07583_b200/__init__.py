@@ -21,6 +21,7 @@ from .build import LIB_PATH, build as build_library  # noqa: F401
 
 ADI_CFD = 0
 ADI_MFD = 1
+ADI_CFD_FULL = 2   # the full-matrix CFD variant with a Cerjan layer (f4)
 ADI_OK = 0
 ADI_EINVAL = -1
 ADI_ENOMEM = -2
@@ -36,6 +37,8 @@ ADI_TILE_CHUNKS = 3
 ADI_TIMING = 4
 ADI_EPS = 5
 ADI_K_MIN = 6
+ADI_ABSORB_WIDTH = 7
+ADI_ABSORB_RATE = 8
 KERNEL_KINDS = ("prologue", "row", "col", "final", "edge")
 
 _STATUS = {0: "ADI_OK", -1: "ADI_EINVAL", -2: "ADI_ENOMEM", -3: "ADI_ECUDA", -4: "ADI_EZEROPIVOT",
@@ -302,6 +305,8 @@ def adi_version():
 
 # ---- convenience wrapper ------------------------------------------------------
 def shapes(method, nx, ny):
+    if method == ADI_CFD_FULL:
+        return (ny, nx), (ny, nx), (ny, nx)
     if method == ADI_CFD:
         return (ny, nx), (ny - 2, nx), (ny, nx - 2)
     return (ny + 1, nx + 1), (ny - 1, nx), (ny, nx - 1)

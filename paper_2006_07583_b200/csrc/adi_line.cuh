@@ -97,6 +97,12 @@ struct KParams {
   double mA, mB, mC, mD;  // MFD interior stencil: cu/24, 9cu/8, cx/24, 9cx/8
   double half_dt;
   int K;
+  // NEXT row f4 (FULL kernels): Cerjan taper G(k) = taper[d], d = min(k, n - k) < nb;
+  // damp = 1: V' *= G(line) G(p) (row sweep); 2: u, w *= G before the fused a2, W*
+  // recomputed (column sweep / final); 0: none
+  const double* taper;
+  int nb;
+  int damp;
   // inner stopping rule (Alg. 3/4): an attempt (KM_*_T) runs K sweeps, adds the
   // owned squared changes of u and x in its last sweep to norms[0], norms[1], and
   // does nothing when *gate is set (the stage is already decided)
@@ -778,7 +784,7 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
 }
 
 // Occupancy targets (resident CTAs per SM) for the NW-warp CTAs.
-template <int METHOD, bool EDGE, int MODE, bool HET = false>
+template <int METHOD, bool EDGE, int MODE, bool HET = false, bool FULL = false>
 struct Occ {
 #ifndef ADI_CFD_OCC
 #define ADI_CFD_OCC 3
@@ -787,7 +793,9 @@ struct Occ {
   // the generic CFD kernel keeps 255 registers
   // (the norm pass of the stopping rule keeps the previous iterates: 255 registers)
   // HET (three staging tiles per line): 2, the CFD edge kernel 1 (shared memory)
-  static constexpr int value = HET ? ((METHOD == M_CFD && EDGE) ? 1 : 2)
+  // FULL (the f4 variant): 2
+  static constexpr int value = FULL ? 2
+                               : HET ? ((METHOD == M_CFD && EDGE) ? 1 : 2)
                                : (MODE == KM_SWEEP_T || MODE == KM_FINAL_T) ? 2
                                : (METHOD == M_MFD) ? 3 : (EDGE ? 2 : ADI_CFD_OCC);
 };
@@ -820,8 +828,12 @@ __device__ __forceinline__ void tma_load_seg(double* dst, const CUtensorMap* tm,
 // are interior and live (the lean path, no generic closures, no per-chunk
 // predicates); EDGE = true: line ends, dead chunks, short lines.
 // ===========================================================================
-template <int METHOD, int M, int NW, int MODE_, bool EDGE, bool HET = false>
+template <int METHOD, int M, int NW, int MODE_, bool EDGE, bool HET = false, bool FULL = false>
 __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, double* smem) {
+  // FULL (NEXT row f4, CFD only, readings F1-F2): every position 0..n is
+  // unknown and both operators are the full D = P^{-1} Q (the x-op's operator)
+  static_assert(!FULL || METHOD == M_CFD, "the full-matrix variant is CFD");
+  constexpr bool UOPK = !FULL;   // cfd_apply flavour of the pressure operator
   // stopping-rule attempts are SWEEP / FINAL tiles with the last-sweep test
   constexpr bool TEST = (MODE_ == KM_SWEEP_T || MODE_ == KM_FINAL_T);
   constexpr int MODE = (MODE_ == KM_SWEEP_T) ? KM_SWEEP : (MODE_ == KM_FINAL_T) ? KM_FINAL : MODE_;
@@ -844,7 +856,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   const int line = P.line0 + blockIdx.x * NW + w;   // cross position of this line
   const int b = blockIdx.z;
   const int n = P.n;
-  const int uhi = (METHOD == M_CFD) ? n - 1 : n;  // u active on [1, uhi]
+  const int ulo = FULL ? 0 : 1;
+  const int uhi = (METHOD == M_CFD && !FULL) ? n - 1 : n;  // u active on [ulo, uhi]
   const int pR = (METHOD == M_CFD) ? n : n + 1;   // position of ū's right Dirichlet value
   const bool lineok = line >= P.line_lo && line < P.nlines;
   const bool tr = P.trace && t == 0;
@@ -1097,7 +1110,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
           V2[i] = make_double2(x[2 * i], x[2 * i + 1]);
         }
       }
-      cfd_apply<M, true, EDGE, HET>(c, P, lane, stU, etab, wv, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
+      cfd_apply<M, UOPK, EDGE, HET>(c, P, lane, FULL ? stXs : stU, etab, wv, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
       if constexpr (HET) het_apply<M, METHOD, true, EDGE>(c, Cm, Sm, u, 1, uhi);
     } else {
       double uo[TEST ? M : 1], xo[TEST ? M : 1];
@@ -1114,7 +1127,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
           um1 = fma(kP, um1, SLp);
           up1 = fma(kN, up1, SFn);
         } else {
-          cfd_apply<M, true, EDGE>(c, P, lane, stU, etab, x, Sm, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
+          cfd_apply<M, UOPK, EDGE>(c, P, lane, FULL ? stXs : stU, etab, x, Sm, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
         }
         if (k + 1 == KK) {
           // park u_K in the (now dead) S tile: u is then dead across every x-op,
@@ -1135,13 +1148,51 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
           if (k + 1 == KK) norm_add(u, uo, x, xo);
         }
       }
-      if (MODE == KM_SWEEP) {
+      // f4: the Cerjan taper at this chunk's points, G(line) G(p) (F2)
+      auto taper_at = [&](int k, int nn) -> double {
+        const int d = min(k, nn - k);
+        return (d >= 0 && d < P.nb) ? P.taper[d] : 1.0;
+      };
+      if (FULL && P.damp == 2) {
+        // column sweep of the full variant: U^{m+1} = G u_K, W^{m+1} = G w_K (parked u_K in
+        // the S tile); FINAL stores them, SWEEP continues with the fused a2 of step m+1:
+        // W* = Gw - beta D(Gu) (explicitly: the 2w - W* identity does not survive the taper)
+        // and S1 = Gu + dt/2 F - alpha D(Gw)
+        const double gl = taper_at(line, P.nlines - 1);
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+          const double g = gl * taper_at(c.s + i, n);
+          x[i] *= g;
+          Sm[i] *= g;
+        }
+        if (MODE == KM_SWEEP) {
+          double e1, e2, d0, d1;
+#pragma unroll
+          for (int i = 0; i < M; ++i) { u[i] = Sm[i]; Vm[i] = x[i]; }   // operand Gu, base Gw
+          __syncwarp();
+          warp_edges<M>(lane, u, d0, um1, up1, d1);
+          cfd_apply<M, false, EDGE>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, 0.0, 0.0, e1, e2);
+#pragma unroll
+          for (int i = 0; i < M; ++i) { u[i] = Vm[i]; Vm[i] = x[i]; }   // operand Gw; Vm = W*
+          __syncwarp();
+          warp_edges<M>(lane, u, d0, xm1, xp1, d1);
+          add_source_global(Sm);   // S = Gu + dt/2 F
+          cfd_apply<M, false, EDGE>(c, P, lane, stXs, etab, u, Sm, x, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
+#pragma unroll
+          for (int i = 0; i < M; ++i) { u[i] = x[i]; x[i] = Vm[i]; }    // u = S1, x = W*
+        }
+      } else if (MODE == KM_SWEEP) {
         double e1, e2;
         add_source_global(Sm);   // S = u_K + dt/2 F
-        cfd_apply<M, true, EDGE, HET>(c, P, lane, stU, etab, x, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
+        cfd_apply<M, UOPK, EDGE, HET>(c, P, lane, FULL ? stXs : stU, etab, x, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
         if constexpr (HET) het_apply<M, METHOD, true, EDGE>(c, Cm, Sm, u, 1, uhi);
 #pragma unroll
         for (int i = 0; i < M; ++i) x[i] = fma(2.0, x[i], -Vm[i]);
+        if (FULL && P.damp == 1) {   // row sweep of the full variant: V^{m+1} = G (2x - X)
+          const double gl = taper_at(line, P.nlines - 1);
+#pragma unroll
+          for (int i = 0; i < M; ++i) x[i] *= gl * taper_at(c.s + i, n);
+        }
       }
     }
   } else {
@@ -1273,7 +1324,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     const bool ok1 = ln + 1 >= P.line_lo && ln + 1 < P.nlines;
     int plo_, phi_;   // output positions of this tile for S / U
     if (MODE == KM_FINAL) { plo_ = max(sg.out_lo, 0); phi_ = min(sg.out_hi, n + 1); }
-    else { plo_ = max(sg.out_lo, 1); phi_ = min(sg.out_hi, uhi + 1); }
+    else { plo_ = max(sg.out_lo, ulo); phi_ = min(sg.out_hi, uhi + 1); }
     const double* r0 = stS + (2 * pr) * LSTR;
     const double* r1 = r0 + LSTR;
     for (int pos = 16 * w + (lane & 15); pos < 32 * M; pos += 16 * NW) {
@@ -1314,8 +1365,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
 //   MODE = KM_FINAL   : as SWEEP without the fused explicit half; writes U_out
 //   MODE = KM_PROLOGUE: U_in, X_in -> a2 (explicit half only)
 // ===========================================================================
-template <int METHOD, int M, int NW, int MODE, bool EDGE, bool HET = false>
-__global__ void __launch_bounds__(32 * NW, (Occ<METHOD, EDGE, MODE, HET>::value))
+template <int METHOD, int M, int NW, int MODE, bool EDGE, bool HET = false, bool FULL = false>
+__global__ void __launch_bounds__(32 * NW, (Occ<METHOD, EDGE, MODE, HET, FULL>::value))
     adi_line_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(128) double smem_raw[];
   // TMA destinations need 128-byte alignment
@@ -1323,7 +1374,7 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD, EDGE, MODE, HET>::value)
   double* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u) / 8u;
   if (P.gate && *P.gate) return;   // stopping rule: the stage was decided by an earlier attempt
   const Seg sg = P.segs[blockIdx.y];
-  line_tile<METHOD, M, NW, MODE, EDGE, HET>(P, sg, smem);
+  line_tile<METHOD, M, NW, MODE, EDGE, HET, FULL>(P, sg, smem);
 }
 
 // The stopping rule after the attempt with k sweeps (Alg. 3/4 "until test <= eps or

@@ -93,6 +93,13 @@ struct adi_ctx {
   double* Ca = nullptr;
   double* Cb = nullptr;
   bool het = false;
+  // NEXT row f4 (ADI_CFD_FULL): the full-matrix CFD variant; every node is unknown, the
+  // interior index i is position i (off = 0; the reduced variants: off = 1)
+  bool full = false;
+  int off = 1;
+  int absorb_nb = 0;          // ADI_ABSORB_WIDTH (Cerjan layer, points)
+  double absorb_a = 0.015;    // ADI_ABSORB_RATE
+  double* d_taper = nullptr;  // taper[d], d < absorb_nb
   // internal layouts: Sa, V, V2 row-major; Sb = S^T; W, W2 = W̄^T (columns contiguous)
   int* flag = nullptr;
   adi::Axis ax, ay;
@@ -476,7 +483,8 @@ bool plan_axis(adi::Axis& A, int method, int cap, int lo_all, int hi_all) {
 int setup_axis(adi_ctx* h, adi::Axis& A, int n, int nlines, int nlmin) {
   A.n = n;
   A.nlines = nlines;
-  if (A.l1 == 0 && A.l0 == 0) { A.l0 = 1; A.l1 = nlines + 1; }  // lines are positions 1..nlines
+  // lines are positions off..nlines-1+off (the full variant: every line)
+  if (A.l1 == 0 && A.l0 == 0) { A.l0 = h->off; A.l1 = nlines + h->off; }
   (void)nlmin;
   // the owned positions: the whole line, or this handle's band (adi_set_band)
   if (!plan_axis(A, h->method, h->tile_chunks, A.o0, A.o1))
@@ -562,9 +570,9 @@ struct TimeScope {
   }
 };
 
-template <int METHOD, int MODE, bool EDGE, bool HET>
+template <int METHOD, int MODE, bool EDGE, bool HET, bool FULL = false>
 int launch_e(adi_ctx* h, const adi::Axis& A, adi::KParams p, int seg0, int nseg) {
-  auto kern = adi::adi_line_kernel<METHOD, adi::TM, adi::NW, MODE, EDGE, HET>;
+  auto kern = adi::adi_line_kernel<METHOD, adi::TM, adi::NW, MODE, EDGE, HET, FULL>;
   const size_t smem = adi::line_smem_bytes<METHOD, adi::TM, adi::NW, EDGE, HET>();
   static bool attr = false;
   if (!attr) {
@@ -591,6 +599,16 @@ int launch_t(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
   return launch_e<METHOD, MODE, true, HET>(h, A, p, A.nint, nseg - A.nint);
 }
 
+// the full-matrix CFD variant (NEXT row f4)
+template <int MODE>
+int launch_full(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
+  if (A.l1 <= A.l0) return ADI_OK;
+  const int nseg = (int)A.segs.size();
+  int rc = launch_e<adi::M_CFD, MODE, false, false, true>(h, A, p, 0, A.nint);
+  if (rc) return rc;
+  return launch_e<adi::M_CFD, MODE, true, false, true>(h, A, p, A.nint, nseg - A.nint);
+}
+
 // heterogeneous-media kernels (fixed K sweeps: the stopping rule is not combined with media)
 template <int METHOD>
 int launch_het(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p) {
@@ -612,6 +630,12 @@ int launch(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p0, int
   if (h->het) {
     if ((rc = tmap_for(h, (&A == &h->ay) ? h->Cb : h->Ca, &p.tmC))) return rc;
     return h->method == ADI_CFD ? launch_het<adi::M_CFD>(h, mode, A, p) : launch_het<adi::M_MFD>(h, mode, A, p);
+  }
+  if (h->full) {
+    if (mode == adi::KM_SWEEP) return launch_full<adi::KM_SWEEP>(h, A, p);
+    if (mode == adi::KM_FINAL) return launch_full<adi::KM_FINAL>(h, A, p);
+    if (mode == adi::KM_PROLOGUE) return launch_full<adi::KM_PROLOGUE>(h, A, p);
+    return fail(h, ADI_EINVAL, "internal: no full-variant kernel for this mode");
   }
   if (h->method == ADI_CFD) {
     if (mode == adi::KM_SWEEP) return launch_t<adi::M_CFD, adi::KM_SWEEP>(h, A, p);
@@ -718,6 +742,9 @@ adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
   p.mC = p.cx * (1.0 / 24.0);
   p.mD = p.cx * (9.0 / 8.0);
   p.half_dt = h->dt / 2.0;
+  p.taper = h->d_taper;
+  p.nb = h->full ? h->absorb_nb : 0;
+  p.damp = (h->full && h->absorb_nb > 0) ? (ydir ? 2 : 1) : 0;
   p.K = h->K;
   p.tabU = A.d_tabU;
   p.tabX = A.d_tabX;
@@ -754,7 +781,7 @@ void free_ctx(adi_ctx* h) {
   for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
   for (double* q : {h->Ubase, h->V, h->W, h->V2, h->W2, h->Sa, h->Sb, h->phi, h->phiT, h->Ca, h->Cb}) dfree(q);
-  for (void* q : {(void*)h->edges, (void*)h->flag, (void*)h->d_norms, (void*)h->d_k})
+  for (void* q : {(void*)h->edges, (void*)h->flag, (void*)h->d_norms, (void*)h->d_k, (void*)h->d_taper})
     if (q) cudaFree(q);
   for (adi::Axis* A : {&h->ax, &h->ay})
     for (void* q : {(void*)A->d_segs, (void*)A->d_tabU, (void*)A->d_tabX, (void*)A->d_ptl,
@@ -794,7 +821,7 @@ int adi_create_batch(int nx, int ny, double hh, double dt, double c, int method,
                      adi_handle* out) {
   if (!out) return ADI_EINVAL;
   *out = nullptr;
-  if (method != ADI_CFD && method != ADI_MFD) return ADI_EINVAL;
+  if (method != ADI_CFD && method != ADI_MFD && method != ADI_CFD_FULL) return ADI_EINVAL;
   if (nx < 9 || ny < 9 || batch < 1) return ADI_EINVAL;
   if (!(hh > 0) || !(dt > 0) || !(c > 0) || !std::isfinite(hh) || !std::isfinite(dt) ||
       !std::isfinite(c))
@@ -805,6 +832,9 @@ int adi_create_batch(int nx, int ny, double hh, double dt, double c, int method,
     return ADI_ECUDA;
   }
   adi_ctx* h = new adi_ctx();
+  h->full = (method == ADI_CFD_FULL);
+  h->off = h->full ? 0 : 1;
+  if (h->full) method = ADI_CFD;   // the CFD operators; every node unknown
   h->method = method; h->nx = nx; h->ny = ny; h->batch = batch;
   h->h = hh; h->dt = dt; h->c = c; h->rho = 1.0;
   if (method == ADI_CFD) {
@@ -812,6 +842,7 @@ int adi_create_batch(int nx, int ny, double hh, double dt, double c, int method,
   } else {
     h->nxu = nx + 1; h->nyu = ny + 1; h->nxi = nx - 1; h->nyi = ny - 1;
   }
+  if (h->full) { h->nxi = nx; h->nyi = ny; }   // U, V, W, F: all ny x nx
   h->nxv = nx; h->nyv = ny;
   h->nU = (size_t)h->nyu * h->nxu;
   h->nV = (size_t)h->nyi * h->nxv;
@@ -880,6 +911,27 @@ int adi_set_param(adi_handle h, int key, double v) {
   } else if (key == ADI_K_MIN) {
     if (!(v >= 2) || v != std::floor(v) || v > 1000) return fail(h, ADI_EINVAL, "k_min must be an integer >= 2");
     h->kmin = (int)v;
+  } else if (key == ADI_ABSORB_WIDTH || key == ADI_ABSORB_RATE) {
+    if (!h->full) return fail(h, ADI_EINVAL, "the absorbing layer belongs to the full-matrix variant");
+    if (h->in_call) return fail(h, ADI_ESTATE, "call in progress");
+    int nb = h->absorb_nb;
+    double a = h->absorb_a;
+    if (key == ADI_ABSORB_WIDTH) {
+      if (!(v >= 0) || v != std::floor(v) || 2 * v > std::min(h->nx, h->ny))
+        return fail(h, ADI_EINVAL, "absorbing width must be an integer in [0, min(nx, ny)/2]");
+      nb = (int)v;
+    } else {
+      if (!(v > 0) || !std::isfinite(v)) return fail(h, ADI_EINVAL, "absorbing rate must be > 0");
+      a = v;
+    }
+    // Cerjan taper G(d) = exp(-(a (nb - d))^2), d = distance (points) from the nearest edge
+    std::vector<double> g((size_t)std::max(nb, 1));
+    for (int d = 0; d < nb; ++d) g[d] = std::exp(-(a * (nb - d)) * (a * (nb - d)));
+    if (h->d_taper) { cudaFree(h->d_taper); h->d_taper = nullptr; }
+    CUDA_TRY(h, cudaMalloc(&h->d_taper, g.size() * sizeof(double)));
+    H2D_SYNC(h, h->d_taper, g.data(), g.size() * sizeof(double));
+    h->absorb_nb = nb;
+    h->absorb_a = a;
   } else if (key == ADI_TILE_CHUNKS) {
     if (!(v >= 0) || v != std::floor(v)) return fail(h, ADI_EINVAL, "tile chunks must be >= 0");
     h->tile_chunks = (int)v;
@@ -924,7 +976,8 @@ static int set_fields_impl(adi_handle h, const double* U, const double* V, const
   const size_t B = (size_t)h->batch;
   int ya, yb;
   field_rows(h, true, &ya, &yb);
-  const int ja = std::max(ya - 1, 0), jb = std::min(yb - 1, h->nyi);   // V̄ row j = y position j + 1
+  const int off = h->off;   // V̄ row j = y position j + off
+  const int ja = std::max(ya - off, 0), jb = std::min(yb - off, h->nyi);
   const int wa = std::min(ya, h->nyv), wb = std::min(yb, h->nyv);      // W̄ rows are y positions
   // user layouts are dense; internal rows are pitched (batch strides aU, aV, aW)
   for (size_t b = 0; b < B; ++b) {
@@ -932,7 +985,7 @@ static int set_fields_impl(adi_handle h, const double* U, const double* V, const
                                   U + b * h->nU + (size_t)ya * h->nxu, h->nxu * 8, h->nxu * 8, yb - ya, kind,
                                   h->stream));
     if (jb > ja)
-      CUDA_TRY(h, cudaMemcpy2DAsync(h->V + b * h->aV + (size_t)(ja + 1) * h->pv, h->pv * 8,
+      CUDA_TRY(h, cudaMemcpy2DAsync(h->V + b * h->aV + (size_t)(ja + off) * h->pv, h->pv * 8,
                                     V + b * h->nV + (size_t)ja * h->nxv, h->nxv * 8, h->nxv * 8, jb - ja, kind,
                                     h->stream));
     // W̄ rows [wa, wb) (dense) -> internal W̄^T (row = x position i + 1, column = y)
@@ -940,7 +993,8 @@ static int set_fields_impl(adi_handle h, const double* U, const double* V, const
     if (wb > wa) {
       CUDA_TRY(h, cudaMemcpyAsync(h->W2, W + b * h->nW + (size_t)wa * h->nxi, (size_t)(wb - wa) * h->nxi * 8,
                                   kind, h->stream));
-      int rc = transpose(h, h->W2, h->W + b * h->aW + h->pw + wa, wb - wa, h->nxi, h->nxi, h->pw, 1, 0, 0);
+      int rc = transpose(h, h->W2, h->W + b * h->aW + (size_t)off * h->pw + wa, wb - wa, h->nxi, h->nxi, h->pw,
+                         1, 0, 0);
       if (rc) return rc;
     }
   }
@@ -963,10 +1017,10 @@ static int set_points(adi_handle h, const int* ix, const int* iy) {
   // x-direction lines are interior rows (line = iy-1, pos = ix); y-direction: line = ix-1, pos = iy
   const int B = h->batch;
   std::vector<int> xl(B), xp(B), yl(B), yp(B);
-  const int uhx = (h->method == ADI_CFD) ? h->nx - 2 : h->nx - 1;
-  const int uhy = (h->method == ADI_CFD) ? h->ny - 2 : h->ny - 1;
+  const int uhx = (h->method == ADI_CFD && !h->full) ? h->nx - 2 : h->nx - 1;
+  const int uhy = (h->method == ADI_CFD && !h->full) ? h->ny - 2 : h->ny - 1;
   for (int b = 0; b < B; ++b) {
-    if (ix[b] < 1 || ix[b] > uhx || iy[b] < 1 || iy[b] > uhy)
+    if (ix[b] < h->off || ix[b] > uhx || iy[b] < h->off || iy[b] > uhy)
       return fail(h, ADI_EINVAL, "point source outside the pressure interior");
     xl[b] = iy[b]; xp[b] = ix[b];   // row sweep: line = y position, pos = x position
     yl[b] = ix[b]; yp[b] = iy[b];
@@ -989,7 +1043,8 @@ int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double
   if (!h) return ADI_EINVAL;
   h->err.clear();
   if (g && ng < 1) return fail(h, ADI_EINVAL, "empty source table");
-  if (ix >= 1 && h->batch != 1) return fail(h, ADI_EINVAL, "use adi_set_point_sources for a batch");
+  const bool has_pt = ix >= h->off;   // (the full variant: every node, ix >= 0)
+  if (has_pt && h->batch != 1) return fail(h, ADI_EINVAL, "use adi_set_point_sources for a batch");
   if (phi) {
     if (!h->phi || !h->phiT) {
       h->tmaps.clear();
@@ -998,10 +1053,12 @@ int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double
     }
     CUDA_TRY(h, cudaMemsetAsync(h->phi, 0, h->aS * 8, h->stream));
     CUDA_TRY(h, cudaMemsetAsync(h->phiT, 0, h->aS * 8, h->stream));
-    // interior point (j, i) of the user's block is position (y, x) = (j + 1, i + 1)
-    CUDA_TRY(h, cudaMemcpy2DAsync(h->phi + h->pa + 1, h->pa * 8, phi, h->nxi * 8, h->nxi * 8, h->nyi,
+    // interior point (j, i) of the user's block is position (y, x) = (j + off, i + off)
+    const int off = h->off;
+    CUDA_TRY(h, cudaMemcpy2DAsync(h->phi + off * h->pa + off, h->pa * 8, phi, h->nxi * 8, h->nxi * 8, h->nyi,
                                   cudaMemcpyHostToDevice, h->stream));
-    int rc = transpose(h, h->phi + h->pa + 1, h->phiT + h->pb + 1, h->nyi, h->nxi, h->pa, h->pb, 1, 0, 0);
+    int rc = transpose(h, h->phi + off * h->pa + off, h->phiT + off * h->pb + off, h->nyi, h->nxi, h->pa, h->pb,
+                       1, 0, 0);
     if (rc) return rc;
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   } else if (h->phi) {
@@ -1012,7 +1069,7 @@ int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double
     h->phiT = nullptr;
   }
   h->has_pt = false;
-  if (ix >= 1) {
+  if (has_pt) {
     int rc = set_points(h, &ix, &iy);
     if (rc) return rc;
   }
@@ -1034,6 +1091,7 @@ int adi_set_boundary(adi_handle h, const double* edges, const double* g, int ng)
   if (!h) return ADI_EINVAL;
   h->err.clear();
   if (g && ng < 1) return fail(h, ADI_EINVAL, "empty boundary table");
+  if (h->full && edges) return fail(h, ADI_EINVAL, "the full-matrix variant has no Dirichlet data");
   const size_t ne = 2 * (size_t)h->nxu + 2 * (size_t)h->nyu;
   if (edges) {
     if (!h->edges) CUDA_TRY(h, cudaMalloc(&h->edges, ne * 8));
@@ -1058,6 +1116,7 @@ int adi_set_media(adi_handle h, const float* kappa, const float* rinv_v, const f
     return ADI_OK;
   }
   if (!kappa || !rinv_v || !rinv_w) return fail(h, ADI_EINVAL, "kappa, rinv_v, rinv_w: all or none");
+  if (h->full) return fail(h, ADI_EINVAL, "media fields are not available for the full-matrix variant");
   // values: finite and > 0; the CFL bound uses max kappa * max rho^-1 >= c_max^2
   double kmax = 0, rmax = 0;
   auto scan = [&](const float* a, size_t n, size_t r0, size_t r1, size_t rowlen, size_t c0, size_t c1,
@@ -1119,6 +1178,8 @@ int adi_step_begin(adi_handle h, int nsteps) {
     return fail(h, ADI_EINVAL, "source table too short for the requested steps");
   if (!h->gb.empty() && (long long)h->gb.size() < 2 * m1 + 1)
     return fail(h, ADI_EINVAL, "boundary table too short for the requested steps");
+  if (h->eps > 0.0 && h->full)
+    return fail(h, ADI_EINVAL, "the stopping rule (ADI_EPS > 0) is not available for the full-matrix variant");
   if (h->eps > 0.0 && h->het)
     return fail(h, ADI_EINVAL, "the stopping rule (ADI_EPS > 0) is not available with media fields");
   if (h->eps > 0.0) {
@@ -1203,7 +1264,7 @@ int adi_step_end(adi_handle h) {
   if (!h) return ADI_EINVAL;
   if (!h->in_call || h->m != h->call_m1) return fail(h, ADI_ESTATE, "steps of the call not finished");
   if (h->Vcur != h->V) std::swap(h->V, h->V2);
-  {  // Dirichlet columns of U^{m1}
+  if (!h->full) {  // Dirichlet columns of U^{m1}
     dim3 g((h->nyu + 255) / 256, h->batch);
     const double* ex0 = h->edges ? h->edges + 2 * h->nxu : nullptr;
     const double* ex1 = h->edges ? h->edges + 2 * h->nxu + h->nyu : nullptr;
@@ -1246,6 +1307,7 @@ int adi_set_band(adi_handle h, int y0, int y1) {
   if (h->in_call) return fail(h, ADI_ESTATE, "call in progress");
   const int ny_pos = h->ay.n + 1;  // y positions 0..n_y
   if (y0 < 0 || y1 > ny_pos || y0 >= y1) return fail(h, ADI_EINVAL, "band out of range");
+  if (h->full) return fail(h, ADI_EINVAL, "no band decomposition for the full-matrix variant");
   h->band_y0 = y0;
   h->band_y1 = y1;
   // row sweep: interior rows (lines = y positions 1..nyi) inside [y0, y1)
@@ -1361,7 +1423,8 @@ static int get_fields_impl(adi_handle h, double* U, double* V, double* W, cudaMe
   const size_t B = (size_t)h->batch;
   int ya, yb;
   field_rows(h, false, &ya, &yb);
-  const int ja = std::max(ya - 1, 0), jb = std::min(yb - 1, h->nyi);
+  const int off = h->off;
+  const int ja = std::max(ya - off, 0), jb = std::min(yb - off, h->nyi);
   const int wa = std::min(ya, h->nyv), wb = std::min(yb, h->nyv);
   for (size_t b = 0; b < B; ++b) {
     CUDA_TRY(h, cudaMemcpy2DAsync(U + b * h->nU + (size_t)ya * h->nxu, h->nxu * 8,
@@ -1369,11 +1432,12 @@ static int get_fields_impl(adi_handle h, double* U, double* V, double* W, cudaMe
                                   h->stream));
     if (jb > ja)
       CUDA_TRY(h, cudaMemcpy2DAsync(V + b * h->nV + (size_t)ja * h->nxv, h->nxv * 8,
-                                    h->V + b * h->aV + (size_t)(ja + 1) * h->pv, h->pv * 8, h->nxv * 8, jb - ja,
+                                    h->V + b * h->aV + (size_t)(ja + off) * h->pv, h->pv * 8, h->nxv * 8, jb - ja,
                                     kind, h->stream));
     // internal W̄^T (columns [wa, wb)) -> W̄ rows via the W2 scratch buffer
     if (wb > wa) {
-      int rc = transpose(h, h->W + b * h->aW + h->pw + wa, h->W2, h->nxi, wb - wa, h->pw, h->nxi, 1, 0, 0);
+      int rc = transpose(h, h->W + b * h->aW + (size_t)off * h->pw + wa, h->W2, h->nxi, wb - wa, h->pw, h->nxi, 1,
+                         0, 0);
       if (rc) return rc;
       CUDA_TRY(h, cudaMemcpyAsync(W + b * h->nW + (size_t)wa * h->nxi, h->W2, (size_t)(wb - wa) * h->nxi * 8,
                                   kind, h->stream));
