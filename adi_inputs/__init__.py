@@ -12,7 +12,7 @@ their inputs from here; nothing here calls either implementation.
 * ``shots`` — Ricker point-source shots (config 5).
 * ``random_state`` — seeded random (U, V̄, W̄) for invariants and parity.
 """
-from .grid import CFD, MFD, Grid, dt_for_cfl, dt_rate_study, shapes, interior_shape  # noqa: F401
+from .grid import CFD, CFD_FULL, MFD, Grid, dt_for_cfl, dt_rate_study, shapes, interior_shape  # noqa: F401
 from .mms import MMS, mms_problem  # noqa: F401
 from .shots import ricker, ricker_problem  # noqa: F401
 from .rates import estimate_rates, trimmed_average  # noqa: F401

@@ -16,15 +16,20 @@ import numpy as np
 
 CFD = 0
 MFD = 1
+CFD_FULL = 2   # the full-matrix CFD variant (NEXT row f4): every node is state
 
 
 def shapes(method: int, nx: int, ny: int):
+    if method == CFD_FULL:
+        return (ny, nx), (ny, nx), (ny, nx)
     if method == CFD:
         return (ny, nx), (ny - 2, nx), (ny, nx - 2)
     return (ny + 1, nx + 1), (ny - 1, nx), (ny, nx - 1)
 
 
 def interior_shape(method: int, nx: int, ny: int):
+    if method == CFD_FULL:
+        return (ny, nx)
     return (ny - 2, nx - 2) if method == CFD else (ny - 1, nx - 1)
 
 

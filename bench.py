@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-n", type=int, default=4097, help="oracle sample grid (nodes)")
+    ap.add_argument("--full", action="store_true",
+                    help="NEXT row f4: the full-matrix CFD variant with a Cerjan layer (ADI_CFD_FULL)")
     ap.add_argument("--media", action="store_true",
                     help="NEXT row f3: the same workload in a smooth heterogeneous medium (adi_set_media)")
     return ap.parse_args()
@@ -56,10 +58,13 @@ def parse():
 
 def methods_of(a):
     from adi_inputs import CFD, MFD
+    if a.full:
+        return [2]   # ADI_CFD_FULL
     return {"both": [MFD, CFD], "mfd": [MFD], "cfd": [CFD]}[a.method]
 
 
-MNAME = {0: "cfd", 1: "mfd"}
+MNAME = {0: "cfd", 1: "mfd", 2: "cfd_full"}
+ABSORB_NB, ABSORB_A = 20, 0.015   # --full: the Cerjan layer (Cerjan et al.'s width and rate)
 
 
 # ---------------------------------------------------------------------------
@@ -164,6 +169,19 @@ def ncu_traffic():
 # ---------------------------------------------------------------------------
 def make_problem(method, n, steps, K, media=False):
     from adi_inputs import MMS, mms_problem
+    if method == 2:
+        # the full-matrix variant: the CFD MMS state on every node (V, W zero at t = 0), the
+        # dense source on every node, no boundary data (the Cerjan layer is set on the handle)
+        from adi_inputs.grid import nodes
+        p = mms_problem(0, n, MMS(), steps=steps, K=K)
+        x = nodes(n)
+        p.method = 2
+        p.V = np.zeros((n, n))
+        p.W = np.zeros((n, n))
+        p.phi = MMS().phi(x[None, :], x[:, None])
+        p.edges = None
+        p.gb = None
+        return p
     p = mms_problem(method, n, MMS(), steps=steps, K=K)
     if media:
         # a smooth medium (adi_inputs.media.Medium, scaled to c <= 1 so the CFL of the
@@ -227,6 +245,9 @@ def run_ours(a, ws, rank, local):
         if a.media:
             s.set_media(p.kappa, p.rinv_v, p.rinv_w)
             p.kappa = p.rinv_v = p.rinv_w = None
+        if m == 2:
+            s.set_param(adi.ADI_ABSORB_WIDTH, ABSORB_NB)
+            s.set_param(adi.ADI_ABSORB_RATE, ABSORB_A)
         p.phi = None  # copied by the library; keep host memory low (8 ranks per box)
         p.V = p.W = None  # zeros for the MMS start; recreated for the e2e leg
         bs = None
@@ -399,8 +420,12 @@ def oracle_rate(methods, n, steps, K, threads=0, media=False):
     for m in methods:
         p = make_problem(m, n, steps + 1, K, media)
         t0 = time.perf_counter()
-        oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, p.U, p.V, p.W, nsteps=steps,
-                   nthreads=threads, **p.oracle_kwargs())
+        if m == 2:
+            oracle.run_full(p.nx, p.ny, p.h, p.dt, p.c, p.K, p.U, p.V, p.W, phi=p.phi, gf=p.gf, nsteps=steps,
+                            nthreads=threads, nb=ABSORB_NB, a=ABSORB_A)
+        else:
+            oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, p.U, p.V, p.W, nsteps=steps,
+                       nthreads=threads, **p.oracle_kwargs())
         tot_s += time.perf_counter() - t0
         tot_pts += n * n * steps
     return tot_pts / tot_s, tot_s
@@ -423,6 +448,11 @@ def main():
            "cfl": {"cfd": 0.91, "mfd": 0.81}, "l2": "inputs larger than L2 (2.1 GB per field); no flush",
            "parallelism": "1 GPU" if ws == 1 else
            f"{ws} GPUs: one grid band-decomposed (rows), NCCL halo exchange per step"}
+    if a.full:
+        cfg["workload"] = (f"config4 size: single {a.n}x{a.n}-node grid, full-matrix CFD variant (NEXT row "
+                           f"f4, ADI_CFD_FULL: every node unknown, no Dirichlet data) with a Cerjan layer "
+                           f"nb={ABSORB_NB}, a={ABSORB_A}; MMS initial state, dense source on every node")
+        cfg["cfl"] = {"cfd_full": 0.91}
     if a.media:
         cfg["workload"] += " + heterogeneous medium (NEXT row f3: fp32 kappa, rho^-1 grids, adi_set_media)"
         cfg["media"] = "smooth: kappa = 0.8 (1 + 0.25 sin(2 pi x + 0.3) cos(2 pi y)), rho^-1 analogous"
