@@ -76,3 +76,19 @@ def test_band_group_batch_shots(adi):
                        **p.oracle_kwargs())
         for a, c in zip(got, o):
             assert rel(a[b], c) <= 1e-12
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+def test_band_group_with_media(adi, method):
+    """Heterogeneous media (f3) inside the band decomposition: each band's handle holds
+    the whole medium; the gathered result equals the oracle."""
+    n, world, split = 1601, 3, [1, 1]
+    p = random_problem(method, n, seed=77, steps=sum(split), media=True)
+    g, solvers = make_group(adi, p, world)
+    for k in split:
+        g.step(k)
+    got = g.gather()
+    o = oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, p.U, p.V, p.W, nsteps=sum(split),
+                   **p.oracle_kwargs())
+    for name, a, c in zip("UVW", got, o):
+        assert rel(a, c) <= 1e-12, (name, rel(a, c))

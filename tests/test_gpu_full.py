@@ -128,3 +128,21 @@ def test_full_api_errors(adi):
     with pytest.raises(adi.AdiError):
         r.set_param(adi.ADI_ABSORB_WIDTH, 5)     # the layer belongs to the full variant
     r.close()
+
+
+def test_full_batch(adi):
+    """A batch of 2 full-variant grids (shared source pattern and layer)."""
+    n, B, steps = 1601, 2, 2
+    qs = [problem(n, n, steps, seed=30 + b) for b in range(B)]
+    q0 = qs[0]
+    s = adi.AdiSolver(n, n, q0["h"], q0["dt"], 1.0, adi.ADI_CFD_FULL, batch=B)
+    s.set_fields(np.stack([q["U"] for q in qs]), np.stack([q["V"] for q in qs]), np.stack([q["W"] for q in qs]))
+    s.set_source(q0["phi"], None, q0["gf"])
+    s.set_param(adi.ADI_ABSORB_WIDTH, 20)
+    s.step(steps)
+    g = s.get_fields()
+    s.close()
+    for b, q in enumerate(qs):
+        o = oracle.run_full(n, n, q0["h"], q0["dt"], 1.0, 8, q["U"], q["V"], q["W"], phi=q0["phi"], gf=q0["gf"],
+                            nsteps=steps, nb=20)
+        assert_parity([x[b] for x in g], o, what=f"full batch member {b}")
