@@ -30,7 +30,12 @@
  *       W̄ = ny x (nx-1) (N_y+1 nodes x N_x centres).
  * The edge velocity lines that the paper never updates are not state [G12].
  *
- * Parity status of each function is listed in DESIGN.md §4 (all pinned).
+ * NEXT rows: heterogeneous media (f3: per-point alpha, beta in stage_line and
+ * or_run, from or_problem.kappa / rv / rw) and the full-matrix CFD variant with a
+ * Cerjan layer (f4: or_run_full, stage_line_full).
+ *
+ * Parity status of each function is listed in DESIGN.md §4, §8.3 and §8.4 (all
+ * pinned).
  */
 #include <math.h>
 #include <stdlib.h>
