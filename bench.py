@@ -478,6 +478,8 @@ def main():
         print(json.dumps(line))
         return
 
+    if a.full and ws > 1:
+        raise SystemExit("bench.py --full: the full-matrix variant has no band decomposition (N = 1 only)")
     r = run_ours(a, ws, rank, local)
     if rank != 0:
         return
