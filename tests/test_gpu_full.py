@@ -146,3 +146,19 @@ def test_full_batch(adi):
         o = oracle.run_full(n, n, q0["h"], q0["dt"], 1.0, 8, q["U"], q["V"], q["W"], phi=q0["phi"], gf=q0["gf"],
                             nsteps=steps, nb=20)
         assert_parity([x[b] for x in g], o, what=f"full batch member {b}")
+
+
+@pytest.mark.parametrize("n,chunks,K", [(301, 16, 8), (517, 6, 3)])
+def test_full_forced_segments(adi, n, chunks, K):
+    """Forced multi-segment tilings (ADI_TILE_CHUNKS: 64-point halos on a small grid)
+    and K != 8."""
+    q = problem(n, n, 3, seed=n + chunks)
+    s = adi.AdiSolver(n, n, q["h"], q["dt"], 1.0, adi.ADI_CFD_FULL, K=K)
+    s.set_param(adi.ADI_TILE_CHUNKS, chunks)
+    s.set_fields(q["U"], q["V"], q["W"])
+    s.set_source(q["phi"], None, q["gf"])
+    s.set_param(adi.ADI_ABSORB_WIDTH, 12)
+    s.step(3)
+    g = s.get_fields()
+    s.close()
+    assert_parity(g, run_oracle(q, 3, nb=12, K=K), what=f"full {n} chunks={chunks} K={K}")

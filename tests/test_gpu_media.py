@@ -160,3 +160,16 @@ def test_media_api_errors(adi):
         kw.pop(k)
     o = oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, p.U, p.V, p.W, m0=1, nsteps=1, **kw)
     assert_parity(g, o, what="media cleared")
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+@pytest.mark.parametrize("n,chunks", [(301, 16), (517, 6)])
+def test_media_forced_segments(adi, method, n, chunks):
+    """Forced multi-segment tilings (halos on a small grid) with media."""
+    p = random_problem(method, n, seed=n + chunks, steps=2, media=True)
+    s = adi.AdiSolver.from_problem(p)
+    s.set_param(adi.ADI_TILE_CHUNKS, chunks)
+    s.step(2)
+    g = s.get_fields()
+    s.close()
+    assert_parity(g, run_oracle(p, 2), what=f"media {n} chunks={chunks}")
