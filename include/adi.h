@@ -84,6 +84,7 @@ enum adi_status {
   ADI_EZEROPIVOT = -4,  /* zero pivot in the LU of P or P̄ */
   ADI_ENONFINITE = -5,  /* a field became NaN/Inf (checked when ADI_CHECK_FINITE=1) */
   ADI_ESTATE = -6,      /* call out of order (e.g. step before set_fields) */
+  ADI_ENCCL = -7,       /* NCCL unavailable or failed (adi_create_dist, adi_nccl_unique_id) */
   ADI_WUNSTABLE = 1     /* warning: c*dt/h above the inner-iteration limit
                            (2/sqrt(6) ~ 0.8165 MFD, 2/sqrt(3) ~ 1.155 CFD; SURVEY SA-3) */
 };
@@ -127,6 +128,12 @@ typedef struct adi_stats {
   int nonfinite;        /* 1 if a non-finite value was produced (needs ADI_CHECK_FINITE) */
   int k_sweeps;
   long long kernel_launches; /* kernels launched by adi_step since creation */
+  /* the last-sweep residuals (ADI_EPS > 0): for the last row [0] and column [1] stage,
+   * the Alg. 3/4 test ||U_k - U_{k-1}||_F + ||V_k - V_{k-1}||_F at the chosen sweep
+   * last_k; -1 and K when the rule is off (reading them
+   * synchronizes the handle's stream) */
+  double last_test[2];
+  int last_k[2];
 } adi_stats;
 
 /* Create a solver for one grid (batch = 1).  nx, ny >= 9 nodes (N >= 8);
@@ -221,6 +228,24 @@ int adi_step_end(adi_handle h);
  * adi_halo_unpack stores the neighbour's message into this band's halo. */
 int adi_set_band(adi_handle h, int y0, int y1);
 int adi_band_info(adi_handle h, int* y0, int* y1, int* halo, int* npos);
+
+/* One rank of a grid line-sharded over `nranks` processes, one GPU each (
+ * DESIGN.md §7), with the exchange INSIDE the library: the handle owns the band
+ * adi_dist_bands gives `rank` (adi_set_band), and adi_step performs the halo exchanges
+ * itself, as NCCL grouped ncclSend/ncclRecv on the handle's stream: U and W̄ before
+ * a call's prologue (skipped right after adi_set_fields), S and W* after every row
+ * sweep.  The handle lives on the calling thread's current CUDA device.
+ * nccl_unique_id: the 128 bytes of adi_nccl_unique_id from one rank, given to all;
+ * every rank must call adi_step with the same n (collective).  adi_set_fields /
+ * adi_get_fields move the band's rows (see adi_set_band).  nranks = 1: a plain handle.
+ * libnccl.so.2 is loaded at run time; ADI_ENCCL if it is missing or fails.  Not for
+ * ADI_CFD_FULL with nranks > 1 (ADI_EINVAL).  The step phases (adi_step_begin ..)
+ * do not exchange: drivers that call them exchange through adi_halo_pack/unpack. */
+int adi_create_dist(int nx, int ny, double h, double dt, double c, int method, int batch,
+                    const void* nccl_unique_id, int rank, int nranks, adi_handle* out);
+int adi_nccl_unique_id(void* out128);
+/* The band cuts of y positions [0, npos) over nranks: cuts[0..nranks] (host logic only). */
+int adi_dist_bands(int npos, int nranks, int* cuts);
 int adi_halo_bytes(adi_handle h, int kind, int side, size_t* bytes);
 int adi_halo_pack(adi_handle h, int kind, int side, void* dev_buf);
 int adi_halo_unpack(adi_handle h, int kind, int side, const void* dev_buf);

@@ -29,6 +29,7 @@ ADI_ECUDA = -3
 ADI_EZEROPIVOT = -4
 ADI_ENONFINITE = -5
 ADI_ESTATE = -6
+ADI_ENCCL = -7
 ADI_WUNSTABLE = 1
 ADI_K_SWEEPS = 0
 ADI_RHO = 1
@@ -42,7 +43,7 @@ ADI_ABSORB_RATE = 8
 KERNEL_KINDS = ("prologue", "row", "col", "final", "edge")
 
 _STATUS = {0: "ADI_OK", -1: "ADI_EINVAL", -2: "ADI_ENOMEM", -3: "ADI_ECUDA", -4: "ADI_EZEROPIVOT",
-           -5: "ADI_ENONFINITE", -6: "ADI_ESTATE", 1: "ADI_WUNSTABLE"}
+           -5: "ADI_ENONFINITE", -6: "ADI_ESTATE", -7: "ADI_ENCCL", 1: "ADI_WUNSTABLE"}
 
 
 class AdiError(RuntimeError):
@@ -53,7 +54,8 @@ class AdiError(RuntimeError):
 
 class adi_stats(ctypes.Structure):
     _fields_ = [("steps", ctypes.c_longlong), ("t", ctypes.c_double), ("nonfinite", ctypes.c_int),
-                ("k_sweeps", ctypes.c_int), ("kernel_launches", ctypes.c_longlong)]
+                ("k_sweeps", ctypes.c_int), ("kernel_launches", ctypes.c_longlong),
+                ("last_test", ctypes.c_double * 2), ("last_k", ctypes.c_int * 2)]
 
 
 _lib = None
@@ -80,6 +82,9 @@ def lib():
         L.adi_set_point_sources.argtypes = [H, P, P, P, I]
         L.adi_set_boundary.argtypes = [H, P, P, I]
         L.adi_set_media.argtypes = [H, P, P, P]
+        L.adi_create_dist.argtypes = [I, I, D, D, D, I, I, P, I, I, ctypes.POINTER(H)]
+        L.adi_nccl_unique_id.argtypes = [P]
+        L.adi_dist_bands.argtypes = [I, I, P]
         L.adi_step.argtypes = [H, I]
         L.adi_get_fields.argtypes = [H, P, P, P]
         L.adi_get_fields_device.argtypes = [H, P, P, P]
@@ -107,7 +112,7 @@ def lib():
 
 EXPORTS = ["adi_create", "adi_create_batch", "adi_set_param", "adi_set_stream", "adi_set_fields",
            "adi_set_fields_device", "adi_set_source", "adi_set_point_sources", "adi_set_boundary",
-           "adi_set_media", "adi_step", "adi_step_begin", "adi_step_rows", "adi_step_cols", "adi_step_end", "adi_set_band",
+           "adi_set_media", "adi_create_dist", "adi_nccl_unique_id", "adi_dist_bands", "adi_step", "adi_step_begin", "adi_step_rows", "adi_step_cols", "adi_step_end", "adi_set_band",
            "adi_band_info", "adi_halo_bytes", "adi_halo_pack", "adi_halo_unpack",
            "adi_get_fields", "adi_get_fields_device", "adi_set_fields_async", "adi_get_fields_async", "adi_get_stats", "adi_get_kernel_times",
            "adi_set_trace", "adi_get_last_sweeps", "adi_last_error",
@@ -143,6 +148,29 @@ def adi_create_batch(nx, ny, h, dt, c, method, batch):
     rc = lib().adi_create_batch(nx, ny, h, dt, c, method, batch, ctypes.byref(hd))
     _check(None, rc, "adi_create")
     return hd, rc
+
+
+def adi_nccl_unique_id():
+    """The 128-byte NCCL unique id for adi_create_dist (call on one rank, share with all)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(None, lib().adi_nccl_unique_id(buf), "adi_nccl_unique_id")
+    return buf.raw
+
+
+def adi_create_dist(nx, ny, h, dt, c, method, batch, unique_id, rank, nranks):
+    """One rank of a line-sharded grid with the NCCL halo exchange inside adi_step."""
+    hd = ctypes.c_void_p()
+    uid = None if unique_id is None else ctypes.create_string_buffer(bytes(unique_id), 128)
+    rc = lib().adi_create_dist(nx, ny, h, dt, c, method, batch, uid, rank, nranks, ctypes.byref(hd))
+    _check(None, rc, "adi_create_dist")
+    return hd, rc
+
+
+def adi_dist_bands(npos, nranks):
+    """Band cuts of y positions [0, npos) over nranks (the library's plan)."""
+    cuts = np.zeros(nranks + 1, dtype=np.int32)
+    _check(None, lib().adi_dist_bands(npos, nranks, _ptr(cuts)), "adi_dist_bands")
+    return [int(x) for x in cuts]
 
 
 def adi_set_param(hd, key, value):
@@ -266,7 +294,8 @@ def adi_get_fields_device(hd, dU, dV, dW):
 def adi_get_stats(hd):
     s = adi_stats()
     _check(hd, lib().adi_get_stats(hd, ctypes.byref(s)), "adi_get_stats")
-    return {k: getattr(s, k) for k, _ in adi_stats._fields_}
+    return {k: (list(getattr(s, k)) if isinstance(getattr(s, k), ctypes.Array) else getattr(s, k))
+            for k, _ in adi_stats._fields_}
 
 
 def adi_set_trace(hd, buf, cap: int, kind: int):

@@ -21,6 +21,9 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>   // types only: libnccl is loaded at run time (adi_create_dist)
+
 #include "adi.h"
 #include "adi_line.cuh"
 
@@ -58,7 +61,7 @@ struct adi_ctx {
   int timing = 0;
   double eps = 0.0;      // ADI_EPS: inner stopping rule off (fixed K sweeps) when 0
   int kmin = 6;          // ADI_K_MIN
-  double* d_norms = nullptr;  // [K+1][2] per-sweep squared changes of one stage
+  double* d_norms = nullptr;  // [2 stages][K+1][2] per-sweep squared changes (rows, columns)
   int d_norms_cap = 0;
   int* d_k = nullptr;         // [4]: chosen sweeps (rows, columns) of the last step, gates
   unsigned long long* trace = nullptr;  // adi_set_trace
@@ -100,6 +103,14 @@ struct adi_ctx {
   int absorb_nb = 0;          // ADI_ABSORB_WIDTH (Cerjan layer, points)
   double absorb_a = 0.015;    // ADI_ABSORB_RATE
   double* d_taper = nullptr;  // taper[d], d < absorb_nb
+  // adi_create_dist: this rank's band of a line-sharded grid; NCCL halo exchange inside
+  // adi_step (the protocol of dist.step_distributed)
+  bool dist = false;
+  int rank = 0, nranks = 1;
+  ncclComm_t comm = nullptr;
+  bool fresh = true;             // every rank holds its band + halo rows (after set_fields)
+  double* hbuf[2][2][2] = {};    // [kind][side][send, recv]
+  size_t hcount[2][2][2] = {};   // elements
   // internal layouts: Sa, V, V2 row-major; Sb = S^T; W, W2 = W̄^T (columns contiguous)
   int* flag = nullptr;
   adi::Axis ax, ay;
@@ -137,6 +148,45 @@ int fail(adi_ctx* h, int code, const std::string& msg) {
     cudaError_t e_ = (call);                                                               \
     if (e_ != cudaSuccess)                                                                 \
       return fail((h), ADI_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+// ---- NCCL, loaded at run time (adi_create_dist) ---------------------------------
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+bool nccl_load() {
+  if (g_nccl.tried) return g_nccl.ok;
+  g_nccl.tried = true;
+  // the process may already hold a libnccl (e.g. torch's); the soname resolves to it
+  void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!lib) return false;
+  auto sym = [&](const char* n) { return dlsym(lib, n); };
+  g_nccl.getUniqueId = (decltype(g_nccl.getUniqueId))sym("ncclGetUniqueId");
+  g_nccl.commInitRank = (decltype(g_nccl.commInitRank))sym("ncclCommInitRank");
+  g_nccl.commDestroy = (decltype(g_nccl.commDestroy))sym("ncclCommDestroy");
+  g_nccl.send = (decltype(g_nccl.send))sym("ncclSend");
+  g_nccl.recv = (decltype(g_nccl.recv))sym("ncclRecv");
+  g_nccl.groupStart = (decltype(g_nccl.groupStart))sym("ncclGroupStart");
+  g_nccl.groupEnd = (decltype(g_nccl.groupEnd))sym("ncclGroupEnd");
+  g_nccl.errorString = (decltype(g_nccl.errorString))sym("ncclGetErrorString");
+  g_nccl.ok = g_nccl.getUniqueId && g_nccl.commInitRank && g_nccl.commDestroy && g_nccl.send && g_nccl.recv &&
+              g_nccl.groupStart && g_nccl.groupEnd && g_nccl.errorString;
+  return g_nccl.ok;
+}
+#define NCCL_TRY(h, call)                                                                          \
+  do {                                                                                             \
+    ncclResult_t r_ = (call);                                                                      \
+    if (r_ != ncclSuccess) return fail((h), ADI_ENCCL, std::string(#call) + ": " + g_nccl.errorString(r_)); \
   } while (0)
 
 // Host -> device copies of set-up data.  They go on the handle's stream and are
@@ -759,17 +809,18 @@ adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
 // exit at once, so the outputs are those of the chosen k (the stage's inputs are
 // never overwritten).
 int stage_with_rule(adi_ctx* h, int mode_t, const adi::Axis& A, adi::KParams p, int kind, int which) {
-  CUDA_TRY(h, cudaMemsetAsync(h->d_norms, 0, sizeof(double) * 2 * (h->K + 1), h->stream));
+  double* norms = h->d_norms + (size_t)which * 2 * (h->K + 1);
+  CUDA_TRY(h, cudaMemsetAsync(norms, 0, sizeof(double) * 2 * (h->K + 1), h->stream));
   CUDA_TRY(h, cudaMemsetAsync(h->d_k + 2 + which, 0, sizeof(int), h->stream));
   p.Kdev = nullptr;
   p.gate = h->d_k + 2 + which;
   for (int k = h->kmin; k <= h->K; ++k) {
     adi::KParams q = p;
     q.K = k;
-    q.norms = h->d_norms + 2 * k;
+    q.norms = norms + 2 * k;
     int rc = launch(h, mode_t, A, q, kind);
     if (rc) return rc;
-    adi::decide_sweeps_kernel<<<1, 1, 0, h->stream>>>(h->d_norms + 2 * k, h->eps, k, h->K,
+    adi::decide_sweeps_kernel<<<1, 1, 0, h->stream>>>(norms + 2 * k, h->eps, k, h->K,
                                                         h->d_k + 2 + which, h->d_k + which);
     CUDA_TRY(h, cudaGetLastError());
     h->launches++;
@@ -778,6 +829,12 @@ int stage_with_rule(adi_ctx* h, int mode_t, const adi::Axis& A, adi::KParams p, 
 }
 
 void free_ctx(adi_ctx* h) {
+  for (auto& k : h->hbuf)
+    for (auto& sd : k)
+      for (double*& b : sd)
+        if (b) { cudaFree(b); b = nullptr; }
+  if (h->comm && g_nccl.ok) g_nccl.commDestroy(h->comm);
+  h->comm = nullptr;
   for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
   for (double* q : {h->Ubase, h->V, h->W, h->V2, h->W2, h->Sa, h->Sb, h->phi, h->phiT, h->Ca, h->Cb}) dfree(q);
@@ -787,6 +844,18 @@ void free_ctx(adi_ctx* h) {
     for (void* q : {(void*)A->d_segs, (void*)A->d_tabU, (void*)A->d_tabX, (void*)A->d_ptl,
                     (void*)A->d_ptp})
       if (q) cudaFree(q);
+}
+
+// band cuts of y positions [0, npos) over nranks (as dist.band_partition, align 4): interior
+// cuts b with (b - 1) % 4 == 0, so each band's row sweep starts on a 4-line group
+void dist_bands(int npos, int nranks, int* cuts) {
+  cuts[0] = 0;
+  for (int k = 1; k < nranks; ++k) {
+    const double b = (double)k * npos / nranks;
+    const int q = std::max(1, (int)std::nearbyint((b - 1.0) / 4.0));   // ties to even, as Python round
+    cuts[k] = 1 + 4 * q;
+  }
+  cuts[nranks] = npos;
 }
 
 // ---- heterogeneous media (NEXT row f3) ------------------------------------------
@@ -1000,6 +1069,7 @@ static int set_fields_impl(adi_handle h, const double* U, const double* V, const
   }
   if (kind == cudaMemcpyHostToDevice && sync) CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   h->fields_set = true;
+  h->fresh = true;   // the band and its halo rows hold the state: no call-start exchange
   return ADI_OK;
 }
 
@@ -1191,7 +1261,7 @@ int adi_step_begin(adi_handle h, int nsteps) {
       if (h->d_norms) cudaFree(h->d_norms);
       h->d_norms = nullptr;
       h->d_norms_cap = 0;
-      CUDA_TRY(h, cudaMalloc(&h->d_norms, sizeof(double) * 2 * (h->K + 1)));
+      CUDA_TRY(h, cudaMalloc(&h->d_norms, sizeof(double) * 4 * (h->K + 1)));
       h->d_norms_cap = h->K + 1;
     }
     if (!h->d_k) CUDA_TRY(h, cudaMalloc(&h->d_k, 4 * sizeof(int)));
@@ -1287,15 +1357,25 @@ int adi_step_end(adi_handle h) {
   return ADI_OK;
 }
 
+static int dist_exchange(adi_ctx* h, int kind);
+
 int adi_step(adi_handle h, int nsteps) {
   if (!h) return ADI_EINVAL;
   if (nsteps < 0) return fail(h, ADI_EINVAL, "n < 0");
   if (nsteps == 0) return ADI_OK;
-  int rc = adi_step_begin(h, nsteps);
+  // a handle of adi_create_dist: the halo exchanges of DESIGN.md §7 happen here (U and W̄
+  // before the call's prologue unless the fields were just set; S and W* after every
+  // row sweep), NCCL grouped send/recv on the handle's stream
+  const bool ex = h->dist && h->nranks > 1;
+  int rc = ADI_OK;
+  if (ex && !h->fresh) rc = dist_exchange(h, 1);
+  if (rc == ADI_OK) rc = adi_step_begin(h, nsteps);
   for (int k = 0; k < nsteps && rc == ADI_OK; ++k) {
     rc = adi_step_rows(h);
+    if (rc == ADI_OK && ex) rc = dist_exchange(h, 0);
     if (rc == ADI_OK) rc = adi_step_cols(h);
   }
+  if (rc == ADI_OK) h->fresh = false;
   if (rc != ADI_OK) { h->in_call = false; return rc; }
   return adi_step_end(h);
 }
@@ -1405,6 +1485,98 @@ int adi_halo_unpack(adi_handle h, int kind, int side, const void* dev_buf) {
   return halo_copy(h, kind, a, b, (double*)dev_buf, 1);
 }
 
+// ---- adi_create_dist: the band decomposition with NCCL inside the library ----------
+static int dist_exchange(adi_ctx* h, int kind) {
+  const int peer[2] = {h->rank - 1, h->rank + 1};   // side 0: low, 1: high
+  for (int side = 0; side < 2; ++side) {
+    if (peer[side] < 0 || peer[side] >= h->nranks) continue;
+    int a, b;
+    halo_range(h, side, 1, &a, &b);
+    int rc = halo_copy(h, kind, a, b, h->hbuf[kind][side][0], 0);
+    if (rc) return rc;
+  }
+  NCCL_TRY(h, g_nccl.groupStart());
+  for (int side = 0; side < 2; ++side) {
+    if (peer[side] < 0 || peer[side] >= h->nranks) continue;
+    NCCL_TRY(h, g_nccl.send(h->hbuf[kind][side][0], h->hcount[kind][side][0], ncclFloat64, peer[side], h->comm,
+                            h->stream));
+    NCCL_TRY(h, g_nccl.recv(h->hbuf[kind][side][1], h->hcount[kind][side][1], ncclFloat64, peer[side], h->comm,
+                            h->stream));
+  }
+  NCCL_TRY(h, g_nccl.groupEnd());
+  for (int side = 0; side < 2; ++side) {
+    if (peer[side] < 0 || peer[side] >= h->nranks) continue;
+    int a, b;
+    halo_range(h, side, 0, &a, &b);
+    int rc = halo_copy(h, kind, a, b, h->hbuf[kind][side][1], 1);
+    if (rc) return rc;
+  }
+  return ADI_OK;
+}
+
+int adi_dist_bands(int npos, int nranks, int* cuts) {
+  if (npos < 1 || nranks < 1 || !cuts) return ADI_EINVAL;
+  dist_bands(npos, nranks, cuts);
+  return ADI_OK;
+}
+
+int adi_nccl_unique_id(void* out) {
+  if (!out) return ADI_EINVAL;
+  if (!nccl_load()) return ADI_ENCCL;
+  ncclUniqueId id;
+  if (g_nccl.getUniqueId(&id) != ncclSuccess) return ADI_ENCCL;
+  std::memcpy(out, &id, sizeof id);
+  return ADI_OK;
+}
+
+int adi_create_dist(int nx, int ny, double hh, double dt, double c, int method, int batch,
+                    const void* nccl_unique_id, int rank, int nranks, adi_handle* out) {
+  if (!out) return ADI_EINVAL;
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !nccl_unique_id)) return ADI_EINVAL;
+  if (method == ADI_CFD_FULL && nranks > 1) return ADI_EINVAL;   // no band decomposition
+  adi_handle h = nullptr;
+  int rc = adi_create_batch(nx, ny, hh, dt, c, method, batch, &h);
+  if (rc < 0) return rc;
+  const int warn = rc;
+  h->dist = true;
+  h->rank = rank;
+  h->nranks = nranks;
+  if (nranks > 1) {
+    std::vector<int> cuts(nranks + 1);
+    dist_bands(h->ay.n + 1, nranks, cuts.data());
+    int e = adi_set_band(h, cuts[rank], cuts[rank + 1]);
+    if (e) { adi_destroy(h); return e; }
+    if (!nccl_load()) { adi_destroy(h); return ADI_ENCCL; }
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof id);
+    if (g_nccl.commInitRank(&h->comm, nranks, id, rank) != ncclSuccess) {
+      h->comm = nullptr;
+      adi_destroy(h);
+      return ADI_ENCCL;
+    }
+    for (int kind = 0; kind < 2; ++kind)
+      for (int side = 0; side < 2; ++side) {
+        const int peer = side == 0 ? rank - 1 : rank + 1;
+        if (peer < 0 || peer >= nranks) continue;
+        for (int own = 1; own >= 0; --own) {   // send = own rows, recv = the neighbour's
+          int a, b;
+          halo_range(h, side, own, &a, &b);
+          const size_t n = halo_elems(h, kind, b - a);
+          double*& buf = h->hbuf[kind][side][own ? 0 : 1];
+          h->hcount[kind][side][own ? 0 : 1] = n;
+          if (cudaMalloc(&buf, std::max<size_t>(n, 1) * sizeof(double)) != cudaSuccess) {
+            cudaGetLastError();
+            adi_destroy(h);
+            return ADI_ENOMEM;
+          }
+        }
+      }
+  }
+  *out = h;
+  return warn;
+}
+
 int adi_band_info(adi_handle h, int* y0, int* y1, int* halo, int* npos) {
   if (!h) return ADI_EINVAL;
   if (y0) *y0 = h->band_y0 > h->ay.n ? 0 : h->band_y0;
@@ -1472,11 +1644,28 @@ int adi_get_last_sweeps(adi_handle h, int* k_rows, int* k_cols) {
 
 int adi_get_stats(adi_handle h, adi_stats* s) {
   if (!h || !s) return ADI_EINVAL;
+  h->err.clear();
   s->steps = h->m;
   s->t = h->m * h->dt;
   s->nonfinite = h->nonfinite;
   s->k_sweeps = h->K;
   s->kernel_launches = h->launches;
+  s->last_test[0] = s->last_test[1] = -1.0;
+  s->last_k[0] = s->last_k[1] = h->K;
+  // the stopping rule's test value (Alg. 3/4) at the chosen sweep of the last row and
+  // column stage; this synchronizes the handle's stream
+  if (h->eps > 0.0 && h->d_norms && h->d_k && h->m > 0 && !h->in_call && h->d_norms_cap >= h->K + 1) {
+    std::vector<double> n(4 * (size_t)(h->K + 1));
+    int k[2];
+    CUDA_TRY(h, cudaMemcpyAsync(n.data(), h->d_norms, n.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaMemcpyAsync(k, h->d_k, sizeof k, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    for (int st = 0; st < 2; ++st) {
+      const double* q = n.data() + (size_t)st * 2 * (h->K + 1) + 2 * k[st];
+      s->last_k[st] = k[st];
+      s->last_test[st] = std::sqrt(q[0]) + std::sqrt(q[1]);
+    }
+  }
   return ADI_OK;
 }
 

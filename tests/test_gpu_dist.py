@@ -92,3 +92,24 @@ def test_band_group_with_media(adi, method):
                    **p.oracle_kwargs())
     for name, a, c in zip("UVW", got, o):
         assert rel(a, c) <= 1e-12, (name, rel(a, c))
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+def test_create_dist_single_rank(adi, method):
+    """adi_create_dist with nranks = 1 is a plain handle: parity with the oracle through
+    the same set/step/get calls (the multi-rank NCCL exchange needs one GPU per rank)."""
+    p = random_problem(method, 1601, seed=21, steps=2)
+    hd, rc = adi.adi_create_dist(p.nx, p.ny, p.h, p.dt, p.c, method, 1, None, 0, 1)
+    assert rc >= 0
+    adi.adi_set_fields(hd, p.U, p.V, p.W)
+    adi.adi_set_source(hd, p.phi, -1, -1, p.gf)
+    adi.adi_set_boundary(hd, p.edges, p.gb)
+    adi.adi_step(hd, 2)
+    import numpy as np
+    from adi_inputs import shapes
+    out = [np.zeros(s) for s in shapes(method, p.nx, p.ny)]
+    adi.adi_get_fields(hd, *out)
+    adi.adi_destroy(hd)
+    o = oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, p.U, p.V, p.W, nsteps=2, **p.oracle_kwargs())
+    for name, a, c in zip("UVW", out, o):
+        assert rel(a, c) <= 1e-12, (name, rel(a, c))

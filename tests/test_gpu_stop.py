@@ -47,6 +47,12 @@ def test_stopping_rule_matches_oracle(adi, method, n):
     for st in range(steps):
         s.step(1)
         assert adi.adi_get_last_sweeps(s.handle) == tuple(int(k) for k in info["k"][st]), st
+        # adi_get_stats: the last-sweep residuals (the Alg. 3/4 test at the chosen k)
+        stt = s.stats()
+        for stage in range(2):
+            k = int(info["k"][st, stage])
+            assert stt["last_k"][stage] == k
+            assert stt["last_test"][stage] == pytest.approx(info["tests"][st, stage, k], rel=1e-10)
     g = s.get_fields()
     s.close()
     assert kmin < info["k"][0, 0] < K           # the rule actually stopped early
@@ -59,6 +65,8 @@ def test_eps_zero_reports_fixed_sweeps(adi):
     s = adi.AdiSolver.from_problem(p)
     s.step(1)
     assert adi.adi_get_last_sweeps(s.handle) == (p.K, p.K)
+    stt = s.stats()
+    assert stt["last_test"] == [-1.0, -1.0] and stt["last_k"] == [p.K, p.K]
     s.close()
 
 
