@@ -223,6 +223,26 @@ def kernel_bytes(method, n, kind, has_phi=True, media=False):
     return 0
 
 
+FP64_PEAK_TFLOPS = 34.2   # measured: profiles/r01/fp64_probe.txt (independent DFMA streams)
+
+
+def kernel_flops(method, n, kind, K):
+    """Algorithmic fp64 flops of one launch (+, -, x one flop each):
+    7 per point and operator application (MFD: the 4-point D4/G4 stencil, 5, then
+    out = B - a s, 2; CFD: the Q̄/Q difference, 1, the Thomas forward and backward steps
+    with precomputed factors, 2 + 2, then out = B - a z, 2).  Row / column kernels apply
+    2K + 1 operators (K sweeps + the fused explicit half) plus 4 flops of epilogue (source
+    and X' = 2x - X); FINAL 2K; the prologue 2 plus the source."""
+    pts = n * n
+    if kind in ("row", "col"):
+        return pts * (7 * (2 * K + 1) + 4)
+    if kind == "final":
+        return pts * 7 * 2 * K
+    if kind == "prologue":
+        return pts * (7 * 2 + 2)
+    return 0
+
+
 def run_ours(a, ws, rank, local):
     """N = 1: one grid per method.  N > 1: the same grid band-decomposed over the
     ranks (NCCL halo exchange through torch.distributed)."""
@@ -322,7 +342,7 @@ def run_ours(a, ws, rank, local):
             "kernel_avg_ms": {k: v[0] / v[1] for k, v in ksum.items()},
             "dominant": kind}
         cand = {"method": MNAME[m], "kind": kind, "achieved": ach, "bytes": byt, "share": kms / tot,
-                "avg_ms": kms / kcnt, "cnt": kcnt}
+                "avg_ms": kms / kcnt, "cnt": kcnt, "flops": kernel_flops(m, n, kind, a.K) / ws}
         if dominant is None or cand["avg_ms"] * kcnt > dominant["avg_ms"] * dominant["cnt"]:
             dominant = cand
     tkey = f"{dominant['method']}_{dominant['kind']}_{n}" + ("_media" if a.media else "")
@@ -332,6 +352,12 @@ def run_ours(a, ws, rank, local):
             "kernel": f"adi_line_kernel[{dominant['method']},{dominant['kind']}]",
             "algorithmic_bytes_per_launch": dominant["bytes"], "peak_source": peak_src,
             "avg_launch_ms": round(dominant["avg_ms"], 4)}
+    # the second roof SURVEY §8d asks for: the same launch against the fp64 pipe
+    fl_ach = dominant["flops"] / (dominant["avg_ms"] * 1e-3) / 1e12
+    roof_fp64 = {"bound": "fp64", "achieved": round(fl_ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                 "frac": round(fl_ach / FP64_PEAK_TFLOPS, 4), "kernel": roof["kernel"],
+                 "algorithmic_flops_per_launch": dominant["flops"],
+                 "peak_source": "measured (profiles/r01/fp64_probe.txt, independent DFMA streams)"}
     # ---- end to end through the C-ABI with host buffers (pinned), copies timed
     e2e = None
     if not a.no_e2e and ws == 1:
@@ -407,7 +433,8 @@ def run_ours(a, ws, rank, local):
                        "the band's rows (pageable), max over ranks; bytes per step of rank 0"}
     for s, _, _ in solvers.values():
         s.close()
-    return {"value": value, "ms_per_step": total_ms / a.steps, "roofline": roof, "clocks": clocks,
+    return {"value": value, "ms_per_step": total_ms / a.steps, "roofline": roof, "roofline_fp64": roof_fp64,
+            "clocks": clocks,
             "e2e": e2e, "gpu_launches": launches, "per_method": per_method}
 
 
@@ -495,7 +522,7 @@ def main():
     line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": ws, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
-            "roofline": r["roofline"], "cpu_baseline": cpu, "clocks": r["clocks"], "e2e": r["e2e"],
+            "roofline": r["roofline"], "roofline_fp64": r["roofline_fp64"], "cpu_baseline": cpu, "clocks": r["clocks"], "e2e": r["e2e"],
             "gpu_launches": r["gpu_launches"], "per_method": r["per_method"]}
     print(json.dumps(line))
 
