@@ -588,7 +588,10 @@ __device__ __forceinline__ void cfd_statics(const Ctx<M>& c, const EdgeTab& T, i
 }
 
 
-constexpr int NSUB = 4;
+#ifndef ADI_NSUB
+#define ADI_NSUB 2
+#endif
+constexpr int NSUB = ADI_NSUB;
 
 // ===========================================================================
 // CFD: one operator application out = B - coef * T^{-1} r(o) on the warp's
