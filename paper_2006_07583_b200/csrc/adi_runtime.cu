@@ -481,7 +481,13 @@ bool plan_axis(adi::Axis& A, int method, int cap, int lo_all, int hi_all) {
   const int M = adi::TM;
   const int chmax = cap > 0 ? std::min(cap, adi::TCH) : adi::TCH;
   const int P = A.n + 1;                       // positions 0..n
-  const int halo = (method == ADI_CFD) ? 64 : 32;
+#ifndef ADI_HALO_CFD
+#define ADI_HALO_CFD 56
+#endif
+#ifndef ADI_HALO_MFD
+#define ADI_HALO_MFD 28
+#endif
+  const int halo = (method == ADI_CFD) ? ADI_HALO_CFD : ADI_HALO_MFD;
   A.halo = halo;
   A.segs.clear();
   lo_all = std::max(lo_all, 0);

@@ -308,3 +308,17 @@ def test_parity_point_sources_batch_lean_tiles(adi):
     for b, p in enumerate(probs):
         o = run_oracle(p, steps)
         assert_parity([x[b] for x in got], o, what=f"shot {b}")
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+@pytest.mark.parametrize("n,chunks,steps", [(1001, 12, 3), (2101, 16, 2)])
+def test_segment_halo_is_exact(adi, method, n, chunks, steps):
+    """The segment halo is exact to round-off: forced short segments
+    (ADI_TILE_CHUNKS, many segment edges) against whole-line tiles on the GPU, max-norm
+    relative difference <= 1e-14 per field (a halo deficit shows up far above that)."""
+    p = random_problem(method, n, seed=n + chunks, steps=steps)
+    a = run_gpu(adi, p, steps)
+    b = run_gpu(adi, p, steps, chunks=chunks)
+    for name, x, y in zip("UVW", a, b):
+        d = np.abs(x - y).max() / np.abs(x).max()
+        assert d <= 1e-14, (name, d)
