@@ -240,7 +240,10 @@ int encode_lines(adi_ctx* h, const double* base, int pitch, int rows, size_t bst
   const cuuint32_t es[5] = {1, 1, 1, 1, 1};
   const CUresult r = g_encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)(base - adi::TMA_P0), dims, strides,
                               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+#ifndef ADI_L2PROMO
+#define ADI_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
+                              ADI_L2PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(h, ADI_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return ADI_OK;
 }
