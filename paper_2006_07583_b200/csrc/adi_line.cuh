@@ -116,6 +116,7 @@ struct KParams {
   // {tile, smid, t_start, t_loaded, t_ops_done, t_end} (%globaltimer ns)
   unsigned long long* trace;
   long long trace_cap;
+  int seg0, nseg_all;   // this launch's first segment, all segments of the axis (trace index)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -834,7 +835,8 @@ __device__ __forceinline__ void tma_load_seg(double* dst, const CUtensorMap* tm,
 // are interior and live (the lean path, no generic closures, no per-chunk
 // predicates); EDGE = true: line ends, dead chunks, short lines.
 // ===========================================================================
-template <int METHOD, int M, int NW, int MODE_, bool EDGE, bool HET = false, bool FULL = false>
+template <int METHOD, int M, int NW, int MODE_, bool EDGE, bool HET = false, bool FULL = false,
+          bool NOEND = false>
 __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, double* smem) {
   // FULL (NEXT row f4, CFD only, readings F1-F2): every position 0..n is
   // unknown and both operators are the full D = P^{-1} Q (the x-op's operator)
@@ -867,7 +869,9 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   const int pR = (METHOD == M_CFD) ? n : n + 1;   // position of ū's right Dirichlet value
   const bool lineok = line >= P.line_lo && line < P.nlines;
   const bool tr = P.trace && t == 0;
-  const long long tile = (long long)blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * b);
+  // trace index unique across the launches of one kernel kind (segment offset seg0 of nseg_all)
+  const long long tile =
+      (long long)blockIdx.x + (long long)gridDim.x * (P.seg0 + blockIdx.y + (long long)P.nseg_all * b);
   unsigned long long tr0 = tr ? gtimer() : 0ull, tr1 = 0ull, tr2 = 0ull;
 
   Ctx<M> c;
@@ -887,7 +891,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     c.nbint = true;
   }
   c.endc = EDGE ? -1 : sg.end - 1;
-  c.me = !EDGE && ((sg.end == 1 && lane == 0) || (sg.end >= 2 && lane == 31));
+  // NOEND: a launch of interior segments only, the line-end fix-ups compile away
+  c.me = !EDGE && !NOEND && ((sg.end == 1 && lane == 0) || (sg.end >= 2 && lane == 31));
 
   // ---- load: one TMA tensor copy per array and warp (zero fill outside the array)
   double* lS = stS + w * LSTR;
@@ -1371,7 +1376,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
 //   MODE = KM_FINAL   : as SWEEP without the fused explicit half; writes U_out
 //   MODE = KM_PROLOGUE: U_in, X_in -> a2 (explicit half only)
 // ===========================================================================
-template <int METHOD, int M, int NW, int MODE, bool EDGE, bool HET = false, bool FULL = false>
+template <int METHOD, int M, int NW, int MODE, bool EDGE, bool HET = false, bool FULL = false,
+          bool NOEND = false>
 __global__ void __launch_bounds__(32 * NW, (Occ<METHOD, EDGE, MODE, HET, FULL>::value))
     adi_line_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(128) double smem_raw[];
@@ -1380,7 +1386,7 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD, EDGE, MODE, HET, FULL>::
   double* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u) / 8u;
   if (P.gate && *P.gate) return;   // stopping rule: the stage was decided by an earlier attempt
   const Seg sg = P.segs[blockIdx.y];
-  line_tile<METHOD, M, NW, MODE, EDGE, HET, FULL>(P, sg, smem);
+  line_tile<METHOD, M, NW, MODE, EDGE, HET, FULL, NOEND>(P, sg, smem);
 }
 
 // The stopping rule after the attempt with k sweeps (Alg. 3/4 "until test <= eps or

@@ -42,7 +42,8 @@ struct Axis {
   int NL = 1;
   int plo = 0, phi = -1;
   std::vector<Seg> segs;   // interior segments (edge == 0) first
-  int nint = 0;            // number of interior segments
+  int nint = 0;            // number of lean segments (edge == 0)
+  int nmid = 0;            // of which without a line end (the first nmid)
   Seg* d_segs = nullptr;
   double* d_tabU = nullptr;  // CFD only
   double* d_tabX = nullptr;
@@ -594,9 +595,12 @@ int setup_axis(adi_ctx* h, adi::Axis& A, int n, int nlines, int nlmin) {
     else if (g.nchunks == adi::TCH && g.start >= 2 && full == n + 1) g.end = 3;
     else g.edge = 1;
   }
+  // launch order: lean interior segments (no line end), lean line-end segments, generic
   std::stable_partition(A.segs.begin(), A.segs.end(), [](const adi::Seg& g) { return g.edge == 0; });
+  std::stable_partition(A.segs.begin(), A.segs.end(), [](const adi::Seg& g) { return g.edge == 0 && g.end == 0; });
   A.nint = 0;
-  for (const adi::Seg& g : A.segs) A.nint += (g.edge == 0);
+  A.nmid = 0;
+  for (const adi::Seg& g : A.segs) { A.nint += (g.edge == 0); A.nmid += (g.edge == 0 && g.end == 0); }
   CUDA_TRY(h, cudaMalloc(&A.d_segs, A.segs.size() * sizeof(adi::Seg)));
   H2D_SYNC(h, A.d_segs, A.segs.data(), A.segs.size() * sizeof(adi::Seg));
   return ADI_OK;
@@ -629,9 +633,9 @@ struct TimeScope {
   }
 };
 
-template <int METHOD, int MODE, bool EDGE, bool HET, bool FULL = false>
+template <int METHOD, int MODE, bool EDGE, bool HET, bool FULL = false, bool NOEND = false>
 int launch_e(adi_ctx* h, const adi::Axis& A, adi::KParams p, int seg0, int nseg) {
-  auto kern = adi::adi_line_kernel<METHOD, adi::TM, adi::NW, MODE, EDGE, HET, FULL>;
+  auto kern = adi::adi_line_kernel<METHOD, adi::TM, adi::NW, MODE, EDGE, HET, FULL, NOEND>;
   const size_t smem = adi::line_smem_bytes<METHOD, adi::TM, adi::NW, EDGE, HET>();
   static bool attr = false;
   if (!attr) {
@@ -641,6 +645,8 @@ int launch_e(adi_ctx* h, const adi::Axis& A, adi::KParams p, int seg0, int nseg)
   if (nseg <= 0) return ADI_OK;
   const int nl = std::max(A.l1 - (A.l0 & ~3), 0);
   p.segs = A.d_segs + seg0;
+  p.seg0 = seg0;
+  p.nseg_all = (int)A.segs.size();
   dim3 grid((nl + adi::NW - 1) / adi::NW, (unsigned)nseg, h->batch);
   kern<<<grid, 32 * adi::NW, smem, h->stream>>>(p);
   CUDA_TRY(h, cudaGetLastError());
@@ -649,23 +655,29 @@ int launch_e(adi_ctx* h, const adi::Axis& A, adi::KParams p, int seg0, int nseg)
 }
 
 // interior segments first (lean kernel), then the segments with line ends
-template <int METHOD, int MODE, bool HET = false>
+#ifndef ADI_SPLIT_END
+#define ADI_SPLIT_END 1
+#endif
+template <int METHOD, int MODE, bool HET = false, bool FULL = false>
 int launch_t(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
   if (A.l1 <= A.l0) return ADI_OK;
   const int nseg = (int)A.segs.size();
-  int rc = launch_e<METHOD, MODE, false, HET>(h, A, p, 0, A.nint);
+  int rc;
+  if (ADI_SPLIT_END) {
+    // interior segments without the line-end code, then the lean line-end segments
+    rc = launch_e<METHOD, MODE, false, HET, FULL, true>(h, A, p, 0, A.nmid);
+    if (!rc) rc = launch_e<METHOD, MODE, false, HET, FULL, false>(h, A, p, A.nmid, A.nint - A.nmid);
+  } else {
+    rc = launch_e<METHOD, MODE, false, HET, FULL, false>(h, A, p, 0, A.nint);
+  }
   if (rc) return rc;
-  return launch_e<METHOD, MODE, true, HET>(h, A, p, A.nint, nseg - A.nint);
+  return launch_e<METHOD, MODE, true, HET, FULL, false>(h, A, p, A.nint, nseg - A.nint);
 }
 
 // the full-matrix CFD variant (NEXT row f4)
 template <int MODE>
 int launch_full(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
-  if (A.l1 <= A.l0) return ADI_OK;
-  const int nseg = (int)A.segs.size();
-  int rc = launch_e<adi::M_CFD, MODE, false, false, true>(h, A, p, 0, A.nint);
-  if (rc) return rc;
-  return launch_e<adi::M_CFD, MODE, true, false, true>(h, A, p, A.nint, nseg - A.nint);
+  return launch_t<adi::M_CFD, MODE, false, true>(h, A, p);
 }
 
 // heterogeneous-media kernels (fixed K sweeps: the stopping rule is not combined with media)
