@@ -476,17 +476,21 @@ __device__ __forceinline__ double shup(double v, int d) { return __shfl_up_sync(
 __device__ __forceinline__ double shdn(double v, int d) { return __shfl_down_sync(0xffffffffu, v, d); }
 
 // prev chunk's a[M-2], a[M-1]; next chunk's a[0], a[1] (0 outside the warp's segment)
-template <int M>
+// ZEND = false (interior-only tiles): the values beyond the segment ends stay whatever the
+// shuffle returns; like zeros they are truncation the halo absorbs (bounded)
+template <int M, bool ZEND = true>
 __device__ __forceinline__ void warp_edges(int lane, const double (&a)[M], double& pm2, double& pm1,
                                            double& np1, double& np2) {
   pm2 = shup(a[M - 2], 1);
   pm1 = shup(a[M - 1], 1);
   np1 = shdn(a[0], 1);
   np2 = shdn(a[1], 1);
-  pm2 = lane == 0 ? 0.0 : pm2;
-  pm1 = lane == 0 ? 0.0 : pm1;
-  np1 = lane == 31 ? 0.0 : np1;
-  np2 = lane == 31 ? 0.0 : np2;
+  if (ZEND) {
+    pm2 = lane == 0 ? 0.0 : pm2;
+    pm1 = lane == 0 ? 0.0 : pm1;
+    np1 = lane == 31 ? 0.0 : np1;
+    np2 = lane == 31 ? 0.0 : np2;
+  }
 }
 
 // Heterogeneous media (NEXT row f3; Alg. 3/4 "K.*( )", "R.*( )"):
@@ -602,7 +606,7 @@ constexpr int NSUB = ADI_NSUB;
 // previous chunk's last and the next chunk's first position (the operand
 // neighbours of the next op).  st: statics of this warp's chunks [5][32].
 // ===========================================================================
-template <int M, bool UOP, bool EDGE, bool NOB = false>
+template <int M, bool UOP, bool EDGE, bool NOB = false, bool ZEND = true>
 __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int lane,
                                           const double* st, const double* etab, const double (&o)[M],
                                           const double* __restrict__ B, double (&out)[M],
@@ -680,14 +684,19 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
   // ---------------- exchange (shuffles) ----------------
   double ylm1 = shup(yl_e, 1), ylm2 = shup(yl_e, 2), ylp1 = shdn(yl_e, 1);
   double wsp1 = shdn(ws, 1), wsp2 = shdn(ws, 2), wem1 = shup(we, 1);
-  ylm1 = lane == 0 ? 0.0 : ylm1;
-  ylm2 = lane <= 1 ? 0.0 : ylm2;
-  wem1 = lane == 0 ? 0.0 : wem1;
-  ylp1 = lane == 31 ? 0.0 : ylp1;
-  wsp1 = lane == 31 ? 0.0 : wsp1;
-  wsp2 = lane >= 30 ? 0.0 : wsp2;
+  if (ZEND) {
+    ylm1 = lane == 0 ? 0.0 : ylm1;
+    ylm2 = lane <= 1 ? 0.0 : ylm2;
+    wem1 = lane == 0 ? 0.0 : wem1;
+    ylp1 = lane == 31 ? 0.0 : ylp1;
+    wsp1 = lane == 31 ? 0.0 : wsp1;
+    wsp2 = lane >= 30 ? 0.0 : wsp2;
+  }
   double Fm1, Fme, Ksp1, Jsp1, Ksp2, Kem1, Jem1;
-  if (!EDGE) {
+  if (!EDGE && !ZEND) {
+    // interior-only tile: constant statics everywhere (the segment ends are halo)
+    Fm1 = Fme = c_cF; Ksp1 = Ksp2 = c_cKs; Jsp1 = c_cJs; Kem1 = c_cKe; Jem1 = c_cJe;
+  } else if (!EDGE) {
     // interior tile: every chunk of the segment has the interior statics; the
     // segment ends carry nothing (truncated SPIKE)
     Fm1 = lane >= 1 ? c_cF : 0.0; Fme = c_cF;
@@ -1101,13 +1110,13 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     const double VLp = lane > 0 ? lX[(lane - 1) * PADM + M - 1] : 0.0;
     const double VFn = lane < 31 ? lX[(lane + 1) * PADM] : 0.0;
     __syncwarp();
-    warp_edges<M>(lane, x, d0, xm1, xp1, d1);
-    warp_edges<M>(lane, u, d0, um1, up1, d1);
+    warp_edges<M, !NOEND>(lane, x, d0, xm1, xp1, d1);
+    warp_edges<M, !NOEND>(lane, u, d0, um1, up1, d1);
     if (MODE == KM_PROLOGUE) {
       // at most two 32-point arrays live: U stays in the S tile, W is re-read from
       // the X tile, W* is staged for output before the u-op
       double e1, e2;
-      cfd_apply<M, false, EDGE, HET>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, 0.0, 0.0, e1, e2);
+      cfd_apply<M, false, EDGE, HET, !NOEND>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, 0.0, 0.0, e1, e2);
       if constexpr (HET) het_apply<M, METHOD, false, EDGE>(c, Cm, Vm, x, 0, n);
       add_source_global(Sm);   // S = U + dt/2 F
       double wv[M];
@@ -1121,7 +1130,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
           V2[i] = make_double2(x[2 * i], x[2 * i + 1]);
         }
       }
-      cfd_apply<M, UOPK, EDGE, HET>(c, P, lane, FULL ? stXs : stU, etab, wv, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
+      cfd_apply<M, UOPK, EDGE, HET, !NOEND>(c, P, lane, FULL ? stXs : stU, etab, wv, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
       if constexpr (HET) het_apply<M, METHOD, true, EDGE>(c, Cm, Sm, u, 1, uhi);
     } else {
       double uo[TEST ? M : 1], xo[TEST ? M : 1];
@@ -1133,12 +1142,12 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
           }
         }
         if constexpr (HET) {
-          cfd_apply<M, true, EDGE, true>(c, P, lane, stU, etab, x, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, um1, up1);
+          cfd_apply<M, true, EDGE, true, !NOEND>(c, P, lane, stU, etab, x, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, um1, up1);
           het_apply<M, METHOD, true, EDGE>(c, Cm, Sm, u, 1, uhi);
           um1 = fma(kP, um1, SLp);
           up1 = fma(kN, up1, SFn);
         } else {
-          cfd_apply<M, UOPK, EDGE>(c, P, lane, FULL ? stXs : stU, etab, x, Sm, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
+          cfd_apply<M, UOPK, EDGE, false, !NOEND>(c, P, lane, FULL ? stXs : stU, etab, x, Sm, u, P.cu, xm1, xp1, SFn, SLp, um1, up1);
         }
         if (k + 1 == KK) {
           // park u_K in the (now dead) S tile: u is then dead across every x-op,
@@ -1148,12 +1157,12 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
           for (int i = 0; i < M / 2; ++i) S2[i] = make_double2(u[2 * i], u[2 * i + 1]);
         }
         if constexpr (HET) {
-          cfd_apply<M, false, EDGE, true>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, 0.0, 0.0, xm1, xp1);
+          cfd_apply<M, false, EDGE, true, !NOEND>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, 0.0, 0.0, xm1, xp1);
           het_apply<M, METHOD, false, EDGE>(c, Cm, Vm, x, 0, n);
           xm1 = fma(rP, xm1, VLp);
           xp1 = fma(rN, xp1, VFn);
         } else {
-          cfd_apply<M, false, EDGE>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, VFn, VLp, xm1, xp1);
+          cfd_apply<M, false, EDGE, false, !NOEND>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, VFn, VLp, xm1, xp1);
         }
         if constexpr (TEST) {
           if (k + 1 == KK) norm_add(u, uo, x, xo);
@@ -1181,21 +1190,21 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
 #pragma unroll
           for (int i = 0; i < M; ++i) { u[i] = Sm[i]; Vm[i] = x[i]; }   // operand Gu, base Gw
           __syncwarp();
-          warp_edges<M>(lane, u, d0, um1, up1, d1);
-          cfd_apply<M, false, EDGE>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, 0.0, 0.0, e1, e2);
+          warp_edges<M, !NOEND>(lane, u, d0, um1, up1, d1);
+          cfd_apply<M, false, EDGE, false, !NOEND>(c, P, lane, stXs, etab, u, Vm, x, P.cx, um1, up1, 0.0, 0.0, e1, e2);
 #pragma unroll
           for (int i = 0; i < M; ++i) { u[i] = Vm[i]; Vm[i] = x[i]; }   // operand Gw; Vm = W*
           __syncwarp();
-          warp_edges<M>(lane, u, d0, xm1, xp1, d1);
+          warp_edges<M, !NOEND>(lane, u, d0, xm1, xp1, d1);
           add_source_global(Sm);   // S = Gu + dt/2 F
-          cfd_apply<M, false, EDGE>(c, P, lane, stXs, etab, u, Sm, x, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
+          cfd_apply<M, false, EDGE, false, !NOEND>(c, P, lane, stXs, etab, u, Sm, x, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
 #pragma unroll
           for (int i = 0; i < M; ++i) { u[i] = x[i]; x[i] = Vm[i]; }    // u = S1, x = W*
         }
       } else if (MODE == KM_SWEEP) {
         double e1, e2;
         add_source_global(Sm);   // S = u_K + dt/2 F
-        cfd_apply<M, UOPK, EDGE, HET>(c, P, lane, FULL ? stXs : stU, etab, x, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
+        cfd_apply<M, UOPK, EDGE, HET, !NOEND>(c, P, lane, FULL ? stXs : stU, etab, x, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
         if constexpr (HET) het_apply<M, METHOD, true, EDGE>(c, Cm, Sm, u, 1, uhi);
 #pragma unroll
         for (int i = 0; i < M; ++i) x[i] = fma(2.0, x[i], -Vm[i]);
@@ -1219,14 +1228,14 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
           for (int i = 0; i < M; ++i) u[i] = 0.0;
           MfdSplit<M>::u_inner(opd, u, cA, cB);
         }
-        warp_edges<M>(lane, opd, xm2, xm1, xp1, xp2);
+        warp_edges<M, !NOEND>(lane, opd, xm2, xm1, xp1, xp2);
         if (c.interior) MfdSplit<M>::u_edges(opd, u, cA, cB, xm2, xm1, xp1);
         else Mfd<M>::template uop<false, true>(c, opd, B, u, au, xm2, xm1, xp1);
         if (!EDGE && c.me) mfd_end_u<M, true>(c, opd, B, u, au);
         het_apply<M, METHOD, true, EDGE>(c, Cm, B, u, 1, uhi);
       } else {
         if (c.interior) { MfdSplit<M>::bases(B, u); MfdSplit<M>::u_inner(opd, u, cA, cB); }
-        warp_edges<M>(lane, opd, xm2, xm1, xp1, xp2);
+        warp_edges<M, !NOEND>(lane, opd, xm2, xm1, xp1, xp2);
         if (c.interior) MfdSplit<M>::u_edges(opd, u, cA, cB, xm2, xm1, xp1);
         else Mfd<M>::template uop<false>(c, opd, B, u, au, xm2, xm1, xp1);
         if (!EDGE && c.me) mfd_end_u<M>(c, opd, B, u, au);
@@ -1239,14 +1248,14 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
           for (int i = 0; i < M; ++i) x[i] = 0.0;
           MfdSplit<M>::x_inner(u, x, cC, cD);
         }
-        warp_edges<M>(lane, u, um2, um1, up1, up2);
+        warp_edges<M, !NOEND>(lane, u, um2, um1, up1, up2);
         if (c.interior) MfdSplit<M>::x_edges(u, x, cC, cD, um1, up1, up2);
         else Mfd<M>::template xop<false, true>(c, u, B, x, bx, um1, up1, up2);
         if (!EDGE && c.me) mfd_end_x<M, true>(c, u, B, x, bx);
         het_apply<M, METHOD, false, EDGE>(c, Cm, B, x, 0, n);
       } else {
         if (c.interior) { MfdSplit<M>::bases(B, x); MfdSplit<M>::x_inner(u, x, cC, cD); }
-        warp_edges<M>(lane, u, um2, um1, up1, up2);
+        warp_edges<M, !NOEND>(lane, u, um2, um1, up1, up2);
         if (c.interior) MfdSplit<M>::x_edges(u, x, cC, cD, um1, up1, up2);
         else Mfd<M>::template xop<false>(c, u, B, x, bx, um1, up1, up2);
         if (!EDGE && c.me) mfd_end_x<M>(c, u, B, x, bx);
