@@ -53,6 +53,10 @@ def parse():
                     help="NEXT row f4: the full-matrix CFD variant with a Cerjan layer (ADI_CFD_FULL)")
     ap.add_argument("--media", action="store_true",
                     help="NEXT row f3: the same workload in a smooth heterogeneous medium (adi_set_media)")
+    ap.add_argument("--shots", action="store_true",
+                    help="config 5: Ricker point-source shots, MFD, a batch of --shots-per-gpu "
+                         "4096^2 grids per rank (weak scaling, no collective)")
+    ap.add_argument("--shots-per-gpu", type=int, default=8)
     return ap.parse_args()
 
 
@@ -439,6 +443,117 @@ def run_ours(a, ws, rank, local):
 
 
 # ---------------------------------------------------------------------------
+SHOT_N = 4096   # config 5: nx = ny = 4096 nodes
+
+
+def shot_problems(rank, nper, steps, K):
+    """Config 5: the shots of rank r are [r nper, (r+1) nper) of a survey of
+    nper x world shots; each is adi_inputs.ricker_problem (zero initial fields, free
+    surface, F = r(t)/h^2 at its own cell, f0 = 100, t0 = 0.015, cfl 0.81)."""
+    from adi_inputs import ricker_problem
+    return [ricker_problem(SHOT_N, shot=rank * nper + j, nshots=64, steps=steps, K=K)
+            for j in range(nper)]
+
+
+def run_shots(a, ws, rank, local):
+    """Config 5 (replicas only): each rank advances its own batch of
+    shots in one batched handle (grid dimension z = shot); no data-path collective."""
+    import torch
+    import paper_2006_07583_b200 as adi
+    from adi_inputs import MFD, shapes
+
+    torch.cuda.set_device(local)
+    stream = torch.cuda.current_stream()
+    B, n = a.shots_per_gpu, SHOT_N
+    total = a.warmup + 2 * a.steps + 4
+    probs = shot_problems(rank, B, total, a.K)
+    p0 = probs[0]
+    s = adi.AdiSolver(n, n, p0.h, p0.dt, 1.0, MFD, batch=B, K=a.K, stream=stream.cuda_stream)
+    s.set_point_sources([p.src[0] for p in probs], [p.src[1] for p in probs], p0.gf)
+    su, sv, sw = shapes(MFD, n, n)
+    # zero initial fields (adi_create's state; set explicitly as a user would)
+    z = [torch.zeros((B,) + sh, dtype=torch.float64, device="cuda") for sh in (su, sv, sw)]
+    s.set_fields(*z)
+    del z
+    s.step(a.warmup)
+    torch.cuda.synchronize()
+    s.set_param(adi.ADI_TIMING, 1)
+    s.kernel_times()
+    l0 = s.stats()["kernel_launches"]
+    with Clocks(local) as clk:
+        barrier(ws)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        s.step(a.steps)
+        e1.record(stream)
+        e1.synchronize()
+        barrier(ws)
+        ms = allmax(ws, e0.elapsed_time(e1))
+    launches = s.stats()["kernel_launches"] - l0
+    kt = {k: v for k, v in s.kernel_times().items() if v[1] > 0}
+    s.set_param(adi.ADI_TIMING, 0)
+    pts = n * n * B * ws
+    value = pts * a.steps / (ms * 1e-3)
+    peak, peak_src = measured_peaks()
+    kind, (kms, kcnt) = max(kt.items(), key=lambda kv: kv[1][0])
+    byt = B * kernel_bytes(MFD, n, kind, has_phi=False)
+    avg = kms / kcnt
+    tot = sum(v[0] for v in kt.values())
+    roof = {"bound": "hbm", "achieved": round(byt / (avg * 1e-3) / 1e9, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(byt / (avg * 1e-3) / 1e9 / peak, 4),
+            "traffic": ncu_traffic().get(f"mfd_{kind}_{n}_b{B}", {}).get("dram_bytes_per_launch"),
+            "kernel": f"adi_line_kernel[mfd,{kind}]", "algorithmic_bytes_per_launch": byt,
+            "peak_source": peak_src, "avg_launch_ms": round(avg, 4)}
+    fl = B * kernel_flops(MFD, n, kind, a.K) / (avg * 1e-3) / 1e12
+    roof_fp64 = {"bound": "fp64", "achieved": round(fl, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                 "frac": round(fl / FP64_PEAK_TFLOPS, 4), "kernel": roof["kernel"],
+                 "algorithmic_flops_per_launch": B * kernel_flops(MFD, n, kind, a.K),
+                 "peak_source": "measured (profiles/r01/fp64_probe.txt, independent DFMA streams)"}
+    e2e = None
+    if not a.no_e2e:
+        # the call a user makes per survey batch: zero initial fields up from pinned host,
+        # adi_step(K steps), the wavefields back to pinned host
+        host = [torch.zeros((B,) + sh, dtype=torch.float64).pin_memory() for sh in (su, sv, sw)]
+        outs = [torch.empty_like(x).pin_memory() for x in host]
+        nb = sum(x.numel() for x in host) * 8
+        barrier(ws)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        adi.adi_set_fields_async(s.handle, *[x.numpy() for x in host])
+        s.step(a.steps)
+        adi.adi_get_fields_async(s.handle, *[x.numpy() for x in outs])
+        stream.synchronize()
+        t1 = time.perf_counter()
+        barrier(ws)
+        e2e_ms = allmax(ws, (t1 - t0) * 1e3)
+        e2e = {"value": pts * a.steps / (e2e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(nb / a.steps), "d2h_bytes_per_step": int(nb / a.steps),
+               "note": "per rank: adi_set_fields_async(pinned zeros) + adi_step(K) + adi_get_fields_async"
+                       "(pinned); host wall clock, max over ranks; bytes per step of one rank"}
+        del host, outs
+    s.close()
+    return {"value": value, "ms_per_step": ms / a.steps, "roofline": roof, "roofline_fp64": roof_fp64,
+            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches,
+            "per_method": {"mfd": {"value": value / ws, "ms_per_step": ms / a.steps,
+                                   "kernel_ms_share": {k: round(v[0] / tot, 4) for k, v in kt.items()},
+                                   "kernel_avg_ms": {k: v[0] / v[1] for k, v in kt.items()},
+                                   "dominant": kind}}}
+
+
+def oracle_rate_shots(nshots, steps, K, threads):
+    """Oracle pt-updates/s on ``nshots`` config-5 shots (bounded CPU work)."""
+    import oracle
+    tot = 0.0
+    for p in shot_problems(0, nshots, steps + 1, K):
+        t0 = time.perf_counter()
+        oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, p.U, p.V, p.W, nsteps=steps,
+                   nthreads=threads, **p.oracle_kwargs())
+        tot += time.perf_counter() - t0
+    return nshots * SHOT_N * SHOT_N * steps / tot, tot
+
+
 def oracle_rate(methods, n, steps, K, threads=0, media=False):
     """Oracle pt-updates/s on an n x n sample (bounded CPU work)."""
     import oracle
@@ -465,6 +580,48 @@ def cpu_cores():
         return os.cpu_count()
 
 
+def main_shots(a, ws, rank, local):
+    """bench.py --shots: config 5, weak scaling over ranks."""
+    B = a.shots_per_gpu
+    cfg = {"workload": f"config5: Ricker point-source shots (f0=100, t0=0.015), MFD, {SHOT_N}x{SHOT_N} "
+                       f"nodes, zero IC, free surface; {B} shots per GPU in one batched handle",
+           "grid_nodes": SHOT_N, "shots_per_gpu": B, "shots_total": B * ws, "methods": ["mfd"],
+           "K_sweeps": a.K, "cfl": {"mfd": 0.81},
+           "l2": f"inputs larger than L2 ({B} x 134 MB per field); no flush",
+           "parallelism": "1 GPU" if ws == 1 else f"{ws} GPUs: independent shots per rank (replicas, no collective)"}
+    common = {"metric": METRIC, "unit": UNIT, "n_gpus": ws, "steps": a.steps, "warmup": a.warmup,
+              "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+              "data": "synthetic", "config": cfg}
+    if a.impl == "reference":
+        if rank != 0:
+            return
+        import oracle
+        oracle.build()
+        nthr = cpu_cores()
+        oracle_rate_shots(1, 1, a.K, nthr)
+        rate, secs = oracle_rate_shots(1, a.steps, a.K, nthr)
+        print(json.dumps({"impl": "reference", **common, "value": rate, "ms_per_step": secs * 1e3 / a.steps,
+                          "cpu_baseline": {"value": rate, "unit": UNIT, "cores": nthr, "kind": "oracle",
+                                           "sample": f"shot 0 only, {a.steps} steps (oracle C, OpenMP over lines)"},
+                          "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+    r = run_shots(a, ws, rank, local)
+    if rank != 0:
+        return
+    cpu = None
+    if not a.no_cpu and ws == 1:
+        import oracle
+        oracle.build()
+        nthr = cpu_cores()
+        rate, secs = oracle_rate_shots(1, 12, a.K, nthr)
+        cpu = {"value": rate, "unit": UNIT, "cores": nthr, "kind": "oracle",
+               "sample": f"shot 0, 12 steps ({secs:.1f} s of CPU time)"}
+    print(json.dumps({**common, "value": r["value"], "ms_per_step": r["ms_per_step"],
+                      "roofline": r["roofline"], "roofline_fp64": r["roofline_fp64"], "cpu_baseline": cpu,
+                      "clocks": r["clocks"], "e2e": r["e2e"], "gpu_launches": r["gpu_launches"],
+                      "per_method": r["per_method"]}))
+
+
 def main():
     a = parse()
     ws, rank, local = dist_setup()
@@ -483,6 +640,8 @@ def main():
     if a.media:
         cfg["workload"] += " + heterogeneous medium (NEXT row f3: fp32 kappa, rho^-1 grids, adi_set_media)"
         cfg["media"] = "smooth: kappa = 0.8 (1 + 0.25 sin(2 pi x + 0.3) cos(2 pi y)), rho^-1 analogous"
+    if a.shots:
+        return main_shots(a, ws, rank, local)
     if a.impl == "reference":
         # Reference arm = the CPU oracle as it stands, bounded sample per step.
         if rank != 0:

@@ -117,6 +117,9 @@ struct KParams {
   unsigned long long* trace;
   long long trace_cap;
   int seg0, nseg_all;   // this launch's first segment, all segments of the axis (trace index)
+  // ADI_PREFETCH: the tile this many CTAs later in launch order (about one resident wave
+  // per unit) has its staging tiles prefetched into L2 at this tile's start; 0 = off
+  int pf_ahead;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -839,6 +842,14 @@ __device__ __forceinline__ void tma_load_seg(double* dst, const CUtensorMap* tm,
       : "memory");
 }
 
+// L2 prefetch of the same box (no shared-memory destination, no completion)
+__device__ __forceinline__ void tma_prefetch_seg(const CUtensorMap* tm, int c1, int c2, int line, int b) {
+  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+                   (unsigned long long)tm),
+               "r"(0), "r"(c1), "r"(c2), "r"(line), "r"(b)
+               : "memory");
+}
+
 // ===========================================================================
 // One tile = NW lines x one segment.  EDGE = false: all 32 chunks of every line
 // are interior and live (the lean path, no generic closures, no per-chunk
@@ -917,6 +928,27 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     tma_load_seg(lX, &P.tmX, c1, c2, line, b, wbar);
     if (HET) tma_load_seg(lC, &P.tmC, c1, c2, line, 0, wbar);   // one medium for the batch
     if (MODE != KM_PROLOGUE) tma_load_seg(lS, &P.tmS, c1, c2, line, b, wbar);
+  }
+  if (!EDGE && P.pf_ahead > 0 && lane == 0) {
+    // L2 prefetch of the staging tiles of the tile pf_ahead CTAs later in launch order:
+    // CTAs are dispatched in linear block order, so that tile starts about one resident
+    // wave later and its TMA loads then hit L2 -- the HBM reads of the next wave overlap
+    // this wave's sweeps (same tensor maps and coordinates as the loads above)
+    const long long gx = gridDim.x, gy = gridDim.y;
+    const long long lin = blockIdx.x + gx * (blockIdx.y + gy * (long long)blockIdx.z) + P.pf_ahead;
+    if (lin < gx * gy * (long long)gridDim.z) {
+      const int tx = (int)(lin % gx);
+      const long long r = lin / gx;
+      const int ty = (int)(r % gy), tz = (int)(r / gy);
+      const int tline = P.line0 + tx * NW + w;
+      if (tline >= P.line_lo && tline < P.nlines) {
+        const int tsh = P.segs[ty].start + TMA_P0;
+        const int tc1 = (tsh & 31) >> 1, tc2 = tsh >> 5;
+        tma_prefetch_seg(&P.tmX, tc1, tc2, tline, tz);
+        if (HET) tma_prefetch_seg(&P.tmC, tc1, tc2, tline, 0);
+        if (MODE != KM_PROLOGUE) tma_prefetch_seg(&P.tmS, tc1, tc2, tline, tz);
+      }
+    }
   }
   __syncwarp();  // the barrier is initialised before any lane waits on it
   if (MODE == KM_PROLOGUE) {

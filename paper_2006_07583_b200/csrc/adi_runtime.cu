@@ -59,6 +59,7 @@ struct adi_ctx {
   int K = 8;
   int check_finite = 0;
   int tile_chunks = 0;  // 0 = auto
+  int prefetch = 0;     // ADI_PREFETCH: L2 prefetch distance in resident waves (0 = off)
   int timing = 0;
   double eps = 0.0;      // ADI_EPS: inner stopping rule off (fixed K sweeps) when 0
   int kmin = 6;          // ADI_K_MIN
@@ -638,11 +639,18 @@ int launch_e(adi_ctx* h, const adi::Axis& A, adi::KParams p, int seg0, int nseg)
   auto kern = adi::adi_line_kernel<METHOD, adi::TM, adi::NW, MODE, EDGE, HET, FULL, NOEND>;
   const size_t smem = adi::line_smem_bytes<METHOD, adi::TM, adi::NW, EDGE, HET>();
   static bool attr = false;
+  static int wave = 0;   // resident CTAs of this instantiation on the device
   if (!attr) {
     CUDA_TRY(h, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, nsm = 0, occ = 0;
+    CUDA_TRY(h, cudaGetDevice(&dev));
+    CUDA_TRY(h, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CUDA_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * adi::NW, smem));
+    wave = nsm * occ;
     attr = true;
   }
   if (nseg <= 0) return ADI_OK;
+  p.pf_ahead = EDGE ? 0 : h->prefetch * wave;
   const int nl = std::max(A.l1 - (A.l0 & ~3), 0);
   p.segs = A.d_segs + seg0;
   p.seg0 = seg0;
@@ -1022,6 +1030,9 @@ int adi_set_param(adi_handle h, int key, double v) {
     H2D_SYNC(h, h->d_taper, g.data(), g.size() * sizeof(double));
     h->absorb_nb = nb;
     h->absorb_a = a;
+  } else if (key == ADI_PREFETCH) {
+    if (!(v >= 0) || v != std::floor(v) || v > 8) return fail(h, ADI_EINVAL, "prefetch must be an integer in [0, 8]");
+    h->prefetch = (int)v;
   } else if (key == ADI_TILE_CHUNKS) {
     if (!(v >= 0) || v != std::floor(v)) return fail(h, ADI_EINVAL, "tile chunks must be >= 0");
     h->tile_chunks = (int)v;

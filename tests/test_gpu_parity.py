@@ -322,3 +322,25 @@ def test_segment_halo_is_exact(adi, method, n, chunks, steps):
     for name, x, y in zip("UVW", a, b):
         d = np.abs(x - y).max() / np.abs(x).max()
         assert d <= 1e-14, (name, d)
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+def test_prefetch_knob_does_not_change_results(adi, method):
+    """ADI_PREFETCH (an L2 prefetch distance, include/adi.h) is a performance knob:
+    results are bitwise identical for every value; out-of-range values are refused."""
+    p = random_problem(method, 2101, seed=4, steps=2)
+    outs = []
+    for v in (0, 1, 3):
+        s = adi.AdiSolver.from_problem(p)
+        s.set_param(adi.ADI_PREFETCH, v)
+        s.step(2)
+        outs.append(s.get_fields())
+        s.close()
+    for o in outs[1:]:
+        for a, b in zip(o, outs[0]):
+            assert np.array_equal(a, b)
+    s = adi.AdiSolver.from_problem(p)
+    for bad in (-1, 9, 1.5):
+        with pytest.raises(adi.AdiError):
+            s.set_param(adi.ADI_PREFETCH, bad)
+    s.close()
