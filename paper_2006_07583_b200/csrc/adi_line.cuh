@@ -745,13 +745,15 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
         else wb_g<C0 + 2>(zz, g0, g1, g2);
       }
     }
-    const double ci = coef * iv;
+    // the signs ride on the per-chunk scalars (exact), so each constant is a plain
+    // constant-bank operand of its DFMA instead of a register loaded by LDC
+    const double ci = -coef * iv;
 #pragma unroll
     for (int j = 0; j < NSUB; ++j) {
-      const double cy = coef * ycT[j], cz = coef * zcT[j];
+      const double cy = -coef * ycT[j], cz = -coef * zcT[j];
 #pragma unroll
       for (int i = 0; i < L; ++i)
-        out[j * L + i] = fma(-c_sJ[i], cz, fma(-c_sK[i], cy, fma(-ci, out[j * L + i], NOB ? 0.0 : B[j * L + i])));
+        out[j * L + i] = fma(c_sJ[i], cz, fma(c_sK[i], cy, fma(ci, out[j * L + i], NOB ? 0.0 : B[j * L + i])));
     }
     if (!EDGE && c.me) {
       if (c.endc == 0) wb_apply<C0, true, M>(out, coef, g0, g1, g2);
@@ -849,6 +851,12 @@ __device__ __forceinline__ void tma_prefetch_seg(const CUtensorMap* tm, int c1, 
                "r"(0), "r"(c1), "r"(c2), "r"(line), "r"(b)
                : "memory");
 }
+
+// unroll factor of the output store loops (several shared loads in flight per lane)
+#ifndef ADI_STORE_UNROLL
+#define ADI_STORE_UNROLL 4
+#endif
+constexpr int STORE_UNROLL = ADI_STORE_UNROLL;
 
 // ===========================================================================
 // One tile = NW lines x one segment.  EDGE = false: all 32 chunks of every line
@@ -1357,6 +1365,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   if (lineok) {
     const int xlo = max(sg.out_lo, 0), xhi = min(sg.out_hi, n + 1);
     double* Xo = P.X_out + (long long)b * P.x_batch + (long long)line * P.x_line;
+#pragma unroll STORE_UNROLL
     for (int p = (xlo & ~1) + 2 * lane; p < xhi; p += 64) {
       const int q = p - sg.start;
       const double2 v = *reinterpret_cast<const double2*>(lX + (q >> 5) * PADM + (q & 31));
@@ -1379,6 +1388,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     else { plo_ = max(sg.out_lo, ulo); phi_ = min(sg.out_hi, uhi + 1); }
     const double* r0 = stS + (2 * pr) * LSTR;
     const double* r1 = r0 + LSTR;
+#pragma unroll STORE_UNROLL
     for (int pos = 16 * w + (lane & 15); pos < 32 * M; pos += 16 * NW) {
       const int p = sg.start + pos;
       if (p < plo_ || p >= phi_) continue;

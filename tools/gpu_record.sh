@@ -10,6 +10,8 @@ timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
 cat $O/bench.json; tail -2 $O/bench.err
 timeout 900 python bench.py --impl reference > $O/bench_ref.json 2> $O/bench_ref.err; echo "ref rc=$?"
 cat $O/bench_ref.json
+timeout 900 python bench.py --shots --steps 1000 --warmup 10 > $O/bench_shots.json 2> $O/bench_shots.err; echo "shots rc=$?"
+cat $O/bench_shots.json
 timeout 600 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > $O/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $O/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > $O/ncu_list.log 2>&1; echo "ncu list rc=$?"
