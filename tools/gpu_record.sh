@@ -19,6 +19,9 @@ for m in mfd cfd; do
   timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv \
     -k regex:adi_line_kernel --log-file $O/dram_$m.csv python tools/prof_one.py $m 16384 2 > $O/ncu_dram_$m.log 2>&1; echo "dram $m rc=$?"
 done
+timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv \
+    -k regex:adi_line_kernel --log-file $O/dram_shots.csv python tools/prof_one.py shots 4096 2 > $O/ncu_dram_shots.log 2>&1; echo "dram shots rc=$?"
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"; tail -3 $O/smoke.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:adi_line_kernel -s 2 -c 1 \
     -o $O/full_cfd_row python tools/prof_one.py cfd 16384 2 > $O/ncu_full.log 2>&1; echo "ncu full rc=$?"
 ncu -i $O/full_cfd_row.ncu-rep --page raw --csv > $O/full_cfd_row_raw.csv 2>/dev/null
