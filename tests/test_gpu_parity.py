@@ -324,12 +324,13 @@ def test_segment_halo_is_exact(adi, method, n, chunks, steps):
         assert d <= 1e-14, (name, d)
 
 
+@pytest.mark.parametrize("media", [False, True])
 @pytest.mark.parametrize("method", [CFD, MFD])
-def test_prefetch_knob_does_not_change_results(adi, method):
+def test_prefetch_knob_does_not_change_results(adi, method, media):
     """ADI_PREFETCH (an L2 prefetch distance, include/adi.h) is a performance knob:
     results are bitwise identical for every value; out-of-range values are refused."""
-    p = random_problem(method, 2101, seed=4, steps=2)
     outs = []
+    p = random_problem(method, 2101, seed=4, steps=2, media=media)
     for v in (0, 1, 3):
         s = adi.AdiSolver.from_problem(p)
         s.set_param(adi.ADI_PREFETCH, v)
@@ -344,3 +345,23 @@ def test_prefetch_knob_does_not_change_results(adi, method):
         with pytest.raises(adi.AdiError):
             s.set_param(adi.ADI_PREFETCH, bad)
     s.close()
+
+
+def test_prefetch_knob_batch(adi):
+    """ADI_PREFETCH with a batch (the prefetch target's grid z = batch index)."""
+    n, B = 1601, 3
+    probs = [random_problem(MFD, n, seed=30 + b, steps=2) for b in range(B)]
+    p0 = probs[0]
+    outs = []
+    for v in (0, 2):
+        s = adi.AdiSolver(n, n, p0.h, p0.dt, p0.c, MFD, batch=B)
+        s.set_fields(np.stack([p.U for p in probs]), np.stack([p.V for p in probs]),
+                     np.stack([p.W for p in probs]))
+        s.set_source(p0.phi, None, p0.gf)
+        s.set_boundary(p0.edges, p0.gb)
+        s.set_param(adi.ADI_PREFETCH, v)
+        s.step(2)
+        outs.append(s.get_fields())
+        s.close()
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
