@@ -857,6 +857,12 @@ __device__ __forceinline__ void tma_prefetch_seg(const CUtensorMap* tm, int c1, 
 #define ADI_STORE_UNROLL 4
 #endif
 constexpr int STORE_UNROLL = ADI_STORE_UNROLL;
+// MFD interior tiles: the epilogue operator accumulates onto u_K in registers (1) or
+// reads a staged base u_K + dt/2 F (0)
+#ifndef ADI_MFD_EPI_REG
+#define ADI_MFD_EPI_REG 1
+#endif
+constexpr bool MFD_EPI_REG = ADI_MFD_EPI_REG;
 
 // ===========================================================================
 // One tile = NW lines x one segment.  EDGE = false: all 32 chunks of every line
@@ -1072,6 +1078,24 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       double f = want_phi ? dst[i] * P.gf : 0.0;
       if (i == ipt) f += ptf;
       dst[i] = fma(P.half_dt, f, src[i]);
+    }
+  };
+
+  // u = u + dt/2 F in registers, the source pattern staged in `ph` (the S tile)
+  auto add_source_reg = [&](const double* ph, double (&uu)[M]) {
+    int ipt = -1;
+    if (P.pt_line && line == P.pt_line[b]) ipt = P.pt_pos[b] - c.s;
+    const double ptf = P.pt_amp * P.gf;
+    if (want_phi) {
+      mbar_wait(wbar, wpar);
+      wpar ^= 1u;
+      __syncwarp();
+    }
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      double f = want_phi ? ph[i] * P.gf : 0.0;
+      if (i == ipt) f += ptf;
+      uu[i] = fma(P.half_dt, f, uu[i]);
     }
   };
 
@@ -1335,8 +1359,18 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
         }
       }
       if (MODE == KM_SWEEP) {
-        add_source(Sm, u);
-        u_op(x, Sm);
+        if constexpr (NOEND && !HET && MFD_EPI_REG) {
+          // interior tiles: the epilogue operator accumulates onto u_K in registers and
+          // the source comes last (S' = u_K - alpha D̄(x_K) + dt/2 F), so the TMA of the
+          // source pattern, issued after the last u-op, has two operators of slack
+          MfdSplit<M>::u_inner(x, u, cA, cB);
+          warp_edges<M, false>(lane, x, xm2, xm1, xp1, xp2);
+          MfdSplit<M>::u_edges(x, u, cA, cB, xm2, xm1, xp1);
+          add_source_reg(Sm, u);
+        } else {
+          add_source(Sm, u);
+          u_op(x, Sm);
+        }
 #pragma unroll
         for (int i = 0; i < M; ++i) x[i] = fma(2.0, x[i], -Vm[i]);
       }
