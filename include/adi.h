@@ -144,7 +144,10 @@ typedef struct adi_stats {
 /* Create a solver for one grid (batch = 1).  nx, ny >= 9 nodes (N >= 8);
  * h > 0 grid spacing, dt > 0, c > 0 wave speed; method ADI_CFD or ADI_MFD.
  * Returns ADI_WUNSTABLE (handle valid) when c*dt/h exceeds the K-sweep
- * iteration limit.  Fields start at zero, t0 = 0. */
+ * iteration limit.  Fields start at zero, t0 = 0.  The handle lives on the calling
+ * thread's current CUDA device; every later call on it runs on that device and
+ * restores the caller's current device (handles on several devices may coexist in
+ * one process; one host thread per handle at a time). */
 int adi_create(int nx, int ny, double h, double dt, double c, int method, adi_handle* out);
 
 /* As adi_create with `batch` independent grids ("shots") of the same shape

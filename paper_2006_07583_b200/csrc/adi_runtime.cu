@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -54,6 +55,7 @@ struct Axis {
 }  // namespace adi
 
 struct adi_ctx {
+  int dev = 0;          // the CUDA device the handle was created on (DevGuard)
   int method, nx, ny, batch;
   double h, dt, c, rho;
   int K = 8;
@@ -138,7 +140,26 @@ struct adi_ctx {
 namespace {
 
 const char* kVersion = "adi-b200 0.1 (sm_100a)";
-bool g_const_ready = false;
+// __constant__ memory and function attributes are per device: the tables are uploaded
+// once per device a handle is created on (one handle per device and host thread, but
+// handles on several devices in one process are allowed)
+constexpr int kMaxDev = 64;
+std::mutex g_const_mu;
+bool g_const_ready[kMaxDev] = {};
+
+// Every call on a handle runs on the handle's device and restores the caller's
+// current device afterwards.
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(const adi_ctx* h) {
+    int cur = 0;
+    if (h && cudaGetDevice(&cur) == cudaSuccess && cur != h->dev && cudaSetDevice(h->dev) == cudaSuccess)
+      prev = cur;
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 
 int fail(adi_ctx* h, int code, const std::string& msg) {
   if (h) h->err = msg;
@@ -362,7 +383,9 @@ void wb_setup(double l, double iv, double V[6][3][4], double Mx[6][32][3]) {
 
 // ---- constants: MFD closures as the printed rationals (App. B), CFD interior LU
 int init_constants(adi_ctx* h) {
-  if (g_const_ready) return ADI_OK;
+  if (h->dev < 0 || h->dev >= kMaxDev) return fail(h, ADI_ECUDA, "device ordinal out of range");
+  std::lock_guard<std::mutex> lock(g_const_mu);
+  if (g_const_ready[h->dev]) return ADI_OK;
   const double d4r0[6] = {-4751.0 / 5192.0, 909.0 / 1298.0, 6091.0 / 15576.0,
                           -1165.0 / 5192.0, 129.0 / 2596.0, -25.0 / 15576.0};
   const double g4r0[6] = {-47888.0 / 14245.0, 1790.0 / 407.0, -14545.0 / 9768.0,
@@ -441,7 +464,7 @@ int init_constants(adi_ctx* h) {
     CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_wbF, F, sizeof F));
     CUDA_TRY(h, cudaMemcpyToSymbol(adi::c_rho, rho, sizeof rho));
   }
-  g_const_ready = true;
+  g_const_ready[h->dev] = true;
   return ADI_OK;
 }
 
@@ -638,19 +661,19 @@ template <int METHOD, int MODE, bool EDGE, bool HET, bool FULL = false, bool NOE
 int launch_e(adi_ctx* h, const adi::Axis& A, adi::KParams p, int seg0, int nseg) {
   auto kern = adi::adi_line_kernel<METHOD, adi::TM, adi::NW, MODE, EDGE, HET, FULL, NOEND>;
   const size_t smem = adi::line_smem_bytes<METHOD, adi::TM, adi::NW, EDGE, HET>();
-  static bool attr = false;
-  static int wave = 0;   // resident CTAs of this instantiation on the device
-  if (!attr) {
+  // per device: the shared-memory attribute, and the resident CTAs of this
+  // instantiation (a race between threads only repeats idempotent calls)
+  static int wave[kMaxDev] = {};
+  const int dev = h->dev;
+  if (wave[dev] == 0) {
     CUDA_TRY(h, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int dev = 0, nsm = 0, occ = 0;
-    CUDA_TRY(h, cudaGetDevice(&dev));
+    int nsm = 0, occ = 0;
     CUDA_TRY(h, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     CUDA_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * adi::NW, smem));
-    wave = nsm * occ;
-    attr = true;
+    wave[dev] = std::max(nsm * occ, 1);
   }
   if (nseg <= 0) return ADI_OK;
-  p.pf_ahead = EDGE ? 0 : h->prefetch * wave;
+  p.pf_ahead = EDGE ? 0 : h->prefetch * wave[dev];
   const int nl = std::max(A.l1 - (A.l0 & ~3), 0);
   p.segs = A.d_segs + seg0;
   p.seg0 = seg0;
@@ -930,6 +953,11 @@ int adi_create_batch(int nx, int ny, double hh, double dt, double c, int method,
     return ADI_ECUDA;
   }
   adi_ctx* h = new adi_ctx();
+  if (cudaGetDevice(&h->dev) != cudaSuccess) {
+    cudaGetLastError();
+    delete h;
+    return ADI_ECUDA;
+  }
   h->full = (method == ADI_CFD_FULL);
   h->off = h->full ? 0 : 1;
   if (h->full) method = ADI_CFD;   // the CFD operators; every node unknown
@@ -991,6 +1019,7 @@ int adi_create(int nx, int ny, double hh, double dt, double c, int method, adi_h
 }
 
 int adi_set_param(adi_handle h, int key, double v) {
+  DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
   h->err.clear();
   if (key == ADI_K_SWEEPS) {
@@ -1046,6 +1075,7 @@ int adi_set_param(adi_handle h, int key, double v) {
 }
 
 int adi_set_stream(adi_handle h, void* s) {
+  DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
   h->err.clear();
   if (h->in_call) return fail(h, ADI_ESTATE, "call in progress");
@@ -1070,6 +1100,7 @@ static void field_rows(adi_ctx* h, bool with_halo, int* ya, int* yb) {
 
 static int set_fields_impl(adi_handle h, const double* U, const double* V, const double* W,
                            cudaMemcpyKind kind, bool sync = true) {
+  DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
   h->err.clear();
   if (!U || !V || !W) return fail(h, ADI_EINVAL, "null field pointer");
@@ -1106,12 +1137,15 @@ static int set_fields_impl(adi_handle h, const double* U, const double* V, const
 }
 
 int adi_set_fields(adi_handle h, const double* U, const double* V, const double* W) {
+  DevGuard dg_(h);
   return set_fields_impl(h, U, V, W, cudaMemcpyHostToDevice);
 }
 int adi_set_fields_device(adi_handle h, const double* U, const double* V, const double* W) {
+  DevGuard dg_(h);
   return set_fields_impl(h, U, V, W, cudaMemcpyDeviceToDevice);
 }
 int adi_set_fields_async(adi_handle h, const double* U, const double* V, const double* W) {
+  DevGuard dg_(h);
   return set_fields_impl(h, U, V, W, cudaMemcpyHostToDevice, false);
 }
 
@@ -1142,6 +1176,7 @@ static int set_points(adi_handle h, const int* ix, const int* iy) {
 }
 
 int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double* g, int ng) {
+  DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
   h->err.clear();
   if (g && ng < 1) return fail(h, ADI_EINVAL, "empty source table");
@@ -1180,6 +1215,7 @@ int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double
 }
 
 int adi_set_point_sources(adi_handle h, const int* ix, const int* iy, const double* g, int ng) {
+  DevGuard dg_(h);
   if (!h || !ix || !iy) return ADI_EINVAL;
   h->err.clear();
   if (g && ng < 1) return fail(h, ADI_EINVAL, "empty source table");
@@ -1190,6 +1226,7 @@ int adi_set_point_sources(adi_handle h, const int* ix, const int* iy, const doub
 }
 
 int adi_set_boundary(adi_handle h, const double* edges, const double* g, int ng) {
+  DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
   h->err.clear();
   if (g && ng < 1) return fail(h, ADI_EINVAL, "empty boundary table");
@@ -1207,6 +1244,7 @@ int adi_set_boundary(adi_handle h, const double* edges, const double* g, int ng)
 }
 
 int adi_set_media(adi_handle h, const float* kappa, const float* rinv_v, const float* rinv_w) {
+  DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
   h->err.clear();
   if (h->in_call) return fail(h, ADI_ESTATE, "call in progress");
@@ -1270,6 +1308,7 @@ int adi_set_media(adi_handle h, const float* kappa, const float* rinv_v, const f
 // ---- one call = begin (prologue), n x {rows, cols}, end.  The phases are public so
 // that a multi-GPU driver can exchange halos between the row and column sweeps.
 int adi_step_begin(adi_handle h, int nsteps) {
+  DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
   h->err.clear();
   if (h->in_call) return fail(h, ADI_ESTATE, "a call is already in progress");
@@ -1316,6 +1355,7 @@ int adi_step_begin(adi_handle h, int nsteps) {
 }
 
 int adi_step_rows(adi_handle h) {
+  DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
   if (!h->in_call || h->m >= h->call_m1) return fail(h, ADI_ESTATE, "no step pending");
   const long long m = h->m;
@@ -1333,6 +1373,7 @@ int adi_step_rows(adi_handle h) {
 }
 
 int adi_step_cols(adi_handle h) {
+  DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
   if (!h->in_call || h->m >= h->call_m1) return fail(h, ADI_ESTATE, "no step pending");
   const long long m = h->m;
@@ -1363,6 +1404,7 @@ int adi_step_cols(adi_handle h) {
 }
 
 int adi_step_end(adi_handle h) {
+  DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
   if (!h->in_call || h->m != h->call_m1) return fail(h, ADI_ESTATE, "steps of the call not finished");
   if (h->Vcur != h->V) std::swap(h->V, h->V2);
@@ -1392,6 +1434,7 @@ int adi_step_end(adi_handle h) {
 static int dist_exchange(adi_ctx* h, int kind);
 
 int adi_step(adi_handle h, int nsteps) {
+  DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
   if (nsteps < 0) return fail(h, ADI_EINVAL, "n < 0");
   if (nsteps == 0) return ADI_OK;
@@ -1414,6 +1457,7 @@ int adi_step(adi_handle h, int nsteps) {
 
 // ---- band decomposition --------------------------------------------------
 int adi_set_band(adi_handle h, int y0, int y1) {
+  DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
   h->err.clear();
   if (h->in_call) return fail(h, ADI_ESTATE, "call in progress");
@@ -1456,6 +1500,7 @@ static size_t halo_elems(adi_ctx* h, int kind, int rows) {
 }
 
 int adi_halo_bytes(adi_handle h, int kind, int side, size_t* bytes) {
+  DevGuard dg_(h);
   if (!h || !bytes || kind < 0 || kind > 1 || side < 0 || side > 1) return ADI_EINVAL;
   int a, b, c, d;
   halo_range(h, side, 1, &a, &b);
@@ -1502,6 +1547,7 @@ static int halo_copy(adi_ctx* h, int kind, int a, int b, double* buf, int dir) {
 }
 
 int adi_halo_pack(adi_handle h, int kind, int side, void* dev_buf) {
+  DevGuard dg_(h);
   if (!h || !dev_buf || kind < 0 || kind > 1 || side < 0 || side > 1) return ADI_EINVAL;
   h->err.clear();
   int a, b;
@@ -1510,6 +1556,7 @@ int adi_halo_pack(adi_handle h, int kind, int side, void* dev_buf) {
 }
 
 int adi_halo_unpack(adi_handle h, int kind, int side, const void* dev_buf) {
+  DevGuard dg_(h);
   if (!h || !dev_buf || kind < 0 || kind > 1 || side < 0 || side > 1) return ADI_EINVAL;
   h->err.clear();
   int a, b;
@@ -1610,6 +1657,7 @@ int adi_create_dist(int nx, int ny, double hh, double dt, double c, int method, 
 }
 
 int adi_band_info(adi_handle h, int* y0, int* y1, int* halo, int* npos) {
+  DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
   if (y0) *y0 = h->band_y0 > h->ay.n ? 0 : h->band_y0;
   if (y1) *y1 = std::min(h->band_y1, h->ay.n + 1);
@@ -1620,6 +1668,7 @@ int adi_band_info(adi_handle h, int* y0, int* y1, int* halo, int* npos) {
 
 static int get_fields_impl(adi_handle h, double* U, double* V, double* W, cudaMemcpyKind kind,
                            bool sync = true) {
+  DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
   h->err.clear();
   if (!U || !V || !W) return fail(h, ADI_EINVAL, "null field pointer");
@@ -1652,16 +1701,20 @@ static int get_fields_impl(adi_handle h, double* U, double* V, double* W, cudaMe
 }
 
 int adi_get_fields(adi_handle h, double* U, double* V, double* W) {
+  DevGuard dg_(h);
   return get_fields_impl(h, U, V, W, cudaMemcpyDeviceToHost);
 }
 int adi_get_fields_async(adi_handle h, double* U, double* V, double* W) {
+  DevGuard dg_(h);
   return get_fields_impl(h, U, V, W, cudaMemcpyDeviceToHost, false);
 }
 int adi_get_fields_device(adi_handle h, double* U, double* V, double* W) {
+  DevGuard dg_(h);
   return get_fields_impl(h, U, V, W, cudaMemcpyDeviceToDevice);
 }
 
 int adi_get_last_sweeps(adi_handle h, int* k_rows, int* k_cols) {
+  DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
   h->err.clear();
   int k[2] = {h->K, h->K};
@@ -1675,6 +1728,7 @@ int adi_get_last_sweeps(adi_handle h, int* k_rows, int* k_cols) {
 }
 
 int adi_get_stats(adi_handle h, adi_stats* s) {
+  DevGuard dg_(h);
   if (!h || !s) return ADI_EINVAL;
   h->err.clear();
   s->steps = h->m;
@@ -1702,6 +1756,7 @@ int adi_get_stats(adi_handle h, adi_stats* s) {
 }
 
 int adi_get_kernel_times(adi_handle h, double* ms, long long* launches, int nkinds) {
+  DevGuard dg_(h);
   if (!h || nkinds < 0) return ADI_EINVAL;
   h->err.clear();
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
@@ -1724,6 +1779,7 @@ int adi_get_kernel_times(adi_handle h, double* ms, long long* launches, int nkin
 }
 
 int adi_set_trace(adi_handle h, void* dev_buf, long long cap, int kind) {
+  DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
   h->err.clear();
   if (dev_buf && (cap < 0 || kind < 0 || kind >= ADI_NKINDS)) return fail(h, ADI_EINVAL, "bad trace arguments");
@@ -1736,6 +1792,7 @@ int adi_set_trace(adi_handle h, void* dev_buf, long long cap, int kind) {
 const char* adi_last_error(adi_handle h) { return h ? h->err.c_str() : "null handle"; }
 
 void adi_destroy(adi_handle h) {
+  DevGuard dg_(h);
   if (!h) return;
   free_ctx(h);
   delete h;
