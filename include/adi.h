@@ -110,11 +110,17 @@ enum adi_param {
                            are multiplied by G(x)G(y), G = exp(-(a (nb - d))^2) at distance d < nb
                            (points) from the nearest edge, else 1 */
   ADI_ABSORB_RATE = 8,  /* ADI_CFD_FULL only: the rate a > 0 of the taper; default 0.015 */
-  ADI_PREFETCH = 9      /* performance knob, no effect on results: each line tile of the lean
+  ADI_PREFETCH = 9,     /* performance knob, no effect on results: each line tile of the lean
                            kernels prefetches into L2 (TMA prefetch) the staging tiles of the tile
                            v resident-CTA waves ahead in the same launch, so that the HBM reads of
                            the next wave overlap this wave's sweeps; integer in [0, 8], 0 = off;
                            default 0 (measured slower: DESIGN.md §5.6) */
+  ADI_CARRY = 10,       /* 1 (default): the last column kernel of a call also computes the next
+                           step's explicit half (a2), so that the next adi_step skips its
+                           prologue kernel, unless a set_* call came in between.  Same results
+                           up to rounding order (the one-call computation).  Used for plain
+                           handles only (no band / dist, no ADI_EPS, no media, not
+                           ADI_CFD_FULL); 0 = always run the prologue */
 };
 
 /* Kernel kinds launched by adi_step (index of adi_get_kernel_times arrays). */

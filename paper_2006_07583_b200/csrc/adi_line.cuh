@@ -120,6 +120,11 @@ struct KParams {
   // ADI_PREFETCH: the tile this many CTAs later in launch order (about one resident wave
   // per unit) has its staging tiles prefetched into L2 at this tile's start; 0 = off
   int pf_ahead;
+  // carry mode (KM_SWEEP, last step of a call): before the fused a2 the
+  // kernel also writes this step's final state, U^{m+1} = u_K to U_out (transposed) and
+  // W̄^{m+1} = x_K to X_out2, so the next call needs no prologue; 0 = off
+  int carry;
+  double* X_out2;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -1118,6 +1123,66 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     }
   };
 
+  // u = u + dt/2 F in registers, phi read from global (warmed in L2 at tile start)
+  auto add_source_global_reg = [&](double (&uu)[M]) {
+    int ipt = -1;
+    if (P.pt_line && line == P.pt_line[b] && (!EDGE || c.live)) ipt = P.pt_pos[b] - c.s;
+    const double ptf = P.pt_amp * P.gf;
+    const double2* ph = reinterpret_cast<const double2*>(P.phi_src + (long long)line * P.s_line + c.s);
+#pragma unroll
+    for (int i = 0; i < M / 2; ++i) {
+      const double2 f2 = (want_phi && lineok) ? __ldg(ph + i) : make_double2(0.0, 0.0);
+      double f0 = f2.x * P.gf, f1 = f2.y * P.gf;
+      if (2 * i == ipt) f0 += ptf;
+      if (2 * i + 1 == ipt) f1 += ptf;
+      uu[2 * i] = fma(P.half_dt, f0, uu[2 * i]);
+      uu[2 * i + 1] = fma(P.half_dt, f1, uu[2 * i + 1]);
+    }
+  };
+
+  // carry mode: this step's final state before the fused a2 -- W̄^{m+1} = x_K from
+  // registers (own line, owned positions), U^{m+1} = u_K from the S tiles, transposed,
+  // with the FINAL kernel's position range and the MFD right Dirichlet row n+1
+  auto carry_store = [&](const double (&xk)[M]) {
+    if (lineok && (!EDGE || c.live)) {
+      const int xlo = max(sg.out_lo, 0), xhi = min(sg.out_hi, n + 1);
+      double* Xo = P.X_out2 + (long long)b * P.x_batch + (long long)line * P.x_line;
+      // 16-byte pairs (segment starts and line pitches are even)
+#pragma unroll
+      for (int i = 0; i < M; i += 2) {
+        const int p = c.s + i;
+        if (p >= xlo && p + 1 < xhi) *reinterpret_cast<double2*>(Xo + p) = make_double2(xk[i], xk[i + 1]);
+        else {
+          if (p >= xlo && p < xhi) Xo[p] = xk[i];
+          if (p + 1 >= xlo && p + 1 < xhi) Xo[p + 1] = xk[i + 1];
+        }
+      }
+    }
+    __syncthreads();   // every warp's u_K is in its S tile
+    const int pr = lane >> 4;
+    const int ln = P.line0 + blockIdx.x * NW + 2 * pr;
+    const bool ok0 = ln >= P.line_lo && ln < P.nlines;
+    const bool ok1 = ln + 1 >= P.line_lo && ln + 1 < P.nlines;
+    const int plo_ = max(sg.out_lo, 0), phi_ = min(sg.out_hi, n + 1);
+    const double* r0 = stS + (2 * pr) * LSTR;
+    const double* r1 = r0 + LSTR;
+    for (int pos = 16 * w + (lane & 15); pos < 32 * M; pos += 16 * NW) {
+      const int p = sg.start + pos;
+      if (p < plo_ || p >= phi_) continue;
+      const int si = (pos >> 5) * PADM + (pos & 31);
+      const double v0 = r0[si], v1 = r1[si];
+      double* Ub = P.U_out + (long long)b * P.u_batch + (long long)p * P.u_pt + (long long)ln * P.u_line;
+      if (ok0 && ok1) *reinterpret_cast<double2*>(Ub) = make_double2(v0, v1);
+      else { if (ok0) Ub[0] = v0; if (ok1) Ub[P.u_line] = v1; }
+      if (METHOD == M_MFD && p == n) {
+        double* Ut = P.U_out + (long long)b * P.u_batch + (long long)(n + 1) * P.u_pt + (long long)ln * P.u_line;
+        if (ok0) Ut[0] = P.edgeR ? P.edgeR[ln] * P.gb : 0.0;
+        if (ok1) Ut[P.u_line] = P.edgeR ? P.edgeR[ln + 1] * P.gb : 0.0;
+      }
+    }
+    __syncthreads();   // the S tiles are read before the epilogue reuses them
+  };
+
   // stopping rule (Alg. 3/4): this warp's share of
   // ||u_s - u_{s-1}||^2 and ||x_s - x_{s-1}||^2 over its owned positions
   auto norm_add = [&](const double (&un)[M], const double (&uo)[M], const double (&xn)[M],
@@ -1267,6 +1332,9 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
         }
       } else if (MODE == KM_SWEEP) {
         double e1, e2;
+        if constexpr (!HET && !FULL) {
+          if (P.carry) carry_store(x);   // U^{m+1} (u_K parked in the S tile), W̄^{m+1}
+        }
         add_source_global(Sm);   // S = u_K + dt/2 F
         cfd_apply<M, UOPK, EDGE, HET, !NOEND>(c, P, lane, FULL ? stXs : stU, etab, x, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
         if constexpr (HET) het_apply<M, METHOD, true, EDGE>(c, Cm, Sm, u, 1, uhi);
@@ -1352,14 +1420,29 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
           }
         }
         u_op(x, Sm);
-        if (MODE == KM_SWEEP && k + 1 == KK) stage_phi();
+        if (MODE == KM_SWEEP && k + 1 == KK && !(!HET && P.carry)) stage_phi();
         x_op(Vm);
         if constexpr (TEST) {
           if (k + 1 == KK) norm_add(u, uo, x, xo);
         }
       }
       if (MODE == KM_SWEEP) {
-        if constexpr (NOEND && !HET && MFD_EPI_REG) {
+        bool carried = false;
+        if constexpr (!HET) {
+          if (P.carry) {
+            // carry mode: u_K to the S tile (no source pattern staged there), the final
+            // state out, then S' = (u_K - alpha D̄(x_K)) + dt/2 F with the source from global
+            double2* S2 = reinterpret_cast<double2*>(Sm);
+#pragma unroll
+            for (int i = 0; i < M / 2; ++i) S2[i] = make_double2(u[2 * i], u[2 * i + 1]);
+            carry_store(x);
+            u_op(x, Sm);
+            add_source_global_reg(u);
+            carried = true;
+          }
+        }
+        if (carried) {
+        } else if constexpr (NOEND && !HET && MFD_EPI_REG) {
           // interior tiles: the epilogue operator accumulates onto u_K in registers and
           // the source comes last (S' = u_K - alpha D̄(x_K) + dt/2 F), so the TMA of the
           // source pattern, issued after the last u-op, has two operators of slack

@@ -91,6 +91,11 @@ struct adi_ctx {
   // device buffers
   double *U = nullptr, *V = nullptr, *W = nullptr;
   double *V2 = nullptr, *W2 = nullptr, *Sa = nullptr, *Sb = nullptr;
+  // carry mode: W3 receives the next step's W* from the last column
+  // kernel of a call, Sa its S1; carry_valid: the next call may skip its prologue
+  double* W3 = nullptr;
+  bool carry_valid = false;
+  int carry_on = 1;     // ADI_CARRY
   double* phi = nullptr;    // source pattern, S layout (row-major)
   double* phiT = nullptr;   // its transpose (column sweep)
   double* edges = nullptr;  // y0 | y1 | x0 | x1
@@ -280,7 +285,7 @@ int tmap_for(adi_ctx* h, const double* ptr, CUtensorMap* out) {
   if (ptr == h->Sa) { pitch = h->pa; rows = h->nyu; bs = h->aS; }
   else if (ptr == h->Sb) { pitch = h->pb; rows = h->nxu; bs = h->aS; }
   else if (ptr == h->V || ptr == h->V2) { pitch = h->pv; rows = h->nyu; bs = h->aV; }
-  else if (ptr == h->W || ptr == h->W2) { pitch = h->pw; rows = h->nxu; bs = h->aW; }
+  else if (ptr == h->W || ptr == h->W2 || ptr == h->W3) { pitch = h->pw; rows = h->nxu; bs = h->aW; }
   else if (ptr == h->phi) { pitch = h->pa; rows = h->nyu; bs = h->aS; batch = 1; }
   else if (ptr == h->phiT) { pitch = h->pb; rows = h->nxu; bs = h->aS; batch = 1; }
   else if (ptr == h->Ca) { pitch = h->pa; rows = h->nyu; bs = h->aS; batch = 1; }
@@ -889,7 +894,7 @@ void free_ctx(adi_ctx* h) {
   h->comm = nullptr;
   for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
-  for (double* q : {h->Ubase, h->V, h->W, h->V2, h->W2, h->Sa, h->Sb, h->phi, h->phiT, h->Ca, h->Cb}) dfree(q);
+  for (double* q : {h->Ubase, h->V, h->W, h->V2, h->W2, h->W3, h->Sa, h->Sb, h->phi, h->phiT, h->Ca, h->Cb}) dfree(q);
   for (void* q : {(void*)h->edges, (void*)h->flag, (void*)h->d_norms, (void*)h->d_k, (void*)h->d_taper})
     if (q) cudaFree(q);
   for (adi::Axis* A : {&h->ax, &h->ay})
@@ -1028,6 +1033,7 @@ int adi_set_param(adi_handle h, int key, double v) {
   } else if (key == ADI_RHO) {
     if (!(v > 0) || !std::isfinite(v)) return fail(h, ADI_EINVAL, "rho must be > 0");
     h->rho = v;
+    h->carry_valid = false;   // alpha, beta of the carried a2 change
   } else if (key == ADI_CHECK_FINITE) {
     h->check_finite = (v != 0);
   } else if (key == ADI_TIMING) {
@@ -1059,6 +1065,10 @@ int adi_set_param(adi_handle h, int key, double v) {
     H2D_SYNC(h, h->d_taper, g.data(), g.size() * sizeof(double));
     h->absorb_nb = nb;
     h->absorb_a = a;
+  } else if (key == ADI_CARRY) {
+    if (v != 0.0 && v != 1.0) return fail(h, ADI_EINVAL, "carry must be 0 or 1");
+    h->carry_on = (int)v;
+    if (!h->carry_on) h->carry_valid = false;
   } else if (key == ADI_PREFETCH) {
     if (!(v >= 0) || v != std::floor(v) || v > 8) return fail(h, ADI_EINVAL, "prefetch must be an integer in [0, 8]");
     h->prefetch = (int)v;
@@ -1102,6 +1112,7 @@ static int set_fields_impl(adi_handle h, const double* U, const double* V, const
                            cudaMemcpyKind kind, bool sync = true) {
   DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
+  h->carry_valid = false;   // the next call recomputes its a2 (prologue)
   h->err.clear();
   if (!U || !V || !W) return fail(h, ADI_EINVAL, "null field pointer");
   if (h->in_call) return fail(h, ADI_ESTATE, "call in progress");
@@ -1178,6 +1189,7 @@ static int set_points(adi_handle h, const int* ix, const int* iy) {
 int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double* g, int ng) {
   DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
+  h->carry_valid = false;   // the next call recomputes its a2 (prologue)
   h->err.clear();
   if (g && ng < 1) return fail(h, ADI_EINVAL, "empty source table");
   const bool has_pt = ix >= h->off;   // (the full variant: every node, ix >= 0)
@@ -1217,6 +1229,7 @@ int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double
 int adi_set_point_sources(adi_handle h, const int* ix, const int* iy, const double* g, int ng) {
   DevGuard dg_(h);
   if (!h || !ix || !iy) return ADI_EINVAL;
+  h->carry_valid = false;   // the next call recomputes its a2 (prologue)
   h->err.clear();
   if (g && ng < 1) return fail(h, ADI_EINVAL, "empty source table");
   int rc = set_points(h, ix, iy);
@@ -1228,6 +1241,7 @@ int adi_set_point_sources(adi_handle h, const int* ix, const int* iy, const doub
 int adi_set_boundary(adi_handle h, const double* edges, const double* g, int ng) {
   DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
+  h->carry_valid = false;   // the next call recomputes its a2 (prologue)
   h->err.clear();
   if (g && ng < 1) return fail(h, ADI_EINVAL, "empty boundary table");
   if (h->full && edges) return fail(h, ADI_EINVAL, "the full-matrix variant has no Dirichlet data");
@@ -1246,6 +1260,7 @@ int adi_set_boundary(adi_handle h, const double* edges, const double* g, int ng)
 int adi_set_media(adi_handle h, const float* kappa, const float* rinv_v, const float* rinv_w) {
   DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
+  h->carry_valid = false;   // the next call recomputes its a2 (prologue)
   h->err.clear();
   if (h->in_call) return fail(h, ADI_ESTATE, "call in progress");
   if (!kappa && !rinv_v && !rinv_w) {   // back to the scalar medium
@@ -1305,6 +1320,15 @@ int adi_set_media(adi_handle h, const float* kappa, const float* rinv_v, const f
   return rc;
 }
 
+// carry mode: the last column kernel of a call also writes the next
+// step's S1 and W* (the fused a2 of a regular column kernel), so that the next call can
+// skip its prologue.  Plain handles only: no band or dist (halo rows of S1 would be
+// stale), no stopping rule, no media, not the full-matrix variant.
+static bool carry_ok(const adi_ctx* h) {
+  return h->carry_on && !h->full && !h->het && h->eps <= 0.0 && !h->dist && h->band_y0 <= 0 &&
+         h->band_y1 >= h->ay.n + 1;
+}
+
 // ---- one call = begin (prologue), n x {rows, cols}, end.  The phases are public so
 // that a multi-GPU driver can exchange halos between the row and column sweeps.
 int adi_step_begin(adi_handle h, int nsteps) {
@@ -1338,17 +1362,23 @@ int adi_step_begin(adi_handle h, int nsteps) {
     if (!h->d_k) CUDA_TRY(h, cudaMalloc(&h->d_k, 4 * sizeof(int)));
   }
   int rc;
-  // a2 (standalone once per call): S1 = U - alpha D̄_y W + dt/2 F(t^m), W* = W - beta D_y U
-  {
+  if (h->carry_valid && carry_ok(h)) {
+    // the previous call's last column kernel left S1 in Sa and W* in W3
+    h->carry_valid = false;
+    h->Vcur = h->V; h->Valt = h->V2;
+    h->Wcur = h->W3; h->Walt = h->W2;
+  } else {
+    h->carry_valid = false;
+    // a2 (standalone once per call): S1 = U - alpha D̄_y W + dt/2 F(t^m), W* = W - beta D_y U
     adi::KParams p = base_params(h, h->ay, true);
     p.U_in = h->U;
     p.X_in = h->W; p.X_out = h->W2;
     p.S_out = h->Sa;
     p.gf = tabv(h->gf, 2 * m0);
     if ((rc = launch(h, adi::KM_PROLOGUE, h->ay, p, ADI_KK_PROLOGUE))) return rc;
+    h->Vcur = h->V; h->Valt = h->V2;
+    h->Wcur = h->W2; h->Walt = h->W;
   }
-  h->Vcur = h->V; h->Valt = h->V2;
-  h->Wcur = h->W2; h->Walt = h->W;
   h->call_m1 = m1;
   h->in_call = true;
   return ADI_OK;
@@ -1384,7 +1414,29 @@ int adi_step_cols(adi_handle h) {
   p.gb = tabv(h->gb, 2 * m + 2);
   p.gf = tabv(h->gf, 2 * m + 2);
   int rc;
-  if (last) {  // write U^{m+1} and W̄^{m+1} into the canonical buffers
+  if (last && carry_ok(h)) {
+    // a regular column kernel (S1, W* of step m+1 into Sa, W3) that also writes
+    // U^{m+1} and W̄^{m+1}; the three W buffers rotate: W = W̄^{m+1}, W3 = W*, W2 = free
+    if (!h->W3 && !(h->W3 = dalloc((size_t)h->batch * h->aW))) return fail(h, ADI_ENOMEM, "carry buffer");
+    double* in = h->Wcur;
+    double* outW = nullptr;
+    double* outC = nullptr;
+    for (double* q : {h->W, h->W2, h->W3}) {
+      if (q == in) continue;
+      if (!outW) outW = q;
+      else if (!outC) outC = q;
+    }
+    p.S_out = h->Sa;
+    p.X_out = outC;
+    p.U_out = h->U;
+    p.X_out2 = outW;
+    p.carry = 1;
+    rc = launch(h, adi::KM_SWEEP, h->ay, p, ADI_KK_FINAL);
+    if (rc) return rc;
+    h->W = outW; h->W3 = outC; h->W2 = in;
+    h->Wcur = h->W; h->Walt = h->W2;
+    h->carry_valid = true;
+  } else if (last) {  // write U^{m+1} and W̄^{m+1} into the canonical buffers
     p.U_out = h->U;
     p.X_out = (h->Wcur == h->W) ? h->W2 : h->W;
     rc = (h->eps > 0.0) ? stage_with_rule(h, adi::KM_FINAL_T, h->ay, p, ADI_KK_FINAL, 1)
@@ -1459,6 +1511,7 @@ int adi_step(adi_handle h, int nsteps) {
 int adi_set_band(adi_handle h, int y0, int y1) {
   DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
+  h->carry_valid = false;   // the next call recomputes its a2 (prologue)
   h->err.clear();
   if (h->in_call) return fail(h, ADI_ESTATE, "call in progress");
   const int ny_pos = h->ay.n + 1;  // y positions 0..n_y
@@ -1558,6 +1611,7 @@ int adi_halo_pack(adi_handle h, int kind, int side, void* dev_buf) {
 int adi_halo_unpack(adi_handle h, int kind, int side, const void* dev_buf) {
   DevGuard dg_(h);
   if (!h || !dev_buf || kind < 0 || kind > 1 || side < 0 || side > 1) return ADI_EINVAL;
+  h->carry_valid = false;   // the next call recomputes its a2 (prologue)
   h->err.clear();
   int a, b;
   halo_range(h, side, 0, &a, &b);

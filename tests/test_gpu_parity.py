@@ -365,3 +365,76 @@ def test_prefetch_knob_batch(adi):
         s.close()
     for a, b in zip(outs[0], outs[1]):
         assert np.array_equal(a, b)
+
+
+def _run_calls(adi, p, plan, carry, n_steps_table=None):
+    """Run `plan` on one handle: ints are adi_step(n) calls, tuples are actions
+    between calls ("get",), ("source", phi, gf), ("fields", U, V, W), ("rho", v)."""
+    s = adi.AdiSolver.from_problem(p)
+    s.set_param(adi.ADI_CARRY, carry)
+    for a in plan:
+        if isinstance(a, int):
+            s.step(a)
+        elif a[0] == "get":
+            s.get_fields()
+        elif a[0] == "source":
+            s.set_source(a[1], None, a[2])
+        elif a[0] == "fields":
+            s.set_fields(a[1], a[2], a[3])
+        elif a[0] == "rho":
+            s.set_param(adi.ADI_RHO, a[1])
+    out = s.get_fields()
+    s.close()
+    return out
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+@pytest.mark.parametrize("n", [37, 1601])
+def test_carry_matches_one_call(adi, method, n):
+    """ADI_CARRY (include/adi.h): the next call starts from the a2 computed by the previous
+    call's last column kernel -- the one-call computation, so split calls match one call
+    to rounding, with and without a get_fields in between; and the oracle at 1e-12."""
+    p = random_problem(method, n, seed=7, steps=6)
+    one = _run_calls(adi, p, [6], 1)
+    split = _run_calls(adi, p, [2, ("get",), 1, 3], 1)
+    nocarry = _run_calls(adi, p, [2, ("get",), 1, 3], 0)
+    assert_parity(split, one, tol=1e-13)
+    assert_parity(nocarry, one, tol=1e-13)
+    assert_parity(split, run_oracle(p, 6))
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+def test_carry_invalidated_by_setters(adi, method):
+    """A set_* call between two calls discards the carried a2: the result equals the
+    same sequence with ADI_CARRY = 0 (a stale a2 would differ at O(dt))."""
+    n = 1601
+    p = random_problem(method, n, seed=8, steps=6)
+    rng = np.random.default_rng(3)
+    phi2 = rng.standard_normal(p.phi.shape)
+    gf2 = rng.standard_normal(p.gf.shape)
+    U2, V2, W2 = (rng.standard_normal(a.shape) for a in (p.U, p.V, p.W))
+    for between in ([("source", phi2, gf2)], [("fields", U2, V2, W2)], [("rho", 1.3)]):
+        plan = [2] + between + [2]
+        a = _run_calls(adi, p, plan, 1)
+        b = _run_calls(adi, p, plan, 0)
+        assert_parity(a, b, tol=1e-13, what=str(between[0][0]))
+
+
+def test_carry_batch_point_sources(adi):
+    """Carry with a batch of Ricker shots (per-grid point sources), split calls."""
+    n, B = 1601, 2
+    probs = [ricker_problem(n, shot=s, nshots=8, method=MFD, steps=8, f0=20.0, t0=0.05) for s in range(B)]
+    p0 = probs[0]
+    outs = []
+    for carry, plan in ((1, [3, 2, 3]), (0, [8])):
+        s = adi.AdiSolver(n, n, p0.h, p0.dt, 1.0, MFD, batch=B)
+        s.set_param(adi.ADI_CARRY, carry)
+        s.set_fields(np.stack([p.U for p in probs]), np.stack([p.V for p in probs]),
+                     np.stack([p.W for p in probs]))
+        s.set_point_sources([p.src[0] for p in probs], [p.src[1] for p in probs], p0.gf)
+        for k in plan:
+            s.step(k)
+        outs.append(s.get_fields())
+        s.close()
+    assert np.abs(outs[1][0]).max() > 0
+    assert_parity(outs[0], outs[1], tol=1e-13)
