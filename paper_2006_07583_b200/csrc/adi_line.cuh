@@ -864,6 +864,13 @@ __device__ __forceinline__ void tma_prefetch_seg(const CUtensorMap* tm, int c1, 
 constexpr int STORE_UNROLL = ADI_STORE_UNROLL;
 // MFD interior tiles: the epilogue operator accumulates onto u_K in registers (1) or
 // reads a staged base u_K + dt/2 F (0)
+#ifndef ADI_CARRY_TILE
+#define ADI_CARRY_TILE 1
+#endif
+// carry mode: W̄^{m+1} = x_K leaves through the warp's X tile with the
+// coalesced pair store of the epilogue (1) instead of per-lane 16-byte stores from
+// registers, 256 B apart across lanes (0)
+constexpr bool CARRY_TILE = ADI_CARRY_TILE;
 #ifndef ADI_MFD_EPI_REG
 #define ADI_MFD_EPI_REG 1
 #endif
@@ -1144,7 +1151,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   // registers (own line, owned positions), U^{m+1} = u_K from the S tiles, transposed,
   // with the FINAL kernel's position range and the MFD right Dirichlet row n+1
   auto carry_store = [&](const double (&xk)[M]) {
-    if (lineok && (!EDGE || c.live)) {
+    if (!CARRY_TILE && lineok && (!EDGE || c.live)) {
       const int xlo = max(sg.out_lo, 0), xhi = min(sg.out_hi, n + 1);
       double* Xo = P.X_out2 + (long long)b * P.x_batch + (long long)line * P.x_line;
       // 16-byte pairs (segment starts and line pitches are even)
@@ -1181,6 +1188,30 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       }
     }
     __syncthreads();   // the S tiles are read before the epilogue reuses them
+  };
+
+  // carry mode with CARRY_TILE, after the epilogue operator (x = x_K no longer an
+  // operand): x_K replaces V^m in the X tile as x becomes 2 x_K - V^m, then the warp
+  // stores W̄^{m+1} from the tile in coalesced pairs (the X-store pattern below)
+  auto carry_x_tile = [&]() {
+#pragma unroll
+    for (int i = 0; i < M; ++i) { const double t = Vm[i]; Vm[i] = x[i]; x[i] = fma(2.0, x[i], -t); }
+    __syncwarp();
+    if (lineok) {
+      const int xlo = max(sg.out_lo, 0), xhi = min(sg.out_hi, n + 1);
+      double* Xo = P.X_out2 + (long long)b * P.x_batch + (long long)line * P.x_line;
+#pragma unroll STORE_UNROLL
+      for (int p = (xlo & ~1) + 2 * lane; p < xhi; p += 64) {
+        const int q = p - sg.start;
+        const double2 v = *reinterpret_cast<const double2*>(lX + (q >> 5) * PADM + (q & 31));
+        if (p >= xlo && p + 1 < xhi) *reinterpret_cast<double2*>(Xo + p) = v;
+        else {
+          if (p >= xlo) Xo[p] = v.x;
+          if (p + 1 >= xlo && p + 1 < xhi) Xo[p + 1] = v.y;
+        }
+      }
+    }
+    __syncwarp();   // the tile is read before the epilogue stages X' over it
   };
 
   // stopping rule (Alg. 3/4): this warp's share of
@@ -1332,14 +1363,18 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
         }
       } else if (MODE == KM_SWEEP) {
         double e1, e2;
+        bool carried = false;
         if constexpr (!HET && !FULL) {
-          if (P.carry) carry_store(x);   // U^{m+1} (u_K parked in the S tile), W̄^{m+1}
+          if (P.carry) { carry_store(x); carried = true; }   // U^{m+1} (u_K parked in the S tile), W̄^{m+1}
         }
         add_source_global(Sm);   // S = u_K + dt/2 F
         cfd_apply<M, UOPK, EDGE, HET, !NOEND>(c, P, lane, FULL ? stXs : stU, etab, x, Sm, u, P.cu, xm1, xp1, 0.0, 0.0, e1, e2);
         if constexpr (HET) het_apply<M, METHOD, true, EDGE>(c, Cm, Sm, u, 1, uhi);
+        if (CARRY_TILE && carried) carry_x_tile();
+        else {
 #pragma unroll
-        for (int i = 0; i < M; ++i) x[i] = fma(2.0, x[i], -Vm[i]);
+          for (int i = 0; i < M; ++i) x[i] = fma(2.0, x[i], -Vm[i]);
+        }
         if (FULL && P.damp == 1) {   // row sweep of the full variant: V^{m+1} = G (2x - X)
           const double gl = taper_at(line, P.nlines - 1);
 #pragma unroll
@@ -1438,6 +1473,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
             carry_store(x);
             u_op(x, Sm);
             add_source_global_reg(u);
+            if (CARRY_TILE) carry_x_tile();
             carried = true;
           }
         }
@@ -1454,8 +1490,10 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
           add_source(Sm, u);
           u_op(x, Sm);
         }
+        if (!(CARRY_TILE && carried)) {
 #pragma unroll
-        for (int i = 0; i < M; ++i) x[i] = fma(2.0, x[i], -Vm[i]);
+          for (int i = 0; i < M; ++i) x[i] = fma(2.0, x[i], -Vm[i]);
+        }
       }
     }
   }
