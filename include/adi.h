@@ -93,7 +93,7 @@ enum adi_param {
   ADI_K_SWEEPS = 0,     /* fixed-point sweeps per stage, integer >= 1; default 8 */
   ADI_RHO = 1,          /* density rho > 0 (kappa = rho c^2); default 1 */
   ADI_CHECK_FINITE = 2, /* 1: adi_step synchronizes and checks for NaN/Inf; default 0 */
-  ADI_TILE_CHUNKS = 3,  /* cap on chunks (16 points each) per line in one tile; 0 = auto.
+  ADI_TILE_CHUNKS = 3,  /* cap on chunks (32 points each) per line in one tile; 0 = auto.
                            Testing aid: forces the segmented (halo) tiling on small grids. */
   ADI_TIMING = 4,       /* 1: bracket every kernel launch with CUDA events on the handle's
                            stream (read with adi_get_kernel_times); default 0 */
@@ -260,6 +260,11 @@ int adi_create_dist(int nx, int ny, double h, double dt, double c, int method, i
 int adi_nccl_unique_id(void* out128);
 /* The band cuts of y positions [0, npos) over nranks: cuts[0..nranks] (host logic only). */
 int adi_dist_bands(int npos, int nranks, int* cuts);
+/* The halo (positions on each side of a band) that the band decomposition of `method`
+ * (ADI_CFD / ADI_MFD) exchanges: the bound of a half-step's domain of influence
+ * (DESIGN.md §5.3).  Host logic only; the value adi_band_info reports for a handle.
+ * EINVAL for another method. */
+int adi_plan_halo(int method, int* halo);
 int adi_halo_bytes(adi_handle h, int kind, int side, size_t* bytes);
 int adi_halo_pack(adi_handle h, int kind, int side, void* dev_buf);
 int adi_halo_unpack(adi_handle h, int kind, int side, const void* dev_buf);

@@ -87,6 +87,7 @@ def lib():
         L.adi_create_dist.argtypes = [I, I, D, D, D, I, I, P, I, I, ctypes.POINTER(H)]
         L.adi_nccl_unique_id.argtypes = [P]
         L.adi_dist_bands.argtypes = [I, I, P]
+        L.adi_plan_halo.argtypes = [I, ctypes.POINTER(I)]
         L.adi_step.argtypes = [H, I]
         L.adi_get_fields.argtypes = [H, P, P, P]
         L.adi_get_fields_device.argtypes = [H, P, P, P]
@@ -114,7 +115,7 @@ def lib():
 
 EXPORTS = ["adi_create", "adi_create_batch", "adi_set_param", "adi_set_stream", "adi_set_fields",
            "adi_set_fields_device", "adi_set_source", "adi_set_point_sources", "adi_set_boundary",
-           "adi_set_media", "adi_create_dist", "adi_nccl_unique_id", "adi_dist_bands", "adi_step", "adi_step_begin", "adi_step_rows", "adi_step_cols", "adi_step_end", "adi_set_band",
+           "adi_set_media", "adi_create_dist", "adi_nccl_unique_id", "adi_dist_bands", "adi_plan_halo", "adi_step", "adi_step_begin", "adi_step_rows", "adi_step_cols", "adi_step_end", "adi_set_band",
            "adi_band_info", "adi_halo_bytes", "adi_halo_pack", "adi_halo_unpack",
            "adi_get_fields", "adi_get_fields_device", "adi_set_fields_async", "adi_get_fields_async", "adi_get_stats", "adi_get_kernel_times",
            "adi_set_trace", "adi_get_last_sweeps", "adi_last_error",
@@ -173,6 +174,13 @@ def adi_dist_bands(npos, nranks):
     cuts = np.zeros(nranks + 1, dtype=np.int32)
     _check(None, lib().adi_dist_bands(npos, nranks, _ptr(cuts)), "adi_dist_bands")
     return [int(x) for x in cuts]
+
+
+def adi_plan_halo(method):
+    """Halo positions per band side of the band decomposition (the library's plan)."""
+    v = ctypes.c_int(0)
+    _check(None, lib().adi_plan_halo(method, ctypes.byref(v)), "adi_plan_halo")
+    return int(v.value)
 
 
 def adi_set_param(hd, key, value):

@@ -34,6 +34,15 @@ constexpr int TM = 32;     // points per thread chunk
 constexpr int NW = 4;      // lines (warps) per CTA: S' is written in 32-byte runs
 constexpr int TCH = 32;    // chunks per line segment (one per lane)
 
+// segment halo of the line tiles and of the band decomposition
+#ifndef ADI_HALO_CFD
+#define ADI_HALO_CFD 56
+#endif
+#ifndef ADI_HALO_MFD
+#define ADI_HALO_MFD 28
+#endif
+inline int plan_halo(int method) { return method == ADI_CFD ? ADI_HALO_CFD : ADI_HALO_MFD; }
+
 struct Axis {
   int n = 0;            // cells along the sweep direction
   int nlines = 0;       // interior pressure lines of the grid
@@ -95,6 +104,8 @@ struct adi_ctx {
   // kernel of a call, Sa its S1; carry_valid: the next call may skip its prologue
   double* W3 = nullptr;
   bool carry_valid = false;
+  bool call_carry = false;   // this call ends with the carry kernel (decided by adi_step_begin)
+  int call_K = 8;            // K of the call in progress (the stopping rule's buffer size)
   int carry_on = 1;     // ADI_CARRY
   double* phi = nullptr;    // source pattern, S layout (row-major)
   double* phiT = nullptr;   // its transpose (column sweep)
@@ -514,13 +525,7 @@ bool plan_axis(adi::Axis& A, int method, int cap, int lo_all, int hi_all) {
   const int M = adi::TM;
   const int chmax = cap > 0 ? std::min(cap, adi::TCH) : adi::TCH;
   const int P = A.n + 1;                       // positions 0..n
-#ifndef ADI_HALO_CFD
-#define ADI_HALO_CFD 56
-#endif
-#ifndef ADI_HALO_MFD
-#define ADI_HALO_MFD 28
-#endif
-  const int halo = (method == ADI_CFD) ? ADI_HALO_CFD : ADI_HALO_MFD;
+  const int halo = adi::plan_halo(method);
   A.halo = halo;
   A.segs.clear();
   lo_all = std::max(lo_all, 0);
@@ -866,18 +871,19 @@ adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
 // exit at once, so the outputs are those of the chosen k (the stage's inputs are
 // never overwritten).
 int stage_with_rule(adi_ctx* h, int mode_t, const adi::Axis& A, adi::KParams p, int kind, int which) {
-  double* norms = h->d_norms + (size_t)which * 2 * (h->K + 1);
-  CUDA_TRY(h, cudaMemsetAsync(norms, 0, sizeof(double) * 2 * (h->K + 1), h->stream));
+  const int K = h->call_K;   // d_norms was sized by adi_step_begin for this K
+  double* norms = h->d_norms + (size_t)which * 2 * (K + 1);
+  CUDA_TRY(h, cudaMemsetAsync(norms, 0, sizeof(double) * 2 * (K + 1), h->stream));
   CUDA_TRY(h, cudaMemsetAsync(h->d_k + 2 + which, 0, sizeof(int), h->stream));
   p.Kdev = nullptr;
   p.gate = h->d_k + 2 + which;
-  for (int k = h->kmin; k <= h->K; ++k) {
+  for (int k = h->kmin; k <= K; ++k) {
     adi::KParams q = p;
     q.K = k;
     q.norms = norms + 2 * k;
     int rc = launch(h, mode_t, A, q, kind);
     if (rc) return rc;
-    adi::decide_sweeps_kernel<<<1, 1, 0, h->stream>>>(norms + 2 * k, h->eps, k, h->K,
+    adi::decide_sweeps_kernel<<<1, 1, 0, h->stream>>>(norms + 2 * k, h->eps, k, K,
                                                         h->d_k + 2 + which, h->d_k + which);
     CUDA_TRY(h, cudaGetLastError());
     h->launches++;
@@ -1027,6 +1033,11 @@ int adi_set_param(adi_handle h, int key, double v) {
   DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
   h->err.clear();
+  // keys that size or plan work already enqueued by adi_step_begin (the stopping rule's
+  // norm buffer, the tile plan, the carry buffer) cannot change inside a call
+  if (h->in_call && (key == ADI_K_SWEEPS || key == ADI_EPS || key == ADI_K_MIN || key == ADI_TILE_CHUNKS ||
+                     key == ADI_CARRY || key == ADI_RHO))
+    return fail(h, ADI_ESTATE, "call in progress");
   if (key == ADI_K_SWEEPS) {
     if (!(v >= 1) || v != std::floor(v) || v > 1000) return fail(h, ADI_EINVAL, "K must be an integer >= 1");
     h->K = (int)v;
@@ -1362,6 +1373,15 @@ int adi_step_begin(adi_handle h, int nsteps) {
     if (!h->d_k) CUDA_TRY(h, cudaMalloc(&h->d_k, 4 * sizeof(int)));
   }
   int rc;
+  // carry mode: the buffer the last column kernel writes the next step's W* into is
+  // allocated here, before any launch of the call; without it the call ends with the
+  // plain FINAL kernel (call_carry = false) instead of failing half way
+  h->call_carry = carry_ok(h);
+  if (h->call_carry && !h->W3 && !(h->W3 = dalloc((size_t)h->batch * h->aW))) {
+    h->call_carry = false;
+    h->carry_valid = false;
+  }
+  h->call_K = h->K;
   if (h->carry_valid && carry_ok(h)) {
     // the previous call's last column kernel left S1 in Sa and W* in W3
     h->carry_valid = false;
@@ -1414,10 +1434,10 @@ int adi_step_cols(adi_handle h) {
   p.gb = tabv(h->gb, 2 * m + 2);
   p.gf = tabv(h->gf, 2 * m + 2);
   int rc;
-  if (last && carry_ok(h)) {
+  if (last && h->call_carry) {
     // a regular column kernel (S1, W* of step m+1 into Sa, W3) that also writes
     // U^{m+1} and W̄^{m+1}; the three W buffers rotate: W = W̄^{m+1}, W3 = W*, W2 = free
-    if (!h->W3 && !(h->W3 = dalloc((size_t)h->batch * h->aW))) return fail(h, ADI_ENOMEM, "carry buffer");
+    // (W3 was allocated by adi_step_begin)
     double* in = h->Wcur;
     double* outW = nullptr;
     double* outC = nullptr;
@@ -1517,6 +1537,14 @@ int adi_set_band(adi_handle h, int y0, int y1) {
   const int ny_pos = h->ay.n + 1;  // y positions 0..n_y
   if (y0 < 0 || y1 > ny_pos || y0 >= y1) return fail(h, ADI_EINVAL, "band out of range");
   if (h->full) return fail(h, ADI_EINVAL, "no band decomposition for the full-matrix variant");
+  if (h->dist && h->nranks > 1)
+    return fail(h, ADI_EINVAL, "the band of an adi_create_dist handle is fixed at creation");
+  // validated before any state changes (a refused band leaves the handle as it was)
+  const int hl = h->ay.halo;
+  if ((y0 > 0 && y1 - y0 < hl) || (y1 < ny_pos && y1 - y0 < hl))
+    return fail(h, ADI_EINVAL, "band thinner than the halo");
+  const adi::Axis ax_old = h->ax, ay_old = h->ay;
+  const int b0_old = h->band_y0, b1_old = h->band_y1;
   h->band_y0 = y0;
   h->band_y1 = y1;
   // row sweep: interior rows (lines = y positions 1..nyi) inside [y0, y1)
@@ -1525,11 +1553,20 @@ int adi_set_band(adi_handle h, int y0, int y1) {
   // column sweep: outputs at y positions [y0, y1)
   h->ay.o0 = y0;
   h->ay.o1 = y1;
+  h->ay.d_segs = nullptr;   // setup_axis allocates a new plan; the old one is kept until it succeeds
+  h->ay.d_tabU = h->ay.d_tabX = nullptr;
   int rc = setup_axis(h, h->ay, h->ny - 1, h->nxi, 4);
-  if (rc) return rc;
-  const int hl = h->ay.halo;
-  if ((y0 > 0 && y1 - y0 < hl) || (y1 < ny_pos && y1 - y0 < hl))
-    return fail(h, ADI_EINVAL, "band thinner than the halo");
+  if (rc) {
+    for (void* q : {(void*)h->ay.d_segs, (void*)h->ay.d_tabU, (void*)h->ay.d_tabX})
+      if (q) cudaFree(q);
+    h->ax = ax_old;
+    h->ay = ay_old;
+    h->band_y0 = b0_old;
+    h->band_y1 = b1_old;
+    return rc;
+  }
+  for (void* q : {(void*)ay_old.d_segs, (void*)ay_old.d_tabU, (void*)ay_old.d_tabX})
+    if (q) cudaFree(q);
   return ADI_OK;
 }
 
@@ -1644,6 +1681,12 @@ static int dist_exchange(adi_ctx* h, int kind) {
     int rc = halo_copy(h, kind, a, b, h->hbuf[kind][side][1], 1);
     if (rc) return rc;
   }
+  return ADI_OK;
+}
+
+int adi_plan_halo(int method, int* halo) {
+  if (!halo || (method != ADI_CFD && method != ADI_MFD)) return ADI_EINVAL;
+  *halo = adi::plan_halo(method);
   return ADI_OK;
 }
 

@@ -20,7 +20,10 @@ from adi_inputs import CFD, MFD
 from paper_2006_07583_b200.dist import (HIGH, LOW, TorchDistTransport, band_partition,
                                         neighbours)
 
-HALO = {CFD: 64, MFD: 32}
+def shipped_halo(method):
+    """The halo the library's band plan uses (adi_plan_halo, host logic: no GPU needed)."""
+    import paper_2006_07583_b200 as adi
+    return adi.adi_plan_halo(method)
 
 
 @pytest.mark.parametrize("npos,world,halo", [(301, 2, 64), (1602, 4, 64), (16384, 8, 64),
@@ -64,7 +67,7 @@ def _worker(rank, world, port, method, n, results):
         gB, gT = 0.3, -0.7
         Sref, Xref = _half_step_column(method, n, h, K, alpha, beta, s_full, w_full, gB, gT, f_full)
         # this rank's band of y positions and its halo
-        halo = HALO[method]
+        halo = shipped_halo(method)
         bands = band_partition(n + 1, world, halo)
         y0, y1 = bands[rank]
         lo, hi = max(y0 - halo, 0), min(y1 + halo, n + 1)
@@ -110,6 +113,7 @@ def test_band_halo_exchange_gloo(method):
     results = mgr.dict()
     port = 29500 + 7 * method + os.getpid() % 500
     mp.spawn(_worker, args=(world, port, method, n, results), nprocs=world, join=True)
+    assert shipped_halo(method) == (56 if method == CFD else 28)
     for r in range(world):
         ex, es, whole = results[r]
         assert ex < 1e-14 and es < 1e-14, (r, ex, es)

@@ -8,6 +8,8 @@ import pytest
 
 import oracle
 
+from parity import assert_parity, rel  # noqa: E402,F401  (rel L2 + rel max)
+
 pytestmark = pytest.mark.gpu
 TOL = 1e-12
 
@@ -48,18 +50,6 @@ def run_gpu(adi, q, split, nb=0, a=0.015, src=None, K=8):
 def run_oracle(q, steps, nb=0, a=0.015, src=None, K=8):
     return oracle.run_full(q["nx"], q["ny"], q["h"], q["dt"], 1.0, K, q["U"], q["V"], q["W"], phi=q["phi"],
                            gf=q["gf"], src=src, nsteps=steps, nb=nb, a=a)
-
-
-def rel(a, b):
-    nb = np.linalg.norm(b)
-    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
-
-
-def assert_parity(g, o, what=""):
-    for name, a, b in zip("UVW", g, o):
-        assert a.shape == b.shape, (name, a.shape, b.shape)
-        r = rel(a, b)
-        assert r <= TOL, f"{what} {name}: rel L2 {r:.3e}"
 
 
 @pytest.mark.parametrize("n,steps", [(21, 4), (41, 3), (333, 2)])

@@ -1,5 +1,6 @@
 """GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py
-times: element by element against the oracle, relative L2 <= 1e-12 per field.
+times: element by element against the oracle, relative L2 <= 1e-12 and relative
+max-norm <= 1e-11 per field (tests/parity.py).
 
 * config 4: the single 16384^2-node grid of the Γ = 0 harmonic MMS (eq. 11,
   PAPER.md:399-407), K = 8, default tiling, both methods, 2 steps in one call (the
@@ -16,6 +17,7 @@ import pytest
 
 import oracle
 from adi_inputs import CFD, MFD, MMS, mms_problem, ricker_problem
+from parity import check
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 TOL = 1e-12
@@ -29,11 +31,6 @@ def adi():
     import paper_2006_07583_b200 as m
     m.lib()
     return m
-
-
-def rel(a, b):
-    nb = np.linalg.norm(b)
-    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
 def host_gb():
@@ -58,8 +55,7 @@ def test_config4_parity_16384(adi, method):
                    **p.oracle_kwargs())
     for name, a, b in zip("UVW", g, o):
         assert np.isfinite(a).all()
-        r = rel(a, b)
-        assert r <= TOL, f"config4 {('CFD', 'MFD')[method]} {name}: rel L2 {r:.3e}"
+        check(a, b, what=f"config4 {('CFD', 'MFD')[method]}", name=name)
 
 
 def test_config5_shot0_parity_4096(adi):
@@ -76,16 +72,20 @@ def test_config5_shot0_parity_4096(adi):
                    **p0.oracle_kwargs())
     assert np.abs(o[0]).max() > 0
     for name, a, b in zip("UVW", (U[0], V[0], W[0]), o):
-        r = rel(a, b)
-        assert r <= TOL, f"config5 shot 0 {name}: rel L2 {r:.3e}"
-    # the other shots (no oracle run each): finite, the same energy as shot 0 to 1e-6
-    # (the same wave shifted along x, far from the side walls at this horizon: 100 steps
-    # at cfl 0.81 travel 81 cells, the nearest side wall is >= 400 cells away), and
-    # centred on their own source column
-    e0 = np.linalg.norm(U[0])
+        check(a, b, what="config5 shot 0", name=name)
+    # the other shots (no oracle run each): the step is translation invariant away from
+    # the walls, so shot j is shot 0 moved by its source offset d = ix_j - ix_0 columns.
+    # Checked in max-norm on a 701-column window around each source (100 steps at cfl
+    # 0.81 travel 81 cells; the window stays >= 60 cells from the side walls, ~270 cells
+    # beyond the wavefront, where the implicit sweeps' tails are far below round-off)
+    ix0 = probs[0].src[0]
+    c0, c1 = ix0 - 350, ix0 + 351
+    assert c0 >= 60
     for j in range(1, B):
+        d = probs[j].src[0] - ix0
+        assert probs[j].src[1] == probs[0].src[1] and c1 + d <= n - 60
         assert np.isfinite(U[j]).all()
-        assert abs(np.linalg.norm(U[j]) / e0 - 1) < 1e-6, f"shot {j} energy"
-        col = np.abs(U[j]).max(axis=0)
-        ix = probs[j].src[0]
-        assert col[ix - 120:ix + 121].max() == col.max(), f"shot {j} wave off its source"
+        for name, a, b in (("U", U[j][:, c0 + d:c1 + d], U[0][:, c0:c1]),
+                           ("V", V[j][:, c0 + d:c1 + d], V[0][:, c0:c1]),
+                           ("W", W[j][:, c0 + d:c1 + d], W[0][:, c0:c1])):
+            check(a, b, what=f"config5 shot {j} = shot 0 shifted by {d}", name=name)

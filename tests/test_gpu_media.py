@@ -13,6 +13,8 @@ import oracle
 from adi_inputs import CFD, MFD, random_problem
 from adi_inputs.media import MediumMMS, medium_error, medium_mms_problem
 
+from parity import assert_parity, rel  # noqa: E402,F401  (rel L2 + rel max)
+
 pytestmark = pytest.mark.gpu
 TOL = 1e-12
 
@@ -39,17 +41,6 @@ def run_gpu(adi, p, nsteps, split=None):
     out = s.get_fields()
     s.close()
     return out
-
-
-def rel(a, b):
-    nb = np.linalg.norm(b)
-    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
-
-
-def assert_parity(g, o, tol=TOL, what=""):
-    for name, a, b in zip("UVW", g, o):
-        r = rel(a, b)
-        assert r <= tol, f"{what} {name}: rel L2 {r:.3e}"
 
 
 @pytest.mark.parametrize("method", [CFD, MFD])

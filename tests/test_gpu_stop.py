@@ -8,6 +8,8 @@ import pytest
 import oracle
 from adi_inputs import CFD, MFD, random_problem
 
+from parity import check, rel  # noqa: E402,F401  (rel L2 + rel max)
+
 pytestmark = pytest.mark.gpu
 
 
@@ -19,10 +21,6 @@ def adi():
     import paper_2006_07583_b200 as m
     m.lib()
     return m
-
-
-def rel(a, b):
-    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
 
 @pytest.mark.parametrize("method", [CFD, MFD])
@@ -57,7 +55,7 @@ def test_stopping_rule_matches_oracle(adi, method, n):
     s.close()
     assert kmin < info["k"][0, 0] < K           # the rule actually stopped early
     for name, a, b in zip("UVW", g, o):
-        assert rel(a, b) <= 1e-12, (name, rel(a, b))
+        check(a, b, name=name)
 
 
 def test_eps_zero_reports_fixed_sweeps(adi):
