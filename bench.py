@@ -57,6 +57,15 @@ def parse():
                     help="config 5: Ricker point-source shots, MFD, a batch of --shots-per-gpu "
                          "4096^2 grids per rank (weak scaling, no collective)")
     ap.add_argument("--shots-per-gpu", type=int, default=8)
+    ap.add_argument("--config", type=int, default=0, choices=[0, 1, 2, 3],
+                    help="BASELINE.json configs 1-3 (the paper's own experiments, PAPER.md:395-407): "
+                         "1 = CFD 41^2, 200 steps; 2 = the MFD ladder 41..321 to 5T; 3 = Gamma=k in {2, 9} at "
+                         "1601^2, CFD and MFD, 100 timed steps.  One JSON line; 0 = config 4 (the default)")
+    ap.add_argument("--no-graph", action="store_true", help="configs 1-3: plain launches instead of ADI_GRAPH")
+    ap.add_argument("--dist-local", type=int, default=0,
+                    help="P > 1: the grid band-decomposed over P ranks of adi_create_dist_local on ONE GPU "
+                         "(the library's multi-GPU code path with a loopback transport; a functional check "
+                         "of the decomposition's overheads, not a scaling number)")
     return ap.parse_args()
 
 
@@ -247,12 +256,49 @@ def kernel_flops(method, n, kind, K):
     return 0
 
 
+class LocalRanks:
+    """The ranks of adi_create_dist_local as one solver (bench.py --dist-local P)."""
+
+    def __init__(self, adi, p, m, P, K, stream):
+        self.adi = adi
+        hs = adi.adi_create_dist_local(p.nx, p.ny, p.h, p.dt, p.c, m, 1, P)
+        self.hs = hs
+        self.ranks = [adi.AdiSolver.adopt(h, p.nx, p.ny, p.h, p.dt, p.c, m, K=K, stream=stream) for h in hs]
+        self.handle = hs[0]
+
+    def __getattr__(self, name):   # set_fields, set_source, set_boundary, set_media, set_param
+        def f(*args, **kw):
+            for r in self.ranks:
+                getattr(r, name)(*args, **kw)
+        return f
+
+    def step(self, k):
+        self.adi.adi_step_dist_local(self.hs, k)
+
+    def stats(self):
+        st = [r.stats() for r in self.ranks]
+        return {"kernel_launches": sum(x["kernel_launches"] for x in st),
+                "device_bytes": max(x["device_bytes"] for x in st)}
+
+    def kernel_times(self):
+        out = {}
+        for r in self.ranks:
+            for k, (ms, cnt) in r.kernel_times().items():
+                a, b = out.get(k, (0.0, 0))
+                out[k] = (a + ms, b + cnt)
+        return out
+
+    def close(self):
+        for r in self.ranks:
+            r.close()
+
+
 def run_ours(a, ws, rank, local):
-    """N = 1: one grid per method.  N > 1: the same grid band-decomposed over the
-    ranks (NCCL halo exchange through torch.distributed)."""
+    """N = 1: one grid per method.  N > 1: the same grid band-decomposed over the ranks
+    through the library's own multi-GPU entry (adi_create_dist: band-local arrays, the
+    NCCL halo exchange inside adi_step overlapping the column sweep)."""
     import torch
     import paper_2006_07583_b200 as adi
-    from paper_2006_07583_b200 import dist as adist
 
     torch.cuda.set_device(local)
     stream = torch.cuda.current_stream()
@@ -260,9 +306,21 @@ def run_ours(a, ws, rank, local):
     n = a.n
     total_steps = a.warmup + a.steps
     solvers = {}
+    uid = None
+    if ws > 1:
+        import torch.distributed as tdist
+        box = [adi.adi_nccl_unique_id() if rank == 0 else None]
+        tdist.broadcast_object_list(box, src=0)
+        uid = box[0]
     for m in methods:
         p = make_problem(m, n, total_steps + a.steps + 4, a.K, a.media)
-        s = adi.AdiSolver(p.nx, p.ny, p.h, p.dt, p.c, m, K=a.K, stream=stream.cuda_stream)
+        if ws > 1:
+            hd, st = adi.adi_create_dist(p.nx, p.ny, p.h, p.dt, p.c, m, 1, uid, rank, ws)
+            s = adi.AdiSolver.adopt(hd, p.nx, p.ny, p.h, p.dt, p.c, m, K=a.K, stream=stream.cuda_stream, status=st)
+        elif a.dist_local > 1:
+            s = LocalRanks(adi, p, m, a.dist_local, a.K, stream.cuda_stream)
+        else:
+            s = adi.AdiSolver(p.nx, p.ny, p.h, p.dt, p.c, m, K=a.K, stream=stream.cuda_stream)
         s.set_fields(p.U, p.V, p.W)
         s.set_source(p.phi, p.src, p.gf)
         s.set_boundary(p.edges, p.gb)
@@ -278,22 +336,17 @@ def run_ours(a, ws, rank, local):
         p.rows = (0, p.U.shape[0])
         if ws > 1:
             y0, y1, halo, npos = adi.adi_band_info(s.handle)
-            bs = adist.BandSolver(s, rank, ws, adist.band_partition(npos, ws, halo))
+            bs = {"y0": y0, "y1": y1, "halo": halo, "npos": npos}
             # a banded handle transfers only the rows it uses (adi_set_fields, include/adi.h):
             # keep just those rows of U for the e2e leg
-            ya = max(bs.y0 - bs.halo, 0)
-            yb = p.U.shape[0] if bs.y1 >= bs.npos else min(bs.y1 + bs.halo, p.U.shape[0])
+            ya = max(y0 - halo, 0)
+            yb = p.U.shape[0] if y1 >= npos else min(y1 + halo, p.U.shape[0])
             p.rows = (ya, yb)
             p.U = p.U[ya:yb].copy()
         solvers[m] = (s, p, bs)
-    transport = adist.TorchDistTransport(rank, ws) if ws > 1 else None
 
     def run(m, k):
-        s, p, bs = solvers[m]
-        if bs is None:
-            s.step(k)
-        else:
-            adist.step_distributed(bs, transport, k)
+        solvers[m][0].step(k)   # adi_step: collective over the ranks of an adi_create_dist grid
 
     for m in solvers:
         run(m, a.warmup)
@@ -324,8 +377,7 @@ def run_ours(a, ws, rank, local):
         s.set_param(adi.ADI_TIMING, 0)
     pts = n * n
     total_ms = sum(per.values())
-    scale = 1 if ws == 1 else 1   # strong scaling: one grid in total
-    value = scale * pts * a.steps * len(methods) / (total_ms * 1e-3)
+    value = pts * a.steps * len(methods) / (total_ms * 1e-3)   # strong scaling: one grid in total
     peak, peak_src = measured_peaks()
     traffic = ncu_traffic()
     per_method = {}
@@ -335,7 +387,8 @@ def run_ours(a, ws, rank, local):
         step_ms = per[m] / a.steps
         tot = sum(v[0] for v in ksum.values())
         kind, (kms, kcnt) = max(ksum.items(), key=lambda kv: kv[1][0])
-        byt = kernel_bytes(m, n, kind, media=a.media) / ws
+        shards = ws if ws > 1 else max(a.dist_local, 1)   # grid shares of one launch
+        byt = kernel_bytes(m, n, kind, media=a.media) / shards
         ach = byt / (kms / kcnt * 1e-3) / 1e9
         bytes_step = (kernel_bytes(m, n, "row", media=a.media) + kernel_bytes(m, n, "col", media=a.media)) / ws
         per_method[MNAME[m]] = {
@@ -346,7 +399,7 @@ def run_ours(a, ws, rank, local):
             "kernel_avg_ms": {k: v[0] / v[1] for k, v in ksum.items()},
             "dominant": kind}
         cand = {"method": MNAME[m], "kind": kind, "achieved": ach, "bytes": byt, "share": kms / tot,
-                "avg_ms": kms / kcnt, "cnt": kcnt, "flops": kernel_flops(m, n, kind, a.K) / ws}
+                "avg_ms": kms / kcnt, "cnt": kcnt, "flops": kernel_flops(m, n, kind, a.K) / shards}
         if dominant is None or cand["avg_ms"] * kcnt > dominant["avg_ms"] * dominant["cnt"]:
             dominant = cand
     tkey = f"{dominant['method']}_{dominant['kind']}_{n}" + ("_media" if a.media else "")
@@ -364,7 +417,7 @@ def run_ours(a, ws, rank, local):
                  "peak_source": "measured (profiles/r01/fp64_probe.txt, independent DFMA streams)"}
     # ---- end to end through the C-ABI with host buffers (pinned), copies timed
     e2e = None
-    if not a.no_e2e and ws == 1:
+    if not a.no_e2e and ws == 1 and a.dist_local <= 1:
         # One GPU: both problems through the async C-ABI calls, each handle on its own
         # stream, so the copies of one overlap the steps of the other (and H2D / D2H
         # overlap each other).  Pinned host buffers; one host wait at the end.
@@ -402,7 +455,7 @@ def run_ours(a, ws, rank, local):
                "note": "adi_set_fields_async(pinned host) + adi_step(K) + adi_get_fields_async(pinned host) "
                        "per method, the two methods on two streams (copies overlap the other "
                        "method's steps), host wall clock from the first copy to the last result"}
-    elif not a.no_e2e:
+    elif not a.no_e2e and ws > 1:
         e2e_ms = 0.0
         bi = bo = 0
         for m, (s, p, bs) in solvers.items():
@@ -415,14 +468,12 @@ def run_ours(a, ws, rank, local):
             hU[ya:yb] = p.U
             nrow = lambda shp, a0, b0: max(min(b0, shp[0]) - max(a0, 0), 0) * shp[1] * 8
             nbi = nrow(su, ya, yb) + nrow(sv, ya - 1, yb - 1) + nrow(sw, ya, yb)
-            ga, gb = bs.y0, (su[0] if bs.y1 >= bs.npos else bs.y1)
+            ga, gb = bs["y0"], (su[0] if bs["y1"] >= bs["npos"] else bs["y1"])
             nbo = nrow(su, ga, gb) + nrow(sv, ga - 1, gb - 1) + nrow(sw, ga, gb)
             barrier(ws)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             adi.adi_set_fields(s.handle, hU, hV, hW)   # H2D
-            if bs is not None:
-                bs.fresh = True
             run(m, a.steps)
             adi.adi_get_fields(s.handle, oU, oV, oW)   # D2H, synchronizes
             t1 = time.perf_counter()
@@ -580,6 +631,39 @@ def cpu_cores():
         return os.cpu_count()
 
 
+def cpu_model():
+    """lscpu-style model name of the host (SURVEY §8d asks for it beside the oracle's rate)."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def cpu_leg(rate_fn, budget_s=8.0, max_steps=12):
+    """The oracle timed on the host at all cores and at 1 thread (the
+    paper's sequential-C++ / OpenMP analogue), each on a bounded
+    sample: ``rate_fn(steps, threads) -> (rate, seconds)``; the step count of each leg
+    is sized from a 1-step probe so that it takes about ``budget_s`` seconds."""
+    nthr = cpu_cores()
+    res = {}
+    for name, thr in (("all", nthr), ("one", 1)):
+        r1, s1 = rate_fn(1, thr)
+        steps = int(max(1, min(max_steps, budget_s / max(s1, 1e-3))))
+        rate, secs = (r1, s1) if steps == 1 else rate_fn(steps, thr)
+        res[name] = (rate, secs, steps)
+    return nthr, res
+
+
 def main_shots(a, ws, rank, local):
     """bench.py --shots: config 5, weak scaling over ranks."""
     B = a.shots_per_gpu
@@ -612,18 +696,153 @@ def main_shots(a, ws, rank, local):
     if not a.no_cpu and ws == 1:
         import oracle
         oracle.build()
-        nthr = cpu_cores()
-        rate, secs = oracle_rate_shots(1, 12, a.K, nthr)
+        nthr, res = cpu_leg(lambda st, thr: oracle_rate_shots(1, st, a.K, thr))
+        (rate, secs, st), (r1, s1, st1) = res["all"], res["one"]
         cpu = {"value": rate, "unit": UNIT, "cores": nthr, "kind": "oracle",
-               "sample": f"shot 0, 12 steps ({secs:.1f} s of CPU time)"}
+               "sample": f"shot 0, {st} steps ({secs:.1f} s)",
+               "single_thread": {"value": r1, "unit": UNIT, "cores": 1, "sample": f"shot 0, {st1} steps ({s1:.1f} s)"},
+               "cpu_model": cpu_model(), "nproc": os.cpu_count()}
     print(json.dumps({**common, "value": r["value"], "ms_per_step": r["ms_per_step"],
                       "roofline": r["roofline"], "roofline_fp64": r["roofline_fp64"], "cpu_baseline": cpu,
                       "clocks": r["clocks"], "e2e": r["e2e"], "gpu_launches": r["gpu_launches"],
                       "per_method": r["per_method"]}))
 
 
+T_PERIOD = 1.0 / math.sqrt(2.0)   # the harmonic test's period T
+
+
+def config_cases(a):
+    """(label, problem, timed steps) of BASELINE.json configs 1-3."""
+    from adi_inputs import CFD, MFD, MMS, mms_problem
+    if a.config == 1:
+        return [("cfd41", mms_problem(CFD, 41, MMS(), steps=200, K=a.K), 200)]
+    if a.config == 2:
+        out = []
+        for nx in (41, 81, 161, 321):
+            p = mms_problem(MFD, nx, MMS(), t_sim=5 * T_PERIOD, K=a.K)
+            out.append((f"mfd{nx}", p, p.meta["steps"]))
+        return out
+    steps = a.steps if a.steps != 20 else 100
+    out = []
+    for gk in (2, 9):
+        for m, name in ((CFD, "cfd"), (MFD, "mfd")):
+            p = mms_problem(m, 1601, MMS(gamma=float(gk), k=gk), steps=steps + 2 + 4, K=a.K)
+            out.append((f"{name}1601_gk{gk}", p, steps))
+    return out
+
+
+def main_config(a):
+    """bench.py --config {1,2,3}: the paper's own experiments, timed on the GPU (with
+    ADI_GRAPH: one launch per call) beside the CPU oracle on the same full runs."""
+    import torch
+    import oracle
+    import paper_2006_07583_b200 as adi
+    from adi_inputs.mms import interior_error
+    torch.cuda.set_device(0)
+    stream = torch.cuda.current_stream()
+    cases = config_cases(a)
+    graph = 0 if a.no_graph else 1
+    per, tot_pts, tot_ms, launches, hlaunch = [], 0.0, 0.0, 0, 0
+    kt_all = {}
+    with Clocks(0) as clk:
+        for label, p, steps in cases:
+            warm = min(a.warmup, steps) if a.config != 3 else 2
+            # warm-up (JIT-free, but the first launches set attributes) on a separate handle
+            w = adi.AdiSolver.from_problem(p, stream=stream.cuda_stream)
+            w.set_param(adi.ADI_GRAPH, graph)
+            w.step(max(warm, 1))
+            w.close()
+            s = adi.AdiSolver.from_problem(p, stream=stream.cuda_stream)
+            s.set_param(adi.ADI_GRAPH, graph)
+            if a.config == 3:
+                s.step(2)          # the two warm-up steps of SURVEY §8d item 3
+            s.set_param(adi.ADI_TIMING, 1)
+            s.kernel_times()
+            st0 = s.stats()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            s.step(steps)
+            e1.record(stream)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            st1 = s.stats()
+            kt = {k: v for k, v in s.kernel_times().items() if v[1] > 0}
+            for k, v in kt.items():
+                x = kt_all.setdefault((label, k), [0.0, 0])
+                x[0] += v[0]
+                x[1] += v[1]
+            U, V, W = s.get_fields()
+            s.close()
+            m0 = 2 if a.config == 3 else 0
+            err = interior_error(p, U, (m0 + steps) * p.dt)
+            # the oracle on the same full run (all host cores), parity of the final state
+            t0 = time.perf_counter()
+            o = oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, p.U, p.V, p.W, nsteps=m0 + steps,
+                           nthreads=cpu_cores(), **p.oracle_kwargs())
+            osec = time.perf_counter() - t0
+            rel = float(np.linalg.norm(U - o[0]) / np.linalg.norm(o[0]))
+            pts = p.nx * p.ny
+            per.append({"case": label, "nodes": p.nx, "steps": steps, "ms": ms, "value": pts * steps / (ms * 1e-3),
+                        "kernel_launches": st1["kernel_launches"] - st0["kernel_launches"],
+                        "host_launches": st1["host_launches"] - st0["host_launches"],
+                        "error_frobenius_interior_U": err, "t_end": (m0 + steps) * p.dt,
+                        "parity_rel_l2_U_vs_oracle": rel,
+                        "oracle_s_all_cores": osec, "oracle_value_all_cores": pts * (m0 + steps) / osec})
+            tot_pts += pts * steps
+            tot_ms += ms
+            launches += per[-1]["kernel_launches"]
+            hlaunch += per[-1]["host_launches"]
+    if a.config == 2:
+        from adi_inputs.rates import estimate_rates
+        rates = estimate_rates([c["error_frobenius_interior_U"] for c in per], [c["nodes"] - 1 for c in per])
+        for c, r in zip(per[1:], rates):
+            c["rate"] = r
+    # roofline of the dominant kernel kind (algorithmic bytes, DESIGN.md §5.5)
+    peak, peak_src = measured_peaks()
+    (lab, kind), (kms, kcnt) = max(kt_all.items(), key=lambda kv: kv[1][0])
+    pcase = next(p for l, p, _ in cases if l == lab)
+    byt = kernel_bytes(pcase.method, pcase.nx, kind)
+    ach = byt / (kms / kcnt * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+            "traffic": None, "kernel": f"adi_line_kernel[{lab},{kind}]", "algorithmic_bytes_per_launch": byt,
+            "peak_source": peak_src, "avg_launch_ms": round(kms / kcnt, 5),
+            "note": ("working set < 1 MB: L1/L2-resident and latency-bound (the K-sweep recurrences), not HBM-bound"
+                     if a.config in (1, 2) else
+                     "working set ~100 MB per method: L2-resident between half-steps; lts bytes in profiles/")}
+    # the oracle on the host: all cores (the full runs above) and 1 thread (bounded sample)
+    osum = sum(c["oracle_s_all_cores"] for c in per)
+    opts = sum(c["nodes"] ** 2 * (c["steps"] + (2 if a.config == 3 else 0)) for c in per)
+    lab0, p0, st0_ = cases[-1]
+    one_steps = max(1, min(st0_, int(2e7 / (p0.nx * p0.ny))))
+    t0 = time.perf_counter()
+    oracle.run(p0.method, p0.nx, p0.ny, p0.h, p0.dt, p0.c, p0.K, p0.U, p0.V, p0.W, nsteps=one_steps, nthreads=1,
+               **p0.oracle_kwargs())
+    s1 = time.perf_counter() - t0
+    cpu = {"value": opts / osum, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+           "sample": f"the full runs of every case ({osum:.1f} s)",
+           "single_thread": {"value": p0.nx * p0.ny * one_steps / s1, "unit": UNIT, "cores": 1,
+                             "sample": f"{lab0}, {one_steps} steps ({s1:.1f} s)"},
+           "cpu_model": cpu_model(), "nproc": os.cpu_count()}
+    names = {1: "config1: CFD 41x41 nodes, Gamma=0 harmonic MMS (eq. 11), dt = 0.91 h, 200 steps, K = 8",
+             2: "config2: MFD ladder 41/81/161/321 nodes, Gamma=0 harmonic MMS to 5T (cfl 0.81), K = 8",
+             3: "config3: Gamma=k in {2, 9} MMS (severe boundary gradients), 1601x1601 nodes, CFD (cfl 0.91) and "
+                "MFD (cfl 0.81), 2 warm-up + 100 timed steps, K = 8"}
+    line = {"metric": METRIC, "value": tot_pts / (tot_ms * 1e-3), "unit": UNIT, "n_gpus": 1,
+            "steps": sum(c["steps"] for c in per), "warmup": a.warmup, "ms_per_step": tot_ms / sum(c["steps"] for c in per),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": names[a.config], "graph": bool(graph),
+                       "l2": "L2-resident working set (configs 1-3 are the paper's small grids)"},
+            "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
+            "e2e": None, "gpu_launches": launches, "host_launches": hlaunch, "cases": per}
+    print(json.dumps(line))
+
+
 def main():
     a = parse()
+    if a.config:
+        return main_config(a)
     ws, rank, local = dist_setup()
     methods = methods_of(a)
     cfg = {"workload": f"config4: single {a.n}x{a.n}-node grid, Gamma=0 harmonic MMS (eq. 11), "
@@ -631,7 +850,11 @@ def main():
            "grid_nodes": a.n, "methods": [MNAME[m] for m in methods], "K_sweeps": a.K,
            "cfl": {"cfd": 0.91, "mfd": 0.81}, "l2": "inputs larger than L2 (2.1 GB per field); no flush",
            "parallelism": "1 GPU" if ws == 1 else
-           f"{ws} GPUs: one grid band-decomposed (rows), NCCL halo exchange per step"}
+           f"{ws} GPUs: one grid band-decomposed (rows) by adi_create_dist, band-local arrays, NCCL "
+           f"halo exchange inside adi_step overlapping the column sweep"}
+    if a.dist_local > 1:
+        cfg["parallelism"] = (f"1 GPU running {a.dist_local} ranks of adi_create_dist_local (band-local arrays, "
+                              f"loopback halo exchange): the decomposition's overhead, not a scaling number")
     if a.full:
         cfg["workload"] = (f"config4 size: single {a.n}x{a.n}-node grid, full-matrix CFD variant (NEXT row "
                            f"f4, ADI_CFD_FULL: every node unknown, no Dirichlet data) with a Cerjan layer "
@@ -650,6 +873,9 @@ def main():
         oracle.build()
         nthr = cpu_cores()
         n = a.cpu_n
+        cfg = dict(cfg, workload=cfg["workload"] + f"; reference arm = the CPU oracle on a bounded "
+                                                   f"{n}x{n}-node sample of this workload per step",
+                   oracle_sample_nodes=n)
         for _ in range(a.warmup):
             oracle_rate(methods, n, 1, a.K, nthr, a.media)
         rate, secs = oracle_rate(methods, n, a.steps, a.K, nthr, a.media)
@@ -673,11 +899,14 @@ def main():
     if not a.no_cpu and ws == 1:
         import oracle
         oracle.build()
-        nthr = cpu_cores()
-        rate, secs = oracle_rate(methods, a.cpu_n, 12, a.K, nthr, a.media)
+        nthr, res = cpu_leg(lambda st, thr: oracle_rate(methods, a.cpu_n, st, a.K, thr, a.media))
+        (rate, secs, st), (r1, s1, st1) = res["all"], res["one"]
         cpu = {"value": rate, "unit": UNIT, "cores": nthr, "kind": "oracle",
-               "sample": f"{a.cpu_n}x{a.cpu_n} nodes, 12 steps per method, same MMS data "
-                         f"({secs:.1f} s of CPU time)"}
+               "sample": f"{a.cpu_n}x{a.cpu_n} nodes (the config-4 MMS data at a bounded size), {st} steps per "
+                         f"method ({secs:.1f} s)",
+               "single_thread": {"value": r1, "unit": UNIT, "cores": 1,
+                                 "sample": f"{a.cpu_n}x{a.cpu_n} nodes, {st1} steps per method ({s1:.1f} s)"},
+               "cpu_model": cpu_model(), "nproc": os.cpu_count()}
     line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": ws, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,

@@ -121,6 +121,12 @@ enum adi_param {
                            up to rounding order (the one-call computation).  Used for plain
                            handles only (no band / dist, no ADI_EPS, no media, not
                            ADI_CFD_FULL); 0 = always run the prologue */
+  ADI_GRAPH = 11,       /* 1: adi_step(n) captures its kernels (prologue, n x {rows, columns},
+                           Dirichlet columns) into one CUDA graph and launches it: one host
+                           launch per call instead of 2n+2 (short lines are launch-bound, the
+                           paper's own observation).  Same kernels, same
+                           results bit for bit.  Plain and banded handles without ADI_EPS;
+                           ignored for adi_create_dist ranks.  Default 0 */
 };
 
 /* Kernel kinds launched by adi_step (index of adi_get_kernel_times arrays). */
@@ -145,6 +151,11 @@ typedef struct adi_stats {
    * synchronizes the handle's stream) */
   double last_test[2];
   int last_k[2];
+  /* device memory the handle allocated (field arrays with their guards, tables excluded,
+   * halo buffers included): a band of adi_create_dist holds its band + halo rows only */
+  long long device_bytes;
+  /* host-side launches (kernel launches, or one per graph launch with ADI_GRAPH = 1) */
+  long long host_launches;
 } adi_stats;
 
 /* Create a solver for one grid (batch = 1).  nx, ny >= 9 nodes (N >= 8);
@@ -231,15 +242,19 @@ int adi_step_end(adi_handle h);
  * adi_set_band restricts this handle to the y positions [y0, y1) of the pressure
  * grid (0 <= y0 < y1 <= number of y positions): its row sweep processes the
  * interior rows inside the band, its column sweep outputs only positions in
- * the band.  Every handle still holds full-size arrays; only its band (plus
- * halo) is kept current, and adi_set/get_fields move only those rows.  The
- * column sweep plans its tiles over the band's own positions.  Between adi_step_rows and adi_step_cols the halo of
+ * the band.  The handle's arrays are re-laid out to hold the band plus `halo`
+ * positions on each side only (device memory ~ 1/P of the grid): the state rows inside
+ * both the old and the new extent are kept, rows new to the extent are zero (call
+ * adi_set_fields after widening a band).  adi_set/get_fields move only those rows.
+ * The column sweep plans its tiles over the band's own positions.  Between adi_step_rows and adi_step_cols the halo of
  * `halo` positions on each side must be refreshed from the neighbour bands
  * (kind 0: S2 and W*), and before adi_step_begin of every call but the first
  * after adi_set_fields (kind 1: U and W̄).  side 0 = low-y neighbour, 1 = high.
  * adi_halo_pack writes this band's edge positions that the neighbour on `side`
  * needs into a contiguous device buffer of adi_halo_bytes bytes;
- * adi_halo_unpack stores the neighbour's message into this band's halo. */
+ * adi_halo_unpack stores the neighbour's message into this band's halo.
+ * EINVAL: a band thinner than the halo, or the handle of an adi_create_dist (fixed band);
+ * a refused band leaves the handle unchanged. */
 int adi_set_band(adi_handle h, int y0, int y1);
 int adi_band_info(adi_handle h, int* y0, int* y1, int* halo, int* npos);
 
@@ -258,6 +273,18 @@ int adi_band_info(adi_handle h, int* y0, int* y1, int* halo, int* npos);
 int adi_create_dist(int nx, int ny, double h, double dt, double c, int method, int batch,
                     const void* nccl_unique_id, int rank, int nranks, adi_handle* out);
 int adi_nccl_unique_id(void* out128);
+/* All `nranks` ranks of the same decomposition in ONE process on the current device
+ * (out[0..nranks-1]), exchanging through loopback device copies instead of NCCL: the
+ * code path of adi_create_dist (band-local arrays, pack -> transfer -> unpack, the
+ * column sweep's halo-free segments overlapping the transfer) with only the transport
+ * replaced.  For verification on one GPU: the ranks are stepped together by
+ * adi_step_dist_local (adi_step on one of them returns ADI_ESTATE), which runs every
+ * rank's phase before any rank's next one, so no rank's kernel waits on another's.
+ * adi_set/get_fields, adi_get_stats and adi_destroy work per rank as for
+ * adi_create_dist.  Destroy all handles. */
+int adi_create_dist_local(int nx, int ny, double h, double dt, double c, int method, int batch, int nranks,
+                          adi_handle* out);
+int adi_step_dist_local(adi_handle* handles, int nranks, int n);
 /* The band cuts of y positions [0, npos) over nranks: cuts[0..nranks] (host logic only). */
 int adi_dist_bands(int npos, int nranks, int* cuts);
 /* The halo (positions on each side of a band) that the band decomposition of `method`

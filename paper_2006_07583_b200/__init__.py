@@ -42,6 +42,7 @@ ADI_ABSORB_WIDTH = 7
 ADI_ABSORB_RATE = 8
 ADI_PREFETCH = 9
 ADI_CARRY = 10
+ADI_GRAPH = 11
 KERNEL_KINDS = ("prologue", "row", "col", "final", "edge")
 
 _STATUS = {0: "ADI_OK", -1: "ADI_EINVAL", -2: "ADI_ENOMEM", -3: "ADI_ECUDA", -4: "ADI_EZEROPIVOT",
@@ -57,7 +58,8 @@ class AdiError(RuntimeError):
 class adi_stats(ctypes.Structure):
     _fields_ = [("steps", ctypes.c_longlong), ("t", ctypes.c_double), ("nonfinite", ctypes.c_int),
                 ("k_sweeps", ctypes.c_int), ("kernel_launches", ctypes.c_longlong),
-                ("last_test", ctypes.c_double * 2), ("last_k", ctypes.c_int * 2)]
+                ("last_test", ctypes.c_double * 2), ("last_k", ctypes.c_int * 2),
+                ("device_bytes", ctypes.c_longlong), ("host_launches", ctypes.c_longlong)]
 
 
 _lib = None
@@ -87,7 +89,12 @@ def lib():
         L.adi_create_dist.argtypes = [I, I, D, D, D, I, I, P, I, I, ctypes.POINTER(H)]
         L.adi_nccl_unique_id.argtypes = [P]
         L.adi_dist_bands.argtypes = [I, I, P]
-        L.adi_plan_halo.argtypes = [I, ctypes.POINTER(I)]
+        try:   # (absent from libraries built before round 2: tools/ab_lib.py loads those too)
+            L.adi_plan_halo.argtypes = [I, ctypes.POINTER(I)]
+            L.adi_create_dist_local.argtypes = [I, I, D, D, D, I, I, I, ctypes.POINTER(H)]
+            L.adi_step_dist_local.argtypes = [ctypes.POINTER(H), I, I]
+        except AttributeError:
+            pass
         L.adi_step.argtypes = [H, I]
         L.adi_get_fields.argtypes = [H, P, P, P]
         L.adi_get_fields_device.argtypes = [H, P, P, P]
@@ -115,7 +122,7 @@ def lib():
 
 EXPORTS = ["adi_create", "adi_create_batch", "adi_set_param", "adi_set_stream", "adi_set_fields",
            "adi_set_fields_device", "adi_set_source", "adi_set_point_sources", "adi_set_boundary",
-           "adi_set_media", "adi_create_dist", "adi_nccl_unique_id", "adi_dist_bands", "adi_plan_halo", "adi_step", "adi_step_begin", "adi_step_rows", "adi_step_cols", "adi_step_end", "adi_set_band",
+           "adi_set_media", "adi_create_dist", "adi_nccl_unique_id", "adi_dist_bands", "adi_plan_halo", "adi_create_dist_local", "adi_step_dist_local", "adi_step", "adi_step_begin", "adi_step_rows", "adi_step_cols", "adi_step_end", "adi_set_band",
            "adi_band_info", "adi_halo_bytes", "adi_halo_pack", "adi_halo_unpack",
            "adi_get_fields", "adi_get_fields_device", "adi_set_fields_async", "adi_get_fields_async", "adi_get_stats", "adi_get_kernel_times",
            "adi_set_trace", "adi_get_last_sweeps", "adi_last_error",
@@ -167,6 +174,21 @@ def adi_create_dist(nx, ny, h, dt, c, method, batch, unique_id, rank, nranks):
     rc = lib().adi_create_dist(nx, ny, h, dt, c, method, batch, uid, rank, nranks, ctypes.byref(hd))
     _check(None, rc, "adi_create_dist")
     return hd, rc
+
+
+def adi_create_dist_local(nx, ny, h, dt, c, method, batch, nranks):
+    """All ranks of a line-sharded grid in this process on the current device (loopback
+    transport, include/adi.h); returns the list of handles."""
+    hs = (ctypes.c_void_p * nranks)()
+    rc = lib().adi_create_dist_local(nx, ny, h, dt, c, method, batch, nranks, hs)
+    if rc < 0:
+        raise AdiError(rc, f"adi_create_dist_local: {_STATUS.get(rc, rc)}")
+    return [ctypes.c_void_p(x) for x in hs]
+
+
+def adi_step_dist_local(handles, n):
+    hs = (ctypes.c_void_p * len(handles))(*[h.value if isinstance(h, ctypes.c_void_p) else h for h in handles])
+    _check(handles[0], lib().adi_step_dist_local(hs, len(handles), n), "adi_step_dist_local")
 
 
 def adi_dist_bands(npos, nranks):
@@ -364,6 +386,19 @@ class AdiSolver:
         if stream is not None:
             adi_set_stream(self.handle, stream)
         self.su, self.sv, self.sw = shapes(method, nx, ny)
+
+    @classmethod
+    def adopt(cls, handle, nx, ny, h, dt, c, method, *, batch=1, K=8, rho=1.0, stream=None, status=0):
+        """Wrap a handle made elsewhere (adi_create_dist, adi_create_dist_local)."""
+        self = cls.__new__(cls)
+        self.nx, self.ny, self.h, self.dt, self.c, self.method, self.batch = nx, ny, h, dt, c, method, batch
+        self.handle, self.create_status = handle, status
+        adi_set_param(self.handle, ADI_K_SWEEPS, K)
+        adi_set_param(self.handle, ADI_RHO, rho)
+        if stream is not None:
+            adi_set_stream(self.handle, stream)
+        self.su, self.sv, self.sw = shapes(method, nx, ny)
+        return self
 
     def close(self):
         if self.handle:

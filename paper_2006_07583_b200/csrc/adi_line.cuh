@@ -125,6 +125,11 @@ struct KParams {
   // W̄^{m+1} = x_K to X_out2, so the next call needs no prologue; 0 = off
   int carry;
   double* X_out2;
+  // origin of the TMA-staged arrays (band-local arrays): TMA line
+  // coordinate = line - tline0, position coordinate = position - tpos0 (even)
+  int tline0, tpos0;
+  // positions of U present in a band-local array (column sweep): [pos_lo, pos_hi)
+  int pos_lo, pos_hi;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -605,6 +610,18 @@ __device__ __forceinline__ void cfd_statics(const Ctx<M>& c, const EdgeTab& T, i
 #define ADI_NSUB 2
 #endif
 constexpr int NSUB = ADI_NSUB;
+// CFD fix-up truncation: with 32-point sub-chunks the carry responses
+// K_i (i >= 27) and J_i (i <= 3) are below 3e-17 and are not applied
+#ifndef ADI_TRIM
+#define ADI_TRIM 1
+#endif
+constexpr bool TRIM = ADI_TRIM && (32 / NSUB == 32);
+// CFD interior solve: fold the base into the backward sweep (see cfd_apply)
+#ifndef ADI_EARLY_BASE
+#define ADI_EARLY_BASE 1
+#endif
+constexpr bool EARLY_BASE = ADI_EARLY_BASE;
+constexpr int TRIM_K = 27, TRIM_J = 4;
 
 // ===========================================================================
 // CFD: one operator application out = B - coef * T^{-1} r(o) on the warp's
@@ -625,6 +642,9 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
   const int np1 = c.n + 1;
   double yl_e, ws, we;
   double ysub[NSUB];
+  // raw backward values the carries need (interior path): sub-chunk starts, the last
+  // element, the 4 elements at the chunk start / end (line-end Woodbury window)
+  double wsub[NSUB], wlast = 0.0, wzs[4] = {0.0, 0.0, 0.0, 0.0}, wze[4] = {0.0, 0.0, 0.0, 0.0};
   // ---------------- phase 1: local solve with zero carries ----------------
   if (c.interior) {
     if (UOP) Cfd<M>::template rhs_u<true>(c, o, out, om1, op1);
@@ -649,10 +669,45 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
       for (int j = 0; j < NSUB; ++j) out[j * L + i] = fma(-l, out[j * L + i - 1], out[j * L + i]);
 #pragma unroll
     for (int j = 0; j < NSUB; ++j) ysub[j] = out[j * L + L - 1];
+    if constexpr (EARLY_BASE) {
+      // backward sweep with the base folded in as soon as each w_i is final: out_i
+      // becomes t_i = B_i - coef iv w_i (the first term of the fix-up, same rounding
+      // order), so the base loads and these FMAs fill the latency-bound recurrence
+      // instead of stalling the fix-up after the exchange.  The raw w the carries need
+      // (sub-chunk starts, the last element, the line-end window) are kept aside.
+      const double ci = -coef * iv;
+      double wn[NSUB];
 #pragma unroll
-    for (int i = L - 2; i >= 0; --i)
+      for (int j = 0; j < NSUB; ++j) wn[j] = out[j * L + L - 1];
+      wlast = wn[NSUB - 1];
+      wze[3] = wlast;
 #pragma unroll
-      for (int j = 0; j < NSUB; ++j) out[j * L + i] = fma(-iv, out[j * L + i + 1], out[j * L + i]);
+      for (int i = L - 2; i >= 0; --i)
+#pragma unroll
+        for (int j = 0; j < NSUB; ++j) {
+          const double w = fma(-iv, wn[j], out[j * L + i]);
+          out[j * L + i + 1] = NOB ? ci * wn[j] : fma(ci, wn[j], B[j * L + i + 1]);
+          wn[j] = w;
+          const int e = j * L + i;
+          if (e < 4) wzs[e] = w;
+          else if (e >= M - 4) wze[e - (M - 4)] = w;
+        }
+#pragma unroll
+      for (int j = 0; j < NSUB; ++j) {
+        wsub[j] = wn[j];
+        out[j * L] = NOB ? ci * wn[j] : fma(ci, wn[j], B[j * L]);
+      }
+    } else {
+#pragma unroll
+      for (int i = L - 2; i >= 0; --i)
+#pragma unroll
+        for (int j = 0; j < NSUB; ++j) out[j * L + i] = fma(-iv, out[j * L + i + 1], out[j * L + i]);
+#pragma unroll
+      for (int j = 0; j < NSUB; ++j) wsub[j] = out[j * L];
+      wlast = out[M - 1];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { wzs[q] = out[q]; wze[q] = out[M - 4 + q]; }
+    }
     double Y[NSUB];
     Y[0] = ysub[0];
 #pragma unroll
@@ -660,9 +715,10 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
     yl_e = Y[NSUB - 1];
     double zc = 0.0;
 #pragma unroll
-    for (int j = NSUB - 2; j >= 0; --j) zc = fma(c_sJ[0], zc, fma(c_sK[0], Y[j], iv * out[(j + 1) * L]));
-    ws = fma(c_sJ[0], zc, iv * out[0]);
-    we = fma(c_sK[L - 1], Y[NSUB - 2], iv * out[M - 1]);
+    for (int j = NSUB - 2; j >= 0; --j) zc = fma(c_sJ[0], zc, fma(c_sK[0], Y[j], iv * wsub[j + 1]));
+    ws = fma(c_sJ[0], zc, iv * wsub[0]);
+    if constexpr (NSUB > 1) we = fma(c_sK[L - 1], Y[NSUB - 2 < 0 ? 0 : NSUB - 2], iv * wlast);
+    else we = iv * wlast;
   } else {
     if (UOP) Cfd<M>::template rhs_u<false>(c, o, out, om1, op1);
     else Cfd<M>::template rhs_x<false>(c, o, out, om1, op1);
@@ -732,20 +788,21 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
     zcT[NSUB - 1] = zcarry;
 #pragma unroll
     for (int j = NSUB - 2; j >= 0; --j)
-      zcT[j] = fma(c_sJ[0], zcT[j + 1], fma(c_sK[0], ycT[j + 1], iv * out[(j + 1) * L]));
-    z0 = fma(c_sJ[0], zcT[0], fma(c_sK[0], ycT[0], iv * out[0]));
+      zcT[j] = fma(c_sJ[0], zcT[j + 1], fma(c_sK[0], ycT[j + 1], iv * wsub[j + 1]));
+    z0 = fma(c_sJ[0], zcT[0], fma(c_sK[0], ycT[0], iv * wsub[0]));
     double g0 = 0.0, g1 = 0.0, g2 = 0.0;  // V^T z of the line-end correction
     constexpr int C0 = UOP ? 0 : 3;
     if (!EDGE && c.me) {
       double zz[4];
       if (c.endc == 0) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) zz[q] = fma(c_sJ[q], zcT[0], fma(c_sK[q], ycT[0], iv * out[q]));
+        for (int q = 0; q < 4; ++q) zz[q] = fma(c_sJ[q], zcT[0], fma(c_sK[q], ycT[0], iv * wzs[q]));
         wb_g<C0>(zz, g0, g1, g2);
       } else {
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          zz[q] = fma(c_sJ[L - 4 + q], zcT[NSUB - 1], fma(c_sK[L - 4 + q], ycT[NSUB - 1], iv * out[M - 4 + q]));
+          zz[q] = fma(c_sJ[L - 4 + q], zcT[NSUB - 1], fma(c_sK[L - 4 + q], ycT[NSUB - 1],
+                                                           iv * wze[q]));
         if (c.endc == 1) wb_g<C0 + 1>(zz, g0, g1, g2);
         else wb_g<C0 + 2>(zz, g0, g1, g2);
       }
@@ -757,8 +814,14 @@ __device__ __forceinline__ void cfd_apply(const Ctx<M>& c, const KParams& P, int
     for (int j = 0; j < NSUB; ++j) {
       const double cy = -coef * ycT[j], cz = -coef * zcT[j];
 #pragma unroll
-      for (int i = 0; i < L; ++i)
-        out[j * L + i] = fma(c_sJ[i], cz, fma(c_sK[i], cy, fma(ci, out[j * L + i], NOB ? 0.0 : B[j * L + i])));
+      for (int i = 0; i < L; ++i) {
+        // truncated responses (TRIM, 32-point sub-chunks): |K_i| < 3e-17 for i >= 27 and
+        // |J_i| < 3e-17 for i <= 3 (relative to the carries) -- below round-off, dropped
+        double acc = EARLY_BASE ? out[j * L + i] : fma(ci, out[j * L + i], NOB ? 0.0 : B[j * L + i]);
+        if (!(TRIM && i >= TRIM_K)) acc = fma(c_sK[i], cy, acc);
+        if (!(TRIM && i < TRIM_J)) acc = fma(c_sJ[i], cz, acc);
+        out[j * L + i] = acc;
+      }
     }
     if (!EDGE && c.me) {
       if (c.endc == 0) wb_apply<C0, true, M>(out, coef, g0, g1, g2);
@@ -946,14 +1009,17 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   double* lC = stC + w * LSTR;
   unsigned long long* wbar = wbars + w;
   unsigned wpar = 0;  // parity of the warp mbarrier's next phase
-  const int sh = sg.start + TMA_P0;
+  // TMA coordinates are relative to the staged arrays' own origin: a band-local array
+  // starts at line tline0 (row sweep) or position tpos0 (column sweep)
+  const int sh = sg.start + TMA_P0 - P.tpos0;
+  const int tl = line - P.tline0;
   const int c1 = (sh & 31) >> 1, c2 = sh >> 5;
   if (lane == 0) {
     mbar_init(wbar, 1);
     mbar_expect_tx(wbar, BOX_BYTES * ((MODE == KM_PROLOGUE ? 1u : 2u) + (HET ? 1u : 0u)));
-    tma_load_seg(lX, &P.tmX, c1, c2, line, b, wbar);
-    if (HET) tma_load_seg(lC, &P.tmC, c1, c2, line, 0, wbar);   // one medium for the batch
-    if (MODE != KM_PROLOGUE) tma_load_seg(lS, &P.tmS, c1, c2, line, b, wbar);
+    tma_load_seg(lX, &P.tmX, c1, c2, tl, b, wbar);
+    if (HET) tma_load_seg(lC, &P.tmC, c1, c2, tl, 0, wbar);   // one medium for the batch
+    if (MODE != KM_PROLOGUE) tma_load_seg(lS, &P.tmS, c1, c2, tl, b, wbar);
   }
   if (!EDGE && P.pf_ahead > 0 && lane == 0) {
     // L2 prefetch of the staging tiles of the tile pf_ahead CTAs later in launch order:
@@ -968,11 +1034,11 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       const int ty = (int)(r % gy), tz = (int)(r / gy);
       const int tline = P.line0 + tx * NW + w;
       if (tline >= P.line_lo && tline < P.nlines) {
-        const int tsh = P.segs[ty].start + TMA_P0;
+        const int tsh = P.segs[ty].start + TMA_P0 - P.tpos0;
         const int tc1 = (tsh & 31) >> 1, tc2 = tsh >> 5;
-        tma_prefetch_seg(&P.tmX, tc1, tc2, tline, tz);
-        if (HET) tma_prefetch_seg(&P.tmC, tc1, tc2, tline, 0);
-        if (MODE != KM_PROLOGUE) tma_prefetch_seg(&P.tmS, tc1, tc2, tline, tz);
+        tma_prefetch_seg(&P.tmX, tc1, tc2, tline - P.tline0, tz);
+        if (HET) tma_prefetch_seg(&P.tmC, tc1, tc2, tline - P.tline0, 0);
+        if (MODE != KM_PROLOGUE) tma_prefetch_seg(&P.tmS, tc1, tc2, tline - P.tline0, tz);
       }
     }
   }
@@ -989,7 +1055,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       const int wl = e % NW, pos = e / NW;
       const int ln = lg0 + wl;
       const int p = sg.start + pos;
-      const bool in = ln >= P.line_lo && ln < P.nlines && (!EDGE || pos < sg.nchunks * M) && p >= 0 && p <= n;
+      const bool in = ln >= P.line_lo && ln < P.nlines && (!EDGE || pos < sg.nchunks * M) && p >= 0 && p <= n &&
+                      p >= P.pos_lo && p < P.pos_hi;
       cp_async8(stS + wl * LSTR + (pos / M) * PADM + pos % M,
                 in ? Ub + (long long)p * P.u_pt + (long long)ln * P.u_line : P.X_in, in);
     }
@@ -1011,8 +1078,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   if ((EDGE || sg.end) && lineok) {
     if (MODE == KM_PROLOGUE) {
       const double* Ub = P.U_in + (long long)b * P.u_batch + (long long)line * P.u_line;
-      c.gL = Ub[0];
-      c.gR = Ub[(long long)pR * P.u_pt];
+      c.gL = (P.pos_lo <= 0) ? Ub[0] : 0.0;                               // (a band without the
+      c.gR = (pR < P.pos_hi) ? Ub[(long long)pR * P.u_pt] : 0.0;          //  line end: not used)
     } else {
       if (P.edgeL) c.gL = P.edgeL[line] * P.gb;
       if (P.edgeR) c.gR = P.edgeR[line] * P.gb;
@@ -1025,7 +1092,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     asm volatile(
         "cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
             (unsigned long long)&P.tmF),
-        "r"(0), "r"(c1), "r"(c2), "r"(line), "r"(0)
+        "r"(0), "r"(c1), "r"(c2), "r"(tl), "r"(0)
         : "memory");
   }
   if (MODE == KM_PROLOGUE) {
@@ -1071,7 +1138,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     __syncwarp();
     if (lane == 0) {
       mbar_expect_tx(wbar, BOX_BYTES);
-      tma_load_seg(lS, &P.tmF, c1, c2, line, 0, wbar);
+      tma_load_seg(lS, &P.tmF, c1, c2, tl, 0, wbar);
     }
   };
   // dst = src + dt/2 F at this chunk's points (F = phi*gf + point source); with

@@ -54,6 +54,8 @@ struct Axis {
   std::vector<Seg> segs;   // interior segments (edge == 0) first
   int nint = 0;            // number of lean segments (edge == 0)
   int nmid = 0;            // of which without a line end (the first nmid)
+  int nfree = 0;           // of which reading no halo position of a band (the first nfree): a
+                           // band's column sweep launches them before its halo exchange lands
   Seg* d_segs = nullptr;
   double* d_tabU = nullptr;  // CFD only
   double* d_tabX = nullptr;
@@ -96,6 +98,13 @@ struct adi_ctx {
   //   phi [y][x] pa,  phiT [x][y] pb
   int pu, pa, pb, pv, pw;
   size_t aU, aS, aV, aW;  // allocation per grid (batch strides)
+  // band-local storage: the arrays hold the y positions [ya, yb) only
+  // (a whole grid: [0, nyu)).  Row-indexed arrays ([y][x]: U, Sa, V, V2, phi, Ca) and
+  // column-indexed arrays ([x][y]: Sb, W, W2, W3, phiT, Cb) keep ABSOLUTE position
+  // indexing through an offset base pointer (rows_in / cols_in); the allocation itself
+  // is rows_raw / cols_raw.  ya is even (16-byte TMA alignment of the staged rows).
+  int ya = 0, yb = 0;
+  long long dev_bytes = 0;   // device memory this handle allocated (adi_get_stats)
   double* Ubase = nullptr;
   // device buffers
   double *U = nullptr, *V = nullptr, *W = nullptr;
@@ -105,6 +114,8 @@ struct adi_ctx {
   double* W3 = nullptr;
   bool carry_valid = false;
   bool call_carry = false;   // this call ends with the carry kernel (decided by adi_step_begin)
+  int cols_phase = 0;        // column launches: 0 all segments, 1 halo-free ones, 2 the rest
+  cudaEvent_t split_wait = nullptr;   // set by an in-flight halo exchange (dist handles)
   int call_K = 8;            // K of the call in progress (the stopping rule's buffer size)
   int carry_on = 1;     // ADI_CARRY
   double* phi = nullptr;    // source pattern, S layout (row-major)
@@ -131,6 +142,12 @@ struct adi_ctx {
   bool fresh = true;             // every rank holds its band + halo rows (after set_fields)
   double* hbuf[2][2][2] = {};    // [kind][side][send, recv]
   size_t hcount[2][2][2] = {};   // elements
+  // transport of the halo messages: NCCL (comm) or, for the ranks of one process on one
+  // device (adi_create_dist_local), loopback copies from the neighbours' send buffers
+  bool loop = false;
+  adi_ctx* peer[2] = {nullptr, nullptr};   // loopback: the low / high neighbour handle
+  cudaStream_t cs = nullptr;               // exchange stream (overlaps the column sweep)
+  cudaEvent_t ev_pack = nullptr, ev_recv = nullptr;
   // internal layouts: Sa, V, V2 row-major; Sb = S^T; W, W2 = W̄^T (columns contiguous)
   int* flag = nullptr;
   adi::Axis ax, ay;
@@ -139,6 +156,13 @@ struct adi_ctx {
   bool has_pt = false;
   long long m = 0;  // steps taken
   long long launches = 0;
+  long long host_launches = 0;   // launch API calls (a graph launch counts once)
+  // ADI_GRAPH: each adi_step(n) is captured into a CUDA graph and launched at once; the
+  // executable graph is kept and updated in place while the captured topology repeats
+  int graph_on = 0;
+  bool capturing = false;
+  cudaStream_t gstream = nullptr;   // capture stream when the handle's stream is the legacy one
+  cudaGraphExec_t gexec = nullptr;
   bool fields_set = false;
   int nonfinite = 0;
   std::string err;
@@ -253,6 +277,35 @@ double* dalloc(size_t n) {
 void dfree(double* p) {
   if (p) cudaFree(p - adi::BUF_GUARD_FRONT);
 }
+double* halloc(adi_ctx* h, size_t n) {
+  double* p = dalloc(n);
+  if (p) h->dev_bytes += (long long)((n + adi::BUF_GUARD_FRONT + adi::BUF_GUARD_TAIL) * sizeof(double));
+  return p;
+}
+void hfree(adi_ctx* h, double* raw, size_t n) {
+  if (!raw) return;
+  dfree(raw);
+  h->dev_bytes -= (long long)((n + adi::BUF_GUARD_FRONT + adi::BUF_GUARD_TAIL) * sizeof(double));
+}
+// absolute-position views of band-local arrays (adi_ctx::ya)
+double* rows_in(const adi_ctx* h, double* raw, int pitch) { return raw ? raw - (ptrdiff_t)h->ya * pitch : nullptr; }
+double* cols_in(const adi_ctx* h, double* raw) { return raw ? raw - h->ya : nullptr; }
+double* rows_raw(const adi_ctx* h, double* p, int pitch) { return p ? p + (ptrdiff_t)h->ya * pitch : nullptr; }
+double* cols_raw(const adi_ctx* h, double* p) { return p ? p + h->ya : nullptr; }
+int padp(int npos) { return (npos + 34 + 3) / 4 * 4; }
+constexpr size_t kSrcSlack = 1152;   // doubles behind the source pattern arrays (see adi_set_source)
+// pitches and per-grid sizes of the y extent [ya, yb)
+void set_extent(adi_ctx* h, int ya, int yb) {
+  h->ya = ya;
+  h->yb = yb;
+  const int ny = yb - ya;
+  h->pb = padp(ny);
+  h->pw = padp(ny);
+  h->aU = (size_t)ny * h->pu;
+  h->aS = std::max((size_t)ny * h->pa, (size_t)h->nxu * h->pb);
+  h->aV = (size_t)ny * h->pv;
+  h->aW = std::max((size_t)h->nxu * h->pw, (size_t)ny * h->nxi);  // W2 also serves as a dense scratch
+}
 
 // ---- TMA tensor maps (driver entry point fetched through the runtime)
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -293,18 +346,22 @@ int tmap_for(adi_ctx* h, const double* ptr, CUtensorMap* out) {
     if (e.ptr == ptr) { *out = e.map; return ADI_OK; }
   int pitch, rows, batch = h->batch;
   size_t bs;
-  if (ptr == h->Sa) { pitch = h->pa; rows = h->nyu; bs = h->aS; }
-  else if (ptr == h->Sb) { pitch = h->pb; rows = h->nxu; bs = h->aS; }
-  else if (ptr == h->V || ptr == h->V2) { pitch = h->pv; rows = h->nyu; bs = h->aV; }
-  else if (ptr == h->W || ptr == h->W2 || ptr == h->W3) { pitch = h->pw; rows = h->nxu; bs = h->aW; }
-  else if (ptr == h->phi) { pitch = h->pa; rows = h->nyu; bs = h->aS; batch = 1; }
-  else if (ptr == h->phiT) { pitch = h->pb; rows = h->nxu; bs = h->aS; batch = 1; }
-  else if (ptr == h->Ca) { pitch = h->pa; rows = h->nyu; bs = h->aS; batch = 1; }
-  else if (ptr == h->Cb) { pitch = h->pb; rows = h->nxu; bs = h->aS; batch = 1; }
+  const int nyb = h->yb - h->ya;   // rows of the band-local row-indexed arrays
+  const double* raw = nullptr;     // the allocation (TMA coordinates: tline0 / tpos0)
+  auto rr = [&](int pt) { return rows_raw(h, const_cast<double*>(ptr), pt); };
+  auto rc_ = [&]() { return cols_raw(h, const_cast<double*>(ptr)); };
+  if (ptr == h->Sa) { pitch = h->pa; rows = nyb; bs = h->aS; raw = rr(pitch); }
+  else if (ptr == h->Sb) { pitch = h->pb; rows = h->nxu; bs = h->aS; raw = rc_(); }
+  else if (ptr == h->V || ptr == h->V2) { pitch = h->pv; rows = nyb; bs = h->aV; raw = rr(pitch); }
+  else if (ptr == h->W || ptr == h->W2 || ptr == h->W3) { pitch = h->pw; rows = h->nxu; bs = h->aW; raw = rc_(); }
+  else if (ptr == h->phi) { pitch = h->pa; rows = nyb; bs = h->aS; batch = 1; raw = rr(pitch); }
+  else if (ptr == h->phiT) { pitch = h->pb; rows = h->nxu; bs = h->aS; batch = 1; raw = rc_(); }
+  else if (ptr == h->Ca) { pitch = h->pa; rows = nyb; bs = h->aS; batch = 1; raw = rr(pitch); }
+  else if (ptr == h->Cb) { pitch = h->pb; rows = h->nxu; bs = h->aS; batch = 1; raw = rc_(); }
   else return fail(h, ADI_EINVAL, "internal: no tensor map for this array");
   adi_ctx::TMap e;
   e.ptr = ptr;
-  int rc = encode_lines(h, ptr, pitch, rows, bs, batch, &e.map);
+  int rc = encode_lines(h, raw, pitch, rows, bs, batch, &e.map);
   if (rc) return rc;
   h->tmaps.push_back(e);
   *out = e.map;
@@ -533,7 +590,9 @@ bool plan_axis(adi::Axis& A, int method, int cap, int lo_all, int hi_all) {
   // Chunk starts are kept even (16-byte aligned rows for the TMA copies).
   const int D = (M - P % M) % M;
   const int nch1 = (P + D) / M;
-  if (nch1 <= chmax) {  // the whole line in one tile
+  // the whole line in one tile -- unless only a band of it is owned (a band-local handle
+  // holds the band and its halo rows only)
+  if (nch1 <= chmax && lo_all <= 0 && hi_all >= P) {
     const int ds = (D / 2) & ~1;   // dead positions before 0 (even); the rest after n
     A.segs.push_back({-ds, nch1, lo_all, hi_all, 1});
     return true;
@@ -557,7 +616,10 @@ bool plan_axis(adi::Axis& A, int method, int cap, int lo_all, int hi_all) {
       } else if (e >= P) {                                // holds the line end
         // end the last chunk at n (or n+1, one dead position, to keep the start even);
         // with the full chunk count the line end sits in chunk 31 (lean end tile)
-        g.nchunks = (CH == adi::TCH) ? CH : (P - a + M - 1) / M;
+        // (a short line -- a band of it -- takes a generic tile of the chunks it needs)
+        // (a band-local array starts at (lo_all - halo) & ~1: the lean end tile must not start below)
+        const int ext_lo = lo_all > 0 ? ((lo_all - halo) & ~1) : 2;
+        g.nchunks = (CH == adi::TCH && P - CH * M >= std::max(2, ext_lo)) ? CH : (P - a + M - 1) / M;
         g.start = P - g.nchunks * M;
         if (g.start & 1) g.start += 1;
         if (g.start > a) { g.nchunks += 1; g.start -= M; }
@@ -635,6 +697,17 @@ int setup_axis(adi_ctx* h, adi::Axis& A, int n, int nlines, int nlmin) {
   A.nint = 0;
   A.nmid = 0;
   for (const adi::Seg& g : A.segs) { A.nint += (g.edge == 0); A.nmid += (g.edge == 0 && g.end == 0); }
+  {
+    // band decomposition: the interior segments whose staged positions stay inside the
+    // owned range [o0, o1) need no halo; they go first (overlap)
+    const int npos = A.n + 1;
+    auto free_of_halo = [&](const adi::Seg& g) {
+      return !((A.o0 > 0 && g.start < A.o0) || (A.o1 < npos && g.start + adi::TCH * adi::TM + 2 > A.o1));
+    };
+    std::stable_partition(A.segs.begin(), A.segs.begin() + A.nmid, free_of_halo);
+    A.nfree = 0;
+    for (int k = 0; k < A.nmid; ++k) A.nfree += free_of_halo(A.segs[k]);
+  }
   CUDA_TRY(h, cudaMalloc(&A.d_segs, A.segs.size() * sizeof(adi::Seg)));
   H2D_SYNC(h, A.d_segs, A.segs.data(), A.segs.size() * sizeof(adi::Seg));
   return ADI_OK;
@@ -655,13 +728,19 @@ struct TimeScope {
   adi_ctx* h;
   int kind;
   cudaEvent_t a = nullptr;
+  // (inside an ADI_GRAPH capture the records become external event nodes of the graph,
+  // recorded when the graph runs)
+  static void rec(adi_ctx* h, cudaEvent_t e) {
+    if (h->capturing) cudaEventRecordWithFlags(e, h->stream, cudaEventRecordExternal);
+    else cudaEventRecord(e, h->stream);
+  }
   TimeScope(adi_ctx* hh, int k) : h(hh), kind(k) {
-    if (h->timing) { a = take_event(h); cudaEventRecord(a, h->stream); }
+    if (h->timing) { a = take_event(h); rec(h, a); }
   }
   ~TimeScope() {
     if (h->timing) {
       cudaEvent_t b = take_event(h);
-      cudaEventRecord(b, h->stream);
+      rec(h, b);
       h->recs.push_back({kind, a, b});
     }
   }
@@ -692,6 +771,7 @@ int launch_e(adi_ctx* h, const adi::Axis& A, adi::KParams p, int seg0, int nseg)
   kern<<<grid, 32 * adi::NW, smem, h->stream>>>(p);
   CUDA_TRY(h, cudaGetLastError());
   h->launches++;
+  if (!h->capturing) h->host_launches++;
   return ADI_OK;
 }
 
@@ -699,17 +779,23 @@ int launch_e(adi_ctx* h, const adi::Axis& A, adi::KParams p, int seg0, int nseg)
 #ifndef ADI_SPLIT_END
 #define ADI_SPLIT_END 1
 #endif
+// phase 0: every segment; phase 1: the first nfree (no halo read); phase 2: the others
 template <int METHOD, int MODE, bool HET = false, bool FULL = false>
 int launch_t(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
   if (A.l1 <= A.l0) return ADI_OK;
+  const int phase = (&A == &h->ay) ? h->cols_phase : 0;   // adi_step_cols of a band (overlap)
   const int nseg = (int)A.segs.size();
   int rc;
+  if (phase == 1) return launch_e<METHOD, MODE, false, HET, FULL, true>(h, A, p, 0, A.nfree);
+  const int s0 = (phase == 2) ? A.nfree : 0;
   if (ADI_SPLIT_END) {
     // interior segments without the line-end code, then the lean line-end segments
-    rc = launch_e<METHOD, MODE, false, HET, FULL, true>(h, A, p, 0, A.nmid);
+    rc = launch_e<METHOD, MODE, false, HET, FULL, true>(h, A, p, s0, A.nmid - s0);
     if (!rc) rc = launch_e<METHOD, MODE, false, HET, FULL, false>(h, A, p, A.nmid, A.nint - A.nmid);
   } else {
-    rc = launch_e<METHOD, MODE, false, HET, FULL, false>(h, A, p, 0, A.nint);
+    rc = (phase == 2) ? launch_e<METHOD, MODE, false, HET, FULL, true>(h, A, p, s0, A.nmid - s0) : ADI_OK;
+    if (!rc) rc = launch_e<METHOD, MODE, false, HET, FULL, false>(h, A, p, phase == 2 ? A.nmid : 0,
+                                                               A.nint - (phase == 2 ? A.nmid : 0));
   }
   if (rc) return rc;
   return launch_e<METHOD, MODE, true, HET, FULL, false>(h, A, p, A.nint, nseg - A.nint);
@@ -790,24 +876,14 @@ int transpose(adi_ctx* h, const double* in, double* out, int R, int C, long long
 }
 
 // Dirichlet columns (x = 0, x = 1) of U at time factor gb, all rows (corners included)
-__global__ void edge_cols_kernel(double* U, int nyu, int nxu, int pu, long long ubatch,
+__global__ void edge_cols_kernel(double* U, int r0, int r1, int nxu, int pu, long long ubatch,
                                  const double* ex0, const double* ex1, double gb) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= nyu) return;
+  const int r = r0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= r1) return;
   double* Ub = U + blockIdx.y * ubatch + (long long)r * pu;
   Ub[0] = ex0 ? ex0[r] * gb : 0.0;
   Ub[nxu - 1] = ex1 ? ex1[r] * gb : 0.0;
 }
-// Dirichlet rows (y = 0, y = 1) of U, all columns (used by adi_set_boundary consistency)
-__global__ void edge_rows_kernel(double* U, int nyu, int nxu, long long ubatch,
-                                 const double* ey0, const double* ey1, double gb) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nxu) return;
-  double* Ub = U + blockIdx.y * ubatch;
-  Ub[i] = ey0 ? ey0[i] * gb : 0.0;
-  Ub[(long long)(nyu - 1) * nxu + i] = ey1 ? ey1[i] * gb : 0.0;
-}
-
 double tabv(const std::vector<double>& g, long long j) { return g.empty() ? 1.0 : g[(size_t)j]; }
 
 adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
@@ -861,6 +937,11 @@ adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
   p.tabU = A.d_tabU;
   p.tabX = A.d_tabX;
   p.flag = h->check_finite ? h->flag : nullptr;
+  // band-local arrays: the row sweep's lines and the column sweep's positions start at ya
+  p.tline0 = ydir ? 0 : h->ya;
+  p.tpos0 = ydir ? h->ya : 0;
+  p.pos_lo = ydir ? h->ya : -(1 << 30);
+  p.pos_hi = ydir ? h->yb : (1 << 30);
   return p;
 }
 
@@ -887,6 +968,7 @@ int stage_with_rule(adi_ctx* h, int mode_t, const adi::Axis& A, adi::KParams p, 
                                                         h->d_k + 2 + which, h->d_k + which);
     CUDA_TRY(h, cudaGetLastError());
     h->launches++;
+    h->host_launches++;
   }
   return ADI_OK;
 }
@@ -898,9 +980,22 @@ void free_ctx(adi_ctx* h) {
         if (b) { cudaFree(b); b = nullptr; }
   if (h->comm && g_nccl.ok) g_nccl.commDestroy(h->comm);
   h->comm = nullptr;
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  if (h->gstream) cudaStreamDestroy(h->gstream);
+  if (h->ev_pack) cudaEventDestroy(h->ev_pack);
+  if (h->ev_recv) cudaEventDestroy(h->ev_recv);
+  if (h->cs) cudaStreamDestroy(h->cs);
+  for (adi_ctx* q : h->peer)
+    if (q)
+      for (adi_ctx*& back : q->peer)
+        if (back == h) back = nullptr;
   for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
-  for (double* q : {h->Ubase, h->V, h->W, h->V2, h->W2, h->W3, h->Sa, h->Sb, h->phi, h->phiT, h->Ca, h->Cb}) dfree(q);
+  for (double* q : {rows_raw(h, h->Ubase, h->pu), rows_raw(h, h->V, h->pv), rows_raw(h, h->V2, h->pv),
+                    rows_raw(h, h->Sa, h->pa), rows_raw(h, h->phi, h->pa), rows_raw(h, h->Ca, h->pa),
+                    cols_raw(h, h->W), cols_raw(h, h->W2), cols_raw(h, h->W3), cols_raw(h, h->Sb),
+                    cols_raw(h, h->phiT), cols_raw(h, h->Cb)})
+    dfree(q);
   for (void* q : {(void*)h->edges, (void*)h->flag, (void*)h->d_norms, (void*)h->d_k, (void*)h->d_taper})
     if (q) cudaFree(q);
   for (adi::Axis* A : {&h->ax, &h->ay})
@@ -923,20 +1018,20 @@ void dist_bands(int npos, int nranks, int* cuts) {
 
 // ---- heterogeneous media (NEXT row f3) ------------------------------------------
 // Ca[y][x] = (kappa(y, x) at u positions x = 1..nxi, rho^-1 of V̄ row y-1 at x = 0..nxv-1)
-__global__ void pack_media_rows(float2* Ca, int pa, int nyi, int nxi, int nxu, int nxv, const float* kap,
+__global__ void pack_media_rows(float2* Ca, int pa, int y_lo, int y_hi, int nxi, int nxu, int nxv, const float* kap,
                                 const float* rv) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y + 1;
-  if (x >= pa || y > nyi) return;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = y_lo + blockIdx.y;
+  if (x >= pa || y > y_hi) return;
   float2 e;
   e.x = (x >= 1 && x <= nxi) ? kap[(size_t)y * nxu + x] : 0.f;
   e.y = (x < nxv) ? rv[(size_t)(y - 1) * nxv + x] : 0.f;
   Ca[(size_t)y * pa + x] = e;
 }
 // Cb[x][y] = (kappa(y, x) at u positions y = 1..nyi, rho^-1 of W̄ (row y, column x-1) at y = 0..nyv-1)
-__global__ void pack_media_cols(float2* Cb, int pb, int nxi, int nyi, int nyv, int nxu, const float* kap,
+__global__ void pack_media_cols(float2* Cb, int pb, int y_lo, int nxi, int nyi, int nyv, int nxu, const float* kap,
                                 const float* rw) {
-  const int y = blockIdx.x * blockDim.x + threadIdx.x, x = blockIdx.y + 1;
-  if (y >= pb || x > nxi) return;
+  const int y = y_lo + blockIdx.x * blockDim.x + threadIdx.x, x = blockIdx.y + 1;
+  if (y >= y_lo + pb || x > nxi) return;
   float2 e;
   e.x = (y >= 1 && y <= nyi) ? kap[(size_t)y * nxu + x] : 0.f;
   e.y = (y < nyv) ? rw[(size_t)y * nxi + (x - 1)] : 0.f;
@@ -949,8 +1044,23 @@ extern "C" {
 
 const char* adi_version(void) { return kVersion; }
 
-int adi_create_batch(int nx, int ny, double hh, double dt, double c, int method, int batch,
-                     adi_handle* out) {
+}  // extern "C"
+
+// The y extent of a band's arrays: its positions [y0, y1) plus `halo` on each side
+// (field_rows with the halo; even start).  A whole grid: [0, nyu).
+static void band_extent(const adi_ctx* h, int y0, int y1, int halo, int* ya, int* yb) {
+  const int npos = h->ay.n + 1;
+  if (y0 <= 0 && y1 >= npos) { *ya = 0; *yb = h->nyu; return; }
+  // (32 positions of margin below the halo: a band tile holding the halo may start up
+  // to one chunk below it, and its TMA coordinates stay non-negative)
+  *ya = std::max(y0 - halo - 32, 0) & ~1;
+  *yb = (y1 >= npos) ? h->nyu : std::min(y1 + halo, h->nyu);
+}
+
+// create a handle whose arrays hold the band [y0, y1) of y positions (plus halo) only,
+// or the whole grid (y0 = 0, y1 >= number of positions)
+static int create_impl(int nx, int ny, double hh, double dt, double c, int method, int batch, int y0, int y1,
+                       adi_handle* out) {
   if (!out) return ADI_EINVAL;
   *out = nullptr;
   if (method != ADI_CFD && method != ADI_MFD && method != ADI_CFD_FULL) return ADI_EINVAL;
@@ -985,16 +1095,15 @@ int adi_create_batch(int nx, int ny, double hh, double dt, double c, int method,
   h->nV = (size_t)h->nyi * h->nxv;
   h->nW = (size_t)h->nyv * h->nxi;
   h->nS = (size_t)h->nyi * h->nxi;
-  auto padp = [](int npos) { return (npos + 34 + 3) / 4 * 4; };
   h->pu = padp(h->nxu);
   h->pa = padp(h->nxu);
-  h->pb = padp(h->nyu);
   h->pv = padp(h->nxu);
-  h->pw = padp(h->nyu);
-  h->aU = (size_t)h->nyu * h->pu;
-  h->aS = std::max((size_t)h->nyu * h->pa, (size_t)h->nxu * h->pb);
-  h->aV = (size_t)h->nyu * h->pv;
-  h->aW = std::max((size_t)h->nxu * h->pw, h->nW);  // W2 also serves as a dense scratch
+  h->ay.n = ny - 1;   // (setup_axis sets it again) band_extent needs the position count
+  {
+    int ya, yb;
+    band_extent(h, y0, y1, adi::plan_halo(method), &ya, &yb);
+    set_extent(h, ya, yb);
+  }
   int rc = init_constants(h);
   auto bail = [&](int code) {
     free_ctx(h);
@@ -1003,11 +1112,21 @@ int adi_create_batch(int nx, int ny, double hh, double dt, double c, int method,
   };
   if (rc) return bail(rc);
   const size_t B = (size_t)batch;
-  if (!(h->Ubase = dalloc(B * h->aU)) || !(h->V = dalloc(B * h->aV)) || !(h->W = dalloc(B * h->aW)) ||
-      !(h->V2 = dalloc(B * h->aV)) || !(h->W2 = dalloc(B * h->aW)) || !(h->Sa = dalloc(B * h->aS)) ||
-      !(h->Sb = dalloc(B * h->aS)) || cudaMalloc(&h->flag, sizeof(int))) {
-    cudaGetLastError();
-    return bail(ADI_ENOMEM);
+  {
+    double *U = halloc(h, B * h->aU), *V = halloc(h, B * h->aV), *V2 = halloc(h, B * h->aV);
+    double *W = halloc(h, B * h->aW), *W2 = halloc(h, B * h->aW);
+    double *Sa = halloc(h, B * h->aS), *Sb = halloc(h, B * h->aS);
+    h->Ubase = rows_in(h, U, h->pu);
+    h->V = rows_in(h, V, h->pv);
+    h->V2 = rows_in(h, V2, h->pv);
+    h->Sa = rows_in(h, Sa, h->pa);
+    h->W = cols_in(h, W);
+    h->W2 = cols_in(h, W2);
+    h->Sb = cols_in(h, Sb);
+    if (!U || !V || !V2 || !W || !W2 || !Sa || !Sb || cudaMalloc(&h->flag, sizeof(int))) {
+      cudaGetLastError();
+      return bail(ADI_ENOMEM);
+    }
   }
   h->U = h->Ubase;
   cudaMemset(h->flag, 0, sizeof(int));
@@ -1015,6 +1134,20 @@ int adi_create_batch(int nx, int ny, double hh, double dt, double c, int method,
   if ((rc = setup_axis(h, h->ay, ny - 1, h->nxi, 4))) return bail(rc);
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(ADI_ECUDA);
   h->fields_set = true;  // zero fields are a valid state
+  if (y0 > 0 || y1 < h->ay.n + 1) {
+    // the band's lines and output positions (adi_set_band on arrays already band-local)
+    const int ny_pos = h->ay.n + 1;
+    if (y0 < 0 || y1 > ny_pos || y0 >= y1) return bail(ADI_EINVAL);
+    const int hl = h->ay.halo;
+    if ((y0 > 0 && y1 - y0 < hl) || (y1 < ny_pos && y1 - y0 < hl)) return bail(ADI_EINVAL);
+    h->band_y0 = y0;
+    h->band_y1 = y1;
+    h->ax.l0 = std::max(y0, 1);
+    h->ax.l1 = std::min(y1, h->nyi + 1);
+    h->ay.o0 = y0;
+    h->ay.o1 = y1;
+    if ((rc = setup_axis(h, h->ay, ny - 1, h->nxi, 4))) return bail(rc);
+  }
   *out = h;
   const double cfl = c * dt / hh;
   const double lim = (method == ADI_MFD) ? 2.0 / std::sqrt(6.0) : 2.0 / std::sqrt(3.0);
@@ -1023,6 +1156,13 @@ int adi_create_batch(int nx, int ny, double hh, double dt, double c, int method,
     return ADI_WUNSTABLE;
   }
   return ADI_OK;
+}
+
+extern "C" {
+
+int adi_create_batch(int nx, int ny, double hh, double dt, double c, int method, int batch,
+                     adi_handle* out) {
+  return create_impl(nx, ny, hh, dt, c, method, batch, 0, 1 << 30, out);
 }
 
 int adi_create(int nx, int ny, double hh, double dt, double c, int method, adi_handle* out) {
@@ -1080,6 +1220,9 @@ int adi_set_param(adi_handle h, int key, double v) {
     if (v != 0.0 && v != 1.0) return fail(h, ADI_EINVAL, "carry must be 0 or 1");
     h->carry_on = (int)v;
     if (!h->carry_on) h->carry_valid = false;
+  } else if (key == ADI_GRAPH) {
+    if (v != 0.0 && v != 1.0) return fail(h, ADI_EINVAL, "graph must be 0 or 1");
+    h->graph_on = (int)v;
   } else if (key == ADI_PREFETCH) {
     if (!(v >= 0) || v != std::floor(v) || v > 8) return fail(h, ADI_EINVAL, "prefetch must be an integer in [0, 8]");
     h->prefetch = (int)v;
@@ -1145,9 +1288,10 @@ static int set_fields_impl(adi_handle h, const double* U, const double* V, const
     // W̄ rows [wa, wb) (dense) -> internal W̄^T (row = x position i + 1, column = y)
     // via the W2 scratch buffer
     if (wb > wa) {
-      CUDA_TRY(h, cudaMemcpyAsync(h->W2, W + b * h->nW + (size_t)wa * h->nxi, (size_t)(wb - wa) * h->nxi * 8,
+      double* scratch = cols_raw(h, h->W2);   // the allocation of W2 as a dense buffer
+      CUDA_TRY(h, cudaMemcpyAsync(scratch, W + b * h->nW + (size_t)wa * h->nxi, (size_t)(wb - wa) * h->nxi * 8,
                                   kind, h->stream));
-      int rc = transpose(h, h->W2, h->W + b * h->aW + (size_t)off * h->pw + wa, wb - wa, h->nxi, h->nxi, h->pw,
+      int rc = transpose(h, scratch, h->W + b * h->aW + (size_t)off * h->pw + wa, wb - wa, h->nxi, h->nxi, h->pw,
                          1, 0, 0);
       if (rc) return rc;
     }
@@ -1208,23 +1352,37 @@ int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double
   if (phi) {
     if (!h->phi || !h->phiT) {
       h->tmaps.clear();
-      if (!h->phi && !(h->phi = dalloc(h->aS))) return fail(h, ADI_ENOMEM, "source pattern");
-      if (!h->phiT && !(h->phiT = dalloc(h->aS))) return fail(h, ADI_ENOMEM, "source pattern");
+      // (the line kernels read the pattern directly, a whole tile of 1026 positions from a
+      // segment start: a band-local phiT gets that much slack behind its last row)
+      if (!h->phi) {
+        double* r = halloc(h, h->aS + kSrcSlack);
+        if (!r) return fail(h, ADI_ENOMEM, "source pattern");
+        h->phi = rows_in(h, r, h->pa);
+      }
+      if (!h->phiT) {
+        double* r = halloc(h, h->aS + kSrcSlack);
+        if (!r) return fail(h, ADI_ENOMEM, "source pattern");
+        h->phiT = cols_in(h, r);
+      }
     }
-    CUDA_TRY(h, cudaMemsetAsync(h->phi, 0, h->aS * 8, h->stream));
-    CUDA_TRY(h, cudaMemsetAsync(h->phiT, 0, h->aS * 8, h->stream));
-    // interior point (j, i) of the user's block is position (y, x) = (j + off, i + off)
+    CUDA_TRY(h, cudaMemsetAsync(rows_raw(h, h->phi, h->pa), 0, (h->aS + kSrcSlack) * 8, h->stream));
+    CUDA_TRY(h, cudaMemsetAsync(cols_raw(h, h->phiT), 0, (h->aS + kSrcSlack) * 8, h->stream));
+    // interior point (j, i) of the user's block is position (y, x) = (j + off, i + off);
+    // a band-local handle keeps the rows y in [ya, yb)
     const int off = h->off;
-    CUDA_TRY(h, cudaMemcpy2DAsync(h->phi + off * h->pa + off, h->pa * 8, phi, h->nxi * 8, h->nxi * 8, h->nyi,
-                                  cudaMemcpyHostToDevice, h->stream));
-    int rc = transpose(h, h->phi + off * h->pa + off, h->phiT + off * h->pb + off, h->nyi, h->nxi, h->pa, h->pb,
-                       1, 0, 0);
-    if (rc) return rc;
+    const int y0 = std::max(h->ya, off), y1 = std::min(h->yb, off + h->nyi);
+    if (y1 > y0) {
+      CUDA_TRY(h, cudaMemcpy2DAsync(h->phi + (size_t)y0 * h->pa + off, h->pa * 8, phi + (size_t)(y0 - off) * h->nxi,
+                                    h->nxi * 8, h->nxi * 8, y1 - y0, cudaMemcpyHostToDevice, h->stream));
+      int rc = transpose(h, h->phi + (size_t)y0 * h->pa + off, h->phiT + (size_t)off * h->pb + y0, y1 - y0, h->nxi,
+                         h->pa, h->pb, 1, 0, 0);
+      if (rc) return rc;
+    }
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   } else if (h->phi) {
     h->tmaps.clear();
-    dfree(h->phi);
-    dfree(h->phiT);
+    hfree(h, rows_raw(h, h->phi, h->pa), h->aS + kSrcSlack);
+    hfree(h, cols_raw(h, h->phiT), h->aS + kSrcSlack);
     h->phi = nullptr;
     h->phiT = nullptr;
   }
@@ -1276,7 +1434,8 @@ int adi_set_media(adi_handle h, const float* kappa, const float* rinv_v, const f
   if (h->in_call) return fail(h, ADI_ESTATE, "call in progress");
   if (!kappa && !rinv_v && !rinv_w) {   // back to the scalar medium
     h->tmaps.clear();
-    dfree(h->Ca); dfree(h->Cb);
+    hfree(h, rows_raw(h, h->Ca, h->pa), h->aS);
+    hfree(h, cols_raw(h, h->Cb), h->aS);
     h->Ca = h->Cb = nullptr;
     h->het = false;
     return ADI_OK;
@@ -1302,10 +1461,14 @@ int adi_set_media(adi_handle h, const float* kappa, const float* rinv_v, const f
     return fail(h, ADI_EINVAL, "media values must be finite normal floats > 0");
   if (!h->Ca) {
     h->tmaps.clear();
-    if (!(h->Ca = dalloc(h->aS)) || !(h->Cb = dalloc(h->aS))) {
-      dfree(h->Ca); h->Ca = nullptr;
+    double* ra = halloc(h, h->aS);
+    double* rb = ra ? halloc(h, h->aS) : nullptr;
+    if (!ra || !rb) {
+      hfree(h, ra, h->aS);
       return fail(h, ADI_ENOMEM, "media arrays");
     }
+    h->Ca = rows_in(h, ra, h->pa);
+    h->Cb = cols_in(h, rb);
   }
   float* tmp = nullptr;
   const size_t nk = h->nU, nv = h->nV, nw = h->nW;
@@ -1315,10 +1478,15 @@ int adi_set_media(adi_handle h, const float* kappa, const float* rinv_v, const f
       cudaMemcpyAsync(tmp + nk, rinv_v, nv * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
       cudaMemcpyAsync(tmp + nk + nv, rinv_w, nw * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess)
     return done(fail(h, ADI_ECUDA, "media copy"));
-  pack_media_rows<<<dim3((h->pa + 255) / 256, h->nyi), 256, 0, h->stream>>>(
-      reinterpret_cast<float2*>(h->Ca), h->pa, h->nyi, h->nxi, h->nxu, h->nxv, tmp, tmp + nk);
-  pack_media_cols<<<dim3((h->pb + 255) / 256, h->nxi), 256, 0, h->stream>>>(
-      reinterpret_cast<float2*>(h->Cb), h->pb, h->nxi, h->nyi, h->nyv, h->nxu, tmp, tmp + nk + nv);
+  {
+    // the rows y of the band-local arrays: [ya, yb) (row sweep lines 1..nyi among them)
+    const int ylo = std::max(h->ya, 1), yhi = std::min(h->yb - 1, h->nyi);
+    if (yhi >= ylo)
+      pack_media_rows<<<dim3((h->pa + 255) / 256, yhi - ylo + 1), 256, 0, h->stream>>>(
+          reinterpret_cast<float2*>(h->Ca), h->pa, ylo, yhi, h->nxi, h->nxu, h->nxv, tmp, tmp + nk);
+    pack_media_cols<<<dim3((h->pb + 255) / 256, h->nxi), 256, 0, h->stream>>>(
+        reinterpret_cast<float2*>(h->Cb), h->pb, h->ya, h->nxi, h->nyi, h->nyv, h->nxu, tmp, tmp + nk + nv);
+  }
   if (cudaGetLastError() != cudaSuccess) return done(fail(h, ADI_ECUDA, "media pack"));
   int rc = done(ADI_OK);
   h->het = true;
@@ -1377,9 +1545,13 @@ int adi_step_begin(adi_handle h, int nsteps) {
   // allocated here, before any launch of the call; without it the call ends with the
   // plain FINAL kernel (call_carry = false) instead of failing half way
   h->call_carry = carry_ok(h);
-  if (h->call_carry && !h->W3 && !(h->W3 = dalloc((size_t)h->batch * h->aW))) {
-    h->call_carry = false;
-    h->carry_valid = false;
+  if (h->call_carry && !h->W3) {
+    double* r = halloc(h, (size_t)h->batch * h->aW);
+    if (r) h->W3 = cols_in(h, r);
+    else {
+      h->call_carry = false;
+      h->carry_valid = false;
+    }
   }
   h->call_K = h->K;
   if (h->carry_valid && carry_ok(h)) {
@@ -1434,6 +1606,24 @@ int adi_step_cols(adi_handle h) {
   p.gb = tabv(h->gb, 2 * m + 2);
   p.gf = tabv(h->gf, 2 * m + 2);
   int rc;
+  // a band whose halo exchange is in flight (split_wait): the segments that
+  // read no halo position run first, the others after the exchange has landed
+  auto cols = [&](int mode, int kind) -> int {
+    if (!h->split_wait) return launch(h, mode, h->ay, p, kind);
+    TimeScope ts(h, kind);          // one record for both launches (one logical kernel)
+    const int timing = h->timing;
+    h->timing = 0;
+    h->cols_phase = 1;
+    int r = launch(h, mode, h->ay, p, kind);
+    h->cols_phase = 2;
+    if (!r && cudaStreamWaitEvent(h->stream, h->split_wait, 0) != cudaSuccess)
+      r = fail(h, ADI_ECUDA, "stream wait on the halo exchange");
+    if (!r) r = launch(h, mode, h->ay, p, kind);
+    h->cols_phase = 0;
+    h->split_wait = nullptr;
+    h->timing = timing;
+    return r;
+  };
   if (last && h->call_carry) {
     // a regular column kernel (S1, W* of step m+1 into Sa, W3) that also writes
     // U^{m+1} and W̄^{m+1}; the three W buffers rotate: W = W̄^{m+1}, W3 = W*, W2 = free
@@ -1460,14 +1650,14 @@ int adi_step_cols(adi_handle h) {
     p.U_out = h->U;
     p.X_out = (h->Wcur == h->W) ? h->W2 : h->W;
     rc = (h->eps > 0.0) ? stage_with_rule(h, adi::KM_FINAL_T, h->ay, p, ADI_KK_FINAL, 1)
-                        : launch(h, adi::KM_FINAL, h->ay, p, ADI_KK_FINAL);
+                        : cols(adi::KM_FINAL, ADI_KK_FINAL);
     if (rc) return rc;
     if (h->Wcur == h->W) std::swap(h->W, h->W2);
   } else {
     p.S_out = h->Sa;
     p.X_out = h->Walt;
     rc = (h->eps > 0.0) ? stage_with_rule(h, adi::KM_SWEEP_T, h->ay, p, ADI_KK_COL, 1)
-                        : launch(h, adi::KM_SWEEP, h->ay, p, ADI_KK_COL);
+                        : cols(adi::KM_SWEEP, ADI_KK_COL);
     if (rc) return rc;
     std::swap(h->Wcur, h->Walt);
   }
@@ -1481,17 +1671,18 @@ int adi_step_end(adi_handle h) {
   if (!h->in_call || h->m != h->call_m1) return fail(h, ADI_ESTATE, "steps of the call not finished");
   if (h->Vcur != h->V) std::swap(h->V, h->V2);
   if (!h->full) {  // Dirichlet columns of U^{m1}
-    dim3 g((h->nyu + 255) / 256, h->batch);
+    dim3 g((h->yb - h->ya + 255) / 256, h->batch);
     const double* ex0 = h->edges ? h->edges + 2 * h->nxu : nullptr;
     const double* ex1 = h->edges ? h->edges + 2 * h->nxu + h->nyu : nullptr;
     TimeScope ts(h, ADI_KK_EDGE);
-    edge_cols_kernel<<<g, 256, 0, h->stream>>>(h->U, h->nyu, h->nxu, h->pu, (long long)h->aU, ex0, ex1,
+    edge_cols_kernel<<<g, 256, 0, h->stream>>>(h->U, h->ya, h->yb, h->nxu, h->pu, (long long)h->aU, ex0, ex1,
                                                 tabv(h->gb, 2 * h->m));
     CUDA_TRY(h, cudaGetLastError());
     h->launches++;
+    if (!h->capturing) h->host_launches++;
   }
   h->in_call = false;
-  if (h->check_finite) {
+  if (h->check_finite && !h->capturing) {   // (a captured call checks after its graph launch)
     int f = 0;
     CUDA_TRY(h, cudaMemcpyAsync(&f, h->flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
@@ -1505,6 +1696,66 @@ int adi_step_end(adi_handle h) {
 
 static int dist_exchange(adi_ctx* h, int kind);
 
+// ADI_GRAPH: capture the call's launches on the capture stream, then launch the graph on
+// the handle's stream (kernel parameters differ from call to call -- time factors, the
+// rotating buffers -- so the kept executable graph is updated with the new capture)
+static int step_graph(adi_ctx* h, int nsteps) {
+  // everything that allocates or synchronizes happens before the capture
+  if (carry_ok(h) && !h->W3) {
+    double* r = halloc(h, (size_t)h->batch * h->aW);
+    if (!r) return fail(h, ADI_ENOMEM, "carry buffer");
+    h->W3 = cols_in(h, r);
+  }
+  if (!h->gstream && cudaStreamCreateWithFlags(&h->gstream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(h, ADI_ECUDA, "capture stream");
+  cudaStream_t user = h->stream;
+  cudaStream_t cap = user ? user : h->gstream;
+  CUDA_TRY(h, cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed));
+  h->stream = cap;
+  h->capturing = true;
+  const long long m0 = h->m;
+  const bool carry0 = h->carry_valid;
+  int rc = adi_step(h, nsteps);
+  h->capturing = false;
+  h->stream = user;
+  cudaGraph_t g = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(cap, &g);
+  if (rc || ec != cudaSuccess) {
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    // nothing ran: the host state goes back to the start of the call
+    h->m = m0;
+    h->in_call = false;
+    h->carry_valid = carry0 && !rc ? carry0 : false;
+    return rc ? rc : fail(h, ADI_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
+  }
+  bool ok = false;
+  if (h->gexec) {
+    cudaGraphExecUpdateResultInfo info;
+    ok = cudaGraphExecUpdate(h->gexec, g, &info) == cudaSuccess;
+    if (!ok) { cudaGetLastError(); cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+  }
+  if (!ok && cudaGraphInstantiate(&h->gexec, g, 0) != cudaSuccess) {
+    cudaGetLastError();
+    cudaGraphDestroy(g);
+    h->gexec = nullptr;
+    return fail(h, ADI_ECUDA, "graph instantiate");
+  }
+  cudaGraphDestroy(g);
+  CUDA_TRY(h, cudaGraphLaunch(h->gexec, h->stream));
+  h->host_launches++;
+  if (h->check_finite) {
+    int f = 0;
+    CUDA_TRY(h, cudaMemcpyAsync(&f, h->flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if (f) {
+      h->nonfinite = 1;
+      return fail(h, ADI_ENONFINITE, "non-finite value in the fields");
+    }
+  }
+  return ADI_OK;
+}
+
 int adi_step(adi_handle h, int nsteps) {
   DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
@@ -1513,6 +1764,9 @@ int adi_step(adi_handle h, int nsteps) {
   // a handle of adi_create_dist: the halo exchanges of DESIGN.md §7 happen here (U and W̄
   // before the call's prologue unless the fields were just set; S and W* after every
   // row sweep), NCCL grouped send/recv on the handle's stream
+  if (h->loop && h->nranks > 1)
+    return fail(h, ADI_ESTATE, "a rank of adi_create_dist_local steps with adi_step_dist_local");
+  if (h->graph_on && !h->capturing && !(h->dist && h->nranks > 1) && h->eps <= 0.0) return step_graph(h, nsteps);
   const bool ex = h->dist && h->nranks > 1;
   int rc = ADI_OK;
   if (ex && !h->fresh) rc = dist_exchange(h, 1);
@@ -1523,11 +1777,77 @@ int adi_step(adi_handle h, int nsteps) {
     if (rc == ADI_OK) rc = adi_step_cols(h);
   }
   if (rc == ADI_OK) h->fresh = false;
-  if (rc != ADI_OK) { h->in_call = false; return rc; }
+  if (rc != ADI_OK) { h->in_call = false; h->split_wait = nullptr; return rc; }
   return adi_step_end(h);
 }
 
 // ---- band decomposition --------------------------------------------------
+// Re-lay the arrays out for the y extent [nya, nyb): the state (U, V̄, W̄)
+// and the static inputs (phi, media) keep their rows inside both extents; the scratch
+// arrays are new.  Rows of the new extent outside the old one are zero.
+static int relayout(adi_ctx* h, int nya, int nyb) {
+  const int oya = h->ya, oyb = h->yb, opb = h->pb, opw = h->pw;
+  const size_t oaU = h->aU, oaS = h->aS, oaV = h->aV, oaW = h->aW;
+  const size_t B = (size_t)h->batch;
+  struct Arr { double** p; bool rows; int pitch_old; size_t a_old; size_t nb; bool live; };
+  double* oraw[12];
+  Arr arrs[12] = {
+      {&h->Ubase, true, h->pu, oaU, B, true},   {&h->V, true, h->pv, oaV, B, true},
+      {&h->V2, true, h->pv, oaV, B, false},     {&h->Sa, true, h->pa, oaS, B, false},
+      {&h->phi, true, h->pa, oaS, 1, true},     {&h->Ca, true, h->pa, oaS, 1, true},
+      {&h->W, false, opw, oaW, B, true},        {&h->W2, false, opw, oaW, B, false},
+      {&h->W3, false, opw, oaW, B, false},      {&h->Sb, false, opb, oaS, B, false},
+      {&h->phiT, false, opb, oaS, 1, true},     {&h->Cb, false, opb, oaS, 1, true}};
+  for (int k = 0; k < 12; ++k)
+    oraw[k] = arrs[k].rows ? rows_raw(h, *arrs[k].p, arrs[k].pitch_old) : cols_raw(h, *arrs[k].p);
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  set_extent(h, nya, nyb);
+  const int ylo = std::max(oya, nya), yhi = std::min(oyb, nyb);
+  double* nraw[12] = {};
+  bool ok = true;
+  for (int k = 0; k < 12 && ok; ++k) {
+    if (!oraw[k] || (k == 8)) continue;   // absent, or the carry buffer W3 (bands do not carry)
+    const Arr& A = arrs[k];
+    const bool isS = (A.p == &h->Sa || A.p == &h->Sb || A.p == &h->phi || A.p == &h->phiT || A.p == &h->Ca ||
+                      A.p == &h->Cb);
+    const bool isPhi = (A.p == &h->phi || A.p == &h->phiT);
+    const size_t an = (isS ? h->aS : A.rows ? (A.p == &h->Ubase ? h->aU : h->aV) : h->aW) + (isPhi ? kSrcSlack : 0);
+    nraw[k] = halloc(h, A.nb * an);
+    if (!nraw[k]) { ok = false; break; }
+    if (!A.live || yhi <= ylo) continue;
+    for (size_t b = 0; b < A.nb; ++b) {
+      cudaError_t e;
+      if (A.rows)
+        e = cudaMemcpyAsync(nraw[k] + b * an + (size_t)(ylo - nya) * A.pitch_old,
+                            oraw[k] + b * A.a_old + (size_t)(ylo - oya) * A.pitch_old,
+                            (size_t)(yhi - ylo) * A.pitch_old * 8, cudaMemcpyDeviceToDevice, h->stream);
+      else
+        e = cudaMemcpy2DAsync(nraw[k] + b * an + (ylo - nya), (A.p == &h->W ? h->pw : h->pb) * 8,
+                              oraw[k] + b * A.a_old + (ylo - oya), A.pitch_old * 8, (size_t)(yhi - ylo) * 8,
+                              h->nxu, cudaMemcpyDeviceToDevice, h->stream);
+      if (e != cudaSuccess) { cudaGetLastError(); ok = false; break; }
+    }
+  }
+  if (ok && cudaStreamSynchronize(h->stream) != cudaSuccess) ok = false;
+  if (!ok) {   // undo: keep the old layout
+    for (int k = 0; k < 12; ++k)
+      if (nraw[k]) hfree(h, nraw[k], 0);
+    h->ya = oya; h->yb = oyb; h->pb = opb; h->pw = opw;
+    h->aU = oaU; h->aS = oaS; h->aV = oaV; h->aW = oaW;
+    return fail(h, ADI_ENOMEM, "band re-layout");
+  }
+  for (int k = 0; k < 12; ++k) {
+    const Arr& A = arrs[k];
+    const size_t an_old = A.a_old * A.nb;
+    if (oraw[k]) hfree(h, oraw[k], an_old);
+    *A.p = nraw[k] ? (A.rows ? rows_in(h, nraw[k], A.pitch_old) : cols_in(h, nraw[k])) : nullptr;
+  }
+  h->U = h->Ubase;
+  h->tmaps.clear();
+  h->carry_valid = false;
+  return ADI_OK;
+}
+
 int adi_set_band(adi_handle h, int y0, int y1) {
   DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
@@ -1556,6 +1876,12 @@ int adi_set_band(adi_handle h, int y0, int y1) {
   h->ay.d_segs = nullptr;   // setup_axis allocates a new plan; the old one is kept until it succeeds
   h->ay.d_tabU = h->ay.d_tabX = nullptr;
   int rc = setup_axis(h, h->ay, h->ny - 1, h->nxi, 4);
+  if (!rc) {
+    // band-local arrays: the band and its halo rows only (memory per handle ~ 1/P)
+    int nya, nyb;
+    band_extent(h, y0, y1, hl, &nya, &nyb);
+    if (nya != h->ya || nyb != h->yb) rc = relayout(h, nya, nyb);
+  }
   if (rc) {
     for (void* q : {(void*)h->ay.d_segs, (void*)h->ay.d_tabU, (void*)h->ay.d_tabX})
       if (q) cudaFree(q);
@@ -1601,7 +1927,7 @@ int adi_halo_bytes(adi_handle h, int kind, int side, size_t* bytes) {
 
 // copy y positions [a, b) of the halo fields between the internal arrays and a
 // contiguous device buffer (pack: dir = 0, unpack: dir = 1)
-static int halo_copy(adi_ctx* h, int kind, int a, int b, double* buf, int dir) {
+static int halo_copy(adi_ctx* h, int kind, int a, int b, double* buf, int dir, cudaStream_t st) {
   const int rows = b - a;
   if (rows <= 0) return ADI_OK;
   double* q = buf;
@@ -1609,8 +1935,8 @@ static int halo_copy(adi_ctx* h, int kind, int a, int b, double* buf, int dir) {
     for (int bb = 0; bb < h->batch; ++bb) {
       double* base = arr + bb * bstride + col0;
       cudaError_t e = dir == 0
-          ? cudaMemcpy2DAsync(q, rows * 8, base, pitch * 8, rows * 8, nr, cudaMemcpyDeviceToDevice, h->stream)
-          : cudaMemcpy2DAsync(base, pitch * 8, q, rows * 8, rows * 8, nr, cudaMemcpyDeviceToDevice, h->stream);
+          ? cudaMemcpy2DAsync(q, rows * 8, base, pitch * 8, rows * 8, nr, cudaMemcpyDeviceToDevice, st)
+          : cudaMemcpy2DAsync(base, pitch * 8, q, rows * 8, rows * 8, nr, cudaMemcpyDeviceToDevice, st);
       if (e != cudaSuccess) return fail(h, ADI_ECUDA, std::string("halo copy: ") + cudaGetErrorString(e));
       q += (size_t)nr * rows;
     }
@@ -1626,8 +1952,8 @@ static int halo_copy(adi_ctx* h, int kind, int a, int b, double* buf, int dir) {
     for (int bb = 0; bb < h->batch; ++bb) {
       double* base = h->U + bb * h->aU + (size_t)a * h->pu;
       cudaError_t e = dir == 0
-          ? cudaMemcpy2DAsync(q, h->nxu * 8, base, h->pu * 8, h->nxu * 8, rows, cudaMemcpyDeviceToDevice, h->stream)
-          : cudaMemcpy2DAsync(base, h->pu * 8, q, h->nxu * 8, h->nxu * 8, rows, cudaMemcpyDeviceToDevice, h->stream);
+          ? cudaMemcpy2DAsync(q, h->nxu * 8, base, h->pu * 8, h->nxu * 8, rows, cudaMemcpyDeviceToDevice, st)
+          : cudaMemcpy2DAsync(base, h->pu * 8, q, h->nxu * 8, h->nxu * 8, rows, cudaMemcpyDeviceToDevice, st);
       if (e != cudaSuccess) return fail(h, ADI_ECUDA, std::string("halo copy: ") + cudaGetErrorString(e));
       q += (size_t)h->nxu * rows;
     }
@@ -1642,7 +1968,7 @@ int adi_halo_pack(adi_handle h, int kind, int side, void* dev_buf) {
   h->err.clear();
   int a, b;
   halo_range(h, side, 1, &a, &b);
-  return halo_copy(h, kind, a, b, (double*)dev_buf, 0);
+  return halo_copy(h, kind, a, b, (double*)dev_buf, 0, h->stream);
 }
 
 int adi_halo_unpack(adi_handle h, int kind, int side, const void* dev_buf) {
@@ -1652,34 +1978,105 @@ int adi_halo_unpack(adi_handle h, int kind, int side, const void* dev_buf) {
   h->err.clear();
   int a, b;
   halo_range(h, side, 0, &a, &b);
-  return halo_copy(h, kind, a, b, (double*)dev_buf, 1);
+  return halo_copy(h, kind, a, b, (double*)dev_buf, 1, h->stream);
 }
 
-// ---- adi_create_dist: the band decomposition with NCCL inside the library ----------
-static int dist_exchange(adi_ctx* h, int kind) {
-  const int peer[2] = {h->rank - 1, h->rank + 1};   // side 0: low, 1: high
+// ---- adi_create_dist: the band decomposition with the exchange inside the library ----
+// One exchange = pack this band's edge rows (main stream) -> transfer
+// (exchange stream cs: NCCL grouped send/recv with the two neighbours, or loopback copies
+// from the neighbour handles' send buffers) -> unpack into the halo rows (cs).  ev_recv
+// marks the landed halo: kind 0 (S2, W*, after the row sweep) only gates the column
+// segments that read the halo (adi_step_cols, split_wait), so the transfer overlaps the
+// others; kind 1 (U, W̄, before a call's prologue) is waited for at once.
+static int nbr(const adi_ctx* h, int side) { return side == 0 ? h->rank - 1 : h->rank + 1; }
+static bool has_nbr(const adi_ctx* h, int side) { const int q = nbr(h, side); return q >= 0 && q < h->nranks; }
+
+static int dist_pack(adi_ctx* h, int kind) {
+  if (h->loop)   // a neighbour may still be copying our previous message
+    for (adi_ctx* q : h->peer)
+      if (q && q->ev_recv) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, q->ev_recv, 0));
   for (int side = 0; side < 2; ++side) {
-    if (peer[side] < 0 || peer[side] >= h->nranks) continue;
+    if (!has_nbr(h, side)) continue;
     int a, b;
     halo_range(h, side, 1, &a, &b);
-    int rc = halo_copy(h, kind, a, b, h->hbuf[kind][side][0], 0);
+    int rc = halo_copy(h, kind, a, b, h->hbuf[kind][side][0], 0, h->stream);
     if (rc) return rc;
+  }
+  CUDA_TRY(h, cudaEventRecord(h->ev_pack, h->stream));
+  return ADI_OK;
+}
+
+static int dist_transfer(adi_ctx* h, int kind) {
+  CUDA_TRY(h, cudaStreamWaitEvent(h->cs, h->ev_pack, 0));
+  if (h->loop) {
+    for (int side = 0; side < 2; ++side) {
+      adi_ctx* q = h->peer[side];
+      if (!has_nbr(h, side)) continue;
+      if (!q) return fail(h, ADI_ESTATE, "loopback neighbour destroyed");
+      if (q->hcount[kind][1 - side][0] != h->hcount[kind][side][1])
+        return fail(h, ADI_EINVAL, "internal: halo message sizes differ");
+      CUDA_TRY(h, cudaStreamWaitEvent(h->cs, q->ev_pack, 0));
+      CUDA_TRY(h, cudaMemcpyAsync(h->hbuf[kind][side][1], q->hbuf[kind][1 - side][0],
+                                  h->hcount[kind][side][1] * sizeof(double), cudaMemcpyDeviceToDevice, h->cs));
+    }
+    return ADI_OK;
   }
   NCCL_TRY(h, g_nccl.groupStart());
   for (int side = 0; side < 2; ++side) {
-    if (peer[side] < 0 || peer[side] >= h->nranks) continue;
-    NCCL_TRY(h, g_nccl.send(h->hbuf[kind][side][0], h->hcount[kind][side][0], ncclFloat64, peer[side], h->comm,
-                            h->stream));
-    NCCL_TRY(h, g_nccl.recv(h->hbuf[kind][side][1], h->hcount[kind][side][1], ncclFloat64, peer[side], h->comm,
-                            h->stream));
+    if (!has_nbr(h, side)) continue;
+    NCCL_TRY(h, g_nccl.send(h->hbuf[kind][side][0], h->hcount[kind][side][0], ncclFloat64, nbr(h, side), h->comm,
+                            h->cs));
+    NCCL_TRY(h, g_nccl.recv(h->hbuf[kind][side][1], h->hcount[kind][side][1], ncclFloat64, nbr(h, side), h->comm,
+                            h->cs));
   }
   NCCL_TRY(h, g_nccl.groupEnd());
+  return ADI_OK;
+}
+
+static int dist_unpack(adi_ctx* h, int kind) {
   for (int side = 0; side < 2; ++side) {
-    if (peer[side] < 0 || peer[side] >= h->nranks) continue;
+    if (!has_nbr(h, side)) continue;
     int a, b;
     halo_range(h, side, 0, &a, &b);
-    int rc = halo_copy(h, kind, a, b, h->hbuf[kind][side][1], 1);
+    int rc = halo_copy(h, kind, a, b, h->hbuf[kind][side][1], 1, h->cs);
     if (rc) return rc;
+  }
+  CUDA_TRY(h, cudaEventRecord(h->ev_recv, h->cs));
+  if (kind == 0) h->split_wait = h->ev_recv;      // the column sweep waits per segment class
+  else CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_recv, 0));
+  return ADI_OK;
+}
+
+static int dist_exchange(adi_ctx* h, int kind) {
+  int rc = dist_pack(h, kind);
+  if (!rc) rc = dist_transfer(h, kind);
+  if (!rc) rc = dist_unpack(h, kind);
+  return rc;
+}
+
+// halo buffers, exchange stream and events of a dist handle (band already set)
+static int dist_init(adi_ctx* h) {
+  for (int kind = 0; kind < 2; ++kind)
+    for (int side = 0; side < 2; ++side) {
+      if (!has_nbr(h, side)) continue;
+      for (int own = 1; own >= 0; --own) {   // send = own rows, recv = the neighbour's
+        int a, b;
+        halo_range(h, side, own, &a, &b);
+        const size_t n = halo_elems(h, kind, b - a);
+        double*& buf = h->hbuf[kind][side][own ? 0 : 1];
+        h->hcount[kind][side][own ? 0 : 1] = n;
+        if (cudaMalloc(&buf, std::max<size_t>(n, 1) * sizeof(double)) != cudaSuccess) {
+          cudaGetLastError();
+          return ADI_ENOMEM;
+        }
+        h->dev_bytes += (long long)(std::max<size_t>(n, 1) * sizeof(double));
+      }
+    }
+  if (cudaStreamCreateWithFlags(&h->cs, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_pack, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_recv, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    return ADI_ECUDA;
   }
   return ADI_OK;
 }
@@ -1705,6 +2102,24 @@ int adi_nccl_unique_id(void* out) {
   return ADI_OK;
 }
 
+// one rank's handle: its band's arrays only (band + halo rows), dist state set
+static int create_rank(int nx, int ny, double hh, double dt, double c, int method, int batch, int rank, int nranks,
+                       adi_handle* out) {
+  *out = nullptr;
+  const int npos = ny;   // y positions 0..ny-1 (the planner's positions of both reduced variants)
+  std::vector<int> cuts(nranks + 1);
+  dist_bands(npos, nranks, cuts.data());
+  adi_handle h = nullptr;
+  int rc = create_impl(nx, ny, hh, dt, c, method, batch, nranks > 1 ? cuts[rank] : 0,
+                       nranks > 1 ? cuts[rank + 1] : 1 << 30, &h);
+  if (rc < 0) return rc;
+  h->dist = true;
+  h->rank = rank;
+  h->nranks = nranks;
+  *out = h;
+  return rc;
+}
+
 int adi_create_dist(int nx, int ny, double hh, double dt, double c, int method, int batch,
                     const void* nccl_unique_id, int rank, int nranks, adi_handle* out) {
   if (!out) return ADI_EINVAL;
@@ -1712,17 +2127,11 @@ int adi_create_dist(int nx, int ny, double hh, double dt, double c, int method, 
   if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !nccl_unique_id)) return ADI_EINVAL;
   if (method == ADI_CFD_FULL && nranks > 1) return ADI_EINVAL;   // no band decomposition
   adi_handle h = nullptr;
-  int rc = adi_create_batch(nx, ny, hh, dt, c, method, batch, &h);
+  int rc = create_rank(nx, ny, hh, dt, c, method, batch, rank, nranks, &h);
   if (rc < 0) return rc;
   const int warn = rc;
-  h->dist = true;
-  h->rank = rank;
-  h->nranks = nranks;
   if (nranks > 1) {
-    std::vector<int> cuts(nranks + 1);
-    dist_bands(h->ay.n + 1, nranks, cuts.data());
-    int e = adi_set_band(h, cuts[rank], cuts[rank + 1]);
-    if (e) { adi_destroy(h); return e; }
+    DevGuard dg_(h);
     if (!nccl_load()) { adi_destroy(h); return ADI_ENCCL; }
     ncclUniqueId id;
     std::memcpy(&id, nccl_unique_id, sizeof id);
@@ -1731,26 +2140,76 @@ int adi_create_dist(int nx, int ny, double hh, double dt, double c, int method, 
       adi_destroy(h);
       return ADI_ENCCL;
     }
-    for (int kind = 0; kind < 2; ++kind)
-      for (int side = 0; side < 2; ++side) {
-        const int peer = side == 0 ? rank - 1 : rank + 1;
-        if (peer < 0 || peer >= nranks) continue;
-        for (int own = 1; own >= 0; --own) {   // send = own rows, recv = the neighbour's
-          int a, b;
-          halo_range(h, side, own, &a, &b);
-          const size_t n = halo_elems(h, kind, b - a);
-          double*& buf = h->hbuf[kind][side][own ? 0 : 1];
-          h->hcount[kind][side][own ? 0 : 1] = n;
-          if (cudaMalloc(&buf, std::max<size_t>(n, 1) * sizeof(double)) != cudaSuccess) {
-            cudaGetLastError();
-            adi_destroy(h);
-            return ADI_ENOMEM;
-          }
-        }
-      }
+    if ((rc = dist_init(h))) { adi_destroy(h); return rc; }
   }
   *out = h;
   return warn;
+}
+
+int adi_create_dist_local(int nx, int ny, double hh, double dt, double c, int method, int batch, int nranks,
+                          adi_handle* out) {
+  if (!out || nranks < 1) return ADI_EINVAL;
+  for (int r = 0; r < nranks; ++r) out[r] = nullptr;
+  if (method == ADI_CFD_FULL && nranks > 1) return ADI_EINVAL;
+  int warn = ADI_OK;
+  for (int r = 0; r < nranks; ++r) {
+    int rc = create_rank(nx, ny, hh, dt, c, method, batch, r, nranks, &out[r]);
+    if (rc < 0) {
+      for (int q = 0; q < r; ++q) { adi_destroy(out[q]); out[q] = nullptr; }
+      return rc;
+    }
+    warn = rc;
+    out[r]->loop = true;
+  }
+  for (int r = 0; r < nranks && nranks > 1; ++r) {
+    out[r]->peer[0] = r > 0 ? out[r - 1] : nullptr;
+    out[r]->peer[1] = r + 1 < nranks ? out[r + 1] : nullptr;
+    DevGuard dg_(out[r]);
+    int rc = dist_init(out[r]);
+    if (rc) {
+      for (int q = 0; q < nranks; ++q) { adi_destroy(out[q]); out[q] = nullptr; }
+      return rc;
+    }
+  }
+  return warn;
+}
+
+int adi_step_dist_local(adi_handle* hs, int nranks, int nsteps) {
+  if (!hs || nranks < 1 || nsteps < 0) return ADI_EINVAL;
+  for (int r = 0; r < nranks; ++r)
+    if (!hs[r] || !hs[r]->loop || hs[r]->nranks != nranks || hs[r]->rank != r) return ADI_EINVAL;
+  if (nsteps == 0) return ADI_OK;
+  // the collective protocol of adi_step, rank by rank in one thread:
+  // every rank's phase runs before any rank's next phase, so no rank waits on another
+  const bool ex = nranks > 1;
+  auto all = [&](auto fn) -> int {
+    for (int r = 0; r < nranks; ++r) {
+      DevGuard dg_(hs[r]);
+      int rc = fn(hs[r]);
+      if (rc) return rc;
+    }
+    return ADI_OK;
+  };
+  int rc = ADI_OK;
+  if (ex && !hs[0]->fresh) {
+    rc = all([](adi_ctx* h) { return dist_pack(h, 1); });
+    if (!rc) rc = all([](adi_ctx* h) { return dist_transfer(h, 1); });
+    if (!rc) rc = all([](adi_ctx* h) { return dist_unpack(h, 1); });
+  }
+  if (!rc) rc = all([&](adi_ctx* h) { return adi_step_begin(h, nsteps); });
+  for (int k = 0; k < nsteps && !rc; ++k) {
+    rc = all([](adi_ctx* h) { return adi_step_rows(h); });
+    if (!rc && ex) rc = all([](adi_ctx* h) { return dist_pack(h, 0); });
+    if (!rc && ex) rc = all([](adi_ctx* h) { return dist_transfer(h, 0); });
+    if (!rc && ex) rc = all([](adi_ctx* h) { return dist_unpack(h, 0); });
+    if (!rc) rc = all([](adi_ctx* h) { return adi_step_cols(h); });
+  }
+  if (rc) {
+    for (int r = 0; r < nranks; ++r) { hs[r]->in_call = false; hs[r]->split_wait = nullptr; }
+    return rc;
+  }
+  for (int r = 0; r < nranks; ++r) hs[r]->fresh = false;
+  return all([](adi_ctx* h) { return adi_step_end(h); });
 }
 
 int adi_band_info(adi_handle h, int* y0, int* y1, int* halo, int* npos) {
@@ -1786,10 +2245,11 @@ static int get_fields_impl(adi_handle h, double* U, double* V, double* W, cudaMe
                                     kind, h->stream));
     // internal W̄^T (columns [wa, wb)) -> W̄ rows via the W2 scratch buffer
     if (wb > wa) {
-      int rc = transpose(h, h->W + b * h->aW + (size_t)off * h->pw + wa, h->W2, h->nxi, wb - wa, h->pw, h->nxi, 1,
+      double* scratch = cols_raw(h, h->W2);
+      int rc = transpose(h, h->W + b * h->aW + (size_t)off * h->pw + wa, scratch, h->nxi, wb - wa, h->pw, h->nxi, 1,
                          0, 0);
       if (rc) return rc;
-      CUDA_TRY(h, cudaMemcpyAsync(W + b * h->nW + (size_t)wa * h->nxi, h->W2, (size_t)(wb - wa) * h->nxi * 8,
+      CUDA_TRY(h, cudaMemcpyAsync(W + b * h->nW + (size_t)wa * h->nxi, scratch, (size_t)(wb - wa) * h->nxi * 8,
                                   kind, h->stream));
     }
   }
@@ -1833,6 +2293,8 @@ int adi_get_stats(adi_handle h, adi_stats* s) {
   s->nonfinite = h->nonfinite;
   s->k_sweeps = h->K;
   s->kernel_launches = h->launches;
+  s->device_bytes = h->dev_bytes;
+  s->host_launches = h->host_launches;
   s->last_test[0] = s->last_test[1] = -1.0;
   s->last_k[0] = s->last_k[1] = h->K;
   // the stopping rule's test value (Alg. 3/4) at the chosen sweep of the last row and

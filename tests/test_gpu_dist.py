@@ -111,3 +111,108 @@ def test_create_dist_single_rank(adi, method):
     o = oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, p.U, p.V, p.W, nsteps=2, **p.oracle_kwargs())
     for name, a, c in zip("UVW", out, o):
         check(a, c)
+
+
+# ---- adi_create_dist_local: the in-library exchange (adi_create_dist's code path with a
+# loopback transport), band-local memory, the column sweep overlapping the transfer ----
+def _dist_local(adi, p, world, **kw):
+    hs = adi.adi_create_dist_local(p.nx, p.ny, p.h, p.dt, p.c, p.method, kw.get("batch", 1), world)
+    ss = [adi.AdiSolver.adopt(h, p.nx, p.ny, p.h, p.dt, p.c, p.method, batch=kw.get("batch", 1), K=p.K)
+          for h in hs]
+    return hs, ss
+
+
+def _gather_local(adi, ss, method, nx, ny, batch=1):
+    """Each rank's band rows (adi_get_fields of a band writes only those) into one grid."""
+    from adi_inputs import shapes
+    from paper_2006_07583_b200 import dist
+    parts = []
+    bands = []
+    for s in ss:
+        out = [np.zeros(((batch,) if batch > 1 else ()) + sh) for sh in shapes(method, nx, ny)]
+        adi.adi_get_fields(s.handle, *out)
+        parts.append(out)
+        y0, y1, _, _ = adi.adi_band_info(s.handle)
+        bands.append((y0, y1))
+    return dist.gather_bands(parts, bands)
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+@pytest.mark.parametrize("n,world,split", [(301, 2, [3]), (1601, 4, [1, 2]), (2101, 8, [2]), (4097, 3, [1, 1])])
+def test_dist_local_equals_single_and_oracle(adi, method, n, world, split):
+    """adi_create_dist_local + adi_step_dist_local (several calls: the kind-1 U/W̄ exchange
+    too) against one plain handle and the oracle, rel L2 and max-norm."""
+    steps = sum(split)
+    p = random_problem(method, n, seed=n + 3 * world, steps=steps)
+    hs, ss = _dist_local(adi, p, world)
+    for s in ss:
+        s.set_fields(p.U, p.V, p.W)
+        s.set_source(p.phi, None, p.gf)
+        s.set_boundary(p.edges, p.gb)
+    for k in split:
+        adi.adi_step_dist_local(hs, k)
+    got = _gather_local(adi, ss, method, p.nx, p.ny)
+    s1 = adi.AdiSolver.from_problem(p)
+    s1.step(steps)
+    ref = s1.get_fields()
+    s1.close()
+    o = oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, p.U, p.V, p.W, nsteps=steps, **p.oracle_kwargs())
+    for name, a, b, c in zip("UVW", got, ref, o):
+        check(a, b, tol=1e-13, name=name, what="dist_local vs one handle")
+        check(a, c, name=name, what="dist_local vs oracle")
+    for s in ss:
+        with pytest.raises(adi.AdiError):
+            adi.adi_step(s.handle, 1)            # ranks of a local group step together
+        with pytest.raises(adi.AdiError):
+            adi.adi_set_band(s.handle, 0, 64)    # the band of a dist handle is fixed
+    for s in ss:
+        s.close()
+
+
+def test_dist_local_media_batch_points(adi):
+    """Media, a batch of point-source shots and the dist-local exchange together."""
+    n, world, B, steps = 1601, 3, 2, 3
+    probs = [ricker_problem(n, shot=s, nshots=4, steps=steps, f0=20.0, t0=0.05) for s in range(B)]
+    p0 = probs[0]
+    rng = np.random.default_rng(5)
+    med = [rng.uniform(0.6, 1.0, a.shape).astype(np.float32) for a in (p0.U, p0.V, p0.W)]
+    hs, ss = _dist_local(adi, p0, world, batch=B)
+    U = np.stack([p.U for p in probs]); V = np.stack([p.V for p in probs]); W = np.stack([p.W for p in probs])
+    rng2 = np.random.default_rng(6)
+    U = U + rng2.standard_normal(U.shape)   # a nonzero start (the sources are weak early)
+    for s in ss:
+        s.set_fields(U, V, W)
+        s.set_point_sources([p.src[0] for p in probs], [p.src[1] for p in probs], p0.gf)
+        s.set_media(*med)
+    adi.adi_step_dist_local(hs, steps)
+    got = _gather_local(adi, ss, MFD, n, n, batch=B)
+    for b, p in enumerate(probs):
+        o = oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, U[b], p.V, p.W, nsteps=steps,
+                       src=p.src, gf=p.gf, kappa=med[0], rinv_v=med[1], rinv_w=med[2])
+        for name, a, c in zip("UVW", got, o):
+            check(a[b], c, name=name, what=f"dist_local media shot {b}")
+    for s in ss:
+        s.close()
+
+
+def test_dist_memory_scales_with_bands(adi):
+    """Per-rank device memory of a band-local handle (adi_get_stats device_bytes): at P = 8
+    each rank holds its band + halo rows, <= 1/6 of the P = 1 handle; adi_set_band on a
+    plain handle re-lays its arrays out the same way."""
+    n = 8193
+    h = 1.0 / (n - 1)
+    for method in (CFD, MFD):
+        hs1 = adi.adi_create_dist_local(n, n, h, 0.5 * h, 1.0, method, 1, 1)
+        b1 = adi.adi_get_stats(hs1[0])["device_bytes"]
+        adi.adi_destroy(hs1[0])
+        hs8 = adi.adi_create_dist_local(n, n, h, 0.5 * h, 1.0, method, 1, 8)
+        b8 = [adi.adi_get_stats(x)["device_bytes"] for x in hs8]
+        for x in hs8:
+            adi.adi_destroy(x)
+        assert max(b8) <= b1 / 6, (method, b1, b8)
+        s = adi.AdiSolver(n, n, h, 0.5 * h, 1.0, method)
+        full = s.stats()["device_bytes"]
+        y0, y1, halo, npos = adi.adi_band_info(s.handle)
+        adi.adi_set_band(s.handle, npos // 2, npos // 2 + 1024)
+        assert s.stats()["device_bytes"] <= full / 6
+        s.close()

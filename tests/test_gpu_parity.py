@@ -382,8 +382,8 @@ def _run_calls(adi, p, plan, carry, n_steps_table=None):
             s.set_point_sources([a[1]], [a[2]], a[3])
         elif a[0] == "media":
             s.set_media(a[1], a[2], a[3])
-        elif a[0] == "band":
-            adi.adi_set_band(s.handle, a[1], a[2])
+        elif a[0] == "band":   # back to the whole grid (all y positions)
+            adi.adi_set_band(s.handle, 0, adi.adi_band_info(s.handle)[3])
     out = s.get_fields()
     s.close()
     return out
@@ -420,11 +420,10 @@ def test_carry_invalidated_by_setters(adi, method, n):
     edges2 = tuple(rng.standard_normal(e.shape) for e in p.edges)
     U2, V2, W2 = (rng.standard_normal(a.shape) for a in (p.U, p.V, p.W))
     med = [rng.uniform(0.6, 1.0, a.shape).astype(np.float32) for a in (p.U, p.V, p.W)]
-    npos = p.ny if method == CFD else p.ny + 1
     ix, iy = p.U.shape[1] // 3, p.U.shape[0] // 2
     cases = ([("source", phi2, gf2)], [("fields", U2, V2, W2)], [("rho", 1.3)],
              [("boundary", edges2, gb2)], [("points", ix, iy, gf2)], [("media",) + tuple(med)],
-             [("band", 0, npos)], [("get",)], [("get_async",)])
+             [("band",)], [("get",)], [("get_async",)])
     for between in cases:
         plan = [2] + between + [2]
         a = _run_calls(adi, p, plan, 1)
