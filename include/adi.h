@@ -127,6 +127,13 @@ enum adi_param {
                            paper's own observation).  Same kernels, same
                            results bit for bit.  Plain and banded handles without ADI_EPS;
                            ignored for adi_create_dist ranks.  Default 0 */
+  ADI_THREAD_LINES = 12, /* the thread-per-line kernels (one thread runs one grid line through a
+                           half-step with the no-pivot LU of App. A) instead of
+                           the warp-per-line tiles: -1 (default) for lines of at most 64 cells,
+                           1 wherever they fit (<= ~260 cells), 0 never.  Plain handles of
+                           ADI_CFD / ADI_MFD with fixed K (no band, media, stopping rule,
+                           ADI_CFD_FULL, ADI_TILE_CHUNKS); results agree with the tile kernels
+                           to rounding (parity-tested against the oracle) */
 };
 
 /* Kernel kinds launched by adi_step (index of adi_get_kernel_times arrays). */

@@ -43,6 +43,7 @@ ADI_ABSORB_RATE = 8
 ADI_PREFETCH = 9
 ADI_CARRY = 10
 ADI_GRAPH = 11
+ADI_THREAD_LINES = 12
 KERNEL_KINDS = ("prologue", "row", "col", "final", "edge")
 
 _STATUS = {0: "ADI_OK", -1: "ADI_EINVAL", -2: "ADI_ENOMEM", -3: "ADI_ECUDA", -4: "ADI_EZEROPIVOT",

@@ -27,6 +27,7 @@
 
 #include "adi.h"
 #include "adi_line.cuh"
+#include "adi_thread.cuh"
 
 namespace adi {
 
@@ -160,6 +161,7 @@ struct adi_ctx {
   // ADI_GRAPH: each adi_step(n) is captured into a CUDA graph and launched at once; the
   // executable graph is kept and updated in place while the captured topology repeats
   int graph_on = 0;
+  int small = -1;   // ADI_THREAD_LINES: -1 auto (short lines), 0 off, 1 on where possible
   bool capturing = false;
   cudaStream_t gstream = nullptr;   // capture stream when the handle's stream is the legacy one
   cudaGraphExec_t gexec = nullptr;
@@ -816,8 +818,51 @@ int launch_het(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p) 
   return fail(h, ADI_EINVAL, "internal: no media kernel for this mode");
 }
 
+// ---- thread-per-line kernels for short lines (adi_thread.cuh) ----------
+#ifndef ADI_THREAD_AUTO_MAX
+#define ADI_THREAD_AUTO_MAX 64    // cells per line up to which the auto mode uses them (measured: faster at 40, slower at 80)
+#endif
+bool thread_mode(const adi_ctx* h) {
+  if (h->small == 0 || h->het || h->full || h->eps > 0.0 || h->tile_chunks > 0) return false;
+  if (h->band_y0 > 0 || h->band_y1 < h->ay.n + 1 || (h->dist && h->nranks > 1)) return false;
+  const int nmax = std::max(h->ax.n, h->ay.n);
+  if (h->small < 0) return nmax <= ADI_THREAD_AUTO_MAX;
+  return adi::thread_smem(nmax, 32) <= 200 * 1024;
+}
+
+template <int METHOD, int MODE>
+int launch_thread(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
+  auto kern = adi::adi_thread_kernel<METHOD, MODE>;
+  const int T = adi::thread_tpb(A.n);
+  const size_t smem = adi::thread_smem(A.n, T);
+  static size_t set_for[kMaxDev] = {};
+  if (set_for[h->dev] < smem) {
+    CUDA_TRY(h, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    set_for[h->dev] = 200 * 1024;
+  }
+  const int nl = std::max(A.l1 - p.line0, 0);
+  if (nl <= 0) return ADI_OK;
+  dim3 grid((nl + T - 1) / T, 1, h->batch);
+  kern<<<grid, T, smem, h->stream>>>(p);
+  CUDA_TRY(h, cudaGetLastError());
+  h->launches++;
+  if (!h->capturing) h->host_launches++;
+  return ADI_OK;
+}
+
 int launch(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p0, int kind) {
   TimeScope ts(h, kind);
+  if (thread_mode(h) && (mode == adi::KM_SWEEP || mode == adi::KM_FINAL || mode == adi::KM_PROLOGUE) &&
+      !p0.carry) {
+    adi::KParams p = p0;
+    const bool cfd = h->method == ADI_CFD;
+    if (mode == adi::KM_SWEEP) return cfd ? launch_thread<adi::M_CFD, adi::KM_SWEEP>(h, A, p)
+                                          : launch_thread<adi::M_MFD, adi::KM_SWEEP>(h, A, p);
+    if (mode == adi::KM_FINAL) return cfd ? launch_thread<adi::M_CFD, adi::KM_FINAL>(h, A, p)
+                                          : launch_thread<adi::M_MFD, adi::KM_FINAL>(h, A, p);
+    return cfd ? launch_thread<adi::M_CFD, adi::KM_PROLOGUE>(h, A, p)
+               : launch_thread<adi::M_MFD, adi::KM_PROLOGUE>(h, A, p);
+  }
   adi::KParams p = p0;
   p.trace = (kind == h->trace_kind) ? h->trace : nullptr;
   p.trace_cap = h->trace_cap;
@@ -1176,7 +1221,7 @@ int adi_set_param(adi_handle h, int key, double v) {
   // keys that size or plan work already enqueued by adi_step_begin (the stopping rule's
   // norm buffer, the tile plan, the carry buffer) cannot change inside a call
   if (h->in_call && (key == ADI_K_SWEEPS || key == ADI_EPS || key == ADI_K_MIN || key == ADI_TILE_CHUNKS ||
-                     key == ADI_CARRY || key == ADI_RHO))
+                     key == ADI_CARRY || key == ADI_RHO || key == ADI_THREAD_LINES))
     return fail(h, ADI_ESTATE, "call in progress");
   if (key == ADI_K_SWEEPS) {
     if (!(v >= 1) || v != std::floor(v) || v > 1000) return fail(h, ADI_EINVAL, "K must be an integer >= 1");
@@ -1220,6 +1265,10 @@ int adi_set_param(adi_handle h, int key, double v) {
     if (v != 0.0 && v != 1.0) return fail(h, ADI_EINVAL, "carry must be 0 or 1");
     h->carry_on = (int)v;
     if (!h->carry_on) h->carry_valid = false;
+  } else if (key == ADI_THREAD_LINES) {
+    if (v != 0.0 && v != 1.0 && v != -1.0) return fail(h, ADI_EINVAL, "thread lines must be -1, 0 or 1");
+    h->small = (int)v;
+    h->carry_valid = false;
   } else if (key == ADI_GRAPH) {
     if (v != 0.0 && v != 1.0) return fail(h, ADI_EINVAL, "graph must be 0 or 1");
     h->graph_on = (int)v;
@@ -1505,7 +1554,7 @@ int adi_set_media(adi_handle h, const float* kappa, const float* rinv_v, const f
 // stale), no stopping rule, no media, not the full-matrix variant.
 static bool carry_ok(const adi_ctx* h) {
   return h->carry_on && !h->full && !h->het && h->eps <= 0.0 && !h->dist && h->band_y0 <= 0 &&
-         h->band_y1 >= h->ay.n + 1;
+         h->band_y1 >= h->ay.n + 1 && !thread_mode(h);
 }
 
 // ---- one call = begin (prologue), n x {rows, cols}, end.  The phases are public so

@@ -33,8 +33,9 @@ def run_oracle(p, nsteps, **over):
     return oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, p.U, p.V, p.W, nsteps=nsteps, **kw)
 
 
-def run_gpu(adi, p, nsteps, chunks=0, split=None):
+def run_gpu(adi, p, nsteps, chunks=0, split=None, thread=-1):
     s = adi.AdiSolver.from_problem(p)
+    s.set_param(adi.ADI_THREAD_LINES, thread)
     if chunks:
         s.set_param(adi.ADI_TILE_CHUNKS, chunks)
     if split:
@@ -56,12 +57,37 @@ def oracle_sensitivity(p, nsteps, o):
     return [rel(c, b) for c, b in zip(o2, o)]
 
 
+@pytest.mark.parametrize("thread", [0, 1])
 @pytest.mark.parametrize("method", [CFD, MFD])
 @pytest.mark.parametrize("n", [9, 17, 33, 41, 100])
-def test_random_parity_small(adi, method, n):
-    """Random state, dense source, boundary data; single-tile lines incl. N=8 and ragged ends."""
+def test_random_parity_small(adi, method, n, thread):
+    """Random state, dense source, boundary data; single-tile lines incl. N=8 and ragged ends;
+    the warp-per-line generic tiles (thread 0) and the thread-per-line kernels (1)."""
     p = random_problem(method, n, seed=n, steps=3)
-    assert_parity(run_gpu(adi, p, 3), run_oracle(p, 3), what=f"n={n}")
+    assert_parity(run_gpu(adi, p, 3, thread=thread), run_oracle(p, 3), what=f"n={n} thread={thread}")
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+@pytest.mark.parametrize("n,ny", [(41, 41), (77, 130), (257, 257), (130, 9)])
+def test_thread_kernels_rectangles_batch_points(adi, method, n, ny):
+    """Thread-per-line kernels: rectangles, the largest forced size, split
+    calls (each call's prologue), a batch with point sources; rel L2 and max-norm."""
+    p = random_problem(method, n, seed=n + ny, steps=5, ny=ny)
+    assert_parity(run_gpu(adi, p, 5, split=[2, 3], thread=1), run_oracle(p, 5), what=f"thread {n}x{ny}")
+    B = 2
+    probs = [random_problem(method, n, seed=40 + b, steps=3, ny=ny) for b in range(B)]
+    s = adi.AdiSolver(n, ny, probs[0].h, probs[0].dt, 1.0, method, batch=B)
+    s.set_param(adi.ADI_THREAD_LINES, 1)
+    s.set_fields(np.stack([q.U for q in probs]), np.stack([q.V for q in probs]), np.stack([q.W for q in probs]))
+    ix, iy = [3, n // 2], [ny // 3, 2]
+    s.set_point_sources(ix, iy, probs[0].gf)
+    s.step(3)
+    got = s.get_fields()
+    s.close()
+    for b, q in enumerate(probs):
+        o = oracle.run(q.method, q.nx, q.ny, q.h, q.dt, q.c, q.K, q.U, q.V, q.W, nsteps=3,
+                       src=(ix[b], iy[b]), gf=probs[0].gf)
+        assert_parity([x[b] for x in got], o, what=f"thread batch {b}")
 
 
 @pytest.mark.parametrize("method", [CFD, MFD])
@@ -107,15 +133,17 @@ def test_split_calls_equal_one_call(adi, method):
     assert_parity(a, run_oracle(p, 5))
 
 
-def test_mfd_mms_ladder_parity(adi):
-    """Config 2: MFD, Γ=0, 5T, cfl 0.81, K=8 on 41, 81, 161 nodes — full runs.
+@pytest.mark.parametrize("thread", [0, 1])
+def test_mfd_mms_ladder_parity(adi, thread):
+    """Config 2: MFD, Γ=0, 5T, cfl 0.81, K=8 on 41, 81, 161 nodes — full runs, with the
+    tile kernels and with the thread-per-line kernels.
     At t = 5T the exact V̄, W̄ vanish (∝ sin ωt), so their relative error is
     judged against the oracle's own sensitivity; U at 1e-12 outright."""
     T = 1 / math.sqrt(2)
     for n in (41, 81, 161):
         p = mms_problem(MFD, n, MMS(), t_sim=5 * T)
         st = p.meta["steps"]
-        g, o = run_gpu(adi, p, st), run_oracle(p, st)
+        g, o = run_gpu(adi, p, st, thread=thread), run_oracle(p, st)
         assert rel(g[0], o[0]) <= TOL
         assert_parity(g, o, what=f"MFD MMS n={n}", floor=oracle_sensitivity(p, st, o))
 
@@ -127,19 +155,21 @@ def test_mfd_mms_midrun_parity(adi, n, steps):
     assert_parity(run_gpu(adi, p, steps), run_oracle(p, steps), what=f"MFD MMS n={n} @{steps}")
 
 
-def test_cfd_config1_short_parity(adi):
+@pytest.mark.parametrize("thread", [0, -1])
+def test_cfd_config1_short_parity(adi, thread):
     """Config 1 (CFD 41x41, Γ=0, Δt = 0.91 h) for the first 60 steps at 1e-12
     (beyond ~75 steps the literal CFD reading has amplified round-off past 1e-12
     in ANY implementation: SURVEY fact 5-6)."""
     p = mms_problem(CFD, 41, MMS(), steps=200)
-    assert_parity(run_gpu(adi, p, 60), run_oracle(p, 60), what="CFD config1 60 steps")
+    assert_parity(run_gpu(adi, p, 60, thread=thread), run_oracle(p, 60), what="CFD config1 60 steps")
 
 
-def test_cfd_config1_full_within_roundoff_amplification(adi):
+@pytest.mark.parametrize("thread", [0, -1])
+def test_cfd_config1_full_within_roundoff_amplification(adi, thread):
     """Config 1 over all 200 steps, judged against the oracle's own 1-ulp
     sensitivity (x10 margin)."""
     p = mms_problem(CFD, 41, MMS(), steps=200)
-    g, o = run_gpu(adi, p, 200), run_oracle(p, 200)
+    g, o = run_gpu(adi, p, 200, thread=thread), run_oracle(p, 200)
     assert_parity(g, o, what="CFD config1 200 steps", floor=oracle_sensitivity(p, 200, o))
 
 
