@@ -62,6 +62,9 @@ def parse():
                          "1 = CFD 41^2, 200 steps; 2 = the MFD ladder 41..321 to 5T; 3 = Gamma=k in {2, 9} at "
                          "1601^2, CFD and MFD, 100 timed steps.  One JSON line; 0 = config 4 (the default)")
     ap.add_argument("--no-graph", action="store_true", help="configs 1-3: plain launches instead of ADI_GRAPH")
+    ap.add_argument("--dist-mode", default="halo", choices=["halo", "transpose"],
+                    help="N > 1 (and --dist-local): the band decomposition with halo exchange (default) or "
+                         "the north_star's all-to-all transpose between the half-steps (ADI_DIST_TRANSPOSE)")
     ap.add_argument("--dist-local", type=int, default=0,
                     help="P > 1: the grid band-decomposed over P ranks of adi_create_dist_local on ONE GPU "
                          "(the library's multi-GPU code path with a loopback transport; a functional check "
@@ -259,9 +262,9 @@ def kernel_flops(method, n, kind, K):
 class LocalRanks:
     """The ranks of adi_create_dist_local as one solver (bench.py --dist-local P)."""
 
-    def __init__(self, adi, p, m, P, K, stream):
+    def __init__(self, adi, p, m, P, K, stream, mode=0):
         self.adi = adi
-        hs = adi.adi_create_dist_local(p.nx, p.ny, p.h, p.dt, p.c, m, 1, P)
+        hs = adi.adi_create_dist_local(p.nx, p.ny, p.h, p.dt, p.c, m, 1, P, mode)
         self.hs = hs
         self.ranks = [adi.AdiSolver.adopt(h, p.nx, p.ny, p.h, p.dt, p.c, m, K=K, stream=stream) for h in hs]
         self.handle = hs[0]
@@ -307,6 +310,7 @@ def run_ours(a, ws, rank, local):
     total_steps = a.warmup + a.steps
     solvers = {}
     uid = None
+    dmode = adi.ADI_DIST_TRANSPOSE if a.dist_mode == "transpose" else adi.ADI_DIST_HALO
     if ws > 1:
         import torch.distributed as tdist
         box = [adi.adi_nccl_unique_id() if rank == 0 else None]
@@ -315,10 +319,10 @@ def run_ours(a, ws, rank, local):
     for m in methods:
         p = make_problem(m, n, total_steps + a.steps + 4, a.K, a.media)
         if ws > 1:
-            hd, st = adi.adi_create_dist(p.nx, p.ny, p.h, p.dt, p.c, m, 1, uid, rank, ws)
+            hd, st = adi.adi_create_dist_ex(p.nx, p.ny, p.h, p.dt, p.c, m, 1, uid, rank, ws, dmode)
             s = adi.AdiSolver.adopt(hd, p.nx, p.ny, p.h, p.dt, p.c, m, K=a.K, stream=stream.cuda_stream, status=st)
         elif a.dist_local > 1:
-            s = LocalRanks(adi, p, m, a.dist_local, a.K, stream.cuda_stream)
+            s = LocalRanks(adi, p, m, a.dist_local, a.K, stream.cuda_stream, dmode)
         else:
             s = adi.AdiSolver(p.nx, p.ny, p.h, p.dt, p.c, m, K=a.K, stream=stream.cuda_stream)
         s.set_fields(p.U, p.V, p.W)
@@ -334,7 +338,7 @@ def run_ours(a, ws, rank, local):
         p.V = p.W = None  # zeros for the MMS start; recreated for the e2e leg
         bs = None
         p.rows = (0, p.U.shape[0])
-        if ws > 1:
+        if ws > 1 and dmode == adi.ADI_DIST_HALO:
             y0, y1, halo, npos = adi.adi_band_info(s.handle)
             bs = {"y0": y0, "y1": y1, "halo": halo, "npos": npos}
             # a banded handle transfers only the rows it uses (adi_set_fields, include/adi.h):
@@ -455,7 +459,7 @@ def run_ours(a, ws, rank, local):
                "note": "adi_set_fields_async(pinned host) + adi_step(K) + adi_get_fields_async(pinned host) "
                        "per method, the two methods on two streams (copies overlap the other "
                        "method's steps), host wall clock from the first copy to the last result"}
-    elif not a.no_e2e and ws > 1:
+    elif not a.no_e2e and ws > 1 and a.dist_mode == "halo":
         e2e_ms = 0.0
         bi = bo = 0
         for m, (s, p, bs) in solvers.items():
@@ -852,9 +856,13 @@ def main():
            "parallelism": "1 GPU" if ws == 1 else
            f"{ws} GPUs: one grid band-decomposed (rows) by adi_create_dist, band-local arrays, NCCL "
            f"halo exchange inside adi_step overlapping the column sweep"}
+    if ws > 1 and a.dist_mode == "transpose":
+        cfg["parallelism"] = (f"{ws} GPUs: one grid, rows and columns owned by different ranks "
+                              f"(adi_create_dist_ex ADI_DIST_TRANSPOSE), NCCL all-to-all of S between the half-steps")
     if a.dist_local > 1:
-        cfg["parallelism"] = (f"1 GPU running {a.dist_local} ranks of adi_create_dist_local (band-local arrays, "
-                              f"loopback halo exchange): the decomposition's overhead, not a scaling number")
+        cfg["parallelism"] = (f"1 GPU running {a.dist_local} ranks of adi_create_dist_local ({a.dist_mode} mode, "
+                              f"band-local arrays, loopback exchange): the decomposition's overhead, not a scaling "
+                              f"number")
     if a.full:
         cfg["workload"] = (f"config4 size: single {a.n}x{a.n}-node grid, full-matrix CFD variant (NEXT row "
                            f"f4, ADI_CFD_FULL: every node unknown, no Dirichlet data) with a Cerjan layer "

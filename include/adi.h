@@ -279,6 +279,22 @@ int adi_band_info(adi_handle h, int* y0, int* y1, int* halo, int* npos);
  * do not exchange: drivers that call them exchange through adi_halo_pack/unpack. */
 int adi_create_dist(int nx, int ny, double h, double dt, double c, int method, int batch,
                     const void* nccl_unique_id, int rank, int nranks, adi_handle* out);
+/* The decomposition of adi_create_dist_ex / adi_create_dist_local_ex:
+ *   ADI_DIST_HALO (the default of adi_create_dist): bands of y positions; each rank keeps
+ *     its band plus a halo and exchanges the halo rows with its two neighbours (§7.1-7.2);
+ *   ADI_DIST_TRANSPOSE (the north_star's plan): rank r owns the rows Y_r for the
+ *     row sweep and the columns X_r for the column sweep (the cuts of adi_dist_bands over the
+ *     y and the x positions); S moves to its next owner by an all-to-all (NCCL grouped
+ *     send/recv, or loopback copies) after the prologue, every row sweep and every column
+ *     sweep but the last (§7.3).  adi_set/get_fields: U and W̄ on the columns, V̄ on the
+ *     rows (a get returns the owned ones: adi_dist_info).  No media, no halo calls. */
+enum { ADI_DIST_HALO = 0, ADI_DIST_TRANSPOSE = 1 };
+int adi_create_dist_ex(int nx, int ny, double h, double dt, double c, int method, int batch,
+                       const void* nccl_unique_id, int rank, int nranks, int mode, adi_handle* out);
+/* This rank's decomposition: mode, the owned rows [rows0, rows1) (y positions: V̄ and, in
+ * halo mode, U and W̄) and columns [cols0, cols1) (x positions: U and W̄ in transpose
+ * mode; all columns in halo mode).  A plain handle: mode halo, everything owned. */
+int adi_dist_info(adi_handle h, int* mode, int* rows0, int* rows1, int* cols0, int* cols1);
 int adi_nccl_unique_id(void* out128);
 /* All `nranks` ranks of the same decomposition in ONE process on the current device
  * (out[0..nranks-1]), exchanging through loopback device copies instead of NCCL: the
@@ -291,6 +307,8 @@ int adi_nccl_unique_id(void* out128);
  * adi_create_dist.  Destroy all handles. */
 int adi_create_dist_local(int nx, int ny, double h, double dt, double c, int method, int batch, int nranks,
                           adi_handle* out);
+int adi_create_dist_local_ex(int nx, int ny, double h, double dt, double c, int method, int batch, int nranks,
+                             int mode, adi_handle* out);
 int adi_step_dist_local(adi_handle* handles, int nranks, int n);
 /* The band cuts of y positions [0, npos) over nranks: cuts[0..nranks] (host logic only). */
 int adi_dist_bands(int npos, int nranks, int* cuts);

@@ -44,6 +44,8 @@ ADI_PREFETCH = 9
 ADI_CARRY = 10
 ADI_GRAPH = 11
 ADI_THREAD_LINES = 12
+ADI_DIST_HALO = 0
+ADI_DIST_TRANSPOSE = 1
 KERNEL_KINDS = ("prologue", "row", "col", "final", "edge")
 
 _STATUS = {0: "ADI_OK", -1: "ADI_EINVAL", -2: "ADI_ENOMEM", -3: "ADI_ECUDA", -4: "ADI_EZEROPIVOT",
@@ -91,6 +93,9 @@ def lib():
         L.adi_nccl_unique_id.argtypes = [P]
         L.adi_dist_bands.argtypes = [I, I, P]
         try:   # (absent from libraries built before round 2: tools/ab_lib.py loads those too)
+            L.adi_create_dist_ex.argtypes = [I, I, D, D, D, I, I, P, I, I, I, ctypes.POINTER(H)]
+            L.adi_create_dist_local_ex.argtypes = [I, I, D, D, D, I, I, I, I, ctypes.POINTER(H)]
+            L.adi_dist_info.argtypes = [H] + [ctypes.POINTER(I)] * 5
             L.adi_plan_halo.argtypes = [I, ctypes.POINTER(I)]
             L.adi_create_dist_local.argtypes = [I, I, D, D, D, I, I, I, ctypes.POINTER(H)]
             L.adi_step_dist_local.argtypes = [ctypes.POINTER(H), I, I]
@@ -123,7 +128,8 @@ def lib():
 
 EXPORTS = ["adi_create", "adi_create_batch", "adi_set_param", "adi_set_stream", "adi_set_fields",
            "adi_set_fields_device", "adi_set_source", "adi_set_point_sources", "adi_set_boundary",
-           "adi_set_media", "adi_create_dist", "adi_nccl_unique_id", "adi_dist_bands", "adi_plan_halo", "adi_create_dist_local", "adi_step_dist_local", "adi_step", "adi_step_begin", "adi_step_rows", "adi_step_cols", "adi_step_end", "adi_set_band",
+           "adi_set_media", "adi_create_dist", "adi_nccl_unique_id", "adi_dist_bands", "adi_plan_halo", "adi_create_dist_local", "adi_step_dist_local", "adi_create_dist_ex",
+           "adi_create_dist_local_ex", "adi_dist_info", "adi_step", "adi_step_begin", "adi_step_rows", "adi_step_cols", "adi_step_end", "adi_set_band",
            "adi_band_info", "adi_halo_bytes", "adi_halo_pack", "adi_halo_unpack",
            "adi_get_fields", "adi_get_fields_device", "adi_set_fields_async", "adi_get_fields_async", "adi_get_stats", "adi_get_kernel_times",
            "adi_set_trace", "adi_get_last_sweeps", "adi_last_error",
@@ -177,14 +183,34 @@ def adi_create_dist(nx, ny, h, dt, c, method, batch, unique_id, rank, nranks):
     return hd, rc
 
 
-def adi_create_dist_local(nx, ny, h, dt, c, method, batch, nranks):
+def adi_create_dist_ex(nx, ny, h, dt, c, method, batch, unique_id, rank, nranks, mode):
+    """adi_create_dist with the decomposition mode (ADI_DIST_HALO / ADI_DIST_TRANSPOSE)."""
+    hd = ctypes.c_void_p()
+    uid = None if unique_id is None else ctypes.create_string_buffer(bytes(unique_id), 128)
+    rc = lib().adi_create_dist_ex(nx, ny, h, dt, c, method, batch, uid, rank, nranks, mode, ctypes.byref(hd))
+    _check(None, rc, "adi_create_dist_ex")
+    return hd, rc
+
+
+def adi_dist_info(hd):
+    """(mode, rows0, rows1, cols0, cols1): the owned rows (y) and columns (x) of a rank."""
+    v = [ctypes.c_int(0) for _ in range(5)]
+    _check(hd, lib().adi_dist_info(hd, *[ctypes.byref(x) for x in v]), "adi_dist_info")
+    return tuple(int(x.value) for x in v)
+
+
+def adi_create_dist_local(nx, ny, h, dt, c, method, batch, nranks, mode=0):
     """All ranks of a line-sharded grid in this process on the current device (loopback
     transport, include/adi.h); returns the list of handles."""
     hs = (ctypes.c_void_p * nranks)()
-    rc = lib().adi_create_dist_local(nx, ny, h, dt, c, method, batch, nranks, hs)
+    rc = lib().adi_create_dist_local_ex(nx, ny, h, dt, c, method, batch, nranks, mode, hs)
     if rc < 0:
         raise AdiError(rc, f"adi_create_dist_local: {_STATUS.get(rc, rc)}")
     return [ctypes.c_void_p(x) for x in hs]
+
+
+def adi_create_dist_local_ex(nx, ny, h, dt, c, method, batch, nranks, mode):
+    return adi_create_dist_local(nx, ny, h, dt, c, method, batch, nranks, mode)
 
 
 def adi_step_dist_local(handles, n):

@@ -147,6 +147,21 @@ struct adi_ctx {
   // device (adi_create_dist_local), loopback copies from the neighbours' send buffers
   bool loop = false;
   adi_ctx* peer[2] = {nullptr, nullptr};   // loopback: the low / high neighbour handle
+  // ADI_DIST_TRANSPOSE (the north_star's decomposition): rank r
+  // owns the rows Y_r = [ty0, ty1) for the row sweep and the columns X_r = [tx0, tx1) for the
+  // column sweep; S changes owner between the half-steps by an all-to-all.  Row-side
+  // arrays (Sa, V, V2, phi) hold rows [ya, yb) ⊇ Y_r; the row sweep writes S2^T into Sb
+  // ([x][y in [ya, yb)]).  Column-side arrays Sc (S2^T input), W, W2, phiT hold the rows
+  // x in [xa, xb) ⊇ X_r with all y (pitch pc); the column sweep writes S1'^T into Sd and U
+  // ([y][x in [xa, xb)], pitch pd = pu).
+  bool tmode = false;
+  int ty0 = 0, ty1 = 0, tx0 = 0, tx1 = 0, xa = 0, xb = 0, pc = 0, pd = 0;
+  size_t aC = 0;                      // per-grid size of Sc, Sd (common batch stride)
+  double *Sc = nullptr, *Sd = nullptr;
+  std::vector<int> cut_y, cut_x;      // the ranks' Y_q, X_q
+  adi_ctx** group = nullptr;          // loopback: all ranks (adi_create_dist_local)
+  std::vector<double*> tsend, trecv;  // NCCL staging per peer (transpose mode)
+  std::vector<size_t> tcount;
   cudaStream_t cs = nullptr;               // exchange stream (overlaps the column sweep)
   cudaEvent_t ev_pack = nullptr, ev_recv = nullptr;
   // internal layouts: Sa, V, V2 row-major; Sb = S^T; W, W2 = W̄^T (columns contiguous)
@@ -350,6 +365,17 @@ int tmap_for(adi_ctx* h, const double* ptr, CUtensorMap* out) {
   size_t bs;
   const int nyb = h->yb - h->ya;   // rows of the band-local row-indexed arrays
   const double* raw = nullptr;     // the allocation (TMA coordinates: tline0 / tpos0)
+  if (h->tmode && (ptr == h->Sc || ptr == h->W || ptr == h->W2 || ptr == h->phiT)) {
+    adi_ctx::TMap e;
+    e.ptr = ptr;
+    const size_t bs = (ptr == h->W || ptr == h->W2) ? h->aW : h->aC;
+    int rc = encode_lines(h, ptr + (ptrdiff_t)h->xa * h->pc, h->pc, h->xb - h->xa, bs,
+                          ptr == h->phiT ? 1 : h->batch, &e.map);
+    if (rc) return rc;
+    h->tmaps.push_back(e);
+    *out = e.map;
+    return ADI_OK;
+  }
   auto rr = [&](int pt) { return rows_raw(h, const_cast<double*>(ptr), pt); };
   auto rc_ = [&]() { return cols_raw(h, const_cast<double*>(ptr)); };
   if (ptr == h->Sa) { pitch = h->pa; rows = nyb; bs = h->aS; raw = rr(pitch); }
@@ -922,12 +948,12 @@ int transpose(adi_ctx* h, const double* in, double* out, int R, int C, long long
 
 // Dirichlet columns (x = 0, x = 1) of U at time factor gb, all rows (corners included)
 __global__ void edge_cols_kernel(double* U, int r0, int r1, int nxu, int pu, long long ubatch,
-                                 const double* ex0, const double* ex1, double gb) {
+                                 const double* ex0, const double* ex1, double gb, int lo, int hi) {
   const int r = r0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= r1) return;
   double* Ub = U + blockIdx.y * ubatch + (long long)r * pu;
-  Ub[0] = ex0 ? ex0[r] * gb : 0.0;
-  Ub[nxu - 1] = ex1 ? ex1[r] * gb : 0.0;
+  if (lo) Ub[0] = ex0 ? ex0[r] * gb : 0.0;
+  if (hi) Ub[nxu - 1] = ex1 ? ex1[r] * gb : 0.0;
 }
 double tabv(const std::vector<double>& g, long long j) { return g.empty() ? 1.0 : g[(size_t)j]; }
 
@@ -959,6 +985,12 @@ adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
   p.s_batch = (long long)h->aS;
   p.x_batch = (long long)(ydir ? h->aW : h->aV);
   p.u_batch = (long long)h->aU;
+  if (h->tmode && ydir) {   // column side of the transpose decomposition (adi_ctx::tmode)
+    p.s_line = h->pc; p.so_pt = h->pd;
+    p.x_line = h->pc;
+    p.u_line = 1; p.u_pt = h->pd;
+    p.s_batch = (long long)h->aC;
+  }
   p.pt_line = h->has_pt ? A.d_ptl : nullptr;
   p.pt_pos = h->has_pt ? A.d_ptp : nullptr;
   p.pt_amp = 1.0 / (h->h * h->h);
@@ -987,6 +1019,12 @@ adi::KParams base_params(adi_ctx* h, const adi::Axis& A, bool ydir) {
   p.tpos0 = ydir ? h->ya : 0;
   p.pos_lo = ydir ? h->ya : -(1 << 30);
   p.pos_hi = ydir ? h->yb : (1 << 30);
+  if (h->tmode && ydir) {   // column-side arrays: the lines (rows) x start at xa, all y
+    p.tline0 = h->xa;
+    p.tpos0 = 0;
+    p.pos_lo = 0;
+    p.pos_hi = h->nyu;
+  }
   return p;
 }
 
@@ -1025,6 +1063,7 @@ void free_ctx(adi_ctx* h) {
         if (b) { cudaFree(b); b = nullptr; }
   if (h->comm && g_nccl.ok) g_nccl.commDestroy(h->comm);
   h->comm = nullptr;
+  if (h->group) delete[] h->group;
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->gstream) cudaStreamDestroy(h->gstream);
   if (h->ev_pack) cudaEventDestroy(h->ev_pack);
@@ -1036,11 +1075,21 @@ void free_ctx(adi_ctx* h) {
         if (back == h) back = nullptr;
   for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
-  for (double* q : {rows_raw(h, h->Ubase, h->pu), rows_raw(h, h->V, h->pv), rows_raw(h, h->V2, h->pv),
-                    rows_raw(h, h->Sa, h->pa), rows_raw(h, h->phi, h->pa), rows_raw(h, h->Ca, h->pa),
-                    cols_raw(h, h->W), cols_raw(h, h->W2), cols_raw(h, h->W3), cols_raw(h, h->Sb),
-                    cols_raw(h, h->phiT), cols_raw(h, h->Cb)})
-    dfree(q);
+  if (h->tmode) {
+    auto cr = [&](double* q) { return q ? q + (ptrdiff_t)h->xa * h->pc : nullptr; };
+    for (double* q : {h->Ubase ? h->Ubase + h->xa : nullptr, rows_raw(h, h->V, h->pv), rows_raw(h, h->V2, h->pv),
+                      rows_raw(h, h->Sa, h->pa), rows_raw(h, h->phi, h->pa), cr(h->W), cr(h->W2), cr(h->Sc),
+                      cr(h->phiT), cols_raw(h, h->Sb), h->Sd ? h->Sd + h->xa : nullptr})
+      dfree(q);
+    for (double* q : h->tsend) if (q) cudaFree(q);
+    for (double* q : h->trecv) if (q) cudaFree(q);
+  } else {
+    for (double* q : {rows_raw(h, h->Ubase, h->pu), rows_raw(h, h->V, h->pv), rows_raw(h, h->V2, h->pv),
+                      rows_raw(h, h->Sa, h->pa), rows_raw(h, h->phi, h->pa), rows_raw(h, h->Ca, h->pa),
+                      cols_raw(h, h->W), cols_raw(h, h->W2), cols_raw(h, h->W3), cols_raw(h, h->Sb),
+                      cols_raw(h, h->phiT), cols_raw(h, h->Cb)})
+      dfree(q);
+  }
   for (void* q : {(void*)h->edges, (void*)h->flag, (void*)h->d_norms, (void*)h->d_k, (void*)h->d_taper})
     if (q) cudaFree(q);
   for (adi::Axis* A : {&h->ax, &h->ay})
@@ -1311,6 +1360,58 @@ static void field_rows(adi_ctx* h, bool with_halo, int* ya, int* yb) {
   *yb = (h->band_y1 >= npos) ? h->nyu : std::min(h->band_y1 + hl, h->nyu);
 }
 
+// ---- fields of a transpose-mode rank (adi_ctx::tmode): U and W̄ on the column side (all
+// rows, the columns [xa, xb)), V̄ on the row side (the rows [ya, yb)); a get returns the
+// owned rows Y_r of V̄ and the owned columns X_r of U and W̄
+static int tm_fields(adi_ctx* h, double* U, double* V, double* W, cudaMemcpyKind kind, bool set) {
+  const int off = h->off;
+  const int x0 = set ? h->xa : h->tx0, x1 = set ? h->xb : (h->tx1 >= h->ax.n + 1 ? h->nxu : h->tx1);
+  const int y0 = set ? h->ya : h->ty0, y1 = set ? h->yb : (h->ty1 >= h->ay.n + 1 ? h->nyu : h->ty1);
+  const int ja = std::max(y0 - off, 0), jb = std::min(y1 - off, h->nyi);
+  const int ia = std::max(x0 - off, 0), ib = std::min(x1 - off, h->nxi);
+  double* scratch = h->W2 + (ptrdiff_t)h->xa * h->pc;   // W2's allocation as a dense buffer
+  for (int b = 0; b < h->batch; ++b) {
+    double* Ui = h->U + b * h->aU + x0;
+    double* Uu = U + b * h->nU + x0;
+    if (set) CUDA_TRY(h, cudaMemcpy2DAsync(Ui, h->pd * 8, Uu, h->nxu * 8, (x1 - x0) * 8, h->nyu, kind, h->stream));
+    else CUDA_TRY(h, cudaMemcpy2DAsync(Uu, h->nxu * 8, Ui, h->pd * 8, (x1 - x0) * 8, h->nyu, kind, h->stream));
+    if (jb > ja) {
+      double* Vi = h->V + b * h->aV + (size_t)(ja + off) * h->pv;
+      double* Vu = V + b * h->nV + (size_t)ja * h->nxv;
+      if (set) CUDA_TRY(h, cudaMemcpy2DAsync(Vi, h->pv * 8, Vu, h->nxv * 8, h->nxv * 8, jb - ja, kind, h->stream));
+      else CUDA_TRY(h, cudaMemcpy2DAsync(Vu, h->nxv * 8, Vi, h->pv * 8, h->nxv * 8, jb - ja, kind, h->stream));
+    }
+    if (ib > ia) {   // W̄ columns [ia, ib) (dense user rows y) <-> W̄^T rows x = i + off
+      double* Wi = h->W + b * h->aW + (size_t)(ia + off) * h->pc;
+      double* Wu = W + b * h->nW + ia;
+      if (set) {
+        CUDA_TRY(h, cudaMemcpy2DAsync(scratch, (ib - ia) * 8, Wu, h->nxi * 8, (ib - ia) * 8, h->nyv, kind, h->stream));
+        int rc = transpose(h, scratch, Wi, h->nyv, ib - ia, ib - ia, h->pc, 1, 0, 0);
+        if (rc) return rc;
+      } else {
+        int rc = transpose(h, Wi, scratch, ib - ia, h->nyv, h->pc, ib - ia, 1, 0, 0);
+        if (rc) return rc;
+        CUDA_TRY(h, cudaMemcpy2DAsync(Wu, h->nxi * 8, scratch, (ib - ia) * 8, (ib - ia) * 8, h->nyv, kind, h->stream));
+      }
+    }
+  }
+  return ADI_OK;
+}
+static int tm_set_fields(adi_ctx* h, const double* U, const double* V, const double* W, cudaMemcpyKind kind,
+                         bool sync) {
+  int rc = tm_fields(h, const_cast<double*>(U), const_cast<double*>(V), const_cast<double*>(W), kind, true);
+  if (rc) return rc;
+  if (kind == cudaMemcpyHostToDevice && sync) CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  h->fields_set = true;
+  return ADI_OK;
+}
+static int tm_get_fields(adi_ctx* h, double* U, double* V, double* W, cudaMemcpyKind kind, bool sync) {
+  int rc = tm_fields(h, U, V, W, kind, false);
+  if (rc) return rc;
+  if (kind == cudaMemcpyDeviceToHost && sync) CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  return ADI_OK;
+}
+
 static int set_fields_impl(adi_handle h, const double* U, const double* V, const double* W,
                            cudaMemcpyKind kind, bool sync = true) {
   DevGuard dg_(h);
@@ -1320,6 +1421,7 @@ static int set_fields_impl(adi_handle h, const double* U, const double* V, const
   if (!U || !V || !W) return fail(h, ADI_EINVAL, "null field pointer");
   if (h->in_call) return fail(h, ADI_ESTATE, "call in progress");
   const size_t B = (size_t)h->batch;
+  if (h->tmode) return tm_set_fields(h, U, V, W, kind, sync);
   int ya, yb;
   field_rows(h, true, &ya, &yb);
   const int off = h->off;   // V̄ row j = y position j + off
@@ -1409,13 +1511,33 @@ int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double
         h->phi = rows_in(h, r, h->pa);
       }
       if (!h->phiT) {
-        double* r = halloc(h, h->aS + kSrcSlack);
+        const size_t n = (h->tmode ? h->aC : h->aS) + kSrcSlack;
+        double* r = halloc(h, n);
         if (!r) return fail(h, ADI_ENOMEM, "source pattern");
-        h->phiT = cols_in(h, r);
+        h->phiT = h->tmode ? r - (ptrdiff_t)h->xa * h->pc : cols_in(h, r);
       }
     }
     CUDA_TRY(h, cudaMemsetAsync(rows_raw(h, h->phi, h->pa), 0, (h->aS + kSrcSlack) * 8, h->stream));
-    CUDA_TRY(h, cudaMemsetAsync(cols_raw(h, h->phiT), 0, (h->aS + kSrcSlack) * 8, h->stream));
+    if (h->tmode) {
+      // the column side: phiT rows x in [xa, xb) (all y), from the user's columns
+      CUDA_TRY(h, cudaMemsetAsync(h->phiT + (ptrdiff_t)h->xa * h->pc, 0, (h->aC + kSrcSlack) * 8, h->stream));
+      const int off = h->off;
+      const int ia = std::max(h->xa - off, 0), ib = std::min(h->xb - off, h->nxi);
+      if (ib > ia) {
+        double* tmp = nullptr;
+        CUDA_TRY(h, cudaMalloc(&tmp, (size_t)h->nyi * (ib - ia) * 8));
+        cudaError_t e = cudaMemcpy2DAsync(tmp, (ib - ia) * 8, phi + ia, h->nxi * 8, (ib - ia) * 8, h->nyi,
+                                          cudaMemcpyHostToDevice, h->stream);
+        int rc = e == cudaSuccess ? transpose(h, tmp, h->phiT + (size_t)(ia + off) * h->pc + off, h->nyi, ib - ia,
+                                              ib - ia, h->pc, 1, 0, 0)
+                                  : fail(h, ADI_ECUDA, "source copy");
+        cudaStreamSynchronize(h->stream);
+        cudaFree(tmp);
+        if (rc) return rc;
+      }
+    } else {
+      CUDA_TRY(h, cudaMemsetAsync(cols_raw(h, h->phiT), 0, (h->aS + kSrcSlack) * 8, h->stream));
+    }
     // interior point (j, i) of the user's block is position (y, x) = (j + off, i + off);
     // a band-local handle keeps the rows y in [ya, yb)
     const int off = h->off;
@@ -1423,15 +1545,18 @@ int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double
     if (y1 > y0) {
       CUDA_TRY(h, cudaMemcpy2DAsync(h->phi + (size_t)y0 * h->pa + off, h->pa * 8, phi + (size_t)(y0 - off) * h->nxi,
                                     h->nxi * 8, h->nxi * 8, y1 - y0, cudaMemcpyHostToDevice, h->stream));
-      int rc = transpose(h, h->phi + (size_t)y0 * h->pa + off, h->phiT + (size_t)off * h->pb + y0, y1 - y0, h->nxi,
-                         h->pa, h->pb, 1, 0, 0);
-      if (rc) return rc;
+      if (!h->tmode) {
+        int rc = transpose(h, h->phi + (size_t)y0 * h->pa + off, h->phiT + (size_t)off * h->pb + y0, y1 - y0,
+                           h->nxi, h->pa, h->pb, 1, 0, 0);
+        if (rc) return rc;
+      }
     }
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   } else if (h->phi) {
     h->tmaps.clear();
     hfree(h, rows_raw(h, h->phi, h->pa), h->aS + kSrcSlack);
-    hfree(h, cols_raw(h, h->phiT), h->aS + kSrcSlack);
+    if (h->tmode) hfree(h, h->phiT + (ptrdiff_t)h->xa * h->pc, h->aC + kSrcSlack);
+    else hfree(h, cols_raw(h, h->phiT), h->aS + kSrcSlack);
     h->phi = nullptr;
     h->phiT = nullptr;
   }
@@ -1490,6 +1615,7 @@ int adi_set_media(adi_handle h, const float* kappa, const float* rinv_v, const f
     return ADI_OK;
   }
   if (!kappa || !rinv_v || !rinv_w) return fail(h, ADI_EINVAL, "kappa, rinv_v, rinv_w: all or none");
+  if (h->tmode) return fail(h, ADI_EINVAL, "media fields are not available in the transpose decomposition");
   if (h->full) return fail(h, ADI_EINVAL, "media fields are not available for the full-matrix variant");
   // values: finite and > 0; the CFL bound uses max kappa * max rho^-1 >= c_max^2
   double kmax = 0, rmax = 0;
@@ -1575,6 +1701,8 @@ int adi_step_begin(adi_handle h, int nsteps) {
     return fail(h, ADI_EINVAL, "the stopping rule (ADI_EPS > 0) is not available for the full-matrix variant");
   if (h->eps > 0.0 && h->het)
     return fail(h, ADI_EINVAL, "the stopping rule (ADI_EPS > 0) is not available with media fields");
+  if (h->eps > 0.0 && h->dist && h->nranks > 1)
+    return fail(h, ADI_EINVAL, "the stopping rule (ADI_EPS > 0) needs the whole grid on one handle");
   if (h->eps > 0.0) {
     // the stopping rule tests norms of the whole grid: no band decomposition
     if (h->band_y0 > 0 || h->band_y1 < h->ay.n + 1)
@@ -1614,7 +1742,7 @@ int adi_step_begin(adi_handle h, int nsteps) {
     adi::KParams p = base_params(h, h->ay, true);
     p.U_in = h->U;
     p.X_in = h->W; p.X_out = h->W2;
-    p.S_out = h->Sa;
+    p.S_out = h->tmode ? h->Sd : h->Sa;
     p.gf = tabv(h->gf, 2 * m0);
     if ((rc = launch(h, adi::KM_PROLOGUE, h->ay, p, ADI_KK_PROLOGUE))) return rc;
     h->Vcur = h->V; h->Valt = h->V2;
@@ -1650,7 +1778,7 @@ int adi_step_cols(adi_handle h) {
   const long long m = h->m;
   const bool last = (m + 1 == h->call_m1);
   adi::KParams p = base_params(h, h->ay, true);
-  p.S_in = h->Sb;
+  p.S_in = h->tmode ? h->Sc : h->Sb;
   p.X_in = h->Wcur;
   p.gb = tabv(h->gb, 2 * m + 2);
   p.gf = tabv(h->gf, 2 * m + 2);
@@ -1703,7 +1831,7 @@ int adi_step_cols(adi_handle h) {
     if (rc) return rc;
     if (h->Wcur == h->W) std::swap(h->W, h->W2);
   } else {
-    p.S_out = h->Sa;
+    p.S_out = h->tmode ? h->Sd : h->Sa;
     p.X_out = h->Walt;
     rc = (h->eps > 0.0) ? stage_with_rule(h, adi::KM_SWEEP_T, h->ay, p, ADI_KK_COL, 1)
                         : cols(adi::KM_SWEEP, ADI_KK_COL);
@@ -1720,12 +1848,15 @@ int adi_step_end(adi_handle h) {
   if (!h->in_call || h->m != h->call_m1) return fail(h, ADI_ESTATE, "steps of the call not finished");
   if (h->Vcur != h->V) std::swap(h->V, h->V2);
   if (!h->full) {  // Dirichlet columns of U^{m1}
-    dim3 g((h->yb - h->ya + 255) / 256, h->batch);
+    dim3 g(((h->tmode ? h->nyu : h->yb - h->ya) + 255) / 256, h->batch);
     const double* ex0 = h->edges ? h->edges + 2 * h->nxu : nullptr;
     const double* ex1 = h->edges ? h->edges + 2 * h->nxu + h->nyu : nullptr;
     TimeScope ts(h, ADI_KK_EDGE);
-    edge_cols_kernel<<<g, 256, 0, h->stream>>>(h->U, h->ya, h->yb, h->nxu, h->pu, (long long)h->aU, ex0, ex1,
-                                                tabv(h->gb, 2 * h->m));
+    // (the transpose decomposition: U holds all rows, the columns [xa, xb))
+    const int r0 = h->tmode ? 0 : h->ya, r1 = h->tmode ? h->nyu : h->yb;
+    const int lo = h->tmode ? (h->xa == 0) : 1, hi = h->tmode ? (h->xb == h->nxu) : 1;
+    edge_cols_kernel<<<g, 256, 0, h->stream>>>(h->U, r0, r1, h->nxu, h->pu, (long long)h->aU, ex0, ex1,
+                                                tabv(h->gb, 2 * h->m), lo, hi);
     CUDA_TRY(h, cudaGetLastError());
     h->launches++;
     if (!h->capturing) h->host_launches++;
@@ -1744,6 +1875,7 @@ int adi_step_end(adi_handle h) {
 }
 
 static int dist_exchange(adi_ctx* h, int kind);
+static int tm_exchange(adi_ctx* h, int kind);
 
 // ADI_GRAPH: capture the call's launches on the capture stream, then launch the graph on
 // the handle's stream (kernel parameters differ from call to call -- time factors, the
@@ -1818,6 +1950,18 @@ int adi_step(adi_handle h, int nsteps) {
   if (h->graph_on && !h->capturing && !(h->dist && h->nranks > 1) && h->eps <= 0.0) return step_graph(h, nsteps);
   const bool ex = h->dist && h->nranks > 1;
   int rc = ADI_OK;
+  if (ex && h->tmode) {   // the transpose decomposition (NCCL all-to-all of S)
+    rc = adi_step_begin(h, nsteps);
+    if (!rc) rc = tm_exchange(h, 1);
+    for (int k = 0; k < nsteps && !rc; ++k) {
+      rc = adi_step_rows(h);
+      if (!rc) rc = tm_exchange(h, 0);
+      if (!rc) rc = adi_step_cols(h);
+      if (!rc && k + 1 < nsteps) rc = tm_exchange(h, 1);
+    }
+    if (rc) { h->in_call = false; return rc; }
+    return adi_step_end(h);
+  }
   if (ex && !h->fresh) rc = dist_exchange(h, 1);
   if (rc == ADI_OK) rc = adi_step_begin(h, nsteps);
   for (int k = 0; k < nsteps && rc == ADI_OK; ++k) {
@@ -1966,7 +2110,7 @@ static size_t halo_elems(adi_ctx* h, int kind, int rows) {
 
 int adi_halo_bytes(adi_handle h, int kind, int side, size_t* bytes) {
   DevGuard dg_(h);
-  if (!h || !bytes || kind < 0 || kind > 1 || side < 0 || side > 1) return ADI_EINVAL;
+  if (!h || !bytes || kind < 0 || kind > 1 || side < 0 || side > 1 || h->tmode) return ADI_EINVAL;
   int a, b, c, d;
   halo_range(h, side, 1, &a, &b);
   halo_range(h, side, 0, &c, &d);
@@ -2013,7 +2157,7 @@ static int halo_copy(adi_ctx* h, int kind, int a, int b, double* buf, int dir, c
 
 int adi_halo_pack(adi_handle h, int kind, int side, void* dev_buf) {
   DevGuard dg_(h);
-  if (!h || !dev_buf || kind < 0 || kind > 1 || side < 0 || side > 1) return ADI_EINVAL;
+  if (!h || !dev_buf || kind < 0 || kind > 1 || side < 0 || side > 1 || h->tmode) return ADI_EINVAL;
   h->err.clear();
   int a, b;
   halo_range(h, side, 1, &a, &b);
@@ -2022,7 +2166,7 @@ int adi_halo_pack(adi_handle h, int kind, int side, void* dev_buf) {
 
 int adi_halo_unpack(adi_handle h, int kind, int side, const void* dev_buf) {
   DevGuard dg_(h);
-  if (!h || !dev_buf || kind < 0 || kind > 1 || side < 0 || side > 1) return ADI_EINVAL;
+  if (!h || !dev_buf || kind < 0 || kind > 1 || side < 0 || side > 1 || h->tmode) return ADI_EINVAL;
   h->carry_valid = false;   // the next call recomputes its a2 (prologue)
   h->err.clear();
   int a, b;
@@ -2151,9 +2295,171 @@ int adi_nccl_unique_id(void* out) {
   return ADI_OK;
 }
 
+// ---- ADI_DIST_TRANSPOSE: the all-to-all decomposition ---------------
+// Re-shape a band handle (rows Y_r) into a transpose-mode rank: the column sweep takes the
+// whole lines x in X_r, and the column-side arrays are allocated for those lines only.
+static int trank_setup(adi_ctx* h, const std::vector<int>& cy, const std::vector<int>& cx) {
+  const int r = h->rank;
+  h->tmode = true;
+  h->cut_y = cy;
+  h->cut_x = cx;
+  h->ty0 = cy[r]; h->ty1 = cy[r + 1];
+  h->tx0 = cx[r]; h->tx1 = cx[r + 1];
+  const int npx = h->ax.n + 1;
+  h->xa = std::max(h->tx0 - 4, 0) & ~3;   // (16-byte pairs of lines in the transposed stores)
+  h->xb = (h->tx1 >= npx) ? h->nxu : h->tx1;
+  // the column sweep: lines x in X_r (interior), every position of each line
+  h->ay.o0 = 0;
+  h->ay.o1 = 1 << 30;
+  h->ay.l0 = std::max(h->tx0, h->off);
+  h->ay.l1 = std::min(h->tx1, h->nxi + h->off);
+  h->band_y0 = 0;                 // (no halo exchange: the band machinery is off)
+  h->band_y1 = 1 << 30;
+  int rc = setup_axis(h, h->ay, h->ny - 1, h->nxi, 4);
+  if (rc) return rc;
+  // column-side arrays: drop the band-shaped ones, allocate [xa, xb) x all y
+  const size_t B = (size_t)h->batch;
+  dfree(cols_raw(h, h->W));
+  dfree(cols_raw(h, h->W2));
+  dfree(rows_raw(h, h->Ubase, h->pu));
+  h->dev_bytes -= (long long)(8 * (2 * B * h->aW + B * h->aU));
+  h->W = h->W2 = h->Ubase = h->U = nullptr;
+  const int nxl = h->xb - h->xa;
+  h->pc = padp(h->nyu);
+  h->pd = padp(nxl);
+  h->pu = h->pd;
+  h->aU = (size_t)h->nyu * h->pd;
+  h->aC = std::max((size_t)nxl * h->pc, (size_t)h->nyu * h->pd);
+  h->aW = std::max((size_t)nxl * h->pc, (size_t)h->nyv * nxl);
+  double *W = halloc(h, B * h->aW), *W2 = halloc(h, B * h->aW), *U = halloc(h, B * h->aU);
+  double *Sc = halloc(h, B * h->aC), *Sd = halloc(h, B * h->aC);
+  if (!W || !W2 || !U || !Sc || !Sd) {
+    for (double* q : {W, W2, U, Sc, Sd}) dfree(q);
+    return fail(h, ADI_ENOMEM, "transpose-mode arrays");
+  }
+  h->W = W - (ptrdiff_t)h->xa * h->pc;
+  h->W2 = W2 - (ptrdiff_t)h->xa * h->pc;
+  h->Sc = Sc - (ptrdiff_t)h->xa * h->pc;
+  h->Sd = Sd - h->xa;
+  h->Ubase = h->U = U - h->xa;
+  h->tmaps.clear();
+  return ADI_OK;
+}
+
+// one all-to-all of the transpose decomposition.  kind 0 (after the row sweep): the block
+// Sb[x in X_q][y in Y_r] of S2^T goes from rank r to rank q's Sc; kind 1 (after the column
+// sweep or the prologue): Sd[y in Y_q][x in X_r] of S1'^T goes from rank r to q's Sa.
+struct TRange { int a0, a1, c0, c1; };   // rows [a0, a1) x columns [c0, c1) of the block
+static TRange trange(const adi_ctx* g, int q, int r, int kind) {
+  auto clip = [](int v, int hi) { return std::min(v, hi); };
+  if (kind == 0)
+    return {g->cut_x[q], clip(g->cut_x[q + 1], g->nxu), g->cut_y[r], clip(g->cut_y[r + 1], g->nyu)};
+  return {g->cut_y[q], clip(g->cut_y[q + 1], g->nyu), g->cut_x[r], clip(g->cut_x[r + 1], g->nxu)};
+}
+static size_t trange_n(const TRange& t) {
+  return (size_t)std::max(t.a1 - t.a0, 0) * (size_t)std::max(t.c1 - t.c0, 0);
+}
+// the block's start and row pitch in the producing (src) or receiving (dst) rank's array
+static double* tsrc(const adi_ctx* h, const TRange& t, int kind, int b, size_t* pitch) {
+  if (kind == 0) { *pitch = h->pb; return h->Sb + b * h->aS + (size_t)t.a0 * h->pb + t.c0; }
+  *pitch = h->pd;
+  return h->Sd + b * h->aC + (size_t)t.a0 * h->pd + t.c0;
+}
+static double* tdst(const adi_ctx* h, const TRange& t, int kind, int b, size_t* pitch) {
+  if (kind == 0) { *pitch = h->pc; return h->Sc + b * h->aC + (size_t)t.a0 * h->pc + t.c0; }
+  *pitch = h->pa;
+  return h->Sa + b * h->aS + (size_t)t.a0 * h->pa + t.c0;
+}
+
+static int tm_exchange(adi_ctx* h, int kind) {
+  const int P = h->nranks, r = h->rank;
+  auto copy2d = [&](double* d, size_t dp, const double* s, size_t sp, const TRange& t) -> int {
+    const size_t w = (size_t)std::max(t.c1 - t.c0, 0), hg = (size_t)std::max(t.a1 - t.a0, 0);
+    if (!w || !hg) return ADI_OK;
+    CUDA_TRY(h, cudaMemcpy2DAsync(d, dp * 8, s, sp * 8, w * 8, hg, cudaMemcpyDeviceToDevice, h->stream));
+    return ADI_OK;
+  };
+  if (h->loop) {
+    // every rank's producing kernel precedes any rank's copy (adi_step_dist_local)
+    for (int q = 0; q < P; ++q)
+      if (q != r) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->group[q]->ev_pack, 0));
+    for (int q = 0; q < P; ++q) {   // the block rank q produced for me
+      const TRange t = trange(h, r, q, kind);
+      for (int b = 0; b < h->batch; ++b) {
+        size_t sp, dp;
+        const double* sptr = tsrc(h->group[q], t, kind, b, &sp);
+        double* dptr = tdst(h, t, kind, b, &dp);
+        int rc = copy2d(dptr, dp, sptr, sp, t);
+        if (rc) return rc;
+      }
+    }
+    return ADI_OK;
+  }
+  // NCCL: pack every peer's block, one grouped send/recv, unpack; the own block is a copy
+  for (int q = 0; q < P; ++q) {
+    const TRange t = trange(h, q, r, kind);   // what I produce for q
+    size_t off = 0;
+    for (int b = 0; b < h->batch; ++b) {
+      size_t sp, dp;
+      const double* sptr = tsrc(h, t, kind, b, &sp);
+      int rc;
+      if (q == r) {
+        double* dptr = tdst(h, t, kind, b, &dp);
+        rc = copy2d(dptr, dp, sptr, sp, t);
+      } else {
+        rc = copy2d(h->tsend[q] + off, (size_t)std::max(t.c1 - t.c0, 1), sptr, sp, t);
+        off += trange_n(t);
+      }
+      if (rc) return rc;
+    }
+  }
+  NCCL_TRY(h, g_nccl.groupStart());
+  for (int q = 0; q < P; ++q) {
+    if (q == r) continue;
+    const size_t ns = h->batch * trange_n(trange(h, q, r, kind));
+    const size_t nr = h->batch * trange_n(trange(h, r, q, kind));
+    if (ns) NCCL_TRY(h, g_nccl.send(h->tsend[q], ns, ncclFloat64, q, h->comm, h->stream));
+    if (nr) NCCL_TRY(h, g_nccl.recv(h->trecv[q], nr, ncclFloat64, q, h->comm, h->stream));
+  }
+  NCCL_TRY(h, g_nccl.groupEnd());
+  for (int q = 0; q < P; ++q) {
+    if (q == r) continue;
+    const TRange t = trange(h, r, q, kind);   // what q produced for me
+    size_t off = 0;
+    for (int b = 0; b < h->batch; ++b) {
+      size_t dp;
+      double* dptr = tdst(h, t, kind, b, &dp);
+      int rc = copy2d(dptr, dp, h->trecv[q] + off, (size_t)std::max(t.c1 - t.c0, 1), t);
+      if (rc) return rc;
+      off += trange_n(t);
+    }
+  }
+  return ADI_OK;
+}
+
+// NCCL staging of the transpose mode (per peer, both directions and kinds)
+static int tm_init(adi_ctx* h) {
+  const int P = h->nranks;
+  h->tsend.assign(P, nullptr);
+  h->trecv.assign(P, nullptr);
+  for (int q = 0; q < P; ++q) {
+    if (q == h->rank) continue;
+    const size_t yq = h->cut_y[q + 1] - h->cut_y[q] + 1, xq = h->cut_x[q + 1] - h->cut_x[q] + 1;
+    const size_t yr = h->cut_y[h->rank + 1] - h->cut_y[h->rank] + 1, xr = h->cut_x[h->rank + 1] - h->cut_x[h->rank] + 1;
+    const size_t n = (size_t)h->batch * std::max(xq * yr, xr * yq) + 8;
+    if (cudaMalloc(&h->tsend[q], n * 8) != cudaSuccess || cudaMalloc(&h->trecv[q], n * 8) != cudaSuccess) {
+      cudaGetLastError();
+      return ADI_ENOMEM;
+    }
+    h->dev_bytes += (long long)(2 * n * 8);
+  }
+  if (cudaEventCreateWithFlags(&h->ev_pack, cudaEventDisableTiming) != cudaSuccess) return ADI_ECUDA;
+  return ADI_OK;
+}
+
 // one rank's handle: its band's arrays only (band + halo rows), dist state set
 static int create_rank(int nx, int ny, double hh, double dt, double c, int method, int batch, int rank, int nranks,
-                       adi_handle* out) {
+                       adi_handle* out, int mode = ADI_DIST_HALO) {
   *out = nullptr;
   const int npos = ny;   // y positions 0..ny-1 (the planner's positions of both reduced variants)
   std::vector<int> cuts(nranks + 1);
@@ -2165,18 +2471,30 @@ static int create_rank(int nx, int ny, double hh, double dt, double c, int metho
   h->dist = true;
   h->rank = rank;
   h->nranks = nranks;
+  if (mode == ADI_DIST_TRANSPOSE && nranks > 1) {
+    std::vector<int> cx(nranks + 1);
+    dist_bands(nx, nranks, cx.data());
+    const int e = trank_setup(h, cuts, cx);
+    if (e) { adi_destroy(h); return e; }
+  }
   *out = h;
   return rc;
 }
 
 int adi_create_dist(int nx, int ny, double hh, double dt, double c, int method, int batch,
                     const void* nccl_unique_id, int rank, int nranks, adi_handle* out) {
+  return adi_create_dist_ex(nx, ny, hh, dt, c, method, batch, nccl_unique_id, rank, nranks, ADI_DIST_HALO, out);
+}
+
+int adi_create_dist_ex(int nx, int ny, double hh, double dt, double c, int method, int batch,
+                       const void* nccl_unique_id, int rank, int nranks, int mode, adi_handle* out) {
   if (!out) return ADI_EINVAL;
   *out = nullptr;
   if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !nccl_unique_id)) return ADI_EINVAL;
   if (method == ADI_CFD_FULL && nranks > 1) return ADI_EINVAL;   // no band decomposition
+  if (mode != ADI_DIST_HALO && mode != ADI_DIST_TRANSPOSE) return ADI_EINVAL;
   adi_handle h = nullptr;
-  int rc = create_rank(nx, ny, hh, dt, c, method, batch, rank, nranks, &h);
+  int rc = create_rank(nx, ny, hh, dt, c, method, batch, rank, nranks, &h, mode);
   if (rc < 0) return rc;
   const int warn = rc;
   if (nranks > 1) {
@@ -2189,7 +2507,7 @@ int adi_create_dist(int nx, int ny, double hh, double dt, double c, int method, 
       adi_destroy(h);
       return ADI_ENCCL;
     }
-    if ((rc = dist_init(h))) { adi_destroy(h); return rc; }
+    if ((rc = h->tmode ? tm_init(h) : dist_init(h))) { adi_destroy(h); return rc; }
   }
   *out = h;
   return warn;
@@ -2197,12 +2515,18 @@ int adi_create_dist(int nx, int ny, double hh, double dt, double c, int method, 
 
 int adi_create_dist_local(int nx, int ny, double hh, double dt, double c, int method, int batch, int nranks,
                           adi_handle* out) {
+  return adi_create_dist_local_ex(nx, ny, hh, dt, c, method, batch, nranks, ADI_DIST_HALO, out);
+}
+
+int adi_create_dist_local_ex(int nx, int ny, double hh, double dt, double c, int method, int batch, int nranks,
+                             int mode, adi_handle* out) {
   if (!out || nranks < 1) return ADI_EINVAL;
   for (int r = 0; r < nranks; ++r) out[r] = nullptr;
   if (method == ADI_CFD_FULL && nranks > 1) return ADI_EINVAL;
+  if (mode != ADI_DIST_HALO && mode != ADI_DIST_TRANSPOSE) return ADI_EINVAL;
   int warn = ADI_OK;
   for (int r = 0; r < nranks; ++r) {
-    int rc = create_rank(nx, ny, hh, dt, c, method, batch, r, nranks, &out[r]);
+    int rc = create_rank(nx, ny, hh, dt, c, method, batch, r, nranks, &out[r], mode);
     if (rc < 0) {
       for (int q = 0; q < r; ++q) { adi_destroy(out[q]); out[q] = nullptr; }
       return rc;
@@ -2214,7 +2538,14 @@ int adi_create_dist_local(int nx, int ny, double hh, double dt, double c, int me
     out[r]->peer[0] = r > 0 ? out[r - 1] : nullptr;
     out[r]->peer[1] = r + 1 < nranks ? out[r + 1] : nullptr;
     DevGuard dg_(out[r]);
-    int rc = dist_init(out[r]);
+    int rc;
+    if (out[r]->tmode) {
+      out[r]->group = new adi_ctx*[nranks];
+      for (int q = 0; q < nranks; ++q) out[r]->group[q] = out[q];
+      rc = cudaEventCreateWithFlags(&out[r]->ev_pack, cudaEventDisableTiming) == cudaSuccess ? ADI_OK : ADI_ECUDA;
+    } else {
+      rc = dist_init(out[r]);
+    }
     if (rc) {
       for (int q = 0; q < nranks; ++q) { adi_destroy(out[q]); out[q] = nullptr; }
       return rc;
@@ -2240,6 +2571,27 @@ int adi_step_dist_local(adi_handle* hs, int nranks, int nsteps) {
     return ADI_OK;
   };
   int rc = ADI_OK;
+  if (ex && hs[0]->tmode) {
+    // the transpose decomposition: an all-to-all of S after the prologue, every row sweep
+    // and every column sweep but the last (each producer records ev_pack first)
+    auto mark = [](adi_ctx* h) { return cudaEventRecord(h->ev_pack, h->stream) == cudaSuccess ? ADI_OK : ADI_ECUDA; };
+    rc = all([&](adi_ctx* h) { return adi_step_begin(h, nsteps); });
+    if (!rc) rc = all(mark);
+    if (!rc) rc = all([](adi_ctx* h) { return tm_exchange(h, 1); });
+    for (int k = 0; k < nsteps && !rc; ++k) {
+      rc = all([](adi_ctx* h) { return adi_step_rows(h); });
+      if (!rc) rc = all(mark);
+      if (!rc) rc = all([](adi_ctx* h) { return tm_exchange(h, 0); });
+      if (!rc) rc = all([](adi_ctx* h) { return adi_step_cols(h); });
+      if (!rc && k + 1 < nsteps) rc = all(mark);
+      if (!rc && k + 1 < nsteps) rc = all([](adi_ctx* h) { return tm_exchange(h, 1); });
+    }
+    if (rc) {
+      for (int r = 0; r < nranks; ++r) hs[r]->in_call = false;
+      return rc;
+    }
+    return all([](adi_ctx* h) { return adi_step_end(h); });
+  }
   if (ex && !hs[0]->fresh) {
     rc = all([](adi_ctx* h) { return dist_pack(h, 1); });
     if (!rc) rc = all([](adi_ctx* h) { return dist_transfer(h, 1); });
@@ -2261,6 +2613,25 @@ int adi_step_dist_local(adi_handle* hs, int nranks, int nsteps) {
   return all([](adi_ctx* h) { return adi_step_end(h); });
 }
 
+int adi_dist_info(adi_handle h, int* mode, int* rows0, int* rows1, int* cols0, int* cols1) {
+  DevGuard dg_(h);
+  if (!h) return ADI_EINVAL;
+  const int npy = h->ay.n + 1, npx = h->ax.n + 1;
+  if (mode) *mode = h->tmode ? ADI_DIST_TRANSPOSE : ADI_DIST_HALO;
+  if (h->tmode) {
+    if (rows0) *rows0 = h->ty0;
+    if (rows1) *rows1 = std::min(h->ty1, npy);
+    if (cols0) *cols0 = h->tx0;
+    if (cols1) *cols1 = std::min(h->tx1, npx);
+  } else {
+    if (rows0) *rows0 = h->band_y0 > h->ay.n ? 0 : h->band_y0;
+    if (rows1) *rows1 = std::min(h->band_y1, npy);
+    if (cols0) *cols0 = 0;
+    if (cols1) *cols1 = npx;
+  }
+  return ADI_OK;
+}
+
 int adi_band_info(adi_handle h, int* y0, int* y1, int* halo, int* npos) {
   DevGuard dg_(h);
   if (!h) return ADI_EINVAL;
@@ -2279,6 +2650,7 @@ static int get_fields_impl(adi_handle h, double* U, double* V, double* W, cudaMe
   if (!U || !V || !W) return fail(h, ADI_EINVAL, "null field pointer");
   if (h->in_call) return fail(h, ADI_ESTATE, "call in progress");
   const size_t B = (size_t)h->batch;
+  if (h->tmode) return tm_get_fields(h, U, V, W, kind, sync);
   int ya, yb;
   field_rows(h, false, &ya, &yb);
   const int off = h->off;

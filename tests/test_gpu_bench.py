@@ -76,9 +76,11 @@ def test_bench_band_decomposition_one_gpu():
     """bench.py --gpus N runs adi_create_dist (NCCL between GPUs; one GPU per rank, so not
     runnable here); --dist-local P runs the same library path with the loopback transport,
     P ranks on this GPU."""
-    d = run(["--dist-local", "3", "--grid", "2049", "--steps", "2", "--warmup", "3", "--no-cpu"])
-    check_line(d, 1, "strong")
-    assert "adi_create_dist_local" in d["config"]["parallelism"]
+    for mode in ("halo", "transpose"):
+        d = run(["--dist-local", "3", "--dist-mode", mode, "--grid", "2049", "--steps", "2", "--warmup", "3",
+                 "--no-cpu"])
+        check_line(d, 1, "strong")
+        assert "adi_create_dist_local" in d["config"]["parallelism"] and mode in d["config"]["parallelism"]
 
 
 def test_bench_shots_two_ranks():

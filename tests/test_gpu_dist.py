@@ -216,3 +216,95 @@ def test_dist_memory_scales_with_bands(adi):
         adi.adi_set_band(s.handle, npos // 2, npos // 2 + 1024)
         assert s.stats()["device_bytes"] <= full / 6
         s.close()
+
+
+# ---- ADI_DIST_TRANSPOSE: the north_star's all-to-all decomposition (loopback transport) ----
+def _gather_dist(adi, ss, method, nx, ny, batch=1):
+    """Assemble a grid from the ranks' owned parts (adi_dist_info): U and W̄ by columns and
+    V̄ by rows in transpose mode; U, V̄, W̄ by rows in halo mode."""
+    from adi_inputs import shapes
+    su, sv, sw = shapes(method, nx, ny)
+    pre = (batch,) if batch > 1 else ()
+    U, V, W = np.zeros(pre + su), np.zeros(pre + sv), np.zeros(pre + sw)
+    off = 1
+    for s in ss:
+        parts = [np.zeros(pre + sh) for sh in (su, sv, sw)]
+        adi.adi_get_fields(s.handle, *parts)
+        mode, r0, r1, c0, c1 = adi.adi_dist_info(s.handle)
+        npy, npx = ny, nx
+        re = None if r1 >= npy else r1
+        ce = None if c1 >= npx else c1
+        V[..., max(r0 - off, 0):(None if re is None else max(re - off, 0)), :] = \
+            parts[1][..., max(r0 - off, 0):(None if re is None else max(re - off, 0)), :]
+        if mode == adi.ADI_DIST_TRANSPOSE:
+            U[..., :, c0:ce] = parts[0][..., :, c0:ce]
+            W[..., :, max(c0 - off, 0):(None if ce is None else max(ce - off, 0))] = \
+                parts[2][..., :, max(c0 - off, 0):(None if ce is None else max(ce - off, 0))]
+        else:
+            U[..., r0:re, :] = parts[0][..., r0:re, :]
+            W[..., r0:re, :] = parts[2][..., r0:re, :]
+    return U, V, W
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+@pytest.mark.parametrize("n,world,split", [(301, 2, [3]), (1601, 4, [1, 2]), (2101, 8, [2]), (517, 3, [1])])
+def test_dist_local_transpose_equals_single_and_oracle(adi, method, n, world, split):
+    """ADI_DIST_TRANSPOSE through adi_create_dist_local_ex: rows and columns owned by
+    different ranks, S moved by the all-to-all; against one handle and the oracle."""
+    steps = sum(split)
+    p = random_problem(method, n, seed=7 * n + world, steps=steps)
+    hs = adi.adi_create_dist_local(p.nx, p.ny, p.h, p.dt, p.c, method, 1, world, adi.ADI_DIST_TRANSPOSE)
+    ss = [adi.AdiSolver.adopt(h, p.nx, p.ny, p.h, p.dt, p.c, method, K=p.K) for h in hs]
+    for s in ss:
+        s.set_fields(p.U, p.V, p.W)
+        s.set_source(p.phi, None, p.gf)
+        s.set_boundary(p.edges, p.gb)
+    for k in split:
+        adi.adi_step_dist_local(hs, k)
+    got = _gather_dist(adi, ss, method, p.nx, p.ny)
+    s1 = adi.AdiSolver.from_problem(p)
+    s1.step(steps)
+    ref = s1.get_fields()
+    s1.close()
+    o = oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, p.U, p.V, p.W, nsteps=steps, **p.oracle_kwargs())
+    for name, a, b, c in zip("UVW", got, ref, o):
+        check(a, b, tol=1e-13, name=name, what="transpose vs one handle")
+        check(a, c, name=name, what="transpose vs oracle")
+    for s in ss:
+        with pytest.raises(adi.AdiError):
+            adi.adi_halo_bytes(s.handle, 0, 0)
+        s.close()
+
+
+def test_dist_local_transpose_batch_points_and_memory(adi):
+    """A batch of point-source shots in the transpose decomposition; per-rank memory at
+    P = 8 is a small fraction of the P = 1 handle."""
+    n, world, B, steps = 1601, 4, 2, 3
+    probs = [ricker_problem(n, shot=s, nshots=4, steps=steps, f0=20.0, t0=0.05) for s in range(B)]
+    p0 = probs[0]
+    rng = np.random.default_rng(8)
+    U = np.stack([p.U for p in probs]) + rng.standard_normal((B,) + p0.U.shape)
+    V = np.stack([p.V for p in probs]); W = np.stack([p.W for p in probs])
+    hs = adi.adi_create_dist_local(n, n, p0.h, p0.dt, 1.0, MFD, B, world, adi.ADI_DIST_TRANSPOSE)
+    ss = [adi.AdiSolver.adopt(h, n, n, p0.h, p0.dt, 1.0, MFD, batch=B) for h in hs]
+    for s in ss:
+        s.set_fields(U, V, W)
+        s.set_point_sources([p.src[0] for p in probs], [p.src[1] for p in probs], p0.gf)
+    adi.adi_step_dist_local(hs, steps)
+    got = _gather_dist(adi, ss, MFD, n, n, batch=B)
+    for b, p in enumerate(probs):
+        o = oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, U[b], p.V, p.W, nsteps=steps, src=p.src, gf=p.gf)
+        for name, a, c in zip("UVW", got, o):
+            check(a[b], c, name=name, what=f"transpose shot {b}")
+    for s in ss:
+        s.close()
+    m = 8193
+    h = 1.0 / (m - 1)
+    one = adi.adi_create_dist_local(m, m, h, 0.5 * h, 1.0, CFD, 1, 1)
+    b1 = adi.adi_get_stats(one[0])["device_bytes"]
+    adi.adi_destroy(one[0])
+    eight = adi.adi_create_dist_local(m, m, h, 0.5 * h, 1.0, CFD, 1, 8, adi.ADI_DIST_TRANSPOSE)
+    b8 = [adi.adi_get_stats(x)["device_bytes"] for x in eight]
+    for x in eight:
+        adi.adi_destroy(x)
+    assert max(b8) <= b1 / 5, (b1, b8)
