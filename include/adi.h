@@ -134,6 +134,11 @@ enum adi_param {
                            ADI_CFD / ADI_MFD with fixed K (no band, media, stopping rule,
                            ADI_CFD_FULL, ADI_TILE_CHUNKS); results agree with the tile kernels
                            to rounding (parity-tested against the oracle) */
+  ADI_ASYNC_STORE = 13, /* 1: the lean ADI-rows / ADI-columns tiles store their outputs
+                           asynchronously -- X' by bulk copies, S'^T by TMA tensor stores of
+                           {4 lines, 4 positions} boxes from a re-staged tile;
+                           0 (default): thread stores.  Bitwise the same results; measured no
+                           faster (the store phase is bound by the memory system) */
 };
 
 /* Kernel kinds launched by adi_step (index of adi_get_kernel_times arrays). */

@@ -130,6 +130,11 @@ struct KParams {
   int tline0, tpos0;
   // positions of U present in a band-local array (column sweep): [pos_lo, pos_hi)
   int pos_lo, pos_hi;
+  // asynchronous output (ADI_ASYNC_STORE): S'^T leaves by TMA tensor
+  // stores of boxes {4 lines, 4 positions} through tmSo (line coordinate = line -
+  // so_line0, position coordinate = p - so_pos0), X' by bulk copies; tma_so = 0: off
+  CUtensorMap tmSo;
+  int so_line0, so_pos0, tma_so;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -484,6 +489,21 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 __device__ __forceinline__ void fence_async_shared() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// bulk (non-tensor) copy shared -> global of `bytes` (16-byte aligned, a multiple of 16)
+__device__ __forceinline__ void bulk_store(double* g, const double* sm, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(smem_u32(sm)),
+               "r"(bytes)
+               : "memory");
+}
+// TMA tensor store of one box of a 3-d map (coordinates d0, d1, d2) from shared memory
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, const double* sm, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                   (unsigned long long)tm),
+               "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(sm))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 
 __device__ __forceinline__ double shup(double v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
 __device__ __forceinline__ double shdn(double v, int d) { return __shfl_down_sync(0xffffffffu, v, d); }
@@ -897,9 +917,12 @@ __host__ __device__ constexpr int LSTR_OF(int M) { return (32 * (M + 2) + 15) / 
 // NW lines (+ CFD statics; the CFD chunk statics are only needed by edge tiles)
 template <int METHOD, int M, int NW, bool EDGE, bool HET = false>
 constexpr size_t line_smem_bytes() {
+#ifndef ADI_SMEM_PAD
+#define ADI_SMEM_PAD 0   // (experiments only: extra bytes per CTA to lower the resident CTAs)
+#endif
   return sizeof(double) * (size_t)((HET ? 3 : 2) * NW * LSTR_OF(M) +
                                    (METHOD == M_CFD && EDGE ? NW * 10 * 32 + 6 * ETAB : 0) + NW) +
-         128;
+         128 + ADI_SMEM_PAD;
 }
 
 // TMA tensor copy of one line segment (box {34,1,32,1,1}) into the staging tile
@@ -938,6 +961,12 @@ constexpr bool CARRY_TILE = ADI_CARRY_TILE;
 #define ADI_MFD_EPI_REG 1
 #endif
 constexpr bool MFD_EPI_REG = ADI_MFD_EPI_REG;
+// the SWEEP tiles' outputs leave asynchronously (bulk copies of X', TMA tensor stores of
+// S'^T from a [position][4 lines] re-staging): the tile's slot frees as soon as the copy
+// engine has read shared memory instead of after every store instruction has issued
+#ifndef ADI_ASYNC_STORE
+#define ADI_ASYNC_STORE 1
+#endif
 
 // ===========================================================================
 // One tile = NW lines x one segment.  EDGE = false: all 32 chunks of every line
@@ -1582,9 +1611,29 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     }
   }
   __syncthreads();
-  // X: this warp's own line, positions [xlo, xhi), pairs of positions per lane
-  // (16-byte loads and stores; chunk starts and line pitches are even)
-  if (lineok) {
+  // asynchronous outputs (ADI_ASYNC_STORE): lean SWEEP tiles whose 4 lines are all processed
+  constexpr bool ASYNC_ST = ADI_ASYNC_STORE && MODE == KM_SWEEP && !EDGE && !HET && !FULL && !TEST;
+  bool async_s = false;
+  if constexpr (ASYNC_ST) {
+    const int lg0 = P.line0 + blockIdx.x * NW;
+    async_s = P.tma_so && !P.carry && lg0 >= P.line_lo && lg0 + NW <= P.nlines;
+  }
+  if (ASYNC_ST && P.tma_so && !P.carry && lineok) {
+    // X': this lane's chunk ∩ the owned range as one bulk copy (16-byte aligned body;
+    // an odd first / last position by a plain store)
+    const int xlo = max(sg.out_lo, 0), xhi = min(sg.out_hi, n + 1);
+    double* Xo = P.X_out + (long long)b * P.x_batch + (long long)line * P.x_line;
+    int a = max(xlo, c.s), e = min(xhi, c.s + M);
+    if (a < e) {
+      if (a & 1) { Xo[a] = Vm[a - c.s]; ++a; }
+      if ((e & 1) && e > a) { Xo[e - 1] = Vm[e - 1 - c.s]; --e; }
+      if (e > a) {
+        fence_async_shared();
+        bulk_store(Xo + a, Vm + (a - c.s), (unsigned)(e - a) * 8u);
+      }
+    }
+    bulk_commit();
+  } else if (lineok) {
     const int xlo = max(sg.out_lo, 0), xhi = min(sg.out_hi, n + 1);
     double* Xo = P.X_out + (long long)b * P.x_batch + (long long)line * P.x_line;
 #pragma unroll STORE_UNROLL
@@ -1598,6 +1647,41 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       }
     }
   }
+  if (ASYNC_ST && async_s) {
+    // S'^T: re-stage the 4 lines as [position][4] in the X tiles (once the bulk copies of X'
+    // have read them), then TMA tensor stores of {4 lines, 4 positions} boxes over the
+    // owned range; its ragged ends (< 4 positions) by plain stores
+    bulk_wait_read();
+    __syncthreads();
+    double* stg = stX;   // [1024][4] doubles (the 4 X tiles hold 4 * LSTR >= 4096)
+    for (int q = t; q < 32 * M; q += NT) {
+      const int si = (q >> 5) * PADM + (q & 31);
+      double2* d = reinterpret_cast<double2*>(stg + 4 * q);
+      d[0] = make_double2(stS[si], stS[LSTR + si]);
+      d[1] = make_double2(stS[2 * LSTR + si], stS[3 * LSTR + si]);
+    }
+    fence_async_shared();
+    __syncthreads();
+    const int lg0 = P.line0 + blockIdx.x * NW;
+    const int plo_ = max(sg.out_lo, ulo), phi_ = min(sg.out_hi, uhi + 1);
+    const int q0 = (plo_ - sg.start + 3) & ~3, q1 = (phi_ - sg.start) & ~3;
+    for (int k = q0 + 4 * t; k < q1; k += 4 * NT)
+      tma_store_3d(&P.tmSo, stg + 4 * k, lg0 - P.so_line0, sg.start + k - P.so_pos0, b);
+    bulk_commit();
+    // ragged ends: positions [plo_, start + q0) and [start + max(q0, q1), phi_)
+    {
+      const int nh = max(min(sg.start + q0, phi_) - plo_, 0);
+      const int tail0 = max(sg.start + max(q0, q1), plo_);
+      const int nt = max(phi_ - tail0, 0);
+      if (t < 4 * (nh + nt)) {
+        const int k = t >> 2, l = t & 3;
+        const int p = (k < nh) ? plo_ + k : tail0 + (k - nh);
+        double* So = P.S_out + (long long)b * P.s_batch + (long long)p * P.so_pt + (long long)(lg0 + l) * P.so_line;
+        *So = stg[4 * (p - sg.start) + l];
+      }
+    }
+    bulk_wait_read();
+  } else
   // S (or U): transposed.  Half-warp h of warp w stores line pair h at positions
   // 16 w + (lane & 15) + 64 k: the two half-warps fill one 32-byte sector each
   {
@@ -1632,6 +1716,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       }
     }
   }
+  if (ASYNC_ST && P.tma_so && !P.carry && !async_s) bulk_wait_read();   // the X' copies read the tile
   if (P.flag && !isfinite(acc)) atomicOr(P.flag, 1);
   if (tr && tile < P.trace_cap) {
     unsigned smid;

@@ -177,6 +177,8 @@ struct adi_ctx {
   // executable graph is kept and updated in place while the captured topology repeats
   int graph_on = 0;
   int small = -1;   // ADI_THREAD_LINES: -1 auto (short lines), 0 off, 1 on where possible
+  int async_store = 0;   // ADI_ASYNC_STORE: the SWEEP tiles' outputs by TMA / bulk copies (measured:
+                         // no gain, the store phase is bound by the memory system)
   bool capturing = false;
   cudaStream_t gstream = nullptr;   // capture stream when the handle's stream is the legacy one
   cudaGraphExec_t gexec = nullptr;
@@ -192,6 +194,8 @@ struct adi_ctx {
   // TMA tensor maps of the staged arrays (keyed by base pointer)
   struct TMap { const double* ptr; CUtensorMap map; };
   std::vector<TMap> tmaps;
+  struct SMap { const double* ptr; CUtensorMap map; int l0, p0; };
+  std::vector<SMap> smaps;   // TMA store maps of the S' outputs (ADI_ASYNC_STORE)
 };
 
 namespace {
@@ -354,6 +358,48 @@ int encode_lines(adi_ctx* h, const double* base, int pitch, int rows, size_t bst
 #endif
                               ADI_L2PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(h, ADI_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return ADI_OK;
+}
+
+// the TMA STORE map of a transposed S' output array (ADI_ASYNC_STORE): dims {lines
+// (contiguous), positions, batch}, box {4 lines, 4 positions, 1}; line / position origins
+int tmap_store_for(adi_ctx* h, const double* ptr, CUtensorMap* out, int* line0, int* pos0) {
+  for (auto& e : h->smaps)
+    if (e.ptr == ptr) { *out = e.map; *line0 = e.l0; *pos0 = e.p0; return ADI_OK; }
+  adi_ctx::SMap e{};
+  e.ptr = ptr;
+  const double* raw;
+  cuuint64_t d0, d1;
+  size_t pitch, bs = h->aS;
+  if (ptr == h->Sb) {          // row sweep output [x][y]: lines y (origin ya), positions x
+    raw = cols_raw(h, const_cast<double*>(ptr)); d0 = h->yb - h->ya; d1 = h->nxu; pitch = h->pb;
+    e.l0 = h->ya; e.p0 = 0;
+  } else if (ptr == h->Sa) {   // column sweep output [y][x]: lines x, positions y (origin ya)
+    raw = rows_raw(h, const_cast<double*>(ptr), h->pa); d0 = h->nxu; d1 = h->yb - h->ya; pitch = h->pa;
+    e.l0 = 0; e.p0 = h->ya;
+  } else if (h->tmode && ptr == h->Sd) {   // transpose mode: [y][x in [xa, xb)]
+    raw = ptr + h->xa; d0 = h->xb - h->xa; d1 = h->nyu; pitch = h->pd; bs = h->aC;
+    e.l0 = h->xa; e.p0 = 0;
+  } else {
+    return fail(h, ADI_EINVAL, "internal: no store map for this array");
+  }
+  if (!g_encode) {
+    CUtensorMap tmp;
+    int rc = encode_lines(h, h->Sa, h->pa, 1, h->aS, 1, &tmp);   // (fetches the entry point)
+    if (rc) return rc;
+  }
+  const cuuint64_t dims[3] = {d0, d1, (cuuint64_t)h->batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)pitch * 8, (cuuint64_t)bs * 8};
+  const cuuint32_t box[3] = {4, 4, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = g_encode(&e.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)raw, dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(h, ADI_ECUDA, "cuTensorMapEncodeTiled (store) failed: " + std::to_string((int)r));
+  h->smaps.push_back(e);
+  *out = e.map;
+  *line0 = e.l0;
+  *pos0 = e.p0;
   return ADI_OK;
 }
 
@@ -895,6 +941,10 @@ int launch(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p0, int
   int rc;
   if (p.S_in && (rc = tmap_for(h, p.S_in, &p.tmS))) return rc;
   if ((rc = tmap_for(h, p.X_in, &p.tmX))) return rc;
+  if (mode == adi::KM_SWEEP && p.S_out && !h->het && !h->full && !p.carry && h->async_store) {
+    if ((rc = tmap_store_for(h, p.S_out, &p.tmSo, &p.so_line0, &p.so_pos0))) return rc;
+    p.tma_so = 1;
+  }
   if (p.phi_src && (rc = tmap_for(h, p.phi_src, &p.tmF))) return rc;
   if (h->het) {
     if ((rc = tmap_for(h, (&A == &h->ay) ? h->Cb : h->Ca, &p.tmC))) return rc;
@@ -1318,6 +1368,9 @@ int adi_set_param(adi_handle h, int key, double v) {
     if (v != 0.0 && v != 1.0 && v != -1.0) return fail(h, ADI_EINVAL, "thread lines must be -1, 0 or 1");
     h->small = (int)v;
     h->carry_valid = false;
+  } else if (key == ADI_ASYNC_STORE) {
+    if (v != 0.0 && v != 1.0) return fail(h, ADI_EINVAL, "async store must be 0 or 1");
+    h->async_store = (int)v;
   } else if (key == ADI_GRAPH) {
     if (v != 0.0 && v != 1.0) return fail(h, ADI_EINVAL, "graph must be 0 or 1");
     h->graph_on = (int)v;
@@ -1503,6 +1556,7 @@ int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double
   if (phi) {
     if (!h->phi || !h->phiT) {
       h->tmaps.clear();
+    h->smaps.clear();
       // (the line kernels read the pattern directly, a whole tile of 1026 positions from a
       // segment start: a band-local phiT gets that much slack behind its last row)
       if (!h->phi) {
@@ -1554,6 +1608,7 @@ int adi_set_source(adi_handle h, const double* phi, int ix, int iy, const double
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   } else if (h->phi) {
     h->tmaps.clear();
+    h->smaps.clear();
     hfree(h, rows_raw(h, h->phi, h->pa), h->aS + kSrcSlack);
     if (h->tmode) hfree(h, h->phiT + (ptrdiff_t)h->xa * h->pc, h->aC + kSrcSlack);
     else hfree(h, cols_raw(h, h->phiT), h->aS + kSrcSlack);
@@ -1608,6 +1663,7 @@ int adi_set_media(adi_handle h, const float* kappa, const float* rinv_v, const f
   if (h->in_call) return fail(h, ADI_ESTATE, "call in progress");
   if (!kappa && !rinv_v && !rinv_w) {   // back to the scalar medium
     h->tmaps.clear();
+    h->smaps.clear();
     hfree(h, rows_raw(h, h->Ca, h->pa), h->aS);
     hfree(h, cols_raw(h, h->Cb), h->aS);
     h->Ca = h->Cb = nullptr;
@@ -1636,6 +1692,7 @@ int adi_set_media(adi_handle h, const float* kappa, const float* rinv_v, const f
     return fail(h, ADI_EINVAL, "media values must be finite normal floats > 0");
   if (!h->Ca) {
     h->tmaps.clear();
+    h->smaps.clear();
     double* ra = halloc(h, h->aS);
     double* rb = ra ? halloc(h, h->aS) : nullptr;
     if (!ra || !rb) {
@@ -2037,6 +2094,7 @@ static int relayout(adi_ctx* h, int nya, int nyb) {
   }
   h->U = h->Ubase;
   h->tmaps.clear();
+    h->smaps.clear();
   h->carry_valid = false;
   return ADI_OK;
 }
@@ -2343,6 +2401,7 @@ static int trank_setup(adi_ctx* h, const std::vector<int>& cy, const std::vector
   h->Sd = Sd - h->xa;
   h->Ubase = h->U = U - h->xa;
   h->tmaps.clear();
+    h->smaps.clear();
   return ADI_OK;
 }
 

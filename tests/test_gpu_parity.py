@@ -479,3 +479,21 @@ def test_carry_batch_point_sources(adi):
         s.close()
     assert np.abs(outs[1][0]).max() > 0
     assert_parity(outs[0], outs[1], tol=1e-13)
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+@pytest.mark.parametrize("n", [1601, 2101])
+def test_async_store_knob_bitwise(adi, method, n):
+    """ADI_ASYNC_STORE (bulk copies of X', TMA tensor stores of S'^T) changes how the outputs
+    leave the tile, not their values: bitwise equal to the thread stores, split calls."""
+    p = random_problem(method, n, seed=n + 11, steps=4)
+    outs = []
+    for v in (0, 1):
+        s = adi.AdiSolver.from_problem(p)
+        s.set_param(adi.ADI_ASYNC_STORE, v)
+        s.step(1)
+        s.step(3)
+        outs.append(s.get_fields())
+        s.close()
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)

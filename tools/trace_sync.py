@@ -12,6 +12,9 @@ import torch
 import paper_2006_07583_b200 as adi
 from adi_inputs import CFD, MFD, MMS, mms_problem
 
+if os.environ.get("ADI_LIB"):   # a build variant (tools/build_variant.sh)
+    adi.LIB_PATH = os.environ["ADI_LIB"]
+
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 meth = CFD if (len(sys.argv) < 3 or sys.argv[2] == "cfd") else MFD
 cap = 1 << 20
@@ -28,7 +31,10 @@ r = r[r[:, 5] > 0]
 t0 = r[:, 2].min()
 a, b, c, d = ((r[:, k] - t0) / 1e3 for k in (2, 3, 4, 5))
 span = d.max()
-print(f"tiles {len(r)} span {span:.1f} us; mean load {np.mean(b-a):.2f} ops {np.mean(c-b):.2f} store {np.mean(d-c):.2f}")
+print(f"tiles {len(r)} span {span:.1f} us; mean load {np.mean(b-a):.2f} ops {np.mean(c-b):.2f} store {np.mean(d-c):.2f}"
+      f"; resident {((d - a).sum() / span):.0f}")
+if os.environ.get("BRIEF"):
+    sys.exit(0)
 mid = span / 2
 for t in np.arange(mid - 60, mid + 60, 1.0):
     nl = int(((a <= t) & (t < b)).sum()); no = int(((b <= t) & (t < c)).sum()); ns = int(((c <= t) & (t < d)).sum())
