@@ -344,6 +344,14 @@ int adi_get_fields_device(adi_handle h, double* dU, double* dV, double* dW);
 
 int adi_get_stats(adi_handle h, adi_stats* s);
 
+/* Testing aid (compute-sanitizer is not available on every host): with ADI_GUARD_CHECK=1
+ * in the environment when the handle's arrays are allocated, the guard regions around
+ * every field array hold a canary pattern instead of zeros; this call (synchronizes the
+ * stream) counts the 8-byte guard words that no longer hold it, i.e. out-of-bounds writes
+ * by a kernel or a copy.  Without the variable the guards are zeros and *bad counts them
+ * all. */
+int adi_check_guards(adi_handle h, long long* bad);
+
 /* With ADI_TIMING = 1: synchronize the stream, then for each kernel kind k < nkinds
  * return the summed device time ms[k] (CUDA events around each launch) and the
  * launch count since the previous call; the accumulators are reset.  Either array

@@ -97,6 +97,7 @@ def lib():
             L.adi_create_dist_ex.argtypes = [I, I, D, D, D, I, I, P, I, I, I, ctypes.POINTER(H)]
             L.adi_create_dist_local_ex.argtypes = [I, I, D, D, D, I, I, I, I, ctypes.POINTER(H)]
             L.adi_dist_info.argtypes = [H] + [ctypes.POINTER(I)] * 5
+            L.adi_check_guards.argtypes = [H, ctypes.POINTER(ctypes.c_longlong)]
             L.adi_plan_halo.argtypes = [I, ctypes.POINTER(I)]
             L.adi_create_dist_local.argtypes = [I, I, D, D, D, I, I, I, ctypes.POINTER(H)]
             L.adi_step_dist_local.argtypes = [ctypes.POINTER(H), I, I]
@@ -130,7 +131,7 @@ def lib():
 EXPORTS = ["adi_create", "adi_create_batch", "adi_set_param", "adi_set_stream", "adi_set_fields",
            "adi_set_fields_device", "adi_set_source", "adi_set_point_sources", "adi_set_boundary",
            "adi_set_media", "adi_create_dist", "adi_nccl_unique_id", "adi_dist_bands", "adi_plan_halo", "adi_create_dist_local", "adi_step_dist_local", "adi_create_dist_ex",
-           "adi_create_dist_local_ex", "adi_dist_info", "adi_step", "adi_step_begin", "adi_step_rows", "adi_step_cols", "adi_step_end", "adi_set_band",
+           "adi_create_dist_local_ex", "adi_dist_info", "adi_check_guards", "adi_step", "adi_step_begin", "adi_step_rows", "adi_step_cols", "adi_step_end", "adi_set_band",
            "adi_band_info", "adi_halo_bytes", "adi_halo_pack", "adi_halo_unpack",
            "adi_get_fields", "adi_get_fields_device", "adi_set_fields_async", "adi_get_fields_async", "adi_get_stats", "adi_get_kernel_times",
            "adi_set_trace", "adi_get_last_sweeps", "adi_last_error",
@@ -191,6 +192,13 @@ def adi_create_dist_ex(nx, ny, h, dt, c, method, batch, unique_id, rank, nranks,
     rc = lib().adi_create_dist_ex(nx, ny, h, dt, c, method, batch, uid, rank, nranks, mode, ctypes.byref(hd))
     _check(None, rc, "adi_create_dist_ex")
     return hd, rc
+
+
+def adi_check_guards(hd):
+    """Guard words overwritten since allocation (needs ADI_GUARD_CHECK=1 at allocation)."""
+    v = ctypes.c_longlong(0)
+    _check(hd, lib().adi_check_guards(hd, ctypes.byref(v)), "adi_check_guards")
+    return int(v.value)
 
 
 def adi_dist_info(hd):

@@ -964,8 +964,8 @@ constexpr bool MFD_EPI_REG = ADI_MFD_EPI_REG;
 // the SWEEP tiles' outputs leave asynchronously (bulk copies of X', TMA tensor stores of
 // S'^T from a [position][4 lines] re-staging): the tile's slot frees as soon as the copy
 // engine has read shared memory instead of after every store instruction has issued
-#ifndef ADI_ASYNC_STORE
-#define ADI_ASYNC_STORE 1
+#ifndef ADI_ASYNC_STORE_CODE
+#define ADI_ASYNC_STORE_CODE 1
 #endif
 
 // ===========================================================================
@@ -1612,7 +1612,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   }
   __syncthreads();
   // asynchronous outputs (ADI_ASYNC_STORE): lean SWEEP tiles whose 4 lines are all processed
-  constexpr bool ASYNC_ST = ADI_ASYNC_STORE && MODE == KM_SWEEP && !EDGE && !HET && !FULL && !TEST;
+  constexpr bool ASYNC_ST = ADI_ASYNC_STORE_CODE && MODE == KM_SWEEP && !EDGE && !HET && !FULL && !TEST;
   bool async_s = false;
   if constexpr (ASYNC_ST) {
     const int lg0 = P.line0 + blockIdx.x * NW;

@@ -17,6 +17,7 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -106,6 +107,7 @@ struct adi_ctx {
   // is rows_raw / cols_raw.  ya is even (16-byte TMA alignment of the staged rows).
   int ya = 0, yb = 0;
   long long dev_bytes = 0;   // device memory this handle allocated (adi_get_stats)
+  std::vector<std::pair<double*, size_t>> allocs;   // the guarded field arrays (adi_check_guards)
   double* Ubase = nullptr;
   // device buffers
   double *U = nullptr, *V = nullptr, *W = nullptr;
@@ -285,6 +287,14 @@ bool nccl_load() {
 // ---- device arrays read by the line kernels' TMA copies carry guard regions
 // (adi_line.cuh: a staged row may start TMA_P0 positions before a line and end
 // past the last line); allocations are zeroed.
+// ADI_GUARD_CHECK=1 in the environment (a testing aid in place of compute-sanitizer, which
+// this pool does not offer): the guards are filled with a canary byte pattern instead of
+// zeros, and adi_check_guards reports guard words that a kernel or copy overwrote
+constexpr unsigned char kCanary = 0xA5;
+static bool guard_canary() {
+  const char* e = std::getenv("ADI_GUARD_CHECK");
+  return e && e[0] == '1';
+}
 double* dalloc(size_t n) {
   void* raw = nullptr;
   const size_t tot = (n + adi::BUF_GUARD_FRONT + adi::BUF_GUARD_TAIL) * sizeof(double);
@@ -293,6 +303,15 @@ double* dalloc(size_t n) {
   if (cudaMemset(raw, 0, tot) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
     cudaGetLastError(); cudaFree(raw); return nullptr;
   }
+  if (guard_canary()) {
+    char* c = static_cast<char*>(raw);
+    if (cudaMemset(c, kCanary, adi::BUF_GUARD_FRONT * sizeof(double)) != cudaSuccess ||
+        cudaMemset(c + tot - adi::BUF_GUARD_TAIL * sizeof(double), kCanary, adi::BUF_GUARD_TAIL * sizeof(double)) !=
+            cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess) {
+      cudaGetLastError(); cudaFree(raw); return nullptr;
+    }
+  }
   return static_cast<double*>(raw) + adi::BUF_GUARD_FRONT;
 }
 void dfree(double* p) {
@@ -300,11 +319,16 @@ void dfree(double* p) {
 }
 double* halloc(adi_ctx* h, size_t n) {
   double* p = dalloc(n);
-  if (p) h->dev_bytes += (long long)((n + adi::BUF_GUARD_FRONT + adi::BUF_GUARD_TAIL) * sizeof(double));
+  if (p) {
+    h->dev_bytes += (long long)((n + adi::BUF_GUARD_FRONT + adi::BUF_GUARD_TAIL) * sizeof(double));
+    h->allocs.push_back({p, n});
+  }
   return p;
 }
 void hfree(adi_ctx* h, double* raw, size_t n) {
   if (!raw) return;
+  for (size_t k = 0; k < h->allocs.size(); ++k)
+    if (h->allocs[k].first == raw) { h->allocs.erase(h->allocs.begin() + k); break; }
   dfree(raw);
   h->dev_bytes -= (long long)((n + adi::BUF_GUARD_FRONT + adi::BUF_GUARD_TAIL) * sizeof(double));
 }
@@ -2377,10 +2401,9 @@ static int trank_setup(adi_ctx* h, const std::vector<int>& cy, const std::vector
   if (rc) return rc;
   // column-side arrays: drop the band-shaped ones, allocate [xa, xb) x all y
   const size_t B = (size_t)h->batch;
-  dfree(cols_raw(h, h->W));
-  dfree(cols_raw(h, h->W2));
-  dfree(rows_raw(h, h->Ubase, h->pu));
-  h->dev_bytes -= (long long)(8 * (2 * B * h->aW + B * h->aU));
+  hfree(h, cols_raw(h, h->W), B * h->aW);
+  hfree(h, cols_raw(h, h->W2), B * h->aW);
+  hfree(h, rows_raw(h, h->Ubase, h->pu), B * h->aU);
   h->W = h->W2 = h->Ubase = h->U = nullptr;
   const int nxl = h->xb - h->xa;
   h->pc = padp(h->nyu);
@@ -2392,7 +2415,7 @@ static int trank_setup(adi_ctx* h, const std::vector<int>& cy, const std::vector
   double *W = halloc(h, B * h->aW), *W2 = halloc(h, B * h->aW), *U = halloc(h, B * h->aU);
   double *Sc = halloc(h, B * h->aC), *Sd = halloc(h, B * h->aC);
   if (!W || !W2 || !U || !Sc || !Sd) {
-    for (double* q : {W, W2, U, Sc, Sd}) dfree(q);
+    for (double* q : {W, W2, U, Sc, Sd}) hfree(h, q, 0);
     return fail(h, ADI_ENOMEM, "transpose-mode arrays");
   }
   h->W = W - (ptrdiff_t)h->xa * h->pc;
@@ -2687,6 +2710,29 @@ int adi_dist_info(adi_handle h, int* mode, int* rows0, int* rows1, int* cols0, i
     if (rows1) *rows1 = std::min(h->band_y1, npy);
     if (cols0) *cols0 = 0;
     if (cols1) *cols1 = npx;
+  }
+  return ADI_OK;
+}
+
+int adi_check_guards(adi_handle h, long long* bad) {
+  DevGuard dg_(h);
+  if (!h || !bad) return ADI_EINVAL;
+  *bad = 0;
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  std::vector<unsigned char> buf(std::max(adi::BUF_GUARD_FRONT, adi::BUF_GUARD_TAIL) * sizeof(double));
+  for (auto& a : h->allocs) {
+    const char* raw = reinterpret_cast<const char*>(a.first - adi::BUF_GUARD_FRONT);
+    const size_t front = adi::BUF_GUARD_FRONT * sizeof(double), tail = adi::BUF_GUARD_TAIL * sizeof(double);
+    const char* tailp = reinterpret_cast<const char*>(a.first + a.second);
+    for (int part = 0; part < 2; ++part) {
+      const size_t nb = part ? tail : front;
+      CUDA_TRY(h, cudaMemcpy(buf.data(), part ? tailp : raw, nb, cudaMemcpyDeviceToHost));
+      for (size_t k = 0; k < nb; k += 8) {
+        bool ok = true;
+        for (int j = 0; j < 8; ++j) ok = ok && buf[k + j] == kCanary;
+        *bad += !ok;
+      }
+    }
   }
   return ADI_OK;
 }

@@ -308,3 +308,23 @@ def test_dist_local_transpose_batch_points_and_memory(adi):
     for x in eight:
         adi.adi_destroy(x)
     assert max(b8) <= b1 / 5, (b1, b8)
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+def test_torchrun_two_ranks_python_band_driver(adi, method):
+    """Two processes under torchrun (gloo, both on device 0, host-staged halo messages: no
+    kernel waits on another rank): the Python band driver (dist.py) against the oracle."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ, PYTHONPATH=os.path.join(root, "tests") + os.pathsep + root)
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), "tools/dist_check.py",
+                          str(method), "1601", "3"], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert "DIST_CHECK_OK" in out.stdout
