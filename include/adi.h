@@ -363,7 +363,8 @@ int adi_get_kernel_times(adi_handle h, double* ms, long long* launches, int nkin
  * dev_buf[8 * tile]: {tile, SM id, t_start, t_loaded, t_ops_done, t_end, 0, 0}, times
  * from the %globaltimer register (ns).  A later launch of that kind overwrites the
  * records.  dev_buf is device memory owned by the caller and must hold 64 * cap bytes;
- * NULL turns tracing off.  EINVAL for cap < 0 or an unknown kind. */
+ * NULL turns tracing off.  EINVAL for cap < 0 or an unknown kind, and in a library built
+ * without -DADI_TILE_TRACE=1 (the production build: the timer reads are compiled out). */
 int adi_set_trace(adi_handle h, void* dev_buf, long long cap, int kind);
 
 /* Sweeps used by the last step's ADI-rows / ADI-columns stages (ADI_K_SWEEPS when

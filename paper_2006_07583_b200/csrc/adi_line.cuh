@@ -137,6 +137,11 @@ struct KParams {
   int so_line0, so_pos0, tma_so;
 };
 
+// per-tile %globaltimer stamps for adi_set_trace (tools/tile_trace.py, trace_sync.py): only in
+// libraries built with -DADI_TILE_TRACE=1 (tools/build_variant.sh), out of production kernels
+#ifndef ADI_TILE_TRACE
+#define ADI_TILE_TRACE 0
+#endif
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1006,7 +1011,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   const int uhi = (METHOD == M_CFD && !FULL) ? n - 1 : n;  // u active on [ulo, uhi]
   const int pR = (METHOD == M_CFD) ? n : n + 1;   // position of ū's right Dirichlet value
   const bool lineok = line >= P.line_lo && line < P.nlines;
-  const bool tr = P.trace && t == 0;
+  const bool tr = ADI_TILE_TRACE && P.trace && t == 0;   // (compiled out of production builds)
   // trace index unique across the launches of one kernel kind (segment offset seg0 of nseg_all)
   const long long tile =
       (long long)blockIdx.x + (long long)gridDim.x * (P.seg0 + blockIdx.y + (long long)P.nseg_all * b);

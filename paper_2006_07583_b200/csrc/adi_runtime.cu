@@ -2868,6 +2868,8 @@ int adi_set_trace(adi_handle h, void* dev_buf, long long cap, int kind) {
   if (!h) return ADI_EINVAL;
   h->err.clear();
   if (dev_buf && (cap < 0 || kind < 0 || kind >= ADI_NKINDS)) return fail(h, ADI_EINVAL, "bad trace arguments");
+  if (dev_buf && !ADI_TILE_TRACE)
+    return fail(h, ADI_EINVAL, "tile tracing needs a library built with -DADI_TILE_TRACE=1 (tools/build_variant.sh)");
   h->trace = (unsigned long long*)dev_buf;
   h->trace_cap = dev_buf ? cap : 0;
   h->trace_kind = dev_buf ? kind : -1;

@@ -4,6 +4,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 import paper_2006_07583_b200 as adi
+
+if os.environ.get("ADI_LIB"):   # a build with -DADI_TILE_TRACE=1 (tools/build_variant.sh)
+    adi.LIB_PATH = os.environ["ADI_LIB"]
 from adi_inputs import CFD, MFD, MMS, mms_problem
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
