@@ -632,7 +632,7 @@ __device__ __forceinline__ void cfd_statics(const Ctx<M>& c, const EdgeTab& T, i
 
 
 #ifndef ADI_NSUB
-#define ADI_NSUB 2
+#define ADI_NSUB 4
 #endif
 constexpr int NSUB = ADI_NSUB;
 // CFD fix-up truncation: with 32-point sub-chunks the carry responses
