@@ -62,6 +62,8 @@ def parse():
                          "1 = CFD 41^2, 200 steps; 2 = the MFD ladder 41..321 to 5T; 3 = Gamma=k in {2, 9} at "
                          "1601^2, CFD and MFD, 100 timed steps.  One JSON line; 0 = config 4 (the default)")
     ap.add_argument("--no-graph", action="store_true", help="configs 1-3: plain launches instead of ADI_GRAPH")
+    ap.add_argument("--set", action="append", default=[], metavar="KEY=VAL",
+                    help="adi_set_param on the timed solvers (A/B of a knob), e.g. --set ADI_WHOLE_LINES=0")
     ap.add_argument("--dist-mode", default="halo", choices=["halo", "transpose"],
                     help="N > 1 (and --dist-local): the band decomposition with halo exchange (default) or "
                          "the north_star's all-to-all transpose between the half-steps (ADI_DIST_TRANSPOSE)")
@@ -302,6 +304,7 @@ def run_ours(a, ws, rank, local):
     NCCL halo exchange inside adi_step overlapping the column sweep)."""
     import torch
     import paper_2006_07583_b200 as adi
+    use_variant(adi)
 
     torch.cuda.set_device(local)
     stream = torch.cuda.current_stream()
@@ -328,6 +331,7 @@ def run_ours(a, ws, rank, local):
         s.set_fields(p.U, p.V, p.W)
         s.set_source(p.phi, p.src, p.gf)
         s.set_boundary(p.edges, p.gb)
+        apply_knobs(adi, s, a)
         if a.media:
             s.set_media(p.kappa, p.rinv_v, p.rinv_w)
             p.kappa = p.rinv_v = p.rinv_w = None
@@ -515,6 +519,7 @@ def run_shots(a, ws, rank, local):
     shots in one batched handle (grid dimension z = shot); no data-path collective."""
     import torch
     import paper_2006_07583_b200 as adi
+    use_variant(adi)
     from adi_inputs import MFD, shapes
 
     torch.cuda.set_device(local)
@@ -525,6 +530,7 @@ def run_shots(a, ws, rank, local):
     p0 = probs[0]
     s = adi.AdiSolver(n, n, p0.h, p0.dt, 1.0, MFD, batch=B, K=a.K, stream=stream.cuda_stream)
     s.set_point_sources([p.src[0] for p in probs], [p.src[1] for p in probs], p0.gf)
+    apply_knobs(adi, s, a)
     su, sv, sw = shapes(MFD, n, n)
     # zero initial fields (adi_create's state; set explicitly as a user would)
     z = [torch.zeros((B,) + sh, dtype=torch.float64, device="cuda") for sh in (su, sv, sw)]
@@ -668,6 +674,21 @@ def cpu_leg(rate_fn, budget_s=8.0, max_steps=12):
     return nthr, res
 
 
+def use_variant(adi):
+    """ADI_LIB=path: time a build variant of libadi.so (tools/build_variant.sh) instead of
+    the in-tree default -- same-box A/B of compile-time knobs; recorded in the line."""
+    v = os.environ.get("ADI_LIB")
+    if v:
+        adi.LIB_PATH = os.path.abspath(v)
+
+
+def apply_knobs(adi, s, a):
+    """--set KEY=VAL: adi_set_param on a timed solver (named ADI_* constants)."""
+    for kv in a.set:
+        k, v = kv.split("=", 1)
+        s.set_param(getattr(adi, k), float(v))
+
+
 def main_shots(a, ws, rank, local):
     """bench.py --shots: config 5, weak scaling over ranks."""
     B = a.shots_per_gpu
@@ -677,6 +698,10 @@ def main_shots(a, ws, rank, local):
            "K_sweeps": a.K, "cfl": {"mfd": 0.81},
            "l2": f"inputs larger than L2 ({B} x 134 MB per field); no flush",
            "parallelism": "1 GPU" if ws == 1 else f"{ws} GPUs: independent shots per rank (replicas, no collective)"}
+    if a.set:
+        cfg["knobs"] = a.set
+    if os.environ.get("ADI_LIB"):
+        cfg["library_variant"] = os.environ["ADI_LIB"]
     common = {"metric": METRIC, "unit": UNIT, "n_gpus": ws, "steps": a.steps, "warmup": a.warmup,
               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
               "data": "synthetic", "config": cfg}
@@ -741,6 +766,7 @@ def main_config(a):
     import torch
     import oracle
     import paper_2006_07583_b200 as adi
+    use_variant(adi)
     from adi_inputs.mms import interior_error
     torch.cuda.set_device(0)
     stream = torch.cuda.current_stream()
@@ -871,6 +897,8 @@ def main():
     if a.media:
         cfg["workload"] += " + heterogeneous medium (NEXT row f3: fp32 kappa, rho^-1 grids, adi_set_media)"
         cfg["media"] = "smooth: kappa = 0.8 (1 + 0.25 sin(2 pi x + 0.3) cos(2 pi y)), rho^-1 analogous"
+    if a.set:
+        cfg["knobs"] = a.set
     if a.shots:
         return main_shots(a, ws, rank, local)
     if a.impl == "reference":

@@ -8,7 +8,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "libadi.so")
 SOURCES = [os.path.join(HERE, "csrc", "adi_runtime.cu")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", "adi_line.cuh"), os.path.join(ROOT, "include", "adi.h")]
+DEPS = SOURCES + [os.path.join(HERE, "csrc", "adi_line.cuh"),
+        os.path.join(HERE, "csrc", "adi_thread.cuh"), os.path.join(ROOT, "include", "adi.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177"]
 

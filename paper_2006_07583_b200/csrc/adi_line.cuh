@@ -646,6 +646,10 @@ constexpr bool TRIM = ADI_TRIM && (32 / NSUB == 32);
 #define ADI_EARLY_BASE 1
 #endif
 constexpr bool EARLY_BASE = ADI_EARLY_BASE;
+// MFD SWEEP tiles: peel the last of the K sweeps (see line_tile)
+#ifndef ADI_MFD_PEEL
+#define ADI_MFD_PEEL 1
+#endif
 constexpr int TRIM_K = 27, TRIM_J = 4;
 
 // ===========================================================================
@@ -1548,18 +1552,33 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       u_op(wv, Sm);             // S1 = S - alpha D̄(W)
     } else {
       double uo[TEST ? M : 1], xo[TEST ? M : 1];
-      for (int k = 0; k < KK; ++k) {
-        if constexpr (TEST) {
-          if (k + 1 == KK) {
+      if constexpr (TEST || MODE != KM_SWEEP || !ADI_MFD_PEEL) {
+        for (int k = 0; k < KK; ++k) {
+          if constexpr (TEST) {
+            if (k + 1 == KK) {
 #pragma unroll
-            for (int i = 0; i < M; ++i) { uo[i] = u[i]; xo[i] = x[i]; }
+              for (int i = 0; i < M; ++i) { uo[i] = u[i]; xo[i] = x[i]; }
+            }
+          }
+          u_op(x, Sm);
+          if (MODE == KM_SWEEP && k + 1 == KK && !(!HET && P.carry)) stage_phi();
+          x_op(Vm);
+          if constexpr (TEST) {
+            if (k + 1 == KK) norm_add(u, uo, x, xo);
           }
         }
-        u_op(x, Sm);
-        if (MODE == KM_SWEEP && k + 1 == KK && !(!HET && P.carry)) stage_phi();
-        x_op(Vm);
-        if constexpr (TEST) {
-          if (k + 1 == KK) norm_add(u, uo, x, xo);
+      } else {
+        // the last sweep peeled: the source staging between its two operators is then
+        // straight-line code, and the loop carries u and x in fixed registers (with the
+        // conditional TMA inside the loop, ptxas re-homed u around it: 64 moves a sweep)
+        for (int k = 0; k + 1 < KK; ++k) {
+          u_op(x, Sm);
+          x_op(Vm);
+        }
+        if (KK > 0) {
+          u_op(x, Sm);
+          if (!(!HET && P.carry)) stage_phi();
+          x_op(Vm);
         }
       }
       if (MODE == KM_SWEEP) {
