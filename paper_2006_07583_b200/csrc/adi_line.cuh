@@ -113,7 +113,7 @@ struct KParams {
   const double* tabU; const double* tabX;
   int* flag;        // if set: becomes 1 when a non-finite value is stored
   // profiling aid (adi_set_trace): per tile, warp 0 records
-  // {tile, smid, t_start, t_loaded, t_ops_done, t_end} (%globaltimer ns)
+  // {tile, smid, t_start, t_loaded, t_ops_done, t_end, t_after_barrier} (%globaltimer ns)
   unsigned long long* trace;
   long long trace_cap;
   int seg0, nseg_all;   // this launch's first segment, all segments of the axis (trace index)
@@ -1635,6 +1635,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     }
   }
   __syncthreads();
+  const unsigned long long tr3 = tr ? gtimer() : 0ull;   // (trace: after the CTA barrier)
   // asynchronous outputs (ADI_ASYNC_STORE): lean SWEEP tiles whose 4 lines are all processed
   constexpr bool ASYNC_ST = ADI_ASYNC_STORE_CODE && MODE == KM_SWEEP && !EDGE && !HET && !FULL && !TEST;
   bool async_s = false;
@@ -1746,7 +1747,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     unsigned long long* r = P.trace + tile * 8;
-    r[0] = tile; r[1] = smid; r[2] = tr0; r[3] = tr1; r[4] = tr2; r[5] = gtimer();
+    r[0] = tile; r[1] = smid; r[2] = tr0; r[3] = tr1; r[4] = tr2; r[5] = gtimer(); r[6] = tr3;
   }
 }
 

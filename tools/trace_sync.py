@@ -31,8 +31,9 @@ r = r[r[:, 5] > 0]
 t0 = r[:, 2].min()
 a, b, c, d = ((r[:, k] - t0) / 1e3 for k in (2, 3, 4, 5))
 span = d.max()
+e = (r[:, 6] - t0) / 1e3   # after the CTA barrier that precedes the stores
 print(f"tiles {len(r)} span {span:.1f} us; mean load {np.mean(b-a):.2f} ops {np.mean(c-b):.2f} store {np.mean(d-c):.2f}"
-      f"; resident {((d - a).sum() / span):.0f}")
+      f" (barrier {np.mean(e-c):.2f} + issue {np.mean(d-e):.2f}); resident {((d - a).sum() / span):.0f}")
 if os.environ.get("BRIEF"):
     sys.exit(0)
 mid = span / 2
