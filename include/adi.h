@@ -139,6 +139,18 @@ enum adi_param {
                            {4 lines, 4 positions} boxes from a re-staged tile;
                            0 (default): thread stores.  Bitwise the same results; measured no
                            faster (the store phase is bound by the memory system) */
+  ADI_DIST_FUSED = 14,  /* transpose-mode handles (ADI_DIST_TRANSPOSE, <= 8 ranks): 1 (default
+                           where available) fuses the all-to-all of S into the kernels -- the
+                           row and column kernels store their transposed S' straight into the
+                           owning rank's array (peer memory over NVLink through CUDA IPC
+                           mappings, or the other ranks' arrays of an adi_create_dist_local
+                           group), and the exchange becomes a barrier (a one-element NCCL
+                           all-reduce, or stream waits in a local group); 0: the NCCL / loopback
+                           all-to-all.  Collective: set it to the same value on every rank,
+                           between calls.  EINVAL where no peer mapping exists (halo mode, more
+                           than 8 ranks, IPC unavailable: adi_create_dist_ex then leaves the
+                           handle unfused on every rank).  Results are bitwise the same;
+                           DESIGN.md §7.2 */
 };
 
 /* Kernel kinds launched by adi_step (index of adi_get_kernel_times arrays). */

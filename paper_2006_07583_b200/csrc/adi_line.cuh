@@ -69,6 +69,7 @@ constexpr int BUF_GUARD_TAIL = 192;
 //   S_out: b*s_batch + L*so_line + p*so_pt    (written transposed)
 //   X_out: b*x_batch + L*x_line  + p
 //   U_in / U_out: b*u_batch + L*u_line + p*u_pt  (prologue / final)
+constexpr int MAX_TRANKS = 8;   // ranks of a fused transpose (KParams peer table)
 struct KParams {
   CUtensorMap tmS;   // S_in (or nothing in the prologue)
   CUtensorMap tmX;   // X_in
@@ -135,6 +136,14 @@ struct KParams {
   // so_line0, position coordinate = p - so_pos0), X' by bulk copies; tma_so = 0: off
   CUtensorMap tmSo;
   int so_line0, so_pos0, tma_so;
+  // fused transpose (ADI_DIST_TRANSPOSE with ADI_DIST_FUSED): the transposed
+  // S' store of position p goes straight into the array of the rank q that owns p
+  // (tcut[q] <= p < tcut[q + 1]), at tso[q] + b tsb[q] + p tpt[q] + line -- peer memory
+  // over NVLink (P2P), or another rank's array of a local group.  tnp = 0: own S_out
+  int tnp;
+  int tcut[MAX_TRANKS + 1];
+  double* tso[MAX_TRANKS];
+  long long tpt[MAX_TRANKS], tsb[MAX_TRANKS];
 };
 
 // per-tile %globaltimer stamps for adi_set_trace (tools/tile_trace.py, trace_sync.py): only in
@@ -1735,13 +1744,24 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
           if (ok1) Ut[P.u_line] = P.edgeR ? P.edgeR[ln + 1] * P.gb : 0.0;
         }
       } else {
-        double* So = P.S_out + (long long)b * P.s_batch + (long long)p * P.so_pt + (long long)ln * P.so_line;
+        double* So;
+        if (P.tnp > 0) {
+          // fused transpose: the owner of position p (the cuts are few and sorted)
+          int q = 0;
+          while (q + 1 < P.tnp && p >= P.tcut[q + 1]) ++q;
+          So = P.tso[q] + (long long)b * P.tsb[q] + (long long)p * P.tpt[q] + (long long)ln;
+        } else {
+          So = P.S_out + (long long)b * P.s_batch + (long long)p * P.so_pt + (long long)ln * P.so_line;
+        }
         if (ok0 && ok1) *reinterpret_cast<double2*>(So) = make_double2(v0, v1);
-        else { if (ok0) So[0] = v0; if (ok1) So[P.so_line] = v1; }
+        else { if (ok0) So[0] = v0; if (ok1) So[P.tnp > 0 ? 1 : P.so_line] = v1; }
       }
     }
   }
   if (ASYNC_ST && P.tma_so && !P.carry && !async_s) bulk_wait_read();   // the X' copies read the tile
+  // fused transpose: this thread's stores into the other ranks' arrays (peer memory) are
+  // performed at system scope before the kernel can complete and the barrier release them
+  if (P.tnp > 0) __threadfence_system();
   if (P.flag && !isfinite(acc)) atomicOr(P.flag, 1);
   if (tr && tile < P.trace_cap) {
     unsigned smid;

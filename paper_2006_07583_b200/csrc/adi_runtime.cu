@@ -163,6 +163,15 @@ struct adi_ctx {
   std::vector<int> cut_y, cut_x;      // the ranks' Y_q, X_q
   adi_ctx** group = nullptr;          // loopback: all ranks (adi_create_dist_local)
   std::vector<double*> tsend, trecv;  // NCCL staging per peer (transpose mode)
+  // fused transpose (ADI_DIST_FUSED): the S' stores of the row / column
+  // kernels write straight into the owning rank's Sc / Sa; the all-to-all becomes a barrier.
+  // tpeer[q]: rank q's arrays as addressed from this process (the group's own pointers, or
+  // CUDA IPC mappings of the peers' allocations); ipc_open: the mappings to close
+  struct TPeer { double* Sc; double* Sa; long long pc, pa, aC, aS; };
+  std::vector<TPeer> tpeer;
+  bool tfused = false;
+  std::vector<void*> ipc_open;
+  double* dbar = nullptr;             // the barrier's one-element all-reduce buffer
   std::vector<size_t> tcount;
   cudaStream_t cs = nullptr;               // exchange stream (overlaps the column sweep)
   cudaEvent_t ev_pack = nullptr, ev_recv = nullptr;
@@ -245,6 +254,8 @@ struct NcclApi {
   ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) =
+      nullptr;
   ncclResult_t (*groupEnd)() = nullptr;
   const char* (*errorString)(ncclResult_t) = nullptr;
 };
@@ -263,6 +274,7 @@ bool nccl_load() {
   g_nccl.send = (decltype(g_nccl.send))sym("ncclSend");
   g_nccl.recv = (decltype(g_nccl.recv))sym("ncclRecv");
   g_nccl.groupStart = (decltype(g_nccl.groupStart))sym("ncclGroupStart");
+  g_nccl.allReduce = (decltype(g_nccl.allReduce))sym("ncclAllReduce");   // (optional: fused transpose)
   g_nccl.groupEnd = (decltype(g_nccl.groupEnd))sym("ncclGroupEnd");
   g_nccl.errorString = (decltype(g_nccl.errorString))sym("ncclGetErrorString");
   g_nccl.ok = g_nccl.getUniqueId && g_nccl.commInitRank && g_nccl.commDestroy && g_nccl.send && g_nccl.recv &&
@@ -946,6 +958,10 @@ int launch_thread(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
   return ADI_OK;
 }
 
+// the fused transpose is in use for this call's kernels (the stopping rule's attempts keep
+// the all-to-all: their stores are provisional)
+bool tm_fused_now(const adi_ctx* h) { return h->tmode && h->tfused && h->eps <= 0.0; }
+
 int launch(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p0, int kind) {
   TimeScope ts(h, kind);
   if (thread_mode(h) && (mode == adi::KM_SWEEP || mode == adi::KM_FINAL || mode == adi::KM_PROLOGUE) &&
@@ -965,7 +981,21 @@ int launch(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p0, int
   int rc;
   if (p.S_in && (rc = tmap_for(h, p.S_in, &p.tmS))) return rc;
   if ((rc = tmap_for(h, p.X_in, &p.tmX))) return rc;
-  if (mode == adi::KM_SWEEP && p.S_out && !h->het && !h->full && !p.carry && h->async_store) {
+  if (tm_fused_now(h) && (mode == adi::KM_SWEEP || mode == adi::KM_PROLOGUE) && (p.S_out == h->Sb || p.S_out == h->Sd)) {
+    // fused transpose: the row kernel's S2^T (positions x) lands in the owners' Sc, the
+    // column / prologue kernel's S1'^T (positions y) in the owners' Sa
+    const bool rows = (p.S_out == h->Sb);
+    const std::vector<int>& cut = rows ? h->cut_x : h->cut_y;
+    p.tnp = h->nranks;
+    for (int q = 0; q < h->nranks; ++q) {
+      const adi_ctx::TPeer& t = h->tpeer[q];
+      p.tcut[q] = cut[q];
+      p.tso[q] = rows ? t.Sc : t.Sa;
+      p.tpt[q] = rows ? t.pc : t.pa;
+      p.tsb[q] = rows ? t.aC : t.aS;
+    }
+    p.tcut[h->nranks] = 1 << 30;
+  } else if (mode == adi::KM_SWEEP && p.S_out && !h->het && !h->full && !p.carry && h->async_store) {
     if ((rc = tmap_store_for(h, p.S_out, &p.tmSo, &p.so_line0, &p.so_pos0))) return rc;
     p.tma_so = 1;
   }
@@ -1157,6 +1187,8 @@ void free_ctx(adi_ctx* h) {
       dfree(q);
     for (double* q : h->tsend) if (q) cudaFree(q);
     for (double* q : h->trecv) if (q) cudaFree(q);
+    for (void* q : h->ipc_open) cudaIpcCloseMemHandle(q);
+    if (h->dbar) cudaFree(h->dbar);
   } else {
     for (double* q : {rows_raw(h, h->Ubase, h->pu), rows_raw(h, h->V, h->pv), rows_raw(h, h->V2, h->pv),
                       rows_raw(h, h->Sa, h->pa), rows_raw(h, h->phi, h->pa), rows_raw(h, h->Ca, h->pa),
@@ -1344,7 +1376,7 @@ int adi_set_param(adi_handle h, int key, double v) {
   // keys that size or plan work already enqueued by adi_step_begin (the stopping rule's
   // norm buffer, the tile plan, the carry buffer) cannot change inside a call
   if (h->in_call && (key == ADI_K_SWEEPS || key == ADI_EPS || key == ADI_K_MIN || key == ADI_TILE_CHUNKS ||
-                     key == ADI_CARRY || key == ADI_RHO || key == ADI_THREAD_LINES))
+                     key == ADI_CARRY || key == ADI_RHO || key == ADI_THREAD_LINES || key == ADI_DIST_FUSED))
     return fail(h, ADI_ESTATE, "call in progress");
   if (key == ADI_K_SWEEPS) {
     if (!(v >= 1) || v != std::floor(v) || v > 1000) return fail(h, ADI_EINVAL, "K must be an integer >= 1");
@@ -1392,6 +1424,11 @@ int adi_set_param(adi_handle h, int key, double v) {
     if (v != 0.0 && v != 1.0 && v != -1.0) return fail(h, ADI_EINVAL, "thread lines must be -1, 0 or 1");
     h->small = (int)v;
     h->carry_valid = false;
+  } else if (key == ADI_DIST_FUSED) {
+    if (v != 0.0 && v != 1.0) return fail(h, ADI_EINVAL, "dist fused must be 0 or 1");
+    if (v == 1.0 && (!h->tmode || (int)h->tpeer.size() != h->nranks))
+      return fail(h, ADI_EINVAL, "no fused transpose on this handle (transpose mode, <= 8 ranks, peer mappings)");
+    h->tfused = (v == 1.0);
   } else if (key == ADI_ASYNC_STORE) {
     if (v != 0.0 && v != 1.0) return fail(h, ADI_EINVAL, "async store must be 0 or 1");
     h->async_store = (int)v;
@@ -1957,6 +1994,7 @@ int adi_step_end(adi_handle h) {
 
 static int dist_exchange(adi_ctx* h, int kind);
 static int tm_exchange(adi_ctx* h, int kind);
+static int tm_barrier(adi_ctx* h);
 
 // ADI_GRAPH: capture the call's launches on the capture stream, then launch the graph on
 // the handle's stream (kernel parameters differ from call to call -- time factors, the
@@ -2031,14 +2069,17 @@ int adi_step(adi_handle h, int nsteps) {
   if (h->graph_on && !h->capturing && !(h->dist && h->nranks > 1) && h->eps <= 0.0) return step_graph(h, nsteps);
   const bool ex = h->dist && h->nranks > 1;
   int rc = ADI_OK;
-  if (ex && h->tmode) {   // the transpose decomposition (NCCL all-to-all of S, DESIGN.md §7.3)
+  if (ex && h->tmode) {   // the transpose decomposition (NCCL all-to-all of S, DESIGN.md §7.2)
+    // fused: the kernels stored S into the owners' arrays; a barrier replaces the exchange
+    const bool fz = tm_fused_now(h);
+    auto xchg = [&](int kind) { return fz ? tm_barrier(h) : tm_exchange(h, kind); };
     rc = adi_step_begin(h, nsteps);
-    if (!rc) rc = tm_exchange(h, 1);
+    if (!rc) rc = xchg(1);
     for (int k = 0; k < nsteps && !rc; ++k) {
       rc = adi_step_rows(h);
-      if (!rc) rc = tm_exchange(h, 0);
+      if (!rc) rc = xchg(0);
       if (!rc) rc = adi_step_cols(h);
-      if (!rc && k + 1 < nsteps) rc = tm_exchange(h, 1);
+      if (!rc && k + 1 < nsteps) rc = xchg(1);
     }
     if (rc) { h->in_call = false; return rc; }
     return adi_step_end(h);
@@ -2519,6 +2560,108 @@ static int tm_exchange(adi_ctx* h, int kind) {
   return ADI_OK;
 }
 
+// the fused transpose's half-step barrier: every rank's kernels before it (which stored S
+// into the owners' arrays) complete before any rank's kernels after it (which read S, or
+// overwrite what the others still read).  A local group: each rank's stream waits for the
+// others' marks (adi_step_dist_local records them); NCCL: a one-element all-reduce, which
+// no rank passes before every rank has reached it in stream order
+static int tm_barrier(adi_ctx* h) {
+  if (h->loop) {
+    for (int q = 0; q < h->nranks; ++q)
+      if (q != h->rank) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->group[q]->ev_pack, 0));
+    return ADI_OK;
+  }
+  NCCL_TRY(h, g_nccl.allReduce(h->dbar, h->dbar, 1, ncclFloat64, ncclSum, h->comm, h->stream));
+  return ADI_OK;
+}
+
+// the fused transpose's peer table of a local group: the ranks' own arrays
+static void tm_fuse_local(adi_ctx** g, int P) {
+  for (int r = 0; r < P; ++r) {
+    g[r]->tpeer.clear();
+    for (int q = 0; q < P; ++q)
+      g[r]->tpeer.push_back({g[q]->Sc, g[q]->Sa, g[q]->pc, g[q]->pa, (long long)g[q]->aC, (long long)g[q]->aS});
+    g[r]->tfused = P <= adi::MAX_TRANKS;
+    if (!g[r]->tfused) g[r]->tpeer.clear();
+  }
+}
+
+// the fused transpose across processes: every rank's Sc and Sa allocations as CUDA IPC
+// handles, with the offsets of the absolute-index views, all-gathered over NCCL (grouped
+// send/recv of the records) and mapped with cudaIpcOpenMemHandle (peer access over
+// NVLink).  All ranks fuse or none: the outcome is agreed by an all-reduce, so the
+// protocols (barrier or all-to-all) match.  Failure of any step leaves the handle unfused
+static int tm_fuse_init(adi_ctx* h) {
+  const int P = h->nranks, r = h->rank;
+  if (P > adi::MAX_TRANKS || !g_nccl.allReduce) return ADI_OK;
+  struct Rec { cudaIpcMemHandle_t hc, ha; long long oc, oa, pc, pa, aC, aS; };
+  std::vector<Rec> recs(P);
+  double* Sc_raw = h->Sc + (ptrdiff_t)h->xa * h->pc;
+  double* Sa_raw = rows_raw(h, h->Sa, h->pa);
+  char* bc = reinterpret_cast<char*>(Sc_raw - adi::BUF_GUARD_FRONT);   // the cudaMalloc'd bases
+  char* ba = reinterpret_cast<char*>(Sa_raw - adi::BUF_GUARD_FRONT);
+  bool ok = cudaIpcGetMemHandle(&recs[r].hc, bc) == cudaSuccess && cudaIpcGetMemHandle(&recs[r].ha, ba) == cudaSuccess;
+  if (!ok) cudaGetLastError();
+  recs[r].oc = (long long)(reinterpret_cast<char*>(h->Sc) - bc);
+  recs[r].oa = (long long)(reinterpret_cast<char*>(h->Sa) - ba);
+  recs[r].pc = h->pc; recs[r].pa = h->pa; recs[r].aC = (long long)h->aC; recs[r].aS = (long long)h->aS;
+  CUDA_TRY(h, cudaMalloc(&h->dbar, 2 * sizeof(double)));
+  char* dbuf = nullptr;
+  CUDA_TRY(h, cudaMalloc(&dbuf, P * sizeof(Rec)));
+  int rc = ADI_OK;
+  const size_t sz = sizeof(Rec);
+  if (cudaMemcpy(dbuf + r * sz, &recs[r], sz, cudaMemcpyHostToDevice) != cudaSuccess) rc = ADI_ECUDA;
+  if (!rc && g_nccl.groupStart() != ncclSuccess) rc = ADI_ENCCL;
+  for (int q = 0; q < P && !rc; ++q) {
+    if (q == r) continue;
+    if (g_nccl.send(dbuf + r * sz, sz, ncclChar, q, h->comm, h->stream) != ncclSuccess ||
+        g_nccl.recv(dbuf + q * sz, sz, ncclChar, q, h->comm, h->stream) != ncclSuccess)
+      rc = ADI_ENCCL;
+  }
+  if (g_nccl.groupEnd() != ncclSuccess && !rc) rc = ADI_ENCCL;
+  if (!rc && (cudaStreamSynchronize(h->stream) != cudaSuccess ||
+              cudaMemcpy(recs.data(), dbuf, P * sz, cudaMemcpyDeviceToHost) != cudaSuccess))
+    rc = ADI_ECUDA;
+  cudaFree(dbuf);
+  if (rc) return fail(h, rc, "fused transpose: exchange of the IPC handles");
+  std::vector<adi_ctx::TPeer> tp(P);
+  for (int q = 0; q < P && ok; ++q) {
+    if (q == r) {
+      tp[q] = {h->Sc, h->Sa, h->pc, h->pa, (long long)h->aC, (long long)h->aS};
+      continue;
+    }
+    void *mc = nullptr, *ma = nullptr;
+    if (cudaIpcOpenMemHandle(&mc, recs[q].hc, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+        cudaIpcOpenMemHandle(&ma, recs[q].ha, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      if (mc) cudaIpcCloseMemHandle(mc);
+      ok = false;
+      break;
+    }
+    h->ipc_open.push_back(mc);
+    h->ipc_open.push_back(ma);
+    tp[q] = {reinterpret_cast<double*>(static_cast<char*>(mc) + recs[q].oc),
+             reinterpret_cast<double*>(static_cast<char*>(ma) + recs[q].oa), recs[q].pc, recs[q].pa, recs[q].aC,
+             recs[q].aS};
+  }
+  // agree: fused only if every rank mapped every peer (sum of failures == 0)
+  const double mine = ok ? 0.0 : 1.0;
+  double tot = 0.0;
+  if (cudaMemcpy(h->dbar, &mine, sizeof mine, cudaMemcpyHostToDevice) != cudaSuccess) return fail(h, ADI_ECUDA, "fused transpose");
+  NCCL_TRY(h, g_nccl.allReduce(h->dbar, h->dbar, 1, ncclFloat64, ncclSum, h->comm, h->stream));
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess ||
+      cudaMemcpy(&tot, h->dbar, sizeof tot, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(h, ADI_ECUDA, "fused transpose: agreement");
+  if (tot == 0.0) {
+    h->tpeer = tp;
+    h->tfused = true;
+  } else {
+    for (void* q : h->ipc_open) cudaIpcCloseMemHandle(q);
+    h->ipc_open.clear();
+  }
+  return ADI_OK;
+}
+
 // NCCL staging of the transpose mode (per peer, both directions and kinds)
 static int tm_init(adi_ctx* h) {
   const int P = h->nranks;
@@ -2590,6 +2733,7 @@ int adi_create_dist_ex(int nx, int ny, double hh, double dt, double c, int metho
       return ADI_ENCCL;
     }
     if ((rc = h->tmode ? tm_init(h) : dist_init(h))) { adi_destroy(h); return rc; }
+    if (h->tmode && (rc = tm_fuse_init(h))) { adi_destroy(h); return rc; }
   }
   *out = h;
   return warn;
@@ -2633,6 +2777,7 @@ int adi_create_dist_local_ex(int nx, int ny, double hh, double dt, double c, int
       return rc;
     }
   }
+  if (nranks > 1 && out[0]->tmode) tm_fuse_local(out, nranks);
   return warn;
 }
 
@@ -2656,17 +2801,20 @@ int adi_step_dist_local(adi_handle* hs, int nranks, int nsteps) {
   if (ex && hs[0]->tmode) {
     // the transpose decomposition: an all-to-all of S after the prologue, every row sweep
     // and every column sweep but the last (each producer records ev_pack first)
+    // (fused: the kernels stored S into the owners' arrays; every rank's stream then waits
+    // for every other rank's phase -- a barrier -- instead of copying)
     auto mark = [](adi_ctx* h) { return cudaEventRecord(h->ev_pack, h->stream) == cudaSuccess ? ADI_OK : ADI_ECUDA; };
+    auto xchg = [](adi_ctx* h, int kind) { return tm_fused_now(h) ? tm_barrier(h) : tm_exchange(h, kind); };
     rc = all([&](adi_ctx* h) { return adi_step_begin(h, nsteps); });
     if (!rc) rc = all(mark);
-    if (!rc) rc = all([](adi_ctx* h) { return tm_exchange(h, 1); });
+    if (!rc) rc = all([&](adi_ctx* h) { return xchg(h, 1); });
     for (int k = 0; k < nsteps && !rc; ++k) {
       rc = all([](adi_ctx* h) { return adi_step_rows(h); });
       if (!rc) rc = all(mark);
-      if (!rc) rc = all([](adi_ctx* h) { return tm_exchange(h, 0); });
+      if (!rc) rc = all([&](adi_ctx* h) { return xchg(h, 0); });
       if (!rc) rc = all([](adi_ctx* h) { return adi_step_cols(h); });
       if (!rc && k + 1 < nsteps) rc = all(mark);
-      if (!rc && k + 1 < nsteps) rc = all([](adi_ctx* h) { return tm_exchange(h, 1); });
+      if (!rc && k + 1 < nsteps) rc = all([&](adi_ctx* h) { return xchg(h, 1); });
     }
     if (rc) {
       for (int r = 0; r < nranks; ++r) hs[r]->in_call = false;

@@ -328,3 +328,78 @@ def test_torchrun_two_ranks_python_band_driver(adi, method):
                           str(method), "1601", "3"], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
     assert "DIST_CHECK_OK" in out.stdout
+
+
+def _run_transpose(adi, p, world, fused, split, batch=1, setup=None):
+    hs = adi.adi_create_dist_local(p.nx, p.ny, p.h, p.dt, p.c, p.method, batch, world, adi.ADI_DIST_TRANSPOSE)
+    ss = [adi.AdiSolver.adopt(h, p.nx, p.ny, p.h, p.dt, p.c, p.method, K=p.K, batch=batch) for h in hs]
+    for s in ss:
+        s.set_param(adi.ADI_DIST_FUSED, fused)
+        if setup:
+            setup(s)
+        else:
+            s.set_fields(p.U, p.V, p.W)
+            s.set_source(p.phi, None, p.gf)
+            s.set_boundary(p.edges, p.gb)
+    for k in split:
+        adi.adi_step_dist_local(hs, k)
+    got = _gather_dist(adi, ss, p.method, p.nx, p.ny, batch=batch)
+    for s in ss:
+        s.close()
+    return got
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+@pytest.mark.parametrize("n,world,split", [(301, 2, [3]), (1601, 4, [1, 2]), (2101, 8, [2]), (517, 3, [2, 1])])
+def test_dist_local_transpose_fused_bitwise(adi, method, n, world, split):
+    """ADI_DIST_FUSED: the row / column kernels store S' straight into the
+    owning rank's array and the all-to-all becomes a barrier -- bitwise the fields of the
+    all-to-all, split calls (prologue after set_fields and between calls), and the oracle."""
+    steps = sum(split)
+    p = random_problem(method, n, seed=5 * n + world, steps=steps)
+    fz = _run_transpose(adi, p, world, 1, split)
+    a2a = _run_transpose(adi, p, world, 0, split)
+    for a, b in zip(fz, a2a):
+        assert np.array_equal(a, b)
+    o = oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, p.U, p.V, p.W, nsteps=steps, **p.oracle_kwargs())
+    for name, a, c in zip("UVW", fz, o):
+        check(a, c, name=name, what="fused transpose vs oracle")
+
+
+def test_dist_local_transpose_fused_batch_points(adi):
+    """Fused transpose with a batch of point-source grids (per-grid peer strides)."""
+    n, world, B, steps = 1601, 4, 3, 3
+    probs = [ricker_problem(n, shot=s, nshots=4, steps=steps, f0=20.0, t0=0.05) for s in range(B)]
+    p0 = probs[0]
+    rng = np.random.default_rng(9)
+    U = np.stack([p.U for p in probs]) + rng.standard_normal((B,) + p0.U.shape)
+    V = np.stack([p.V for p in probs]); W = np.stack([p.W for p in probs])
+
+    def setup(s):
+        s.set_fields(U, V, W)
+        s.set_point_sources([p.src[0] for p in probs], [p.src[1] for p in probs], p0.gf)
+    fz = _run_transpose(adi, p0, world, 1, [steps], batch=B, setup=setup)
+    a2a = _run_transpose(adi, p0, world, 0, [steps], batch=B, setup=setup)
+    for a, b in zip(fz, a2a):
+        assert np.array_equal(a, b)
+    for b, p in enumerate(probs):
+        o = oracle.run(p.method, p.nx, p.ny, p.h, p.dt, p.c, p.K, U[b], p.V, p.W, nsteps=steps, src=p.src, gf=p.gf)
+        for name, a, c in zip("UVW", fz, o):
+            check(a[b], c, name=name, what=f"fused transpose shot {b}")
+
+
+def test_dist_fused_param_validation(adi):
+    """ADI_DIST_FUSED exists only on transpose-mode ranks with a peer table."""
+    p = random_problem(MFD, 129, seed=3, steps=1)
+    hs = adi.adi_create_dist_local(p.nx, p.ny, p.h, p.dt, p.c, MFD, 1, 2)   # halo mode
+    for h in hs:
+        with pytest.raises(adi.AdiError):
+            adi.adi_set_param(h, adi.ADI_DIST_FUSED, 1)
+        adi.adi_set_param(h, adi.ADI_DIST_FUSED, 0)
+        adi.adi_destroy(h)
+    s = adi.AdiSolver.from_problem(p)
+    with pytest.raises(adi.AdiError):
+        s.set_param(adi.ADI_DIST_FUSED, 1)
+    with pytest.raises(adi.AdiError):
+        s.set_param(adi.ADI_DIST_FUSED, 2)
+    s.close()
