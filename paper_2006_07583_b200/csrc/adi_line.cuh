@@ -1728,40 +1728,48 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     else { plo_ = max(sg.out_lo, ulo); phi_ = min(sg.out_hi, uhi + 1); }
     const double* r0 = stS + (2 * pr) * LSTR;
     const double* r1 = r0 + LSTR;
+    if (MODE != KM_FINAL && P.tnp > 0) {
+      // fused transpose: position p lands in the array of its owner q
+      // (the cuts are few and sorted; positions grow along a lane's loop), as P2P stores
+      int q = 0;
 #pragma unroll STORE_UNROLL
-    for (int pos = 16 * w + (lane & 15); pos < 32 * M; pos += 16 * NW) {
-      const int p = sg.start + pos;
-      if (p < plo_ || p >= phi_) continue;
-      const int si = (pos >> 5) * PADM + (pos & 31);
-      const double v0 = r0[si], v1 = r1[si];
-      if (MODE == KM_FINAL) {
-        double* Ub = P.U_out + (long long)b * P.u_batch + (long long)p * P.u_pt + (long long)ln * P.u_line;
-        if (ok0 && ok1) *reinterpret_cast<double2*>(Ub) = make_double2(v0, v1);
-        else { if (ok0) Ub[0] = v0; if (ok1) Ub[P.u_line] = v1; }
-        if (METHOD == M_MFD && p == n) {
-          double* Ut = P.U_out + (long long)b * P.u_batch + (long long)(n + 1) * P.u_pt + (long long)ln * P.u_line;
-          if (ok0) Ut[0] = P.edgeR ? P.edgeR[ln] * P.gb : 0.0;
-          if (ok1) Ut[P.u_line] = P.edgeR ? P.edgeR[ln + 1] * P.gb : 0.0;
-        }
-      } else {
-        double* So;
-        if (P.tnp > 0) {
-          // fused transpose: the owner of position p (the cuts are few and sorted)
-          int q = 0;
-          while (q + 1 < P.tnp && p >= P.tcut[q + 1]) ++q;
-          So = P.tso[q] + (long long)b * P.tsb[q] + (long long)p * P.tpt[q] + (long long)ln;
+      for (int pos = 16 * w + (lane & 15); pos < 32 * M; pos += 16 * NW) {
+        const int p = sg.start + pos;
+        if (p < plo_ || p >= phi_) continue;
+        while (q + 1 < P.tnp && p >= P.tcut[q + 1]) ++q;
+        const int si = (pos >> 5) * PADM + (pos & 31);
+        double* So = P.tso[q] + (long long)b * P.tsb[q] + (long long)p * P.tpt[q] + (long long)ln;
+        if (ok0 && ok1) *reinterpret_cast<double2*>(So) = make_double2(r0[si], r1[si]);
+        else { if (ok0) So[0] = r0[si]; if (ok1) So[1] = r1[si]; }
+      }
+      // this thread's peer stores are performed at system scope before the kernel can
+      // complete (and the barrier after it release them to the owners)
+      __threadfence_system();
+    } else {
+#pragma unroll STORE_UNROLL
+      for (int pos = 16 * w + (lane & 15); pos < 32 * M; pos += 16 * NW) {
+        const int p = sg.start + pos;
+        if (p < plo_ || p >= phi_) continue;
+        const int si = (pos >> 5) * PADM + (pos & 31);
+        const double v0 = r0[si], v1 = r1[si];
+        if (MODE == KM_FINAL) {
+          double* Ub = P.U_out + (long long)b * P.u_batch + (long long)p * P.u_pt + (long long)ln * P.u_line;
+          if (ok0 && ok1) *reinterpret_cast<double2*>(Ub) = make_double2(v0, v1);
+          else { if (ok0) Ub[0] = v0; if (ok1) Ub[P.u_line] = v1; }
+          if (METHOD == M_MFD && p == n) {
+            double* Ut = P.U_out + (long long)b * P.u_batch + (long long)(n + 1) * P.u_pt + (long long)ln * P.u_line;
+            if (ok0) Ut[0] = P.edgeR ? P.edgeR[ln] * P.gb : 0.0;
+            if (ok1) Ut[P.u_line] = P.edgeR ? P.edgeR[ln + 1] * P.gb : 0.0;
+          }
         } else {
-          So = P.S_out + (long long)b * P.s_batch + (long long)p * P.so_pt + (long long)ln * P.so_line;
+          double* So = P.S_out + (long long)b * P.s_batch + (long long)p * P.so_pt + (long long)ln * P.so_line;
+          if (ok0 && ok1) *reinterpret_cast<double2*>(So) = make_double2(v0, v1);
+          else { if (ok0) So[0] = v0; if (ok1) So[P.so_line] = v1; }
         }
-        if (ok0 && ok1) *reinterpret_cast<double2*>(So) = make_double2(v0, v1);
-        else { if (ok0) So[0] = v0; if (ok1) So[P.tnp > 0 ? 1 : P.so_line] = v1; }
       }
     }
   }
   if (ASYNC_ST && P.tma_so && !P.carry && !async_s) bulk_wait_read();   // the X' copies read the tile
-  // fused transpose: this thread's stores into the other ranks' arrays (peer memory) are
-  // performed at system scope before the kernel can complete and the barrier release them
-  if (P.tnp > 0) __threadfence_system();
   if (P.flag && !isfinite(acc)) atomicOr(P.flag, 1);
   if (tr && tile < P.trace_cap) {
     unsigned smid;
