@@ -884,10 +884,15 @@ def main():
            f"halo exchange inside adi_step overlapping the column sweep"}
     if ws > 1 and a.dist_mode == "transpose":
         cfg["parallelism"] = (f"{ws} GPUs: one grid, rows and columns owned by different ranks "
-                              f"(adi_create_dist_ex ADI_DIST_TRANSPOSE), NCCL all-to-all of S between the half-steps")
+                              f"(adi_create_dist_ex ADI_DIST_TRANSPOSE); S changes owner between the half-steps "
+                              f"by the fused transpose (the kernels store S' into the owners' arrays over NVLink "
+                              f"P2P, ADI_DIST_FUSED) where every rank maps its peers, else by an NCCL all-to-all")
     if a.dist_local > 1:
+        fused = a.dist_mode == "transpose" and "ADI_DIST_FUSED=0" not in a.set
+        xfer = ("fused transpose: the kernels store S' into the other ranks' arrays, a barrier between "
+                "the half-steps" if fused else "loopback exchange")
         cfg["parallelism"] = (f"1 GPU running {a.dist_local} ranks of adi_create_dist_local ({a.dist_mode} mode, "
-                              f"band-local arrays, loopback exchange): the decomposition's overhead, not a scaling "
+                              f"band-local arrays, {xfer}): the decomposition's overhead, not a scaling "
                               f"number")
     if a.full:
         cfg["workload"] = (f"config4 size: single {a.n}x{a.n}-node grid, full-matrix CFD variant (NEXT row "
