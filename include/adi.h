@@ -151,6 +151,15 @@ enum adi_param {
                            than 8 ranks, IPC unavailable: adi_create_dist_ex then leaves the
                            handle unfused on every rank).  Results are bitwise the same;
                            DESIGN.md §7.2 */
+  ADI_WARP_LINES = 15,  /* 1 (default): where ADI_THREAD_LINES selects the short-line kernels and
+                           every line has at most 64 stored positions (62 cells), one WARP runs
+                           a line (two positions per lane; the CFD solves as warp scans of the
+                           paper's LU recurrences); 0: one thread per line.
+                           Results agree to rounding */
+  ADI_STEP_INDEX = 16,  /* the handle's time level m (steps taken; t = m dt): the index into the
+                           source and boundary time tables of the next step.  Integer >= 0,
+                           between calls; drops the carried explicit half (ADI_CARRY).  With
+                           adi_set_fields, restarts a run from an initial state */
 };
 
 /* Kernel kinds launched by adi_step (index of adi_get_kernel_times arrays). */

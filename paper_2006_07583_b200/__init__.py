@@ -46,6 +46,8 @@ ADI_GRAPH = 11
 ADI_THREAD_LINES = 12
 ADI_ASYNC_STORE = 13
 ADI_DIST_FUSED = 14
+ADI_WARP_LINES = 15
+ADI_STEP_INDEX = 16
 ADI_DIST_HALO = 0
 ADI_DIST_TRANSPOSE = 1
 KERNEL_KINDS = ("prologue", "row", "col", "final", "edge")

@@ -9,7 +9,8 @@ ROOT = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "libadi.so")
 SOURCES = [os.path.join(HERE, "csrc", "adi_runtime.cu")]
 DEPS = SOURCES + [os.path.join(HERE, "csrc", "adi_line.cuh"),
-        os.path.join(HERE, "csrc", "adi_thread.cuh"), os.path.join(ROOT, "include", "adi.h")]
+        os.path.join(HERE, "csrc", "adi_thread.cuh"),
+        os.path.join(HERE, "csrc", "adi_warp.cuh"), os.path.join(ROOT, "include", "adi.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177"]
 

@@ -29,6 +29,7 @@
 #include "adi.h"
 #include "adi_line.cuh"
 #include "adi_thread.cuh"
+#include "adi_warp.cuh"
 
 namespace adi {
 
@@ -188,6 +189,7 @@ struct adi_ctx {
   // executable graph is kept and updated in place while the captured topology repeats
   int graph_on = 0;
   int small = -1;   // ADI_THREAD_LINES: -1 auto (short lines), 0 off, 1 on where possible
+  int warp_lines = 1;   // ADI_WARP_LINES: short lines (<= 64 positions) on the warp-per-line kernels
   int async_store = 0;   // ADI_ASYNC_STORE: the SWEEP tiles' outputs by TMA / bulk copies (measured:
                          // no gain, the store phase is bound by the memory system)
   bool capturing = false;
@@ -958,6 +960,23 @@ int launch_thread(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
   return ADI_OK;
 }
 
+// warp-per-line kernels (adi_warp.cuh): short lines of at most 64 stored positions
+bool warp_fits(const adi_ctx* h) {
+  return h->warp_lines && std::max(h->ax.n, h->ay.n) + 2 <= adi::WK_POS;
+}
+template <int METHOD, int MODE>
+int launch_warp(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
+  auto kern = adi::adi_warp_kernel<METHOD, MODE>;
+  const int nl = std::max(A.l1 - p.line0, 0);
+  if (nl <= 0) return ADI_OK;
+  dim3 grid((nl + adi::WK_WARPS - 1) / adi::WK_WARPS, 1, h->batch);
+  kern<<<grid, 32 * adi::WK_WARPS, 0, h->stream>>>(p);
+  CUDA_TRY(h, cudaGetLastError());
+  h->launches++;
+  if (!h->capturing) h->host_launches++;
+  return ADI_OK;
+}
+
 // the fused transpose is in use for this call's kernels (the stopping rule's attempts keep
 // the all-to-all: their stores are provisional)
 bool tm_fused_now(const adi_ctx* h) { return h->tmode && h->tfused && h->eps <= 0.0; }
@@ -968,6 +987,14 @@ int launch(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p0, int
       !p0.carry) {
     adi::KParams p = p0;
     const bool cfd = h->method == ADI_CFD;
+    if (warp_fits(h)) {
+      if (mode == adi::KM_SWEEP) return cfd ? launch_warp<adi::M_CFD, adi::KM_SWEEP>(h, A, p)
+                                            : launch_warp<adi::M_MFD, adi::KM_SWEEP>(h, A, p);
+      if (mode == adi::KM_FINAL) return cfd ? launch_warp<adi::M_CFD, adi::KM_FINAL>(h, A, p)
+                                            : launch_warp<adi::M_MFD, adi::KM_FINAL>(h, A, p);
+      return cfd ? launch_warp<adi::M_CFD, adi::KM_PROLOGUE>(h, A, p)
+                 : launch_warp<adi::M_MFD, adi::KM_PROLOGUE>(h, A, p);
+    }
     if (mode == adi::KM_SWEEP) return cfd ? launch_thread<adi::M_CFD, adi::KM_SWEEP>(h, A, p)
                                           : launch_thread<adi::M_MFD, adi::KM_SWEEP>(h, A, p);
     if (mode == adi::KM_FINAL) return cfd ? launch_thread<adi::M_CFD, adi::KM_FINAL>(h, A, p)
@@ -1376,7 +1403,8 @@ int adi_set_param(adi_handle h, int key, double v) {
   // keys that size or plan work already enqueued by adi_step_begin (the stopping rule's
   // norm buffer, the tile plan, the carry buffer) cannot change inside a call
   if (h->in_call && (key == ADI_K_SWEEPS || key == ADI_EPS || key == ADI_K_MIN || key == ADI_TILE_CHUNKS ||
-                     key == ADI_CARRY || key == ADI_RHO || key == ADI_THREAD_LINES || key == ADI_DIST_FUSED))
+                     key == ADI_CARRY || key == ADI_RHO || key == ADI_THREAD_LINES || key == ADI_DIST_FUSED ||
+                     key == ADI_STEP_INDEX))
     return fail(h, ADI_ESTATE, "call in progress");
   if (key == ADI_K_SWEEPS) {
     if (!(v >= 1) || v != std::floor(v) || v > 1000) return fail(h, ADI_EINVAL, "K must be an integer >= 1");
@@ -1429,6 +1457,13 @@ int adi_set_param(adi_handle h, int key, double v) {
     if (v == 1.0 && (!h->tmode || (int)h->tpeer.size() != h->nranks))
       return fail(h, ADI_EINVAL, "no fused transpose on this handle (transpose mode, <= 8 ranks, peer mappings)");
     h->tfused = (v == 1.0);
+  } else if (key == ADI_STEP_INDEX) {
+    if (!(v >= 0) || v != std::floor(v) || v > 1e15) return fail(h, ADI_EINVAL, "step index must be an integer >= 0");
+    h->m = (long long)v;
+    h->carry_valid = false;   // the carried explicit half belongs to the old time level
+  } else if (key == ADI_WARP_LINES) {
+    if (v != 0.0 && v != 1.0) return fail(h, ADI_EINVAL, "warp lines must be 0 or 1");
+    h->warp_lines = (int)v;
   } else if (key == ADI_ASYNC_STORE) {
     if (v != 0.0 && v != 1.0) return fail(h, ADI_EINVAL, "async store must be 0 or 1");
     h->async_store = (int)v;

@@ -14,11 +14,19 @@
 //
 // The line's working arrays (u, x and a temporary) live in shared memory as
 // [array][position][thread] (consecutive threads, consecutive banks); the bases S, X are
-// read from global memory (L1-resident at these sizes); the LU tables are broadcast.
+// read from global memory (L1-resident at these sizes).  A line's half-step is one long
+// dependent chain, so the kernel is built for latency: the LU tables are staged in shared
+// memory once per CTA (l, 1/d and c/d per position: the backward step is then ONE
+// dependent FMA, z = r/d - (c/d) z, with r/d off the chain), every array is addressed
+// through __restrict__ shared pointers, and the loops are unrolled so the loads of later
+// positions are issued ahead of the recurrence.
 #pragma once
 #include "adi_line.cuh"
 
 namespace adi {
+
+// doubles of the staged CFD LU tables ([2 systems][3][n + 1], rounded to 2 for alignment)
+__host__ __device__ inline int thread_tab_doubles(int n) { return (6 * (n + 1) + 1) & ~1; }
 
 template <int METHOD, int MODE>
 __global__ void __launch_bounds__(128) adi_thread_kernel(const __grid_constant__ KParams P) {
@@ -28,10 +36,23 @@ __global__ void __launch_bounds__(128) adi_thread_kernel(const __grid_constant__
   const int np = n + 2;   // stored positions 0..n+1 (the MFD ū_{n+1} slot)
   const int line = P.line0 + blockIdx.x * T + t;
   const int b = blockIdx.z;
+  // CFD: the LU tables of both systems, [u-op, x-op][l, 1/d, c/d][n + 1]
+  double* __restrict__ tab = tsm;
+  if (METHOD == M_CFD) {
+    const int n1 = n + 1;
+    for (int i = t; i < n1; i += T) {
+      const double ul = P.tabU[i], ui = P.tabU[n1 + i], uc = P.tabU[2 * n1 + i];
+      const double xl = P.tabX[i], xi = P.tabX[n1 + i], xc = P.tabX[2 * n1 + i];
+      tab[i] = ul; tab[n1 + i] = ui; tab[2 * n1 + i] = uc * ui;
+      tab[3 * n1 + i] = xl; tab[4 * n1 + i] = xi; tab[5 * n1 + i] = xc * xi;
+    }
+    __syncthreads();
+  }
   if (line < P.line_lo || line >= P.nlines) return;
-  double* U = tsm + t;                 // u (pressure of this direction), slots 0 and n (CFD) / n+1 (MFD)
-  double* X = tsm + (size_t)np * T + t;       // x (velocity of this direction)
-  double* R = tsm + (size_t)2 * np * T + t;   // temporary (stencil, Thomas)
+  double* const arr = tsm + (METHOD == M_CFD ? thread_tab_doubles(n) : 0);
+  double* __restrict__ U = arr + t;                          // u (pressure of this direction), slots 0 and n (CFD) / n+1 (MFD)
+  double* __restrict__ X = arr + (size_t)np * T + t;         // x (velocity of this direction)
+  double* __restrict__ R = arr + (size_t)2 * np * T + t;     // temporary (stencil, Thomas)
   auto u = [&](int p) -> double& { return U[(size_t)p * T]; };
   auto x = [&](int p) -> double& { return X[(size_t)p * T]; };
   auto r = [&](int p) -> double& { return R[(size_t)p * T]; };
@@ -63,44 +84,54 @@ __global__ void __launch_bounds__(128) adi_thread_kernel(const __grid_constant__
   // u-op: out_p = B_p - alpha D̄(x)_p on the u positions [1, uhi]; out may alias B
   auto uop = [&](auto&& B, auto&& out) {
     if (METHOD == M_CFD) {
-      const double* tl = P.tabU;
-      const double* ti = P.tabU + (n + 1);
-      const double* tc = P.tabU + 2 * (n + 1);
+      const double* __restrict__ tl = tab;
+      const double* __restrict__ ti = tab + (n + 1);
+      const double* __restrict__ tc = tab + 2 * (n + 1);   // c/d
       r(1) = (-x(0) - 9.0 * x(1) + 9.0 * x(2) + x(3)) * (1.0 / 3.0);
+#pragma unroll 4
       for (int p = 2; p <= n - 2; ++p) r(p) = x(p + 1) - x(p - 1);
       r(n - 1) = (-x(n - 3) - 9.0 * x(n - 2) + 9.0 * x(n - 1) + x(n)) * (1.0 / 3.0);
       double y = r(1);
+#pragma unroll 8
       for (int p = 2; p <= n - 1; ++p) { y = fma(-tl[p], y, r(p)); r(p) = y; }
       double z = y * ti[n - 1];
       r(n - 1) = z;
-      for (int p = n - 2; p >= 1; --p) { z = (r(p) - tc[p] * z) * ti[p]; r(p) = z; }
+#pragma unroll 8
+      for (int p = n - 2; p >= 1; --p) { z = fma(-tc[p], z, r(p) * ti[p]); r(p) = z; }
+#pragma unroll 4
       for (int p = 1; p <= n - 1; ++p) out(p) = fma(-P.cu, r(p), B(p));
     } else {
       const double a = P.cu, cA = P.mA, cB = P.mB;
       double s = 0.0;
       for (int k = 0; k < 6; ++k) s = fma(c_d4r0[k], x(k), s);
       r(1) = fma(-a, s, B(1));
+#pragma unroll 4
       for (int p = 2; p <= n - 1; ++p) r(p) = fma(cA, x(p + 1) - x(p - 2), fma(cB, x(p - 1) - x(p), B(p)));
       s = 0.0;
       for (int k = 0; k < 6; ++k) s = fma(-c_d4r0[5 - k], x(n - 5 + k), s);
       r(n) = fma(-a, s, B(n));
+#pragma unroll 4
       for (int p = 1; p <= n; ++p) out(p) = r(p);
     }
   };
   // x-op: out_p = B_p - beta D([gL, u, gR])_p on the nodes [0, n]; out may alias B
   auto xop = [&](auto&& B, auto&& out) {
     if (METHOD == M_CFD) {
-      const double* tl = P.tabX;
-      const double* ti = P.tabX + (n + 1);
-      const double* tc = P.tabX + 2 * (n + 1);
+      const double* __restrict__ tl = tab + 3 * (n + 1);
+      const double* __restrict__ ti = tab + 4 * (n + 1);
+      const double* __restrict__ tc = tab + 5 * (n + 1);   // c/d
       r(0) = (-17.0 * u(0) + 9.0 * u(1) + 9.0 * u(2) - u(3)) * (1.0 / 3.0);
+#pragma unroll 4
       for (int p = 1; p <= n - 1; ++p) r(p) = u(p + 1) - u(p - 1);
       r(n) = (u(n - 3) - 9.0 * u(n - 2) - 9.0 * u(n - 1) + 17.0 * u(n)) * (1.0 / 3.0);
       double y = r(0);
+#pragma unroll 8
       for (int p = 1; p <= n; ++p) { y = fma(-tl[p], y, r(p)); r(p) = y; }
       double z = y * ti[n];
       r(n) = z;
-      for (int p = n - 1; p >= 0; --p) { z = (r(p) - tc[p] * z) * ti[p]; r(p) = z; }
+#pragma unroll 8
+      for (int p = n - 1; p >= 0; --p) { z = fma(-tc[p], z, r(p) * ti[p]); r(p) = z; }
+#pragma unroll 4
       for (int p = 0; p <= n; ++p) out(p) = fma(-P.cx, r(p), B(p));
     } else {
       const double bb = P.cx, cC = P.mC, cD = P.mD;
@@ -110,6 +141,7 @@ __global__ void __launch_bounds__(128) adi_thread_kernel(const __grid_constant__
       s = 0.0;
       for (int k = 0; k < 5; ++k) s = fma(c_g4r1[k], u(k), s);
       r(1) = fma(-bb, s, B(1));
+#pragma unroll 4
       for (int p = 2; p <= n - 2; ++p) r(p) = fma(cC, u(p + 2) - u(p - 1), fma(cD, u(p) - u(p + 1), B(p)));
       s = 0.0;
       for (int k = 0; k < 4; ++k) s = fma(-c_g4r1[4 - k], u(n - 3 + k), s);
@@ -119,6 +151,7 @@ __global__ void __launch_bounds__(128) adi_thread_kernel(const __grid_constant__
       for (int k = 0; k < 5; ++k) s = fma(-c_g4r0[5 - k], u(n - 4 + k), s);
       s = fma(-c_g4r0[0], gR, s);
       r(n) = fma(-bb, s, B(n));
+#pragma unroll 4
       for (int p = 0; p <= n; ++p) out(p) = r(p);
     }
   };
@@ -170,12 +203,12 @@ __global__ void __launch_bounds__(128) adi_thread_kernel(const __grid_constant__
 }
 
 // threads per CTA of the thread kernels for lines of n cells: three [n+2][T] arrays of
-// doubles within 200 KB of shared memory
+// doubles and the CFD LU tables within 200 KB of shared memory
 inline int thread_tpb(int n) {
   int T = 128;
-  while (T > 32 && (size_t)3 * (n + 2) * T * 8 > 200 * 1024) T /= 2;
+  while (T > 32 && ((size_t)3 * (n + 2) * T + thread_tab_doubles(n)) * 8 > 200 * 1024) T /= 2;
   return T;
 }
-inline size_t thread_smem(int n, int T) { return (size_t)3 * (n + 2) * T * sizeof(double); }
+inline size_t thread_smem(int n, int T) { return ((size_t)3 * (n + 2) * T + thread_tab_doubles(n)) * sizeof(double); }
 
 }  // namespace adi

@@ -497,3 +497,77 @@ def test_async_store_knob_bitwise(adi, method, n):
         s.close()
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
+
+
+def _short_run(adi, p, steps, warp, split=None, batch_probs=None):
+    s = adi.AdiSolver.from_problem(p)
+    s.set_param(adi.ADI_THREAD_LINES, 1)
+    s.set_param(adi.ADI_WARP_LINES, warp)
+    for k in (split or [steps]):
+        s.step(k)
+    out = s.get_fields()
+    s.close()
+    return out
+
+
+@pytest.mark.parametrize("method", [CFD, MFD])
+@pytest.mark.parametrize("nx,ny", [(9, 9), (17, 33), (41, 41), (61, 61), (41, 9), (9, 61), (62, 40)])
+def test_warp_kernels_parity(adi, method, nx, ny):
+    """Warp-per-line kernels (adi_warp.cuh): lines of up to 64 stored positions,
+    random state, dense source, boundary data, split calls (prologue twice), against the
+    oracle, and against the thread-per-line kernels to rounding (same LU recurrences,
+    reassociated into warp scans)."""
+    steps = 5
+    p = random_problem(method, nx, ny=ny, seed=3 * nx + ny, steps=steps)
+    w = _short_run(adi, p, steps, 1, split=[2, 3])
+    assert_parity(w, run_oracle(p, steps), what=f"warp {nx}x{ny}")
+    t = _short_run(adi, p, steps, 0, split=[2, 3])
+    for name, a, b in zip("UVW", w, t):
+        d = np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+        assert d <= 1e-13, (name, d)
+
+
+def test_warp_kernels_batch_points(adi):
+    """A batch of point-source grids on the warp kernels (41^2, MFD and CFD)."""
+    for method in (CFD, MFD):
+        n, B, steps = 41, 3, 6
+        probs = [random_problem(method, n, seed=60 + k, steps=steps, source=False) for k in range(B)]
+        gf = np.random.default_rng(6).standard_normal(2 * steps + 1)
+        for k, p in enumerate(probs):
+            p.src = (5 + 7 * k, 30 - 9 * k)
+            p.gf = gf
+        p0 = probs[0]
+        s = adi.AdiSolver(n, n, p0.h, p0.dt, p0.c, method, batch=B, K=p0.K)
+        s.set_param(adi.ADI_THREAD_LINES, 1)
+        s.set_fields(np.stack([p.U for p in probs]), np.stack([p.V for p in probs]), np.stack([p.W for p in probs]))
+        s.set_point_sources([p.src[0] for p in probs], [p.src[1] for p in probs], gf)
+        s.set_boundary(p0.edges, p0.gb)
+        s.step(steps)
+        got = s.get_fields()
+        s.close()
+        for k, p in enumerate(probs):
+            q = p
+            q.edges, q.gb = p0.edges, p0.gb
+            assert_parity([x[k] for x in got], run_oracle(q, steps), what=f"warp batch {k} m{method}")
+
+
+@pytest.mark.parametrize("method,n,graph", [(CFD, 41, 1), (MFD, 301, 0), (CFD, 1601, 0)])
+def test_step_index_restart_bitwise(adi, method, n, graph):
+    """ADI_STEP_INDEX with adi_set_fields restarts a run: a second call from the initial state
+    at time level 0 reproduces the first call bitwise (graph replay, carried explicit half
+    dropped, tables re-read from step 0)."""
+    steps = 3
+    p = random_problem(method, n, seed=n + 5, steps=steps)
+    s = adi.AdiSolver.from_problem(p)
+    s.set_param(adi.ADI_GRAPH, graph)
+    s.step(steps)
+    a = s.get_fields()
+    s.set_fields(p.U, p.V, p.W)
+    s.set_param(adi.ADI_STEP_INDEX, 0)
+    s.step(steps)
+    b = s.get_fields()
+    with pytest.raises(adi.AdiError):
+        s.set_param(adi.ADI_STEP_INDEX, -1)
+    s.close()
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
