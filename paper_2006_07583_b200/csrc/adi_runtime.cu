@@ -932,12 +932,20 @@ int launch_het(adi_ctx* h, int mode, const adi::Axis& A, const adi::KParams& p) 
 #ifndef ADI_THREAD_AUTO_MAX
 #define ADI_THREAD_AUTO_MAX 64    // cells per line up to which the auto mode uses them (measured: faster at 40, slower at 80)
 #endif
+#ifndef ADI_WARP_AUTO_MAX
+#define ADI_WARP_AUTO_MAX 382     // cells per line up to which the auto mode uses the warp kernels (§5.9)
+#endif
+// warp-per-line kernels (adi_warp.cuh): lines of at most 384 stored positions
+bool warp_fits(const adi_ctx* h) {
+  return h->warp_lines && adi::warp_npl(std::max(h->ax.n, h->ay.n)) > 0;
+}
+// the short-line kernels (warp- or thread-per-line) run this handle's sweeps
 bool thread_mode(const adi_ctx* h) {
   if (h->small == 0 || h->het || h->full || h->eps > 0.0 || h->tile_chunks > 0) return false;
   if (h->band_y0 > 0 || h->band_y1 < h->ay.n + 1 || (h->dist && h->nranks > 1)) return false;
   const int nmax = std::max(h->ax.n, h->ay.n);
-  if (h->small < 0) return nmax <= ADI_THREAD_AUTO_MAX;
-  return adi::thread_smem(nmax, 32) <= 200 * 1024;
+  if (h->small < 0) return warp_fits(h) ? nmax <= ADI_WARP_AUTO_MAX : nmax <= ADI_THREAD_AUTO_MAX;
+  return warp_fits(h) || adi::thread_smem(nmax, 32) <= 200 * 1024;
 }
 
 template <int METHOD, int MODE>
@@ -960,21 +968,30 @@ int launch_thread(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
   return ADI_OK;
 }
 
-// warp-per-line kernels (adi_warp.cuh): short lines of at most 64 stored positions
-bool warp_fits(const adi_ctx* h) {
-  return h->warp_lines && std::max(h->ax.n, h->ay.n) + 2 <= adi::WK_POS;
-}
-template <int METHOD, int MODE>
-int launch_warp(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
-  auto kern = adi::adi_warp_kernel<METHOD, MODE>;
+template <int METHOD, int MODE, int NPL>
+int launch_warp_n(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
+  auto kern = adi::adi_warp_kernel<METHOD, MODE, NPL>;
   const int nl = std::max(A.l1 - p.line0, 0);
   if (nl <= 0) return ADI_OK;
   dim3 grid((nl + adi::WK_WARPS - 1) / adi::WK_WARPS, 1, h->batch);
-  kern<<<grid, 32 * adi::WK_WARPS, 0, h->stream>>>(p);
+  kern<<<grid, 32 * adi::WK_WARPS, adi::warp_smem_bytes<NPL>(), h->stream>>>(p);
   CUDA_TRY(h, cudaGetLastError());
   h->launches++;
   if (!h->capturing) h->host_launches++;
   return ADI_OK;
+}
+// positions per lane from the handle's longer line (both sweeps use one instantiation)
+template <int METHOD, int MODE>
+int launch_warp(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
+  switch (adi::warp_npl(std::max(h->ax.n, h->ay.n))) {
+    case 2: return launch_warp_n<METHOD, MODE, 2>(h, A, p);
+    case 4: return launch_warp_n<METHOD, MODE, 4>(h, A, p);
+    case 6: return launch_warp_n<METHOD, MODE, 6>(h, A, p);
+    case 8: return launch_warp_n<METHOD, MODE, 8>(h, A, p);
+    case 10: return launch_warp_n<METHOD, MODE, 10>(h, A, p);
+    case 12: return launch_warp_n<METHOD, MODE, 12>(h, A, p);
+    default: return fail(h, ADI_EINVAL, "internal: line too long for the warp kernels");
+  }
 }
 
 // the fused transpose is in use for this call's kernels (the stopping rule's attempts keep
