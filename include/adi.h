@@ -127,13 +127,15 @@ enum adi_param {
                            paper's own observation).  Same kernels, same
                            results bit for bit.  Plain and banded handles without ADI_EPS;
                            ignored for adi_create_dist ranks.  Default 0 */
-  ADI_THREAD_LINES = 12, /* the thread-per-line kernels (one thread runs one grid line through a
-                           half-step with the no-pivot LU of App. A) instead of
-                           the warp-per-line tiles: -1 (default) for lines of at most 64 cells,
-                           1 wherever they fit (<= ~260 cells), 0 never.  Plain handles of
-                           ADI_CFD / ADI_MFD with fixed K (no band, media, stopping rule,
-                           ADI_CFD_FULL, ADI_TILE_CHUNKS); results agree with the tile kernels
-                           to rounding (parity-tested against the oracle) */
+  ADI_THREAD_LINES = 12, /* the short-line kernels (one warp -- ADI_WARP_LINES --
+                           or one thread per grid line through a half-step, with the no-pivot
+                           LU of App. A) instead of the 1024-position line tiles: -1 (default)
+                           for lines of at most 382 cells (warp kernels; 64 with
+                           ADI_WARP_LINES = 0), 1 wherever they fit (warp: <= 382 cells, thread:
+                           <= ~260), 0 never.  Plain handles of ADI_CFD / ADI_MFD with fixed K
+                           (no band, media, stopping rule, ADI_CFD_FULL, ADI_TILE_CHUNKS);
+                           results agree with the tile kernels to rounding (parity-tested
+                           against the oracle) */
   ADI_ASYNC_STORE = 13, /* 1: the lean ADI-rows / ADI-columns tiles store their outputs
                            asynchronously -- X' by bulk copies, S'^T by TMA tensor stores of
                            {4 lines, 4 positions} boxes from a re-staged tile;
@@ -152,8 +154,8 @@ enum adi_param {
                            handle unfused on every rank).  Results are bitwise the same;
                            DESIGN.md §7.2 */
   ADI_WARP_LINES = 15,  /* 1 (default): where ADI_THREAD_LINES selects the short-line kernels and
-                           every line has at most 64 stored positions (62 cells), one WARP runs
-                           a line (two positions per lane; the CFD solves as warp scans of the
+                           every line has at most 384 stored positions (382 cells), one WARP runs
+                           a line (2..12 positions per lane; the CFD solves as warp scans of the
                            paper's LU recurrences); 0: one thread per line.
                            Results agree to rounding */
   ADI_STEP_INDEX = 16,  /* the handle's time level m (steps taken; t = m dt): the index into the
