@@ -315,14 +315,16 @@ def run_ours(a, ws, rank, local):
     uid = None
     dmode = adi.ADI_DIST_TRANSPOSE if a.dist_mode == "transpose" else adi.ADI_DIST_HALO
     if ws > 1:
+        # one NCCL unique id per communicator (one per method): an id's bootstrap serves
+        # a single ncclCommInitRank
         import torch.distributed as tdist
-        box = [adi.adi_nccl_unique_id() if rank == 0 else None]
+        box = [[adi.adi_nccl_unique_id() for _ in methods] if rank == 0 else None]
         tdist.broadcast_object_list(box, src=0)
         uid = box[0]
-    for m in methods:
+    for mi, m in enumerate(methods):
         p = make_problem(m, n, total_steps + a.steps + 4, a.K, a.media)
         if ws > 1:
-            hd, st = adi.adi_create_dist_ex(p.nx, p.ny, p.h, p.dt, p.c, m, 1, uid, rank, ws, dmode)
+            hd, st = adi.adi_create_dist_ex(p.nx, p.ny, p.h, p.dt, p.c, m, 1, uid[mi], rank, ws, dmode)
             s = adi.AdiSolver.adopt(hd, p.nx, p.ny, p.h, p.dt, p.c, m, K=a.K, stream=stream.cuda_stream, status=st)
         elif a.dist_local > 1:
             s = LocalRanks(adi, p, m, a.dist_local, a.K, stream.cuda_stream, dmode)
