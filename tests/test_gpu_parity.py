@@ -512,13 +512,14 @@ def _short_run(adi, p, steps, warp, split=None, batch_probs=None):
 
 @pytest.mark.parametrize("method", [CFD, MFD])
 @pytest.mark.parametrize("nx,ny", [(9, 9), (17, 33), (41, 41), (61, 61), (41, 9), (9, 61), (62, 40),
-                                   (63, 63), (81, 81), (130, 97), (161, 161), (321, 257), (383, 40)])
+                                   (63, 63), (81, 81), (130, 97), (161, 161), (321, 257), (383, 40),
+                                   (384, 40)])
 def test_warp_kernels_parity(adi, method, nx, ny):
     """Warp-per-line kernels (adi_warp.cuh): lines of up to 384 stored
-    positions (2 .. 12 per lane, the instantiation edges 62/63 and 382/383 cells), random
-    state, dense source, boundary data, split calls (prologue twice), against the oracle,
-    and against the thread-per-line (or, where those do not fit, the tile) kernels to
-    rounding (same LU recurrences, reassociated into warp scans)."""
+    positions (2 .. 12 per lane, the instantiation edges 62/63 and 382/383 cells; 383 cells
+    back on the tiles), random state, dense source, boundary data, split calls (prologue
+    twice), against the oracle, and against the thread-per-line (or, where those do not
+    fit, the tile) kernels to rounding (same LU recurrences, reassociated into warp scans)."""
     steps = 5
     p = random_problem(method, nx, ny=ny, seed=3 * nx + ny, steps=steps)
     w = _short_run(adi, p, steps, 1, split=[2, 3])
