@@ -1,7 +1,7 @@
 """Out-of-bounds writes, checked without compute-sanitizer (which this pool does not run):
 with ADI_GUARD_CHECK=1 every field array's guard regions hold a canary pattern, and
 adi_check_guards counts overwritten guard words.  Every kernel kind runs here -- lean and
-generic tiles, the carry kernel, FINAL, the thread-per-line kernels, media, the full-matrix
+generic tiles, the carry kernel, FINAL, the warp- and thread-per-line kernels, media, the full-matrix
 variant, the stopping rule, graph capture, the async stores, band-local re-layouts and both
 dist-local decompositions -- and no guard word may change.  The results must also equal
 those of zero guards bit for bit (no result depends on what lies beyond an array)."""
@@ -41,7 +41,9 @@ def _plain(adi, p, params, plan):
 
 CASES = [("lean", 1601, [], [2, 1, ("ADI_CARRY", 0), 1]),
          ("generic", 333, [("ADI_THREAD_LINES", 0)], [2, 1]),
-         ("thread", 41, [("ADI_THREAD_LINES", 1)], [2, 1]),
+         ("warp", 41, [("ADI_THREAD_LINES", 1)], [2, 1]),
+         ("warp12", 321, [("ADI_THREAD_LINES", 1)], [2, 1]),
+         ("thread", 41, [("ADI_THREAD_LINES", 1), ("ADI_WARP_LINES", 0)], [2, 1]),
          ("segments", 1001, [("ADI_TILE_CHUNKS", 12)], [2]),
          ("graph", 1601, [("ADI_GRAPH", 1)], [2, 2]),
          ("async", 2101, [("ADI_ASYNC_STORE", 1)], [2, 1]),
@@ -81,10 +83,12 @@ def test_no_guard_word_written_full_bands_dist(adi):
         s.step(1)
         assert adi.adi_check_guards(s.handle) == 0
         s.close()
-        for mode in (adi.ADI_DIST_HALO, adi.ADI_DIST_TRANSPOSE):
+        for mode, fused in ((adi.ADI_DIST_HALO, 0), (adi.ADI_DIST_TRANSPOSE, 1), (adi.ADI_DIST_TRANSPOSE, 0)):
             hs = adi.adi_create_dist_local(p.nx, p.ny, p.h, p.dt, p.c, method, 1, 3, mode)
             ss = [adi.AdiSolver.adopt(x, p.nx, p.ny, p.h, p.dt, p.c, method) for x in hs]
             for x in ss:
+                if mode == adi.ADI_DIST_TRANSPOSE:
+                    x.set_param(adi.ADI_DIST_FUSED, fused)   # the peer stores / the all-to-all
                 x.set_fields(p.U, p.V, p.W)
                 x.set_source(p.phi, None, p.gf)
                 x.set_boundary(p.edges, p.gb)
