@@ -2663,14 +2663,19 @@ static int tm_fuse_init(adi_ctx* h) {
   int rc = ADI_OK;
   const size_t sz = sizeof(Rec);
   if (cudaMemcpy(dbuf + r * sz, &recs[r], sz, cudaMemcpyHostToDevice) != cudaSuccess) rc = ADI_ECUDA;
-  if (!rc && g_nccl.groupStart() != ncclSuccess) rc = ADI_ENCCL;
-  for (int q = 0; q < P && !rc; ++q) {
-    if (q == r) continue;
-    if (g_nccl.send(dbuf + r * sz, sz, ncclChar, q, h->comm, h->stream) != ncclSuccess ||
-        g_nccl.recv(dbuf + q * sz, sz, ncclChar, q, h->comm, h->stream) != ncclSuccess)
+  if (!rc) {
+    if (g_nccl.groupStart() != ncclSuccess) {
       rc = ADI_ENCCL;
+    } else {
+      for (int q = 0; q < P && !rc; ++q) {
+        if (q == r) continue;
+        if (g_nccl.send(dbuf + r * sz, sz, ncclChar, q, h->comm, h->stream) != ncclSuccess ||
+            g_nccl.recv(dbuf + q * sz, sz, ncclChar, q, h->comm, h->stream) != ncclSuccess)
+          rc = ADI_ENCCL;
+      }
+      if (g_nccl.groupEnd() != ncclSuccess && !rc) rc = ADI_ENCCL;
+    }
   }
-  if (g_nccl.groupEnd() != ncclSuccess && !rc) rc = ADI_ENCCL;
   if (!rc && (cudaStreamSynchronize(h->stream) != cudaSuccess ||
               cudaMemcpy(recs.data(), dbuf, P * sz, cudaMemcpyDeviceToHost) != cudaSuccess))
     rc = ADI_ECUDA;
