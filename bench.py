@@ -63,7 +63,7 @@ def parse():
                          "1601^2, CFD and MFD, 100 timed steps.  One JSON line; 0 = config 4 (the default)")
     ap.add_argument("--no-graph", action="store_true", help="configs 1-3: plain launches instead of ADI_GRAPH")
     ap.add_argument("--set", action="append", default=[], metavar="KEY=VAL",
-                    help="adi_set_param on the timed solvers (A/B of a knob), e.g. --set ADI_WHOLE_LINES=0")
+                    help="adi_set_param on the timed solvers (A/B of a knob), e.g. --set ADI_WARP_LINES=0")
     ap.add_argument("--dist-mode", default="halo", choices=["halo", "transpose"],
                     help="N > 1 (and --dist-local): the band decomposition with halo exchange (default) or "
                          "the north_star's all-to-all transpose between the half-steps (ADI_DIST_TRANSPOSE)")
