@@ -162,6 +162,11 @@ enum adi_param {
                            source and boundary time tables of the next step.  Integer >= 0,
                            between calls; drops the carried explicit half (ADI_CARRY).  With
                            adi_set_fields, restarts a run from an initial state */
+  ADI_FRAG_TILES = 17,  /* performance knob: 1 (default) runs the MFD sweeps of whole lines whose
+                           1024-position tiles leave a short middle gap (4096 positions: 4 tiles
+                           and a 168-position gap instead of 5 tiles) as the lean tiles plus one
+                           8-chunk fragment per line, 4 lines' fragments per warp (DESIGN.md
+                           §5.12); 0: the standard tile plan.  Results agree to rounding */
 };
 
 /* Kernel kinds launched by adi_step (index of adi_get_kernel_times arrays). */

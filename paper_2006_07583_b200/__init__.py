@@ -48,6 +48,7 @@ ADI_ASYNC_STORE = 13
 ADI_DIST_FUSED = 14
 ADI_WARP_LINES = 15
 ADI_STEP_INDEX = 16
+ADI_FRAG_TILES = 17
 ADI_DIST_HALO = 0
 ADI_DIST_TRANSPOSE = 1
 KERNEL_KINDS = ("prologue", "row", "col", "final", "edge")

@@ -991,8 +991,13 @@ constexpr bool MFD_EPI_REG = ADI_MFD_EPI_REG;
 // are interior and live (the lean path, no generic closures, no per-chunk
 // predicates); EDGE = true: line ends, dead chunks, short lines.
 // ===========================================================================
+// PACK (fragment tiles): a warp carries the FC-chunk middle fragments of
+// 32 / FC lines -- lanes [g FC, (g+1) FC) hold line g's chunks; the CTA's 4 warps hold
+// 16 consecutive lines.  MFD SWEEP interior segments only; the shuffles at the fragment
+// seams read the next fragment's values, which the 28-point halos absorb
+constexpr int FRAG_CH = 8;
 template <int METHOD, int M, int NW, int MODE_, bool EDGE, bool HET = false, bool FULL = false,
-          bool NOEND = false>
+          bool NOEND = false, bool PACK = false>
 __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, double* smem) {
   // FULL (NEXT row f4, CFD only, readings F1-F2): every position 0..n is
   // unknown and both operators are the full D = P^{-1} Q (the x-op's operator)
@@ -1017,7 +1022,13 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
 
   const int t = threadIdx.x;
   const int w = t >> 5, lane = t & 31;
-  const int line = P.line0 + blockIdx.x * NW + w;   // cross position of this line
+  static_assert(!PACK || (METHOD == M_MFD && MODE_ == KM_SWEEP && !EDGE && !HET && !FULL && NOEND),
+                "fragment tiles: MFD interior SWEEP");
+  constexpr int LPW = PACK ? 32 / FRAG_CH : 1;   // lines per warp
+  const int grp = PACK ? lane / FRAG_CH : 0;      // this lane's line within the warp
+  const int cl = PACK ? lane % FRAG_CH : lane;    // this lane's chunk within its line
+  const int line = PACK ? P.line0 + (blockIdx.x * NW + w) * LPW + grp
+                        : P.line0 + blockIdx.x * NW + w;   // cross position of this line
   const int b = blockIdx.z;
   const int n = P.n;
   const int ulo = FULL ? 0 : 1;
@@ -1031,8 +1042,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   unsigned long long tr0 = tr ? gtimer() : 0ull, tr1 = 0ull, tr2 = 0ull;
 
   Ctx<M> c;
-  c.t = t; c.line = line; c.chunk = lane; c.n = n;
-  c.s = sg.start + lane * M;
+  c.t = t; c.line = line; c.chunk = cl; c.n = n;
+  c.s = sg.start + cl * M;
   if (EDGE) {
     c.live = lineok && (lane < sg.nchunks);
     // dead chunks also run the branch-free interior path: their values only reach
@@ -1061,14 +1072,27 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   const int sh = sg.start + TMA_P0 - P.tpos0;
   const int tl = line - P.tline0;
   const int c1 = (sh & 31) >> 1, c2 = sh >> 5;
-  if (lane == 0) {
+  if (PACK) {
+    // fragment tiles: each lane copies its chunk (+ the 2 overlap positions) of S and X
+    double* dS = lS + lane * PADM;
+    double* dX = lX + lane * PADM;
+    const double* gS = P.S_in + (long long)b * P.s_batch + (long long)line * P.s_line + c.s;
+    const double* gX = P.X_in + (long long)b * P.x_batch + (long long)line * P.x_line + c.s;
+#pragma unroll
+    for (int i = 0; i < (M + 2) / 2; ++i) {
+      const double2 vs = lineok ? __ldg(reinterpret_cast<const double2*>(gS) + i) : make_double2(0.0, 0.0);
+      const double2 vx = lineok ? __ldg(reinterpret_cast<const double2*>(gX) + i) : make_double2(0.0, 0.0);
+      reinterpret_cast<double2*>(dS)[i] = vs;
+      reinterpret_cast<double2*>(dX)[i] = vx;
+    }
+  } else if (lane == 0) {
     mbar_init(wbar, 1);
     mbar_expect_tx(wbar, BOX_BYTES * ((MODE == KM_PROLOGUE ? 1u : 2u) + (HET ? 1u : 0u)));
     tma_load_seg(lX, &P.tmX, c1, c2, tl, b, wbar);
     if (HET) tma_load_seg(lC, &P.tmC, c1, c2, tl, 0, wbar);   // one medium for the batch
     if (MODE != KM_PROLOGUE) tma_load_seg(lS, &P.tmS, c1, c2, tl, b, wbar);
   }
-  if (!EDGE && P.pf_ahead > 0 && lane == 0) {
+  if (!EDGE && !PACK && P.pf_ahead > 0 && lane == 0) {
     // L2 prefetch of the staging tiles of the tile pf_ahead CTAs later in launch order:
     // CTAs are dispatched in linear block order, so that tile starts about one resident
     // wave later and its TMA loads then hit L2 -- the HBM reads of the next wave overlap
@@ -1134,7 +1158,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   }
   const bool want_phi = (MODE != KM_FINAL) && P.phi_src;
   const int KK = P.Kdev ? *P.Kdev : P.K;   // sweeps (the stopping rule's choice, if any)
-  if (want_phi && lane == 0) {
+  if (want_phi && lane == 0 && !PACK) {
     // the source pattern is staged late (after the last u-op): warm L2 now
     asm volatile(
         "cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
@@ -1146,8 +1170,10 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();  // the U gather filled every warp's tile
   }
-  mbar_wait(wbar, wpar);
-  wpar ^= 1u;
+  if (!PACK) {
+    mbar_wait(wbar, wpar);
+    wpar ^= 1u;
+  }
   __syncwarp();
   if (tr) tr1 = gtimer();
 
@@ -1181,6 +1207,15 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   // S is dead (after the last u-op that uses it as a base).
   auto stage_phi = [&]() {
     if (!want_phi) return;
+    if constexpr (PACK) {   // the lane's own chunk of the source pattern into its S slot
+      const double* gF = P.phi_src + (long long)line * P.s_line + c.s;
+      double* dF = lS + lane * PADM;
+#pragma unroll
+      for (int i = 0; i < M / 2; ++i)
+        reinterpret_cast<double2*>(dF)[i] = lineok ? __ldg(reinterpret_cast<const double2*>(gF) + i)
+                                                   : make_double2(0.0, 0.0);
+      return;
+    }
     fence_async_shared();   // generic-proxy reads of the S tile before the async overwrite
     __syncwarp();
     if (lane == 0) {
@@ -1194,7 +1229,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     int ipt = -1;
     if (P.pt_line && line == P.pt_line[b] && (!EDGE || c.live)) ipt = P.pt_pos[b] - c.s;
     const double ptf = P.pt_amp * P.gf;
-    if (want_phi) {
+    if (want_phi && !PACK) {
       mbar_wait(wbar, wpar);
       wpar ^= 1u;
       __syncwarp();
@@ -1212,7 +1247,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     int ipt = -1;
     if (P.pt_line && line == P.pt_line[b]) ipt = P.pt_pos[b] - c.s;
     const double ptf = P.pt_amp * P.gf;
-    if (want_phi) {
+    if (want_phi && !PACK) {
       mbar_wait(wbar, wpar);
       wpar ^= 1u;
       __syncwarp();
@@ -1646,13 +1681,52 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   __syncthreads();
   const unsigned long long tr3 = tr ? gtimer() : 0ull;   // (trace: after the CTA barrier)
   // asynchronous outputs (ADI_ASYNC_STORE): lean SWEEP tiles whose 4 lines are all processed
-  constexpr bool ASYNC_ST = ADI_ASYNC_STORE_CODE && MODE == KM_SWEEP && !EDGE && !HET && !FULL && !TEST;
+  constexpr bool ASYNC_ST = ADI_ASYNC_STORE_CODE && MODE == KM_SWEEP && !EDGE && !HET && !FULL && !TEST && !PACK;
   bool async_s = false;
   if constexpr (ASYNC_ST) {
     const int lg0 = P.line0 + blockIdx.x * NW;
     async_s = P.tma_so && !P.carry && lg0 >= P.line_lo && lg0 + NW <= P.nlines;
   }
-  if (ASYNC_ST && P.tma_so && !P.carry && lineok) {
+  if constexpr (PACK) {
+    // fragment tiles.  X': the 8 lanes of a line store its owned positions in pairs
+    {
+      const int xlo = max(sg.out_lo, 0), xhi = min(sg.out_hi, n + 1);
+      const double* tX = lX + grp * FRAG_CH * PADM;   // this line's chunks
+      double* Xo = P.X_out + (long long)b * P.x_batch + (long long)line * P.x_line;
+      if (lineok) {
+        for (int p = (xlo & ~1) + 2 * cl; p < xhi; p += 2 * FRAG_CH) {
+          const int q = p - sg.start;
+          const double2 v = *reinterpret_cast<const double2*>(tX + (q >> 5) * PADM + (q & 31));
+          if (p >= xlo && p + 1 < xhi) *reinterpret_cast<double2*>(Xo + p) = v;
+          else {
+            if (p >= xlo) Xo[p] = v.x;
+            if (p + 1 >= xlo && p + 1 < xhi) Xo[p + 1] = v.y;
+          }
+        }
+      }
+    }
+    // S'^T: the CTA's 16 consecutive lines make 128 contiguous bytes per position; thread
+    // t stores lines (2 (t & 7), +1) of position plo_ + (t >> 3) + 16 k
+    {
+      const int plo_ = max(sg.out_lo, ulo), phi_ = min(sg.out_hi, uhi + 1);
+      const int pair = t & 7;
+      const int L0 = 2 * pair;                                   // CTA line of the pair's first
+      const int wl = L0 / LPW, gl = L0 % LPW;                    // its warp and fragment
+      const double* r0 = stS + wl * LSTR + gl * FRAG_CH * PADM;  // (L0 + 1: same warp, next fragment)
+      const double* r1 = r0 + FRAG_CH * PADM;
+      const int ln = P.line0 + blockIdx.x * NW * LPW + L0;
+      const bool ok0 = ln >= P.line_lo && ln < P.nlines;
+      const bool ok1 = ln + 1 >= P.line_lo && ln + 1 < P.nlines;
+      for (int p = plo_ + (t >> 3); p < phi_; p += NT / 8) {
+        const int q = p - sg.start;
+        const int si = (q >> 5) * PADM + (q & 31);
+        const double v0 = r0[si], v1 = r1[si];
+        double* So = P.S_out + (long long)b * P.s_batch + (long long)p * P.so_pt + (long long)ln * P.so_line;
+        if (ok0 && ok1) *reinterpret_cast<double2*>(So) = make_double2(v0, v1);
+        else { if (ok0) So[0] = v0; if (ok1) So[P.so_line] = v1; }
+      }
+    }
+  } else if (ASYNC_ST && P.tma_so && !P.carry && lineok) {
     // X': this lane's chunk ∩ the owned range as one bulk copy (16-byte aligned body;
     // an odd first / last position by a plain store)
     const int xlo = max(sg.out_lo, 0), xhi = min(sg.out_hi, n + 1);
@@ -1715,7 +1789,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       }
     }
     bulk_wait_read();
-  } else
+  } else if (!PACK)
   // S (or U): transposed.  Half-warp h of warp w stores line pair h at positions
   // 16 w + (lane & 15) + 64 k: the two half-warps fill one 32-byte sector each
   {
@@ -1788,7 +1862,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
 //   MODE = KM_PROLOGUE: U_in, X_in -> a2 (explicit half only)
 // ===========================================================================
 template <int METHOD, int M, int NW, int MODE, bool EDGE, bool HET = false, bool FULL = false,
-          bool NOEND = false>
+          bool NOEND = false, bool PACK = false>
 __global__ void __launch_bounds__(32 * NW, (Occ<METHOD, EDGE, MODE, HET, FULL>::value))
     adi_line_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(128) double smem_raw[];
@@ -1797,7 +1871,7 @@ __global__ void __launch_bounds__(32 * NW, (Occ<METHOD, EDGE, MODE, HET, FULL>::
   double* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u) / 8u;
   if (P.gate && *P.gate) return;   // stopping rule: the stage was decided by an earlier attempt
   const Seg sg = P.segs[blockIdx.y];
-  line_tile<METHOD, M, NW, MODE, EDGE, HET, FULL, NOEND>(P, sg, smem);
+  line_tile<METHOD, M, NW, MODE, EDGE, HET, FULL, NOEND, PACK>(P, sg, smem);
 }
 
 // The stopping rule after the attempt with k sweeps (Alg. 3/4 "until test <= eps or

@@ -60,6 +60,13 @@ struct Axis {
   int nfree = 0;           // of which reading no halo position of a band (the first nfree): a
                            // band's column sweep launches them before its halo exchange lands
   Seg* d_segs = nullptr;
+  // the fragment plan of the MFD SWEEP launches: fsegs = lean tiles
+  // (interior first, fnmid of them, then the two line-end tiles), ffrag = the middle
+  // fragment of FRAG_CH chunks that the PACK kernel runs for 4 lines per warp
+  bool fplan = false;
+  std::vector<Seg> fsegs;
+  int fnmid = 0;
+  Seg* d_fsegs = nullptr;    // fsegs then ffrag
   double* d_tabU = nullptr;  // CFD only
   double* d_tabX = nullptr;
   int* d_ptl = nullptr;      // per batch: point source line / position for this direction
@@ -190,6 +197,7 @@ struct adi_ctx {
   int graph_on = 0;
   int small = -1;   // ADI_THREAD_LINES: -1 auto (short lines), 0 off, 1 on where possible
   int warp_lines = 1;   // ADI_WARP_LINES: short lines (<= 64 positions) on the warp-per-line kernels
+  int frag_on = 1;      // ADI_FRAG_TILES: the MFD fragment plan where it applies
   int async_store = 0;   // ADI_ASYNC_STORE: the SWEEP tiles' outputs by TMA / bulk copies (measured:
                          // no gain, the store phase is bound by the memory system)
   bool capturing = false;
@@ -765,6 +773,9 @@ int setup_axis(adi_ctx* h, adi::Axis& A, int n, int nlines, int nlmin) {
     if (A.segs.empty()) A.segs.push_back({0, 0, 0, 0, 1});  // nothing to output: an idle tile
   }
   if (A.d_segs) { cudaFree(A.d_segs); A.d_segs = nullptr; }
+  if (A.d_fsegs) { cudaFree(A.d_fsegs); A.d_fsegs = nullptr; }
+  A.fplan = false;
+  A.fsegs.clear();
   if (A.d_tabU) { cudaFree(A.d_tabU); A.d_tabU = nullptr; }
   if (A.d_tabX) { cudaFree(A.d_tabX); A.d_tabX = nullptr; }
   if (h->method == ADI_CFD) {
@@ -822,6 +833,49 @@ int setup_axis(adi_ctx* h, adi::Axis& A, int n, int nlines, int nlmin) {
   }
   CUDA_TRY(h, cudaMalloc(&A.d_segs, A.segs.size() * sizeof(adi::Seg)));
   H2D_SYNC(h, A.d_segs, A.segs.data(), A.segs.size() * sizeof(adi::Seg));
+  // the fragment plan (MFD, whole lines, lean tiles only): the two line-end tiles own
+  // 1024 - halo positions, k interior tiles 1024 - 2 halo each, and the gap between them
+  // goes to one FRAG_CH-chunk fragment -- used when that is fewer tile-times than the
+  // standard plan (4.25 instead of 5 at 4096 positions)
+  {
+    const int P = A.n + 1, H = A.halo, L = adi::TCH * adi::TM, FL = adi::FRAG_CH * adi::TM;
+    const bool whole = A.o0 <= 0 && A.o1 >= P && h->tile_chunks == 0;
+    const bool lean = A.nint == (int)A.segs.size() && A.nint - A.nmid == 2;
+    const int span = P - 2 * (L - H);
+    if (h->method == ADI_MFD && whole && lean && span > 0) {
+      const int k = span / (L - 2 * H), gap = span - k * (L - 2 * H);
+      if (gap > 0 && gap <= FL - 2 * H && 2 + k + 0.25 < (double)A.segs.size() - 0.5) {
+        std::vector<adi::Seg> mid, ends;
+        for (const adi::Seg& g : A.segs)
+          if (g.end != 0) ends.push_back(g);   // (the standard plan's line-start / line-end tiles)
+        adi::Seg s0 = ends[0].end == 1 ? ends[0] : ends[1], s1 = ends[0].end == 1 ? ends[1] : ends[0];
+        s0.out_lo = 0; s0.out_hi = L - H;               // line start: positions [0, L - H)
+        s1.out_lo = s1.start + H; s1.out_hi = P;        // line end
+        const int k1 = (k + 1) / 2, k2 = k - k1;
+        int lo = L - H;
+        for (int i = 0; i < k1; ++i, lo += L - 2 * H)
+          mid.push_back({lo - H, adi::TCH, lo, lo + L - 2 * H, 0, 0});
+        const int glo = lo;
+        int hi = s1.out_lo;
+        for (int i = 0; i < k2; ++i, hi -= L - 2 * H)
+          mid.push_back({hi - (L - 2 * H) - H, adi::TCH, hi - (L - 2 * H), hi, 0, 0});
+        const int ghi = hi;
+        adi::Seg fr{(glo - H) & ~1, adi::FRAG_CH, glo, ghi, 0, 0};
+        bool ok = s1.out_lo == glo + gap + k2 * (L - 2 * H) && fr.start + FL >= ghi + H && ghi - glo == gap;
+        for (const adi::Seg& g : mid) ok = ok && (g.start & 1) == 0 && g.start >= 2 && g.start + L - 1 <= A.n - 2;
+        if (ok) {
+          A.fsegs = mid;
+          A.fnmid = (int)mid.size();
+          A.fsegs.push_back(s0);
+          A.fsegs.push_back(s1);
+          A.fsegs.push_back(fr);
+          CUDA_TRY(h, cudaMalloc(&A.d_fsegs, A.fsegs.size() * sizeof(adi::Seg)));
+          H2D_SYNC(h, A.d_fsegs, A.fsegs.data(), A.fsegs.size() * sizeof(adi::Seg));
+          A.fplan = true;
+        }
+      }
+    }
+  }
   return ADI_OK;
 }
 
@@ -887,6 +941,29 @@ int launch_e(adi_ctx* h, const adi::Axis& A, adi::KParams p, int seg0, int nseg)
   return ADI_OK;
 }
 
+// the fragment tiles of the fragment plan: 4 lines per warp, 16 per CTA (one segment)
+int launch_frag(adi_ctx* h, const adi::Axis& A, adi::KParams p) {
+  auto kern = adi::adi_line_kernel<adi::M_MFD, adi::TM, adi::NW, adi::KM_SWEEP, false, false, false, true, true>;
+  const size_t smem = adi::line_smem_bytes<adi::M_MFD, adi::TM, adi::NW, false, false>();
+  static bool set_[kMaxDev] = {};
+  if (!set_[h->dev]) {
+    CUDA_TRY(h, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_[h->dev] = true;
+  }
+  const int nl = std::max(A.l1 - (A.l0 & ~3), 0);
+  const int lpc = adi::NW * (32 / adi::FRAG_CH);   // lines per CTA
+  p.segs = A.d_fsegs + (A.fsegs.size() - 1);
+  p.seg0 = 0;
+  p.nseg_all = 1;
+  p.pf_ahead = 0;
+  dim3 grid((nl + lpc - 1) / lpc, 1, h->batch);
+  kern<<<grid, 32 * adi::NW, smem, h->stream>>>(p);
+  CUDA_TRY(h, cudaGetLastError());
+  h->launches++;
+  if (!h->capturing) h->host_launches++;
+  return ADI_OK;
+}
+
 // interior segments first (lean kernel), then the segments with line ends
 #ifndef ADI_SPLIT_END
 #define ADI_SPLIT_END 1
@@ -898,6 +975,19 @@ int launch_t(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
   const int phase = (&A == &h->ay) ? h->cols_phase : 0;   // adi_step_cols of a band (overlap)
   const int nseg = (int)A.segs.size();
   int rc;
+  if (METHOD == adi::M_MFD && MODE == adi::KM_SWEEP && !HET && !FULL && A.fplan && h->frag_on && phase == 0 &&
+      !p.carry && !p.tma_so && !p.trace) {
+    // the fragment plan: interior tiles, the two line-end tiles, then
+    // the middle fragments packed 4 lines per warp
+    adi::Axis F;
+    F.l0 = A.l0; F.l1 = A.l1;
+    F.segs = std::vector<adi::Seg>(A.fsegs.begin(), A.fsegs.end() - 1);
+    F.d_segs = A.d_fsegs;
+    rc = launch_e<METHOD, MODE, false, HET, FULL, true>(h, F, p, 0, A.fnmid);
+    if (!rc) rc = launch_e<METHOD, MODE, false, HET, FULL, false>(h, F, p, A.fnmid, 2);
+    if (!rc) rc = launch_frag(h, A, p);
+    return rc;
+  }
   if (phase == 1) return launch_e<METHOD, MODE, false, HET, FULL, true>(h, A, p, 0, A.nfree);
   const int s0 = (phase == 2) ? A.nfree : 0;
   if (ADI_SPLIT_END) {
@@ -1243,7 +1333,7 @@ void free_ctx(adi_ctx* h) {
   for (void* q : {(void*)h->edges, (void*)h->flag, (void*)h->d_norms, (void*)h->d_k, (void*)h->d_taper})
     if (q) cudaFree(q);
   for (adi::Axis* A : {&h->ax, &h->ay})
-    for (void* q : {(void*)A->d_segs, (void*)A->d_tabU, (void*)A->d_tabX, (void*)A->d_ptl,
+    for (void* q : {(void*)A->d_segs, (void*)A->d_fsegs, (void*)A->d_tabU, (void*)A->d_tabX, (void*)A->d_ptl,
                     (void*)A->d_ptp})
       if (q) cudaFree(q);
 }
@@ -1481,6 +1571,9 @@ int adi_set_param(adi_handle h, int key, double v) {
   } else if (key == ADI_WARP_LINES) {
     if (v != 0.0 && v != 1.0) return fail(h, ADI_EINVAL, "warp lines must be 0 or 1");
     h->warp_lines = (int)v;
+  } else if (key == ADI_FRAG_TILES) {
+    if (v != 0.0 && v != 1.0) return fail(h, ADI_EINVAL, "fragment tiles must be 0 or 1");
+    h->frag_on = (int)v;
   } else if (key == ADI_ASYNC_STORE) {
     if (v != 0.0 && v != 1.0) return fail(h, ADI_EINVAL, "async store must be 0 or 1");
     h->async_store = (int)v;

@@ -574,3 +574,54 @@ def test_step_index_restart_bitwise(adi, method, n, graph):
     s.close()
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("nx,ny", [(4096, 41), (41, 4096), (3000, 77), (4096, 4096)])
+def test_frag_tiles_bitwise(adi, nx, ny):
+    """ADI_FRAG_TILES: MFD lines whose tile plan leaves a short middle gap
+    (4096 positions: 4 lean tiles + a 168-position fragment; 3000: 3 + 40) run the gap as
+    8-chunk fragments packed 4 lines per warp.  The MFD halos are exact; positions owned by
+    a line-end tile in one plan and an interior tile in the other differ only in the
+    epilogue's rounding order, so max-norm <= 1e-14; split calls, and the
+    oracle agrees."""
+    steps = 2 if nx * ny > 1e6 else 3
+    p = random_problem(MFD, nx, ny=ny, seed=nx + 7 * ny, steps=steps)
+    outs = []
+    for v in (1, 0):
+        s = adi.AdiSolver.from_problem(p)
+        s.set_param(adi.ADI_FRAG_TILES, v)
+        s.step(1)
+        s.step(steps - 1)
+        outs.append(s.get_fields())
+        s.close()
+    for name, a, b in zip("UVW", *outs):
+        d = np.abs(a - b).max() / np.abs(b).max()
+        assert d <= 1e-14, (name, d)
+    if nx * ny < 1e6:
+        assert_parity(outs[0], run_oracle(p, steps), what=f"frag {nx}x{ny}")
+
+
+def test_frag_tiles_batch_points(adi):
+    """Fragment tiles with a batch of point-source grids (the config-5 launch shape, reduced),
+    a source inside a fragment and one inside a lean tile; the standard plan to rounding."""
+    n, B, steps = 4096, 3, 3
+    probs = [random_problem(MFD, n, ny=40, seed=80 + k, steps=steps, source=False, boundary=False)
+             for k in range(B)]
+    gf = np.random.default_rng(8).standard_normal(2 * steps + 1)
+    srcs = [(2000, 17), (500, 30), (2100, 3)]    # (x in the 4096 line's middle fragment: 1964..2131)
+    outs = []
+    for v in (1, 0):
+        s = adi.AdiSolver(n, 40, probs[0].h, probs[0].dt, 1.0, MFD, batch=B)
+        s.set_param(adi.ADI_FRAG_TILES, v)
+        s.set_fields(np.stack([p.U for p in probs]), np.stack([p.V for p in probs]), np.stack([p.W for p in probs]))
+        s.set_point_sources([a for a, _ in srcs], [b for _, b in srcs], gf)
+        s.step(steps)
+        outs.append(s.get_fields())
+        s.close()
+    for name, a, b in zip("UVW", *outs):
+        d = np.abs(a - b).max() / np.abs(b).max()
+        assert d <= 1e-14, (name, d)
+    for k, p in enumerate(probs):
+        p.src = srcs[k]
+        p.gf = gf
+        assert_parity([x[k] for x in outs[0]], run_oracle(p, steps), what=f"frag batch {k}")

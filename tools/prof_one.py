@@ -15,6 +15,9 @@ if sys.argv[1] == "shots":
     probs = shot_problems(0, 8, steps + 2, 8)
     p0 = probs[0]
     s = adi.AdiSolver(SHOT_N, SHOT_N, p0.h, p0.dt, 1.0, MFD, batch=8)
+    for kv in filter(None, os.environ.get("ADI_SET", "").split(",")):   # knobs, e.g. ADI_FRAG_TILES=0
+        k, v = kv.split("=")
+        s.set_param(getattr(adi, k), float(v))
     s.set_point_sources([p.src[0] for p in probs], [p.src[1] for p in probs], p0.gf)
     s.set_fields(*(np.zeros((8,) + a.shape) for a in (p0.U, p0.V, p0.W)))
     s.step(steps)
