@@ -1072,25 +1072,18 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   const int sh = sg.start + TMA_P0 - P.tpos0;
   const int tl = line - P.tline0;
   const int c1 = (sh & 31) >> 1, c2 = sh >> 5;
-  if (PACK) {
-    // fragment tiles: each lane copies its chunk (+ the 2 overlap positions) of S and X
-    double* dS = lS + lane * PADM;
-    double* dX = lX + lane * PADM;
-    const double* gS = P.S_in + (long long)b * P.s_batch + (long long)line * P.s_line + c.s;
-    const double* gX = P.X_in + (long long)b * P.x_batch + (long long)line * P.x_line + c.s;
-#pragma unroll
-    for (int i = 0; i < (M + 2) / 2; ++i) {
-      const double2 vs = lineok ? __ldg(reinterpret_cast<const double2*>(gS) + i) : make_double2(0.0, 0.0);
-      const double2 vx = lineok ? __ldg(reinterpret_cast<const double2*>(gX) + i) : make_double2(0.0, 0.0);
-      reinterpret_cast<double2*>(dS)[i] = vs;
-      reinterpret_cast<double2*>(dX)[i] = vx;
-    }
-  } else if (lane == 0) {
+  // PACK: the 4 fragment lines' leader lanes each copy FRAG_CH chunks (8-chunk boxes) into
+  // the line's quarter of the tile, on the warp's one barrier (same byte count in total)
+  const int go = PACK ? grp * FRAG_CH * PADM : 0;
+  if (lane == 0) {
     mbar_init(wbar, 1);
     mbar_expect_tx(wbar, BOX_BYTES * ((MODE == KM_PROLOGUE ? 1u : 2u) + (HET ? 1u : 0u)));
-    tma_load_seg(lX, &P.tmX, c1, c2, tl, b, wbar);
+  }
+  if (PACK) __syncwarp();   // the barrier exists before the other leaders' copies
+  if (PACK ? cl == 0 : lane == 0) {
+    tma_load_seg(lX + go, &P.tmX, c1, c2, tl, b, wbar);
     if (HET) tma_load_seg(lC, &P.tmC, c1, c2, tl, 0, wbar);   // one medium for the batch
-    if (MODE != KM_PROLOGUE) tma_load_seg(lS, &P.tmS, c1, c2, tl, b, wbar);
+    if (MODE != KM_PROLOGUE) tma_load_seg(lS + go, &P.tmS, c1, c2, tl, b, wbar);
   }
   if (!EDGE && !PACK && P.pf_ahead > 0 && lane == 0) {
     // L2 prefetch of the staging tiles of the tile pf_ahead CTAs later in launch order:
@@ -1158,7 +1151,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   }
   const bool want_phi = (MODE != KM_FINAL) && P.phi_src;
   const int KK = P.Kdev ? *P.Kdev : P.K;   // sweeps (the stopping rule's choice, if any)
-  if (want_phi && lane == 0 && !PACK) {
+  if (want_phi && (PACK ? cl == 0 : lane == 0)) {
     // the source pattern is staged late (after the last u-op): warm L2 now
     asm volatile(
         "cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
@@ -1170,10 +1163,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();  // the U gather filled every warp's tile
   }
-  if (!PACK) {
-    mbar_wait(wbar, wpar);
-    wpar ^= 1u;
-  }
+  mbar_wait(wbar, wpar);
+  wpar ^= 1u;
   __syncwarp();
   if (tr) tr1 = gtimer();
 
@@ -1207,21 +1198,11 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   // S is dead (after the last u-op that uses it as a base).
   auto stage_phi = [&]() {
     if (!want_phi) return;
-    if constexpr (PACK) {   // the lane's own chunk of the source pattern into its S slot
-      const double* gF = P.phi_src + (long long)line * P.s_line + c.s;
-      double* dF = lS + lane * PADM;
-#pragma unroll
-      for (int i = 0; i < M / 2; ++i)
-        reinterpret_cast<double2*>(dF)[i] = lineok ? __ldg(reinterpret_cast<const double2*>(gF) + i)
-                                                   : make_double2(0.0, 0.0);
-      return;
-    }
     fence_async_shared();   // generic-proxy reads of the S tile before the async overwrite
     __syncwarp();
-    if (lane == 0) {
-      mbar_expect_tx(wbar, BOX_BYTES);
-      tma_load_seg(lS, &P.tmF, c1, c2, tl, 0, wbar);
-    }
+    if (lane == 0) mbar_expect_tx(wbar, BOX_BYTES);
+    if (PACK) __syncwarp();
+    if (PACK ? cl == 0 : lane == 0) tma_load_seg(lS + go, &P.tmF, c1, c2, tl, 0, wbar);
   };
   // dst = src + dt/2 F at this chunk's points (F = phi*gf + point source); with
   // a dense source, dst is the S tile holding the staged phi
@@ -1229,7 +1210,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     int ipt = -1;
     if (P.pt_line && line == P.pt_line[b] && (!EDGE || c.live)) ipt = P.pt_pos[b] - c.s;
     const double ptf = P.pt_amp * P.gf;
-    if (want_phi && !PACK) {
+    if (want_phi) {
       mbar_wait(wbar, wpar);
       wpar ^= 1u;
       __syncwarp();
@@ -1247,7 +1228,7 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     int ipt = -1;
     if (P.pt_line && line == P.pt_line[b]) ipt = P.pt_pos[b] - c.s;
     const double ptf = P.pt_amp * P.gf;
-    if (want_phi && !PACK) {
+    if (want_phi) {
       mbar_wait(wbar, wpar);
       wpar ^= 1u;
       __syncwarp();

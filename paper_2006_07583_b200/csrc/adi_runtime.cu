@@ -213,7 +213,7 @@ struct adi_ctx {
   long long call_m1 = 0;
   double *Vcur = nullptr, *Valt = nullptr, *Wcur = nullptr, *Walt = nullptr;
   // TMA tensor maps of the staged arrays (keyed by base pointer)
-  struct TMap { const double* ptr; CUtensorMap map; };
+  struct TMap { const double* ptr; CUtensorMap map; int box = 32; };   // box: chunks per copy
   std::vector<TMap> tmaps;
   struct SMap { const double* ptr; CUtensorMap map; int l0, p0; };
   std::vector<SMap> smaps;   // TMA store maps of the S' outputs (ADI_ASYNC_STORE)
@@ -382,7 +382,7 @@ EncodeTiledFn g_encode = nullptr;
 
 // the overlapping-row view of a pitched line array (adi_line.cuh, TMA_P0)
 int encode_lines(adi_ctx* h, const double* base, int pitch, int rows, size_t bstride, int batch,
-                 CUtensorMap* out) {
+                 CUtensorMap* out, int boxch = 32) {
   if (!g_encode) {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
@@ -395,7 +395,7 @@ int encode_lines(adi_ctx* h, const double* base, int pitch, int rows, size_t bst
   const cuuint64_t dims[5] = {34, 16, (cuuint64_t)((pitch + adi::TMA_P0 + 31) / 32 + 1), (cuuint64_t)rows,
                               (cuuint64_t)batch};
   const cuuint64_t strides[4] = {16, 256, (cuuint64_t)pitch * 8, (cuuint64_t)bstride * 8};
-  const cuuint32_t box[5] = {34, 1, 32, 1, 1};
+  const cuuint32_t box[5] = {34, 1, (cuuint32_t)boxch, 1, 1};
   const cuuint32_t es[5] = {1, 1, 1, 1, 1};
   const CUresult r = g_encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)(base - adi::TMA_P0), dims, strides,
                               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -450,9 +450,9 @@ int tmap_store_for(adi_ctx* h, const double* ptr, CUtensorMap* out, int* line0, 
 }
 
 // tensor map of one of the handle's staged arrays
-int tmap_for(adi_ctx* h, const double* ptr, CUtensorMap* out) {
+int tmap_for(adi_ctx* h, const double* ptr, CUtensorMap* out, int boxch = 32) {
   for (auto& e : h->tmaps)
-    if (e.ptr == ptr) { *out = e.map; return ADI_OK; }
+    if (e.ptr == ptr && e.box == boxch) { *out = e.map; return ADI_OK; }
   int pitch, rows, batch = h->batch;
   size_t bs;
   const int nyb = h->yb - h->ya;   // rows of the band-local row-indexed arrays
@@ -461,8 +461,9 @@ int tmap_for(adi_ctx* h, const double* ptr, CUtensorMap* out) {
     adi_ctx::TMap e;
     e.ptr = ptr;
     const size_t bs = (ptr == h->W || ptr == h->W2) ? h->aW : h->aC;
+    e.box = boxch;
     int rc = encode_lines(h, ptr + (ptrdiff_t)h->xa * h->pc, h->pc, h->xb - h->xa, bs,
-                          ptr == h->phiT ? 1 : h->batch, &e.map);
+                          ptr == h->phiT ? 1 : h->batch, &e.map, boxch);
     if (rc) return rc;
     h->tmaps.push_back(e);
     *out = e.map;
@@ -481,7 +482,8 @@ int tmap_for(adi_ctx* h, const double* ptr, CUtensorMap* out) {
   else return fail(h, ADI_EINVAL, "internal: no tensor map for this array");
   adi_ctx::TMap e;
   e.ptr = ptr;
-  int rc = encode_lines(h, raw, pitch, rows, bs, batch, &e.map);
+  e.box = boxch;
+  int rc = encode_lines(h, raw, pitch, rows, bs, batch, &e.map, boxch);
   if (rc) return rc;
   h->tmaps.push_back(e);
   *out = e.map;
@@ -950,6 +952,11 @@ int launch_frag(adi_ctx* h, const adi::Axis& A, adi::KParams p) {
     CUDA_TRY(h, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     set_[h->dev] = true;
   }
+  // TMA copies of FRAG_CH chunks (each fragment line's leader lane loads its line)
+  int rc;
+  if ((rc = tmap_for(h, p.S_in, &p.tmS, adi::FRAG_CH))) return rc;
+  if ((rc = tmap_for(h, p.X_in, &p.tmX, adi::FRAG_CH))) return rc;
+  if (p.phi_src && (rc = tmap_for(h, p.phi_src, &p.tmF, adi::FRAG_CH))) return rc;
   const int nl = std::max(A.l1 - (A.l0 & ~3), 0);
   const int lpc = adi::NW * (32 / adi::FRAG_CH);   // lines per CTA
   p.segs = A.d_fsegs + (A.fsegs.size() - 1);
