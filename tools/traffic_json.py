@@ -36,8 +36,12 @@ def main():
     groups = []
     for d in L:
         args = re.search(r"adi_line_kernel<([^>]*)>", d["name"]).group(1).split(", ")
-        mode, noend = args[3], args[-1] == "1"
+        # template args: METHOD, M, NW, MODE, EDGE, HET, FULL, NOEND[, PACK]
+        mode = args[3]
+        pack = len(args) > 8 and args[8] == "1"
+        noend = args[7] == "1" and not pack
         # a kind = its interior (NOEND) launch followed by its line-end / generic launches
+        # (and, in the fragment plan, its PACK launch of the middle fragments)
         if groups and groups[-1][0] == mode and not noend:
             groups[-1][1].append(d)
         else:
