@@ -1698,14 +1698,24 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       const int ln = P.line0 + blockIdx.x * NW * LPW + L0;
       const bool ok0 = ln >= P.line_lo && ln < P.nlines;
       const bool ok1 = ln + 1 >= P.line_lo && ln + 1 < P.nlines;
+      int own = 0;   // fused transpose: the owner of position p (positions grow along the loop)
       for (int p = plo_ + (t >> 3); p < phi_; p += NT / 8) {
         const int q = p - sg.start;
         const int si = (q >> 5) * PADM + (q & 31);
         const double v0 = r0[si], v1 = r1[si];
-        double* So = P.S_out + (long long)b * P.s_batch + (long long)p * P.so_pt + (long long)ln * P.so_line;
+        double* So;
+        long long sl = P.so_line;
+        if (P.tnp > 0) {
+          while (own + 1 < P.tnp && p >= P.tcut[own + 1]) ++own;
+          So = P.tso[own] + (long long)b * P.tsb[own] + (long long)p * P.tpt[own] + (long long)ln;
+          sl = 1;
+        } else {
+          So = P.S_out + (long long)b * P.s_batch + (long long)p * P.so_pt + (long long)ln * P.so_line;
+        }
         if (ok0 && ok1) *reinterpret_cast<double2*>(So) = make_double2(v0, v1);
-        else { if (ok0) So[0] = v0; if (ok1) So[P.so_line] = v1; }
+        else { if (ok0) So[0] = v0; if (ok1) So[sl] = v1; }
       }
+      if (P.tnp > 0) __threadfence_system();   // (peer stores, as in the tiles' fused store)
     }
   } else if (ASYNC_ST && P.tma_so && !P.carry && lineok) {
     // X': this lane's chunk ∩ the owned range as one bulk copy (16-byte aligned body;

@@ -863,7 +863,9 @@ int setup_axis(adi_ctx* h, adi::Axis& A, int n, int nlines, int nlmin) {
           mid.push_back({hi - (L - 2 * H) - H, adi::TCH, hi - (L - 2 * H), hi, 0, 0});
         const int ghi = hi;
         adi::Seg fr{(glo - H) & ~1, adi::FRAG_CH, glo, ghi, 0, 0};
-        bool ok = s1.out_lo == glo + gap + k2 * (L - 2 * H) && fr.start + FL >= ghi + H && ghi - glo == gap;
+        // (the line-end tile's start is even, so the gap may differ from span's remainder)
+        bool ok = ghi > glo && ghi - glo <= FL - 2 * H && fr.start >= 2 && fr.start + FL >= ghi + H &&
+                  fr.start + FL - 1 <= A.n - 2;
         for (const adi::Seg& g : mid) ok = ok && (g.start & 1) == 0 && g.start >= 2 && g.start + L - 1 <= A.n - 2;
         if (ok) {
           A.fsegs = mid;

@@ -403,3 +403,20 @@ def test_dist_fused_param_validation(adi):
     with pytest.raises(adi.AdiError):
         s.set_param(adi.ADI_DIST_FUSED, 2)
     s.close()
+
+
+def test_dist_local_transpose_fused_with_fragment_plan(adi):
+    """MFD lines with a fragment plan (4096 positions) in the transpose
+    decomposition: the PACK fragments store their S' into the owning ranks' arrays too, so
+    fused and all-to-all agree bitwise, and one handle to rounding."""
+    p = random_problem(MFD, 4096, ny=200, seed=21, steps=3)
+    fz = _run_transpose(adi, p, 2, 1, [1, 2])
+    a2a = _run_transpose(adi, p, 2, 0, [1, 2])
+    s = adi.AdiSolver.from_problem(p)
+    s.step(1)
+    s.step(2)
+    one = s.get_fields()
+    s.close()
+    for name, a, b, c in zip("UVW", fz, a2a, one):
+        assert np.array_equal(a, b), name
+        assert np.abs(a - c).max() <= 1e-14 * np.abs(c).max(), name

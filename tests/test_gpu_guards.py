@@ -45,6 +45,7 @@ CASES = [("lean", 1601, [], [2, 1, ("ADI_CARRY", 0), 1]),
          ("warp12", 321, [("ADI_THREAD_LINES", 1)], [2, 1]),
          ("thread", 41, [("ADI_THREAD_LINES", 1), ("ADI_WARP_LINES", 0)], [2, 1]),
          ("segments", 1001, [("ADI_TILE_CHUNKS", 12)], [2]),
+         ("frag", 2101, [], [2, 1]),   # MFD: the fragment plan (4 lines per warp)
          ("graph", 1601, [("ADI_GRAPH", 1)], [2, 2]),
          ("async", 2101, [("ADI_ASYNC_STORE", 1)], [2, 1]),
          ("stop", 333, [("ADI_K_SWEEPS", 10), ("ADI_EPS", 1e-6), ("ADI_K_MIN", 3)], [2])]

@@ -576,7 +576,7 @@ def test_step_index_restart_bitwise(adi, method, n, graph):
         assert np.array_equal(x, y)
 
 
-@pytest.mark.parametrize("nx,ny", [(4096, 41), (41, 4096), (3000, 77), (4096, 4096)])
+@pytest.mark.parametrize("nx,ny", [(4096, 41), (41, 4096), (3000, 77), (2101, 66), (4096, 4096)])
 def test_frag_tiles_bitwise(adi, nx, ny):
     """ADI_FRAG_TILES: MFD lines whose tile plan leaves a short middle gap
     (4096 positions: 4 lean tiles + a 168-position fragment; 3000: 3 + 40) run the gap as
