@@ -985,7 +985,7 @@ int launch_t(adi_ctx* h, const adi::Axis& A, const adi::KParams& p) {
   const int nseg = (int)A.segs.size();
   int rc;
   if (METHOD == adi::M_MFD && MODE == adi::KM_SWEEP && !HET && !FULL && A.fplan && h->frag_on && phase == 0 &&
-      !p.carry && !p.tma_so && !p.trace) {
+      !p.carry && !p.trace) {   // (ADI_ASYNC_STORE: the tiles' stores; PACK stores by threads)
     // the fragment plan: interior tiles, the two line-end tiles, then
     // the middle fragments packed 4 lines per warp
     adi::Axis F;
