@@ -1661,6 +1661,12 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   }
   __syncthreads();
   const unsigned long long tr3 = tr ? gtimer() : 0ull;   // (trace: after the CTA barrier)
+// 256-bit global stores (STG.E.256, sm_100): the transposed S' of a CTA's 4 lines is one
+// 32-byte sector per position, written by one thread (MFD rows -6%)
+#ifndef ADI_S256
+#define ADI_S256 1
+#endif
+// (X' along the line stays in 16-byte pairs: 32-byte runs per lane measured slower)
   // asynchronous outputs (ADI_ASYNC_STORE): lean SWEEP tiles whose 4 lines are all processed
   constexpr bool ASYNC_ST = ADI_ASYNC_STORE_CODE && MODE == KM_SWEEP && !EDGE && !HET && !FULL && !TEST && !PACK;
   bool async_s = false;
@@ -1687,22 +1693,24 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       }
     }
     // S'^T: the CTA's 16 consecutive lines make 128 contiguous bytes per position; thread
-    // t stores lines (2 (t & 7), +1) of position plo_ + (t >> 3) + 16 k
+    // t stores lines 4 (t & 3) .. +3 -- one fragment slot of each warp row, i.e. warp
+    // (t & 3)'s 4 fragments -- of position plo_ + (t >> 2) + 32 k, as one 32-byte store
     {
       const int plo_ = max(sg.out_lo, ulo), phi_ = min(sg.out_hi, uhi + 1);
-      const int pair = t & 7;
-      const int L0 = 2 * pair;                                   // CTA line of the pair's first
-      const int wl = L0 / LPW, gl = L0 % LPW;                    // its warp and fragment
-      const double* r0 = stS + wl * LSTR + gl * FRAG_CH * PADM;  // (L0 + 1: same warp, next fragment)
-      const double* r1 = r0 + FRAG_CH * PADM;
-      const int ln = P.line0 + blockIdx.x * NW * LPW + L0;
-      const bool ok0 = ln >= P.line_lo && ln < P.nlines;
-      const bool ok1 = ln + 1 >= P.line_lo && ln + 1 < P.nlines;
+      const int wq = t & 3;                                   // the warp whose 4 fragment lines
+      const double* r0 = stS + wq * LSTR;                     // line 4 wq + g: fragment g of warp wq
+      const int ln = P.line0 + blockIdx.x * NW * LPW + 4 * wq;
+      bool ok[4];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) ok[g] = ln + g >= P.line_lo && ln + g < P.nlines;
+      const bool all = ok[0] && ok[1] && ok[2] && ok[3];
       int own = 0;   // fused transpose: the owner of position p (positions grow along the loop)
-      for (int p = plo_ + (t >> 3); p < phi_; p += NT / 8) {
+      for (int p = plo_ + (t >> 2); p < phi_; p += NT / 4) {
         const int q = p - sg.start;
         const int si = (q >> 5) * PADM + (q & 31);
-        const double v0 = r0[si], v1 = r1[si];
+        double v[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) v[g] = r0[g * FRAG_CH * PADM + si];
         double* So;
         long long sl = P.so_line;
         if (P.tnp > 0) {
@@ -1712,8 +1720,15 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
         } else {
           So = P.S_out + (long long)b * P.s_batch + (long long)p * P.so_pt + (long long)ln * P.so_line;
         }
-        if (ok0 && ok1) *reinterpret_cast<double2*>(So) = make_double2(v0, v1);
-        else { if (ok0) So[0] = v0; if (ok1) So[sl] = v1; }
+        if (all && sl == 1) {
+          asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(So), "d"(v[0]), "d"(v[1]), "d"(v[2]),
+                       "d"(v[3])
+                       : "memory");
+        } else {
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            if (ok[g]) So[g * sl] = v[g];
+        }
       }
       if (P.tnp > 0) __threadfence_system();   // (peer stores, as in the tiles' fused store)
     }
@@ -1793,7 +1808,24 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     else { plo_ = max(sg.out_lo, ulo); phi_ = min(sg.out_hi, uhi + 1); }
     const double* r0 = stS + (2 * pr) * LSTR;
     const double* r1 = r0 + LSTR;
-    if (MODE != KM_FINAL && P.tnp > 0) {
+    const bool all4 = P.line0 + (int)blockIdx.x * NW >= P.line_lo && P.line0 + (int)blockIdx.x * NW + NW <= P.nlines;
+    if (ADI_S256 && MODE != KM_FINAL && P.tnp > 0 && all4) {
+      // fused transpose, one 32-byte sector (the CTA's 4 lines) per thread and position
+      const long long lg0 = P.line0 + (long long)blockIdx.x * NW;
+      int q = 0;
+#pragma unroll STORE_UNROLL
+      for (int pos = t; pos < 32 * M; pos += NT) {
+        const int p = sg.start + pos;
+        if (p < plo_ || p >= phi_) continue;
+        while (q + 1 < P.tnp && p >= P.tcut[q + 1]) ++q;
+        const int si = (pos >> 5) * PADM + (pos & 31);
+        double* So = P.tso[q] + (long long)b * P.tsb[q] + (long long)p * P.tpt[q] + lg0;
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(So), "d"(stS[si]), "d"(stS[LSTR + si]),
+                     "d"(stS[2 * LSTR + si]), "d"(stS[3 * LSTR + si])
+                     : "memory");
+      }
+      __threadfence_system();
+    } else if (MODE != KM_FINAL && P.tnp > 0) {
       // fused transpose: position p lands in the array of its owner q
       // (the cuts are few and sorted; positions grow along a lane's loop), as P2P stores
       int q = 0;
@@ -1810,6 +1842,19 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       // this thread's peer stores are performed at system scope before the kernel can
       // complete (and the barrier after it release them to the owners)
       __threadfence_system();
+    } else if (ADI_S256 && MODE != KM_FINAL && all4) {
+      // a whole 32-byte sector per thread: the CTA's 4 lines at one position
+      const long long lg0 = P.line0 + (long long)blockIdx.x * NW;
+#pragma unroll STORE_UNROLL
+      for (int pos = t; pos < 32 * M; pos += NT) {
+        const int p = sg.start + pos;
+        if (p < plo_ || p >= phi_) continue;
+        const int si = (pos >> 5) * PADM + (pos & 31);
+        double* So = P.S_out + (long long)b * P.s_batch + (long long)p * P.so_pt + lg0;
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(So), "d"(stS[si]), "d"(stS[LSTR + si]),
+                     "d"(stS[2 * LSTR + si]), "d"(stS[3 * LSTR + si])
+                     : "memory");
+      }
     } else {
 #pragma unroll STORE_UNROLL
       for (int pos = 16 * w + (lane & 15); pos < 32 * M; pos += 16 * NW) {
