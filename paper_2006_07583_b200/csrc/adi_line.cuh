@@ -953,6 +953,16 @@ __device__ __forceinline__ void tma_load_seg(double* dst, const CUtensorMap* tm,
       : "memory");
 }
 
+// 256-bit global stores (STG.E.256, sm_100): the transposed S' of a CTA's 4 lines is one
+// 32-byte sector per position, written by one thread (DESIGN.md §5.12; MFD rows -6%)
+#ifndef ADI_S256
+#define ADI_S256 1
+#endif
+// one 32-byte global store (STG.E.256, sm_100); dst 32-byte aligned
+__device__ __forceinline__ void st256(double* dst, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
 // L2 prefetch of the same box (no shared-memory destination, no completion)
 __device__ __forceinline__ void tma_prefetch_seg(const CUtensorMap* tm, int c1, int c2, int line, int b) {
   asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
@@ -1303,6 +1313,24 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
     const int plo_ = max(sg.out_lo, 0), phi_ = min(sg.out_hi, n + 1);
     const double* r0 = stS + (2 * pr) * LSTR;
     const double* r1 = r0 + LSTR;
+    const int lg0 = P.line0 + blockIdx.x * NW;
+    if (ADI_S256 && P.u_line == 1 && lg0 >= P.line_lo && lg0 + NW <= P.nlines) {
+      // the CTA's 4 lines of a position as one 32-byte store (as the S' store)
+      for (int pos = t; pos < 32 * M; pos += NT) {
+        const int p = sg.start + pos;
+        if (p < plo_ || p >= phi_) continue;
+        const int si = (pos >> 5) * PADM + (pos & 31);
+        st256(P.U_out + (long long)b * P.u_batch + (long long)p * P.u_pt + lg0, stS[si], stS[LSTR + si],
+              stS[2 * LSTR + si], stS[3 * LSTR + si]);
+        if (METHOD == M_MFD && p == n) {
+          double e[4];
+          for (int l = 0; l < 4; ++l) e[l] = P.edgeR ? P.edgeR[lg0 + l] * P.gb : 0.0;
+          st256(P.U_out + (long long)b * P.u_batch + (long long)(n + 1) * P.u_pt + lg0, e[0], e[1], e[2], e[3]);
+        }
+      }
+      __syncthreads();   // the S tiles are read before the epilogue reuses them
+      return;
+    }
     for (int pos = 16 * w + (lane & 15); pos < 32 * M; pos += 16 * NW) {
       const int p = sg.start + pos;
       if (p < plo_ || p >= phi_) continue;
@@ -1661,12 +1689,8 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
   }
   __syncthreads();
   const unsigned long long tr3 = tr ? gtimer() : 0ull;   // (trace: after the CTA barrier)
-// 256-bit global stores (STG.E.256, sm_100): the transposed S' of a CTA's 4 lines is one
-// 32-byte sector per position, written by one thread (DESIGN.md §5.12; MFD rows -6%)
-#ifndef ADI_S256
-#define ADI_S256 1
-#endif
-// (X' along the line stays in 16-byte pairs: 32-byte runs per lane measured slower)
+
+  // (X' along the line stays in 16-byte pairs: 32-byte runs per lane measured slower)
   // asynchronous outputs (ADI_ASYNC_STORE): lean SWEEP tiles whose 4 lines are all processed
   constexpr bool ASYNC_ST = ADI_ASYNC_STORE_CODE && MODE == KM_SWEEP && !EDGE && !HET && !FULL && !TEST && !PACK;
   bool async_s = false;
@@ -1842,6 +1866,22 @@ __device__ __forceinline__ void line_tile(const KParams& P, const Seg& sg, doubl
       // this thread's peer stores are performed at system scope before the kernel can
       // complete (and the barrier after it release them to the owners)
       __threadfence_system();
+    } else if (ADI_S256 && MODE == KM_FINAL && all4 && P.u_line == 1) {
+      // U (FINAL): the CTA's 4 lines of a position as one 32-byte store; MFD row n+1 = gR
+      const long long lg0 = P.line0 + (long long)blockIdx.x * NW;
+#pragma unroll STORE_UNROLL
+      for (int pos = t; pos < 32 * M; pos += NT) {
+        const int p = sg.start + pos;
+        if (p < plo_ || p >= phi_) continue;
+        const int si = (pos >> 5) * PADM + (pos & 31);
+        st256(P.U_out + (long long)b * P.u_batch + (long long)p * P.u_pt + lg0, stS[si], stS[LSTR + si],
+              stS[2 * LSTR + si], stS[3 * LSTR + si]);
+        if (METHOD == M_MFD && p == n) {
+          double e[4];
+          for (int l = 0; l < 4; ++l) e[l] = P.edgeR ? P.edgeR[lg0 + l] * P.gb : 0.0;
+          st256(P.U_out + (long long)b * P.u_batch + (long long)(n + 1) * P.u_pt + lg0, e[0], e[1], e[2], e[3]);
+        }
+      }
     } else if (ADI_S256 && MODE != KM_FINAL && all4) {
       // a whole 32-byte sector per thread: the CTA's 4 lines at one position
       const long long lg0 = P.line0 + (long long)blockIdx.x * NW;
