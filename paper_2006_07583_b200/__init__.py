@@ -49,6 +49,13 @@ ADI_DIST_FUSED = 14
 ADI_WARP_LINES = 15
 ADI_STEP_INDEX = 16
 ADI_FRAG_TILES = 17
+# kernel kinds (adi_get_kernel_times index, include/adi.h enum adi_kernel_kind)
+ADI_KK_PROLOGUE = 0
+ADI_KK_ROW = 1
+ADI_KK_COL = 2
+ADI_KK_FINAL = 3
+ADI_KK_EDGE = 4
+ADI_NKINDS = 5
 ADI_DIST_HALO = 0
 ADI_DIST_TRANSPOSE = 1
 KERNEL_KINDS = ("prologue", "row", "col", "final", "edge")

@@ -84,3 +84,19 @@ def test_bad_arguments_rejected_before_device(libpath):
         with pytest.raises(adi.AdiError) as e:
             adi.adi_create(*args)
         assert e.value.code == adi.ADI_EINVAL
+
+
+def test_binding_constants_match_the_header():
+    """Every enumerator of include/adi.h (methods, statuses, parameters, kernel kinds, dist
+    modes) exists in the binding with the header's value -- no drift between the two."""
+    import re
+    import paper_2006_07583_b200 as adi
+    text = open(os.path.join(ROOT, "include", "adi.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)   # (comments may mention names)
+    found = 0
+    for body in re.findall(r"enum\s*\w*\s*\{(.*?)\}", text, flags=re.S):
+        for name, val in re.findall(r"(ADI_[A-Z0-9_]+)\s*=\s*(-?\d+)", body):
+            assert hasattr(adi, name), f"binding lacks {name}"
+            assert getattr(adi, name) == int(val), (name, getattr(adi, name), val)
+            found += 1
+    assert found >= 35, found
