@@ -420,7 +420,7 @@ def _run_calls(adi, p, plan, carry, n_steps_table=None):
 
 
 @pytest.mark.parametrize("method", [CFD, MFD])
-@pytest.mark.parametrize("n", [37, 1601])
+@pytest.mark.parametrize("n", [37, 1601, 2101])
 def test_carry_matches_one_call(adi, method, n):
     """ADI_CARRY (include/adi.h): the next call starts from the a2 computed by the previous
     call's last column kernel -- the one-call computation, so split calls match one call
